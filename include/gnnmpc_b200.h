@@ -1,0 +1,202 @@
+/*
+ * gnnmpc_b200.h -- C ABI of the B200-native GNN-MPC hot path.
+ *
+ * One shared library (libgnnmpc_b200.so, sm_100a) exports the per-step hot
+ * path of the reference package ``gnnmpc`` (arXiv 2602.17601) as plain
+ * C entry points: pointers + sizes, no torch types.  The reference is pure
+ * Python; the functions below are what its Python API
+ * for this path would bind through an FFI (ctypes stub in INTEGRATION.md).
+ * Each entry point names the reference function it replaces
+ * (paths relative to /root/reference/pkg/src/gnnmpc/).
+ *
+ * Conventions
+ *   - M nodes per instance, N horizon stages, nx = 2*n_p state, nu inputs,
+ *     E directed edges in the canonical node-major order of
+ *     GraphTopology.edges (graph.py:60-63).
+ *   - B independent instances (scenarios) share one model and one topology;
+ *     every per-instance array is instance-major.  B = 1 reproduces the
+ *     reference call exactly.
+ *   - "device" pointers are CUDA device memory on the context's device and
+ *     are owned by the caller; the context owns weights, graph tables and
+ *     scratch.  All device work is stream-ordered on `stream` (a
+ *     cudaStream_t passed as void*); no entry point synchronises the host
+ *     unless stated.
+ *   - Gamma work array ("gamma"): fp32 (B*M, N+1, nx, ld) with
+ *     Gamma_u (condensing.py:187) in columns [0, N*nu) and Gamma_x in
+ *     column N*nu; ld = gm_gamma_ld(N, nu) (>= N*nu+2, multiple of 32).
+ *   - Return codes: GM_OK, GM_ERR_CONFIG (the reference raises ValueError /
+ *     ConfigurationError, condensing.py:36-37), GM_ERR_NUMERIC (numerical
+ *     abort, cli.py:332-338 exit 3), GM_ERR_CUDA (CUDA / NCCL failure).
+ *     The message is available from gm_last_error().  QP failures are
+ *     statuses, not errors (qpsolver.py:24-28).
+ */
+#ifndef GNNMPC_B200_H
+#define GNNMPC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GM_OK 0
+#define GM_ERR_CONFIG 2
+#define GM_ERR_NUMERIC 3
+#define GM_ERR_CUDA 4
+
+/* QpStatus, declaration order of qpsolver.py:24-28 */
+#define GM_QP_OPTIMAL 0
+#define GM_QP_MAX_ITERATIONS 1
+#define GM_QP_PRIMAL_INFEASIBLE 2
+#define GM_QP_NUMERICAL_FAILURE 3
+
+typedef struct gm_ctx gm_ctx;
+
+/* SolverSettings (qpsolver.py:66-76); warm_start is a separate pointer. */
+typedef struct gm_qp_settings {
+  double tolerance;            /* 1e-8 */
+  int32_t max_iterations;      /* 50 */
+  double regularization;       /* 1e-9 */
+  double fraction_to_boundary; /* 0.995 */
+} gm_qp_settings;
+
+int gm_abi_version(void);
+
+/* Context.  device < 0 creates a host-only context: graph index
+ * construction works, every device entry point returns GM_ERR_CONFIG. */
+int gm_create(gm_ctx** out, int device);
+void gm_destroy(gm_ctx* ctx);
+const char* gm_last_error(const gm_ctx* ctx);
+
+/* ---- graph (graph.py:25-74) ------------------------------------------- */
+/* Replaces GraphTopology validation (graph.py:35-54) + the index tables of
+ * _edge_index (gnn.py:107-126) and _padded_neighborhood
+ * (condensing.py:158-172).  Host inputs: in-neighbour lists as CSR,
+ * nbr_ptr (node_count+1), nbr_list (nbr_ptr[node_count]). */
+int gm_set_graph(gm_ctx* ctx, int64_t node_count, int64_t neighbor_bound,
+                 const int64_t* nbr_ptr, const int64_t* nbr_list);
+int64_t gm_edge_count(const gm_ctx* ctx);
+int64_t gm_max_degree(const gm_ctx* ctx);
+/* Host outputs, bit-exact with the reference tables:
+ *   dst, src   (E)                   gnn.py:116-117
+ *   gather     (M, max(d,1)) pad E   gnn.py:120-125
+ *   nbr_slots  (M, 1+d)      pad M   condensing.py:163-171
+ *   edge_slot  (E)                   condensing.py:166-172
+ * Any pointer may be NULL to skip that table. */
+int gm_graph_tables(const gm_ctx* ctx, int64_t* dst, int64_t* src, int64_t* gather,
+                    int64_t* nbr_slots, int64_t* edge_slot);
+
+/* ---- model (gnn.py:44-104, mlp.py:15-64) ------------------------------- */
+/* Host inputs.  psi_w / phi_w: the row-major (out, in) weight matrices of
+ * each layer concatenated; *_b: biases concatenated; dims arrays have
+ * n_layers+1 entries. */
+int gm_set_model(gm_ctx* ctx, int n_p, int n_u, int n_m, double dt,
+                 int psi_layers, const int32_t* psi_dims, const double* psi_w, const double* psi_b,
+                 int phi_layers, const int32_t* phi_dims, const double* phi_w, const double* phi_b,
+                 const double* state_mean, const double* state_scale,
+                 const double* input_mean, const double* input_scale);
+
+/* State / input dimensions used by the condensing entry points when the
+ * linearisation was not produced by gm_linearize (set_model sets both). */
+int gm_set_dims(gm_ctx* ctx, int nx, int nu);
+
+/* Restrict node-wise work to owned nodes [lo, hi) of every instance (graph
+ * partition for multi-GPU; default = all nodes). */
+int gm_set_node_range(gm_ctx* ctx, int64_t lo, int64_t hi);
+
+/* ---- stage 1: linearize_trajectory (gnn.py:308-321 -> :237-298) ------- */
+/* P = B*K linearisation points.  Device inputs X (P, M, nx) fp64,
+ * U (P, nu) fp64.  Device outputs: a_self (P, M, nx, nx), a_nbr (P, E, nx,
+ * nx) in edge order, b (P, M, nx, nu) in fp32 and the offset c (P, M, nx) in
+ * fp64, evaluated from the stored fp32 blocks so the affine model is exact at
+ * the linearisation point to fp64 round-off (gnn.py:290-297).
+ * f_next (P, M, nx) fp64 = step_array(X, U) (gnn.py:153-159), may be NULL. */
+int gm_linearize(gm_ctx* ctx, int64_t P, const double* X, const double* U, float* a_self,
+                 float* a_nbr, float* b, double* c, double* f_next, void* stream);
+
+/* step_array only (gnn.py:153-159): f (P, M, nx) fp64. */
+int gm_step(gm_ctx* ctx, int64_t P, const double* X, const double* U, double* f, void* stream);
+
+/* ---- stage 2: condense_gammas (condensing.py:182-228) ------------------ */
+int gm_gamma_ld(int N, int nu);
+/* lin blocks as produced by gm_linearize with P = B*N; x0 (B, M, nx) fp64. */
+int gm_condense_gammas(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_nbr,
+                       const float* b, const double* c, const double* x0, float* gamma, int ld,
+                       void* stream);
+/* One stage n -> n+1 only (for the node-partitioned recursion whose halo
+ * rows are exchanged between stages).  Stage 0 is written by n = -1. */
+int gm_condense_gammas_stage(gm_ctx* ctx, int B, int N, int n, const float* a_self,
+                             const float* a_nbr, const float* b, const double* c,
+                             const double* x0, float* gamma, int ld, void* stream);
+
+/* ---- stage 3: condense_ocp cost part (condensing.py:363-389, :402-403) -- */
+/* H (B, n0, n0) fp64 symmetrised, g (B, n0) fp64, n0 = N*nu.
+ * q (B, M, N+1, nx, nx), x_ref (B, M, N+1, nx), r (B, N, nu, nu),
+ * u_ref (B, N, nu): fp64 device; a per-instance stride of 0 broadcasts
+ * one array to all instances (strides in elements).
+ * partial != 0 writes only the (symmetrised) node sums over the owned node
+ * range, without R-bar and r_lin: the multi-GPU partial that is all-reduced
+ * (rank 0 passes partial = 0, so the sum over ranks is the full H, g). */
+int gm_condense_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const double* q,
+                     int64_t q_stride, const double* x_ref, int64_t xref_stride, const double* r,
+                     int64_t r_stride, const double* u_ref, int64_t uref_stride, double* H,
+                     double* g, int partial, void* stream);
+
+/* Constraint rows (condensing.py:263-282, :312-323), per instance:
+ * rows [0, n_in) are input rows: row k has coefficients in_c (nu) at
+ * column block in_stage[k]; rows [n_in, n_in+n_st) are state rows:
+ * C = st_c . Gamma_u[node, stage], d = st_d - st_c . Gamma_x[node, stage].
+ * Row data shared by all instances; outputs C (B, m0, n0), d (B, m0) fp64. */
+int gm_constraint_rows(gm_ctx* ctx, int B, int N, const float* gamma, int ld, int n_in,
+                       const int32_t* in_stage, const double* in_c, const double* in_d, int n_st,
+                       const int32_t* st_node, const int32_t* st_stage, const double* st_c,
+                       const double* st_d, double* C, double* d, void* stream);
+
+/* expand_soft_constraints (condensing.py:419-439), batched.  soft_idx (ns)
+ * row indices into the m0 rows; rho1/rho2 (ns).  Outputs H (B, n, n),
+ * g (B, n), C (B, m, n), d (B, m) with n = n0+ns, m = m0+ns. */
+int gm_expand_soft(gm_ctx* ctx, int B, int n0, int m0, const double* H0, const double* g0,
+                   const double* C0, const double* d0, int ns, const int32_t* soft_idx,
+                   const double* rho1, const double* rho2, double* H, double* g, double* C,
+                   double* d, void* stream);
+
+/* ---- stage 4: solve_qp (qpsolver.py:112-243), batched ------------------ */
+/* One QP per instance: H (B, n, n), g (B, n), C (B, m, n), d (B, m),
+ * warm (B, n) or NULL.  Outputs u (B, n), lam (B, m), status (B),
+ * iterations (B), resid (B, 3) = stationarity, primal_infeas,
+ * complementarity of the returned iterate. */
+int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, const double* g,
+                const double* C, const double* d, const double* warm,
+                const gm_qp_settings* settings, double* u, double* lam, int32_t* status,
+                int32_t* iterations, double* resid, void* stream);
+
+/* ---- reconstruct_states (condensing.py:409-416) ------------------------ */
+/* u (B, ldu) fp64 (first N*nu used); x (B, M, N+1, nx) fp64. */
+int gm_reconstruct_states(gm_ctx* ctx, int B, int N, const float* gamma, int ld,
+                          const double* u, int ldu, double* x, void* stream);
+
+/* ---- mpc_step tail (mpc.py:151-200) ------------------------------------ */
+/* Device-side RTI epilogue, no host sync.  Per instance, when status is
+ * OPTIMAL or MAX_ITERATIONS: planned = reconstruct(u) and the trajectory
+ * becomes (1-a) lin + a planned (a = sqp_damping), u_applied = its input 0;
+ * otherwise the trajectory falls back to fb_states / fb_inputs (the
+ * previous plan with x_measured at stage 0) and u_applied follows the
+ * fallback policy (0 hold-previous-input using u_prev when has_prev != 0,
+ * 1 zero-input).  Outputs: cur_states (B, N+1, M, nx) unshifted (may be
+ * NULL), planned_states (B, M, N+1, nx), planned_inputs (B, N, nu), the
+ * shifted successor next_states (B, N+1, M, nx) / next_inputs (B, N, nu)
+ * (mpc.py:90-99), u_applied (B, nu) and summary (B, nu+2) = [u_applied,
+ * status, iterations] for a single small device->host read (may be NULL). */
+int gm_mpc_finish(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const double* u,
+                  int ldu, const int32_t* status, const int32_t* iterations,
+                  const double* lin_states, const double* lin_inputs, const double* fb_states,
+                  const double* fb_inputs, double sqp_damping, int fallback,
+                  const double* u_prev, int has_prev, double* cur_states,
+                  double* planned_states, double* planned_inputs, double* next_states,
+                  double* next_inputs, double* u_applied, double* summary, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GNNMPC_B200_H */

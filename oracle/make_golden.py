@@ -1,0 +1,268 @@
+"""Generate golden fixtures from the REFERENCE implementation (test infrastructure).
+
+Runs only in the build container, where the read-only reference package is
+importable from /root/reference/pkg/src.  Writes small compressed fixtures to
+tests/golden/ that pin (a) the oracle port (oracle/ref_port.py) and (b) the
+GPU path, on the GPU box where the reference does not exist.
+
+    python oracle/make_golden.py
+
+Every fixture is produced by calling the reference's own public functions;
+nothing in here reimplements the algorithm.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parents[1] / "tests" / "golden"
+
+
+def _ref():
+    sys.path.insert(0, str(REF))
+    import gnnmpc.condensing as rc
+    import gnnmpc.experiments as rex
+    import gnnmpc.gnn as rg
+    import gnnmpc.graph as rgr
+    import gnnmpc.mlp as rmlp
+    import gnnmpc.mpc as rm
+    import gnnmpc.qpsolver as rq
+    return rc, rex, rg, rgr, rmlp, rm, rq
+
+
+def _model_arrays(prefix, model, out):
+    for name, mlp in (("psi", model.psi), ("phi", model.phi)):
+        out[f"{prefix}{name}_dims"] = np.asarray(mlp.layer_dims)
+        for l, (W, b) in enumerate(zip(mlp.weights, mlp.biases)):
+            out[f"{prefix}{name}_W{l}"] = W
+            out[f"{prefix}{name}_b{l}"] = b
+    n = model.normalization
+    out[f"{prefix}norm"] = np.concatenate([n.state_mean, n.state_scale, n.input_mean, n.input_scale])
+    out[f"{prefix}meta"] = np.array([model.dt, model.n_p, model.n_u, model.n_m])
+
+
+def _spec_arrays(prefix, spec, out):
+    out[f"{prefix}q"] = spec.q
+    out[f"{prefix}x_ref"] = spec.x_ref
+    out[f"{prefix}r"] = spec.r
+    out[f"{prefix}u_ref"] = spec.u_ref
+    if spec.input_constraints is not None:
+        out[f"{prefix}icons_C"] = np.stack([C for C, _ in spec.input_constraints])
+        out[f"{prefix}icons_d"] = np.stack([d for _, d in spec.input_constraints])
+    sc = spec.state_constraints
+    out[f"{prefix}scons_meta"] = np.array([[s.node, s.stage, int(s.soft), s.rho1, s.rho2, s.c.shape[0]]
+                                           for s in sc], dtype=float).reshape(-1, 6)
+    out[f"{prefix}scons_c"] = (np.concatenate([s.c for s in sc]) if sc
+                               else np.zeros((0, spec.q.shape[-1])))
+    out[f"{prefix}scons_d"] = np.concatenate([s.d for s in sc]) if sc else np.zeros(0)
+
+
+def _pipeline(prefix, model, topo, spec, states, inputs, x0, out, rc, rg, rq, rm, rgr):
+    lin = rg.linearize_trajectory(model, topo, states, inputs)
+    for k in ("a_self", "a_nbr", "b", "c"):
+        out[f"{prefix}lin_{k}"] = getattr(lin, k)
+    gu, gx = rc.condense_gammas(lin, x0)
+    out[f"{prefix}gamma_u"] = gu
+    out[f"{prefix}gamma_x"] = gx
+    qp = rc.condense_ocp(spec, lin, x0, gammas=(gu, gx))
+    for k in ("h", "g", "c", "d", "soft", "rho1", "rho2"):
+        out[f"{prefix}qp_{k}"] = getattr(qp, k)
+    H, g, C, d, n0 = rc.expand_soft_constraints(qp)
+    out[f"{prefix}x_H"], out[f"{prefix}x_g"], out[f"{prefix}x_C"], out[f"{prefix}x_d"] = H, g, C, d
+    sol = rq.solve_qp(rq.QpProblem(H, g, C, d))
+    out[f"{prefix}sol_u"] = sol.u
+    out[f"{prefix}sol_duals"] = sol.duals
+    out[f"{prefix}sol_meta"] = np.array([["optimal", "max_iterations", "primal_infeasible",
+                                          "numerical_failure"].index(sol.status.value),
+                                         sol.iterations, sol.stationarity, sol.primal_infeas,
+                                         sol.complementarity])
+    out[f"{prefix}recon"] = rc.reconstruct_states(gu, gx, sol.u[:n0])
+    cfg = rm.MpcConfig(horizon=spec.horizon, dt=model.dt)
+    xs = rgr.SystemState(x0)
+    st = rm.mpc_init(xs, cfg, spec.r.shape[-1])
+    u1, st1 = rm.mpc_step(model, topo, spec, xs, st, cfg)
+    out[f"{prefix}mpc_u"] = u1.u
+    out[f"{prefix}mpc_lin_states"] = st1.lin_states
+    out[f"{prefix}mpc_lin_inputs"] = st1.lin_inputs
+    out[f"{prefix}mpc_planned_states"] = st1.planned_states
+    out[f"{prefix}mpc_meta"] = np.array([["optimal", "max_iterations", "primal_infeasible",
+                                          "numerical_failure"].index(st1.last_status.value),
+                                         st1.last_iterations])
+    # second step from the shifted state (warm start path)
+    u2, st2 = rm.mpc_step(model, topo, spec, xs, st1, cfg)
+    out[f"{prefix}mpc2_u"] = u2.u
+    out[f"{prefix}mpc2_lin_states"] = st2.lin_states
+    out[f"{prefix}mpc2_meta"] = np.array([["optimal", "max_iterations", "primal_infeasible",
+                                           "numerical_failure"].index(st2.last_status.value),
+                                          st2.last_iterations])
+
+
+def random_instance(rng, rc, rg, rgr, max_m=8, max_nx=4, max_nu=3, max_n=10, with_constraints=True):
+    """Same generator as the reference test-suite's random_instance
+    (tests/test_condensing.py:40-80), so fixtures cover its case family."""
+    M = int(rng.integers(1, max_m + 1))
+    nx = int(rng.integers(1, max_nx + 1))
+    nu = int(rng.integers(1, max_nu + 1))
+    N = int(rng.integers(1, max_n + 1))
+    nbrs = []
+    for i in range(M):
+        others = [j for j in range(M) if j != i]
+        k = int(rng.integers(0, min(2, len(others)) + 1))
+        pick = sorted(rng.choice(others, size=k, replace=False).tolist()) if k else []
+        nbrs.append(tuple(int(v) for v in pick))
+    topo = rgr.GraphTopology(M, tuple(nbrs), 2)
+    E = len(topo.edges)
+    scale = 0.9 / max(1, nx)
+    lin = rg.LinearizedDynamics(topo, N, a_self=rng.standard_normal((N, M, nx, nx)) * scale,
+                                a_nbr=rng.standard_normal((N, E, nx, nx)) * scale,
+                                b=rng.standard_normal((N, M, nx, nu)),
+                                c=rng.standard_normal((N, M, nx)))
+    q = rng.standard_normal((M, N + 1, nx, nx))
+    q = np.einsum("mkab,mkcb->mkac", q, q) * 0.3
+    r = rng.standard_normal((N, nu, nu))
+    r = np.einsum("kab,kcb->kac", r, r) + np.eye(nu) * 0.5
+    icons, scons = None, []
+    if with_constraints:
+        icons = [(rng.standard_normal((2, nu)), rng.standard_normal(2)) for _ in range(N)]
+        for _ in range(int(rng.integers(0, 5))):
+            scons.append(rc.StateConstraint(int(rng.integers(0, M)), int(rng.integers(0, N + 1)),
+                                            rng.standard_normal((1, nx)), rng.standard_normal(1)))
+    spec = rc.OcpSpec(topo, N, q, rng.standard_normal((M, N + 1, nx)), r,
+                      rng.standard_normal((N, nu)), icons, scons)
+    return spec, lin, rng.standard_normal((M, nx))
+
+
+def main():
+    rc, rex, rg, rgr, rmlp, rm, rq = _ref()
+    OUT.mkdir(parents=True, exist_ok=True)
+
+    # cfg1: the reference's own benchmark recipe at chain M=10, N=10 (experiments.py:465-489)
+    out = {}
+    topo, model, states, inputs, spec = rex._scaling_problem(10, 10, 0.01, 0)
+    out["states"], out["inputs"] = states, inputs
+    _model_arrays("", model, out)
+    _spec_arrays("", spec, out)
+    _pipeline("", model, topo, spec, states, inputs, states[0], out, rc, rg, rq, rm, rgr)
+    np.savez_compressed(OUT / "cfg1_chain10.npz", **out)
+
+    # P3: random biases + non-identity normalisation (c != 0; tests/test_gnn.py:91-93 style)
+    out = {}
+    rng = np.random.default_rng(77)
+    topo = rgr.chain_topology(6)
+    model = rg.init_model(3, 6, 0.02, rng, n_m=8, psi_hidden=(16, 12), phi_hidden=(24, 20),
+                          out_scale=0.3)
+    for mlp in (model.psi, model.phi):
+        for b in mlp.biases:
+            b[...] = 0.2 * rng.standard_normal(b.shape)
+    model.normalization = rg.Normalization(0.1 * rng.standard_normal(6), rng.random(6) + 0.5,
+                                           rng.standard_normal(6), rng.random(6) + 0.5)
+    N = 5
+    states = 0.3 * rng.standard_normal((N + 1, 6, 6))
+    inputs = rng.standard_normal((N, 6))
+    q = np.tile(np.diag(rng.random(6) + 0.1), (6, N + 1, 1, 1))
+    spec = rc.OcpSpec(topo, N, q, 0.1 * rng.standard_normal((6, N + 1, 6)),
+                      np.tile(np.eye(6) * 0.5, (N, 1, 1)), np.zeros((N, 6)),
+                      [rc.stage_input_box(6, -1.0, 1.0)] * N,
+                      [rc.StateConstraint(2, 3, rng.standard_normal((2, 6)), np.array([0.5, 0.2])),
+                       rc.StateConstraint(5, N, np.eye(6)[:1], np.array([0.1]), soft=True,
+                                          rho1=10.0, rho2=100.0)])
+    out["states"], out["inputs"] = states, inputs
+    _model_arrays("", model, out)
+    _spec_arrays("", spec, out)
+    _pipeline("", model, topo, spec, states, inputs, states[0], out, rc, rg, rq, rm, rgr)
+    np.savez_compressed(OUT / "p3_biases_norm.npz", **out)
+
+    # P4: interior-solution QP (R = 1.0 I so the optimum is off the box bounds)
+    out = {}
+    topo, model, states, inputs, spec = rex._scaling_problem(12, 8, 0.01, 3)
+    spec = rc.OcpSpec(topo, 8, spec.q, spec.x_ref, np.tile(np.eye(6) * 1.0, (8, 1, 1)),
+                      spec.u_ref, spec.input_constraints, spec.state_constraints)
+    out["states"], out["inputs"] = states, inputs
+    _model_arrays("", model, out)
+    _spec_arrays("", spec, out)
+    _pipeline("", model, topo, spec, states, inputs, states[0], out, rc, rg, rq, rm, rgr)
+    np.savez_compressed(OUT / "p4_interior.npz", **out)
+
+    # P2: random condensing instances from the reference test generator
+    out = {}
+    rng = np.random.default_rng(5)
+    for t in range(12):
+        spec, lin, x0 = random_instance(rng, rc, rg, rgr, with_constraints=(t % 3 != 2))
+        p = f"c{t}_"
+        out[p + "nbr_ptr"] = np.concatenate([[0], np.cumsum([len(n) for n in lin.topology.in_neighbors])])
+        out[p + "nbr_list"] = np.array([j for ns in lin.topology.in_neighbors for j in ns], dtype=np.int64)
+        for k in ("a_self", "a_nbr", "b", "c"):
+            out[p + k] = getattr(lin, k)
+        out[p + "x0"] = x0
+        _spec_arrays(p, spec, out)
+        gu, gx = rc.condense_gammas(lin, x0)
+        out[p + "gamma_u"], out[p + "gamma_x"] = gu, gx
+        qp = rc.condense_ocp(spec, lin, x0)
+        for k in ("h", "g", "c", "d", "soft"):
+            out[p + "qp_" + k] = getattr(qp, k)
+    np.savez_compressed(OUT / "p2_random_condense.npz", **out)
+
+    # QP: random feasible problems (tests/test_qpsolver.py:31-41 family) + reference solutions
+    out = {}
+    rng = np.random.default_rng(42)
+    for t in range(40):
+        n = int(rng.integers(1, 7))
+        m = int(rng.integers(0, 9))
+        A = rng.standard_normal((n, n))
+        H = A @ A.T + np.eye(n) * (0.1 + rng.random())
+        g = rng.standard_normal(n)
+        uf = rng.standard_normal(n)
+        C = rng.standard_normal((m, n))
+        d = C @ uf + rng.random(m) + 0.05
+        sol = rq.solve_qp(rq.QpProblem(H, g, C, d))
+        p = f"q{t}_"
+        out[p + "H"], out[p + "g"], out[p + "C"], out[p + "d"] = H, g, C, d
+        out[p + "u"], out[p + "duals"] = sol.u, sol.duals
+        out[p + "meta"] = np.array([["optimal", "max_iterations", "primal_infeasible",
+                                     "numerical_failure"].index(sol.status.value), sol.iterations])
+    np.savez_compressed(OUT / "qp_random.npz", **out)
+
+    # graph index tables (gnn.py:107-126, condensing.py:158-172), bit-exact targets
+    out = {}
+    graphs = {"chain1": rgr.chain_topology(1), "chain3": rgr.chain_topology(3),
+              "chain7": rgr.chain_topology(7),
+              "iso": rgr.GraphTopology(3, ((), (), ()), 1),
+              "mixed": rgr.GraphTopology(5, ((3, 1), (), (0, 4, 1), (2,), (0,)), 3)}
+    rows, cols = 3, 4
+    mesh = []
+    for r in range(rows):
+        for c in range(cols):
+            ns = []
+            if r > 0: ns.append((r - 1) * cols + c)
+            if c > 0: ns.append(r * cols + c - 1)
+            if c < cols - 1: ns.append(r * cols + c + 1)
+            if r < rows - 1: ns.append((r + 1) * cols + c)
+            mesh.append(tuple(ns))
+    graphs["mesh3x4"] = rgr.GraphTopology(rows * cols, tuple(mesh), 4)
+    for name, topo in graphs.items():
+        dst, src, gather = rg._edge_index(topo)
+        lin = rg.LinearizedDynamics(topo, 1, np.zeros((1, topo.node_count, 1, 1)),
+                                    np.zeros((1, len(topo.edges), 1, 1)),
+                                    np.zeros((1, topo.node_count, 1, 1)),
+                                    np.zeros((1, topo.node_count, 1)))
+        nbr_idx, _ = rc._padded_neighborhood(lin)
+        # edge_slot as the reference computes it inside _padded_neighborhood
+        slots = [s + 1 for ns in topo.in_neighbors for s in range(len(ns))]
+        out[name + "_nbr_ptr"] = np.concatenate([[0], np.cumsum([len(n) for n in topo.in_neighbors])])
+        out[name + "_nbr_list"] = np.array([j for ns in topo.in_neighbors for j in ns], dtype=np.int64)
+        out[name + "_bound"] = np.array(topo.neighbor_bound)
+        out[name + "_dst"], out[name + "_src"], out[name + "_gather"] = dst, src, gather
+        out[name + "_nbr_idx"] = nbr_idx
+        out[name + "_edge_slot"] = np.array(slots, dtype=np.int64)
+        out[name + "_edges"] = np.array(topo.edges, dtype=np.int64).reshape(-1, 2)
+    np.savez_compressed(OUT / "graph_tables.npz", **out)
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,452 @@
+"""Structure-exploiting condensing -- reference-compatible API on the GPU.
+
+Mirrors ``gnnmpc/condensing.py``: ``StateConstraint`` / ``OcpSpec``
+(``:45-129``), ``stage_input_box`` (``:132-138``),
+``cost_to_standard_form`` (``:141-155``), ``condense_gammas``
+(``:182-228``), ``CondensedQp`` / ``condense_ocp`` (``:298-406``),
+``reconstruct_states`` (``:409-416``), ``expand_soft_constraints``
+(``:419-439``).  Conventions kept: the QP objective is ``u'Hu + g'u`` (no 1/2,
+so g carries the factor-2 term), constraint rows are input rows first
+(stage-major), then state rows by node ascending and stage ascending.
+
+The recursion (K-REC), the H/g contraction (K-HG), the constraint mapping and
+the soft expansion run in ``csrc/k_condense.cu``.  Gamma lives on the device
+as one fp32 work array (Gamma_u columns + a Gamma_x column); the arrays
+returned to callers are read-only fp64 NumPy views, and passing them back
+(``condense_ocp(..., gammas=...)``, ``reconstruct_states``) reuses the device
+copy instead of re-uploading.
+"""
+
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import device as _dev
+from .errors import ConfigurationError
+from .graph import GraphTopology, chain_topology
+
+__all__ = [
+    "ConfigurationError", "StateConstraint", "OcpSpec", "stage_input_box", "StandardFormCost",
+    "cost_to_standard_form", "CondensedQp", "condense_gammas", "condense_ocp",
+    "reconstruct_states", "expand_soft_constraints", "min_eig_sym",
+]
+
+
+def min_eig_sym(A: np.ndarray) -> float:
+    return float(np.linalg.eigvalsh(0.5 * (A + A.T))[0])
+
+
+@dataclass
+class StateConstraint:
+    """Half-space rows ``C x_i[k] <= d`` on one node at one stage (``:45-63``)."""
+
+    node: int
+    stage: int
+    c: np.ndarray
+    d: np.ndarray
+    soft: bool = False
+    rho1: float = 1e3
+    rho2: float = 1e4
+
+    def __post_init__(self):
+        self.c = np.atleast_2d(np.asarray(self.c, dtype=float))
+        self.d = np.atleast_1d(np.asarray(self.d, dtype=float))
+        if self.c.shape[0] != self.d.shape[0]:
+            raise ConfigurationError("constraint row count does not match bound length")
+        if self.soft and self.rho2 <= 0:
+            raise ConfigurationError("soft constraints need rho2 > 0")
+
+
+@dataclass
+class OcpSpec:
+    """Tracking OCP data (``condensing.py:66-129``).
+
+    ``freeze()`` marks the cost / reference arrays read-only; frozen arrays are
+    uploaded to the GPU once and reused across ``mpc_step`` calls (unfrozen
+    arrays are re-uploaded on every call, which honours in-place edits)."""
+
+    topology: GraphTopology
+    horizon: int
+    q: np.ndarray
+    x_ref: np.ndarray
+    r: np.ndarray
+    u_ref: np.ndarray
+    input_constraints: list | None = None
+    state_constraints: list = field(default_factory=list)
+
+    def __post_init__(self):
+        M = self.topology.node_count
+        N = self.horizon
+        self.q = np.asarray(self.q, dtype=float)
+        self.x_ref = np.asarray(self.x_ref, dtype=float)
+        self.r = np.asarray(self.r, dtype=float)
+        self.u_ref = np.asarray(self.u_ref, dtype=float)
+        nx = self.q.shape[-1]
+        if self.q.shape != (M, N + 1, nx, nx):
+            raise ConfigurationError("q must be (M, N+1, n_state, n_state)")
+        if self.x_ref.shape != (M, N + 1, nx):
+            raise ConfigurationError("x_ref must be (M, N+1, n_state)")
+        nu = self.r.shape[-1]
+        if self.r.shape != (N, nu, nu):
+            raise ConfigurationError("r must be (N, n_u, n_u)")
+        if self.u_ref.shape != (N, nu):
+            raise ConfigurationError("u_ref must be (N, n_u)")
+        if self.input_constraints is not None:
+            if len(self.input_constraints) != N:
+                raise ConfigurationError("need one input constraint pair per stage")
+            norm = []
+            for C, d in self.input_constraints:
+                C = np.atleast_2d(np.asarray(C, dtype=float))
+                d = np.atleast_1d(np.asarray(d, dtype=float))
+                if C.shape != (d.shape[0], nu):
+                    raise ConfigurationError("input constraint shape mismatch")
+                norm.append((C, d))
+            self.input_constraints = norm
+        for sc in self.state_constraints:
+            if not 0 <= sc.node < M or not 0 <= sc.stage <= N:
+                raise ConfigurationError("state constraint node/stage out of range")
+            if sc.c.shape[1] != nx:
+                raise ConfigurationError("state constraint column count != n_state")
+
+    @property
+    def n_state(self) -> int:
+        return self.q.shape[-1]
+
+    @property
+    def n_u(self) -> int:
+        return self.r.shape[-1]
+
+    def validate_costs(self) -> None:
+        qs = 0.5 * (self.q + np.swapaxes(self.q, -1, -2))
+        if float(np.min(np.linalg.eigvalsh(qs))) < -1e-10:
+            raise ConfigurationError("state cost has eigenvalue below -1e-10")
+        rs = 0.5 * (self.r + np.swapaxes(self.r, -1, -2))
+        if float(np.min(np.linalg.eigvalsh(rs))) < 1e-12:
+            raise ConfigurationError("input cost is not positive definite")
+
+    def freeze(self) -> "OcpSpec":
+        for a in (self.q, self.x_ref, self.r, self.u_ref):
+            a.flags.writeable = False
+        return self
+
+
+def stage_input_box(n_u: int, lo, hi):
+    """Box ``lo <= u <= hi`` as half-space rows ``[I; -I] u <= [hi; -lo]``."""
+    lo = np.broadcast_to(np.asarray(lo, dtype=float), (n_u,))
+    hi = np.broadcast_to(np.asarray(hi, dtype=float), (n_u,))
+    return np.vstack([np.eye(n_u), -np.eye(n_u)]), np.concatenate([hi, -lo])
+
+
+@dataclass
+class StandardFormCost:
+    q_blocks: np.ndarray
+    q_lin: np.ndarray
+    r_blocks: np.ndarray
+    r_lin: np.ndarray
+
+
+def cost_to_standard_form(spec) -> StandardFormCost:
+    """q = -2 Q x_ref, r = -2 R u_ref (``:152-155``).  Host-side data prep for
+    callers; the device path forms the same terms inside K-HG."""
+    q_lin = -2.0 * np.einsum("mkab,mkb->mka", spec.q, spec.x_ref)
+    r_lin = -2.0 * np.einsum("kab,kb->ka", spec.r, spec.u_ref)
+    return StandardFormCost(spec.q, q_lin, spec.r, r_lin)
+
+
+@dataclass
+class CondensedQp:
+    h: np.ndarray
+    g: np.ndarray
+    c: np.ndarray
+    d: np.ndarray
+    soft: np.ndarray
+    rho1: np.ndarray
+    rho2: np.ndarray
+
+
+# ---------------------------------------------------------------------------
+# spec -> device
+# ---------------------------------------------------------------------------
+
+@dataclass
+class SpecRows:
+    """Constraint rows flattened in the reference's stacking order."""
+
+    n_in: int
+    in_stage: np.ndarray
+    in_c: np.ndarray
+    in_d: np.ndarray
+    n_st: int
+    st_node: np.ndarray
+    st_stage: np.ndarray
+    st_c: np.ndarray
+    st_d: np.ndarray
+    soft: np.ndarray
+    rho1: np.ndarray
+    rho2: np.ndarray
+
+    @property
+    def m0(self) -> int:
+        return self.n_in + self.n_st
+
+    @property
+    def soft_idx(self) -> np.ndarray:
+        return np.flatnonzero(self.soft).astype(np.int32)
+
+
+def spec_rows(spec, nx: int, nu: int) -> SpecRows:
+    """Input rows stage-major (``:312-323``), then state rows grouped by node
+    ascending, stage ascending within a node (stable, ``:265-267``)."""
+    in_stage, in_c, in_d = [], [], []
+    if spec.input_constraints is not None:
+        for k, (Ck, dk) in enumerate(spec.input_constraints):
+            Ck = np.atleast_2d(np.asarray(Ck, dtype=float))
+            in_stage.extend([k] * Ck.shape[0])
+            in_c.append(Ck)
+            in_d.append(np.atleast_1d(np.asarray(dk, dtype=float)))
+    n_in = len(in_stage)
+    scs = sorted(spec.state_constraints, key=lambda s: (s.node, s.stage))
+    st_node, st_stage, st_c, st_d, soft, r1, r2 = [], [], [], [], [], [], []
+    for sc in scs:
+        cc = np.atleast_2d(np.asarray(sc.c, dtype=float))
+        rows = cc.shape[0]
+        st_node.extend([sc.node] * rows)
+        st_stage.extend([sc.stage] * rows)
+        st_c.append(cc)
+        st_d.append(np.atleast_1d(np.asarray(sc.d, dtype=float)))
+        soft.extend([bool(sc.soft)] * rows)
+        r1.extend([float(sc.rho1)] * rows)
+        r2.extend([float(sc.rho2)] * rows)
+    n_st = len(st_node)
+    return SpecRows(
+        n_in=n_in, in_stage=np.asarray(in_stage, dtype=np.int32),
+        in_c=np.vstack(in_c) if in_c else np.zeros((0, nu)),
+        in_d=np.concatenate(in_d) if in_d else np.zeros(0),
+        n_st=n_st, st_node=np.asarray(st_node, dtype=np.int32),
+        st_stage=np.asarray(st_stage, dtype=np.int32),
+        st_c=np.vstack(st_c) if st_c else np.zeros((0, nx)),
+        st_d=np.concatenate(st_d) if st_d else np.zeros(0),
+        soft=np.concatenate([np.zeros(n_in, dtype=bool), np.asarray(soft, dtype=bool)]),
+        rho1=np.concatenate([np.zeros(n_in), np.asarray(r1, dtype=float)]),
+        rho2=np.concatenate([np.zeros(n_in), np.asarray(r2, dtype=float)]))
+
+
+def upload_const(eng, arr, dtype):
+    """Upload ``arr``; read-only arrays are cached per engine by identity."""
+    if isinstance(arr, np.ndarray) and not arr.flags.writeable:
+        key = ("const", id(arr), arr.__array_interface__["data"][0], arr.shape, np.dtype(dtype).str)
+        hit = eng.cache.get(key)
+        if hit is not None and hit[0] is arr:
+            return hit[1]
+        t = eng.h2d(arr, dtype)
+        eng.cache[key] = (arr, t)
+        if len(eng.cache) > 64:
+            for k in [k for k in eng.cache if k and k[0] == "const"][:16]:
+                eng.cache.pop(k, None)
+        return t
+    return eng.h2d(arr, dtype)
+
+
+def _ptr(t):
+    return None if t is None or t.numel() == 0 else t.data_ptr()
+
+
+def cost_device(eng, spec, W, ld, N, nx, nu, H0, g0, partial=0):
+    """K-HG: H0 (n0,n0), g0 (n0) fp64 from the device work array W."""
+    q = upload_const(eng, spec.q, np.float64)
+    xr = upload_const(eng, spec.x_ref, np.float64)
+    r = upload_const(eng, spec.r, np.float64)
+    ur = upload_const(eng, spec.u_ref, np.float64)
+    eng.ctx.call("gm_condense_cost", 1, N, W.data_ptr(), ld, q.data_ptr(), 0, xr.data_ptr(), 0,
+                 r.data_ptr(), 0, ur.data_ptr(), 0, H0.data_ptr(), g0.data_ptr(), int(partial),
+                 eng.stream_ptr())
+
+
+def rows_device(eng, rows: SpecRows, W, ld, N, C0, d0):
+    """K-CON: constraint rows C0 (m0, n0), d0 (m0) fp64."""
+    if rows.m0 == 0:
+        return
+    ist = eng.h2d(rows.in_stage, np.int32) if rows.n_in else None
+    ic = eng.h2d(rows.in_c, np.float64) if rows.n_in else None
+    idd = eng.h2d(rows.in_d, np.float64) if rows.n_in else None
+    sn = eng.h2d(rows.st_node, np.int32) if rows.n_st else None
+    ss = eng.h2d(rows.st_stage, np.int32) if rows.n_st else None
+    sc = eng.h2d(rows.st_c, np.float64) if rows.n_st else None
+    sd = eng.h2d(rows.st_d, np.float64) if rows.n_st else None
+    eng.ctx.call("gm_constraint_rows", 1, N, W.data_ptr(), ld, rows.n_in, _ptr(ist), _ptr(ic),
+                 _ptr(idd), rows.n_st, _ptr(sn), _ptr(ss), _ptr(sc), _ptr(sd), C0.data_ptr(),
+                 d0.data_ptr(), eng.stream_ptr())
+
+
+# ---------------------------------------------------------------------------
+# Gamma work array registry (device copy reuse for returned views)
+# ---------------------------------------------------------------------------
+
+_gamma_registry: dict = {}
+
+
+def _register_gammas(gu, gx, W, ld, N, nu):
+    key = id(gu)
+    _gamma_registry[key] = (weakref.ref(gu), weakref.ref(gx), W, ld, N, nu)
+    weakref.finalize(gu, _gamma_registry.pop, key, None)
+
+
+def _lookup_gammas(gammas, eng):
+    gu, gx = gammas
+    hit = _gamma_registry.get(id(gu))
+    if hit is None:
+        return None
+    rgu, rgx, W, ld, N, nu = hit
+    if rgu() is gu and rgx() is gx and W.device == eng.device:
+        return W, ld
+    return None
+
+
+def _upload_gammas(eng, gu, gx, N, nx, nu):
+    """Pack host (gamma_u, gamma_x) into the device work-array layout."""
+    from ._runtime import lib
+
+    M = gu.shape[0]
+    ld = lib().gm_gamma_ld(N, nu)
+    Wh = np.zeros((M, N + 1, nx, ld), dtype=np.float32)
+    Wh[..., : N * nu] = gu
+    Wh[..., N * nu] = gx
+    return eng.h2d(Wh, np.float32), ld
+
+
+def gammas_device(eng, lin, x0, N, nx, nu):
+    """Run K-REC; returns (W, ld) with W (M, N+1, nx, ld) fp32 on the device."""
+    from ._runtime import lib
+
+    ld = lib().gm_gamma_ld(N, nu)
+    a_self, a_nbr, b, c = lin
+    W = eng.empty((eng.M, N + 1, nx, ld), np.float32)
+    eng.ctx.call("gm_condense_gammas", 1, N, a_self.data_ptr(), _ptr(a_nbr), b.data_ptr(),
+                 c.data_ptr(), x0.data_ptr(), W.data_ptr(), ld, eng.stream_ptr())
+    return W, ld
+
+
+def _materialise(W, N, nu):
+    Wn = W.double().cpu().numpy()
+    Wn.flags.writeable = False
+    return Wn[..., : N * nu], Wn[..., N * nu]
+
+
+# ---------------------------------------------------------------------------
+# public API
+# ---------------------------------------------------------------------------
+
+def condense_gammas(lin, x0, threads: int = 1):
+    """Per-node prediction maps (``condensing.py:182-228``) computed by K-REC.
+
+    Returns ``(gamma_u (M, N+1, nx, N*nu), gamma_x (M, N+1, nx))``.  ``threads``
+    is accepted for API compatibility; the GPU parallelises over nodes and
+    columns regardless (results are bitwise independent of it, like the
+    reference's)."""
+    topo = lin.topology
+    N, nx, nu = lin.horizon, lin.n_state, lin.n_u
+    eng = _dev.engine(topo)
+    eng.set_dims(nx, nu)
+    blocks = lin.device_blocks(eng)
+    x0d = eng.h2d(np.asarray(x0, dtype=float).reshape(topo.node_count, nx), np.float64)
+    W, ld = gammas_device(eng, blocks, x0d, N, nx, nu)
+    gu, gx = _materialise(W, N, nu)
+    _register_gammas(gu, gx, W, ld, N, nu)
+    return gu, gx
+
+
+def condense_ocp(spec, lin, x0, threads: int = 1, gammas=None) -> CondensedQp:
+    """Condensed QP ``min u'Hu + g'u s.t. Cu <= d`` (``condensing.py:363-406``)."""
+    topo = spec.topology
+    N, nx, nu = spec.horizon, spec.n_state, spec.n_u
+    eng = _dev.engine(topo)
+    eng.set_dims(nx, nu)
+    if gammas is not None:
+        hit = _lookup_gammas(gammas, eng)
+        if hit is None:
+            W, ld = _upload_gammas(eng, np.asarray(gammas[0]), np.asarray(gammas[1]), N, nx, nu)
+        else:
+            W, ld = hit
+    else:
+        blocks = lin.device_blocks(eng)
+        x0d = eng.h2d(np.asarray(x0, dtype=float).reshape(topo.node_count, nx), np.float64)
+        W, ld = gammas_device(eng, blocks, x0d, N, nx, nu)
+    n0 = N * nu
+    rows = spec_rows(spec, nx, nu)
+    H0 = eng.empty((n0, n0), np.float64)
+    g0 = eng.empty((n0,), np.float64)
+    cost_device(eng, spec, W, ld, N, nx, nu, H0, g0)
+    C0 = eng.empty((rows.m0, n0), np.float64)
+    d0 = eng.empty((rows.m0,), np.float64)
+    rows_device(eng, rows, W, ld, N, C0, d0)
+    return CondensedQp(h=H0.cpu().numpy(), g=g0.cpu().numpy(), c=C0.cpu().numpy(),
+                       d=d0.cpu().numpy(), soft=rows.soft.copy(), rho1=rows.rho1.copy(),
+                       rho2=rows.rho2.copy())
+
+
+def expand_soft_device(eng, n0, m0, H0, g0, C0, d0, soft_idx, rho1, rho2):
+    """Device soft-constraint expansion; returns (H, g, C, d) tensors."""
+    ns = int(soft_idx.size)
+    n, m = n0 + ns, m0 + ns
+    H = eng.empty((n, n), np.float64)
+    g = eng.empty((n,), np.float64)
+    C = eng.empty((m, n), np.float64)
+    d = eng.empty((m,), np.float64)
+    idx = eng.h2d(soft_idx, np.int32)
+    r1 = eng.h2d(rho1, np.float64)
+    r2 = eng.h2d(rho2, np.float64)
+    eng.ctx.call("gm_expand_soft", 1, n0, m0, H0.data_ptr(), g0.data_ptr(), _ptr(C0), _ptr(d0), ns,
+                 idx.data_ptr(), r1.data_ptr(), r2.data_ptr(), H.data_ptr(), g.data_ptr(),
+                 C.data_ptr(), d.data_ptr(), eng.stream_ptr())
+    return H, g, C, d
+
+
+_qp_topo = chain_topology(1)
+
+
+def expand_soft_constraints(qp: CondensedQp):
+    """One penalised slack per soft row (``condensing.py:419-439``).
+    Returns ``(H, g, C, d, n_original)``."""
+    idx = np.flatnonzero(qp.soft)
+    n = qp.h.shape[0]
+    if idx.size == 0:
+        return qp.h, qp.g, qp.c, qp.d, n
+    eng = _dev.engine(_qp_topo)
+    m0 = qp.c.shape[0]
+    H, g, C, d = expand_soft_device(
+        eng, n, m0, eng.h2d(qp.h, np.float64), eng.h2d(qp.g, np.float64),
+        eng.h2d(qp.c, np.float64), eng.h2d(qp.d, np.float64), idx.astype(np.int32),
+        np.asarray(qp.rho1, dtype=float)[idx], np.asarray(qp.rho2, dtype=float)[idx])
+    return H.cpu().numpy(), g.cpu().numpy(), C.cpu().numpy(), d.cpu().numpy(), n
+
+
+def reconstruct_states(gamma_u, gamma_x, u) -> np.ndarray:
+    """Planned trajectories ``x^i = Gamma_u^i u + Gamma_x^i`` (``:409-416``);
+    accepts all-node (M, N+1, nx, N*nu) or single-node (N+1, nx, N*nu) maps."""
+    u = np.asarray(u, dtype=float).reshape(-1)
+    gu = np.asarray(gamma_u)
+    single = gu.ndim == 3
+    if single:
+        gu = gu[None]
+    gx = np.asarray(gamma_x)
+    if single:
+        gx = gx[None]
+    M, Np1, nx, n0 = gu.shape
+    N = Np1 - 1
+    nu = n0 // N if N else 1
+    eng = _dev.engine(_qp_topo)  # one-node graph: every node is an "instance"
+    eng.set_dims(nx, nu)
+    hit = None if single else _lookup_gammas((gamma_u, gamma_x), eng)
+    if hit is None:
+        W, ld = _upload_gammas(eng, gu, gx, N, nx, nu)
+    else:
+        W, ld = hit
+    ud = eng.h2d(u, np.float64)
+    x = eng.empty((M, N + 1, nx), np.float64)
+    eng.ctx.call("gm_reconstruct_states", M, N, W.data_ptr(), ld, ud.data_ptr(), 0, x.data_ptr(),
+                 eng.stream_ptr())
+    out = x.cpu().numpy()
+    return out[0] if single else out

@@ -1,0 +1,65 @@
+"""Full-size parity: the cfg3 workload (chain M=1000, N=20, the paper's 100 Hz
+headline) on the GPU against the CPU oracle on the same seeded inputs, and
+size-independent properties at the larger configs."""
+
+import numpy as np
+import pytest
+
+from tests.golden_io import rel
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    from oracle import ref_port as O
+    from paper_2602_17601_b200 import workloads
+
+    topo, model, states, inputs, spec = workloads.scaling_problem(1000, 20, 0.01, 0)
+    lin = O.linearize_trajectory(model, topo, states, inputs)
+    gu, gx = O.condense_gammas(lin, states[0])
+    qp = O.condense_ocp(spec, lin, states[0], gammas=(gu, gx))
+    H, g, C, d, n0 = O.expand_soft_constraints(qp)
+    sol = O.solve_qp(H, g, C, d)
+    return dict(topo=topo, model=model, states=states, inputs=inputs, spec=spec, lin=lin, gu=gu,
+                gx=gx, qp=qp, sol=sol, n0=n0)
+
+
+def test_cfg3_stages(cfg3):
+    import paper_2602_17601_b200 as pkg
+
+    c = cfg3
+    lin = pkg.linearize_trajectory(c["model"], c["topo"], c["states"], c["inputs"])
+    for k in ("a_self", "a_nbr", "b"):
+        assert rel(getattr(lin, k), getattr(c["lin"], k)) <= TOL, k
+    assert np.max(np.abs(lin.c - c["lin"].c)) / np.max(np.abs(c["states"])) <= TOL
+    gu, gx = pkg.condense_gammas(lin, c["states"][0])
+    assert rel(gu, c["gu"]) <= TOL
+    assert rel(gx, c["gx"]) <= TOL
+    qp = pkg.condense_ocp(c["spec"], lin, c["states"][0], gammas=(gu, gx))
+    assert rel(qp.h, c["qp"].h) <= TOL
+    assert rel(qp.g, c["qp"].g) <= TOL
+    assert rel(qp.c, c["qp"].c) <= TOL
+
+
+def test_cfg3_mpc_step_u0(cfg3):
+    import paper_2602_17601_b200 as pkg
+
+    c = cfg3
+    N = 20
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+    x = pkg.SystemState(c["states"][0])
+    st = pkg.mpc_init(x, cfg, 6)
+    st.lin_states = np.concatenate([c["states"], c["states"][-1:]], axis=0)
+    st.lin_inputs = c["inputs"]
+    u, st1 = pkg.mpc_step(c["model"], c["topo"], c["spec"], x, st, cfg)
+    from oracle import ref_port as O
+
+    ref = O.mpc_step(c["model"], c["topo"], c["spec"], c["states"][0], st.lin_states,
+                     st.lin_inputs, N)
+    assert st1.last_status.value == ref["status"]
+    scale = max(1.0, float(np.max(np.abs(ref["u_applied"]))))
+    assert float(np.max(np.abs(u.u - ref["u_applied"]))) / scale <= TOL
+    assert rel(st1.planned_inputs, ref["planned_inputs"]) <= TOL

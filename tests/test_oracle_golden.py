@@ -1,0 +1,117 @@
+"""Pin the CPU oracle (oracle/ref_port.py) against golden vectors produced by
+the reference itself (oracle/make_golden.py), and pin the synthetic-workload
+generator against the reference's own recipe (experiments.py:465-489).
+CPU only."""
+
+import numpy as np
+import pytest
+
+from oracle import ref_port as O
+from tests.golden_io import (STATUS, load, pipeline_case, random_condense_cases, random_qps, rel,
+                             topo_from_ptr)
+
+CASES = ["cfg1_chain10", "p3_biases_norm", "p4_interior"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_pipeline_matches_reference(name):
+    cs = pipeline_case(name)
+    d = cs.d
+    lin = O.linearize_trajectory(cs.model, cs.topo, cs.states, cs.inputs)
+    for k in ("a_self", "a_nbr", "b", "c"):
+        assert np.max(np.abs(getattr(lin, k) - d["lin_" + k])) <= 1e-13, k
+    gu, gx = O.condense_gammas(lin, cs.x0)
+    assert rel(gu, d["gamma_u"]) <= 1e-13 and rel(gx, d["gamma_x"]) <= 1e-13
+    qp = O.condense_ocp(cs.spec, lin, cs.x0, gammas=(gu, gx))
+    assert rel(qp.h, d["qp_h"]) <= 1e-13 and rel(qp.g, d["qp_g"]) <= 1e-13
+    if qp.c.size:
+        assert rel(qp.c, d["qp_c"]) <= 1e-13
+    assert np.array_equal(qp.soft, d["qp_soft"])
+    H, g, C, dd, n0 = O.expand_soft_constraints(qp)
+    assert rel(H, d["x_H"]) <= 1e-13 and rel(C, d["x_C"]) <= 1e-13
+    sol = O.solve_qp(H, g, C, dd)
+    assert sol.status == STATUS[int(d["sol_meta"][0])]
+    assert sol.iterations == int(d["sol_meta"][1])
+    assert np.max(np.abs(sol.u - d["sol_u"])) <= 1e-8
+    rec = O.reconstruct_states(gu, gx, sol.u[:n0])
+    assert rel(rec, d["recon"]) <= 1e-10
+    out = O.mpc_step(cs.model, cs.topo, cs.spec, cs.x0, np.tile(cs.x0, (cs.spec.horizon + 1, 1, 1)),
+                     np.zeros((cs.spec.horizon, cs.spec.n_u)), cs.spec.horizon)
+    assert out["status"] == STATUS[int(d["mpc_meta"][0])]
+    assert np.max(np.abs(out["u_applied"] - d["mpc_u"])) <= 1e-8
+    assert rel(out["lin_states"], d["mpc_lin_states"]) <= 1e-10
+    out2 = O.mpc_step(cs.model, cs.topo, cs.spec, cs.x0, out["lin_states"], out["lin_inputs"],
+                      cs.spec.horizon)
+    assert np.max(np.abs(out2["u_applied"] - d["mpc2_u"])) <= 1e-8
+
+
+def test_oracle_random_condense_instances():
+    for t, cs in enumerate(random_condense_cases()):
+        gu, gx = O.condense_gammas(cs.lin, cs.x0)
+        assert rel(gu, cs.gamma_u) <= 1e-13, t
+        assert rel(gx, cs.gamma_x) <= 1e-13, t
+        qp = O.condense_ocp(cs.spec, cs.lin, cs.x0)
+        assert rel(qp.h, cs.qp["h"]) <= 1e-13, t
+        assert rel(qp.g, cs.qp["g"]) <= 1e-13, t
+        assert qp.c.shape == cs.qp["c"].shape
+        assert np.array_equal(qp.soft, cs.qp["soft"])
+
+
+def test_oracle_random_qps():
+    for t, q in enumerate(random_qps()):
+        sol = O.solve_qp(q.H, q.g, q.C, q.d)
+        assert sol.status == q.status, t
+        assert sol.iterations == q.iterations, t
+        assert np.max(np.abs(sol.u - q.u)) <= 1e-9, t
+
+
+def test_oracle_graph_tables():
+    d = load("graph_tables")
+    names = sorted({k.rsplit("_", 2)[0] for k in d if k.endswith("_nbr_ptr")})
+    assert names
+    for name in names:
+        topo = topo_from_ptr(d[name + "_nbr_ptr"], d[name + "_nbr_list"], d[name + "_bound"])
+        dst, src, gather = O.edge_lists(topo)
+        nbr_idx, slots = O.slot_tables(topo)
+        assert np.array_equal(dst, d[name + "_dst"]) and np.array_equal(src, d[name + "_src"])
+        assert np.array_equal(gather, d[name + "_gather"])
+        assert np.array_equal(nbr_idx, d[name + "_nbr_idx"])
+        assert np.array_equal(slots, d[name + "_edge_slot"])
+
+
+def test_workload_generator_matches_reference_recipe():
+    """workloads.scaling_problem reproduces _scaling_problem bit for bit."""
+    from paper_2602_17601_b200 import workloads
+
+    cs = pipeline_case("cfg1_chain10")
+    topo, model, states, inputs, spec = workloads.scaling_problem(10, 10, 0.01, 0)
+    assert np.array_equal(states, cs.states) and np.array_equal(inputs, cs.inputs)
+    for a, b in zip(model.psi.weights + model.phi.weights,
+                    cs.model.psi.weights + cs.model.phi.weights):
+        assert np.array_equal(a, b)
+    assert np.array_equal(spec.q, cs.spec.q) and np.array_equal(spec.x_ref, cs.spec.x_ref)
+    assert np.array_equal(spec.r, cs.spec.r)
+    assert [(s.node, s.stage, s.soft) for s in spec.state_constraints] == \
+        [(s.node, s.stage, s.soft) for s in cs.spec.state_constraints]
+    assert all(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+               for a, b in zip(spec.input_constraints, cs.spec.input_constraints))
+
+
+def test_hand_known_answers():
+    """Known answers from the reference tests."""
+    from types import SimpleNamespace
+
+    from paper_2602_17601_b200.graph import GraphTopology, chain_topology
+
+    topo = GraphTopology(1, ((),), 1)
+    lin = SimpleNamespace(topology=topo, horizon=2, a_self=np.full((2, 1, 1, 1), 2.0),
+                          a_nbr=np.zeros((2, 0, 1, 1)), b=np.full((2, 1, 1, 1), 1.0),
+                          c=np.zeros((2, 1, 1)))
+    gu, gx = O.condense_gammas(lin, np.array([[1.0]]))
+    assert np.allclose(gu[0].reshape(3, 2), [[0, 0], [1, 0], [2, 1]])
+    assert np.allclose(gx[0].reshape(3), [1, 2, 4])
+    sol = O.solve_qp(np.array([[1.0]]), np.array([-2.0]), np.array([[1.0]]), np.array([0.5]))
+    assert sol.status == "optimal" and abs(sol.u[0] - 0.5) <= 1e-7 and abs(sol.duals[0] - 1) <= 1e-6
+    t3 = chain_topology(3)
+    assert t3.edges == [(0, 1), (1, 0), (1, 2), (2, 1)]
+    assert t3.closed_neighbors(1) == (1, 0, 2)
