@@ -1,0 +1,336 @@
+"""Benchmark of the B200 GNN-MPC hot path (one RTI step: linearize + condense +
+QP + epilogue) on BASELINE.json's headline workload, cfg3: chain graph with
+M = 1,000 nodes, horizon N = 20 (the paper's 100 Hz claim).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on stdout (rank 0).  A "step" is one mpc_step of the cfg3
+instance from the same initial controller state (identical work every step):
+
+* value      device time of the captured kernel chain with every input already
+             in HBM, L2 flushed (256 MiB write) between timed steps; whole-job
+             solves/s = n_gpus * 1000 / max-over-ranks ms.
+* e2e        the public API mpc_step(model, topo, spec, x_measured, state, cfg)
+             with the measurement in pinned host memory: H2D of x_measured,
+             the kernels, D2H of [u_applied, status, iterations], wall clock.
+* roofline   the dominant kernel (per-launch CUDA-event time inside the timed
+             region) against its hardware ceiling.
+* cpu_baseline / --impl reference: the CPU oracle port of the reference path
+  (oracle/ref_port.py; the reference is pure Python and is not on the GPU box).
+
+Multi-GPU (torchrun): every rank solves its own independent instance (weak
+scaling, no data-path collective); timing is max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MPC step latency ms (linearize+condense+QP) & Hz at N nodes; solves/sec batched"
+M_NODES, HORIZON = 1000, 20
+WORKLOAD = "cfg3: chain graph M=1000 nodes, horizon N=20, _scaling_problem recipe (paper 100 Hz headline)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--nodes", type=int, default=M_NODES)
+    ap.add_argument("--horizon", type=int, default=HORIZON)
+    ap.add_argument("--cpu-steps", type=int, default=8, help="oracle steps for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-l2-flush", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def problem(M, N):
+    from paper_2602_17601_b200 import workloads
+
+    topo, model, states, inputs, spec = workloads.scaling_problem(M, N, 0.01, 0)
+    return topo, model, states, inputs, spec
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port = the reference algorithm on the host cores)
+# ---------------------------------------------------------------------------
+
+def cpu_oracle_steps(M, N, steps, warmup, threads):
+    from threadpoolctl import threadpool_limits
+
+    from oracle import ref_port as O
+
+    topo, model, states, inputs, spec = problem(M, N)
+    x0 = states[0]
+    ls0 = np.tile(x0, (N + 1, 1, 1))
+    li0 = np.zeros((N, 6))
+    times = []
+    with threadpool_limits(limits=threads):
+        for k in range(warmup + steps):
+            t0 = time.perf_counter()
+            O.mpc_step(model, topo, spec, x0, ls0, li0, N, threads=threads)
+            dt = time.perf_counter() - t0
+            if k >= warmup:
+                times.append(dt)
+    return float(np.mean(times)) * 1e3
+
+
+def reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    ms = cpu_oracle_steps(args.nodes, args.horizon, args.steps, args.warmup, cores)
+    v = 1000.0 / ms
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "nodes": args.nodes,
+                                        "horizon": args.horizon, "parallelism": "host cores"},
+        "cpu_baseline": {"value": v, "unit": "solves/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} oracle mpc_step calls (after {args.warmup} "
+                                   f"warm-up) at M={args.nodes}, N={args.horizon}, BLAS threads "
+                                   f"= condense threads = {cores}"},
+        "e2e": {"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1].split()[0]))
+                smax = float(parts[2].split()[0])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def qp_flops(n, m, ng, iters):
+    """Algorithmic fp64 flops of the IPM on the expanded QP (qpsolver.py:170-229):
+    per iteration Schur build 2*ng*n^2/2, Cholesky n^3/3, 4 triangular solves 4n^2,
+    H u / C products ~ 2n^2 + 4 m n (dense count of single-nonzero rows excluded)."""
+    per = ng * n * n + n ** 3 / 3.0 + 4.0 * n * n + 2.0 * n * n + 4.0 * ng * n
+    return per * max(iters, 1)
+
+
+def ours_arm(args, world, rank, local):
+    import torch
+
+    import paper_2602_17601_b200 as pkg
+    from paper_2602_17601_b200 import _runtime
+    from paper_2602_17601_b200.mpc import get_plan
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    M, N = args.nodes, args.horizon
+    topo, model, states, inputs, spec = problem(M, N)
+    spec.freeze()
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+    x0 = states[0]
+    xs = pkg.SystemState(x0)
+    # device-resident initial controller state (mpc_init values)
+    st0 = pkg.MpcState(lin_states=torch.from_numpy(np.tile(x0, (N + 1, 1, 1))).to(dev),
+                       lin_inputs=torch.zeros((N, 6), dtype=torch.float64, device=dev))
+    # first calls: upload, eager run, CUDA-graph capture
+    for _ in range(3):
+        u, st1 = pkg.mpc_step(model, topo, spec, xs, st0, cfg)
+    eng = pkg.device.engine(topo, model)
+    plan = get_plan(eng, spec, N, 6, 6, cfg, True)
+    assert plan.graphs is not None, "plan was not captured as CUDA graphs"
+    status, iters = st1.last_status.value, st1.last_iterations
+
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    L = _runtime.lib()
+
+    # ---- device-resident timing (value) ----
+    for _ in range(args.warmup):
+        plan.enqueue(timed=True)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    step_ms, lin_ms, cond_ms, solve_ms = [], [], [], []
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        if not args.no_l2_flush:
+            flush.fill_(1.0)
+        plan.enqueue(timed=True)
+        torch.cuda.synchronize()
+        a, b, c = plan.stage_ms()
+        lin_ms.append(a)
+        cond_ms.append(b)
+        solve_ms.append(c)
+        step_ms.append(plan.events[0].elapsed_time(plan.events[3]))
+    torch.cuda.synchronize()
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- end to end through the public API (value e2e) ----
+    e2e = []
+    for _ in range(args.warmup):
+        pkg.mpc_step(model, topo, spec, xs, st0, cfg)
+    for _ in range(args.steps):
+        if not args.no_l2_flush:
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        u, st1 = pkg.mpc_step(model, topo, spec, xs, st0, cfg)
+        e2e.append(time.perf_counter() - t0)
+    clk = clocks.stop()
+    e2e_ms = float(np.mean(e2e)) * 1e3
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # kernels launched per step: count one eager (uncaptured) enqueue
+    l1 = L.gm_launch_count()
+    saved = plan.graphs
+    plan.graphs = None
+    plan.enqueue(timed=False)
+    plan.graphs = saved
+    torch.cuda.synchronize()
+    kernels_per_step = int(L.gm_launch_count() - l1)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    # ---- roofline of the dominant kernel ----
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else {}
+    smax = (peaks.get("sm_max_mhz") or 1965.0) * 1e6
+    solve = float(np.mean(solve_ms))
+    n, m = plan.n, plan.m
+    ng = plan.ds.ns + (plan.ds.rows.n_st)  # general (multi-nonzero) rows: the soft rows
+    fl = qp_flops(n, m, ng, iters)
+    fp64_sm_peak = 64 * 2 * smax / 1e12  # one CTA on one SM: 64 DFMA/clk
+    roof = {"kernel": "k_solve_qp (+k_finish)", "bound": "fp64-one-SM",
+            "achieved": fl / (solve * 1e-3) / 1e12, "peak": fp64_sm_peak, "unit": "TFLOP/s",
+            "frac": (fl / (solve * 1e-3) / 1e12) / fp64_sm_peak, "traffic": None,
+            "note": "latency-bound single-CTA fp64 IPM; peak = FP64 FMA rate of one SM at max clock"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cms = cpu_oracle_steps(M, N, args.cpu_steps, 1, 1)
+        cpu = {"value": 1000.0 / cms, "unit": "solves/s", "cores": 1, "kind": "port",
+               "sample": f"{args.cpu_steps} oracle mpc_step calls at M={M}, N={N} (1 warm-up), "
+                         "BLAS pinned to 1 thread (reference protocol experiments.py:492-528)",
+               "ms_per_step": cms}
+    out = {
+        "metric": METRIC, "value": world * 1000.0 / ms, "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "hz": 1000.0 / ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 (linearize Jacobians, Gamma, H) / f64 (MLP forward, offsets, QP)",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "nodes": M, "horizon": N, "instances_per_gpu": 1,
+                   "parallelism": f"independent instance per GPU x{world}",
+                   "l2": "flushed (256 MiB write) between timed steps" if not args.no_l2_flush
+                   else "not flushed", "qp": {"n": n, "m": m, "status": status,
+                                              "iterations": iters}},
+        "stage_ms": {"linearize": float(np.mean(lin_ms)), "condense": float(np.mean(cond_ms)),
+                     "solve_and_epilogue": solve},
+        "e2e": {"value": world * 1000.0 / e2e_ms, "unit": "solves/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": M * 6 * 8, "d2h_bytes_per_step": (6 + 2) * 8,
+                "path": "paper_2602_17601_b200.mpc_step (public API), host numpy measurement"},
+        "gpu_launches": kernels_per_step,
+        "gpu_launch_mode": "CUDA graphs (3 replays/step)",
+        "clocks": clk,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+        return
+    ours_arm(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -62,6 +62,10 @@ typedef struct gm_qp_settings {
 
 int gm_abi_version(void);
 
+/* Number of kernels this library has launched in the process (all
+ * contexts); bench.py reports the per-step delta as gpu_launches. */
+int64_t gm_launch_count(void);
+
 /* Context.  device < 0 creates a host-only context: graph index
  * construction works, every device entry point returns GM_ERR_CONFIG. */
 int gm_create(gm_ctx** out, int device);

@@ -128,8 +128,20 @@ class OcpSpec:
             raise ConfigurationError("input cost is not positive definite")
 
     def freeze(self) -> "OcpSpec":
+        """Make the spec immutable (arrays read-only, constraint lists tuples) so
+        its device copy can be cached across steps."""
         for a in (self.q, self.x_ref, self.r, self.u_ref):
             a.flags.writeable = False
+        if self.input_constraints is not None:
+            for C, d in self.input_constraints:
+                C.flags.writeable = False
+                d.flags.writeable = False
+            self.input_constraints = tuple(self.input_constraints)
+        for sc in self.state_constraints:
+            sc.c.flags.writeable = False
+            sc.d.flags.writeable = False
+        self.state_constraints = tuple(self.state_constraints)
+        object.__setattr__(self, "_frozen", True)
         return self
 
 
@@ -234,51 +246,65 @@ def spec_rows(spec, nx: int, nu: int) -> SpecRows:
         rho2=np.concatenate([np.zeros(n_in), np.asarray(r2, dtype=float)]))
 
 
-def upload_const(eng, arr, dtype):
-    """Upload ``arr``; read-only arrays are cached per engine by identity."""
-    if isinstance(arr, np.ndarray) and not arr.flags.writeable:
-        key = ("const", id(arr), arr.__array_interface__["data"][0], arr.shape, np.dtype(dtype).str)
-        hit = eng.cache.get(key)
-        if hit is not None and hit[0] is arr:
-            return hit[1]
-        t = eng.h2d(arr, dtype)
-        eng.cache[key] = (arr, t)
-        if len(eng.cache) > 64:
-            for k in [k for k in eng.cache if k and k[0] == "const"][:16]:
-                eng.cache.pop(k, None)
-        return t
-    return eng.h2d(arr, dtype)
+class DeviceSpec:
+    """Everything of an OcpSpec the device path reads, uploaded once."""
+
+    def __init__(self, eng, spec, nx: int, nu: int):
+        f64, i32 = np.float64, np.int32
+        self.rows = rows = spec_rows(spec, nx, nu)
+        self.q = eng.h2d(spec.q, f64)
+        self.x_ref = eng.h2d(spec.x_ref, f64)
+        self.r = eng.h2d(spec.r, f64)
+        self.u_ref = eng.h2d(spec.u_ref, f64)
+        self.in_stage = eng.h2d(rows.in_stage, i32) if rows.n_in else None
+        self.in_c = eng.h2d(rows.in_c, f64) if rows.n_in else None
+        self.in_d = eng.h2d(rows.in_d, f64) if rows.n_in else None
+        self.st_node = eng.h2d(rows.st_node, i32) if rows.n_st else None
+        self.st_stage = eng.h2d(rows.st_stage, i32) if rows.n_st else None
+        self.st_c = eng.h2d(rows.st_c, f64) if rows.n_st else None
+        self.st_d = eng.h2d(rows.st_d, f64) if rows.n_st else None
+        self.soft_idx = rows.soft_idx
+        self.ns = int(self.soft_idx.size)
+        if self.ns:
+            self.idx = eng.h2d(self.soft_idx, i32)
+            self.rho1 = eng.h2d(rows.rho1[self.soft_idx], f64)
+            self.rho2 = eng.h2d(rows.rho2[self.soft_idx], f64)
+
+
+def device_spec(eng, spec, nx: int, nu: int) -> DeviceSpec:
+    """Device copy of ``spec``; cached per engine for frozen specs
+    (``OcpSpec.freeze``), rebuilt on every call otherwise."""
+    if not getattr(spec, "_frozen", False):
+        return DeviceSpec(eng, spec, nx, nu)
+    key = ("spec", id(spec), nx, nu)
+    hit = eng.cache.get(key)
+    if hit is not None and hit[0]() is spec:
+        return hit[1]
+    ds = DeviceSpec(eng, spec, nx, nu)
+    eng.cache[key] = (weakref.ref(spec), ds)
+    weakref.finalize(spec, eng.cache.pop, key, None)
+    return ds
 
 
 def _ptr(t):
     return None if t is None or t.numel() == 0 else t.data_ptr()
 
 
-def cost_device(eng, spec, W, ld, N, nx, nu, H0, g0, partial=0):
+def cost_device(eng, ds: DeviceSpec, W, ld, N, H0, g0, partial=0):
     """K-HG: H0 (n0,n0), g0 (n0) fp64 from the device work array W."""
-    q = upload_const(eng, spec.q, np.float64)
-    xr = upload_const(eng, spec.x_ref, np.float64)
-    r = upload_const(eng, spec.r, np.float64)
-    ur = upload_const(eng, spec.u_ref, np.float64)
-    eng.ctx.call("gm_condense_cost", 1, N, W.data_ptr(), ld, q.data_ptr(), 0, xr.data_ptr(), 0,
-                 r.data_ptr(), 0, ur.data_ptr(), 0, H0.data_ptr(), g0.data_ptr(), int(partial),
-                 eng.stream_ptr())
+    eng.ctx.call("gm_condense_cost", 1, N, W.data_ptr(), ld, ds.q.data_ptr(), 0,
+                 ds.x_ref.data_ptr(), 0, ds.r.data_ptr(), 0, ds.u_ref.data_ptr(), 0,
+                 H0.data_ptr(), g0.data_ptr(), int(partial), eng.stream_ptr())
 
 
-def rows_device(eng, rows: SpecRows, W, ld, N, C0, d0):
+def rows_device(eng, ds: DeviceSpec, W, ld, N, C0, d0):
     """K-CON: constraint rows C0 (m0, n0), d0 (m0) fp64."""
+    rows = ds.rows
     if rows.m0 == 0:
         return
-    ist = eng.h2d(rows.in_stage, np.int32) if rows.n_in else None
-    ic = eng.h2d(rows.in_c, np.float64) if rows.n_in else None
-    idd = eng.h2d(rows.in_d, np.float64) if rows.n_in else None
-    sn = eng.h2d(rows.st_node, np.int32) if rows.n_st else None
-    ss = eng.h2d(rows.st_stage, np.int32) if rows.n_st else None
-    sc = eng.h2d(rows.st_c, np.float64) if rows.n_st else None
-    sd = eng.h2d(rows.st_d, np.float64) if rows.n_st else None
-    eng.ctx.call("gm_constraint_rows", 1, N, W.data_ptr(), ld, rows.n_in, _ptr(ist), _ptr(ic),
-                 _ptr(idd), rows.n_st, _ptr(sn), _ptr(ss), _ptr(sc), _ptr(sd), C0.data_ptr(),
-                 d0.data_ptr(), eng.stream_ptr())
+    eng.ctx.call("gm_constraint_rows", 1, N, W.data_ptr(), ld, rows.n_in, _ptr(ds.in_stage),
+                 _ptr(ds.in_c), _ptr(ds.in_d), rows.n_st, _ptr(ds.st_node), _ptr(ds.st_stage),
+                 _ptr(ds.st_c), _ptr(ds.st_d), C0.data_ptr(), d0.data_ptr(), eng.stream_ptr())
 
 
 # ---------------------------------------------------------------------------
@@ -375,13 +401,14 @@ def condense_ocp(spec, lin, x0, threads: int = 1, gammas=None) -> CondensedQp:
         x0d = eng.h2d(np.asarray(x0, dtype=float).reshape(topo.node_count, nx), np.float64)
         W, ld = gammas_device(eng, blocks, x0d, N, nx, nu)
     n0 = N * nu
-    rows = spec_rows(spec, nx, nu)
+    ds = device_spec(eng, spec, nx, nu)
+    rows = ds.rows
     H0 = eng.empty((n0, n0), np.float64)
     g0 = eng.empty((n0,), np.float64)
-    cost_device(eng, spec, W, ld, N, nx, nu, H0, g0)
+    cost_device(eng, ds, W, ld, N, H0, g0)
     C0 = eng.empty((rows.m0, n0), np.float64)
     d0 = eng.empty((rows.m0,), np.float64)
-    rows_device(eng, rows, W, ld, N, C0, d0)
+    rows_device(eng, ds, W, ld, N, C0, d0)
     return CondensedQp(h=H0.cpu().numpy(), g=g0.cpu().numpy(), c=C0.cpu().numpy(),
                        d=d0.cpu().numpy(), soft=rows.soft.copy(), rho1=rows.rho1.copy(),
                        rho2=rows.rho2.copy())

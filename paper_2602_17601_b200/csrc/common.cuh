@@ -77,6 +77,7 @@ struct gm_ctx {
   // scratch (grown on demand, stream-ordered use only)
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  std::vector<void*> retired;  // outgrown scratch kept alive: captured CUDA graphs may use it
   int sm_count = 148;
   size_t smem_optin = 227 * 1024;
 };
@@ -93,8 +94,11 @@ void* gm_scratch(gm_ctx* ctx, size_t bytes);
     if (_e != cudaSuccess) return gm_cuda_check((ctx), _e, #expr); \
   } while (0)
 
+void gm_count_launch();
+
 #define GM_LAUNCH_CHECK(ctx, what)                                 \
   do {                                                             \
+    gm_count_launch();                                             \
     cudaError_t _e = cudaGetLastError();                           \
     if (_e != cudaSuccess) return gm_cuda_check((ctx), _e, what); \
   } while (0)

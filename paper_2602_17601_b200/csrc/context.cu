@@ -13,6 +13,11 @@
 
 #include "common.cuh"
 
+#include <atomic>
+
+static std::atomic<int64_t> g_launches{0};
+void gm_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 int gm_fail(gm_ctx* ctx, int code, const std::string& msg) {
   if (ctx) ctx->err = msg;
   return code;
@@ -33,9 +38,9 @@ int gm_need_device(gm_ctx* ctx) {
 
 void* gm_scratch(gm_ctx* ctx, size_t bytes) {
   if (bytes <= ctx->scratch_bytes) return ctx->scratch;
-  // grow: the caller's stream ordering is respected by synchronising first
-  cudaDeviceSynchronize();
-  if (ctx->scratch) cudaFree(ctx->scratch);
+  // grow; the old buffer is retired, not freed, so CUDA graphs captured with
+  // it stay valid until the context is destroyed
+  if (ctx->scratch) ctx->retired.push_back(ctx->scratch);
   size_t want = bytes + bytes / 4 + (1 << 20);
   if (cudaMalloc(&ctx->scratch, want) != cudaSuccess) {
     ctx->scratch = nullptr;
@@ -58,6 +63,8 @@ static void free_mlp(MlpHost& m) {
 extern "C" {
 
 int gm_abi_version(void) { return 1; }
+
+int64_t gm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int gm_create(gm_ctx** out, int device) {
   if (!out) return GM_ERR_CONFIG;
@@ -89,6 +96,7 @@ void gm_destroy(gm_ctx* ctx) {
     cudaFree(ctx->d_dst);
     cudaFree(ctx->d_norm);
     cudaFree(ctx->scratch);
+    for (void* p : ctx->retired) cudaFree(p);
     free_mlp(ctx->psi);
     free_mlp(ctx->phi);
   }

@@ -22,13 +22,13 @@ NumPy views are materialised lazily when a caller reads them.
 from __future__ import annotations
 
 import time
-from dataclasses import dataclass, field, replace
+from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import device as _dev
 from ._runtime import lib
-from .condensing import cost_device, rows_device, spec_rows
+from .condensing import cost_device, rows_device
 from .gnn import LinearizedDynamics, linearize_device
 from .graph import InputVector, SystemState, Trajectory
 from .qpsolver import STATUS_BY_CODE, QpStatus, SolverSettings
@@ -123,190 +123,277 @@ def _is_gnn_model(model) -> bool:
                                            "normalization"))
 
 
-class _Workspace:
-    """Device buffers reused across steps for one (engine, N, constraint layout)."""
+class StepPlan:
+    """Device buffers and the kernel chain of one RTI step for a fixed
+    (engine, spec, horizon, config).  ``enqueue`` issues
 
-    def __init__(self, eng, N, nx, nu, rows):
-        self.N, self.nx, self.nu = N, nx, nu
+        K-LIN -> K-REC -> K-HG -> K-CON -> soft expansion -> K-QP -> K-RS
+
+    on the current stream with no host synchronisation and no host->device
+    copies; every input it reads lives in the plan's static buffers, so the
+    three stage groups can be captured once as CUDA graphs and replayed."""
+
+    def __init__(self, eng, ds, N, nx, nu, cfg, gnn):
+        torch = eng.torch
+        self.eng, self.ds, self.N, self.nx, self.nu, self.gnn = eng, ds, N, nx, nu, gnn
+        self.cfg = cfg
         M, E = eng.M, eng.E
+        self.M = M
         self.ld = lib().gm_gamma_ld(N, nu)
         self.n0 = N * nu
-        self.m0 = rows.m0
-        self.soft_idx = rows.soft_idx
-        self.ns = int(self.soft_idx.size)
+        self.m0 = ds.rows.m0
+        self.ns = ds.ns
         self.n = self.n0 + self.ns
         self.m = self.m0 + self.ns
         f32, f64, i32 = np.float32, np.float64, np.int32
-        self.a_self = eng.empty((N, M, nx, nx), f32)
-        self.a_nbr = eng.empty((N, E, nx, nx), f32)
-        self.b = eng.empty((N, M, nx, nu), f32)
-        self.c = eng.empty((N, M, nx), f64)
-        self.W = eng.empty((M, N + 1, nx, self.ld), f32)
-        self.H0 = eng.empty((self.n0, self.n0), f64)
-        self.g0 = eng.empty((self.n0,), f64)
-        self.C0 = eng.empty((self.m0, self.n0), f64)
-        self.d0 = eng.empty((self.m0,), f64)
+        e = eng.empty
+        # static inputs
+        self.x_meas = e((M, nx), f64)
+        self.ls = e((N + 1, M, nx), f64)    # linearisation trajectory, [0] = x_measured
+        self.li = e((N, nu), f64)
+        self.fb_states = self.ls            # RTI: fallback plan == input plan
+        self.fb_inputs = self.li
+        self.u_prev = eng.zeros((nu,), f64)  # zeros == "no previous input" (mpc.py:413)
+        # scratch
+        self.a_self = e((N, M, nx, nx), f32)
+        self.a_nbr = e((N, max(E, 1), nx, nx), f32)
+        self.b = e((N, M, nx, nu), f32)
+        self.c = e((N, M, nx), f64)
+        self.W = e((M, N + 1, nx, self.ld), f32)
+        self.H0 = e((self.n0, self.n0), f64)
+        self.g0 = e((self.n0,), f64)
+        self.C0 = e((max(self.m0, 1), self.n0), f64)
+        self.d0 = e((max(self.m0, 1),), f64)
         if self.ns:
-            self.H = eng.empty((self.n, self.n), f64)
-            self.g = eng.empty((self.n,), f64)
-            self.C = eng.empty((self.m, self.n), f64)
-            self.d = eng.empty((self.m,), f64)
-            self.idx = eng.h2d(self.soft_idx, i32)
+            self.H = e((self.n, self.n), f64)
+            self.g = e((self.n,), f64)
+            self.C = e((self.m, self.n), f64)
+            self.d = e((self.m,), f64)
         else:
             self.H, self.g, self.C, self.d = self.H0, self.g0, self.C0, self.d0
         self.warm = eng.zeros((self.n,), f64)
-        self.u = eng.empty((self.n,), f64)
-        self.lam = eng.empty((max(self.m, 1),), f64)
-        self.status = eng.empty((1,), i32)
-        self.iters = eng.empty((1,), i32)
-        self.resid = eng.empty((1, 3), f64)
-        self.summary = eng.empty((nu + 2,), f64)
-        self.host_summary = eng.torch.empty((nu + 2,), dtype=eng.torch.float64, pin_memory=True)
-        self.events = [eng.torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        self.u = e((self.n,), f64)
+        self.lam = e((max(self.m, 1),), f64)
+        self.status = e((1,), i32)
+        self.iters = e((1,), i32)
+        self.resid = e((1, 3), f64)
+        # static outputs
+        self.cur = e((N + 1, M, nx), f64)
+        self.planned_states = e((M, N + 1, nx), f64)
+        self.planned_inputs = e((N, nu), f64)
+        self.next_states = e((N + 1, M, nx), f64)
+        self.next_inputs = e((N, nu), f64)
+        self.u_applied = e((nu,), f64)
+        self.summary = e((nu + 2,), f64)
+        self.host_summary = torch.empty((nu + 2,), dtype=torch.float64, pin_memory=True)
+        self.host_x = torch.empty((M, nx), dtype=torch.float64, pin_memory=True)
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        self.graphs = None
+        self.settings_c = cfg.solver.as_c()
+
+    # -- the three stage groups ------------------------------------------------
+    def _linearize(self):
+        eng, N = self.eng, self.N
+        eng.ctx.call("gm_linearize", N, self.ls.data_ptr(), self.li.data_ptr(),
+                     self.a_self.data_ptr(), self.a_nbr.data_ptr() if eng.E else None,
+                     self.b.data_ptr(), self.c.data_ptr(), None, eng.stream_ptr())
+
+    def _condense(self):
+        eng, N, ds = self.eng, self.N, self.ds
+        sp = eng.stream_ptr()
+        eng.ctx.call("gm_condense_gammas", 1, N, self.a_self.data_ptr(),
+                     self.a_nbr.data_ptr() if eng.E else None, self.b.data_ptr(),
+                     self.c.data_ptr(), self.x_meas.data_ptr(), self.W.data_ptr(), self.ld, sp)
+        cost_device(eng, ds, self.W, self.ld, N, self.H0, self.g0)
+        rows_device(eng, ds, self.W, self.ld, N, self.C0, self.d0)
+        if self.ns:
+            eng.ctx.call("gm_expand_soft", 1, self.n0, self.m0, self.H0.data_ptr(),
+                         self.g0.data_ptr(), self.C0.data_ptr(), self.d0.data_ptr(), self.ns,
+                         ds.idx.data_ptr(), ds.rho1.data_ptr(), ds.rho2.data_ptr(),
+                         self.H.data_ptr(), self.g.data_ptr(), self.C.data_ptr(),
+                         self.d.data_ptr(), sp)
+
+    def _solve_finish(self):
+        import ctypes
+
+        eng, N, cfg = self.eng, self.N, self.cfg
+        sp = eng.stream_ptr()
+        warm = None
+        if cfg.warm_start:  # warm start [lin_inputs; 0] (mpc.py:384-388)
+            self.warm[: N * self.nu].copy_(self.li.reshape(-1))
+            warm = self.warm.data_ptr()
+        eng.ctx.call("gm_solve_qp", 1, self.n, self.m, self.H.data_ptr(), self.g.data_ptr(),
+                     self.C.data_ptr() if self.m else None, self.d.data_ptr() if self.m else None,
+                     warm, ctypes.byref(self.settings_c), self.u.data_ptr(), self.lam.data_ptr(),
+                     self.status.data_ptr(), self.iters.data_ptr(), self.resid.data_ptr(), sp)
+        eng.ctx.call("gm_mpc_finish", 1, N, self.W.data_ptr(), self.ld, self.u.data_ptr(), self.n,
+                     self.status.data_ptr(), self.iters.data_ptr(), self.ls.data_ptr(),
+                     self.li.data_ptr(), self.fb_states.data_ptr(), self.fb_inputs.data_ptr(),
+                     float(cfg.sqp_damping), 0 if cfg.fallback == "hold-previous-input" else 1,
+                     self.u_prev.data_ptr(), 1, self.cur.data_ptr(),
+                     self.planned_states.data_ptr(), self.planned_inputs.data_ptr(),
+                     self.next_states.data_ptr(), self.next_inputs.data_ptr(),
+                     self.u_applied.data_ptr(), self.summary.data_ptr(), sp)
+
+    def groups(self):
+        return (self._linearize, self._condense, self._solve_finish) if self.gnn \
+            else (self._condense, self._solve_finish)
+
+    def capture(self):
+        """Record each stage group as a CUDA graph (after one eager run)."""
+        torch = self.eng.torch
+        graphs = []
+        for fn in self.groups():
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            graphs.append(g)
+        self.graphs = graphs
+
+    def enqueue(self, timed=True):
+        """Issue one step on the current stream (graph replay if captured).
+        Events bracket linearize | condense | solve+epilogue for StepTiming."""
+        torch = self.eng.torch
+        stream = torch.cuda.current_stream(self.eng.device)
+        ev = self.events
+        groups = self.graphs if self.graphs is not None else self.groups()
+        marks = [1, 2, 3] if len(groups) == 3 else [2, 3]
+        if timed:
+            ev[0].record(stream)
+            if len(groups) == 2:
+                ev[1].record(stream)
+        for g, mark in zip(groups, marks):
+            if self.graphs is not None:
+                g.replay()
+            else:
+                g()
+            if timed:
+                ev[mark].record(stream)
+
+    def stage_ms(self):
+        ev = self.events
+        return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])
 
 
-def _workspace(eng, N, nx, nu, rows):
-    key = ("ws", N, nx, nu, rows.m0, tuple(rows.soft_idx.tolist()))
-    ws = eng.cache.get(key)
-    if ws is None:
-        ws = _Workspace(eng, N, nx, nu, rows)
-        eng.cache[key] = ws
-    return ws
+def get_plan(eng, spec, N, nx, nu, cfg, gnn) -> StepPlan:
+    from .condensing import device_spec
+
+    ds = device_spec(eng, spec, nx, nu)
+    s = cfg.solver
+    key = ("plan", id(ds), N, nx, nu, gnn, bool(cfg.warm_start), float(cfg.sqp_damping),
+           cfg.fallback, float(s.tolerance), int(s.max_iterations), float(s.regularization),
+           float(s.fraction_to_boundary))
+    plan = eng.cache.get(key)
+    if plan is None or plan.ds is not ds:
+        plan = StepPlan(eng, ds, N, nx, nu, cfg, gnn)
+        plan.use_graphs = getattr(spec, "_frozen", False)  # only frozen specs are replayable
+        plan.runs = 0
+        eng.cache[key] = plan
+    return plan
 
 
-def _as_device(eng, value, shape, dtype=np.float64):
-    if value is None:
-        return None
-    if isinstance(value, np.ndarray) or not hasattr(value, "data_ptr"):
-        return eng.h2d(np.asarray(value, dtype=float).reshape(shape), dtype)
-    return value
+def _copy_in(dst, value, pinned=None):
+    """Device copy of a state field (tensor -> D2D, ndarray -> H2D)."""
+    if hasattr(value, "data_ptr") and not isinstance(value, np.ndarray):
+        dst.copy_(value.reshape(dst.shape))
+        return
+    arr = np.asarray(value, dtype=float).reshape(tuple(dst.shape))
+    if pinned is not None:
+        pinned.numpy()[...] = arr
+        dst.copy_(pinned, non_blocking=True)
+    else:
+        import torch
+
+        dst.copy_(torch.from_numpy(np.ascontiguousarray(arr)))
 
 
 def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: MpcConfig):
     """One control step of the receding-horizon loop (``mpc.py:102-200``).
 
     Returns the applied ``InputVector`` and the successor ``MpcState`` whose
-    linearisation trajectory is the one-step-shifted plan."""
+    linearisation trajectory is the one-step-shifted plan.  All stages run on
+    the device; the only host<->device traffic is the measurement in, the
+    (device-resident) previous plan, and one small read of
+    [u_applied, status, iterations] out."""
     t_start = time.perf_counter()
-    torch = _dev.require_cuda() if hasattr(_dev, "require_cuda") else None
     N = cfg.horizon
     gnn = _is_gnn_model(model)
     if not gnn and not callable(model):
         raise TypeError("model must be a GnnModel or a linearizer callable")
     eng = _dev.engine(topo, model if gnn else None)
     torch = eng.torch
-    M = topo.node_count
     lin_in_prev = state.device_value("lin_inputs")
     n_u = int(lin_in_prev.shape[1])
     nx = int(np.asarray(x_measured.array).shape[1])
     eng.set_dims(nx, n_u)
-    rows = spec_rows(spec, nx, n_u)
-    ws = _workspace(eng, N, nx, n_u, rows)
-    sp = eng.stream_ptr()
-    ev = ws.events
+    plan = get_plan(eng, spec, N, nx, n_u, cfg, gnn)
     stream = torch.cuda.current_stream(eng.device)
 
-    # trajectory with the measurement at stage 0 (mpc.py:120-122)
-    x_meas = eng.h2d(x_measured.array, np.float64)
-    fb_states = torch.empty((N + 1, M, nx), dtype=torch.float64, device=eng.device)
-    fb_states.copy_(_as_device(eng, state.device_value("lin_states"), (N + 1, M, nx)))
-    fb_states[0].copy_(x_meas)
-    fb_inputs = _as_device(eng, lin_in_prev, (N, n_u)).clone()
-    ls, li = fb_states, fb_inputs
+    # inputs: measurement, previous plan with x_measured at stage 0 (mpc.py:120-122)
+    _copy_in(plan.x_meas, x_measured.array, plan.host_x)
+    _copy_in(plan.ls, state.device_value("lin_states"))
+    plan.ls[0].copy_(plan.x_meas)
+    _copy_in(plan.li, lin_in_prev)
     prev = state.device_value("last_applied")
-    u_prev = _as_device(eng, prev, (n_u,)) if prev is not None else None
-
-    cur = torch.empty_like(fb_states) if cfg.sqp_iterations > 1 else None
-    planned_states = torch.empty((M, N + 1, nx), dtype=torch.float64, device=eng.device)
-    planned_inputs = torch.empty((N, n_u), dtype=torch.float64, device=eng.device)
-    next_states = torch.empty((N + 1, M, nx), dtype=torch.float64, device=eng.device)
-    next_inputs = torch.empty((N, n_u), dtype=torch.float64, device=eng.device)
-    u_applied = torch.empty((n_u,), dtype=torch.float64, device=eng.device)
+    if prev is None:
+        plan.u_prev.zero_()
+    else:
+        _copy_in(plan.u_prev, prev)
 
     timing = StepTiming()
     total_iters = 0
-    status_code = None
+    if cfg.sqp_iterations > 1:  # the SQP loop keeps the original plan as the fallback
+        plan.fb_states = plan.ls.clone()
+        plan.fb_inputs = plan.li.clone()
+    else:
+        plan.fb_states, plan.fb_inputs = plan.ls, plan.li
     for it in range(cfg.sqp_iterations):
-        ev[0].record(stream)
-        # stage 1: linearise along the first N states (mpc.py:130-132)
-        if gnn:
-            if not ls.is_contiguous():
-                ls = ls.contiguous()
-            a_self, a_nbr, b, c = ws.a_self, ws.a_nbr, ws.b, ws.c
-            eng.ctx.call("gm_linearize", N, ls.data_ptr(), li.data_ptr(), a_self.data_ptr(),
-                         a_nbr.data_ptr() if eng.E else None, b.data_ptr(), c.data_ptr(), None, sp)
-        else:
-            lin = model(ls[:N].cpu().numpy(), li.cpu().numpy())
-            a_self, a_nbr, b, c = lin.device_blocks(eng) if isinstance(lin, LinearizedDynamics) \
-                else tuple(eng.h2d(getattr(lin, k), np.float64 if k == "c" else np.float32)
-                           for k in ("a_self", "a_nbr", "b", "c"))
-        ev[1].record(stream)
-        # stage 2-3: condensing (mpc.py:135-137)
-        eng.ctx.call("gm_condense_gammas", 1, N, a_self.data_ptr(),
-                     a_nbr.data_ptr() if eng.E else None, b.data_ptr(), c.data_ptr(),
-                     x_meas.data_ptr(), ws.W.data_ptr(), ws.ld, sp)
-        cost_device(eng, spec, ws.W, ws.ld, N, nx, n_u, ws.H0, ws.g0)
-        rows_device(eng, rows, ws.W, ws.ld, N, ws.C0, ws.d0)
-        if ws.ns:
-            r1 = eng.h2d(rows.rho1[ws.soft_idx], np.float64)
-            r2 = eng.h2d(rows.rho2[ws.soft_idx], np.float64)
-            eng.ctx.call("gm_expand_soft", 1, ws.n0, ws.m0, ws.H0.data_ptr(), ws.g0.data_ptr(),
-                         ws.C0.data_ptr(), ws.d0.data_ptr(), ws.ns, ws.idx.data_ptr(),
-                         r1.data_ptr(), r2.data_ptr(), ws.H.data_ptr(), ws.g.data_ptr(),
-                         ws.C.data_ptr(), ws.d.data_ptr(), sp)
-        ev[2].record(stream)
-        # stage 4: QP with warm start [lin_inputs; 0] (mpc.py:140-147)
-        warm = None
-        if cfg.warm_start:
-            ws.warm[: N * n_u].copy_(li.reshape(-1))
-            warm = ws.warm.data_ptr()
-        cs = cfg.solver.as_c()
-        import ctypes
-
-        eng.ctx.call("gm_solve_qp", 1, ws.n, ws.m, ws.H.data_ptr(), ws.g.data_ptr(),
-                     ws.C.data_ptr() if ws.m else None, ws.d.data_ptr() if ws.m else None, warm,
-                     ctypes.byref(cs), ws.u.data_ptr(), ws.lam.data_ptr(), ws.status.data_ptr(),
-                     ws.iters.data_ptr(), ws.resid.data_ptr(), sp)
-        ev[3].record(stream)
-        # RTI epilogue on the device (mpc.py:151-200)
-        eng.ctx.call("gm_mpc_finish", 1, N, ws.W.data_ptr(), ws.ld, ws.u.data_ptr(), ws.n,
-                     ws.status.data_ptr(), ws.iters.data_ptr(), ls.data_ptr(), li.data_ptr(),
-                     fb_states.data_ptr(), fb_inputs.data_ptr(), float(cfg.sqp_damping),
-                     0 if cfg.fallback == "hold-previous-input" else 1,
-                     u_prev.data_ptr() if u_prev is not None else None, int(u_prev is not None),
-                     cur.data_ptr() if cur is not None else None, planned_states.data_ptr(),
-                     planned_inputs.data_ptr(), next_states.data_ptr(), next_inputs.data_ptr(),
-                     u_applied.data_ptr(), ws.summary.data_ptr(), sp)
-        ws.host_summary.copy_(ws.summary, non_blocking=True)
+        if not gnn:  # plug-in Linearizer (mpc.py:23, :82-87): upload its blocks
+            lin = model(plan.ls[:N].cpu().numpy(), plan.li.cpu().numpy())
+            blocks = lin.device_blocks(eng) if isinstance(lin, LinearizedDynamics) else tuple(
+                eng.h2d(getattr(lin, k), np.float64 if k == "c" else np.float32)
+                for k in ("a_self", "a_nbr", "b", "c"))
+            for dst, src in zip((plan.a_self, plan.a_nbr, plan.b, plan.c), blocks):
+                if src.numel():
+                    dst.view(-1)[: src.numel()].copy_(src.reshape(-1))
+        graphable = plan.use_graphs and cfg.sqp_iterations == 1
+        if graphable and plan.graphs is None and plan.runs >= 1:
+            plan.capture()
+        plan.enqueue()
+        plan.runs += 1
+        plan.host_summary.copy_(plan.summary, non_blocking=True)
         stream.synchronize()
-        summ = ws.host_summary.numpy()
+        summ = plan.host_summary.numpy()
         status_code = int(summ[n_u])
         total_iters += int(summ[n_u + 1])
-        timing.linearize_ms += ev[0].elapsed_time(ev[1])
-        timing.condense_ms += ev[1].elapsed_time(ev[2])
-        timing.solve_ms += ev[2].elapsed_time(ev[3])
+        lm, cm, sm = plan.stage_ms()
+        timing.linearize_ms += lm if gnn else 0.0
+        timing.condense_ms += cm
+        timing.solve_ms += sm
         if status_code > 1:  # not OPTIMAL / MAX_ITERATIONS: fallback already applied
             break
         if it + 1 < cfg.sqp_iterations:
-            ls, li = cur.clone(), planned_inputs.clone()
+            plan.ls.copy_(plan.cur)
+            plan.li.copy_(plan.planned_inputs)
 
     u_app = summ[:n_u].copy()
     filtered = state.device_value("filtered_input")
     if cfg.input_filter_tau is not None:  # optional first-order smoothing (mpc.py:178-183)
         alpha = cfg.dt / (cfg.input_filter_tau + cfg.dt)
-        prevf = np.asarray(filtered.cpu().numpy() if hasattr(filtered, "cpu") else filtered,
-                           dtype=float) if filtered is not None else u_app
+        prevf = (np.asarray(filtered.cpu().numpy() if hasattr(filtered, "cpu") else filtered,
+                            dtype=float) if filtered is not None else u_app)
         u_app = prevf + alpha * (u_app - prevf)
         filtered = u_app.copy()
         last_applied = u_app.copy()
     else:
-        last_applied = u_applied
-    timing.total_ms = (time.perf_counter() - t_start) * 1e3
-    new_state = MpcState(lin_states=next_states, lin_inputs=next_inputs,
+        last_applied = plan.u_applied.clone()
+    new_state = MpcState(lin_states=plan.next_states.clone(), lin_inputs=plan.next_inputs.clone(),
                          step_count=state.step_count + 1, last_applied=last_applied,
-                         planned_states=planned_states, planned_inputs=planned_inputs,
+                         planned_states=plan.planned_states.clone(),
+                         planned_inputs=plan.planned_inputs.clone(),
                          last_status=STATUS_BY_CODE[status_code], last_iterations=total_iters,
                          last_timing=timing, filtered_input=filtered)
+    timing.total_ms = (time.perf_counter() - t_start) * 1e3
     return InputVector(u_app), new_state
 
 
