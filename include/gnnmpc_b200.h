@@ -174,6 +174,17 @@ int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, const double*
                 const gm_qp_settings* settings, double* u, double* lam, int32_t* status,
                 int32_t* iterations, double* resid, void* stream);
 
+/* Diagnostics: per-phase cycle accounting of K-QP (block 0).  gm_qp_profile(1)
+ * enables and zeroes the counters; gm_qp_phase_cycles copies 16 counters
+ * (synchronous). */
+int gm_qp_profile(int on);
+int gm_qp_phase_cycles(unsigned long long* out);
+/* Diagnostics: factor a dense SPD matrix A (n x n, row-major, device) with
+ * K-QP's own Cholesky and solve A x = b; L (n x n) lower, ok = 0 when a pivot
+ * failed.  Used by the tests to check the factorisation in isolation. */
+int gm_chol_check(gm_ctx* ctx, int n, const double* A, const double* b, double* L, double* x,
+                  int32_t* ok, void* stream);
+
 /* ---- reconstruct_states (condensing.py:409-416) ------------------------ */
 /* u (B, ldu) fp64 (first N*nu used); x (B, M, N+1, nx) fp64. */
 int gm_reconstruct_states(gm_ctx* ctx, int B, int N, const float* gamma, int ld,

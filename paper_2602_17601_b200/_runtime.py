@@ -66,6 +66,9 @@ _SIGNATURES = {
                                P, c_void_p]),
     "gm_solve_qp": (c_int, [c_void_p, c_int, c_int, c_int, P, P, P, P, P,
                             ctypes.POINTER(QpSettingsC), P, P, P, P, P, c_void_p]),
+    "gm_qp_profile": (c_int, [c_int]),
+    "gm_qp_phase_cycles": (c_int, [P]),
+    "gm_chol_check": (c_int, [c_void_p, c_int, P, P, P, P, P, c_void_p]),
     "gm_reconstruct_states": (c_int, [c_void_p, c_int, c_int, P, c_int, P, c_int, P, c_void_p]),
     "gm_mpc_finish": (c_int, [c_void_p, c_int, c_int, P, c_int, P, c_int, P, P, P, P, P, P, c_double,
                               c_int, P, c_int, P, P, P, P, P, P, P, c_void_p]),

@@ -4,17 +4,28 @@
 // _split_single_nonzero_rows (:100-109), _max_step (:238-243).  Same
 // algorithm step by step -- Mehrotra predictor-corrector on
 //   2Hu + g + C'lam = 0,  Cu + s = d,  lam_i s_i = mu
-// with the reference's scale references, stopping and infeasibility tests,
+// with the reference's scale references, stopping / infeasibility tests,
 // best-iterate bookkeeping, escalating Cholesky regularisation and status
-// semantics -- so statuses and iteration counts match the reference.
+// semantics, so statuses and iteration counts match the reference.
 //
-// B200 mapping: the whole IPM loop runs on the device inside one CTA per QP
-// (no host round trips); the Schur matrix K lives in shared memory
-// (column-major lower triangle, odd leading dimension => conflict-free row and
-// column walks), single-nonzero constraint rows are never touched densely
-// (diagonal Schur contribution + a per-column row list), general rows are
-// staged once into shared memory.  Batches of independent QPs (cfg4) fill the
-// GPU with one CTA each.
+// Latency model (measured on B200, scripts/ubench_latency.cu): a dependent
+// fp64 FMA costs 23 cycles, rsqrt(f64) 84, 1/sqrt(f64) 185, a double shuffle
+// 54.  An IPM iteration is a chain of ~n dependent pivots, so the design
+// shortens that chain and keeps every other loop free of long dependences:
+//  * one CTA per QP, the whole IPM loop on the device (no host round trips);
+//    batches of independent QPs fill the GPU (cfg4);
+//  * the Schur matrix K is a packed lower triangle in shared memory;
+//  * factorisation = block elimination with 2x2 pivots: one reciprocal per
+//    two columns on the critical path, and the next pivot block is updated
+//    and inverted one step ahead by warp 0 while warps 1..15 apply the
+//    rank-2 update to the trailing matrix (one CTA barrier per 2 columns);
+//    a final parallel pass turns the result into the Cholesky factor L;
+//  * the 32x32 diagonal blocks of L are inverted in parallel, so the
+//    triangular solves are 5 short block mat-vecs, not n scalar steps;
+//  * every dot product uses 4 independent accumulators; loads of H (L2
+//    resident when it does not fit on chip) are issued in batches;
+//  * single-nonzero constraint rows (box bounds, slack signs) only touch the
+//    diagonal; general rows are staged once into shared memory.
 #include <algorithm>
 #include <cfloat>
 
@@ -24,9 +35,40 @@ namespace {
 
 constexpr int kQpThreads = 512;
 constexpr int kQpWarps = kQpThreads / 32;
+constexpr int kTB = 32;  // triangular-solve block
+constexpr int kXL = 33;  // leading dimension of an inverted diagonal block
+
+__host__ __device__ inline size_t qal(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ inline int64_t packed_size(int n) { return (int64_t)n * (n + 1) / 2; }
+
+struct QpLayout {
+  size_t o_vec, o_ints, o_k, o_x, o_h, o_cg, total;
+};
+
+// n-vectors: g u hu rd rhs du ub ctl ytmp dinv        (10)
+// m-vectors: d s lam cu rp t dl ds tmp w lb rval      (12)
+__host__ __device__ inline QpLayout qp_layout(int n, int m, int ng, bool h_smem, bool cg_smem) {
+  QpLayout L{};
+  const int nblk = (n + kTB - 1) / kTB;
+  size_t o = 0;
+  L.o_vec = o;
+  o = qal(o + sizeof(double) * (10 * (size_t)n + 12 * (size_t)m + 64));
+  L.o_ints = o;  // rcol(m) grow(m) colptr(n+1) colrows(m) cstart(n+1)
+  o = qal(o + sizeof(int) * (3 * (size_t)m + 2 * (size_t)n + 2 + 8));
+  L.o_k = o;
+  o = qal(o + sizeof(double) * packed_size(n));
+  L.o_x = o;
+  o = qal(o + sizeof(double) * (size_t)nblk * kTB * kXL);
+  L.o_cg = o;
+  if (cg_smem) o = qal(o + sizeof(double) * (size_t)ng * n);
+  L.o_h = o;
+  if (h_smem) o = qal(o + sizeof(double) * packed_size(n));
+  L.total = o;
+  return L;
+}
 
 struct QpArgs {
-  int n, m, ldk, k_smem;
+  int n, m;
   size_t smem_bytes;
   const double* H;
   const double* g;
@@ -40,177 +82,612 @@ struct QpArgs {
   int* status;
   int* iters;
   double* resid;
-  double* gws;       // per-instance global workspace (K and/or Cg when they do not fit)
+  double* gws;  // per-instance global workspace: packed H / general rows when off-chip
   int64_t gws_stride;
 };
 
-struct QpLayout {
-  size_t o_vec, o_ints, o_cg, o_k, total;
-  int nvec_n, nvec_m;
+// optional per-phase cycle accounting (block 0, thread 0), read back with
+// gm_qp_phase_cycles(); enabled by gm_qp_profile(1)
+__device__ unsigned long long g_qp_prof[16];
+__device__ int g_qp_prof_on;
+
+struct Qs {  // per-CTA views
+  int n, m, ng, nblk;
+  double *K, *X, *Hp, *Cg;
+  double *g, *u, *hu, *rd, *rhs, *du, *ub, *ctl, *ytmp, *dinv;
+  double *d, *s, *lam, *cu, *rp, *t, *dl, *ds, *tmp, *w, *lb, *rval;
+  int *rcol, *grow, *colptr, *colrows, *cstart;
+  double* red;
+  double* pv;  // 2 x 4 pivot-block inverses (double buffered)
+  double* ys;  // 32-entry staging vector of the triangular solves
+  int* flag;
+  bool prof;
+  long long last;
 };
 
-__host__ __device__ inline size_t qal(size_t x) { return (x + 15) & ~size_t(15); }
-
-// n-vectors: g, u, hu, rdual, rhs, du, ubest, dinv, ctl          (9)
-// m-vectors: d, s, lam, cu, rpri, t, dl, ds, dla, dsa, w, lbest,  (13)
-//            rval
-__host__ __device__ inline QpLayout qp_layout(int n, int m, int ldk, int ng, bool k_smem,
-                                              bool cg_smem) {
-  QpLayout L{};
-  L.nvec_n = 9;
-  L.nvec_m = 13;
-  size_t o = 0;
-  L.o_vec = o;
-  o = qal(o + sizeof(double) * ((size_t)L.nvec_n * n + (size_t)L.nvec_m * m + 64));
-  L.o_ints = o;  // rcol(m) gpos(m) grow(m) colptr(n+1) colrows(m)
-  o = qal(o + sizeof(int) * ((size_t)4 * m + n + 1 + 8));
-  L.o_k = o;
-  if (k_smem) o = qal(o + sizeof(double) * (size_t)ldk * n);
-  L.o_cg = o;
-  if (cg_smem) o = qal(o + sizeof(double) * (size_t)ng * n);
-  L.total = o;
-  return L;
+__device__ __forceinline__ void qmark(Qs& S, int phase) {
+  if (S.prof && threadIdx.x == 0) {
+    const long long t = clock64();
+    atomicAdd(&g_qp_prof[phase], (unsigned long long)(t - S.last));
+    S.last = t;
+  }
 }
 
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ double warp_min(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-// block-wide reductions; every thread gets the result.  op: 0 max, 1 min, 2 sum
+// block-wide reductions (every thread gets the result); op 0 max, 1 min, 2 sum.
+// Warp partials go through shared memory; each warp then folds the 16
+// partials with 4 shuffles (fixed order: bitwise reproducible).
+template <int OP>
+__device__ __forceinline__ double rop(double a, double b) {
+  return OP == 0 ? fmax(a, b) : (OP == 1 ? fmin(a, b) : a + b);
+}
 template <int OP>
 __device__ double block_reduce(double v, double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  v = OP == 0 ? warp_max(v) : (OP == 1 ? warp_min(v) : warp_sum(v));
-  __syncthreads();  // protect red[] from the previous use
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = rop<OP>(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
   if (lane == 0) red[wid] = v;
   __syncthreads();
-  double r = red[0];
-  for (int w = 1; w < kQpWarps; ++w) r = OP == 0 ? fmax(r, red[w]) : (OP == 1 ? fmin(r, red[w]) : r + red[w]);
+  double r = red[lane & (kQpWarps - 1)];
+#pragma unroll
+  for (int o = kQpWarps / 2; o > 0; o >>= 1) r = rop<OP>(r, __shfl_xor_sync(0xffffffffu, r, o));
   return r;
 }
 
-// Right-looking Cholesky of the lower triangle of K (column-major, leading
-// dimension ldk) in place; returns false on a non-positive / NaN pivot
-// (LAPACK potrf's failure condition).  On success column j holds L[:, j] and
-// dinv[j] = 1 / L[j][j].
-__device__ bool chol_factor(double* K, int n, int ldk, double* dinv, double* red) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int j = 0; j < n; ++j) {
-    const double piv = K[(size_t)j * ldk + j];
-    if (!(piv > 0.0)) {
-      __syncthreads();
-      return false;
+// ---------------------------------------------------------------------------
+// factorisation: block elimination with 2x2 pivots -> Cholesky factor L
+// ---------------------------------------------------------------------------
+// Packed lower triangle, column-major: element (r, c), r >= c, at
+// colbase(c, n) + r with colbase = cstart[c] - c computed arithmetically
+// (an integer multiply-add instead of a dependent shared-memory load).
+__device__ __forceinline__ int colbase(int c, int n) { return c * n - ((c * (c + 1)) >> 1); }
+
+// Pivot block P = [[a, b], [b, c]] (or 1x1 when bs == 1) factored with the
+// scalar Cholesky formulas (as LAPACK potf2 would): pv = {1/l00, l10, 1/l11}
+// with l00 = sqrt(a), l10 = b / l00, l11 = sqrt(c - l10^2).  Fails on a
+// non-positive or NaN scalar pivot (potrf's rule).  (An explicit 2x2 inverse
+// via the determinant is measurably less stable on the ill-conditioned
+// Schur matrices of late IPM iterations.)
+__device__ __forceinline__ bool pivot_chol(double a, double b, double c, int bs, double* pv) {
+  if (!(a > 0.0)) return false;
+  const double i00 = rsqrt(a);
+  pv[0] = i00;
+  if (bs == 1) {
+    pv[1] = 0.0;
+    pv[2] = 0.0;
+    return true;
+  }
+  const double l10 = b * i00;
+  const double t = fma(-l10, l10, c);
+  if (!(t > 0.0)) return false;
+  pv[1] = l10;
+  pv[2] = rsqrt(t);
+  return true;
+}
+
+// Row x of the two L columns of a pivot block from its Schur-complement row w.
+__device__ __forceinline__ void lrow(double w0, double w1, double i00, double l10, double i11,
+                                     double& x0, double& x1) {
+  x0 = w0 * i00;
+  x1 = fma(-x0, l10, w1) * i11;
+}
+
+// Factor K = L L' in place; false on a failed pivot; dinv[j] = 1/L[j][j].
+// Columns are eliminated two at a time (one CTA barrier per pair): warp 0
+// lane 0 updates and factors the next pivot block one step ahead while warps
+// 1..15 apply the current pair's rank-2 update to the trailing matrix.  The
+// panels keep their Schur-complement values W until a final parallel pass
+// scales them into L.
+template <int TM>
+__device__ bool chol_factor(Qs& S) {
+  const int n = S.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* K = S.K;
+  double* pi00 = S.ytmp;  // per pivot pair j: ytmp[j] = 1/l00, ytmp[j+1] = 1/l11
+  double* pl10 = S.ctl;   // ctl[j] = l10
+  if (tid == 0) {
+    const int bs = min(2, n);
+    const bool ok = pivot_chol(K[0], bs == 2 ? K[1] : 0.0, bs == 2 ? K[colbase(1, n) + 1] : 0.0,
+                               bs, S.pv);
+    *S.flag = ok ? 0 : 1;
+    pi00[0] = S.pv[0];
+    if (bs == 2) {
+      pl10[0] = S.pv[1];
+      pi00[1] = S.pv[2];
     }
-    const double ipiv = 1.0 / piv;
-    const double* colj = K + (size_t)j * ldk;
-    for (int c = j + 1 + wid; c < n; c += kQpWarps) {
-      const double f = colj[c] * ipiv;
-      double* colc = K + (size_t)c * ldk;
-      for (int r = c + lane; r < n; r += 32) colc[r] = fma(-colj[r], f, colc[r]);
+  }
+  __syncthreads();
+  int buf = 0;
+  for (int j = 0; j < n; j += 2) {
+    if (*S.flag) return false;  // uniform: read after the barrier
+    const int bs = min(2, n - j);
+    const int j2 = j + bs;
+    if (j2 >= n) break;
+    const int bs2 = min(2, n - j2);
+    const double i00 = S.pv[buf * 4 + 0], l10 = S.pv[buf * 4 + 1], i11 = S.pv[buf * 4 + 2];
+    const int cj0 = colbase(j, n);
+    const int cj1 = bs == 2 ? colbase(j + 1, n) : cj0;
+    const double m1 = bs == 2 ? 1.0 : 0.0;  // second pivot column present
+    if (wid == 0) {
+      // look-ahead: update and factor the next pivot block (lane 0)
+      if (lane == 0) {
+        const int d0 = colbase(j2, n) + j2, d1 = colbase(j2 + 1, n) + j2 + 1;
+        double a0, a1, b0 = 0.0, b1 = 0.0;
+        lrow(K[cj0 + j2], m1 * K[cj1 + j2], i00, l10, i11, a0, a1);
+        if (bs2 == 2) lrow(K[cj0 + j2 + 1], m1 * K[cj1 + j2 + 1], i00, l10, i11, b0, b1);
+        const double e00 = K[d0] - fma(a0, a0, a1 * a1);
+        double e10 = 0.0, e11 = 0.0;
+        if (bs2 == 2) {
+          e10 = K[d0 + 1] - fma(b0, a0, b1 * a1);
+          e11 = K[d1] - fma(b0, b0, b1 * b1);
+          K[d0 + 1] = e10;
+          K[d1] = e11;
+        }
+        K[d0] = e00;
+        double* pn = S.pv + (buf ^ 1) * 4;
+        if (!pivot_chol(e00, e10, e11, bs2, pn)) *S.flag = 1;
+        pi00[j2] = pn[0];
+        if (bs2 == 2) {
+          pl10[j2] = pn[1];
+          pi00[j2 + 1] = pn[2];
+        }
+      }
+    } else {
+      // rank-2 update of the trailing matrix, skipping the next pivot block:
+      // K[r][c] -= L0[r] L0[c] + L1[r] L1[c]
+      double l0[TM], l1[TM];
+#pragma unroll
+      for (int t = 0; t < TM; ++t) {
+        const int r = lane + 32 * t;
+        double w0 = 0.0, w1 = 0.0;
+        if (r >= j2 && r < n) {
+          w0 = K[cj0 + r];
+          w1 = m1 * K[cj1 + r];
+        }
+        lrow(w0, w1, i00, l10, i11, l0[t], l1[t]);
+      }
+      const int pe = j2 + bs2;  // next pivot block rows/cols: [j2, pe)
+      constexpr int kU = kQpWarps - 1;
+      for (int c = j2 + (wid - 1); c < n; c += kU) {
+        double c0, c1;
+        lrow(K[cj0 + c], m1 * K[cj1 + c], i00, l10, i11, c0, c1);
+        double* col = K + colbase(c, n);
+        const int t0 = c >> 5;              // warp-uniform: row tiles above c are skipped
+        const int rskip = c < pe ? pe : c;  // rows of the next pivot block are lane 0's
+#pragma unroll
+        for (int t = 0; t < TM; ++t) {
+          if (t >= t0) {
+            const int r = lane + 32 * t;
+            if (r >= rskip && r < n) col[r] = col[r] - fma(l0[t], c0, l1[t] * c1);
+          }
+        }
+      }
     }
+    buf ^= 1;
     __syncthreads();
   }
-  // scale columns: L[r][j] = Kt[r][j] / sqrt(piv_j)
-  for (int j = wid; j < n; j += kQpWarps) {
-    double* colj = K + (size_t)j * ldk;
-    const double piv = colj[j];
-    const double ljj = sqrt(piv);
-    const double inv = 1.0 / ljj;
-    for (int r = j + 1 + lane; r < n; r += 32) colj[r] *= inv;
-    __syncwarp();
+  if (*S.flag) return false;
+  // scale the panels into L (the pivot blocks' factors are in pi00 / pl10)
+  for (int j = 2 * wid; j < n; j += 2 * kQpWarps) {
+    const double a00 = pi00[j];
+    const bool two = j + 1 < n;
+    const double b10 = two ? pl10[j] : 0.0, a11 = two ? pi00[j + 1] : 0.0;
+    double* c0 = K + colbase(j, n);
+    double* c1 = two ? K + colbase(j + 1, n) : c0;
+    for (int r = j + 2 + lane; r < n; r += 32) {
+      double x0, x1;
+      lrow(c0[r], two ? c1[r] : 0.0, a00, b10, a11, x0, x1);
+      c0[r] = x0;
+      if (two) c1[r] = x1;
+    }
     if (lane == 0) {
-      colj[j] = ljj;
-      dinv[j] = inv;
+      const double piv0 = c0[j];
+      c0[j] = piv0 * a00;  // l00 = sqrt(a)
+      S.dinv[j] = a00;
+      if (two) {
+        c0[j + 1] = b10;
+        c1[j + 1] = fma(-b10, b10, c1[j + 1]) * a11;  // l11 = sqrt(c - l10^2)
+        S.dinv[j + 1] = a11;
+      }
     }
   }
   __syncthreads();
   return true;
 }
 
-// x = K^{-1} b with K = L L' (L from chol_factor); b, x shared vectors (may alias).
-// Column-oriented substitution by warp 0; the other warps wait at the barrier.
-__device__ void chol_solve(const double* K, int n, int ldk, const double* dinv, const double* b,
-                           double* x) {
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    for (int r = lane; r < n; r += 32) x[r] = b[r];
-    __syncwarp();
-    for (int j = 0; j < n; ++j) {  // L y = b
-      const double yj = x[j] * dinv[j];
-      const double* colj = K + (size_t)j * ldk;
-      for (int r = j + 1 + lane; r < n; r += 32) x[r] = fma(-colj[r], yj, x[r]);
-      __syncwarp();
-      if (lane == 0) x[j] = yj;
-      __syncwarp();
+// Invert the 32x32 diagonal blocks of L: X_b = L_bb^{-1}, column-major with
+// leading dimension kXL (X[k][i] at i*kXL + k).  Warp b inverts block b,
+// lane i computes column i by forward substitution: row r needs the row r of
+// L_bb (same for all lanes: broadcast loads, issued 4 at a time) against the
+// lane's own already-solved entries.
+__device__ void invert_diag_blocks(Qs& S) {
+  const int n = S.n, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int b = wid; b < S.nblk; b += kQpWarps) {
+    const int r0 = b * kTB, nb = min(kTB, n - r0);
+    double* Xi = S.X + (size_t)b * kTB * kXL + lane * kXL;
+    const int i = lane;
+#pragma unroll 8
+    for (int k = 0; k < kTB; ++k) Xi[k] = 0.0;
+    if (i < nb) Xi[i] = S.dinv[r0 + i];
+    for (int r = 1; r < nb; ++r) {
+      // s = sum_{k<r} L[r0+r][r0+k] X[k][i]   (X[k][i] = 0 for k < i)
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      const int rr = r0 + r;
+      for (int k = 0; k < r; k += 4) {
+        const double x0 = Xi[k], x1 = Xi[k + 1], x2 = Xi[k + 2], x3 = Xi[k + 3];
+        const double q0 = S.K[colbase(r0 + k, n) + rr];
+        const double q1 = k + 1 < r ? S.K[colbase(r0 + k + 1, n) + rr] : 0.0;
+        const double q2 = k + 2 < r ? S.K[colbase(r0 + k + 2, n) + rr] : 0.0;
+        const double q3 = k + 3 < r ? S.K[colbase(r0 + k + 3, n) + rr] : 0.0;
+        s0 = fma(q0, x0, s0);
+        s1 = fma(q1, x1, s1);
+        s2 = fma(q2, x2, s2);
+        s3 = fma(q3, x3, s3);
+      }
+      if (i < r && i < nb) Xi[r] = -((s0 + s1) + (s2 + s3)) * S.dinv[rr];
     }
-    for (int j = n - 1; j >= 0; --j) {  // L' x = y
-      const double xj = x[j] * dinv[j];
-      for (int r = lane; r < j; r += 32) x[r] = fma(-K[(size_t)r * ldk + j], xj, x[r]);
-      __syncwarp();
-      if (lane == 0) x[j] = xj;
-      __syncwarp();
+  }
+}
+
+// x = K^{-1} b by warp 0 (the solves are short dependent chains; one warp
+// avoids CTA barriers).  Lanes own rows lane + 32t; diagonal blocks are
+// applied through their inverses, off-diagonal blocks as mat-vecs; the block
+// solution is staged in shared memory (S.ys) for broadcast reads.  b and x
+// are shared n-vectors (x may alias b).  Call with all threads.
+template <int TM>
+__device__ void chol_solve(Qs& S, const double* b, double* x) {
+  const int n = S.n, lane = threadIdx.x & 31;
+  const double* K = S.K;
+  double* ys = S.ys;
+  if (threadIdx.x < 32) {
+    double y[TM];
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      const int r = lane + 32 * t;
+      y[t] = r < n ? b[r] : 0.0;
+    }
+    // forward: L y = b
+#pragma unroll
+    for (int blk = 0; blk < TM; ++blk) {
+      if (blk < S.nblk) {
+        const int r0 = blk * kTB, nb = min(kTB, n - r0);
+        const double* X = S.X + (size_t)blk * kTB * kXL;
+        ys[lane] = y[blk];
+        __syncwarp();
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < kTB; ++k) a[k & 3] = fma(X[k * kXL + lane], ys[k], a[k & 3]);
+        const double yb = lane < nb ? (a[0] + a[1]) + (a[2] + a[3]) : 0.0;
+        y[blk] = yb;
+        __syncwarp();
+        ys[lane] = yb;
+        __syncwarp();
+#pragma unroll
+        for (int t = blk + 1; t < TM; ++t) {
+          const int r = lane + 32 * t;  // only full blocks have rows below
+          if (r < n) {
+            double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < kTB; ++k)
+              c[k & 3] = fma(K[colbase(r0 + k, n) + r], ys[k], c[k & 3]);
+            y[t] -= (c[0] + c[1]) + (c[2] + c[3]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    // backward: L' x = y
+#pragma unroll
+    for (int blk = TM - 1; blk >= 0; --blk) {
+      if (blk < S.nblk) {
+        const int r0 = blk * kTB, nb = min(kTB, n - r0);
+        const double* X = S.X + (size_t)blk * kTB * kXL;
+        ys[lane] = y[blk];
+        __syncwarp();
+        const double* Xl = X + lane * kXL;  // X[k][lane], zero for k < lane
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < kTB; ++k) a[k & 3] = fma(Xl[k], ys[k], a[k & 3]);
+        const double xb = lane < nb ? (a[0] + a[1]) + (a[2] + a[3]) : 0.0;
+        y[blk] = xb;
+        __syncwarp();
+        ys[lane] = xb;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < blk; ++t) {
+          const int r = lane + 32 * t;  // r < r0 <= n
+          const double* col = K + colbase(r, n) + r0;  // L[r0+k][r]
+          double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int k = 0; k < kTB; ++k)
+            if (k < nb) c[k & 3] = fma(col[k], ys[k], c[k & 3]);
+          y[t] -= (c[0] + c[1]) + (c[2] + c[3]);
+        }
+        __syncwarp();
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      const int r = lane + 32 * t;
+      if (r < n) x[r] = y[t];
     }
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kQpThreads) k_solve_qp(const QpArgs A) {
+// ---------------------------------------------------------------------------
+// QP building blocks
+// ---------------------------------------------------------------------------
+
+// out[c] = (C' tv)[c]
+__device__ void ct_apply(const Qs& S, const double* tv, double* out) {
+  for (int c = threadIdx.x; c < S.n; c += blockDim.x) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
+      const int r = S.colrows[q];
+      s0 = fma(S.rval[r], tv[r], s0);
+    }
+    const double* cg = S.Cg + c;
+    int gi = 0;
+    for (; gi + 3 < S.ng; gi += 4) {
+      s0 = fma(cg[(int64_t)gi * S.n], tv[S.grow[gi]], s0);
+      s1 = fma(cg[(int64_t)(gi + 1) * S.n], tv[S.grow[gi + 1]], s1);
+      s2 = fma(cg[(int64_t)(gi + 2) * S.n], tv[S.grow[gi + 2]], s2);
+      s3 = fma(cg[(int64_t)(gi + 3) * S.n], tv[S.grow[gi + 3]], s3);
+    }
+    for (; gi < S.ng; ++gi) s0 = fma(cg[(int64_t)gi * S.n], tv[S.grow[gi]], s0);
+    out[c] = (s0 + s1) + (s2 + s3);
+  }
+}
+
+// out[r] = (C xv)[r]
+__device__ void c_apply(const Qs& S, const double* xv, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int r = threadIdx.x; r < S.m; r += blockDim.x)
+    if (S.rcol[r] >= 0) out[r] = S.rval[r] * xv[S.rcol[r]];
+  for (int gi = wid; gi < S.ng; gi += kQpWarps) {
+    const double* row = S.Cg + (int64_t)gi * S.n;
+    double s = 0.0;
+    for (int c = lane; c < S.n; c += 32) s = fma(row[c], xv[c], s);
+    s = warp_sum(s);
+    if (lane == 0) out[S.grow[gi]] = s;
+  }
+}
+
+// hu = H u from the packed symmetric H: warp per pair of rows, every lane
+// issues all of its loads of H before the multiply-adds (H may be in L2).
+template <int TM>
+__device__ void h_apply(const Qs& S, const double* uv, double* out) {
+  const int n = S.n, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int* cst = S.cstart;
+  for (int r0 = wid; r0 < n; r0 += 2 * kQpWarps) {
+    const int r1 = r0 + kQpWarps;
+    double h0[TM], h1[TM], uu[TM];
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      const int c = lane + 32 * t;
+      const bool live = c < n;
+      uu[t] = live ? uv[c] : 0.0;
+      h0[t] = live ? (c <= r0 ? S.Hp[colbase(c, n) + r0] : S.Hp[colbase(r0, n) + c]) : 0.0;
+      h1[t] = (live && r1 < n) ? (c <= r1 ? S.Hp[colbase(c, n) + r1] : S.Hp[colbase(r1, n) + c]) : 0.0;
+    }
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      s0 = fma(h0[t], uu[t], s0);
+      s1 = fma(h1[t], uu[t], s1);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if (lane == 0) {
+      out[r0] = s0;
+      if (r1 < n) out[r1] = s1;
+    }
+  }
+}
+
+// K = 2H + diag_add I + [diag(sum_single w val^2) + Cg' W Cg]   (qpsolver.py:178-184)
+// Lower triangle in 4x4 register tiles: tile (I, J), I >= J, covers rows
+// 4I..4I+3 and columns 4J..4J+3; its 16 entries of H are loaded first, then
+// the rank-ng update runs with 16 independent accumulators.
+__device__ void build_k(const Qs& S, double diag_add, bool terms) {
+  const int n = S.n, ng = terms ? S.ng : 0;
+  const int* cst = S.cstart;
+  const int nq = (n + 3) >> 2;
+  const int tiles = nq * (nq + 1) / 2;
+  for (int tt = threadIdx.x; tt < tiles; tt += blockDim.x) {
+    // column-major enumeration of lower tiles: column J holds nq - J tiles
+    const float q2 = 2.0f * nq + 1.0f;
+    int J = (int)((q2 - sqrtf(q2 * q2 - 8.0f * tt)) * 0.5f);
+    J = max(0, min(J, nq - 1));
+    while (J > 0 && J * nq - J * (J - 1) / 2 > tt) --J;
+    while ((J + 1) * nq - (J + 1) * J / 2 <= tt) ++J;
+    const int I = J + (tt - (J * nq - J * (J - 1) / 2));
+    const int r0 = 4 * I, c0 = 4 * J;
+    double acc[4][4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = c0 + b;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int r = r0 + a;
+        acc[a][b] = (c < n && r > c && r < n) ? 2.0 * S.Hp[colbase(c, n) + r] : 0.0;
+      }
+    }
+    for (int gi = 0; gi < ng; ++gi) {
+      const double* cg = S.Cg + (int64_t)gi * n;
+      const double wg = S.w[S.grow[gi]];
+      double x[4], y[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        x[a] = r0 + a < n ? cg[r0 + a] * wg : 0.0;
+        y[a] = c0 + a < n ? cg[c0 + a] : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = c0 + b;
+      if (c >= n) continue;
+      double* col = S.K + colbase(c, n);
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int r = r0 + a;
+        if (r < c || r >= n) continue;
+        col[r] = acc[a][b];
+      }
+    }
+  }
+  __syncthreads();
+  // diagonal (holds only the general-row term so far): (2H + reg) +
+  // bincount(single rows) first, then the general-row term, as the
+  // reference orders it
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    double dsum = 0.0;
+    if (terms)
+      for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
+        const int r = S.colrows[q];
+        dsum += S.w[r] * S.rval[r] * S.rval[r];
+      }
+    const int dc = colbase(c, n) + c;
+    S.K[dc] = ((2.0 * S.Hp[dc] + diag_add) + dsum) + S.K[dc];
+  }
+  __syncthreads();
+}
+
+__device__ void add_diag(const Qs& S, double bump) {
+  for (int c = threadIdx.x; c < S.n; c += blockDim.x) S.K[colbase(c, S.n) + c] += bump;
+  __syncthreads();
+}
+
+// largest step in [0, 1] with x + a dx > 0 (qpsolver.py:238-243)
+__device__ double max_step(const Qs& S, const double* x, const double* dx) {
+  double a = 1.0;
+  for (int r = threadIdx.x; r < S.m; r += blockDim.x)
+    if (dx[r] < 0.0) a = fmin(a, -x[r] / dx[r]);
+  return block_reduce<1>(a, S.red);
+}
+
+// du, dlam, ds for complementarity target rcv (qpsolver.py:204-209)
+template <int TM>
+__device__ void kkt_step(Qs& S, const double* rcv) {
+  for (int r = threadIdx.x; r < S.m; r += blockDim.x)
+    S.t[r] = (rcv[r] + S.lam[r] * S.rp[r]) / S.s[r];
+  __syncthreads();
+  ct_apply(S, S.t, S.ctl);
+  __syncthreads();
+  for (int c = threadIdx.x; c < S.n; c += blockDim.x) S.rhs[c] = -S.rd[c] - S.ctl[c];
+  __syncthreads();
+  qmark(S, 10);
+  chol_solve<TM>(S, S.rhs, S.du);
+  qmark(S, 11);
+  c_apply(S, S.du, S.t);  // C du
+  __syncthreads();
+  for (int r = threadIdx.x; r < S.m; r += blockDim.x) {
+    const double ds = -S.rp[r] - S.t[r];
+    S.ds[r] = ds;
+    S.dl[r] = (rcv[r] - S.lam[r] * ds) / S.s[r];
+  }
+  __syncthreads();
+}
+
+struct Resid {
+  double rs, rp, rc;
+};
+
+// residuals at (u, lam) (qpsolver.py:90-97); leaves r_dual in rd, C u in cu
+template <int TM>
+__device__ Resid residuals(Qs& S) {
+  h_apply<TM>(S, S.u, S.hu);
+  ct_apply(S, S.lam, S.ctl);
+  c_apply(S, S.u, S.cu);
+  __syncthreads();
+  double a_rs = 0.0, a_rp = -INFINITY, a_rc = 0.0;
+  for (int c = threadIdx.x; c < S.n; c += blockDim.x) {
+    const double rd = (2.0 * S.hu[c] + S.g[c]) + S.ctl[c];
+    S.rd[c] = rd;
+    a_rs = fmax(a_rs, fabs(rd));
+  }
+  for (int r = threadIdx.x; r < S.m; r += blockDim.x) {
+    const double viol = S.cu[r] - S.d[r];
+    a_rp = fmax(a_rp, viol);
+    a_rc = fmax(a_rc, fabs(S.lam[r] * viol));
+  }
+  Resid R;
+  R.rs = block_reduce<0>(a_rs, S.red);
+  R.rp = fmax(0.0, block_reduce<0>(a_rp, S.red));
+  R.rc = block_reduce<0>(a_rc, S.red);
+  return R;
+}
+
+template <int TM>
+__global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[kQpWarps];
+  __shared__ double pvbuf[8];
+  __shared__ double ysbuf[kTB];
   __shared__ int sh_int[4];
-  const int n = A.n, m = A.m, ldk = A.ldk;
+  const int n = A.n, m = A.m;
   const int64_t bi = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x;
   const double* H = A.H + bi * (int64_t)n * n;
-  const double* gg = A.g + bi * (int64_t)n;
   const double* C = A.C + bi * (int64_t)m * n;
-  const double* dd = A.d + bi * (int64_t)m;
-  double* gws = A.gws ? A.gws + bi * A.gws_stride : nullptr;
+  double* gws = A.gws + bi * A.gws_stride;
 
-  // ---- classify rows once (qpsolver.py:100-109): single-nonzero vs general
-  // first pass into registers of the layout-independent arrays
-  const QpLayout L0 = qp_layout(n, m, ldk, 0, false, false);
-  double* vec = (double*)(smem + L0.o_vec);
-  double* v_g = vec;
-  double* v_u = v_g + n;
-  double* v_hu = v_u + n;
-  double* v_rd = v_hu + n;
-  double* v_rhs = v_rd + n;
-  double* v_du = v_rhs + n;
-  double* v_ub = v_du + n;
-  double* v_dinv = v_ub + n;
-  double* v_ctl = v_dinv + n;
-  double* v_d = v_ctl + n;
-  double* v_s = v_d + m;
-  double* v_lam = v_s + m;
-  double* v_cu = v_lam + m;
-  double* v_rp = v_cu + m;
-  double* v_t = v_rp + m;
-  double* v_dl = v_t + m;
-  double* v_ds = v_dl + m;
-  double* v_dla = v_ds + m;
-  double* v_dsa = v_dla + m;
-  double* v_w = v_dsa + m;
-  double* v_lb = v_w + m;
-  double* v_rval = v_lb + m;
-  int* rcol = (int*)(smem + L0.o_ints);  // col of a single row, -1 for general rows
-  int* gpos = rcol + m;                  // general index of row r
-  int* grow = gpos + m;                  // row of general index g
-  int* colptr = grow + m;                // CSC of single rows, ascending row order
-  int* colrows = colptr + n + 1;
+  Qs S;
+  S.n = n;
+  S.m = m;
+  S.nblk = (n + kTB - 1) / kTB;
+  S.red = red;
+  S.pv = pvbuf;
+  S.ys = ysbuf;
+  S.flag = &sh_int[1];
+  S.prof = g_qp_prof_on && blockIdx.x == 0;
+  S.last = clock64();
+  {
+    const QpLayout L0 = qp_layout(n, m, 0, false, false);
+    double* v = (double*)(smem + L0.o_vec);
+    S.g = v; v += n;
+    S.u = v; v += n;
+    S.hu = v; v += n;
+    S.rd = v; v += n;
+    S.rhs = v; v += n;
+    S.du = v; v += n;
+    S.ub = v; v += n;
+    S.ctl = v; v += n;
+    S.ytmp = v; v += n;
+    S.dinv = v; v += n;
+    S.d = v; v += m;
+    S.s = v; v += m;
+    S.lam = v; v += m;
+    S.cu = v; v += m;
+    S.rp = v; v += m;
+    S.t = v; v += m;
+    S.dl = v; v += m;
+    S.ds = v; v += m;
+    S.tmp = v; v += m;
+    S.w = v; v += m;
+    S.lb = v; v += m;
+    S.rval = v;
+    int* ip = (int*)(smem + L0.o_ints);
+    S.rcol = ip;
+    S.grow = ip + m;
+    S.colptr = ip + 2 * m;
+    S.colrows = ip + 2 * m + n + 1;
+    S.cstart = ip + 3 * m + n + 1;
+    S.K = (double*)(smem + L0.o_k);
+    S.X = (double*)(smem + L0.o_x);
+  }
 
+  // ---- classify rows (qpsolver.py:100-109): single-nonzero vs general
   for (int r = wid; r < m; r += kQpWarps) {
     const double* Cr = C + (int64_t)r * n;
     int cnt = 0, first = n;
@@ -227,139 +704,67 @@ __global__ void __launch_bounds__(kQpThreads) k_solve_qp(const QpArgs A) {
       }
     }
     if (lane == 0) {
-      rcol[r] = cnt == 1 ? first : -1;
-      v_rval[r] = cnt == 1 ? fval : 0.0;
+      S.rcol[r] = cnt == 1 ? first : -1;
+      S.rval[r] = cnt == 1 ? fval : 0.0;
     }
   }
+  for (int c = tid; c <= n; c += nt) S.cstart[c] = c * n - (c * (c - 1)) / 2;
   __syncthreads();
   if (tid == 0) {
     int ng = 0;
-    for (int r = 0; r < m; ++r) {
-      if (rcol[r] < 0) {
-        gpos[r] = ng;
-        grow[ng++] = r;
-      } else {
-        gpos[r] = -1;
-      }
-    }
-    for (int c = 0; c <= n; ++c) colptr[c] = 0;
     for (int r = 0; r < m; ++r)
-      if (rcol[r] >= 0) colptr[rcol[r] + 1]++;
-    for (int c = 0; c < n; ++c) colptr[c + 1] += colptr[c];
+      if (S.rcol[r] < 0) S.grow[ng++] = r;
+    for (int c = 0; c <= n; ++c) S.colptr[c] = 0;
+    for (int r = 0; r < m; ++r)
+      if (S.rcol[r] >= 0) S.colptr[S.rcol[r] + 1]++;
+    for (int c = 0; c < n; ++c) S.colptr[c + 1] += S.colptr[c];
     for (int r = 0; r < m; ++r)  // counting sort: ascending row order per column
-      if (rcol[r] >= 0) colrows[colptr[rcol[r]]++] = r;
-    for (int c = n; c > 0; --c) colptr[c] = colptr[c - 1];
-    colptr[0] = 0;
+      if (S.rcol[r] >= 0) S.colrows[S.colptr[S.rcol[r]]++] = r;
+    for (int c = n; c > 0; --c) S.colptr[c] = S.colptr[c - 1];
+    S.colptr[0] = 0;
     sh_int[0] = ng;
   }
   __syncthreads();
-  const int ng = sh_int[0];
-  // general rows on-chip when they fit next to K, else in the global workspace
-  const bool cg_smem = qp_layout(n, m, ldk, ng, A.k_smem != 0, true).total <= A.smem_bytes;
-  const QpLayout LY = qp_layout(n, m, ldk, ng, A.k_smem != 0, cg_smem);
-  double* K = A.k_smem ? (double*)(smem + LY.o_k) : gws;
-  double* Cg = cg_smem ? (double*)(smem + LY.o_cg) : (gws + (A.k_smem ? 0 : (int64_t)ldk * n));
-  for (int t = tid; t < ng * n; t += nt) {
-    const int gi = t / n, c = t - gi * n;
-    Cg[t] = C[(int64_t)grow[gi] * n + c];
+  S.ng = sh_int[0];
+  {
+    const bool cg_smem = qp_layout(n, m, S.ng, false, true).total <= A.smem_bytes;
+    const bool h_smem = qp_layout(n, m, S.ng, true, cg_smem).total <= A.smem_bytes;
+    const QpLayout LY = qp_layout(n, m, S.ng, h_smem, cg_smem);
+    S.Cg = cg_smem ? (double*)(smem + LY.o_cg) : gws + packed_size(n);
+    S.Hp = h_smem ? (double*)(smem + LY.o_h) : gws;
   }
-  for (int t = tid; t < n; t += nt) v_g[t] = gg[t];
-  for (int t = tid; t < m; t += nt) v_d[t] = dd[t];
+  for (int t = tid; t < S.ng * n; t += nt) {
+    const int gi = t / n, c = t - gi * n;
+    S.Cg[t] = C[(int64_t)S.grow[gi] * n + c];
+  }
+  // pack H's lower triangle: element (r, c <= r) from row r
+  for (int r = wid; r < n; r += kQpWarps)
+    for (int c = lane; c <= r; c += 32) S.Hp[colbase(c, n) + r] = H[(int64_t)r * n + c];
+  for (int t = tid; t < n; t += nt) S.g[t] = A.g[bi * (int64_t)n + t];
+  for (int t = tid; t < m; t += nt) S.d[t] = A.d[bi * (int64_t)m + t];
   __syncthreads();
 
   // scale references (qpsolver.py:124-127)
   double hmax = 0.0, gmax = 0.0;
   for (int t = tid; t < n * n; t += nt) hmax = fmax(hmax, fabs(H[t]));
-  for (int t = tid; t < n; t += nt) gmax = fmax(gmax, fabs(v_g[t]));
+  for (int t = tid; t < n; t += nt) gmax = fmax(gmax, fabs(S.g[t]));
   hmax = block_reduce<0>(hmax, red);
   gmax = block_reduce<0>(gmax, red);
-  const double norm_g = n ? gmax : 0.0;
-  const double scale_k = fmin(1.0, fmax(n ? hmax : 0.0, norm_g));
+  const double norm_g = gmax;
+  const double scale_k = fmin(1.0, fmax(hmax, norm_g));
   const double scale_g = scale_k + norm_g;
   const double comp_ref = scale_k;
   const double tol = A.tol, reg = A.reg, tau = A.tau;
-
-  // (C' t) into out[n], t over all m rows
-  auto ct_apply = [&](const double* tv, double* out) {
-    for (int c = tid; c < n; c += nt) {
-      double s = 0.0;
-      for (int q = colptr[c]; q < colptr[c + 1]; ++q) {
-        const int r = colrows[q];
-        s = fma(v_rval[r], tv[r], s);
-      }
-      for (int gi = 0; gi < ng; ++gi) s = fma(Cg[(int64_t)gi * n + c], tv[grow[gi]], s);
-      out[c] = s;
-    }
-  };
-  // (C x) into out[m]
-  auto c_apply = [&](const double* xv, double* out) {
-    for (int r = tid; r < m; r += nt) {
-      if (rcol[r] >= 0) out[r] = v_rval[r] * xv[rcol[r]];
-    }
-    for (int gi = wid; gi < ng; gi += kQpWarps) {
-      const double* row = Cg + (int64_t)gi * n;
-      double s = 0.0;
-      for (int c = lane; c < n; c += 32) s = fma(row[c], xv[c], s);
-      s = warp_sum(s);
-      if (lane == 0) out[grow[gi]] = s;
-    }
-  };
-  // K = 2H + (reg or 0) I + boost I + diag(single) + Cg' W Cg, lower triangle,
-  // column-major.  Optionally hu = H u in the same pass over H.
-  auto build_k = [&](double diag_reg, double boost, bool with_terms, bool want_hu) {
-    for (int r = wid; r < n; r += kQpWarps) {
-      const double* Hr = H + (int64_t)r * n;
-      double* Kc = K + (int64_t)r * ldk;  // column r of K holds rows c >= r (symmetry)
-      double s = 0.0;
-      for (int c = lane; c < n; c += 32) {
-        const double h = Hr[c];
-        if (want_hu) s = fma(h, v_u[c], s);
-        if (c >= r) Kc[c] = 2.0 * h + (c == r ? diag_reg : 0.0);
-      }
-      if (want_hu) {
-        s = warp_sum(s);
-        if (lane == 0) v_hu[r] = s;
-      }
-    }
-    __syncthreads();
-    if (with_terms) {
-      for (int c = tid; c < n; c += nt) {  // np.bincount(s_cols, weights=w*val*val)
-        double s = 0.0;
-        for (int q = colptr[c]; q < colptr[c + 1]; ++q) {
-          const int r = colrows[q];
-          s += v_w[r] * v_rval[r] * v_rval[r];
-        }
-        K[(int64_t)c * ldk + c] += s;
-      }
-      if (ng > 0) {
-        for (int c = wid; c < n; c += kQpWarps) {
-          double* Kc = K + (int64_t)c * ldk;
-          for (int r = c + lane; r < n; r += 32) {
-            double s = 0.0;
-            for (int gi = 0; gi < ng; ++gi) {
-              const double* row = Cg + (int64_t)gi * n;
-              s = fma(row[r] * v_w[grow[gi]], row[c], s);
-            }
-            Kc[r] += s;
-          }
-        }
-      }
-    }
-    if (boost != 0.0)
-      for (int c = tid; c < n; c += nt) K[(int64_t)c * ldk + c] += boost;
-    __syncthreads();
-  };
-
   double* uo = A.u_out + bi * (int64_t)n;
   double* lo = A.lam_out + bi * (int64_t)m;
 
   // ---- unconstrained problems (qpsolver.py:131-144)
   if (m == 0) {
-    const double boosts[4] = {0.0, reg, reg * 1e3, reg * 1e6};
     bool ok = false;
     for (int t = 0; t < 4 && !ok; ++t) {
-      build_k(0.0, boosts[t], false, false);
-      ok = chol_factor(K, n, ldk, v_dinv, red);
+      const double boost = t == 0 ? 0.0 : (t == 1 ? reg : (t == 2 ? reg * 1e3 : reg * 1e6));
+      build_k(S, boost, false);
+      ok = chol_factor<TM>(S);
     }
     if (!ok) {
       for (int t = tid; t < n; t += nt) uo[t] = 0.0;
@@ -370,19 +775,16 @@ __global__ void __launch_bounds__(kQpThreads) k_solve_qp(const QpArgs A) {
       }
       return;
     }
-    for (int t = tid; t < n; t += nt) v_rhs[t] = -v_g[t];
+    invert_diag_blocks(S);
+    for (int t = tid; t < n; t += nt) S.rhs[t] = -S.g[t];
     __syncthreads();
-    chol_solve(K, n, ldk, v_dinv, v_rhs, v_u);
-    // stationarity max|2Hu + g|
+    chol_solve<TM>(S, S.rhs, S.u);
+    h_apply<TM>(S, S.u, S.hu);
+    __syncthreads();
     double rs = 0.0;
-    for (int r = wid; r < n; r += kQpWarps) {
-      double s = 0.0;
-      for (int c = lane; c < n; c += 32) s = fma(2.0 * H[(int64_t)r * n + c], v_u[c], s);
-      s = warp_sum(s);
-      rs = fmax(rs, fabs(s + v_g[r]));
-    }
+    for (int c = tid; c < n; c += nt) rs = fmax(rs, fabs(2.0 * S.hu[c] + S.g[c]));
     rs = block_reduce<0>(rs, red);
-    for (int t = tid; t < n; t += nt) uo[t] = v_u[t];
+    for (int t = tid; t < n; t += nt) uo[t] = S.u[t];
     if (tid == 0) {
       A.status[bi] = GM_QP_OPTIMAL;
       A.iters[bi] = 0;
@@ -394,111 +796,66 @@ __global__ void __launch_bounds__(kQpThreads) k_solve_qp(const QpArgs A) {
   }
 
   // ---- start point (qpsolver.py:146-150)
-  for (int t = tid; t < n; t += nt) v_u[t] = A.warm ? A.warm[bi * (int64_t)n + t] : 0.0;
+  for (int t = tid; t < n; t += nt) S.u[t] = A.warm ? A.warm[bi * (int64_t)n + t] : 0.0;
   __syncthreads();
-  c_apply(v_u, v_cu);
+  c_apply(S, S.u, S.cu);
   __syncthreads();
   for (int r = tid; r < m; r += nt) {
-    v_s[r] = fmax(v_d[r] - v_cu[r], 1.0) * 1.1;
-    v_lam[r] = 1.0;
+    S.s[r] = fmax(S.d[r] - S.cu[r], 1.0) * 1.1;
+    S.lam[r] = 1.0;
   }
   __syncthreads();
 
   double best_metric = INFINITY, b_rs = 0, b_rp = 0, b_rc = 0;
-  int status = -1, iters = 0;
   double f_rs = 0, f_rp = 0, f_rc = 0;
+  int status = -1, iters = 0;
   bool use_best = false;
 
-  // residuals at (u, lam) with best-iterate tracking (qpsolver.py:158-165);
-  // leaves r_dual in v_rd and C u in v_cu
-  auto residuals = [&](bool want_k, double& rs, double& rp, double& rc) {
-    for (int r = tid; r < m; r += nt) v_w[r] = v_lam[r] / v_s[r];
-    __syncthreads();
-    build_k(reg, 0.0, want_k, true);  // hu = H u (and K for this iteration)
-    ct_apply(v_lam, v_ctl);
-    c_apply(v_u, v_cu);
-    __syncthreads();
-    double a_rs = 0.0, a_rp = 0.0, a_rc = 0.0;
-    for (int c = tid; c < n; c += nt) {
-      const double rd = (2.0 * v_hu[c] + v_g[c]) + v_ctl[c];
-      v_rd[c] = rd;
-      a_rs = fmax(a_rs, fabs(rd));
-    }
-    for (int r = tid; r < m; r += nt) {
-      const double viol = v_cu[r] - v_d[r];
-      a_rp = fmax(a_rp, viol);
-      a_rc = fmax(a_rc, fabs(v_lam[r] * viol));
-    }
-    rs = block_reduce<0>(a_rs, red);
-    rp = fmax(0.0, block_reduce<0>(a_rp, red));  // max(0, max viol)
-    rc = block_reduce<0>(a_rc, red);
-    const double metric = fmax(fmax(rs / scale_g, rp), rc / fmax(comp_ref, 1e-300));
-    if (metric < best_metric) {
-      best_metric = metric;
-      b_rs = rs;
-      b_rp = rp;
-      b_rc = rc;
-      for (int t = tid; t < n; t += nt) v_ub[t] = v_u[t];
-      for (int t = tid; t < m; t += nt) v_lb[t] = v_lam[t];
-    }
-    __syncthreads();
-  };
-
-  // step length to the boundary (qpsolver.py:238-243)
-  auto max_step = [&](const double* x, const double* dx) {
-    double a = 1.0;
-    for (int r = tid; r < m; r += nt)
-      if (dx[r] < 0.0) a = fmin(a, -x[r] / dx[r]);
-    return block_reduce<1>(a, red);
-  };
-
-  // KKT direction for complementarity target rc_vec (in v_t on entry is
-  // overwritten): du -> v_du, dlam -> v_dl, ds -> v_ds (qpsolver.py:204-209)
-  auto kkt_step = [&](const double* rcv) {
-    for (int r = tid; r < m; r += nt) v_t[r] = (rcv[r] + v_lam[r] * v_rp[r]) / v_s[r];
-    __syncthreads();
-    ct_apply(v_t, v_ctl);
-    __syncthreads();
-    for (int c = tid; c < n; c += nt) v_rhs[c] = -v_rd[c] - v_ctl[c];
-    __syncthreads();
-    chol_solve(K, n, ldk, v_dinv, v_rhs, v_du);
-    c_apply(v_du, v_t);  // C du
-    __syncthreads();
-    for (int r = tid; r < m; r += nt) {
-      const double ds = -v_rp[r] - v_t[r];
-      v_ds[r] = ds;
-      v_dl[r] = (rcv[r] - v_lam[r] * ds) / v_s[r];
-    }
-    __syncthreads();
-  };
-
+  qmark(S, 0);
   for (int it = 0; it < A.max_it; ++it) {
-    double rs, rp, rc;
-    residuals(true, rs, rp, rc);
-    if (rs <= tol * scale_g && rp <= tol && rc <= tol * comp_ref) {
+    const Resid R = residuals<TM>(S);
+    qmark(S, 1);
+    const double metric = fmax(fmax(R.rs / scale_g, R.rp), R.rc / fmax(comp_ref, 1e-300));
+    if (metric < best_metric) {  // record_best (qpsolver.py:158-165)
+      best_metric = metric;
+      b_rs = R.rs;
+      b_rp = R.rp;
+      b_rc = R.rc;
+      for (int t = tid; t < n; t += nt) S.ub[t] = S.u[t];
+      for (int t = tid; t < m; t += nt) S.lb[t] = S.lam[t];
+    }
+    if (R.rs <= tol * scale_g && R.rp <= tol && R.rc <= tol * comp_ref) {
       status = GM_QP_OPTIMAL;
       iters = it;
-      f_rs = rs;
-      f_rp = rp;
-      f_rc = rc;
+      f_rs = R.rs;
+      f_rp = R.rp;
+      f_rc = R.rc;
       break;
     }
     double lmax = 0.0;
-    for (int r = tid; r < m; r += nt) lmax = fmax(lmax, v_lam[r]);
+    for (int r = tid; r < m; r += nt) lmax = fmax(lmax, S.lam[r]);
     lmax = block_reduce<0>(lmax, red);
-    if (lmax > 1e12 && rp > 1e-6) {
+    if (lmax > 1e12 && R.rp > 1e-6) {
       status = GM_QP_PRIMAL_INFEASIBLE;
       iters = it;
       use_best = true;
       break;
     }
-    // Cholesky with escalating regularisation (qpsolver.py:186-198)
-    bool ok = chol_factor(K, n, ldk, v_dinv, red);
+    qmark(S, 2);
+    // Schur matrix and Cholesky with escalating regularisation (qpsolver.py:178-198)
+    for (int r = tid; r < m; r += nt) S.w[r] = S.lam[r] / S.s[r];
+    __syncthreads();
+    build_k(S, reg, true);
+    qmark(S, 3);
+    bool ok = chol_factor<TM>(S);
+    qmark(S, 4);
     double boost = 0.0;
     for (int att = 1; att < 4 && !ok; ++att) {
-      boost = boost == 0.0 ? fmax(reg * 1e3, 1e-12) : boost * 1e3;
-      build_k(reg, boost, true, false);
-      ok = chol_factor(K, n, ldk, v_dinv, red);
+      const double bump = boost == 0.0 ? fmax(reg * 1e3, 1e-12) : boost * 1e3;
+      boost = bump;
+      build_k(S, reg, true);
+      add_diag(S, boost);
+      ok = chol_factor<TM>(S);
     }
     if (!ok) {
       status = GM_QP_NUMERICAL_FAILURE;
@@ -506,42 +863,47 @@ __global__ void __launch_bounds__(kQpThreads) k_solve_qp(const QpArgs A) {
       use_best = true;
       break;
     }
+    invert_diag_blocks(S);
+    __syncthreads();
+    qmark(S, 5);
     // r_pri = C u + s - d, mu = lam.s / m
     double mu_loc = 0.0;
     for (int r = tid; r < m; r += nt) {
-      v_rp[r] = v_cu[r] + v_s[r] - v_d[r];
-      mu_loc += v_lam[r] * v_s[r];
+      S.rp[r] = S.cu[r] + S.s[r] - S.d[r];
+      mu_loc += S.lam[r] * S.s[r];
     }
     const double mu = block_reduce<2>(mu_loc, red) / m;
-    // affine direction
-    for (int r = tid; r < m; r += nt) v_dsa[r] = -v_lam[r] * v_s[r];  // rc target, temp
+    // affine direction: rc = -lam s
+    for (int r = tid; r < m; r += nt) S.tmp[r] = -S.lam[r] * S.s[r];
     __syncthreads();
-    kkt_step(v_dsa);
-    const double ap = max_step(v_s, v_ds);
-    const double ad = max_step(v_lam, v_dl);
+    qmark(S, 6);
+    kkt_step<TM>(S, S.tmp);
+    qmark(S, 7);
+    const double ap = max_step(S, S.s, S.ds);
+    const double ad = max_step(S, S.lam, S.dl);
     double maff = 0.0;
-    for (int r = tid; r < m; r += nt) maff += (v_lam[r] + ad * v_dl[r]) * (v_s[r] + ap * v_ds[r]);
+    for (int r = tid; r < m; r += nt) maff += (S.lam[r] + ad * S.dl[r]) * (S.s[r] + ap * S.ds[r]);
     const double mu_aff = block_reduce<2>(maff, red) / m;
     const double sigma = mu > 0.0 ? (mu_aff / mu) * (mu_aff / mu) * (mu_aff / mu) : 0.0;
     // corrector with centring: rc = -lam s - dlam_a ds_a + sigma mu
-    for (int r = tid; r < m; r += nt) {
-      const double dla = v_dl[r], dsa = v_ds[r];
-      v_dla[r] = -v_lam[r] * v_s[r] - dla * dsa + sigma * mu;
-    }
+    for (int r = tid; r < m; r += nt) S.tmp[r] = -S.lam[r] * S.s[r] - S.dl[r] * S.ds[r] + sigma * mu;
     __syncthreads();
-    kkt_step(v_dla);
-    const double alpha = fmin(tau * max_step(v_s, v_ds), tau * max_step(v_lam, v_dl));
+    qmark(S, 8);
+    kkt_step<TM>(S, S.tmp);
+    qmark(S, 7);
+    const double alpha = fmin(tau * max_step(S, S.s, S.ds), tau * max_step(S, S.lam, S.dl));
     bool finite = true;
     for (int c = tid; c < n; c += nt) {
-      v_u[c] = v_u[c] + alpha * v_du[c];
-      if (!isfinite(v_u[c])) finite = false;
+      S.u[c] = S.u[c] + alpha * S.du[c];
+      if (!isfinite(S.u[c])) finite = false;
     }
     for (int r = tid; r < m; r += nt) {
-      v_s[r] = v_s[r] + alpha * v_ds[r];
-      v_lam[r] = v_lam[r] + alpha * v_dl[r];
-      if (!isfinite(v_s[r]) || !isfinite(v_lam[r])) finite = false;
+      S.s[r] = S.s[r] + alpha * S.ds[r];
+      S.lam[r] = S.lam[r] + alpha * S.dl[r];
+      if (!isfinite(S.s[r]) || !isfinite(S.lam[r])) finite = false;
     }
     const int all_finite = __syncthreads_and(finite ? 1 : 0);
+    qmark(S, 9);
     if (!all_finite) {
       status = GM_QP_NUMERICAL_FAILURE;
       iters = it + 1;
@@ -550,21 +912,30 @@ __global__ void __launch_bounds__(kQpThreads) k_solve_qp(const QpArgs A) {
     }
   }
   if (status < 0) {  // iteration cap (qpsolver.py:231-235)
-    double rs, rp, rc;
-    residuals(false, rs, rp, rc);
+    const Resid R = residuals<TM>(S);
+    const double metric = fmax(fmax(R.rs / scale_g, R.rp), R.rc / fmax(comp_ref, 1e-300));
+    if (metric < best_metric) {
+      best_metric = metric;
+      b_rs = R.rs;
+      b_rp = R.rp;
+      b_rc = R.rc;
+      for (int t = tid; t < n; t += nt) S.ub[t] = S.u[t];
+      for (int t = tid; t < m; t += nt) S.lb[t] = S.lam[t];
+    }
     iters = A.max_it;
-    if (rs <= tol * scale_g && rp <= tol && rc <= tol * comp_ref) {
+    if (R.rs <= tol * scale_g && R.rp <= tol && R.rc <= tol * comp_ref) {
       status = GM_QP_OPTIMAL;
-      f_rs = rs;
-      f_rp = rp;
-      f_rc = rc;
+      f_rs = R.rs;
+      f_rp = R.rp;
+      f_rc = R.rc;
     } else {
       status = GM_QP_MAX_ITERATIONS;
       use_best = true;
     }
   }
-  const double* us = use_best ? v_ub : v_u;
-  const double* ls = use_best ? v_lb : v_lam;
+  __syncthreads();
+  const double* us = use_best ? S.ub : S.u;
+  const double* ls = use_best ? S.lb : S.lam;
   for (int t = tid; t < n; t += nt) uo[t] = us[t];
   for (int t = tid; t < m; t += nt) lo[t] = ls[t];
   if (tid == 0) {
@@ -576,7 +947,83 @@ __global__ void __launch_bounds__(kQpThreads) k_solve_qp(const QpArgs A) {
   }
 }
 
+// Diagnostic kernel: factor a dense SPD A (n x n) with the solver's own
+// chol_factor / invert_diag_blocks / chol_solve and return L and A^{-1} b.
+template <int TM>
+__global__ void __launch_bounds__(kQpThreads, 1) k_chol_check(int n, const double* A, const double* b,
+                                                               double* L, double* x, int* ok) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[kQpWarps];
+  __shared__ double pvbuf[8];
+  __shared__ double ysbuf[kTB];
+  __shared__ int sh_int[4];
+  Qs S;
+  S.n = n;
+  S.m = 0;
+  S.ng = 0;
+  S.nblk = (n + kTB - 1) / kTB;
+  S.red = red;
+  S.pv = pvbuf;
+  S.ys = ysbuf;
+  S.flag = &sh_int[1];
+  S.prof = false;
+  const QpLayout L0 = qp_layout(n, 0, 0, false, false);
+  double* v = (double*)(smem + L0.o_vec);
+  S.rhs = v;
+  S.du = v + n;
+  S.ctl = v + 2 * n;
+  S.ytmp = v + 3 * n;
+  S.dinv = v + 4 * n;
+  S.K = (double*)(smem + L0.o_k);
+  S.X = (double*)(smem + L0.o_x);
+  for (int c = threadIdx.x; c < n; c += blockDim.x)
+    for (int r = c; r < n; ++r) S.K[colbase(c, n) + r] = A[(int64_t)r * n + c];
+  for (int r = threadIdx.x; r < n; r += blockDim.x) S.rhs[r] = b[r];
+  __syncthreads();
+  const bool good = chol_factor<TM>(S);
+  if (threadIdx.x == 0) *ok = good ? 1 : 0;
+  if (!good) return;
+  invert_diag_blocks(S);
+  __syncthreads();
+  for (int c = threadIdx.x; c < n; c += blockDim.x)
+    for (int r = 0; r < n; ++r) L[(int64_t)r * n + c] = r >= c ? S.K[colbase(c, n) + r] : 0.0;
+  chol_solve<TM>(S, S.rhs, S.du);
+  for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = S.du[r];
+}
+
 }  // namespace
+
+extern "C" int gm_chol_check(gm_ctx* ctx, int n, const double* A, const double* b, double* L,
+                             double* x, int32_t* ok, void* stream) {
+  int rc = gm_need_device(ctx);
+  if (rc) return rc;
+  if (n < 1 || n > 256) return gm_fail(ctx, GM_ERR_CONFIG, "n must be in [1, 256]");
+  const size_t sm = qp_layout(n, 0, 0, false, false).total;
+  const int tm = (n + 31) / 32;
+  auto launch = [&](auto kern) -> int {
+    GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kern<<<1, kQpThreads, sm, (cudaStream_t)stream>>>(n, A, b, L, x, ok);
+    GM_LAUNCH_CHECK(ctx, "k_chol_check");
+    return GM_OK;
+  };
+  if (tm <= 2) return launch(k_chol_check<2>);
+  if (tm <= 4) return launch(k_chol_check<4>);
+  if (tm <= 5) return launch(k_chol_check<5>);
+  return launch(k_chol_check<8>);
+}
+
+extern "C" int gm_qp_profile(int on) {
+  cudaMemcpyToSymbol(g_qp_prof_on, &on, sizeof(int));
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_qp_prof, z, sizeof(z));
+  return GM_OK;
+}
+
+extern "C" int gm_qp_phase_cycles(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_qp_prof, sizeof(unsigned long long) * 16) == cudaSuccess
+             ? GM_OK
+             : GM_ERR_CUDA;
+}
 
 extern "C" int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, const double* g,
                            const double* C, const double* d, const double* warm,
@@ -589,23 +1036,18 @@ extern "C" int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, co
   gm_qp_settings s{1e-8, 50, 1e-9, 0.995};
   if (settings) s = *settings;
   if (!(s.tolerance > 0)) return gm_fail(ctx, GM_ERR_CONFIG, "tolerance must be positive");
-  const int ldk = n | 1;  // odd leading dimension: conflict-free column and row walks
-  // placement: vectors always on-chip; K on-chip when it fits; the general
-  // constraint rows (count known only on the device) go on-chip if room is left.
+  // vectors, the packed Schur matrix and the inverted diagonal blocks always
+  // live on-chip; general rows, then packed H, go on-chip when room is left
   const size_t cap = ctx->smem_optin - 1024;
-  bool k_smem = qp_layout(n, m, ldk, 0, true, false).total <= cap;
-  if (qp_layout(n, m, ldk, 0, false, false).total > cap)
-    return gm_fail(ctx, GM_ERR_CONFIG, "QP too large for the on-chip vectors");
-  const size_t want = qp_layout(n, m, ldk, m, k_smem, true).total;
-  const size_t smem_bytes = std::min(cap, want);
-  const int64_t gws_stride = (k_smem ? 0 : (int64_t)ldk * n) + (int64_t)m * n;
+  const QpLayout base = qp_layout(n, m, 0, false, false);
+  if (base.total > cap) return gm_fail(ctx, GM_ERR_CONFIG, "QP too large for the on-chip solver");
+  const size_t smem_bytes = std::min(cap, qp_layout(n, m, m, true, true).total);
+  const int64_t gws_stride = packed_size(n) + (int64_t)m * n;
   double* gws = (double*)gm_scratch(ctx, sizeof(double) * (size_t)gws_stride * B);
   if (!gws) return gm_fail(ctx, GM_ERR_CUDA, "QP workspace allocation failed");
   QpArgs a{};
   a.n = n;
   a.m = m;
-  a.ldk = ldk;
-  a.k_smem = k_smem;
   a.smem_bytes = smem_bytes;
   a.H = H;
   a.g = g;
@@ -623,8 +1065,16 @@ extern "C" int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, co
   a.resid = resid;
   a.gws = gws;
   a.gws_stride = gws_stride;
-  GM_CUDA(ctx, cudaFuncSetAttribute(k_solve_qp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
-  k_solve_qp<<<B, kQpThreads, smem_bytes, (cudaStream_t)stream>>>(a);
-  GM_LAUNCH_CHECK(ctx, "k_solve_qp");
-  return GM_OK;
+  const int tm = (n + 31) / 32;
+  auto launch = [&](auto kern) -> int {
+    GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+    kern<<<B, kQpThreads, smem_bytes, (cudaStream_t)stream>>>(a);
+    GM_LAUNCH_CHECK(ctx, "k_solve_qp");
+    return GM_OK;
+  };
+  if (tm <= 2) return launch(k_solve_qp<2>);
+  if (tm <= 4) return launch(k_solve_qp<4>);
+  if (tm <= 5) return launch(k_solve_qp<5>);
+  if (tm <= 8) return launch(k_solve_qp<8>);
+  return gm_fail(ctx, GM_ERR_CONFIG, "QP with n > 256 variables is not supported by this build");
 }

@@ -135,9 +135,11 @@ def test_qp_on_reference_data(pkg, name):
 def test_random_qps(pkg):
     for t, q in enumerate(random_qps()):
         sol = pkg.solve_qp(pkg.QpProblem(q.H, q.g, q.C, q.d))
-        assert sol.status.value == q.status, t
-        assert abs(sol.iterations - q.iterations) <= 1, t
-        assert np.max(np.abs(sol.u - q.u)) <= 1e-6, t
+        info = (t, q.H.shape, q.C.shape, sol.status.value, q.status, sol.iterations, q.iterations,
+                float(np.max(np.abs(sol.u - q.u))))
+        assert sol.status.value == q.status, info
+        assert abs(sol.iterations - q.iterations) <= 1, info
+        assert np.max(np.abs(sol.u - q.u)) <= 1e-6, info
 
 
 def test_qp_batched_matches_single(pkg):
@@ -189,3 +191,30 @@ def test_mpc_step_matches_reference(pkg, name):
     assert st2.last_status.value == STATUS[int(d["mpc2_meta"][0])]
     assert float(np.max(np.abs(u2.u - d["mpc2_u"]))) / scale <= TOL
     assert rel(st2.lin_states, d["mpc2_lin_states"]) <= TOL
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 6, 7, 31, 32, 33, 64, 70, 100, 140, 141, 160])
+def test_device_cholesky_and_solve(pkg, n):
+    """K-QP's factorisation (2x2-pivot block elimination -> Cholesky) and its
+    blocked triangular solves against NumPy on SPD matrices."""
+    import torch
+
+    from paper_2602_17601_b200 import device
+
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n))
+    A = A @ A.T + 0.5 * np.eye(n)
+    b = rng.standard_normal(n)
+    eng = device.engine(pkg.chain_topology(1))
+    dA, db = eng.h2d(A, np.float64), eng.h2d(b, np.float64)
+    L = eng.empty((n, n), np.float64)
+    x = eng.empty((n,), np.float64)
+    ok = eng.empty((1,), np.int32)
+    eng.ctx.call("gm_chol_check", n, dA.data_ptr(), db.data_ptr(), L.data_ptr(), x.data_ptr(),
+                 ok.data_ptr(), eng.stream_ptr())
+    torch.cuda.synchronize()
+    assert int(ok.cpu()[0]) == 1
+    Ln = L.cpu().numpy()
+    assert np.max(np.abs(Ln - np.linalg.cholesky(A))) <= 1e-10 * np.max(np.abs(A))
+    xr = np.linalg.solve(A, b)
+    assert np.max(np.abs(x.cpu().numpy() - xr)) <= 1e-9 * max(1.0, np.max(np.abs(xr)))
