@@ -33,7 +33,7 @@
 
 namespace {
 
-constexpr int kQpThreads = 512;
+constexpr int kQpThreads = 256;
 constexpr int kQpWarps = kQpThreads / 32;
 constexpr int kTB = 32;  // triangular-solve block
 constexpr int kXL = 33;  // leading dimension of an inverted diagonal block
@@ -98,7 +98,7 @@ struct Qs {  // per-CTA views
   double *d, *s, *lam, *cu, *rp, *t, *dl, *ds, *tmp, *w, *lb, *rval;
   int *rcol, *grow, *colptr, *colrows, *cstart;
   double* red;
-  double* pv;  // 2 x 4 pivot-block inverses (double buffered)
+  double* pv;  // 2 x 16 pivot-block factors (double buffered)
   double* ys;  // 32-entry staging vector of the triangular solves
   int* flag;
   bool prof;
@@ -148,152 +148,246 @@ __device__ double block_reduce(double v, double* red) {
 // (an integer multiply-add instead of a dependent shared-memory load).
 __device__ __forceinline__ int colbase(int c, int n) { return c * n - ((c * (c + 1)) >> 1); }
 
-// Pivot block P = [[a, b], [b, c]] (or 1x1 when bs == 1) factored with the
-// scalar Cholesky formulas (as LAPACK potf2 would): pv = {1/l00, l10, 1/l11}
-// with l00 = sqrt(a), l10 = b / l00, l11 = sqrt(c - l10^2).  Fails on a
-// non-positive or NaN scalar pivot (potrf's rule).  (An explicit 2x2 inverse
-// via the determinant is measurably less stable on the ill-conditioned
-// Schur matrices of late IPM iterations.)
-__device__ __forceinline__ bool pivot_chol(double a, double b, double c, int bs, double* pv) {
-  if (!(a > 0.0)) return false;
-  const double i00 = rsqrt(a);
-  pv[0] = i00;
-  if (bs == 1) {
-    pv[1] = 0.0;
-    pv[2] = 0.0;
-    return true;
+// Blocked right-looking Cholesky, kNB = 4 columns per step.
+//
+// Pivot block factor F (4x4 lower, scalar Cholesky formulas as LAPACK potf2):
+//   pv[0..3] = 1 / L[q][q],  pv[4..9] = l10 l20 l21 l30 l31 l32.
+// Row x of L in the block's columns from its Schur-complement row w:
+//   x = w F^{-T}  (forward substitution with F).
+constexpr int kNB = 4;
+
+__device__ __forceinline__ void lrow4(const double (&w)[kNB], const double* pv, double (&x)[kNB]) {
+  x[0] = w[0] * pv[0];
+  x[1] = fma(-pv[4], x[0], w[1]) * pv[1];
+  x[2] = fma(-pv[6], x[1], fma(-pv[5], x[0], w[2])) * pv[2];
+  x[3] = fma(-pv[9], x[2], fma(-pv[8], x[1], fma(-pv[7], x[0], w[3]))) * pv[3];
+}
+
+// Factor the (updated) bs x bs pivot block E (lower, E[a][b] a >= b) into pv.
+// Missing columns (bs < 4) get zero entries so lrow4 yields zeros for them.
+// Fails on a non-positive / NaN scalar pivot (potrf's rule).
+__device__ __forceinline__ bool factor_pivot(const double (&E)[kNB][kNB], int bs, double* pv) {
+  double i[kNB] = {0.0, 0.0, 0.0, 0.0}, l[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  bool ok = true;
+  if (!(E[0][0] > 0.0)) ok = false;
+  i[0] = rsqrt(E[0][0]);
+  if (bs > 1) {
+    l[0] = E[1][0] * i[0];
+    const double t1 = fma(-l[0], l[0], E[1][1]);
+    if (!(t1 > 0.0)) ok = false;
+    i[1] = rsqrt(t1);
   }
-  const double l10 = b * i00;
-  const double t = fma(-l10, l10, c);
-  if (!(t > 0.0)) return false;
-  pv[1] = l10;
-  pv[2] = rsqrt(t);
-  return true;
+  if (bs > 2) {
+    l[1] = E[2][0] * i[0];
+    l[2] = fma(-l[1], l[0], E[2][1]) * i[1];
+    const double t2 = fma(-l[2], l[2], fma(-l[1], l[1], E[2][2]));
+    if (!(t2 > 0.0)) ok = false;
+    i[2] = rsqrt(t2);
+  }
+  if (bs > 3) {
+    l[3] = E[3][0] * i[0];
+    l[4] = fma(-l[3], l[0], E[3][1]) * i[1];
+    l[5] = fma(-l[4], l[2], fma(-l[3], l[1], E[3][2])) * i[2];
+    const double t3 = fma(-l[5], l[5], fma(-l[4], l[4], fma(-l[3], l[3], E[3][3])));
+    if (!(t3 > 0.0)) ok = false;
+    i[3] = rsqrt(t3);
+  }
+#pragma unroll
+  for (int q = 0; q < kNB; ++q) pv[q] = i[q];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) pv[4 + q] = l[q];
+  return ok;
 }
 
-// Row x of the two L columns of a pivot block from its Schur-complement row w.
-__device__ __forceinline__ void lrow(double w0, double w1, double i00, double l10, double i11,
-                                     double& x0, double& x1) {
-  x0 = w0 * i00;
-  x1 = fma(-x0, l10, w1) * i11;
+// Rank-4 update of one group of 4 adjacent columns [c0g, c0g+4) for the rows
+// this lane owns (lane + 32t): K[r][c] -= Lr[t] . Lc[u].  Row tiles t < T0 lie
+// entirely above the group and are not generated (T0 is a template
+// parameter), so the body is straight-line: all loads, then the FMAs, then
+// predicated stores -- the chains of all 4 x (TM - T0) slots overlap.
+// cjq[q] = colbase(j + q) (pivot column q; W[x][q] = K[cjq[q] + x]).
+template <int TM, int T0>
+__device__ __forceinline__ void update_group(double* K, int n, int c0g, int pe, const int (&cjq)[kNB],
+                                             const double* pv, const double (&Lr)[TM][kNB],
+                                             int lane) {
+  double Lc[kNB][kNB];
+  double* col[kNB];
+#pragma unroll
+  for (int u = 0; u < kNB; ++u) {
+    const int c = min(c0g + u, n - 1);
+    double w[kNB];
+#pragma unroll
+    for (int q = 0; q < kNB; ++q) w[q] = K[cjq[q] + c];
+    lrow4(w, pv, Lc[u]);
+    col[u] = K + colbase(c, n);
+  }
+  double v[kNB][TM];
+#pragma unroll
+  for (int u = 0; u < kNB; ++u)
+#pragma unroll
+    for (int t = T0; t < TM; ++t) v[u][t] = col[u][min(lane + 32 * t, n - 1)];
+#pragma unroll
+  for (int u = 0; u < kNB; ++u) {
+    const int c = c0g + u;
+    const int rlo = c < pe ? pe : c;  // next pivot block rows belong to the look-ahead
+#pragma unroll
+    for (int t = T0; t < TM; ++t) {
+      const int r = lane + 32 * t;
+      const double nv = fma(-Lr[t][3], Lc[u][3],
+                            fma(-Lr[t][2], Lc[u][2],
+                                fma(-Lr[t][1], Lc[u][1], fma(-Lr[t][0], Lc[u][0], v[u][t]))));
+      if (c < n && r >= rlo && r < n) col[u][r] = nv;
+    }
+  }
 }
 
-// Factor K = L L' in place; false on a failed pivot; dinv[j] = 1/L[j][j].
-// Columns are eliminated two at a time (one CTA barrier per pair): warp 0
-// lane 0 updates and factors the next pivot block one step ahead while warps
-// 1..15 apply the current pair's rank-2 update to the trailing matrix.  The
-// panels keep their Schur-complement values W until a final parallel pass
-// scales them into L.
+template <int TM, int T0>
+__device__ __forceinline__ void update_group_dispatch(int t0, double* K, int n, int c0g, int pe,
+                                                      const int (&cjq)[kNB], const double* pv,
+                                                      const double (&Lr)[TM][kNB], int lane) {
+  if constexpr (T0 < TM - 1) {
+    if (t0 > T0) {
+      update_group_dispatch<TM, T0 + 1>(t0, K, n, c0g, pe, cjq, pv, Lr, lane);
+      return;
+    }
+  }
+  update_group<TM, T0>(K, n, c0g, pe, cjq, pv, Lr, lane);
+}
+
+// Factor K = L L' in place (packed lower); false on a failed pivot;
+// dinv[j] = 1/L[j][j].  Steps of kNB columns, one CTA barrier per step:
+// warp 0 lane 0 updates and factors the NEXT 4x4 pivot block (look-ahead)
+// while warps 1.. apply the current block's rank-4 update to the trailing
+// matrix in groups of 4 adjacent columns.  Panels keep their Schur-complement
+// values W until a final parallel pass turns them into L.
 template <int TM>
 __device__ bool chol_factor(Qs& S) {
   const int n = S.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double* K = S.K;
-  double* pi00 = S.ytmp;  // per pivot pair j: ytmp[j] = 1/l00, ytmp[j+1] = 1/l11
-  double* pl10 = S.ctl;   // ctl[j] = l10
+  double* fl = S.ytmp;  // per block j: ytmp[j..j+3] = l10 l20 l21 l30, ctl[j..j+1] = l31 l32
+  double* fl2 = S.ctl;
+  auto save_factor = [&](int jb, const double* pv) {
+#pragma unroll
+    for (int q = 0; q < kNB; ++q)
+      if (jb + q < n) S.dinv[jb + q] = pv[q];
+    if (jb + 0 < n) fl[jb + 0] = pv[4];
+    if (jb + 1 < n) fl[jb + 1] = pv[5];
+    if (jb + 2 < n) fl[jb + 2] = pv[6];
+    if (jb + 3 < n) fl[jb + 3] = pv[7];
+    if (jb + 0 < n) fl2[jb + 0] = pv[8];
+    if (jb + 1 < n) fl2[jb + 1] = pv[9];
+  };
   if (tid == 0) {
-    const int bs = min(2, n);
-    const bool ok = pivot_chol(K[0], bs == 2 ? K[1] : 0.0, bs == 2 ? K[colbase(1, n) + 1] : 0.0,
-                               bs, S.pv);
-    *S.flag = ok ? 0 : 1;
-    pi00[0] = S.pv[0];
-    if (bs == 2) {
-      pl10[0] = S.pv[1];
-      pi00[1] = S.pv[2];
-    }
+    const int bs = min(kNB, n);
+    double E[kNB][kNB];
+#pragma unroll
+    for (int a = 0; a < kNB; ++a)
+#pragma unroll
+      for (int b = 0; b < kNB; ++b) E[a][b] = (a < bs && b <= a) ? K[colbase(b, n) + a] : 0.0;
+    *S.flag = factor_pivot(E, bs, S.pv) ? 0 : 1;
+    save_factor(0, S.pv);
   }
   __syncthreads();
   int buf = 0;
-  for (int j = 0; j < n; j += 2) {
+  for (int j = 0; j < n; j += kNB) {
     if (*S.flag) return false;  // uniform: read after the barrier
-    const int bs = min(2, n - j);
+    const int bs = min(kNB, n - j);
     const int j2 = j + bs;
     if (j2 >= n) break;
-    const int bs2 = min(2, n - j2);
-    const double i00 = S.pv[buf * 4 + 0], l10 = S.pv[buf * 4 + 1], i11 = S.pv[buf * 4 + 2];
-    const int cj0 = colbase(j, n);
-    const int cj1 = bs == 2 ? colbase(j + 1, n) : cj0;
-    const double m1 = bs == 2 ? 1.0 : 0.0;  // second pivot column present
+    const long long tstep = S.prof ? clock64() : 0;
+    const int bs2 = min(kNB, n - j2);
+    const int pe = j2 + bs2;  // next pivot block: rows/cols [j2, pe)
+    const double* pv = S.pv + buf * 16;
+    int cjq[kNB];
+#pragma unroll
+    for (int q = 0; q < kNB; ++q) cjq[q] = j + q < j2 ? colbase(j + q, n) : colbase(j, n);
+    // zero weights for missing pivot columns make their W entries irrelevant
     if (wid == 0) {
-      // look-ahead: update and factor the next pivot block (lane 0)
-      if (lane == 0) {
-        const int d0 = colbase(j2, n) + j2, d1 = colbase(j2 + 1, n) + j2 + 1;
-        double a0, a1, b0 = 0.0, b1 = 0.0;
-        lrow(K[cj0 + j2], m1 * K[cj1 + j2], i00, l10, i11, a0, a1);
-        if (bs2 == 2) lrow(K[cj0 + j2 + 1], m1 * K[cj1 + j2 + 1], i00, l10, i11, b0, b1);
-        const double e00 = K[d0] - fma(a0, a0, a1 * a1);
-        double e10 = 0.0, e11 = 0.0;
-        if (bs2 == 2) {
-          e10 = K[d0 + 1] - fma(b0, a0, b1 * a1);
-          e11 = K[d1] - fma(b0, b0, b1 * b1);
-          K[d0 + 1] = e10;
-          K[d1] = e11;
+      if (lane == 0) {  // look-ahead
+        double La[kNB][kNB];
+#pragma unroll
+        for (int a = 0; a < kNB; ++a) {
+          const int r = min(j2 + a, n - 1);
+          double w[kNB];
+#pragma unroll
+          for (int q = 0; q < kNB; ++q) w[q] = K[cjq[q] + r];
+          lrow4(w, pv, La[a]);
         }
-        K[d0] = e00;
-        double* pn = S.pv + (buf ^ 1) * 4;
-        if (!pivot_chol(e00, e10, e11, bs2, pn)) *S.flag = 1;
-        pi00[j2] = pn[0];
-        if (bs2 == 2) {
-          pl10[j2] = pn[1];
-          pi00[j2 + 1] = pn[2];
-        }
+        double E[kNB][kNB];
+#pragma unroll
+        for (int a = 0; a < kNB; ++a)
+#pragma unroll
+          for (int b = 0; b < kNB; ++b) {
+            if (a < bs2 && b <= a) {
+              const int idx = colbase(j2 + b, n) + j2 + a;
+              const double e = K[idx] - fma(La[a][3], La[b][3], fma(La[a][2], La[b][2],
+                                        fma(La[a][1], La[b][1], La[a][0] * La[b][0])));
+              K[idx] = e;
+              E[a][b] = e;
+            } else {
+              E[a][b] = 0.0;
+            }
+          }
+        double* pn = S.pv + (buf ^ 1) * 16;
+        if (!factor_pivot(E, bs2, pn)) *S.flag = 1;
+        save_factor(j2, pn);
+        if (S.prof) atomicAdd(&g_qp_prof[12], (unsigned long long)(clock64() - tstep));
       }
     } else {
-      // rank-2 update of the trailing matrix, skipping the next pivot block:
-      // K[r][c] -= L0[r] L0[c] + L1[r] L1[c]
-      double l0[TM], l1[TM];
+      // this lane's rows of the current block's L columns (rows >= pe only)
+      double Lr[TM][kNB];
 #pragma unroll
       for (int t = 0; t < TM; ++t) {
-        const int r = lane + 32 * t;
-        double w0 = 0.0, w1 = 0.0;
-        if (r >= j2 && r < n) {
-          w0 = K[cj0 + r];
-          w1 = m1 * K[cj1 + r];
-        }
-        lrow(w0, w1, i00, l10, i11, l0[t], l1[t]);
-      }
-      const int pe = j2 + bs2;  // next pivot block rows/cols: [j2, pe)
-      constexpr int kU = kQpWarps - 1;
-      for (int c = j2 + (wid - 1); c < n; c += kU) {
-        double c0, c1;
-        lrow(K[cj0 + c], m1 * K[cj1 + c], i00, l10, i11, c0, c1);
-        double* col = K + colbase(c, n);
-        const int t0 = c >> 5;              // warp-uniform: row tiles above c are skipped
-        const int rskip = c < pe ? pe : c;  // rows of the next pivot block are lane 0's
+        const int r = min(lane + 32 * t, n - 1);
+        double w[kNB];
 #pragma unroll
-        for (int t = 0; t < TM; ++t) {
-          if (t >= t0) {
-            const int r = lane + 32 * t;
-            if (r >= rskip && r < n) col[r] = col[r] - fma(l0[t], c0, l1[t] * c1);
-          }
-        }
+        for (int q = 0; q < kNB; ++q) w[q] = K[cjq[q] + r];
+        lrow4(w, pv, Lr[t]);
       }
+      // column groups of 4 adjacent columns starting at j2, round-robin over warps
+      constexpr int kU = kQpWarps - 1;
+      for (int c0g = j2 + kNB * (wid - 1); c0g < n; c0g += kNB * kU)
+        update_group_dispatch<TM, 0>(c0g >> 5, K, n, c0g, pe, cjq, pv, Lr, lane);
     }
+    if (S.prof && lane == 0 && (wid == 1 || wid == kQpWarps - 1))
+      atomicAdd(&g_qp_prof[wid == 1 ? 13 : 14], (unsigned long long)(clock64() - tstep));
     buf ^= 1;
     __syncthreads();
+    if (S.prof && tid == 0) atomicAdd(&g_qp_prof[15], (unsigned long long)(clock64() - tstep));
   }
   if (*S.flag) return false;
-  // scale the panels into L (the pivot blocks' factors are in pi00 / pl10)
-  for (int j = 2 * wid; j < n; j += 2 * kQpWarps) {
-    const double a00 = pi00[j];
-    const bool two = j + 1 < n;
-    const double b10 = two ? pl10[j] : 0.0, a11 = two ? pi00[j + 1] : 0.0;
-    double* c0 = K + colbase(j, n);
-    double* c1 = two ? K + colbase(j + 1, n) : c0;
-    for (int r = j + 2 + lane; r < n; r += 32) {
-      double x0, x1;
-      lrow(c0[r], two ? c1[r] : 0.0, a00, b10, a11, x0, x1);
-      c0[r] = x0;
-      if (two) c1[r] = x1;
+  // scale the panels into L: rows below each block, x = w F^{-T}; the
+  // diagonal block gets F itself
+  for (int j = kNB * wid; j < n; j += kNB * kQpWarps) {
+    double pvj[10];
+#pragma unroll
+    for (int q = 0; q < kNB; ++q) pvj[q] = j + q < n ? S.dinv[j + q] : 0.0;
+    pvj[4] = fl[j];
+    pvj[5] = j + 1 < n ? fl[j + 1] : 0.0;
+    pvj[6] = j + 2 < n ? fl[j + 2] : 0.0;
+    pvj[7] = j + 3 < n ? fl[j + 3] : 0.0;
+    pvj[8] = fl2[j];
+    pvj[9] = j + 1 < n ? fl2[j + 1] : 0.0;
+    const int bs = min(kNB, n - j);
+    int cq[kNB];
+#pragma unroll
+    for (int q = 0; q < kNB; ++q) cq[q] = q < bs ? colbase(j + q, n) : colbase(j, n);
+    for (int r = j + bs + lane; r < n; r += 32) {
+      double w[kNB], x[kNB];
+#pragma unroll
+      for (int q = 0; q < kNB; ++q) w[q] = q < bs ? K[cq[q] + r] : 0.0;
+      lrow4(w, pvj, x);
+#pragma unroll
+      for (int q = 0; q < kNB; ++q)
+        if (q < bs) K[cq[q] + r] = x[q];
     }
     if (lane == 0) {
-      const double piv0 = c0[j];
-      c0[j] = piv0 * a00;  // l00 = sqrt(a)
-      S.dinv[j] = a00;
-      if (two) {
-        c0[j + 1] = b10;
-        c1[j + 1] = fma(-b10, b10, c1[j + 1]) * a11;  // l11 = sqrt(c - l10^2)
-        S.dinv[j + 1] = a11;
-      }
+      const double* lv = pvj + 4;  // l10 l20 l21 l30 l31 l32
+      const int li[4][4] = {{-1, -1, -1, -1}, {0, -1, -1, -1}, {1, 2, -1, -1}, {3, 4, 5, -1}};
+#pragma unroll
+      for (int a = 0; a < kNB; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b)
+          if (a < bs) K[cq[b] + j + a] = a == b ? 1.0 / pvj[a] : lv[li[a][b]];
     }
   }
   __syncthreads();
@@ -314,20 +408,23 @@ __device__ void invert_diag_blocks(Qs& S) {
 #pragma unroll 8
     for (int k = 0; k < kTB; ++k) Xi[k] = 0.0;
     if (i < nb) Xi[i] = S.dinv[r0 + i];
+    const int cb0 = colbase(r0, n);
     for (int r = 1; r < nb; ++r) {
-      // s = sum_{k<r} L[r0+r][r0+k] X[k][i]   (X[k][i] = 0 for k < i)
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      // s = sum_{k<r} L[r0+r][r0+k] X[k][i]; X[k][i] = 0 for k < i and for
+      // k >= r (not yet solved), so the 4-wide tail needs no guard (the
+      // packed entries it touches are finite)
       const int rr = r0 + r;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int base = cb0 + rr;  // colbase(r0 + k) + rr, advanced incrementally
       for (int k = 0; k < r; k += 4) {
-        const double x0 = Xi[k], x1 = Xi[k + 1], x2 = Xi[k + 2], x3 = Xi[k + 3];
-        const double q0 = S.K[colbase(r0 + k, n) + rr];
-        const double q1 = k + 1 < r ? S.K[colbase(r0 + k + 1, n) + rr] : 0.0;
-        const double q2 = k + 2 < r ? S.K[colbase(r0 + k + 2, n) + rr] : 0.0;
-        const double q3 = k + 3 < r ? S.K[colbase(r0 + k + 3, n) + rr] : 0.0;
-        s0 = fma(q0, x0, s0);
-        s1 = fma(q1, x1, s1);
-        s2 = fma(q2, x2, s2);
-        s3 = fma(q3, x3, s3);
+        const int b1 = base + (n - (r0 + k) - 1);
+        const int b2 = b1 + (n - (r0 + k) - 2);
+        const int b3 = b2 + (n - (r0 + k) - 3);
+        s0 = fma(S.K[base], Xi[k], s0);
+        s1 = fma(S.K[b1], Xi[k + 1], s1);
+        s2 = fma(S.K[b2], Xi[k + 2], s2);
+        s3 = fma(S.K[b3], Xi[k + 3], s3);
+        base = b3 + (n - (r0 + k) - 4);
       }
       if (i < r && i < nb) Xi[r] = -((s0 + s1) + (s2 + s3)) * S.dinv[rr];
     }
@@ -372,9 +469,12 @@ __device__ void chol_solve(Qs& S, const double* b, double* x) {
           const int r = lane + 32 * t;  // only full blocks have rows below
           if (r < n) {
             double c[4] = {0.0, 0.0, 0.0, 0.0};
+            int base = colbase(r0, n) + r;  // colbase(r0 + k) + r
 #pragma unroll
-            for (int k = 0; k < kTB; ++k)
-              c[k & 3] = fma(K[colbase(r0 + k, n) + r], ys[k], c[k & 3]);
+            for (int k = 0; k < kTB; ++k) {
+              c[k & 3] = fma(K[base], ys[k], c[k & 3]);
+              base += n - (r0 + k) - 1;
+            }
             y[t] -= (c[0] + c[1]) + (c[2] + c[3]);
           }
         }
@@ -632,7 +732,7 @@ template <int TM>
 __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[kQpWarps];
-  __shared__ double pvbuf[8];
+  __shared__ double pvbuf[32];
   __shared__ double ysbuf[kTB];
   __shared__ int sh_int[4];
   const int n = A.n, m = A.m;
@@ -954,7 +1054,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_chol_check(int n, const doubl
                                                                double* L, double* x, int* ok) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[kQpWarps];
-  __shared__ double pvbuf[8];
+  __shared__ double pvbuf[32];
   __shared__ double ysbuf[kTB];
   __shared__ int sh_int[4];
   Qs S;

@@ -7,7 +7,8 @@ import paper_2602_17601_b200 as pkg
 from paper_2602_17601_b200 import _runtime
 from tests.golden_io import load
 names = ["setup", "residuals", "tests+best", "w+build_k", "cholesky", "inv_diag", "rp/mu+aff_rhs",
-         "kkt(excl solve)", "steps/sigma", "update", "pre-solve", "chol_solve"]
+         "kkt(excl solve)", "steps/sigma", "update", "pre-solve", "chol_solve",
+         "[chol] lookahead", "[chol] warp1 upd", "[chol] warp15 upd", "[chol] step total"]
 for case in sys.argv[1:] or ["cfg1_chain10"]:
     if case == "cfg3":
         from paper_2602_17601_b200 import workloads
@@ -26,8 +27,8 @@ for case in sys.argv[1:] or ["cfg1_chain10"]:
     out = np.zeros(16, dtype=np.uint64)
     L.gm_qp_phase_cycles(out.ctypes.data)
     L.gm_qp_profile(0)
-    tot = out.sum()
+    tot = out[:12].sum()
     print(f"{case}: n={p.n} m={p.m} iters={s.iterations} total={tot} cycles ({tot/1.96e3:.0f} us @1.96GHz), per-iter {tot/max(1,s.iterations):.0f}")
     for i, nm in enumerate(names):
         if out[i]:
-            print(f"   {nm:18s} {int(out[i]):10d}  {100*out[i]/tot:5.1f}%  per-iter {out[i]/max(1,s.iterations):9.0f}")
+            print(f"   {nm:18s} {int(out[i]):10d}  {100*out[i]/tot:5.1f}%  per-iter {out[i]/max(1,s.iterations):9.0f}  per-step {out[i]/max(1,s.iterations)/(p.n/2):7.0f}")
