@@ -1,0 +1,80 @@
+"""GPU tests of the batched (cfg4) and node-partitioned (cfg5) step drivers.
+
+Only one GPU is available to the test runner, so the partitioned driver runs
+with a world-size-1 NCCL group here (the exchange/reduction logic itself is
+covered with 2-3 gloo ranks in tests/test_distributed_cpu.py)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from tests.golden_io import STATUS
+
+pytestmark = pytest.mark.gpu
+
+
+def test_batched_step_matches_oracle_per_instance():
+    import paper_2602_17601_b200 as pkg
+    from oracle import ref_port as O
+    from paper_2602_17601_b200 import workloads
+    from paper_2602_17601_b200.batch import BatchedMpc
+
+    M, N, B = 12, 8, 3
+    topo, model, _, _, spec = workloads.scaling_problem(M, N, 0.01, 0)
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+    xs, ls, li, xr = [], [], [], []
+    for b in range(B):
+        st, inp = workloads.batch_instance(b, M, N)
+        xs.append(st[0])
+        ls.append(np.concatenate([st, st[-1:]], axis=0))
+        li.append(inp)
+        xr.append(np.repeat(st[0][:, None, :], N + 1, axis=1))
+    bm = BatchedMpc(model, topo, spec, cfg, B)
+    res = bm.step(np.stack(xs), np.stack(ls), np.stack(li), np.stack(xr))
+    nxt = res.next_states.cpu().numpy()
+    for b in range(B):
+        spec_b = pkg.OcpSpec(topo, N, spec.q, xr[b], spec.r, spec.u_ref, spec.input_constraints,
+                             spec.state_constraints)
+        ref = O.mpc_step(model, topo, spec_b, xs[b], ls[b], li[b], N)
+        assert res.status[b].value == ref["status"]
+        scale = max(1.0, float(np.max(np.abs(ref["u_applied"]))))
+        assert float(np.max(np.abs(res.u_applied[b] - ref["u_applied"]))) / scale <= 1e-4
+        assert np.max(np.abs(nxt[b] - ref["lin_states"])) / np.max(np.abs(ref["lin_states"])) <= 1e-4
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_partitioned_step_world1_matches_single_device():
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_17601_b200 as pkg
+    from paper_2602_17601_b200 import workloads
+    from paper_2602_17601_b200.partition import PartitionedMpc, partition_nodes
+
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(_free_port())
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        topo, model, states, inputs, spec = workloads.mesh_problem(6, 5, 6, 0.01, 0)
+        N = 6
+        cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+        x = pkg.SystemState(states[0])
+        st = pkg.mpc_init(x, cfg, 6)
+        u_ref, st1 = pkg.mpc_step(model, topo, spec, x, st, cfg)
+        pm = PartitionedMpc(model, topo, spec, cfg, partition_nodes(topo, 1, 0))
+        u, status, iters = pm.step(states[0], st.lin_states, st.lin_inputs)
+        assert status == ["optimal", "max_iterations", "primal_infeasible",
+                          "numerical_failure"].index(st1.last_status.value)
+        assert np.max(np.abs(u - u_ref.u)) <= 1e-9 * max(1.0, np.max(np.abs(u_ref.u)))
+        assert np.max(np.abs(pm.next_states.cpu().numpy() - st1.lin_states)) <= 1e-9
+    finally:
+        dist.destroy_process_group()
