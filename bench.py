@@ -54,6 +54,11 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=8, help="oracle steps for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-l2-flush", action="store_true")
+    ap.add_argument("--workload", choices=["cfg3", "cfg4", "cfg5"], default="cfg3",
+                    help="cfg3 (default, headline latency); cfg4: 4096 instances of M=200 "
+                         "sharded over ranks; cfg5: 400x250 mesh, node-partitioned over ranks")
+    ap.add_argument("--batch", type=int, default=4096, help="cfg4 total instances")
+    ap.add_argument("--wave", type=int, default=1024, help="cfg4 instances per launch wave")
     return ap.parse_args()
 
 
@@ -323,13 +328,149 @@ def ours_arm(args, world, rank, local):
         torch.distributed.destroy_process_group()
 
 
+def cfg4_arm(args, world, rank, local):
+    """4096 independent M=200, N=20 instances, sharded over ranks (strong
+    scaling of a fixed batch; no data-path collective)."""
+    import torch
+
+    import paper_2602_17601_b200 as pkg
+    from paper_2602_17601_b200 import workloads
+    from paper_2602_17601_b200.batch import BatchedMpc, shard_range
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    M, N = 200, 20
+    topo, model, _, _, spec = workloads.scaling_problem(M, N, 0.01, 0)
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+    lo, hi = shard_range(args.batch, world, rank)
+    waves = [(a, min(a + args.wave, hi)) for a in range(lo, hi, args.wave)]
+    data = []
+    for a, b in waves:
+        xs, ls, li, xr = [], [], [], []
+        for i in range(a, b):
+            st, inp = workloads.batch_instance(i, M, N)
+            xs.append(st[0]); ls.append(np.concatenate([st, st[-1:]], 0)); li.append(inp)
+            xr.append(np.repeat(st[0][:, None, :], N + 1, axis=1))
+        data.append(tuple(np.stack(v) for v in (xs, ls, li, xr)))
+    bms = {}
+    def run_step():
+        stats = []
+        for (a, b), d in zip(waves, data):
+            bm = bms.get(b - a)
+            if bm is None:
+                bm = bms[b - a] = BatchedMpc(model, topo, spec, cfg, b - a)
+            stats.append(bm.step(*d))
+        return stats
+    for _ in range(args.warmup):
+        run_step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local); clocks.start(); time.sleep(0.3)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = run_step()
+    torch.cuda.synchronize()
+    el = (time.perf_counter() - t0) / args.steps
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([el], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        el = float(t.item())
+    if rank == 0:
+        iters = [int(i) for r in res for i in r.iterations]
+        print(json.dumps({
+            "metric": METRIC, "value": args.batch / el, "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32/f64", "data": "synthetic",
+            "config": {"workload": f"cfg4: {args.batch} independent chain M=200, N=20 instances",
+                       "instances_per_gpu": hi - lo, "wave": args.wave,
+                       "parallelism": f"instance shards x{world}",
+                       "qp_iterations_mean_rank0": float(np.mean(iters))},
+            "e2e": {"value": args.batch / el, "unit": "solves/s",
+                    "h2d_bytes_per_step": (hi - lo) * (M * 6 + (N + 1) * M * 6 + N * 6 + M * (N + 1) * 6) * 8,
+                    "d2h_bytes_per_step": (hi - lo) * 8 * 8,
+                    "path": "BatchedMpc.step (host numpy in, u/status out, wall clock)"},
+            "clocks": clk}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cfg5_arm(args, world, rank, local):
+    """400x250 mesh (1e5 nodes), N=20, node-partitioned over ranks with a
+    per-stage NCCL halo exchange and an all-reduce of H and g."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_17601_b200 as pkg
+    from paper_2602_17601_b200 import workloads
+    from paper_2602_17601_b200.partition import PartitionedMpc, partition_nodes
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    N = 20
+    topo, model, states, inputs, spec = workloads.mesh_problem(400, 250, N, 0.01, 0)
+    spec.freeze()
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+    pm = PartitionedMpc(model, topo, spec, cfg, partition_nodes(topo, world, rank))
+    ls = torch.from_numpy(np.concatenate([states, states[-1:]], 0)).to(dev)
+    li = torch.from_numpy(inputs).to(dev)
+    x0 = torch.from_numpy(states[0]).to(dev)
+    for _ in range(args.warmup):
+        pm.step(x0, ls, li)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local); clocks.start(); time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms = []
+    for _ in range(args.steps):
+        ev0.record()
+        u, st, it = pm.step(x0, ls, li)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms.append(ev0.elapsed_time(ev1))
+    clk = clocks.stop()
+    m = torch.tensor([float(np.mean(ms))], device=dev, dtype=torch.float64)
+    dist.all_reduce(m, op=dist.ReduceOp.MAX)
+    m = float(m.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": 1000.0 / m, "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": m,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32/f64", "data": "synthetic",
+            "config": {"workload": "cfg5: 2D mesh 400x250 = 100000 nodes, horizon 20",
+                       "parallelism": f"node partition x{world} (row slabs), NCCL halo per stage",
+                       "qp": {"status": st, "iterations": it}},
+            "e2e": {"value": 1000.0 / m, "unit": "solves/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 64,
+                    "path": "PartitionedMpc.step (device-resident trajectory)"},
+            "clocks": clk}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     world, rank, local = dist_setup()
     if args.impl == "reference":
         reference_arm(args, world, rank)
         return
-    ours_arm(args, world, rank, local)
+    if args.workload == "cfg4":
+        cfg4_arm(args, world, rank, local)
+    elif args.workload == "cfg5":
+        cfg5_arm(args, world, rank, local)
+    else:
+        ours_arm(args, world, rank, local)
 
 
 if __name__ == "__main__":
