@@ -343,6 +343,15 @@ def _upload_gammas(eng, gu, gx, N, nx, nu):
     return eng.h2d(Wh, np.float32), ld
 
 
+def lin_blocks(lin, eng):
+    """Device blocks of any LinearizedDynamics-like object (ours or the
+    reference's NumPy dataclass)."""
+    if hasattr(lin, "device_blocks"):
+        return lin.device_blocks(eng)
+    return tuple(eng.h2d(np.asarray(getattr(lin, k)), np.float64 if k == "c" else np.float32)
+                 for k in ("a_self", "a_nbr", "b", "c"))
+
+
 def gammas_device(eng, lin, x0, N, nx, nu):
     """Run K-REC; returns (W, ld) with W (M, N+1, nx, ld) fp32 on the device."""
     from ._runtime import lib
@@ -376,7 +385,7 @@ def condense_gammas(lin, x0, threads: int = 1):
     N, nx, nu = lin.horizon, lin.n_state, lin.n_u
     eng = _dev.engine(topo)
     eng.set_dims(nx, nu)
-    blocks = lin.device_blocks(eng)
+    blocks = lin_blocks(lin, eng)
     x0d = eng.h2d(np.asarray(x0, dtype=float).reshape(topo.node_count, nx), np.float64)
     W, ld = gammas_device(eng, blocks, x0d, N, nx, nu)
     gu, gx = _materialise(W, N, nu)
@@ -397,7 +406,7 @@ def condense_ocp(spec, lin, x0, threads: int = 1, gammas=None) -> CondensedQp:
         else:
             W, ld = hit
     else:
-        blocks = lin.device_blocks(eng)
+        blocks = lin_blocks(lin, eng)
         x0d = eng.h2d(np.asarray(x0, dtype=float).reshape(topo.node_count, nx), np.float64)
         W, ld = gammas_device(eng, blocks, x0d, N, nx, nu)
     n0 = N * nu

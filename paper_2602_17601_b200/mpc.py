@@ -28,7 +28,7 @@ import numpy as np
 
 from . import device as _dev
 from ._runtime import lib
-from .condensing import cost_device, rows_device
+from .condensing import cost_device, lin_blocks, rows_device
 from .gnn import LinearizedDynamics, linearize_device
 from .graph import InputVector, SystemState, Trajectory
 from .qpsolver import STATUS_BY_CODE, QpStatus, SolverSettings
@@ -116,6 +116,14 @@ def mpc_init(x_measured: SystemState, cfg: MpcConfig, n_u: int) -> MpcState:
     N = cfg.horizon
     return MpcState(lin_states=np.tile(x_measured.array, (N + 1, 1, 1)),
                     lin_inputs=np.zeros((N, n_u)))
+
+
+def _field(state, name):
+    """Raw value of an MpcState field for ours (device tensors kept) or the
+    reference's NumPy dataclass."""
+    if hasattr(state, "device_value"):
+        return state.device_value(name)
+    return getattr(state, name, None)
 
 
 def _is_gnn_model(model) -> bool:
@@ -322,7 +330,7 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
         raise TypeError("model must be a GnnModel or a linearizer callable")
     eng = _dev.engine(topo, model if gnn else None)
     torch = eng.torch
-    lin_in_prev = state.device_value("lin_inputs")
+    lin_in_prev = _field(state, "lin_inputs")
     n_u = int(lin_in_prev.shape[1])
     nx = int(np.asarray(x_measured.array).shape[1])
     eng.set_dims(nx, n_u)
@@ -331,10 +339,10 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
 
     # inputs: measurement, previous plan with x_measured at stage 0 (mpc.py:120-122)
     _copy_in(plan.x_meas, x_measured.array, plan.host_x)
-    _copy_in(plan.ls, state.device_value("lin_states"))
+    _copy_in(plan.ls, _field(state, "lin_states"))
     plan.ls[0].copy_(plan.x_meas)
     _copy_in(plan.li, lin_in_prev)
-    prev = state.device_value("last_applied")
+    prev = _field(state, "last_applied")
     if prev is None:
         plan.u_prev.zero_()
     else:
@@ -350,9 +358,7 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
     for it in range(cfg.sqp_iterations):
         if not gnn:  # plug-in Linearizer (mpc.py:23, :82-87): upload its blocks
             lin = model(plan.ls[:N].cpu().numpy(), plan.li.cpu().numpy())
-            blocks = lin.device_blocks(eng) if isinstance(lin, LinearizedDynamics) else tuple(
-                eng.h2d(getattr(lin, k), np.float64 if k == "c" else np.float32)
-                for k in ("a_self", "a_nbr", "b", "c"))
+            blocks = lin_blocks(lin, eng)
             for dst, src in zip((plan.a_self, plan.a_nbr, plan.b, plan.c), blocks):
                 if src.numel():
                     dst.view(-1)[: src.numel()].copy_(src.reshape(-1))
@@ -377,7 +383,7 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
             plan.li.copy_(plan.planned_inputs)
 
     u_app = summ[:n_u].copy()
-    filtered = state.device_value("filtered_input")
+    filtered = _field(state, "filtered_input")
     if cfg.input_filter_tau is not None:  # optional first-order smoothing (mpc.py:178-183)
         alpha = cfg.dt / (cfg.input_filter_tau + cfg.dt)
         prevf = (np.asarray(filtered.cpu().numpy() if hasattr(filtered, "cpu") else filtered,

@@ -218,3 +218,37 @@ def test_device_cholesky_and_solve(pkg, n):
     assert np.max(np.abs(Ln - np.linalg.cholesky(A))) <= 1e-10 * np.max(np.abs(A))
     xr = np.linalg.solve(A, b)
     assert np.max(np.abs(x.cpu().numpy() - xr)) <= 1e-9 * max(1.0, np.max(np.abs(xr)))
+
+
+def test_plugin_linearizer_and_reference_style_state(pkg):
+    """The reference's plug-in point (mpc.py:23, :82-87): mpc_step accepts any
+    callable returning LinearizedDynamics-like NumPy blocks and a NumPy
+    MpcState-like object; stages 2-4 still run on the GPU."""
+    from types import SimpleNamespace
+
+    from oracle import ref_port as O
+
+    cs = pipeline_case("p4_interior")
+    N, M = cs.spec.horizon, cs.topo.node_count
+    E = len(cs.topo.edges)
+    rng = np.random.default_rng(0)
+    A = np.eye(6) + 0.01 * rng.standard_normal((6, 6))
+    Bm = 0.01 * rng.standard_normal((6, 6))
+
+    def linearizer(states, inputs):
+        K = inputs.shape[0]
+        return SimpleNamespace(topology=cs.topo, horizon=K, a_self=np.tile(A, (K, M, 1, 1)),
+                               a_nbr=np.full((K, E, 6, 6), 1e-3), b=np.tile(Bm, (K, M, 1, 1)),
+                               c=np.zeros((K, M, 6)), n_state=6, n_u=6)
+
+    state = SimpleNamespace(lin_states=np.tile(cs.x0, (N + 1, 1, 1)), lin_inputs=np.zeros((N, 6)),
+                            step_count=0, last_applied=None, filtered_input=None)
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+    u, st1 = pkg.mpc_step(linearizer, cs.topo, cs.spec, pkg.SystemState(cs.x0), state, cfg)
+    lin = linearizer(state.lin_states[:N], state.lin_inputs)
+    gu, gx = O.condense_gammas(lin, cs.x0)
+    qp = O.condense_ocp(cs.spec, lin, cs.x0, gammas=(gu, gx))
+    H, g, C, d, n0 = O.expand_soft_constraints(qp)
+    sol = O.solve_qp(H, g, C, d, warm_start=np.zeros(H.shape[0]))
+    assert st1.last_status.value == sol.status
+    assert np.max(np.abs(u.u - sol.u[:6])) <= 1e-4 * max(1.0, np.max(np.abs(sol.u)))
