@@ -13,11 +13,12 @@
 //        no separate memset.
 // K-HG   condense_ocp cost part (condensing.py:376-389, :402-403): the
 //        tall-skinny contraction H = R + sum_{k,i} G_ki' Q_ki G_ki is a split-K
-//        reduction over nodes; each CTA keeps a 128x128 fp32 tile of H in
-//        registers (8x8 per thread), stages the node's rows of G and Q G in
-//        shared memory, and skips the non-causal part of every row.  Partials
-//        are reduced in a fixed order in fp64 (bitwise reproducible), R-bar is
-//        added and H is symmetrised as the reference does.
+//        reduction over nodes with one persistent CTA per SM; each CTA streams
+//        its nodes' Gamma / Q / x_ref rows through a bulk-copy (TMA) ring in
+//        shared memory and keeps a 128x128 fp32 tile of H in registers (8x8
+//        per thread, upper blocks only), skipping the non-causal part of every
+//        row.  Partials are reduced in a fixed order in fp64 (bitwise
+//        reproducible), R-bar is added and H is mirrored.
 // K-CON  constraint rows (condensing.py:263-282, :312-323) and
 //        expand_soft_constraints (condensing.py:419-439).
 #include <algorithm>
@@ -162,94 +163,207 @@ int check_dims(gm_ctx* ctx, int B, int N, int ld) {
 // ---------------------------------------------------------------------------
 // K-HG
 // ---------------------------------------------------------------------------
-constexpr int kTile = 128;  // output tile of H per CTA (8x8 per thread, 256 threads)
+constexpr int kTile = 128;   // output tile of H per CTA (8x8 per thread, 256 threads)
+constexpr int kRing = 3;     // bulk-copy ring depth (stage chunks in flight per CTA)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 
 struct CostArgs {
-  int M, N, nx, nu, ld, n0, lo, nodes, splits, tilesT, kc;
+  int M, N, nx, nu, ld, n0, lo, nodes, splits, tilesT, npairU, kc, bulk;
   const float* W;
   const double* q;
   int64_t q_stride;
   const double* xref;
   int64_t xref_stride;
-  float* partH;  // (B, tilesT*tilesT, splits, 128, 128)
+  float* partH;  // (B, npairU, splits, 128, 128); upper 8x8 blocks only on diagonal pairs
   double* partg; // (B, splits, n0)
 };
 
-__global__ void __launch_bounds__(256) k_cost_partial(const CostArgs a) {
-  extern __shared__ __align__(16) float sm[];
+// Split-K over nodes, one persistent CTA per (instance, upper tile pair, node
+// range).  The rows of Gamma / Q / x_ref a CTA needs are contiguous per
+// (node, stage chunk), so each chunk is ONE bulk copy per array into a
+// kRing-deep shared-memory ring (mbarrier complete_tx), issued kRing chunks
+// ahead of the consumer: the CTA streams its ~64 KB per node at copy-engine
+// rate instead of one dependent global load chain per element.
+//   per chunk:  QG = Qs G (column tile; Qs = (Q+Q')/2 so S = G' Qs G is already
+//               the symmetrised sum 0.5(S+S') of condensing.py:403),
+//               w  = 2 Q Gamma_x - 2 Q x_ref (fp64, condensing.py:153, :388)
+//               acc += G(:, row tile)' QG         (8x8 fp32 per thread)
+//               g   += G(:, row tile)' w          (fp64, diagonal pairs)
+// Rows of stage k only reach columns < k*nu: chunks whose live columns end
+// before the column tile are never copied, and per row a thread skips when its
+// column block is non-causal.  On diagonal tile pairs only the 136 upper 8x8
+// blocks are computed, packed onto the first 136 threads.
+__global__ void __launch_bounds__(256, 1) k_cost_partial(const CostArgs a) {
+  extern __shared__ __align__(128) unsigned char smraw[];
   const int nx = a.nx, nu = a.nu, ld = a.ld, N = a.N, KC = a.kc;
-  const int npair = a.tilesT * a.tilesT;
-  const int64_t bi = blockIdx.x / ((int64_t)a.splits * npair);
-  const int rem = (int)(blockIdx.x % ((int64_t)a.splits * npair));
-  const int split = rem / npair, pair = rem % npair;
-  const int ti = pair / a.tilesT, tj = pair % a.tilesT;
+  const int rows_max = KC * nx;
+  const int64_t slotW = (int64_t)rows_max * ld;            // floats
+  const int64_t slotQ = (int64_t)rows_max * nx;            // doubles
+  uint64_t* full = (uint64_t*)smraw;                       // kRing mbarriers
+  float* Wr = (float*)(smraw + 128);                       // kRing * slotW (+ kTile pad)
+  float* QG = Wr + kRing * slotW + kTile;                  // rows_max x 128
+  double* Qr = (double*)(QG + (int64_t)rows_max * kTile);  // kRing * slotQ
+  double* Xr = Qr + kRing * slotQ;                         // kRing * rows_max
+  double* wv = Xr + kRing * rows_max;                      // rows_max
+
+  const int64_t bi = blockIdx.x / ((int64_t)a.splits * a.npairU);
+  const int rem = (int)(blockIdx.x % ((int64_t)a.splits * a.npairU));
+  const int split = rem / a.npairU, pair = rem % a.npairU;
+  int ti = 0, tj = pair;
+  while (tj >= a.tilesT - ti) { tj -= a.tilesT - ti; ++ti; }
+  tj += ti;
   const int c1b = ti * kTile, c2b = tj * kTile;
+  const bool diag = ti == tj;
   const int per = (a.nodes + a.splits - 1) / a.splits;
   const int nb = a.lo + split * per, ne = min(a.lo + a.nodes, nb + per);
-  const int rows_max = KC * nx;
-  float* G1 = sm;                          // rows x 128 (row tile columns)
-  float* G2 = G1 + rows_max * kTile;       // rows x 128 (Q G, column tile)
-  double* wv = (double*)(G2 + rows_max * kTile);  // rows
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int cpn = (N + KC - 1) / KC;
+  int g0 = 0;  // first stage chunk whose live columns reach the column tile
+  while (g0 < cpn && min(N, (g0 + 1) * KC) * nu <= c2b) ++g0;
+  const int act = cpn - g0;
+  const int nchunks = ne > nb ? (ne - nb) * act : 0;
+
+  // thread -> 8x8 block of the tile
+  int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  bool active = true;
+  if (diag) {
+    int t = threadIdx.x;
+    active = t < 136;
+    ty = 0;
+    while (ty < 16 && t >= 16 - ty) { t -= 16 - ty; ++ty; }
+    tx = ty + t;
+    if (!active) { ty = 15; tx = 15; }
+  }
+  const bool do_g = diag;
+  const int64_t stage_stride = (int64_t)nx * ld;
+  const int XC = N * nu;
+
+  auto chunk_src = [&](int c, int& node, int& k0, int& k1) {
+    node = nb + c / act;
+    const int grp = g0 + c % act;
+    k0 = 1 + grp * KC;
+    k1 = min(N + 1, k0 + KC);
+  };
+  auto issue = [&](int c) {  // one thread
+    int node, k0, k1;
+    chunk_src(c, node, k0, k1);
+    const int slot = c % kRing;
+    const int nk = k1 - k0;
+    const int64_t gi = bi * a.M + node;
+    const uint32_t bw = (uint32_t)(nk * stage_stride * sizeof(float));
+    const uint32_t bq = (uint32_t)(nk * nx * nx * sizeof(double));
+    const uint32_t bx = (uint32_t)(nk * nx * sizeof(double));
+    mbar_expect_tx(&full[slot], bw + bq + bx);
+    bulk_g2s(Wr + slot * slotW, a.W + (gi * (N + 1) + k0) * stage_stride, bw, &full[slot]);
+    bulk_g2s(Qr + slot * slotQ, a.q + bi * a.q_stride + ((int64_t)node * (N + 1) + k0) * nx * nx, bq,
+             &full[slot]);
+    bulk_g2s(Xr + slot * rows_max, a.xref + bi * a.xref_stride + ((int64_t)node * (N + 1) + k0) * nx, bx,
+             &full[slot]);
+  };
+  auto load_sync = [&](int c) {  // all threads, when bulk copies are not usable
+    int node, k0, k1;
+    chunk_src(c, node, k0, k1);
+    const int slot = c % kRing;
+    const int nk = k1 - k0;
+    const int64_t gi = bi * a.M + node;
+    const float* sw = a.W + (gi * (N + 1) + k0) * stage_stride;
+    const double* sq = a.q + bi * a.q_stride + ((int64_t)node * (N + 1) + k0) * nx * nx;
+    const double* sx = a.xref + bi * a.xref_stride + ((int64_t)node * (N + 1) + k0) * nx;
+    for (int64_t t = threadIdx.x; t < nk * stage_stride; t += blockDim.x) Wr[slot * slotW + t] = sw[t];
+    for (int t = threadIdx.x; t < nk * nx * nx; t += blockDim.x) Qr[slot * slotQ + t] = sq[t];
+    for (int t = threadIdx.x; t < nk * nx; t += blockDim.x) Xr[slot * rows_max + t] = sx[t];
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRing; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int t = threadIdx.x; t < kTile; t += blockDim.x) Wr[kRing * slotW + t] = 0.f;
+  __syncthreads();
+  if (a.bulk && threadIdx.x == 0)
+    for (int c = 0; c < min(kRing, nchunks); ++c) issue(c);
+
   float acc[8][8];
 #pragma unroll
   for (int u = 0; u < 8; ++u)
 #pragma unroll
     for (int v = 0; v < 8; ++v) acc[u][v] = 0.f;
   double gacc = 0.0;
-  const bool do_g = (tj == 0);  // g rides on the first column-tile CTAs
-  const int gcol = c1b + (threadIdx.x & (kTile - 1));
-  const int64_t stage_stride = (int64_t)nx * ld;
-  const int XC = N * nu;
-  for (int i = nb; i < ne; ++i) {
-    const int64_t gi = bi * a.M + i;
-    const float* Wi = a.W + gi * (int64_t)(N + 1) * stage_stride;
-    const double* Qi = a.q + bi * a.q_stride + (int64_t)i * (N + 1) * nx * nx;
-    const double* Xi = a.xref + bi * a.xref_stride + (int64_t)i * (N + 1) * nx;
-    for (int k0 = 1; k0 <= N; k0 += KC) {
-      const int k1 = min(N + 1, k0 + KC);
-      const int live_max = (k1 - 1) * nu;
-      if (c1b >= live_max || c2b >= live_max) continue;  // tile entirely non-causal
-      const int rows = (k1 - k0) * nx;
-      __syncthreads();
-      // stage rows: G1 = Gamma rows on the row tile, G2 = Q Gamma on the column tile
-      for (int t = threadIdx.x; t < rows * kTile; t += blockDim.x) {
-        const int r = t / kTile, cc = t % kTile;
-        const int k = k0 + r / nx, ar = r % nx;
-        const float* Wk = Wi + (int64_t)k * stage_stride;
-        const int c1 = c1b + cc, c2 = c2b + cc;
-        const int live = k * nu;
-        G1[t] = (c1 < live) ? Wk[(int64_t)ar * ld + c1] : 0.f;
-        float s = 0.f;
-        if (c2 < live) {
-          const double* Qk = Qi + (int64_t)k * nx * nx + ar * nx;
-          for (int bb = 0; bb < nx; ++bb) s = fmaf((float)Qk[bb], Wk[(int64_t)bb * ld + c2], s);
+
+  for (int c = 0; c < nchunks; ++c) {
+    int node, k0, k1;
+    chunk_src(c, node, k0, k1);
+    const int slot = c % kRing;
+    const int rows = (k1 - k0) * nx;
+    if (a.bulk) mbar_wait(&full[slot], (uint32_t)((c / kRing) & 1));
+    else load_sync(c);
+    if (!a.bulk) __syncthreads();
+    const float* Ws = Wr + slot * slotW;
+    const double* Qs = Qr + slot * slotQ;
+    // QG on the column tile
+    for (int t = threadIdx.x; t < rows * kTile; t += blockDim.x) {
+      const int r = t >> 7, cc = t & (kTile - 1);
+      const int kk = r / nx, ar = r - kk * nx;
+      const double* Qk = Qs + (int64_t)kk * nx * nx;
+      const float* Wk = Ws + (int64_t)kk * stage_stride + c2b + cc;
+      float s = 0.f;
+      for (int b2 = 0; b2 < nx; ++b2)
+        s = fmaf((float)(0.5 * (Qk[ar * nx + b2] + Qk[b2 * nx + ar])), Wk[(int64_t)b2 * ld], s);
+      QG[t] = s;
+    }
+    if (do_g) {
+      for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+        const int kk = r / nx, ar = r - kk * nx;
+        const double* Qk = Qs + (int64_t)kk * nx * nx + ar * nx;
+        const float* Wk = Ws + (int64_t)kk * stage_stride + XC;
+        const double* xr = Xr + slot * rows_max + kk * nx;
+        double qg = 0.0, qx = 0.0;
+        for (int b2 = 0; b2 < nx; ++b2) {
+          qg += Qk[b2] * (double)Wk[(int64_t)b2 * ld];
+          qx += Qk[b2] * xr[b2];
         }
-        G2[t] = s;
+        wv[r] = 2.0 * qg + (-2.0 * qx);
       }
-      if (do_g) {
-        // w = 2 Q Gamma_x + q_lin, q_lin = -2 Q x_ref (condensing.py:153, :388), fp64
-        for (int r = threadIdx.x; r < rows; r += blockDim.x) {
-          const int k = k0 + r / nx, ar = r % nx;
-          const float* Wk = Wi + (int64_t)k * stage_stride;
-          const double* Qk = Qi + (int64_t)k * nx * nx + ar * nx;
-          const double* xr = Xi + (int64_t)k * nx;
-          double qg = 0.0, qx = 0.0;
-          for (int bb = 0; bb < nx; ++bb) {
-            qg += Qk[bb] * (double)Wk[(int64_t)bb * ld + XC];
-            qx += Qk[bb] * xr[bb];
-          }
-          wv[r] = 2.0 * qg + (-2.0 * qx);
-        }
-      }
-      __syncthreads();
+    }
+    __syncthreads();
+    if (active) {
+      const int cb2 = c2b + tx * 8;
       for (int r = 0; r < rows; ++r) {
         const int live = (k0 + r / nx) * nu;
-        if (c1b + ty * 8 >= live || c2b + tx * 8 >= live) continue;
-        const float4 g1a = *(const float4*)(G1 + r * kTile + ty * 8);
-        const float4 g1b = *(const float4*)(G1 + r * kTile + ty * 8 + 4);
-        const float4 g2a = *(const float4*)(G2 + r * kTile + tx * 8);
-        const float4 g2b = *(const float4*)(G2 + r * kTile + tx * 8 + 4);
+        if (cb2 >= live) continue;
+        const float* Gr = Ws + (int64_t)(r / nx) * stage_stride + (int64_t)(r % nx) * ld + c1b + ty * 8;
+        const float4 g1a = *(const float4*)(Gr);
+        const float4 g1b = *(const float4*)(Gr + 4);
+        const float4 g2a = *(const float4*)(QG + r * kTile + tx * 8);
+        const float4 g2b = *(const float4*)(QG + r * kTile + tx * 8 + 4);
         const float x[8] = {g1a.x, g1a.y, g1a.z, g1a.w, g1b.x, g1b.y, g1b.z, g1b.w};
         const float y[8] = {g2a.x, g2a.y, g2a.z, g2a.w, g2b.x, g2b.y, g2b.z, g2b.w};
 #pragma unroll
@@ -257,26 +371,38 @@ __global__ void __launch_bounds__(256) k_cost_partial(const CostArgs a) {
 #pragma unroll
           for (int v = 0; v < 8; ++v) acc[u][v] = fmaf(x[u], y[v], acc[u][v]);
       }
-      if (do_g && threadIdx.x < kTile) {
-        for (int r = 0; r < rows; ++r) gacc += (double)G1[r * kTile + threadIdx.x] * wv[r];
-      }
+    }
+    if (do_g && threadIdx.x < kTile) {
+      for (int r = 0; r < rows; ++r)
+        gacc += (double)Ws[(int64_t)(r / nx) * stage_stride + (int64_t)(r % nx) * ld + c1b + threadIdx.x] *
+                wv[r];
+    }
+    __syncthreads();  // slot and QG free
+    if (a.bulk && threadIdx.x == 0 && c + kRing < nchunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(c + kRing);
     }
   }
-  float* P = a.partH + ((bi * npair + pair) * (int64_t)a.splits + split) * kTile * kTile;
+  float* P = a.partH + ((bi * a.npairU + pair) * (int64_t)a.splits + split) * kTile * kTile;
+  if (active) {
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    float4* dst = (float4*)(P + (int64_t)(ty * 8 + u) * kTile + tx * 8);
-    dst[0] = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
-    dst[1] = make_float4(acc[u][4], acc[u][5], acc[u][6], acc[u][7]);
+    for (int u = 0; u < 8; ++u) {
+      float4* dst = (float4*)(P + (int64_t)(ty * 8 + u) * kTile + tx * 8);
+      dst[0] = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+      dst[1] = make_float4(acc[u][4], acc[u][5], acc[u][6], acc[u][7]);
+    }
   }
+  const int gcol = c1b + threadIdx.x;
   if (do_g && threadIdx.x < kTile && gcol < a.n0)
     a.partg[(bi * a.splits + split) * a.n0 + gcol] = gacc;
 }
 
 struct ReduceArgs {
-  int N, nu, n0, splits, tilesT, partial;
+  int N, nu, n0, splits, tilesT, groups, partial;
   const float* partH;
   const double* partg;
+  double* tmpH;  // (B, groups, n0, n0)
+  double* tmpg;  // (B, groups, n0)
   const double* r;
   int64_t r_stride;
   const double* uref;
@@ -285,43 +411,70 @@ struct ReduceArgs {
   double* g;
 };
 
-// H = 0.5 (S + S') + R-bar in fp64, splits summed in a fixed order.
-__global__ void k_cost_reduce(const ReduceArgs a) {
+__device__ __forceinline__ int upper_pair(int ti, int tj, int T) { return ti * T - ti * (ti - 1) / 2 + (tj - ti); }
+
+// pass 1: sum the splits of one group for every upper element (c1 <= c2), in
+// a fixed order (bitwise reproducible); coalesced over c2.
+__global__ void k_cost_reduce1(const ReduceArgs a) {
+  const int n0 = a.n0;
+  const int64_t bi = blockIdx.z;
+  const int grp = blockIdx.y;
+  const int per = (a.splits + a.groups - 1) / a.groups;
+  const int s0 = grp * per, s1 = min(a.splits, s0 + per);
+  const int npairU = a.tilesT * (a.tilesT + 1) / 2;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < n0 * n0) {
+    const int c1 = idx / n0, c2 = idx - c1 * n0;
+    if (c1 <= c2) {
+      const int pr = upper_pair(c1 / kTile, c2 / kTile, a.tilesT);
+      const float* P = a.partH + ((bi * npairU + pr) * (int64_t)a.splits) * kTile * kTile +
+                       (int64_t)(c1 % kTile) * kTile + (c2 % kTile);
+      double s = 0.0;
+#pragma unroll 4
+      for (int sp = s0; sp < s1; ++sp) s += (double)P[(int64_t)sp * kTile * kTile];
+      a.tmpH[(bi * a.groups + grp) * (int64_t)n0 * n0 + idx] = s;
+    }
+  }
+  if (idx < n0) {
+    double s = 0.0;
+    for (int sp = s0; sp < s1; ++sp) s += a.partg[(bi * a.splits + sp) * n0 + idx];
+    a.tmpg[(bi * a.groups + grp) * n0 + idx] = s;
+  }
+}
+
+// pass 2: H = S + R-bar (mirrored), g = sum + r_lin.
+__global__ void k_cost_reduce2(const ReduceArgs a) {
   const int n0 = a.n0, nu = a.nu;
   const int64_t bi = blockIdx.y;
-  const int npair = a.tilesT * a.tilesT;
-  auto S = [&](int c1, int c2) -> double {
-    const int ti = c1 / kTile, tj = c2 / kTile;
-    const float* P = a.partH + ((bi * npair + ti * a.tilesT + tj) * (int64_t)a.splits) * kTile * kTile +
-                     (int64_t)(c1 % kTile) * kTile + (c2 % kTile);
-    double s = 0.0;
-    for (int sp = 0; sp < a.splits; ++sp) s += (double)P[(int64_t)sp * kTile * kTile];
-    return s;
-  };
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n0 * n0; idx += gridDim.x * blockDim.x) {
-    const int c1 = idx / n0, c2 = idx % n0;
-    double h = 0.5 * (S(c1, c2) + S(c2, c1));
-    if (!a.partial && c1 / nu == c2 / nu) {
-      const int k = c1 / nu;
-      const double* Rk = a.r + bi * a.r_stride + (int64_t)k * nu * nu;
-      // R-bar is symmetrised with the rest (condensing.py:380-381, :403)
-      h += 0.5 * (Rk[(c1 % nu) * nu + (c2 % nu)] + Rk[(c2 % nu) * nu + (c1 % nu)]);
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < n0 * n0) {
+    const int c1 = idx / n0, c2 = idx - c1 * n0;
+    if (c1 <= c2) {
+      double h = 0.0;
+      for (int grp = 0; grp < a.groups; ++grp) h += a.tmpH[(bi * a.groups + grp) * (int64_t)n0 * n0 + idx];
+      if (!a.partial && c1 / nu == c2 / nu) {
+        const int k = c1 / nu;
+        const double* Rk = a.r + bi * a.r_stride + (int64_t)k * nu * nu;
+        // R-bar is symmetrised with the rest (condensing.py:380-381, :403)
+        h += 0.5 * (Rk[(c1 % nu) * nu + (c2 % nu)] + Rk[(c2 % nu) * nu + (c1 % nu)]);
+      }
+      a.H[bi * (int64_t)n0 * n0 + (int64_t)c1 * n0 + c2] = h;
+      a.H[bi * (int64_t)n0 * n0 + (int64_t)c2 * n0 + c1] = h;
     }
-    a.H[bi * (int64_t)n0 * n0 + idx] = h;
   }
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n0; c += gridDim.x * blockDim.x) {
+  if (idx < n0) {
     double s = 0.0;
-    for (int sp = 0; sp < a.splits; ++sp) s += a.partg[(bi * a.splits + sp) * n0 + c];
+    for (int grp = 0; grp < a.groups; ++grp) s += a.tmpg[(bi * a.groups + grp) * n0 + idx];
     if (!a.partial) {
       // r_lin = -2 R u_ref (condensing.py:154)
-      const int k = c / nu, row = c % nu;
+      const int k = idx / nu, row = idx % nu;
       const double* Rk = a.r + bi * a.r_stride + (int64_t)k * nu * nu + row * nu;
       const double* uk = a.uref + bi * a.uref_stride + (int64_t)k * nu;
       double ru = 0.0;
       for (int j = 0; j < nu; ++j) ru += Rk[j] * uk[j];
       s = -2.0 * ru + s;
     }
-    a.g[bi * n0 + c] = s;
+    a.g[bi * n0 + idx] = s;
   }
 }
 
@@ -452,20 +605,33 @@ int gm_condense_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, cons
   const int nx = ctx->nx, nu = ctx->n_u;
   const int n0 = N * nu;
   const int tilesT = (n0 + kTile - 1) / kTile;
-  const int npair = tilesT * tilesT;
+  const int npairU = tilesT * (tilesT + 1) / 2;
   const int nodes = (int)(gm_node_hi(ctx) - ctx->node_lo);
-  // split-K over nodes: about two CTAs per SM in total
-  int splits = std::max(1, std::min(nodes, (2 * ctx->sm_count + B * npair - 1) / (B * npair)));
-  // stage chunk so the staged rows fit the shared-memory budget
-  int kc = N;
+  // split-K over nodes: one persistent CTA per SM in total
+  const int splits = std::max(1, std::min(nodes, (ctx->sm_count + B * npairU - 1) / (B * npairU)));
+  // stage chunk: the largest balanced chunk whose ring fits shared memory
   auto smem_for = [&](int k) {
-    return sizeof(float) * 2 * (size_t)k * nx * kTile + sizeof(double) * (size_t)k * nx + 16;
+    const size_t rows = (size_t)k * nx;
+    return 128 + sizeof(float) * (kRing * rows * ld + kTile + rows * kTile) +
+           sizeof(double) * (kRing * rows * nx + kRing * rows + rows);
   };
-  while (kc > 1 && smem_for(kc) > 120 * 1024) kc = (kc + 1) / 2;
+  const size_t budget = std::min<size_t>(ctx->smem_optin, 200 * 1024);
+  int kmax = N;
+  while (kmax > 1 && smem_for(kmax) > budget) --kmax;
+  if (smem_for(kmax) > budget) return gm_fail(ctx, GM_ERR_CONFIG, "gamma rows too wide for K-HG tiles");
+  const int kc = gm_ceil_div(N, gm_ceil_div(N, kmax));
   const size_t sm = smem_for(kc);
-  const size_t partH_bytes = sizeof(float) * (size_t)B * npair * splits * kTile * kTile;
+  // bulk copies need 16-byte aligned sources and sizes
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  const int bulk = al(gamma) && al(q) && al(x_ref) && (ld % 4 == 0) && (nx % 2 == 0) &&
+                   (q_stride % 2 == 0) && (xref_stride % 2 == 0);
+  const int groups = std::min(splits, 16);
+  const size_t partH_bytes = sizeof(float) * (size_t)B * npairU * splits * kTile * kTile;
   const size_t partg_bytes = sizeof(double) * (size_t)B * splits * n0;
-  char* scr = (char*)gm_scratch(ctx, partH_bytes + partg_bytes + 256);
+  const size_t tmpH_bytes = sizeof(double) * (size_t)B * groups * n0 * n0;
+  const size_t tmpg_bytes = sizeof(double) * (size_t)B * groups * n0;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  char* scr = (char*)gm_scratch(ctx, up(partH_bytes) + up(partg_bytes) + up(tmpH_bytes) + tmpg_bytes + 256);
   if (!scr) return gm_fail(ctx, GM_ERR_CUDA, "scratch allocation failed");
   CostArgs a{};
   a.M = (int)ctx->M;
@@ -478,16 +644,18 @@ int gm_condense_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, cons
   a.nodes = nodes;
   a.splits = splits;
   a.tilesT = tilesT;
+  a.npairU = npairU;
   a.kc = kc;
+  a.bulk = bulk;
   a.W = gamma;
   a.q = q;
   a.q_stride = q_stride;
   a.xref = x_ref;
   a.xref_stride = xref_stride;
   a.partH = (float*)scr;
-  a.partg = (double*)(scr + ((partH_bytes + 255) & ~size_t(255)));
+  a.partg = (double*)(scr + up(partH_bytes));
   GM_CUDA(ctx, cudaFuncSetAttribute(k_cost_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  const int64_t blocks = (int64_t)B * splits * npair;
+  const int64_t blocks = (int64_t)B * splits * npairU;
   k_cost_partial<<<(unsigned)blocks, 256, sm, st>>>(a);
   GM_LAUNCH_CHECK(ctx, "k_cost_partial");
   ReduceArgs ra{};
@@ -496,18 +664,23 @@ int gm_condense_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, cons
   ra.n0 = n0;
   ra.splits = splits;
   ra.tilesT = tilesT;
+  ra.groups = groups;
   ra.partial = partial;
   ra.partH = a.partH;
   ra.partg = a.partg;
+  ra.tmpH = (double*)(scr + up(partH_bytes) + up(partg_bytes));
+  ra.tmpg = (double*)(scr + up(partH_bytes) + up(partg_bytes) + up(tmpH_bytes));
   ra.r = r;
   ra.r_stride = r_stride;
   ra.uref = u_ref;
   ra.uref_stride = uref_stride;
   ra.H = H;
   ra.g = g;
-  dim3 grid((unsigned)std::min(64, (n0 * n0 + 255) / 256), (unsigned)B);
-  k_cost_reduce<<<grid, 256, 0, st>>>(ra);
-  GM_LAUNCH_CHECK(ctx, "k_cost_reduce");
+  const unsigned eb = (unsigned)gm_ceil_div((int64_t)n0 * n0, 256);
+  k_cost_reduce1<<<dim3(eb, (unsigned)groups, (unsigned)B), 256, 0, st>>>(ra);
+  GM_LAUNCH_CHECK(ctx, "k_cost_reduce1");
+  k_cost_reduce2<<<dim3(eb, (unsigned)B), 256, 0, st>>>(ra);
+  GM_LAUNCH_CHECK(ctx, "k_cost_reduce2");
   return GM_OK;
 }
 

@@ -1,0 +1,32 @@
+"""Per-source-line samples / instructions / top stalls of an ncu report."""
+import collections, csv, subprocess, sys
+out = subprocess.run(['ncu', '-i', sys.argv[1], '--page', 'source', '--csv', '--print-source=cuda,sass'],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+hdr = next(r for r in rows if len(r) > 20 and r[0] == "Line No")
+stall_cols = [i for i, x in enumerate(hdr) if x.startswith("stall_") and "Not Issued" not in x]
+per = collections.defaultdict(lambda: [0, 0, "", collections.Counter()])
+cur = None
+for r in rows:
+    if len(r) < 8:
+        continue
+    if r[0] != "":
+        if r[0].isdigit():
+            cur = int(r[0]); per[cur][2] = r[1][:80]
+        continue
+    if cur is None:
+        continue
+    try:
+        per[cur][0] += int(r[4]); per[cur][1] += int(r[7])
+        for c in stall_cols:
+            if c < len(r) and r[c].isdigit():
+                per[cur][3][hdr[c]] += int(r[c])
+    except ValueError:
+        pass
+tot = sum(v[0] for v in per.values()) or 1
+toti = sum(v[1] for v in per.values()) or 1
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+print(f"samples {tot}  warp-instr {toti}")
+for ln, (s, e, src, st) in sorted(per.items(), key=lambda kv: -kv[1][1])[:n]:
+    top = ", ".join(f"{k.replace('stall_', '')}:{v}" for k, v in st.most_common(2))
+    print(f"{ln:4d} {100*s/tot:5.1f}%s {100*e/toti:5.1f}%i {src[:64]:64s} | {top}")
