@@ -146,6 +146,19 @@ int gm_condense_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, cons
                      int64_t r_stride, const double* u_ref, int64_t uref_stride, double* H,
                      double* g, int partial, void* stream);
 
+/* Fused condensing: gm_condense_gammas followed by gm_condense_cost (partial
+ * = 0) in one persistent kernel plus a two-pass fixed-order reduction
+ * (condense_gammas condensing.py:182-228 + the cost part of condense_ocp
+ * :376-389, :402-403).  Same arguments and outputs as the two calls; gamma is
+ * fully written.  Requires the whole node range (gm_set_node_range unset);
+ * shapes outside the fused kernel's instantiations run the two-kernel path.
+ * One launch per context at a time (per-context stage counters). */
+int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_nbr,
+                      const float* b, const double* c, const double* x0, float* gamma, int ld,
+                      const double* q, int64_t q_stride, const double* x_ref, int64_t xref_stride,
+                      const double* r, int64_t r_stride, const double* u_ref, int64_t uref_stride,
+                      double* H, double* g, void* stream);
+
 /* Constraint rows (condensing.py:263-282, :312-323), per instance:
  * rows [0, n_in) are input rows: row k has coefficients in_c (nu) at
  * column block in_stage[k]; rows [n_in, n_in+n_st) are state rows:

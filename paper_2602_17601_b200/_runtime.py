@@ -60,6 +60,8 @@ _SIGNATURES = {
                                          c_void_p]),
     "gm_condense_cost": (c_int, [c_void_p, c_int, c_int, P, c_int, P, c_i64, P, c_i64, P, c_i64, P,
                                  c_i64, P, P, c_int, c_void_p]),
+    "gm_condense_fused": (c_int, [c_void_p, c_int, c_int, P, P, P, P, P, P, c_int, P, c_i64, P,
+                                  c_i64, P, c_i64, P, c_i64, P, P, c_void_p]),
     "gm_constraint_rows": (c_int, [c_void_p, c_int, c_int, P, c_int, c_int, P, P, P, c_int, P, P,
                                    P, P, P, P, c_void_p]),
     "gm_expand_soft": (c_int, [c_void_p, c_int, c_int, c_int, P, P, P, P, c_int, P, P, P, P, P, P,

@@ -138,12 +138,12 @@ class BatchedMpc:
         ctx.call("gm_linearize", B * N, Xlin.data_ptr(), self.U.data_ptr(), self.a_self.data_ptr(),
                  self.a_nbr.data_ptr() if E else None, self.b.data_ptr(), self.c.data_ptr(), None,
                  sp)
-        ctx.call("gm_condense_gammas", B, N, self.a_self.data_ptr(),
+        # K-COND: Gamma recursion + H/g reduction in one persistent kernel
+        ctx.call("gm_condense_fused", B, N, self.a_self.data_ptr(),
                  self.a_nbr.data_ptr() if E else None, self.b.data_ptr(), self.c.data_ptr(),
-                 self.x0.data_ptr(), self.W.data_ptr(), self.ld, sp)
-        ctx.call("gm_condense_cost", B, N, self.W.data_ptr(), self.ld, self.q.data_ptr(), 0,
+                 self.x0.data_ptr(), self.W.data_ptr(), self.ld, self.q.data_ptr(), 0,
                  self.xref.data_ptr(), M * (N + 1) * nx, self.r.data_ptr(), 0,
-                 self.uref.data_ptr(), 0, self.H0.data_ptr(), self.g0.data_ptr(), 0, sp)
+                 self.uref.data_ptr(), 0, self.H0.data_ptr(), self.g0.data_ptr(), sp)
         rows = self.rows
         if rows.m0:
             p = [t.data_ptr() if t is not None else None for t in self.dev_rows]

@@ -297,6 +297,14 @@ def cost_device(eng, ds: DeviceSpec, W, ld, N, H0, g0, partial=0):
                  H0.data_ptr(), g0.data_ptr(), int(partial), eng.stream_ptr())
 
 
+def fused_device(eng, ds: DeviceSpec, a_self, a_nbr, b, c, x0, W, ld, N, H0, g0):
+    """K-COND: Gamma recursion into W and H0, g0 in one persistent kernel."""
+    eng.ctx.call("gm_condense_fused", 1, N, a_self.data_ptr(), _ptr(a_nbr), b.data_ptr(),
+                 c.data_ptr(), x0.data_ptr(), W.data_ptr(), ld, ds.q.data_ptr(), 0,
+                 ds.x_ref.data_ptr(), 0, ds.r.data_ptr(), 0, ds.u_ref.data_ptr(), 0,
+                 H0.data_ptr(), g0.data_ptr(), eng.stream_ptr())
+
+
 def rows_device(eng, ds: DeviceSpec, W, ld, N, C0, d0):
     """K-CON: constraint rows C0 (m0, n0), d0 (m0) fp64."""
     rows = ds.rows
@@ -395,6 +403,8 @@ def condense_gammas(lin, x0, threads: int = 1):
 
 def condense_ocp(spec, lin, x0, threads: int = 1, gammas=None) -> CondensedQp:
     """Condensed QP ``min u'Hu + g'u s.t. Cu <= d`` (``condensing.py:363-406``)."""
+    from ._runtime import lib
+
     topo = spec.topology
     N, nx, nu = spec.horizon, spec.n_state, spec.n_u
     eng = _dev.engine(topo)
@@ -405,16 +415,19 @@ def condense_ocp(spec, lin, x0, threads: int = 1, gammas=None) -> CondensedQp:
             W, ld = _upload_gammas(eng, np.asarray(gammas[0]), np.asarray(gammas[1]), N, nx, nu)
         else:
             W, ld = hit
-    else:
-        blocks = lin_blocks(lin, eng)
-        x0d = eng.h2d(np.asarray(x0, dtype=float).reshape(topo.node_count, nx), np.float64)
-        W, ld = gammas_device(eng, blocks, x0d, N, nx, nu)
     n0 = N * nu
     ds = device_spec(eng, spec, nx, nu)
     rows = ds.rows
     H0 = eng.empty((n0, n0), np.float64)
     g0 = eng.empty((n0,), np.float64)
-    cost_device(eng, ds, W, ld, N, H0, g0)
+    if gammas is None:  # K-COND: recursion and cost reduction fused
+        a_self, a_nbr, b, c = lin_blocks(lin, eng)
+        x0d = eng.h2d(np.asarray(x0, dtype=float).reshape(topo.node_count, nx), np.float64)
+        ld = lib().gm_gamma_ld(N, nu)
+        W = eng.empty((eng.M, N + 1, nx, ld), np.float32)
+        fused_device(eng, ds, a_self, a_nbr, b, c, x0d, W, ld, N, H0, g0)
+    else:
+        cost_device(eng, ds, W, ld, N, H0, g0)
     C0 = eng.empty((rows.m0, n0), np.float64)
     d0 = eng.empty((rows.m0,), np.float64)
     rows_device(eng, ds, W, ld, N, C0, d0)

@@ -80,6 +80,13 @@ struct gm_ctx {
   std::vector<void*> retired;  // outgrown scratch kept alive: captured CUDA graphs may use it
   int sm_count = 148;
   size_t smem_optin = 227 * 1024;
+  // fused condensing (k_condense_fused.cu): per-CTA stage flags (self-resetting,
+  // zero between launches) and the CTA dependency lists of the node partition
+  int* d_flags = nullptr;
+  int64_t flag_cap = 0;
+  int64_t dep_per = -1;
+  int* d_dep_ptr = nullptr;
+  int* d_dep = nullptr;
 };
 
 // error helpers -------------------------------------------------------------

@@ -96,6 +96,9 @@ void gm_destroy(gm_ctx* ctx) {
     cudaFree(ctx->d_dst);
     cudaFree(ctx->d_norm);
     cudaFree(ctx->scratch);
+    cudaFree(ctx->d_flags);
+    cudaFree(ctx->d_dep_ptr);
+    cudaFree(ctx->d_dep);
     for (void* p : ctx->retired) cudaFree(p);
     free_mlp(ctx->psi);
     free_mlp(ctx->phi);
@@ -165,6 +168,10 @@ int gm_set_graph(gm_ctx* ctx, int64_t node_count, int64_t neighbor_bound, const 
   cudaFree(ctx->d_src);
   cudaFree(ctx->d_dst);
   ctx->d_ptr = ctx->d_src = ctx->d_dst = nullptr;
+  if (ctx->d_dep_ptr) ctx->retired.push_back(ctx->d_dep_ptr);
+  if (ctx->d_dep) ctx->retired.push_back(ctx->d_dep);
+  ctx->d_dep_ptr = ctx->d_dep = nullptr;
+  ctx->dep_per = -1;
   GM_CUDA(ctx, cudaMalloc(&ctx->d_ptr, sizeof(int) * (node_count + 1)));
   GM_CUDA(ctx, cudaMalloc(&ctx->d_src, sizeof(int) * src32.size()));
   GM_CUDA(ctx, cudaMalloc(&ctx->d_dst, sizeof(int) * dst32.size()));

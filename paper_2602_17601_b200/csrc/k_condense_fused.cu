@@ -1,0 +1,545 @@
+// K-COND: fused Gamma recursion + cost reduction (stages 2 and 3a in one
+// persistent kernel).
+//
+// Reference: condense_gammas (condensing.py:182-228) followed by the cost part
+// of condense_ocp (condensing.py:376-389, :402-403).
+//
+// The two-kernel path (k_condense.cu) launches K-REC once per stage (N + 1
+// launches, each a few microseconds of work behind a full-device dependency)
+// and then re-reads all of Gamma (64 MB at M=1000, N=20) for K-HG.  Here:
+//
+//   * CTA s owns the node range [s*per, (s+1)*per) of one instance for the
+//     whole horizon.  Stage n+1 of a node needs stage n of its neighbours, so
+//     instead of a grid-wide barrier per stage a CTA waits only on the CTAs
+//     that own its nodes' neighbours (dependency lists built on the host from
+//     the CSR), through per-CTA stage counters in global memory
+//     (st.release / ld.acquire at gpu scope).  On a chain or mesh a CTA has
+//     two neighbours, so stages pipeline across the device like a wavefront.
+//     All CTAs are co-resident (grid <= SMs x occupancy; the host checks), so
+//     the waits cannot deadlock.  The last CTA to finish resets the counters.
+//   * the stage-(n+1) rows a CTA computes stay in shared memory and are
+//     folded into H right away: thread t owns the nu x nu block pair (p, q),
+//     p <= q, of H, ordered by q, so at stage k exactly the first k(k+1)/2
+//     threads are live (Gamma rows of stage k only reach input blocks < k):
+//       acc(p,q) += G(:, p-block)' Qs G(:, q-block),   Qs = (Q + Q')/2
+//     which is the symmetrised sum 0.5 (S + S') of condensing.py:403.
+//     g += G' (2 Q Gamma_x - 2 Q x_ref) in fp64 per column (condensing.py:388).
+//   * per-CTA fp32 partials are reduced in a fixed order in fp64 (bitwise
+//     reproducible) by two small kernels that add R-bar and mirror H.
+//
+// Numerics equal the two-kernel path: the same fp32 Gamma recursion (c rounded
+// once to fp32, as K-REC), fp32 partial sums, fp64 reduction.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kFusedSmemBudget = 160 * 1024;
+
+struct FusedArgs {
+  int M, E, N, ld, per, splits, sc, npairs, dslot;
+  const int* ptr;
+  const int* src;
+  const int* dep_ptr;
+  const int* dep;
+  const float* a_self;
+  const float* a_nbr;
+  const float* b;
+  const double* c;
+  const double* x0;
+  float* W;
+  const double* q;
+  int64_t q_stride;
+  const double* xref;
+  int64_t xref_stride;
+  float* partH;   // (B, splits, npairs * nu * nu)
+  double* partg;  // (B, splits, n0)
+  int* flags;     // (B * splits) stage counters, then one completion counter
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int NX, int NU>
+__global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int N = a.N, ld = a.ld, SC = a.sc, M = a.M;
+  const int n0 = N * NU, XC = N * NU;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t bi = blockIdx.x / a.splits;
+  const int split = (int)(blockIdx.x % a.splits);
+  const int nb = split * a.per, ne = min(M, nb + a.per);
+  int* flags = a.flags + bi * a.splits;
+  const int64_t stage_stride = (int64_t)NX * ld;
+  const int64_t node_stride = (int64_t)(N + 1) * stage_stride;
+  float* Wb = a.W + bi * (int64_t)M * node_stride;
+
+  // shared memory carve-up
+  float* Gc = (float*)smraw;                          // SC x NX x ld  current-stage rows
+  float* QGc = Gc + (int64_t)SC * NX * ld;            // SC x NX x ld  Qs G (live columns)
+  float* Ab = QGc + (int64_t)SC * NX * ld;            // SC x dslot x NX*NX  closed-nbhd blocks
+  float* Bb = Ab + (int64_t)SC * a.dslot * NX * NX;   // SC x NX*NU
+  float* Qs = Bb + SC * NX * NU;                      // SC x NX*NX  (Q + Q')/2
+  float* cs = Qs + SC * NX * NX;                      // SC x NX
+  double* wv = (double*)(((uintptr_t)(cs + SC * NX) + 15) & ~(uintptr_t)15);  // SC x NX
+  double* gs = wv + SC * NX;                          // n0  (g accumulator)
+
+  // block pair owned by this thread (ordered by q, then p)
+  int bq = (int)((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f);
+  while ((bq + 1) * (bq + 2) / 2 <= tid) ++bq;
+  while (bq * (bq + 1) / 2 > tid) --bq;
+  const int bp = tid - bq * (bq + 1) / 2;
+  const bool owner = tid < a.npairs;
+  float acc[NU][NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u)
+#pragma unroll
+    for (int v = 0; v < NU; ++v) acc[u][v] = 0.f;
+  for (int t = tid; t < n0; t += nt) gs[t] = 0.0;
+
+  // stage 0: Gamma_u = 0, Gamma_x = x0 (condensing.py:205-206)
+  for (int i = nb; i < ne; ++i) {
+    float* Wo = Wb + (int64_t)i * node_stride;
+    for (int t = tid; t < NX * ld; t += nt) {
+      const int r = t / ld, col = t - r * ld;
+      Wo[t] = (col == XC) ? (float)a.x0[(bi * M + i) * NX + r] : 0.f;
+    }
+  }
+  const int d0 = a.dep_ptr[split], d1 = a.dep_ptr[split + 1];
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(&flags[split], 1);
+  }
+
+  for (int n = 0; n < N; ++n) {
+    const int k = n + 1;            // stage being produced
+    const int live = n * NU;        // live Gamma_u columns of stage n
+    // wait until every CTA owning a neighbour has published stage n
+    for (int d = d0 + tid; d < d1; d += nt) {
+      const int* f = &flags[a.dep[d]];
+      while (ld_acquire(f) < k) __nanosleep(32);
+    }
+    __syncthreads();
+    const int64_t pstage = bi * N + n;
+    for (int s0 = nb; s0 < ne; s0 += SC) {
+      const int sc = min(SC, ne - s0);
+      // stage the chunk's blocks (a_self / a_nbr / b / c of stage n, Q of stage k)
+      for (int li = 0; li < sc; ++li) {
+        const int i = s0 + li;
+        const int e0 = a.ptr[i], deg = a.ptr[i + 1] - e0;
+        float* A = Ab + (int64_t)li * a.dslot * NX * NX;
+        for (int t = tid; t < (1 + deg) * NX * NX; t += nt) {
+          const int s = t / (NX * NX), qq = t - s * NX * NX;
+          A[t] = s == 0 ? a.a_self[(pstage * M + i) * NX * NX + qq]
+                        : a.a_nbr[(pstage * a.E + e0 + s - 1) * NX * NX + qq];
+        }
+      }
+      for (int t = tid; t < sc * NX * NU; t += nt)
+        Bb[t] = a.b[(pstage * M + s0) * NX * NU + t];
+      for (int t = tid; t < sc * NX; t += nt) cs[t] = (float)a.c[(pstage * M + s0) * NX + t];
+      for (int t = tid; t < sc * NX * NX; t += nt) {
+        const int li = t / (NX * NX), e = t - li * NX * NX, r = e / NX, cc = e - r * NX;
+        const double* Qk = a.q + bi * a.q_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX * NX;
+        Qs[t] = (float)(0.5 * (Qk[r * NX + cc] + Qk[cc * NX + r]));
+      }
+      __syncthreads();
+      // Gamma rows of stage k (condensing.py:213-224), same per-column
+      // recursion as K-REC: live columns and Gamma_x via the closed
+      // neighbourhood, block n <- B_n, zero elsewhere
+      for (int t = tid; t < sc * ld; t += nt) {
+        const int li = t / ld, col = t - li * ld;
+        const int i = s0 + li;
+        float r6[NX];
+#pragma unroll
+        for (int r = 0; r < NX; ++r) r6[r] = 0.f;
+        if (col < live || col == XC) {
+          const int e0 = a.ptr[i], deg = a.ptr[i + 1] - e0;
+          const float* A = Ab + (int64_t)li * a.dslot * NX * NX;
+          for (int s = 0; s <= deg; ++s) {
+            const int j = s == 0 ? i : a.src[e0 + s - 1];
+            const float* Wj = Wb + (int64_t)j * node_stride + (int64_t)n * stage_stride + col;
+            float w[NX];
+#pragma unroll
+            for (int qq = 0; qq < NX; ++qq) w[qq] = __ldcg(Wj + (int64_t)qq * ld);
+            const float* As = A + s * NX * NX;
+#pragma unroll
+            for (int r = 0; r < NX; ++r)
+#pragma unroll
+              for (int qq = 0; qq < NX; ++qq) r6[r] = fmaf(As[r * NX + qq], w[qq], r6[r]);
+          }
+          if (col == XC) {
+#pragma unroll
+            for (int r = 0; r < NX; ++r) r6[r] += cs[li * NX + r];
+          }
+        } else if (col >= live && col < live + NU) {
+#pragma unroll
+          for (int r = 0; r < NX; ++r) r6[r] = Bb[(li * NX + r) * NU + (col - live)];
+        }
+        float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + col;
+        float* Gs = Gc + (int64_t)li * NX * ld + col;
+#pragma unroll
+        for (int r = 0; r < NX; ++r) {
+          Wo[(int64_t)r * ld] = r6[r];
+          Gs[(int64_t)r * ld] = r6[r];
+        }
+      }
+      __syncthreads();
+      if (s0 + SC >= ne && tid == 0) {  // all of this CTA's stage-k rows are out
+        __threadfence();
+        st_release(&flags[split], k + 1);
+      }
+      // Qs G on the live columns of stage k, and w = 2 Q Gamma_x - 2 Q x_ref
+      const int lk = k * NU;
+      for (int t = tid; t < sc * lk; t += nt) {
+        const int li = t / lk, col = t - li * lk;
+        const float* Gs = Gc + (int64_t)li * NX * ld + col;
+        float gcol[NX];
+#pragma unroll
+        for (int qq = 0; qq < NX; ++qq) gcol[qq] = Gs[(int64_t)qq * ld];
+        const float* Qn = Qs + li * NX * NX;
+        float* Os = QGc + (int64_t)li * NX * ld + col;
+#pragma unroll
+        for (int r = 0; r < NX; ++r) {
+          float s = 0.f;
+#pragma unroll
+          for (int qq = 0; qq < NX; ++qq) s = fmaf(Qn[r * NX + qq], gcol[qq], s);
+          Os[(int64_t)r * ld] = s;
+        }
+      }
+      for (int t = tid; t < sc * NX; t += nt) {
+        const int li = t / NX, r = t - li * NX;
+        const int i = s0 + li;
+        const double* Qk = a.q + bi * a.q_stride + ((int64_t)i * (N + 1) + k) * NX * NX + r * NX;
+        const double* xr = a.xref + bi * a.xref_stride + ((int64_t)i * (N + 1) + k) * NX;
+        const float* gx = Gc + (int64_t)li * NX * ld + XC;
+        double qg = 0.0, qx = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < NX; ++qq) {
+          qg += Qk[qq] * (double)gx[(int64_t)qq * ld];
+          qx += Qk[qq] * xr[qq];
+        }
+        wv[t] = 2.0 * qg + (-2.0 * qx);
+      }
+      __syncthreads();
+      // H block pairs live at stage k: q < k  <=>  tid < k(k+1)/2
+      if (owner && bq < k) {
+        for (int li = 0; li < sc; ++li) {
+#pragma unroll
+          for (int r = 0; r < NX; ++r) {
+            const float* gp = Gc + ((int64_t)li * NX + r) * ld + bp * NU;
+            const float* gq = QGc + ((int64_t)li * NX + r) * ld + bq * NU;
+            float x[NU], y[NU];
+#pragma unroll
+            for (int u = 0; u < NU; ++u) {
+              x[u] = gp[u];
+              y[u] = gq[u];
+            }
+#pragma unroll
+            for (int u = 0; u < NU; ++u)
+#pragma unroll
+              for (int v = 0; v < NU; ++v) acc[u][v] = fmaf(x[u], y[v], acc[u][v]);
+          }
+        }
+      }
+      for (int cidx = tid; cidx < lk; cidx += nt) {
+        double s = gs[cidx];
+        for (int li = 0; li < sc; ++li)
+#pragma unroll
+          for (int r = 0; r < NX; ++r)
+            s += (double)Gc[((int64_t)li * NX + r) * ld + cidx] * wv[li * NX + r];
+        gs[cidx] = s;
+      }
+      __syncthreads();
+    }
+  }
+
+  // partials
+  const int PU = a.npairs * NU * NU;
+  float* P = a.partH + (bi * a.splits + split) * (int64_t)PU;
+  if (owner) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u)
+#pragma unroll
+      for (int v = 0; v < NU; ++v) P[tid * NU * NU + u * NU + v] = acc[u][v];
+  }
+  for (int t = tid; t < n0; t += nt) a.partg[(bi * a.splits + split) * n0 + t] = gs[t];
+  // the last CTA out resets the stage counters for the next launch
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    int* done = a.flags + (int64_t)gridDim.x;
+    if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
+      for (int s = 0; s < (int)gridDim.x; ++s) a.flags[s] = 0;
+      *done = 0;
+      __threadfence();
+    }
+  }
+}
+
+struct PairReduceArgs {
+  int nu, n0, npairs, splits, groups;
+  const float* partH;
+  const double* partg;
+  double* tmpH;  // (B, groups, npairs*nu*nu)
+  double* tmpg;  // (B, groups, n0)
+  const double* r;
+  int64_t r_stride;
+  const double* uref;
+  int64_t uref_stride;
+  double* H;
+  double* g;
+};
+
+// pass 1: fixed-order sum of one group of CTA partials, coalesced
+__global__ void k_pair_reduce1(const PairReduceArgs a) {
+  const int PU = a.npairs * a.nu * a.nu;
+  const int64_t bi = blockIdx.z;
+  const int grp = blockIdx.y;
+  const int per = (a.splits + a.groups - 1) / a.groups;
+  const int s0 = grp * per, s1 = min(a.splits, s0 + per);
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < PU) {
+    const float* P = a.partH + bi * a.splits * (int64_t)PU + u;
+    double s = 0.0;
+#pragma unroll 4
+    for (int sp = s0; sp < s1; ++sp) s += (double)P[(int64_t)sp * PU];
+    a.tmpH[(bi * a.groups + grp) * (int64_t)PU + u] = s;
+  }
+  if (u < a.n0) {
+    double s = 0.0;
+    for (int sp = s0; sp < s1; ++sp) s += a.partg[(bi * a.splits + sp) * a.n0 + u];
+    a.tmpg[(bi * a.groups + grp) * a.n0 + u] = s;
+  }
+}
+
+// pass 2: H = S + R-bar, mirrored (diagonal blocks averaged so H is exactly
+// symmetric), g = sum + r_lin (condensing.py:154, :380-381, :388, :403)
+__global__ void k_pair_reduce2(const PairReduceArgs a) {
+  const int nu = a.nu, nn = nu * nu, n0 = a.n0;
+  const int PU = a.npairs * nn;
+  const int64_t bi = blockIdx.y;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const double* T = a.tmpH + bi * a.groups * (int64_t)PU;
+  auto S = [&](int idx) {
+    double s = 0.0;
+    for (int grp = 0; grp < a.groups; ++grp) s += T[(int64_t)grp * PU + idx];
+    return s;
+  };
+  if (u < PU) {
+    const int t = u / nn, e = u - t * nn, ea = e / nu, eb = e - ea * nu;
+    int q = (int)((sqrtf(8.f * t + 1.f) - 1.f) * 0.5f);
+    while ((q + 1) * (q + 2) / 2 <= t) ++q;
+    while (q * (q + 1) / 2 > t) --q;
+    const int p = t - q * (q + 1) / 2;
+    const int c1 = p * nu + ea, c2 = q * nu + eb;
+    double* Hb = a.H + bi * (int64_t)n0 * n0;
+    if (p < q) {
+      const double h = S(u);
+      Hb[(int64_t)c1 * n0 + c2] = h;
+      Hb[(int64_t)c2 * n0 + c1] = h;
+    } else if (ea <= eb) {
+      double h = 0.5 * (S(u) + S(t * nn + eb * nu + ea));
+      if (a.r) {
+        const double* Rk = a.r + bi * a.r_stride + (int64_t)p * nn;
+        h += 0.5 * (Rk[ea * nu + eb] + Rk[eb * nu + ea]);
+      }
+      Hb[(int64_t)c1 * n0 + c2] = h;
+      Hb[(int64_t)c2 * n0 + c1] = h;
+    }
+  }
+  if (u < n0) {
+    double s = 0.0;
+    for (int grp = 0; grp < a.groups; ++grp) s += a.tmpg[(bi * a.groups + grp) * n0 + u];
+    if (a.r) {
+      const int k = u / nu, row = u % nu;
+      const double* Rk = a.r + bi * a.r_stride + (int64_t)k * nn + row * nu;
+      const double* uk = a.uref + bi * a.uref_stride + (int64_t)k * nu;
+      double ru = 0.0;
+      for (int j = 0; j < nu; ++j) ru += Rk[j] * uk[j];
+      s = -2.0 * ru + s;
+    }
+    a.g[bi * n0 + u] = s;
+  }
+}
+
+using FusedKernel = void (*)(const FusedArgs);
+
+FusedKernel pick_kernel(int nx, int nu) {
+  if (nx == 6 && nu == 6) return k_condense_fused<6, 6>;
+  if (nx == 6 && nu == 3) return k_condense_fused<6, 3>;
+  if (nx == 6 && nu == 2) return k_condense_fused<6, 2>;
+  if (nx == 6 && nu == 1) return k_condense_fused<6, 1>;
+  if (nx == 4 && nu == 2) return k_condense_fused<4, 2>;
+  if (nx == 2 && nu == 1) return k_condense_fused<2, 1>;
+  return nullptr;
+}
+
+size_t fused_smem(int SC, int nx, int nu, int ld, int dslot, int n0) {
+  size_t f = (size_t)SC * nx * ld * 2 + (size_t)SC * dslot * nx * nx + (size_t)SC * nx * nu +
+             (size_t)SC * nx * nx + (size_t)SC * nx;
+  return ((f * sizeof(float) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)SC * nx + n0) + 16;
+}
+
+// CTA dependency lists for node partition `per`: CTA s waits on the owners of
+// every in-neighbour of its nodes (graph.py CSR), itself excluded.
+int ensure_deps(gm_ctx* ctx, int64_t per, int splits) {
+  if (ctx->dep_per == per && ctx->d_dep_ptr) return GM_OK;
+  std::vector<int> dptr(splits + 1, 0), dl;
+  for (int s = 0; s < splits; ++s) {
+    std::vector<int> mine;
+    const int64_t lo = s * per, hi = std::min<int64_t>(ctx->M, lo + per);
+    for (int64_t i = lo; i < hi; ++i)
+      for (int64_t e = ctx->h_ptr[i]; e < ctx->h_ptr[i + 1]; ++e) {
+        const int o = (int)(ctx->h_src[e] / per);
+        if (o != s) mine.push_back(o);
+      }
+    std::sort(mine.begin(), mine.end());
+    mine.erase(std::unique(mine.begin(), mine.end()), mine.end());
+    dl.insert(dl.end(), mine.begin(), mine.end());
+    dptr[s + 1] = (int)dl.size();
+  }
+  if (dl.empty()) dl.push_back(0);
+  if (ctx->d_dep_ptr) ctx->retired.push_back(ctx->d_dep_ptr);  // captured graphs may hold them
+  if (ctx->d_dep) ctx->retired.push_back(ctx->d_dep);
+  ctx->d_dep_ptr = ctx->d_dep = nullptr;
+  GM_CUDA(ctx, cudaMalloc(&ctx->d_dep_ptr, sizeof(int) * dptr.size()));
+  GM_CUDA(ctx, cudaMalloc(&ctx->d_dep, sizeof(int) * dl.size()));
+  GM_CUDA(ctx, cudaMemcpy(ctx->d_dep_ptr, dptr.data(), sizeof(int) * dptr.size(), cudaMemcpyHostToDevice));
+  GM_CUDA(ctx, cudaMemcpy(ctx->d_dep, dl.data(), sizeof(int) * dl.size(), cudaMemcpyHostToDevice));
+  ctx->dep_per = per;
+  return GM_OK;
+}
+
+int ensure_flags(gm_ctx* ctx, int64_t n) {
+  if (n <= ctx->flag_cap) return GM_OK;
+  if (ctx->d_flags) ctx->retired.push_back(ctx->d_flags);
+  ctx->d_flags = nullptr;
+  const int64_t cap = std::max<int64_t>(n, 1024);
+  GM_CUDA(ctx, cudaMalloc(&ctx->d_flags, sizeof(int) * cap));
+  GM_CUDA(ctx, cudaMemset(ctx->d_flags, 0, sizeof(int) * cap));
+  ctx->flag_cap = cap;
+  return GM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_nbr,
+                      const float* b, const double* c, const double* x0, float* gamma, int ld,
+                      const double* q, int64_t q_stride, const double* x_ref, int64_t xref_stride,
+                      const double* r, int64_t r_stride, const double* u_ref, int64_t uref_stride,
+                      double* H, double* g, void* stream) {
+  int rc = gm_need_device(ctx);
+  if (rc) return rc;
+  if (ctx->M < 1) return gm_fail(ctx, GM_ERR_CONFIG, "graph not set");
+  if (ctx->nx < 1 || ctx->n_u < 1) return gm_fail(ctx, GM_ERR_CONFIG, "dimensions not set");
+  if (B < 0 || N < 1) return gm_fail(ctx, GM_ERR_CONFIG, "need B >= 0 and horizon >= 1");
+  if (ld < N * ctx->n_u + 1) return gm_fail(ctx, GM_ERR_CONFIG, "gamma leading dimension too small");
+  if (B == 0) return GM_OK;
+  const int nx = ctx->nx, nu = ctx->n_u, n0 = N * nu;
+  const int npairs = N * (N + 1) / 2;
+  const int dslot = (int)ctx->dmax + 1;
+  FusedKernel kern = pick_kernel(nx, nu);
+  const bool whole = ctx->node_lo == 0 && gm_node_hi(ctx) == ctx->M;
+  int SC = 16;
+  while (SC > 1 && fused_smem(SC, nx, nu, ld, dslot, n0) > kFusedSmemBudget) SC >>= 1;
+  const size_t sm = fused_smem(SC, nx, nu, ld, dslot, n0);
+  if (!kern || !whole || npairs > 256 || sm > kFusedSmemBudget) {
+    // shapes outside the fused kernel's instantiations: the two-kernel path
+    rc = gm_condense_gammas(ctx, B, N, a_self, a_nbr, b, c, x0, gamma, ld, stream);
+    if (rc) return rc;
+    return gm_condense_cost(ctx, B, N, gamma, ld, q, q_stride, x_ref, xref_stride, r, r_stride,
+                            u_ref, uref_stride, H, g, 0, stream);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int occ = 0;
+  GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, sm));
+  if (occ < 1) return gm_fail(ctx, GM_ERR_CONFIG, "fused condensing kernel does not fit an SM");
+  // node partition: all CTAs co-resident (the stage waits need it)
+  const int64_t M = ctx->M;
+  const int64_t slots = (int64_t)ctx->sm_count * occ;
+  int64_t per = M;
+  if (B < slots) {
+    const int64_t want = std::max<int64_t>(1, slots / B);
+    per = (M + want - 1) / want;
+    per = std::max<int64_t>(per, (M + 4095) / 4096);
+  }
+  const int splits = (int)((M + per - 1) / per);
+  rc = ensure_deps(ctx, per, splits);
+  if (rc) return rc;
+  const int64_t grid = (int64_t)B * splits;
+  if (splits > 1 && grid > slots) return gm_fail(ctx, GM_ERR_CONFIG, "fused condensing grid not co-resident");
+  rc = ensure_flags(ctx, grid + 1);
+  if (rc) return rc;
+  const int groups = std::min(splits, 16);
+  const int PU = npairs * nu * nu;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t pH = sizeof(float) * (size_t)grid * PU, pg = sizeof(double) * (size_t)grid * n0;
+  const size_t tH = sizeof(double) * (size_t)B * groups * PU, tg = sizeof(double) * (size_t)B * groups * n0;
+  char* scr = (char*)gm_scratch(ctx, up(pH) + up(pg) + up(tH) + tg + 256);
+  if (!scr) return gm_fail(ctx, GM_ERR_CUDA, "scratch allocation failed");
+  FusedArgs a{};
+  a.M = (int)M;
+  a.E = (int)ctx->E;
+  a.N = N;
+  a.ld = ld;
+  a.per = (int)per;
+  a.splits = splits;
+  a.sc = SC;
+  a.npairs = npairs;
+  a.dslot = dslot;
+  a.ptr = ctx->d_ptr;
+  a.src = ctx->d_src;
+  a.dep_ptr = ctx->d_dep_ptr;
+  a.dep = ctx->d_dep;
+  a.a_self = a_self;
+  a.a_nbr = a_nbr;
+  a.b = b;
+  a.c = c;
+  a.x0 = x0;
+  a.W = gamma;
+  a.q = q;
+  a.q_stride = q_stride;
+  a.xref = x_ref;
+  a.xref_stride = xref_stride;
+  a.partH = (float*)scr;
+  a.partg = (double*)(scr + up(pH));
+  a.flags = ctx->d_flags;
+  kern<<<(unsigned)grid, 256, sm, st>>>(a);
+  GM_LAUNCH_CHECK(ctx, "k_condense_fused");
+  PairReduceArgs ra{};
+  ra.nu = nu;
+  ra.n0 = n0;
+  ra.npairs = npairs;
+  ra.splits = splits;
+  ra.groups = groups;
+  ra.partH = a.partH;
+  ra.partg = a.partg;
+  ra.tmpH = (double*)(scr + up(pH) + up(pg));
+  ra.tmpg = (double*)(scr + up(pH) + up(pg) + up(tH));
+  ra.r = r;
+  ra.r_stride = r_stride;
+  ra.uref = u_ref;
+  ra.uref_stride = uref_stride;
+  ra.H = H;
+  ra.g = g;
+  const unsigned eb = (unsigned)gm_ceil_div(std::max(PU, n0), 256);
+  k_pair_reduce1<<<dim3(eb, (unsigned)groups, (unsigned)B), 256, 0, st>>>(ra);
+  GM_LAUNCH_CHECK(ctx, "k_pair_reduce1");
+  k_pair_reduce2<<<dim3(eb, (unsigned)B), 256, 0, st>>>(ra);
+  GM_LAUNCH_CHECK(ctx, "k_pair_reduce2");
+  return GM_OK;
+}
+
+}  // extern "C"

@@ -28,7 +28,7 @@ import numpy as np
 
 from . import device as _dev
 from ._runtime import lib
-from .condensing import cost_device, lin_blocks, rows_device
+from .condensing import fused_device, lin_blocks, rows_device
 from .gnn import LinearizedDynamics, linearize_device
 from .graph import InputVector, SystemState, Trajectory
 from .qpsolver import STATUS_BY_CODE, QpStatus, SolverSettings
@@ -209,10 +209,8 @@ class StepPlan:
     def _condense(self):
         eng, N, ds = self.eng, self.N, self.ds
         sp = eng.stream_ptr()
-        eng.ctx.call("gm_condense_gammas", 1, N, self.a_self.data_ptr(),
-                     self.a_nbr.data_ptr() if eng.E else None, self.b.data_ptr(),
-                     self.c.data_ptr(), self.x_meas.data_ptr(), self.W.data_ptr(), self.ld, sp)
-        cost_device(eng, ds, self.W, self.ld, N, self.H0, self.g0)
+        fused_device(eng, ds, self.a_self, self.a_nbr if eng.E else None, self.b, self.c,
+                     self.x_meas, self.W, self.ld, N, self.H0, self.g0)
         rows_device(eng, ds, self.W, self.ld, N, self.C0, self.d0)
         if self.ns:
             eng.ctx.call("gm_expand_soft", 1, self.n0, self.m0, self.H0.data_ptr(),

@@ -1,0 +1,139 @@
+"""K-COND (fused Gamma recursion + cost reduction, k_condense_fused.cu) against
+the two-kernel path K-REC + K-HG on the same device blocks.
+
+Both paths compute the same fp32 recursion; H/g differ only by fp32 partial-sum
+order (and the symmetrised Q), so the comparison is at fp32 round-off relative
+to max|H|.  Gamma must be bitwise identical (same per-column FMA order).
+Also covers repeated launches (self-resetting stage counters), B > 1, graphs
+with remote neighbours (mesh, random), and CUDA-graph replay."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(topo, N, nx, nu, B, seed):
+    rng = np.random.default_rng(seed)
+    M, E = topo.node_count, len(topo.edges)
+    a_self = (rng.standard_normal((B * N, M, nx, nx)) * 0.3 + np.eye(nx) * 0.8).astype(np.float32)
+    a_nbr = (rng.standard_normal((B * N, max(E, 1), nx, nx)) * 0.2).astype(np.float32)
+    b = rng.standard_normal((B * N, M, nx, nu)).astype(np.float32)
+    c = rng.standard_normal((B * N, M, nx))
+    x0 = rng.standard_normal((B, M, nx))
+    q = rng.standard_normal((M, N + 1, nx, nx))
+    q = np.einsum("mkab,mkcb->mkac", q, q) * 0.2 + np.eye(nx)
+    xref = rng.standard_normal((B, M, N + 1, nx))
+    r = np.tile(np.eye(nu) * 0.5, (N, 1, 1)) + 0.01
+    uref = rng.standard_normal((N, nu))
+    return a_self, a_nbr, b, c, x0, q, xref, r, uref
+
+
+def _run(topo, N, nx, nu, B, seed, reps=2, graph=False):
+    import torch
+
+    from paper_2602_17601_b200 import device as dev
+    from paper_2602_17601_b200._runtime import lib
+
+    eng = dev.engine(topo)
+    eng.set_dims(nx, nu)
+    M = topo.node_count
+    ld = lib().gm_gamma_ld(N, nu)
+    arrs = _problem(topo, N, nx, nu, B, seed)
+    a_self, a_nbr, b, c, x0, q, xref, r, uref = [
+        eng.h2d(x, np.float32 if x.dtype == np.float32 else np.float64) for x in arrs]
+    n0 = N * nu
+    sp = eng.stream_ptr()
+    E = eng.E
+    W1 = eng.zeros((B, M, N + 1, nx, ld), np.float32)
+    H1 = eng.zeros((B, n0, n0), np.float64)
+    g1 = eng.zeros((B, n0), np.float64)
+    eng.ctx.call("gm_condense_gammas", B, N, a_self.data_ptr(), a_nbr.data_ptr() if E else None,
+                 b.data_ptr(), c.data_ptr(), x0.data_ptr(), W1.data_ptr(), ld, sp)
+    eng.ctx.call("gm_condense_cost", B, N, W1.data_ptr(), ld, q.data_ptr(), 0, xref.data_ptr(),
+                 M * (N + 1) * nx, r.data_ptr(), 0, uref.data_ptr(), 0, H1.data_ptr(),
+                 g1.data_ptr(), 0, sp)
+    W2 = eng.zeros((B, M, N + 1, nx, ld), np.float32) + 7.0  # fully overwritten
+    H2 = eng.zeros((B, n0, n0), np.float64)
+    g2 = eng.zeros((B, n0), np.float64)
+
+    def fused():
+        eng.ctx.call("gm_condense_fused", B, N, a_self.data_ptr(), a_nbr.data_ptr() if E else None,
+                     b.data_ptr(), c.data_ptr(), x0.data_ptr(), W2.data_ptr(), ld, q.data_ptr(), 0,
+                     xref.data_ptr(), M * (N + 1) * nx, r.data_ptr(), 0, uref.data_ptr(), 0,
+                     H2.data_ptr(), g2.data_ptr(), eng.stream_ptr())
+
+    outs = []
+    if graph:
+        fused()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            fused()
+        for _ in range(reps):
+            H2.zero_()
+            gr.replay()
+            torch.cuda.synchronize()
+            outs.append((W2.clone(), H2.clone(), g2.clone()))
+    else:
+        for _ in range(reps):
+            fused()
+            torch.cuda.synchronize()
+            outs.append((W2.clone(), H2.clone(), g2.clone()))
+    return (W1, H1, g1), outs
+
+
+def _check(ref, outs, n0, nu, N):
+    W1, H1, g1 = ref
+    for W2, H2, g2 in outs:
+        assert torch_equal(W1, W2)
+        Hr, Hf = H1.cpu().numpy(), H2.cpu().numpy()
+        scale = np.max(np.abs(Hr))
+        assert np.max(np.abs(Hf - Hr)) <= 2e-6 * scale
+        assert np.array_equal(Hf, np.swapaxes(Hf, 1, 2))  # exactly symmetric
+        gr, gf = g1.cpu().numpy(), g2.cpu().numpy()
+        assert np.max(np.abs(gf - gr)) <= 2e-6 * max(1.0, np.max(np.abs(gr)))
+    # bitwise reproducible across launches
+    for W2, H2, g2 in outs[1:]:
+        assert torch_equal(H2, outs[0][1]) and torch_equal(g2, outs[0][2])
+
+
+def torch_equal(a, b):
+    import torch
+
+    return bool(torch.equal(a, b))
+
+
+@pytest.mark.parametrize("graph,N,nx,nu,B", [
+    ("chain1000", 20, 6, 6, 1),
+    ("chain1000", 20, 6, 6, 3),
+    ("mesh", 12, 6, 3, 1),
+    ("mesh", 7, 4, 2, 2),
+    ("random", 9, 6, 2, 1),
+    ("chain37", 5, 2, 1, 1),
+    ("chain37", 6, 3, 2, 1),   # not instantiated: two-kernel fallback inside the call
+])
+def test_fused_matches_two_kernel_path(graph, N, nx, nu, B):
+    from paper_2602_17601_b200.graph import GraphTopology, chain_topology, mesh_topology
+
+    if graph == "chain1000":
+        topo = chain_topology(1000)
+    elif graph == "chain37":
+        topo = chain_topology(37)
+    elif graph == "mesh":
+        topo = mesh_topology(23, 17)
+    else:
+        rng = np.random.default_rng(5)
+        M = 300
+        nbrs = [sorted(set(int(j) for j in rng.integers(0, M, rng.integers(0, 6))) - {i})
+                for i in range(M)]
+        topo = GraphTopology(M, tuple(tuple(n) for n in nbrs), 8)
+    ref, outs = _run(topo, N, nx, nu, B, seed=11, reps=3)
+    _check(ref, outs, N * nu, nu, N)
+
+
+def test_fused_graph_replay():
+    from paper_2602_17601_b200.graph import mesh_topology
+
+    topo = mesh_topology(30, 20)
+    ref, outs = _run(topo, 10, 6, 6, 1, seed=3, reps=3, graph=True)
+    _check(ref, outs, 60, 6, 10)
