@@ -68,6 +68,55 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Per-item staging buffer (one (stage, node sub-chunk) work item), double
+// buffered: item j+1 is fetched with cp.async while item j computes.
+template <int NX, int NU>
+struct Stage {
+  float* as;    // SC x NX*NX      a_self[n]
+  float* an;    // SC*dmax x NX*NX a_nbr[n] of the chunk's edge range
+  float* bb;    // SC x NX*NU      b[n]
+  double* cc;   // SC x NX         c[n]
+  double* qd;   // SC x NX*NX      Q[k]
+  double* xd;   // SC x NX         x_ref[k]
+  int* src;     // SC*dmax         in-neighbour ids of the chunk's edges
+};
+
+template <int NX, int NU>
+__device__ __forceinline__ Stage<NX, NU> stage_at(unsigned char* base, int SC, int emax) {
+  Stage<NX, NU> s;
+  double* d = (double*)base;
+  s.cc = d;
+  s.qd = s.cc + SC * NX;
+  s.xd = s.qd + SC * NX * NX;
+  float* f = (float*)(s.xd + SC * NX);
+  s.as = f;
+  s.an = s.as + SC * NX * NX;
+  s.bb = s.an + (int64_t)emax * NX * NX;
+  s.src = (int*)(s.bb + SC * NX * NU);
+  return s;
+}
+
+template <int NX, int NU>
+__host__ __device__ inline size_t stage_bytes(int SC, int emax) {
+  size_t b = sizeof(double) * ((size_t)SC * NX * 2 + (size_t)SC * NX * NX) +
+             sizeof(float) * ((size_t)SC * NX * NX + (size_t)emax * NX * NX + (size_t)SC * NX * NU) +
+             sizeof(int) * (size_t)emax;
+  return (b + 15) & ~size_t(15);
+}
+
 template <int NX, int NU>
 __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -77,21 +126,24 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
   const int64_t bi = blockIdx.x / a.splits;
   const int split = (int)(blockIdx.x % a.splits);
   const int nb = split * a.per, ne = min(M, nb + a.per);
+  const int nn = ne - nb;
+  const int nsub = (nn + SC - 1) / SC;
+  const int emax = SC * (a.dslot - 1) > 0 ? SC * (a.dslot - 1) : 1;
   int* flags = a.flags + bi * a.splits;
   const int64_t stage_stride = (int64_t)NX * ld;
   const int64_t node_stride = (int64_t)(N + 1) * stage_stride;
   float* Wb = a.W + bi * (int64_t)M * node_stride;
 
   // shared memory carve-up
-  float* Gc = (float*)smraw;                          // SC x NX x ld  current-stage rows
-  float* QGc = Gc + (int64_t)SC * NX * ld;            // SC x NX x ld  Qs G (live columns)
-  float* Ab = QGc + (int64_t)SC * NX * ld;            // SC x dslot x NX*NX  closed-nbhd blocks
-  float* Bb = Ab + (int64_t)SC * a.dslot * NX * NX;   // SC x NX*NU
-  float* Qs = Bb + SC * NX * NU;                      // SC x NX*NX  (Q + Q')/2
-  float* cs = Qs + SC * NX * NX;                      // SC x NX
-  double* wv = (double*)(((uintptr_t)(cs + SC * NX) + 15) & ~(uintptr_t)15);  // SC x NX
-  double* gs = wv + SC * NX;                          // n0  (g accumulator)
+  const size_t sbytes = stage_bytes<NX, NU>(SC, emax);
+  float* Gc = (float*)(smraw + 2 * sbytes);        // SC x NX x ld  current-stage rows
+  float* QGc = Gc + (int64_t)SC * NX * ld;         // SC x NX x ld  Qs G (live columns)
+  float* Qs = QGc + (int64_t)SC * NX * ld;         // SC x NX*NX    (Q + Q')/2
+  double* wv = (double*)(((uintptr_t)(Qs + SC * NX * NX) + 15) & ~(uintptr_t)15);  // SC x NX
+  double* gs = wv + SC * NX;                       // n0 (g accumulator)
+  int* nptr = (int*)(gs + n0);                     // nn + 1 CSR offsets of the owned nodes
 
+  for (int t = tid; t <= nn; t += nt) nptr[t] = a.ptr[nb + t];
   // block pair owned by this thread (ordered by q, then p)
   int bq = (int)((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f);
   while ((bq + 1) * (bq + 2) / 2 <= tid) ++bq;
@@ -104,14 +156,45 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
 #pragma unroll
     for (int v = 0; v < NU; ++v) acc[u][v] = 0.f;
   for (int t = tid; t < n0; t += nt) gs[t] = 0.0;
+  __syncthreads();
+
+  // work item j = (stage n = j / nsub, sub-chunk j % nsub); cp.async prefetch
+  auto prefetch = [&](int j) {
+    const int n = j / nsub, s0 = nb + (j % nsub) * SC;
+    const int sc = min(SC, ne - s0), k = n + 1;
+    const Stage<NX, NU> S = stage_at<NX, NU>(smraw + (j & 1) * sbytes, SC, emax);
+    const int64_t pstage = bi * N + n;
+    const int eb = nptr[s0 - nb], ee = nptr[s0 - nb + sc];
+    const int nE = ee - eb;
+    const float* gas = a.a_self + (pstage * M + s0) * NX * NX;
+    for (int t = tid; t < sc * NX * NX; t += nt) cp_async4(S.as + t, gas + t);
+    if (nE > 0) {
+      const float* gan = a.a_nbr + (pstage * a.E + eb) * NX * NX;
+      for (int t = tid; t < nE * NX * NX; t += nt) cp_async4(S.an + t, gan + t);
+      for (int t = tid; t < nE; t += nt) cp_async4(S.src + t, a.src + eb + t);
+    }
+    const float* gb = a.b + (pstage * M + s0) * NX * NU;
+    for (int t = tid; t < sc * NX * NU; t += nt) cp_async4(S.bb + t, gb + t);
+    const double* gc = a.c + (pstage * M + s0) * NX;
+    for (int t = tid; t < sc * NX; t += nt) cp_async8(S.cc + t, gc + t);
+    for (int t = tid; t < sc * NX * NX; t += nt) {
+      const int li = t / (NX * NX), e = t - li * NX * NX;
+      cp_async8(S.qd + t, a.q + bi * a.q_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX * NX + e);
+    }
+    for (int t = tid; t < sc * NX; t += nt) {
+      const int li = t / NX, e = t - li * NX;
+      cp_async8(S.xd + t, a.xref + bi * a.xref_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX + e);
+    }
+    cp_async_commit();
+  };
+  const int items = N * nsub;
+  if (items > 0) prefetch(0);
 
   // stage 0: Gamma_u = 0, Gamma_x = x0 (condensing.py:205-206)
-  for (int i = nb; i < ne; ++i) {
-    float* Wo = Wb + (int64_t)i * node_stride;
-    for (int t = tid; t < NX * ld; t += nt) {
-      const int r = t / ld, col = t - r * ld;
-      Wo[t] = (col == XC) ? (float)a.x0[(bi * M + i) * NX + r] : 0.f;
-    }
+  for (int t = tid; t < nn * NX * ld; t += nt) {
+    const int li = t / (NX * ld), rem = t - li * NX * ld, r = rem / ld, col = rem - r * ld;
+    Wb[(int64_t)(nb + li) * node_stride + rem] =
+        (col == XC) ? (float)a.x0[(bi * M + nb + li) * NX + r] : 0.f;
   }
   const int d0 = a.dep_ptr[split], d1 = a.dep_ptr[split + 1];
   __syncthreads();
@@ -120,146 +203,146 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
     st_release(&flags[split], 1);
   }
 
-  for (int n = 0; n < N; ++n) {
-    const int k = n + 1;            // stage being produced
-    const int live = n * NU;        // live Gamma_u columns of stage n
-    // wait until every CTA owning a neighbour has published stage n
-    for (int d = d0 + tid; d < d1; d += nt) {
-      const int* f = &flags[a.dep[d]];
-      while (ld_acquire(f) < k) __nanosleep(32);
+  for (int j = 0; j < items; ++j) {
+    const int n = j / nsub, sub = j % nsub;
+    const int s0 = nb + sub * SC, sc = min(SC, ne - s0);
+    const int k = n + 1;       // stage being produced
+    const int live = n * NU;   // live Gamma_u columns of stage n
+    const Stage<NX, NU> S = stage_at<NX, NU>(smraw + (j & 1) * sbytes, SC, emax);
+    if (sub == 0) {
+      // wait until every CTA owning a neighbour has published stage n
+      for (int d = d0 + tid; d < d1; d += nt) {
+        const int* f = &flags[a.dep[d]];
+        while (ld_acquire(f) < k) __nanosleep(32);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (j + 1 < items) prefetch(j + 1);  // into the other buffer (free since item j-1 ended)
+    for (int t = tid; t < sc * NX * NX; t += nt) {
+      const int li = t / (NX * NX), e = t - li * NX * NX, r = e / NX, cc = e - r * NX;
+      const double* Qk = S.qd + li * NX * NX;
+      Qs[t] = (float)(0.5 * (Qk[r * NX + cc] + Qk[cc * NX + r]));
+    }
+    const int ebase = nptr[s0 - nb];
+    // Gamma rows of stage k (condensing.py:213-224), same per-column
+    // recursion and FMA order as K-REC: live columns and Gamma_x via the
+    // closed neighbourhood, block n <- B_n, zero elsewhere
+    for (int t = tid; t < sc * ld; t += nt) {
+      const int li = t / ld, col = t - li * ld;
+      const int i = s0 + li;
+      float r6[NX];
+#pragma unroll
+      for (int r = 0; r < NX; ++r) r6[r] = 0.f;
+      if (col < live || col == XC) {
+        const int el0 = nptr[i - nb] - ebase, deg = nptr[i - nb + 1] - nptr[i - nb];
+        const float* Wn = Wb + (int64_t)n * stage_stride + col;
+        for (int s = 0; s <= deg; s += 4) {
+          float w[4][NX];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ss = s + u;
+            if (ss <= deg) {
+              const int jn = ss == 0 ? i : S.src[el0 + ss - 1];
+              const float* Wj = Wn + (int64_t)jn * node_stride;
+#pragma unroll
+              for (int qq = 0; qq < NX; ++qq) w[u][qq] = __ldcg(Wj + (int64_t)qq * ld);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ss = s + u;
+            if (ss <= deg) {
+              const float* As = ss == 0 ? S.as + li * NX * NX : S.an + (el0 + ss - 1) * NX * NX;
+#pragma unroll
+              for (int r = 0; r < NX; ++r)
+#pragma unroll
+                for (int qq = 0; qq < NX; ++qq) r6[r] = fmaf(As[r * NX + qq], w[u][qq], r6[r]);
+            }
+          }
+        }
+        if (col == XC) {
+#pragma unroll
+          for (int r = 0; r < NX; ++r) r6[r] += (float)S.cc[li * NX + r];
+        }
+      } else if (col >= live && col < live + NU) {
+#pragma unroll
+        for (int r = 0; r < NX; ++r) r6[r] = S.bb[(li * NX + r) * NU + (col - live)];
+      }
+      float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + col;
+      float* Gs = Gc + (int64_t)li * NX * ld + col;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) {
+        Wo[(int64_t)r * ld] = r6[r];
+        Gs[(int64_t)r * ld] = r6[r];
+      }
     }
     __syncthreads();
-    const int64_t pstage = bi * N + n;
-    for (int s0 = nb; s0 < ne; s0 += SC) {
-      const int sc = min(SC, ne - s0);
-      // stage the chunk's blocks (a_self / a_nbr / b / c of stage n, Q of stage k)
-      for (int li = 0; li < sc; ++li) {
-        const int i = s0 + li;
-        const int e0 = a.ptr[i], deg = a.ptr[i + 1] - e0;
-        float* A = Ab + (int64_t)li * a.dslot * NX * NX;
-        for (int t = tid; t < (1 + deg) * NX * NX; t += nt) {
-          const int s = t / (NX * NX), qq = t - s * NX * NX;
-          A[t] = s == 0 ? a.a_self[(pstage * M + i) * NX * NX + qq]
-                        : a.a_nbr[(pstage * a.E + e0 + s - 1) * NX * NX + qq];
-        }
-      }
-      for (int t = tid; t < sc * NX * NU; t += nt)
-        Bb[t] = a.b[(pstage * M + s0) * NX * NU + t];
-      for (int t = tid; t < sc * NX; t += nt) cs[t] = (float)a.c[(pstage * M + s0) * NX + t];
-      for (int t = tid; t < sc * NX * NX; t += nt) {
-        const int li = t / (NX * NX), e = t - li * NX * NX, r = e / NX, cc = e - r * NX;
-        const double* Qk = a.q + bi * a.q_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX * NX;
-        Qs[t] = (float)(0.5 * (Qk[r * NX + cc] + Qk[cc * NX + r]));
-      }
-      __syncthreads();
-      // Gamma rows of stage k (condensing.py:213-224), same per-column
-      // recursion as K-REC: live columns and Gamma_x via the closed
-      // neighbourhood, block n <- B_n, zero elsewhere
-      for (int t = tid; t < sc * ld; t += nt) {
-        const int li = t / ld, col = t - li * ld;
-        const int i = s0 + li;
-        float r6[NX];
-#pragma unroll
-        for (int r = 0; r < NX; ++r) r6[r] = 0.f;
-        if (col < live || col == XC) {
-          const int e0 = a.ptr[i], deg = a.ptr[i + 1] - e0;
-          const float* A = Ab + (int64_t)li * a.dslot * NX * NX;
-          for (int s = 0; s <= deg; ++s) {
-            const int j = s == 0 ? i : a.src[e0 + s - 1];
-            const float* Wj = Wb + (int64_t)j * node_stride + (int64_t)n * stage_stride + col;
-            float w[NX];
-#pragma unroll
-            for (int qq = 0; qq < NX; ++qq) w[qq] = __ldcg(Wj + (int64_t)qq * ld);
-            const float* As = A + s * NX * NX;
-#pragma unroll
-            for (int r = 0; r < NX; ++r)
-#pragma unroll
-              for (int qq = 0; qq < NX; ++qq) r6[r] = fmaf(As[r * NX + qq], w[qq], r6[r]);
-          }
-          if (col == XC) {
-#pragma unroll
-            for (int r = 0; r < NX; ++r) r6[r] += cs[li * NX + r];
-          }
-        } else if (col >= live && col < live + NU) {
-#pragma unroll
-          for (int r = 0; r < NX; ++r) r6[r] = Bb[(li * NX + r) * NU + (col - live)];
-        }
-        float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + col;
-        float* Gs = Gc + (int64_t)li * NX * ld + col;
-#pragma unroll
-        for (int r = 0; r < NX; ++r) {
-          Wo[(int64_t)r * ld] = r6[r];
-          Gs[(int64_t)r * ld] = r6[r];
-        }
-      }
-      __syncthreads();
-      if (s0 + SC >= ne && tid == 0) {  // all of this CTA's stage-k rows are out
-        __threadfence();
-        st_release(&flags[split], k + 1);
-      }
-      // Qs G on the live columns of stage k, and w = 2 Q Gamma_x - 2 Q x_ref
-      const int lk = k * NU;
-      for (int t = tid; t < sc * lk; t += nt) {
-        const int li = t / lk, col = t - li * lk;
-        const float* Gs = Gc + (int64_t)li * NX * ld + col;
-        float gcol[NX];
-#pragma unroll
-        for (int qq = 0; qq < NX; ++qq) gcol[qq] = Gs[(int64_t)qq * ld];
-        const float* Qn = Qs + li * NX * NX;
-        float* Os = QGc + (int64_t)li * NX * ld + col;
-#pragma unroll
-        for (int r = 0; r < NX; ++r) {
-          float s = 0.f;
-#pragma unroll
-          for (int qq = 0; qq < NX; ++qq) s = fmaf(Qn[r * NX + qq], gcol[qq], s);
-          Os[(int64_t)r * ld] = s;
-        }
-      }
-      for (int t = tid; t < sc * NX; t += nt) {
-        const int li = t / NX, r = t - li * NX;
-        const int i = s0 + li;
-        const double* Qk = a.q + bi * a.q_stride + ((int64_t)i * (N + 1) + k) * NX * NX + r * NX;
-        const double* xr = a.xref + bi * a.xref_stride + ((int64_t)i * (N + 1) + k) * NX;
-        const float* gx = Gc + (int64_t)li * NX * ld + XC;
-        double qg = 0.0, qx = 0.0;
-#pragma unroll
-        for (int qq = 0; qq < NX; ++qq) {
-          qg += Qk[qq] * (double)gx[(int64_t)qq * ld];
-          qx += Qk[qq] * xr[qq];
-        }
-        wv[t] = 2.0 * qg + (-2.0 * qx);
-      }
-      __syncthreads();
-      // H block pairs live at stage k: q < k  <=>  tid < k(k+1)/2
-      if (owner && bq < k) {
-        for (int li = 0; li < sc; ++li) {
-#pragma unroll
-          for (int r = 0; r < NX; ++r) {
-            const float* gp = Gc + ((int64_t)li * NX + r) * ld + bp * NU;
-            const float* gq = QGc + ((int64_t)li * NX + r) * ld + bq * NU;
-            float x[NU], y[NU];
-#pragma unroll
-            for (int u = 0; u < NU; ++u) {
-              x[u] = gp[u];
-              y[u] = gq[u];
-            }
-#pragma unroll
-            for (int u = 0; u < NU; ++u)
-#pragma unroll
-              for (int v = 0; v < NU; ++v) acc[u][v] = fmaf(x[u], y[v], acc[u][v]);
-          }
-        }
-      }
-      for (int cidx = tid; cidx < lk; cidx += nt) {
-        double s = gs[cidx];
-        for (int li = 0; li < sc; ++li)
-#pragma unroll
-          for (int r = 0; r < NX; ++r)
-            s += (double)Gc[((int64_t)li * NX + r) * ld + cidx] * wv[li * NX + r];
-        gs[cidx] = s;
-      }
-      __syncthreads();
+    if (sub == nsub - 1 && tid == 0) {  // all of this CTA's stage-k rows are out
+      __threadfence();
+      st_release(&flags[split], k + 1);
     }
+    // Qs G on the live columns of stage k, and w = 2 Q Gamma_x - 2 Q x_ref
+    const int lk = k * NU;
+    for (int t = tid; t < sc * lk; t += nt) {
+      const int li = t / lk, col = t - li * lk;
+      const float* Gs = Gc + (int64_t)li * NX * ld + col;
+      float gcol[NX];
+#pragma unroll
+      for (int qq = 0; qq < NX; ++qq) gcol[qq] = Gs[(int64_t)qq * ld];
+      const float* Qn = Qs + li * NX * NX;
+      float* Os = QGc + (int64_t)li * NX * ld + col;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) {
+        float s = 0.f;
+#pragma unroll
+        for (int qq = 0; qq < NX; ++qq) s = fmaf(Qn[r * NX + qq], gcol[qq], s);
+        Os[(int64_t)r * ld] = s;
+      }
+    }
+    for (int t = tid; t < sc * NX; t += nt) {
+      const int li = t / NX, r = t - li * NX;
+      const double* Qk = S.qd + li * NX * NX + r * NX;
+      const double* xr = S.xd + li * NX;
+      const float* gx = Gc + (int64_t)li * NX * ld + XC;
+      double qg = 0.0, qx = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < NX; ++qq) {
+        qg += Qk[qq] * (double)gx[(int64_t)qq * ld];
+        qx += Qk[qq] * xr[qq];
+      }
+      wv[t] = 2.0 * qg + (-2.0 * qx);
+    }
+    __syncthreads();
+    // H block pairs live at stage k: q < k  <=>  tid < k(k+1)/2
+    if (owner && bq < k) {
+      for (int li = 0; li < sc; ++li) {
+#pragma unroll
+        for (int r = 0; r < NX; ++r) {
+          const float* gp = Gc + ((int64_t)li * NX + r) * ld + bp * NU;
+          const float* gq = QGc + ((int64_t)li * NX + r) * ld + bq * NU;
+          float x[NU], y[NU];
+#pragma unroll
+          for (int u = 0; u < NU; ++u) {
+            x[u] = gp[u];
+            y[u] = gq[u];
+          }
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int v = 0; v < NU; ++v) acc[u][v] = fmaf(x[u], y[v], acc[u][v]);
+        }
+      }
+    }
+    for (int cidx = tid; cidx < lk; cidx += nt) {
+      double s = gs[cidx];
+      for (int li = 0; li < sc; ++li)
+#pragma unroll
+        for (int r = 0; r < NX; ++r)
+          s += (double)Gc[((int64_t)li * NX + r) * ld + cidx] * wv[li * NX + r];
+      gs[cidx] = s;
+    }
+    __syncthreads();
   }
 
   // partials
@@ -383,10 +466,15 @@ FusedKernel pick_kernel(int nx, int nu) {
   return nullptr;
 }
 
-size_t fused_smem(int SC, int nx, int nu, int ld, int dslot, int n0) {
-  size_t f = (size_t)SC * nx * ld * 2 + (size_t)SC * dslot * nx * nx + (size_t)SC * nx * nu +
-             (size_t)SC * nx * nx + (size_t)SC * nx;
-  return ((f * sizeof(float) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)SC * nx + n0) + 16;
+size_t fused_smem(int SC, int nx, int nu, int ld, int dslot, int n0, int64_t per) {
+  const int emax = SC * (dslot - 1) > 0 ? SC * (dslot - 1) : 1;
+  size_t st = sizeof(double) * ((size_t)SC * nx * 2 + (size_t)SC * nx * nx) +
+              sizeof(float) * ((size_t)SC * nx * nx + (size_t)emax * nx * nx + (size_t)SC * nx * nu) +
+              sizeof(int) * (size_t)emax;
+  st = (st + 15) & ~size_t(15);
+  size_t f = (size_t)SC * nx * ld * 2 + (size_t)SC * nx * nx;
+  size_t b = 2 * st + ((f * sizeof(float) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)SC * nx + n0);
+  return b + sizeof(int) * (size_t)(per + 1) + 16;
 }
 
 // CTA dependency lists for node partition `per`: CTA s waits on the owners of
@@ -451,9 +539,17 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   const int dslot = (int)ctx->dmax + 1;
   FusedKernel kern = pick_kernel(nx, nu);
   const bool whole = ctx->node_lo == 0 && gm_node_hi(ctx) == ctx->M;
+  // node partition: one CTA per SM, all co-resident (the stage waits need it)
+  const int64_t M = ctx->M;
+  const int64_t slots = ctx->sm_count;
+  int64_t per = M;
+  if (B < slots) {
+    const int64_t want = std::max<int64_t>(1, slots / B);
+    per = (M + want - 1) / want;
+  }
   int SC = 16;
-  while (SC > 1 && fused_smem(SC, nx, nu, ld, dslot, n0) > kFusedSmemBudget) SC >>= 1;
-  const size_t sm = fused_smem(SC, nx, nu, ld, dslot, n0);
+  while (SC > 1 && fused_smem(SC, nx, nu, ld, dslot, n0, per) > kFusedSmemBudget) SC >>= 1;
+  const size_t sm = fused_smem(SC, nx, nu, ld, dslot, n0, per);
   if (!kern || !whole || npairs > 256 || sm > kFusedSmemBudget) {
     // shapes outside the fused kernel's instantiations: the two-kernel path
     rc = gm_condense_gammas(ctx, B, N, a_self, a_nbr, b, c, x0, gamma, ld, stream);
@@ -466,20 +562,11 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   int occ = 0;
   GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, sm));
   if (occ < 1) return gm_fail(ctx, GM_ERR_CONFIG, "fused condensing kernel does not fit an SM");
-  // node partition: all CTAs co-resident (the stage waits need it)
-  const int64_t M = ctx->M;
-  const int64_t slots = (int64_t)ctx->sm_count * occ;
-  int64_t per = M;
-  if (B < slots) {
-    const int64_t want = std::max<int64_t>(1, slots / B);
-    per = (M + want - 1) / want;
-    per = std::max<int64_t>(per, (M + 4095) / 4096);
-  }
   const int splits = (int)((M + per - 1) / per);
   rc = ensure_deps(ctx, per, splits);
   if (rc) return rc;
   const int64_t grid = (int64_t)B * splits;
-  if (splits > 1 && grid > slots) return gm_fail(ctx, GM_ERR_CONFIG, "fused condensing grid not co-resident");
+  if (splits > 1 && grid > slots * occ) return gm_fail(ctx, GM_ERR_CONFIG, "fused condensing grid not co-resident");
   rc = ensure_flags(ctx, grid + 1);
   if (rc) return rc;
   const int groups = std::min(splits, 16);

@@ -26,7 +26,8 @@ for r in rows:
 tot = sum(v[0] for v in per.values()) or 1
 toti = sum(v[1] for v in per.values()) or 1
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+key = 0 if len(sys.argv) > 3 and sys.argv[3] == 'samples' else 1
 print(f"samples {tot}  warp-instr {toti}")
-for ln, (s, e, src, st) in sorted(per.items(), key=lambda kv: -kv[1][1])[:n]:
+for ln, (s, e, src, st) in sorted(per.items(), key=lambda kv: -kv[1][key])[:n]:
     top = ", ".join(f"{k.replace('stall_', '')}:{v}" for k, v in st.most_common(2))
     print(f"{ln:4d} {100*s/tot:5.1f}%s {100*e/toti:5.1f}%i {src[:64]:64s} | {top}")
