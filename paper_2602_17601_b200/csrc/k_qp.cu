@@ -45,24 +45,26 @@ struct QpLayout {
   size_t o_vec, o_ints, o_k, o_x, o_h, o_cg, total;
 };
 
-// n-vectors: g u hu rd rhs du ub ctl ytmp dinv        (10)
-// m-vectors: d s lam cu rp t dl ds tmp w lb rval      (12)
-__host__ __device__ inline QpLayout qp_layout(int n, int m, int ng, bool h_smem, bool cg_smem) {
+// n-vectors: g u hu rd rhs du ub ctl ytmp dinv kee hde ea   (13)
+// m-vectors: d s lam cu rp t dl ds tmp w lb rval wg ga cf    (15)
+// nf: dimension of the factorised system (K, X and packed H), <= n
+__host__ __device__ inline QpLayout qp_layout(int n, int m, int ng, bool h_smem, bool cg_smem, int nf = -1) {
   QpLayout L{};
-  const int nblk = (n + kTB - 1) / kTB;
+  if (nf < 0) nf = n;
+  const int nblk = (nf + kTB - 1) / kTB;
   size_t o = 0;
   L.o_vec = o;
-  o = qal(o + sizeof(double) * (10 * (size_t)n + 12 * (size_t)m + 64));
-  L.o_ints = o;  // rcol(m) grow(m) colptr(n+1) colrows(m) cstart(n+1)
-  o = qal(o + sizeof(int) * (3 * (size_t)m + 2 * (size_t)n + 2 + 8));
+  o = qal(o + sizeof(double) * (13 * (size_t)n + 15 * (size_t)m + 64));
+  L.o_ints = o;  // rcol(m) grow(m) colptr(n+1) colrows(m) cstart(n+1) kidx(n) eidx(n) egi(n) ge(m) elig(n)
+  o = qal(o + sizeof(int) * (4 * (size_t)m + 6 * (size_t)n + 2 + 8));
   L.o_k = o;
-  o = qal(o + sizeof(double) * packed_size(n));
+  o = qal(o + sizeof(double) * packed_size(nf));
   L.o_x = o;
   o = qal(o + sizeof(double) * (size_t)nblk * kTB * kXL);
   L.o_cg = o;
   if (cg_smem) o = qal(o + sizeof(double) * (size_t)ng * n);
   L.o_h = o;
-  if (h_smem) o = qal(o + sizeof(double) * packed_size(n));
+  if (h_smem) o = qal(o + sizeof(double) * packed_size(nf));
   L.total = o;
   return L;
 }
@@ -92,7 +94,16 @@ __device__ unsigned long long g_qp_prof[16];
 __device__ int g_qp_prof_on;
 
 struct Qs {  // per-CTA views
-  int n, m, ng, nblk;
+  // n: variables; nf: variables kept in the factorised (reduced) system.
+  // Variables with a diagonal-only Hessian row that meet at most one general
+  // constraint row (the soft-constraint slacks of expand_soft_constraints,
+  // condensing.py:419-439) are eliminated exactly by a Schur complement:
+  // kidx[0..nf) / eidx[0..ne) list kept / eliminated variables, egi[e] is the
+  // general row of eliminated e (or -1) with coefficient ea[e], ge[gi] the
+  // eliminated variable of general row gi (or -1) with coefficient ga[gi].
+  int n, m, ng, nblk, nf, ne;
+  int *kidx, *eidx, *egi, *ge, *elig;
+  double *kee, *hde, *ea, *wg, *ga, *cf;
   double *K, *X, *Hp, *Cg;
   double *g, *u, *hu, *rd, *rhs, *du, *ub, *ctl, *ytmp, *dinv;
   double *d, *s, *lam, *cu, *rp, *t, *dl, *ds, *tmp, *w, *lb, *rval;
@@ -200,24 +211,21 @@ __device__ __forceinline__ bool factor_pivot(const double (&E)[kNB][kNB], int bs
 }
 
 // Rank-4 update of one group of 4 adjacent columns [c0g, c0g+4) for the rows
-// this lane owns (lane + 32t): K[r][c] -= Lr[t] . Lc[u].  Row tiles t < T0 lie
-// entirely above the group and are not generated (T0 is a template
-// parameter), so the body is straight-line: all loads, then the FMAs, then
-// predicated stores -- the chains of all 4 x (TM - T0) slots overlap.
-// cjq[q] = colbase(j + q) (pivot column q; W[x][q] = K[cjq[q] + x]).
+// this lane owns (lane + 32t): K[r][c] -= Lr[t] . Lc[u], with the pivot
+// block's L rows already in K (panel phase).  Row tiles t < T0 lie entirely
+// above the group and are not generated (T0 is a template parameter), so the
+// body is straight-line: all loads, then the FMAs, then predicated stores.
+// cjq[q] = colbase(j + q) (pivot column q; L[x][q] = K[cjq[q] + x]).
 template <int TM, int T0>
 __device__ __forceinline__ void update_group(double* K, int n, int c0g, int pe, const int (&cjq)[kNB],
-                                             const double* pv, const double (&Lr)[TM][kNB],
-                                             int lane) {
+                                             const double (&Lr)[TM][kNB], int lane) {
   double Lc[kNB][kNB];
   double* col[kNB];
 #pragma unroll
   for (int u = 0; u < kNB; ++u) {
     const int c = min(c0g + u, n - 1);
-    double w[kNB];
 #pragma unroll
-    for (int q = 0; q < kNB; ++q) w[q] = K[cjq[q] + c];
-    lrow4(w, pv, Lc[u]);
+    for (int q = 0; q < kNB; ++q) Lc[u][q] = K[cjq[q] + c];
     col[u] = K + colbase(c, n);
   }
   double v[kNB][TM];
@@ -228,7 +236,7 @@ __device__ __forceinline__ void update_group(double* K, int n, int c0g, int pe, 
 #pragma unroll
   for (int u = 0; u < kNB; ++u) {
     const int c = c0g + u;
-    const int rlo = c < pe ? pe : c;  // next pivot block rows belong to the look-ahead
+    const int rlo = c < pe ? pe : c;  // the next pivot block belongs to the look-ahead
 #pragma unroll
     for (int t = T0; t < TM; ++t) {
       const int r = lane + 32 * t;
@@ -242,39 +250,115 @@ __device__ __forceinline__ void update_group(double* K, int n, int c0g, int pe, 
 
 template <int TM, int T0>
 __device__ __forceinline__ void update_group_dispatch(int t0, double* K, int n, int c0g, int pe,
-                                                      const int (&cjq)[kNB], const double* pv,
-                                                      const double (&Lr)[TM][kNB], int lane) {
+                                                      const int (&cjq)[kNB], const double (&Lr)[TM][kNB],
+                                                      int lane) {
   if constexpr (T0 < TM - 1) {
     if (t0 > T0) {
-      update_group_dispatch<TM, T0 + 1>(t0, K, n, c0g, pe, cjq, pv, Lr, lane);
+      update_group_dispatch<TM, T0 + 1>(t0, K, n, c0g, pe, cjq, Lr, lane);
       return;
     }
   }
-  update_group<TM, T0>(K, n, c0g, pe, cjq, pv, Lr, lane);
+  update_group<TM, T0>(K, n, c0g, pe, cjq, Lr, lane);
+}
+
+// Rank-4 trailing update with the fp64 tensor cores: K[r][c] -= L[r][j..] .
+// L[c][j..] over 8x8 tiles (DMMA m8n8k4: D = A B + C with A = -L rows (8x4),
+// B = L cols' (4x8)), for every element with c >= j2, r >= c, r < n that is
+// not in the next pivot block [j2, pe)^2 (the look-ahead owns it).  Fragments
+// are loaded straight from the packed lower triangle; invalid slots load 0
+// and are not stored.  Tiles (R, C), C >= j2/8, R >= max(C, pe/8), are dealt
+// round-robin to warps w0, w0 + nw, ...; each warp runs 4 tiles at a time
+// (all loads, then 4 DMMAs, then the stores) for ILP.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b, double c0, double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+__device__ __forceinline__ void update_tiles(double* K, int n, int bs, int j2, int pe, const int (&cjq)[kNB],
+                                             int widx, int nw, int lane) {
+  const int T = (n + 7) >> 3;
+  const int rmin0 = pe >> 3;
+  const int i = lane >> 2, p = lane & 3;
+  const int cq = cjq[p];  // column base of pivot column j + p
+  const bool pl = p < bs;
+  int C = j2 >> 3, R = max(C, rmin0);
+  auto adv = [&](int k) {
+    R += k;
+    while (C < T && R >= T) {
+      const int over = R - T;
+      ++C;
+      R = max(C, rmin0) + over;
+    }
+  };
+  adv(widx);
+  while (C < T) {
+    int tr[4], tc[4];
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      tr[u] = R;
+      tc[u] = C;
+      if (C < T) {
+        ++cnt;
+        adv(nw);
+      }
+    }
+    double a[4], b[4], c0[4], c1[4];
+    int o0[4], o1[4];
+    bool v0[4], v1[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool live = u < cnt;
+      const int ra = 8 * tr[u] + i, rb = 8 * tc[u] + i;
+      a[u] = (live && pl && ra < n) ? -K[cq + ra] : 0.0;
+      b[u] = (live && pl && rb < n) ? K[cq + rb] : 0.0;
+      const int cc = 8 * tc[u] + 2 * p;
+      const bool rin = live && ra < n;
+      v0[u] = rin && cc >= j2 && cc < n && ra >= cc && !(ra < pe && cc < pe);
+      v1[u] = rin && cc + 1 >= j2 && cc + 1 < n && ra >= cc + 1 && !(ra < pe && cc + 1 < pe);
+      o0[u] = colbase(cc, n) + ra;
+      o1[u] = colbase(cc + 1, n) + ra;
+      c0[u] = v0[u] ? K[o0[u]] : 0.0;
+      c1[u] = v1[u] ? K[o1[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma884(c0[u], c1[u], a[u], b[u], c0[u], c1[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (v0[u]) K[o0[u]] = c0[u];
+      if (v1[u]) K[o1[u]] = c1[u];
+    }
+  }
 }
 
 // Factor K = L L' in place (packed lower); false on a failed pivot;
-// dinv[j] = 1/L[j][j].  Steps of kNB columns, one CTA barrier per step:
-// warp 0 lane 0 updates and factors the NEXT 4x4 pivot block (look-ahead)
-// while warps 1.. apply the current block's rank-4 update to the trailing
-// matrix in groups of 4 adjacent columns.  Panels keep their Schur-complement
-// values W until a final parallel pass turns them into L.
+// dinv[j] = 1/L[j][j].  Steps of kNB columns with the pivot block's factor
+// already known (look-ahead), two CTA barriers per step:
+//   panel:  all threads turn the block's Schur-complement rows below the
+//           pivot block into L rows (x = w F^{-T}) in place; thread 0 writes
+//           the pivot block's own L entries;
+//   update: warp 0 lane 0 updates and factors the NEXT 4x4 pivot block
+//           (the critical path: 4 rsqrt + short FMA chains) while warps 1..
+//           apply the rank-4 update to the trailing matrix in groups of 4
+//           adjacent columns, loading L instead of recomputing it.
 template <int TM>
 __device__ bool chol_factor(Qs& S) {
-  const int n = S.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int n = S.nf, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (n == 0) return true;  // every variable eliminated
   double* K = S.K;
-  double* fl = S.ytmp;  // per block j: ytmp[j..j+3] = l10 l20 l21 l30, ctl[j..j+1] = l31 l32
-  double* fl2 = S.ctl;
-  auto save_factor = [&](int jb, const double* pv) {
+  auto diag_block = [&](int jb, const double* pv) {  // L's pivot block from its factor
+    const int bs = min(kNB, n - jb);
+    const double* lv = pv + 4;  // l10 l20 l21 l30 l31 l32
+    const int li[4][4] = {{-1, -1, -1, -1}, {0, -1, -1, -1}, {1, 2, -1, -1}, {3, 4, 5, -1}};
 #pragma unroll
     for (int q = 0; q < kNB; ++q)
-      if (jb + q < n) S.dinv[jb + q] = pv[q];
-    if (jb + 0 < n) fl[jb + 0] = pv[4];
-    if (jb + 1 < n) fl[jb + 1] = pv[5];
-    if (jb + 2 < n) fl[jb + 2] = pv[6];
-    if (jb + 3 < n) fl[jb + 3] = pv[7];
-    if (jb + 0 < n) fl2[jb + 0] = pv[8];
-    if (jb + 1 < n) fl2[jb + 1] = pv[9];
+      if (q < bs) S.dinv[jb + q] = pv[q];
+#pragma unroll
+    for (int a = 0; a < kNB; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b)
+        if (a < bs) K[colbase(jb + b, n) + jb + a] = a == b ? 1.0 / pv[a] : lv[li[a][b]];
   };
   if (tid == 0) {
     const int bs = min(kNB, n);
@@ -284,7 +368,6 @@ __device__ bool chol_factor(Qs& S) {
 #pragma unroll
       for (int b = 0; b < kNB; ++b) E[a][b] = (a < bs && b <= a) ? K[colbase(b, n) + a] : 0.0;
     *S.flag = factor_pivot(E, bs, S.pv) ? 0 : 1;
-    save_factor(0, S.pv);
   }
   __syncthreads();
   int buf = 0;
@@ -292,25 +375,37 @@ __device__ bool chol_factor(Qs& S) {
     if (*S.flag) return false;  // uniform: read after the barrier
     const int bs = min(kNB, n - j);
     const int j2 = j + bs;
-    if (j2 >= n) break;
-    const long long tstep = S.prof ? clock64() : 0;
-    const int bs2 = min(kNB, n - j2);
-    const int pe = j2 + bs2;  // next pivot block: rows/cols [j2, pe)
     const double* pv = S.pv + buf * 16;
+    const long long tstep = S.prof ? clock64() : 0;
     int cjq[kNB];
 #pragma unroll
     for (int q = 0; q < kNB; ++q) cjq[q] = j + q < j2 ? colbase(j + q, n) : colbase(j, n);
-    // zero weights for missing pivot columns make their W entries irrelevant
+    // panel: L rows below the pivot block (zero weights for missing pivot
+    // columns make their entries irrelevant)
+    for (int r = j2 + tid; r < n; r += blockDim.x) {
+      double w[kNB], x[kNB];
+#pragma unroll
+      for (int q = 0; q < kNB; ++q) w[q] = K[cjq[q] + r];
+      lrow4(w, pv, x);
+#pragma unroll
+      for (int q = 0; q < kNB; ++q)
+        if (q < bs) K[cjq[q] + r] = x[q];
+    }
+    if (tid == blockDim.x - 1) diag_block(j, pv);
+    if (j2 >= n) break;
+    __syncthreads();
+    const long long tmid = S.prof ? clock64() : 0;
+    if (S.prof && tid == 0) atomicAdd(&g_qp_prof[14], (unsigned long long)(tmid - tstep));
+    const int bs2 = min(kNB, n - j2);
+    const int pe = j2 + bs2;  // next pivot block: rows/cols [j2, pe)
     if (wid == 0) {
       if (lane == 0) {  // look-ahead
         double La[kNB][kNB];
 #pragma unroll
         for (int a = 0; a < kNB; ++a) {
           const int r = min(j2 + a, n - 1);
-          double w[kNB];
 #pragma unroll
-          for (int q = 0; q < kNB; ++q) w[q] = K[cjq[q] + r];
-          lrow4(w, pv, La[a]);
+          for (int q = 0; q < kNB; ++q) La[a][q] = q < bs ? K[cjq[q] + r] : 0.0;
         }
         double E[kNB][kNB];
 #pragma unroll
@@ -319,79 +414,36 @@ __device__ bool chol_factor(Qs& S) {
           for (int b = 0; b < kNB; ++b) {
             if (a < bs2 && b <= a) {
               const int idx = colbase(j2 + b, n) + j2 + a;
-              const double e = K[idx] - fma(La[a][3], La[b][3], fma(La[a][2], La[b][2],
-                                        fma(La[a][1], La[b][1], La[a][0] * La[b][0])));
-              K[idx] = e;
-              E[a][b] = e;
+              E[a][b] = K[idx] - fma(La[a][3], La[b][3], fma(La[a][2], La[b][2],
+                                     fma(La[a][1], La[b][1], La[a][0] * La[b][0])));
             } else {
               E[a][b] = 0.0;
             }
           }
-        double* pn = S.pv + (buf ^ 1) * 16;
-        if (!factor_pivot(E, bs2, pn)) *S.flag = 1;
-        save_factor(j2, pn);
-        if (S.prof) atomicAdd(&g_qp_prof[12], (unsigned long long)(clock64() - tstep));
+        if (!factor_pivot(E, bs2, S.pv + (buf ^ 1) * 16)) *S.flag = 1;
+        if (S.prof) atomicAdd(&g_qp_prof[12], (unsigned long long)(clock64() - tmid));
       }
     } else {
-      // this lane's rows of the current block's L columns (rows >= pe only)
+      // this lane's rows of the block's L columns (rows >= pe only matter)
       double Lr[TM][kNB];
 #pragma unroll
       for (int t = 0; t < TM; ++t) {
         const int r = min(lane + 32 * t, n - 1);
-        double w[kNB];
 #pragma unroll
-        for (int q = 0; q < kNB; ++q) w[q] = K[cjq[q] + r];
-        lrow4(w, pv, Lr[t]);
+        for (int q = 0; q < kNB; ++q) Lr[t][q] = q < bs ? K[cjq[q] + r] : 0.0;
       }
       // column groups of 4 adjacent columns starting at j2, round-robin over warps
       constexpr int kU = kQpWarps - 1;
       for (int c0g = j2 + kNB * (wid - 1); c0g < n; c0g += kNB * kU)
-        update_group_dispatch<TM, 0>(c0g >> 5, K, n, c0g, pe, cjq, pv, Lr, lane);
+        update_group_dispatch<TM, 0>(max(c0g, pe) >> 5, K, n, c0g, pe, cjq, Lr, lane);
     }
-    if (S.prof && lane == 0 && (wid == 1 || wid == kQpWarps - 1))
-      atomicAdd(&g_qp_prof[wid == 1 ? 13 : 14], (unsigned long long)(clock64() - tstep));
+    if (S.prof && lane == 0 && wid == 1) atomicAdd(&g_qp_prof[13], (unsigned long long)(clock64() - tmid));
     buf ^= 1;
     __syncthreads();
     if (S.prof && tid == 0) atomicAdd(&g_qp_prof[15], (unsigned long long)(clock64() - tstep));
   }
-  if (*S.flag) return false;
-  // scale the panels into L: rows below each block, x = w F^{-T}; the
-  // diagonal block gets F itself
-  for (int j = kNB * wid; j < n; j += kNB * kQpWarps) {
-    double pvj[10];
-#pragma unroll
-    for (int q = 0; q < kNB; ++q) pvj[q] = j + q < n ? S.dinv[j + q] : 0.0;
-    pvj[4] = fl[j];
-    pvj[5] = j + 1 < n ? fl[j + 1] : 0.0;
-    pvj[6] = j + 2 < n ? fl[j + 2] : 0.0;
-    pvj[7] = j + 3 < n ? fl[j + 3] : 0.0;
-    pvj[8] = fl2[j];
-    pvj[9] = j + 1 < n ? fl2[j + 1] : 0.0;
-    const int bs = min(kNB, n - j);
-    int cq[kNB];
-#pragma unroll
-    for (int q = 0; q < kNB; ++q) cq[q] = q < bs ? colbase(j + q, n) : colbase(j, n);
-    for (int r = j + bs + lane; r < n; r += 32) {
-      double w[kNB], x[kNB];
-#pragma unroll
-      for (int q = 0; q < kNB; ++q) w[q] = q < bs ? K[cq[q] + r] : 0.0;
-      lrow4(w, pvj, x);
-#pragma unroll
-      for (int q = 0; q < kNB; ++q)
-        if (q < bs) K[cq[q] + r] = x[q];
-    }
-    if (lane == 0) {
-      const double* lv = pvj + 4;  // l10 l20 l21 l30 l31 l32
-      const int li[4][4] = {{-1, -1, -1, -1}, {0, -1, -1, -1}, {1, 2, -1, -1}, {3, 4, 5, -1}};
-#pragma unroll
-      for (int a = 0; a < kNB; ++a)
-#pragma unroll
-        for (int b = 0; b <= a; ++b)
-          if (a < bs) K[cq[b] + j + a] = a == b ? 1.0 / pvj[a] : lv[li[a][b]];
-    }
-  }
   __syncthreads();
-  return true;
+  return !*S.flag;
 }
 
 // Invert the 32x32 diagonal blocks of L: X_b = L_bb^{-1}, column-major with
@@ -400,7 +452,7 @@ __device__ bool chol_factor(Qs& S) {
 // L_bb (same for all lanes: broadcast loads, issued 4 at a time) against the
 // lane's own already-solved entries.
 __device__ void invert_diag_blocks(Qs& S) {
-  const int n = S.n, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int n = S.nf, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int b = wid; b < S.nblk; b += kQpWarps) {
     const int r0 = b * kTB, nb = min(kTB, n - r0);
     double* Xi = S.X + (size_t)b * kTB * kXL + lane * kXL;
@@ -438,7 +490,7 @@ __device__ void invert_diag_blocks(Qs& S) {
 // are shared n-vectors (x may alias b).  Call with all threads.
 template <int TM>
 __device__ void chol_solve(Qs& S, const double* b, double* x) {
-  const int n = S.n, lane = threadIdx.x & 31;
+  const int n = S.nf, lane = threadIdx.x & 31;
   const double* K = S.K;
   double* ys = S.ys;
   if (threadIdx.x < 32) {
@@ -524,15 +576,18 @@ __device__ void chol_solve(Qs& S, const double* b, double* x) {
 // QP building blocks
 // ---------------------------------------------------------------------------
 
-// out[c] = (C' tv)[c]
+// out = C' tv.  General rows are stored column-permuted: Cg[gi][k] is the
+// coefficient of kept variable kidx[k]; a row's eliminated variable (if any)
+// is (ge[gi], ga[gi]).
 __device__ void ct_apply(const Qs& S, const double* tv, double* out) {
-  for (int c = threadIdx.x; c < S.n; c += blockDim.x) {
+  for (int k = threadIdx.x; k < S.nf; k += blockDim.x) {
+    const int c = S.kidx[k];
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
       const int r = S.colrows[q];
       s0 = fma(S.rval[r], tv[r], s0);
     }
-    const double* cg = S.Cg + c;
+    const double* cg = S.Cg + k;
     int gi = 0;
     for (; gi + 3 < S.ng; gi += 4) {
       s0 = fma(cg[(int64_t)gi * S.n], tv[S.grow[gi]], s0);
@@ -542,6 +597,16 @@ __device__ void ct_apply(const Qs& S, const double* tv, double* out) {
     }
     for (; gi < S.ng; ++gi) s0 = fma(cg[(int64_t)gi * S.n], tv[S.grow[gi]], s0);
     out[c] = (s0 + s1) + (s2 + s3);
+  }
+  for (int e = threadIdx.x; e < S.ne; e += blockDim.x) {
+    const int c = S.eidx[e];
+    double s0 = 0.0;
+    for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
+      const int r = S.colrows[q];
+      s0 = fma(S.rval[r], tv[r], s0);
+    }
+    if (S.egi[e] >= 0) s0 = fma(S.ea[e], tv[S.grow[S.egi[e]]], s0);
+    out[c] = s0;
   }
 }
 
@@ -553,18 +618,21 @@ __device__ void c_apply(const Qs& S, const double* xv, double* out) {
   for (int gi = wid; gi < S.ng; gi += kQpWarps) {
     const double* row = S.Cg + (int64_t)gi * S.n;
     double s = 0.0;
-    for (int c = lane; c < S.n; c += 32) s = fma(row[c], xv[c], s);
+    for (int k = lane; k < S.nf; k += 32) s = fma(row[k], xv[S.kidx[k]], s);
     s = warp_sum(s);
-    if (lane == 0) out[S.grow[gi]] = s;
+    if (lane == 0) {
+      if (S.ge[gi] >= 0) s = fma(S.ga[gi], xv[S.eidx[S.ge[gi]]], s);
+      out[S.grow[gi]] = s;
+    }
   }
 }
 
-// hu = H u from the packed symmetric H: warp per pair of rows, every lane
-// issues all of its loads of H before the multiply-adds (H may be in L2).
+// hu = H u: packed H over the kept variables (warp per pair of rows, every
+// lane issues all of its loads first: H may be in L2) plus the diagonal of
+// the eliminated ones.
 template <int TM>
 __device__ void h_apply(const Qs& S, const double* uv, double* out) {
-  const int n = S.n, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int* cst = S.cstart;
+  const int n = S.nf, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int r0 = wid; r0 < n; r0 += 2 * kQpWarps) {
     const int r1 = r0 + kQpWarps;
     double h0[TM], h1[TM], uu[TM];
@@ -572,7 +640,7 @@ __device__ void h_apply(const Qs& S, const double* uv, double* out) {
     for (int t = 0; t < TM; ++t) {
       const int c = lane + 32 * t;
       const bool live = c < n;
-      uu[t] = live ? uv[c] : 0.0;
+      uu[t] = live ? uv[S.kidx[c]] : 0.0;
       h0[t] = live ? (c <= r0 ? S.Hp[colbase(c, n) + r0] : S.Hp[colbase(r0, n) + c]) : 0.0;
       h1[t] = (live && r1 < n) ? (c <= r1 ? S.Hp[colbase(c, n) + r1] : S.Hp[colbase(r1, n) + c]) : 0.0;
     }
@@ -585,19 +653,50 @@ __device__ void h_apply(const Qs& S, const double* uv, double* out) {
     s0 = warp_sum(s0);
     s1 = warp_sum(s1);
     if (lane == 0) {
-      out[r0] = s0;
-      if (r1 < n) out[r1] = s1;
+      out[S.kidx[r0]] = s0;
+      if (r1 < n) out[S.kidx[r1]] = s1;
     }
   }
+  for (int e = threadIdx.x; e < S.ne; e += blockDim.x) out[S.eidx[e]] = S.hde[e] * uv[S.eidx[e]];
 }
 
-// K = 2H + diag_add I + [diag(sum_single w val^2) + Cg' W Cg]   (qpsolver.py:178-184)
-// Lower triangle in 4x4 register tiles: tile (I, J), I >= J, covers rows
-// 4I..4I+3 and columns 4J..4J+3; its 16 entries of H are loaded first, then
-// the rank-ng update runs with 16 independent accumulators.
-__device__ void build_k(const Qs& S, double diag_add, bool terms) {
-  const int n = S.n, ng = terms ? S.ng : 0;
-  const int* cst = S.cstart;
+// K = 2H + diag_add I + diag(sum_single w val^2) + Cg' W Cg  (qpsolver.py:178-184)
+// on the reduced system: with an eliminated variable e in general row g,
+//   K_ee = 2 H_ee + diag_add + sum_single w val^2 + w_g a^2,
+//   K_red = K_kk - K_ke K_ee^{-1} K_ek  =  ... + w'_g Cg_g' Cg_g,
+//   w'_g = w_g - (w_g a)^2 / K_ee            (a rank-one change per such row).
+// Lower triangle of K_red in 4x4 register tiles: tile (I, J), I >= J, covers
+// rows 4I..4I+3 and columns 4J..4J+3; its 16 entries of H are loaded first,
+// then the rank-ng update runs with 16 independent accumulators.  Returns
+// false when an eliminated pivot K_ee is not positive (potrf's failure rule
+// applied to the eliminated block).
+__device__ bool build_k(const Qs& S, double diag_add, bool terms) {
+  const int n = S.nf, ng = terms ? S.ng : 0;
+  bool ok = true;
+  for (int e = threadIdx.x; e < S.ne; e += blockDim.x) {
+    const int c = S.eidx[e];
+    double dsum = 0.0;
+    if (terms)
+      for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
+        const int r = S.colrows[q];
+        dsum += S.w[r] * S.rval[r] * S.rval[r];
+      }
+    double kee = (2.0 * S.hde[e] + diag_add) + dsum;
+    if (terms && S.egi[e] >= 0) kee += S.w[S.grow[S.egi[e]]] * S.ea[e] * S.ea[e];
+    if (!(kee > 0.0)) ok = false;
+    S.kee[e] = kee;
+  }
+  __syncthreads();
+  for (int gi = threadIdx.x; gi < ng; gi += blockDim.x) {
+    const double wgi = S.w[S.grow[gi]];
+    double wr = wgi;
+    if (S.ge[gi] >= 0) {
+      const double t = wgi * S.ga[gi];
+      wr = wgi - t * t / S.kee[S.ge[gi]];
+    }
+    S.wg[gi] = wr;
+  }
+  __syncthreads();
   const int nq = (n + 3) >> 2;
   const int tiles = nq * (nq + 1) / 2;
   for (int tt = threadIdx.x; tt < tiles; tt += blockDim.x) {
@@ -620,12 +719,12 @@ __device__ void build_k(const Qs& S, double diag_add, bool terms) {
       }
     }
     for (int gi = 0; gi < ng; ++gi) {
-      const double* cg = S.Cg + (int64_t)gi * n;
-      const double wg = S.w[S.grow[gi]];
+      const double* cg = S.Cg + (int64_t)gi * S.n;
+      const double wgi = S.wg[gi];
       double x[4], y[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        x[a] = r0 + a < n ? cg[r0 + a] * wg : 0.0;
+        x[a] = r0 + a < n ? cg[r0 + a] * wgi : 0.0;
         y[a] = c0 + a < n ? cg[c0 + a] : 0.0;
       }
 #pragma unroll
@@ -650,22 +749,18 @@ __device__ void build_k(const Qs& S, double diag_add, bool terms) {
   // diagonal (holds only the general-row term so far): (2H + reg) +
   // bincount(single rows) first, then the general-row term, as the
   // reference orders it
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int c = S.kidx[k];
     double dsum = 0.0;
     if (terms)
       for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
         const int r = S.colrows[q];
         dsum += S.w[r] * S.rval[r] * S.rval[r];
       }
-    const int dc = colbase(c, n) + c;
+    const int dc = colbase(k, n) + k;
     S.K[dc] = ((2.0 * S.Hp[dc] + diag_add) + dsum) + S.K[dc];
   }
-  __syncthreads();
-}
-
-__device__ void add_diag(const Qs& S, double bump) {
-  for (int c = threadIdx.x; c < S.n; c += blockDim.x) S.K[colbase(c, S.n) + c] += bump;
-  __syncthreads();
+  return __syncthreads_and(ok ? 1 : 0) != 0;
 }
 
 // largest step in [0, 1] with x + a dx > 0 (qpsolver.py:238-243)
@@ -674,6 +769,51 @@ __device__ double max_step(const Qs& S, const double* x, const double* dx) {
   for (int r = threadIdx.x; r < S.m; r += blockDim.x)
     if (dx[r] < 0.0) a = fmin(a, -x[r] / dx[r]);
   return block_reduce<1>(a, S.red);
+}
+
+// x = K^{-1} b for the full Schur matrix through the reduced system:
+//   b_red = b_k - K_ke K_ee^{-1} b_e,  K_red x_k = b_red,
+//   x_e = (b_e - K_ek x_k) / K_ee,   K_ke = w_g a Cg_g (kept part).
+// Uses ytmp (reduced rhs / solution) and cf (per-row coefficients).
+template <int TM>
+__device__ void reduced_solve(Qs& S, const double* b, double* x) {
+  double* yr = S.ytmp;
+  double* coef = S.cf;
+  if (S.ne == 0) {
+    for (int k = threadIdx.x; k < S.nf; k += blockDim.x) yr[k] = b[S.kidx[k]];
+    __syncthreads();
+    chol_solve<TM>(S, yr, yr);
+    for (int k = threadIdx.x; k < S.nf; k += blockDim.x) x[S.kidx[k]] = yr[k];
+    __syncthreads();
+    return;
+  }
+  for (int gi = threadIdx.x; gi < S.ng; gi += blockDim.x) {
+    const int e = S.ge[gi];
+    coef[gi] = e >= 0 ? S.w[S.grow[gi]] * S.ga[gi] * b[S.eidx[e]] / S.kee[e] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < S.nf; k += blockDim.x) {
+    double s = b[S.kidx[k]];
+    for (int gi = 0; gi < S.ng; ++gi) s = fma(-coef[gi], S.Cg[(int64_t)gi * S.n + k], s);
+    yr[k] = s;
+  }
+  __syncthreads();
+  chol_solve<TM>(S, yr, yr);
+  for (int k = threadIdx.x; k < S.nf; k += blockDim.x) x[S.kidx[k]] = yr[k];
+  // eliminated: one warp per eliminated variable
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = wid; e < S.ne; e += kQpWarps) {
+    const int gi = S.egi[e];
+    double s = 0.0;
+    if (gi >= 0) {
+      const double* row = S.Cg + (int64_t)gi * S.n;
+      for (int k = lane; k < S.nf; k += 32) s = fma(row[k], yr[k], s);
+      s = warp_sum(s);
+      s *= S.w[S.grow[gi]] * S.ea[e];
+    }
+    if (lane == 0) x[S.eidx[e]] = (b[S.eidx[e]] - s) / S.kee[e];
+  }
+  __syncthreads();
 }
 
 // du, dlam, ds for complementarity target rcv (qpsolver.py:204-209)
@@ -687,7 +827,7 @@ __device__ void kkt_step(Qs& S, const double* rcv) {
   for (int c = threadIdx.x; c < S.n; c += blockDim.x) S.rhs[c] = -S.rd[c] - S.ctl[c];
   __syncthreads();
   qmark(S, 10);
-  chol_solve<TM>(S, S.rhs, S.du);
+  reduced_solve<TM>(S, S.rhs, S.du);
   qmark(S, 11);
   c_apply(S, S.du, S.t);  // C du
   __syncthreads();
@@ -765,6 +905,9 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.ctl = v; v += n;
     S.ytmp = v; v += n;
     S.dinv = v; v += n;
+    S.kee = v; v += n;
+    S.hde = v; v += n;
+    S.ea = v; v += n;
     S.d = v; v += m;
     S.s = v; v += m;
     S.lam = v; v += m;
@@ -776,13 +919,21 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.tmp = v; v += m;
     S.w = v; v += m;
     S.lb = v; v += m;
-    S.rval = v;
+    S.rval = v; v += m;
+    S.wg = v; v += m;
+    S.ga = v; v += m;
+    S.cf = v;
     int* ip = (int*)(smem + L0.o_ints);
     S.rcol = ip;
     S.grow = ip + m;
     S.colptr = ip + 2 * m;
     S.colrows = ip + 2 * m + n + 1;
     S.cstart = ip + 3 * m + n + 1;
+    S.kidx = ip + 3 * m + 2 * n + 2;
+    S.eidx = S.kidx + n;
+    S.egi = S.eidx + n;
+    S.ge = S.egi + n;
+    S.elig = S.ge + m;
     S.K = (double*)(smem + L0.o_k);
     S.X = (double*)(smem + L0.o_x);
   }
@@ -826,20 +977,83 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   }
   __syncthreads();
   S.ng = sh_int[0];
+  // ---- eliminable variables: diagonal-only Hessian row, at most one general
+  // row, and alone in that row (otherwise K_ee would not be diagonal)
+  for (int c = wid; c < n; c += kQpWarps) {
+    const double* Hr = H + (int64_t)c * n;
+    bool off = false;
+    for (int c2 = lane; c2 < n; c2 += 32) off |= (c2 != c && Hr[c2] != 0.0);
+    off = __any_sync(0xffffffffu, off);
+    if (lane == 0) S.elig[c] = (m > 0 && !off) ? 1 : 0;
+  }
+  __syncthreads();
+  for (int c = tid; c < n; c += nt) {
+    if (!S.elig[c]) { S.egi[c] = -1; continue; }
+    int cnt = 0, gs = -1;
+    for (int gi = 0; gi < S.ng; ++gi)
+      if (C[(int64_t)S.grow[gi] * n + c] != 0.0) { ++cnt; gs = gi; }
+    S.egi[c] = gs;  // temporarily indexed by column
+    if (cnt > 1) S.elig[c] = 0;
+  }
+  __syncthreads();
+  for (int gi = tid; gi < S.ng; gi += nt) {  // rows meeting several candidates keep them all
+    int cnt = 0;
+    for (int c = 0; c < n; ++c) cnt += (S.elig[c] && S.egi[c] == gi) ? 1 : 0;
+    S.ge[gi] = cnt;
+  }
+  __syncthreads();
+  for (int c = tid; c < n; c += nt)
+    if (S.elig[c] && S.egi[c] >= 0 && S.ge[S.egi[c]] > 1) S.elig[c] = 0;
+  __syncthreads();
+  if (tid == 0) {
+    int nf = 0, ne = 0;
+    for (int gi = 0; gi < S.ng; ++gi) S.ge[gi] = -1;
+    for (int c = 0; c < n; ++c) {
+      if (S.elig[c]) {
+        const int gs = S.egi[c];
+        S.eidx[ne] = c;
+        S.hde[ne] = H[(int64_t)c * n + c];
+        if (gs >= 0) {
+          const double a = C[(int64_t)S.grow[gs] * n + c];
+          S.ge[gs] = ne;
+          S.ga[gs] = a;
+          S.ea[ne] = a;
+        } else {
+          S.ea[ne] = 0.0;
+        }
+        S.elig[ne] = gs;  // egi by eliminated index, staged (egi is column-indexed here)
+        ++ne;
+      } else {
+        S.kidx[nf++] = c;
+      }
+    }
+    for (int e = 0; e < ne; ++e) S.egi[e] = S.elig[e];
+    sh_int[2] = nf;
+    sh_int[3] = ne;
+  }
+  __syncthreads();
+  S.nf = sh_int[2];
+  S.ne = sh_int[3];
+  S.nblk = (S.nf + kTB - 1) / kTB;
   {
-    const bool cg_smem = qp_layout(n, m, S.ng, false, true).total <= A.smem_bytes;
-    const bool h_smem = qp_layout(n, m, S.ng, true, cg_smem).total <= A.smem_bytes;
-    const QpLayout LY = qp_layout(n, m, S.ng, h_smem, cg_smem);
+    const bool cg_smem = qp_layout(n, m, S.ng, false, true, S.nf).total <= A.smem_bytes;
+    const bool h_smem = qp_layout(n, m, S.ng, true, cg_smem, S.nf).total <= A.smem_bytes;
+    const QpLayout LY = qp_layout(n, m, S.ng, h_smem, cg_smem, S.nf);
+    S.K = (double*)(smem + LY.o_k);
+    S.X = (double*)(smem + LY.o_x);
     S.Cg = cg_smem ? (double*)(smem + LY.o_cg) : gws + packed_size(n);
     S.Hp = h_smem ? (double*)(smem + LY.o_h) : gws;
   }
-  for (int t = tid; t < S.ng * n; t += nt) {
-    const int gi = t / n, c = t - gi * n;
-    S.Cg[t] = C[(int64_t)S.grow[gi] * n + c];
+  // general rows, column-permuted to the kept variables
+  for (int t = tid; t < S.ng * S.nf; t += nt) {
+    const int gi = t / S.nf, k = t - gi * S.nf;
+    S.Cg[(int64_t)gi * n + k] = C[(int64_t)S.grow[gi] * n + S.kidx[k]];
   }
-  // pack H's lower triangle: element (r, c <= r) from row r
-  for (int r = wid; r < n; r += kQpWarps)
-    for (int c = lane; c <= r; c += 32) S.Hp[colbase(c, n) + r] = H[(int64_t)r * n + c];
+  // pack H's lower triangle over the kept variables
+  for (int kr = wid; kr < S.nf; kr += kQpWarps) {
+    const double* Hr = H + (int64_t)S.kidx[kr] * n;
+    for (int kc = lane; kc <= kr; kc += 32) S.Hp[colbase(kc, S.nf) + kr] = Hr[S.kidx[kc]];
+  }
   for (int t = tid; t < n; t += nt) S.g[t] = A.g[bi * (int64_t)n + t];
   for (int t = tid; t < m; t += nt) S.d[t] = A.d[bi * (int64_t)m + t];
   __syncthreads();
@@ -945,17 +1159,15 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     // Schur matrix and Cholesky with escalating regularisation (qpsolver.py:178-198)
     for (int r = tid; r < m; r += nt) S.w[r] = S.lam[r] / S.s[r];
     __syncthreads();
-    build_k(S, reg, true);
+    bool ok = build_k(S, reg, true);
     qmark(S, 3);
-    bool ok = chol_factor<TM>(S);
+    ok = ok && chol_factor<TM>(S);
     qmark(S, 4);
     double boost = 0.0;
     for (int att = 1; att < 4 && !ok; ++att) {
       const double bump = boost == 0.0 ? fmax(reg * 1e3, 1e-12) : boost * 1e3;
       boost = bump;
-      build_k(S, reg, true);
-      add_diag(S, boost);
-      ok = chol_factor<TM>(S);
+      ok = build_k(S, reg + boost, true) && chol_factor<TM>(S);
     }
     if (!ok) {
       status = GM_QP_NUMERICAL_FAILURE;
@@ -1059,6 +1271,8 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_chol_check(int n, const doubl
   __shared__ int sh_int[4];
   Qs S;
   S.n = n;
+  S.nf = n;
+  S.ne = 0;
   S.m = 0;
   S.ng = 0;
   S.nblk = (n + kTB - 1) / kTB;
