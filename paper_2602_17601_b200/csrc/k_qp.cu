@@ -30,37 +30,44 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "qp_chol.cuh"
 
 namespace {
 
 constexpr int kQpThreads = 256;
 constexpr int kQpWarps = kQpThreads / 32;
 constexpr int kTB = 32;  // triangular-solve block
-constexpr int kXL = 33;  // leading dimension of an inverted diagonal block
 
 __host__ __device__ inline size_t qal(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline int64_t packed_size(int n) { return (int64_t)n * (n + 1) / 2; }
 
 struct QpLayout {
-  size_t o_vec, o_ints, o_k, o_x, o_h, o_cg, total;
+  size_t o_vec, o_ints, o_k, o_x, o_h, o_cg, o_gv, total;
 };
 
-// n-vectors: g u hu rd rhs du ub ctl ytmp dinv kee hde ea   (13)
-// m-vectors: d s lam cu rp t dl ds tmp w lb rval wg ga cf    (15)
-// nf: dimension of the factorised system (K, X and packed H), <= n
+// n-vectors: g u hu rd rhs du ub ctl ytmp kee hde ea          (12)
+// m-vectors: d s lam cu rp t dl ds tmp w lb rval              (12)
+// ng-vectors (after the row classification): wg ga cf         (3)
+// nf: dimension of the factorised system, <= n.  K: lower 8x8 tiles of the
+// padded Schur matrix (qp_chol.cuh); X region: inverted diagonal
+// superblocks, per-warp scratch tiles, 1/diag(L) and the padded solve vector.
+__host__ __device__ inline size_t xregion_doubles(int nf) {
+  return (size_t)qpchol::xinv_doubles(nf) + 64 * kQpWarps + 16 * (size_t)qpchol::tiles_for(nf);
+}
 __host__ __device__ inline QpLayout qp_layout(int n, int m, int ng, bool h_smem, bool cg_smem, int nf = -1) {
   QpLayout L{};
   if (nf < 0) nf = n;
-  const int nblk = (nf + kTB - 1) / kTB;
   size_t o = 0;
   L.o_vec = o;
-  o = qal(o + sizeof(double) * (13 * (size_t)n + 15 * (size_t)m + 64));
+  o = qal(o + sizeof(double) * (12 * (size_t)n + 12 * (size_t)m + 64));
   L.o_ints = o;  // rcol(m) grow(m) colptr(n+1) colrows(m) cstart(n+1) kidx(n) eidx(n) egi(n) ge(m) elig(n)
   o = qal(o + sizeof(int) * (4 * (size_t)m + 6 * (size_t)n + 2 + 8));
+  L.o_gv = o;
+  o = qal(o + sizeof(double) * 3 * (size_t)ng);
   L.o_k = o;
-  o = qal(o + sizeof(double) * packed_size(nf));
+  o = qal(o + sizeof(double) * (size_t)qpchol::tile_doubles(nf));
   L.o_x = o;
-  o = qal(o + sizeof(double) * (size_t)nblk * kTB * kXL);
+  o = qal(o + sizeof(double) * xregion_doubles(nf));
   L.o_cg = o;
   if (cg_smem) o = qal(o + sizeof(double) * (size_t)ng * n);
   L.o_h = o;
@@ -101,10 +108,10 @@ struct Qs {  // per-CTA views
   // kidx[0..nf) / eidx[0..ne) list kept / eliminated variables, egi[e] is the
   // general row of eliminated e (or -1) with coefficient ea[e], ge[gi] the
   // eliminated variable of general row gi (or -1) with coefficient ga[gi].
-  int n, m, ng, nblk, nf, ne;
+  int n, m, ng, nblk, nf, ne, T;
   int *kidx, *eidx, *egi, *ge, *elig;
   double *kee, *hde, *ea, *wg, *ga, *cf;
-  double *K, *X, *Hp, *Cg;
+  double *K, *X, *Hp, *Cg, *scr, *yv;
   double *g, *u, *hu, *rd, *rhs, *du, *ub, *ctl, *ytmp, *dinv;
   double *d, *s, *lam, *cu, *rp, *t, *dl, *ds, *tmp, *w, *lb, *rval;
   int *rcol, *grow, *colptr, *colrows, *cstart;
@@ -152,423 +159,34 @@ __device__ double block_reduce(double v, double* red) {
 }
 
 // ---------------------------------------------------------------------------
-// factorisation: block elimination with 2x2 pivots -> Cholesky factor L
+// factorisation and solves (qp_chol.cuh): tiled Cholesky of the reduced Schur
+// matrix, inverted 32x32 diagonal superblocks, superblock triangular solves
 // ---------------------------------------------------------------------------
-// Packed lower triangle, column-major: element (r, c), r >= c, at
-// colbase(c, n) + r with colbase = cstart[c] - c computed arithmetically
-// (an integer multiply-add instead of a dependent shared-memory load).
+// Packed lower triangle of H, column-major: element (r, c), r >= c, at
+// colbase(c, n) + r.
 __device__ __forceinline__ int colbase(int c, int n) { return c * n - ((c * (c + 1)) >> 1); }
 
-// Blocked right-looking Cholesky, kNB = 4 columns per step.
-//
-// Pivot block factor F (4x4 lower, scalar Cholesky formulas as LAPACK potf2):
-//   pv[0..3] = 1 / L[q][q],  pv[4..9] = l10 l20 l21 l30 l31 l32.
-// Row x of L in the block's columns from its Schur-complement row w:
-//   x = w F^{-T}  (forward substitution with F).
-constexpr int kNB = 4;
-
-__device__ __forceinline__ void lrow4(const double (&w)[kNB], const double* pv, double (&x)[kNB]) {
-  x[0] = w[0] * pv[0];
-  x[1] = fma(-pv[4], x[0], w[1]) * pv[1];
-  x[2] = fma(-pv[6], x[1], fma(-pv[5], x[0], w[2])) * pv[2];
-  x[3] = fma(-pv[9], x[2], fma(-pv[8], x[1], fma(-pv[7], x[0], w[3]))) * pv[3];
-}
-
-// Factor the (updated) bs x bs pivot block E (lower, E[a][b] a >= b) into pv.
-// Missing columns (bs < 4) get zero entries so lrow4 yields zeros for them.
-// Fails on a non-positive / NaN scalar pivot (potrf's rule).
-__device__ __forceinline__ bool factor_pivot(const double (&E)[kNB][kNB], int bs, double* pv) {
-  double i[kNB] = {0.0, 0.0, 0.0, 0.0}, l[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  bool ok = true;
-  if (!(E[0][0] > 0.0)) ok = false;
-  i[0] = rsqrt(E[0][0]);
-  if (bs > 1) {
-    l[0] = E[1][0] * i[0];
-    const double t1 = fma(-l[0], l[0], E[1][1]);
-    if (!(t1 > 0.0)) ok = false;
-    i[1] = rsqrt(t1);
-  }
-  if (bs > 2) {
-    l[1] = E[2][0] * i[0];
-    l[2] = fma(-l[1], l[0], E[2][1]) * i[1];
-    const double t2 = fma(-l[2], l[2], fma(-l[1], l[1], E[2][2]));
-    if (!(t2 > 0.0)) ok = false;
-    i[2] = rsqrt(t2);
-  }
-  if (bs > 3) {
-    l[3] = E[3][0] * i[0];
-    l[4] = fma(-l[3], l[0], E[3][1]) * i[1];
-    l[5] = fma(-l[4], l[2], fma(-l[3], l[1], E[3][2])) * i[2];
-    const double t3 = fma(-l[5], l[5], fma(-l[4], l[4], fma(-l[3], l[3], E[3][3])));
-    if (!(t3 > 0.0)) ok = false;
-    i[3] = rsqrt(t3);
-  }
-#pragma unroll
-  for (int q = 0; q < kNB; ++q) pv[q] = i[q];
-#pragma unroll
-  for (int q = 0; q < 6; ++q) pv[4 + q] = l[q];
+__device__ __forceinline__ bool chol_factor(Qs& S) {
+  if (S.T == 0) return true;  // every variable eliminated
+  if (threadIdx.x == 0) *S.flag = 0;
+  __syncthreads();
+  const bool ok = qpchol::factor<kQpThreads>(S.K, S.T, S.dinv, S.flag);
+  __syncthreads();
   return ok;
 }
 
-// Rank-4 update of one group of 4 adjacent columns [c0g, c0g+4) for the rows
-// this lane owns (lane + 32t): K[r][c] -= Lr[t] . Lc[u], with the pivot
-// block's L rows already in K (panel phase).  Row tiles t < T0 lie entirely
-// above the group and are not generated (T0 is a template parameter), so the
-// body is straight-line: all loads, then the FMAs, then predicated stores.
-// cjq[q] = colbase(j + q) (pivot column q; L[x][q] = K[cjq[q] + x]).
-template <int TM, int T0>
-__device__ __forceinline__ void update_group(double* K, int n, int c0g, int pe, const int (&cjq)[kNB],
-                                             const double (&Lr)[TM][kNB], int lane) {
-  double Lc[kNB][kNB];
-  double* col[kNB];
-#pragma unroll
-  for (int u = 0; u < kNB; ++u) {
-    const int c = min(c0g + u, n - 1);
-#pragma unroll
-    for (int q = 0; q < kNB; ++q) Lc[u][q] = K[cjq[q] + c];
-    col[u] = K + colbase(c, n);
-  }
-  double v[kNB][TM];
-#pragma unroll
-  for (int u = 0; u < kNB; ++u)
-#pragma unroll
-    for (int t = T0; t < TM; ++t) v[u][t] = col[u][min(lane + 32 * t, n - 1)];
-#pragma unroll
-  for (int u = 0; u < kNB; ++u) {
-    const int c = c0g + u;
-    const int rlo = c < pe ? pe : c;  // the next pivot block belongs to the look-ahead
-#pragma unroll
-    for (int t = T0; t < TM; ++t) {
-      const int r = lane + 32 * t;
-      const double nv = fma(-Lr[t][3], Lc[u][3],
-                            fma(-Lr[t][2], Lc[u][2],
-                                fma(-Lr[t][1], Lc[u][1], fma(-Lr[t][0], Lc[u][0], v[u][t]))));
-      if (c < n && r >= rlo && r < n) col[u][r] = nv;
-    }
-  }
+__device__ __forceinline__ void invert_diag_blocks(Qs& S) {
+  qpchol::invert_superblocks<kQpThreads>(S.K, S.T, S.dinv, S.X, S.scr);
 }
 
-template <int TM, int T0>
-__device__ __forceinline__ void update_group_dispatch(int t0, double* K, int n, int c0g, int pe,
-                                                      const int (&cjq)[kNB], const double (&Lr)[TM][kNB],
-                                                      int lane) {
-  if constexpr (T0 < TM - 1) {
-    if (t0 > T0) {
-      update_group_dispatch<TM, T0 + 1>(t0, K, n, c0g, pe, cjq, Lr, lane);
-      return;
-    }
-  }
-  update_group<TM, T0>(K, n, c0g, pe, cjq, Lr, lane);
-}
-
-// Rank-4 trailing update with the fp64 tensor cores: K[r][c] -= L[r][j..] .
-// L[c][j..] over 8x8 tiles (DMMA m8n8k4: D = A B + C with A = -L rows (8x4),
-// B = L cols' (4x8)), for every element with c >= j2, r >= c, r < n that is
-// not in the next pivot block [j2, pe)^2 (the look-ahead owns it).  Fragments
-// are loaded straight from the packed lower triangle; invalid slots load 0
-// and are not stored.  Tiles (R, C), C >= j2/8, R >= max(C, pe/8), are dealt
-// round-robin to warps w0, w0 + nw, ...; each warp runs 4 tiles at a time
-// (all loads, then 4 DMMAs, then the stores) for ILP.
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b, double c0, double c1) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
-               : "=d"(d0), "=d"(d1)
-               : "d"(a), "d"(b), "d"(c0), "d"(c1));
-}
-
-__device__ __forceinline__ void update_tiles(double* K, int n, int bs, int j2, int pe, const int (&cjq)[kNB],
-                                             int widx, int nw, int lane) {
-  const int T = (n + 7) >> 3;
-  const int rmin0 = pe >> 3;
-  const int i = lane >> 2, p = lane & 3;
-  const int cq = cjq[p];  // column base of pivot column j + p
-  const bool pl = p < bs;
-  int C = j2 >> 3, R = max(C, rmin0);
-  auto adv = [&](int k) {
-    R += k;
-    while (C < T && R >= T) {
-      const int over = R - T;
-      ++C;
-      R = max(C, rmin0) + over;
-    }
-  };
-  adv(widx);
-  while (C < T) {
-    int tr[4], tc[4];
-    int cnt = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      tr[u] = R;
-      tc[u] = C;
-      if (C < T) {
-        ++cnt;
-        adv(nw);
-      }
-    }
-    double a[4], b[4], c0[4], c1[4];
-    int o0[4], o1[4];
-    bool v0[4], v1[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const bool live = u < cnt;
-      const int ra = 8 * tr[u] + i, rb = 8 * tc[u] + i;
-      a[u] = (live && pl && ra < n) ? -K[cq + ra] : 0.0;
-      b[u] = (live && pl && rb < n) ? K[cq + rb] : 0.0;
-      const int cc = 8 * tc[u] + 2 * p;
-      const bool rin = live && ra < n;
-      v0[u] = rin && cc >= j2 && cc < n && ra >= cc && !(ra < pe && cc < pe);
-      v1[u] = rin && cc + 1 >= j2 && cc + 1 < n && ra >= cc + 1 && !(ra < pe && cc + 1 < pe);
-      o0[u] = colbase(cc, n) + ra;
-      o1[u] = colbase(cc + 1, n) + ra;
-      c0[u] = v0[u] ? K[o0[u]] : 0.0;
-      c1[u] = v1[u] ? K[o1[u]] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) dmma884(c0[u], c1[u], a[u], b[u], c0[u], c1[u]);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (v0[u]) K[o0[u]] = c0[u];
-      if (v1[u]) K[o1[u]] = c1[u];
-    }
-  }
-}
-
-// Factor K = L L' in place (packed lower); false on a failed pivot;
-// dinv[j] = 1/L[j][j].  Steps of kNB columns with the pivot block's factor
-// already known (look-ahead), two CTA barriers per step:
-//   panel:  all threads turn the block's Schur-complement rows below the
-//           pivot block into L rows (x = w F^{-T}) in place; thread 0 writes
-//           the pivot block's own L entries;
-//   update: warp 0 lane 0 updates and factors the NEXT 4x4 pivot block
-//           (the critical path: 4 rsqrt + short FMA chains) while warps 1..
-//           apply the rank-4 update to the trailing matrix in groups of 4
-//           adjacent columns, loading L instead of recomputing it.
-template <int TM>
-__device__ bool chol_factor(Qs& S) {
-  const int n = S.nf, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (n == 0) return true;  // every variable eliminated
-  double* K = S.K;
-  auto diag_block = [&](int jb, const double* pv) {  // L's pivot block from its factor
-    const int bs = min(kNB, n - jb);
-    const double* lv = pv + 4;  // l10 l20 l21 l30 l31 l32
-    const int li[4][4] = {{-1, -1, -1, -1}, {0, -1, -1, -1}, {1, 2, -1, -1}, {3, 4, 5, -1}};
-#pragma unroll
-    for (int q = 0; q < kNB; ++q)
-      if (q < bs) S.dinv[jb + q] = pv[q];
-#pragma unroll
-    for (int a = 0; a < kNB; ++a)
-#pragma unroll
-      for (int b = 0; b <= a; ++b)
-        if (a < bs) K[colbase(jb + b, n) + jb + a] = a == b ? 1.0 / pv[a] : lv[li[a][b]];
-  };
-  if (tid == 0) {
-    const int bs = min(kNB, n);
-    double E[kNB][kNB];
-#pragma unroll
-    for (int a = 0; a < kNB; ++a)
-#pragma unroll
-      for (int b = 0; b < kNB; ++b) E[a][b] = (a < bs && b <= a) ? K[colbase(b, n) + a] : 0.0;
-    *S.flag = factor_pivot(E, bs, S.pv) ? 0 : 1;
-  }
-  __syncthreads();
-  int buf = 0;
-  for (int j = 0; j < n; j += kNB) {
-    if (*S.flag) return false;  // uniform: read after the barrier
-    const int bs = min(kNB, n - j);
-    const int j2 = j + bs;
-    const double* pv = S.pv + buf * 16;
-    const long long tstep = S.prof ? clock64() : 0;
-    int cjq[kNB];
-#pragma unroll
-    for (int q = 0; q < kNB; ++q) cjq[q] = j + q < j2 ? colbase(j + q, n) : colbase(j, n);
-    // panel: L rows below the pivot block (zero weights for missing pivot
-    // columns make their entries irrelevant)
-    for (int r = j2 + tid; r < n; r += blockDim.x) {
-      double w[kNB], x[kNB];
-#pragma unroll
-      for (int q = 0; q < kNB; ++q) w[q] = K[cjq[q] + r];
-      lrow4(w, pv, x);
-#pragma unroll
-      for (int q = 0; q < kNB; ++q)
-        if (q < bs) K[cjq[q] + r] = x[q];
-    }
-    if (tid == blockDim.x - 1) diag_block(j, pv);
-    if (j2 >= n) break;
-    __syncthreads();
-    const long long tmid = S.prof ? clock64() : 0;
-    if (S.prof && tid == 0) atomicAdd(&g_qp_prof[14], (unsigned long long)(tmid - tstep));
-    const int bs2 = min(kNB, n - j2);
-    const int pe = j2 + bs2;  // next pivot block: rows/cols [j2, pe)
-    if (wid == 0) {
-      if (lane == 0) {  // look-ahead
-        double La[kNB][kNB];
-#pragma unroll
-        for (int a = 0; a < kNB; ++a) {
-          const int r = min(j2 + a, n - 1);
-#pragma unroll
-          for (int q = 0; q < kNB; ++q) La[a][q] = q < bs ? K[cjq[q] + r] : 0.0;
-        }
-        double E[kNB][kNB];
-#pragma unroll
-        for (int a = 0; a < kNB; ++a)
-#pragma unroll
-          for (int b = 0; b < kNB; ++b) {
-            if (a < bs2 && b <= a) {
-              const int idx = colbase(j2 + b, n) + j2 + a;
-              E[a][b] = K[idx] - fma(La[a][3], La[b][3], fma(La[a][2], La[b][2],
-                                     fma(La[a][1], La[b][1], La[a][0] * La[b][0])));
-            } else {
-              E[a][b] = 0.0;
-            }
-          }
-        if (!factor_pivot(E, bs2, S.pv + (buf ^ 1) * 16)) *S.flag = 1;
-        if (S.prof) atomicAdd(&g_qp_prof[12], (unsigned long long)(clock64() - tmid));
-      }
-    } else {
-      // this lane's rows of the block's L columns (rows >= pe only matter)
-      double Lr[TM][kNB];
-#pragma unroll
-      for (int t = 0; t < TM; ++t) {
-        const int r = min(lane + 32 * t, n - 1);
-#pragma unroll
-        for (int q = 0; q < kNB; ++q) Lr[t][q] = q < bs ? K[cjq[q] + r] : 0.0;
-      }
-      // column groups of 4 adjacent columns starting at j2, round-robin over warps
-      constexpr int kU = kQpWarps - 1;
-      for (int c0g = j2 + kNB * (wid - 1); c0g < n; c0g += kNB * kU)
-        update_group_dispatch<TM, 0>(max(c0g, pe) >> 5, K, n, c0g, pe, cjq, Lr, lane);
-    }
-    if (S.prof && lane == 0 && wid == 1) atomicAdd(&g_qp_prof[13], (unsigned long long)(clock64() - tmid));
-    buf ^= 1;
-    __syncthreads();
-    if (S.prof && tid == 0) atomicAdd(&g_qp_prof[15], (unsigned long long)(clock64() - tstep));
-  }
-  __syncthreads();
-  return !*S.flag;
-}
-
-// Invert the 32x32 diagonal blocks of L: X_b = L_bb^{-1}, column-major with
-// leading dimension kXL (X[k][i] at i*kXL + k).  Warp b inverts block b,
-// lane i computes column i by forward substitution: row r needs the row r of
-// L_bb (same for all lanes: broadcast loads, issued 4 at a time) against the
-// lane's own already-solved entries.
-__device__ void invert_diag_blocks(Qs& S) {
-  const int n = S.nf, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int b = wid; b < S.nblk; b += kQpWarps) {
-    const int r0 = b * kTB, nb = min(kTB, n - r0);
-    double* Xi = S.X + (size_t)b * kTB * kXL + lane * kXL;
-    const int i = lane;
-#pragma unroll 8
-    for (int k = 0; k < kTB; ++k) Xi[k] = 0.0;
-    if (i < nb) Xi[i] = S.dinv[r0 + i];
-    const int cb0 = colbase(r0, n);
-    for (int r = 1; r < nb; ++r) {
-      // s = sum_{k<r} L[r0+r][r0+k] X[k][i]; X[k][i] = 0 for k < i and for
-      // k >= r (not yet solved), so the 4-wide tail needs no guard (the
-      // packed entries it touches are finite)
-      const int rr = r0 + r;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int base = cb0 + rr;  // colbase(r0 + k) + rr, advanced incrementally
-      for (int k = 0; k < r; k += 4) {
-        const int b1 = base + (n - (r0 + k) - 1);
-        const int b2 = b1 + (n - (r0 + k) - 2);
-        const int b3 = b2 + (n - (r0 + k) - 3);
-        s0 = fma(S.K[base], Xi[k], s0);
-        s1 = fma(S.K[b1], Xi[k + 1], s1);
-        s2 = fma(S.K[b2], Xi[k + 2], s2);
-        s3 = fma(S.K[b3], Xi[k + 3], s3);
-        base = b3 + (n - (r0 + k) - 4);
-      }
-      if (i < r && i < nb) Xi[r] = -((s0 + s1) + (s2 + s3)) * S.dinv[rr];
-    }
-  }
-}
-
-// x = K^{-1} b by warp 0 (the solves are short dependent chains; one warp
-// avoids CTA barriers).  Lanes own rows lane + 32t; diagonal blocks are
-// applied through their inverses, off-diagonal blocks as mat-vecs; the block
-// solution is staged in shared memory (S.ys) for broadcast reads.  b and x
-// are shared n-vectors (x may alias b).  Call with all threads.
-template <int TM>
+// x = K^{-1} b through the padded solve vector S.yv (padding stays zero);
+// b and x are shared nf-vectors (x may alias b).  Call with all threads.
 __device__ void chol_solve(Qs& S, const double* b, double* x) {
-  const int n = S.nf, lane = threadIdx.x & 31;
-  const double* K = S.K;
-  double* ys = S.ys;
-  if (threadIdx.x < 32) {
-    double y[TM];
-#pragma unroll
-    for (int t = 0; t < TM; ++t) {
-      const int r = lane + 32 * t;
-      y[t] = r < n ? b[r] : 0.0;
-    }
-    // forward: L y = b
-#pragma unroll
-    for (int blk = 0; blk < TM; ++blk) {
-      if (blk < S.nblk) {
-        const int r0 = blk * kTB, nb = min(kTB, n - r0);
-        const double* X = S.X + (size_t)blk * kTB * kXL;
-        ys[lane] = y[blk];
-        __syncwarp();
-        double a[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < kTB; ++k) a[k & 3] = fma(X[k * kXL + lane], ys[k], a[k & 3]);
-        const double yb = lane < nb ? (a[0] + a[1]) + (a[2] + a[3]) : 0.0;
-        y[blk] = yb;
-        __syncwarp();
-        ys[lane] = yb;
-        __syncwarp();
-#pragma unroll
-        for (int t = blk + 1; t < TM; ++t) {
-          const int r = lane + 32 * t;  // only full blocks have rows below
-          if (r < n) {
-            double c[4] = {0.0, 0.0, 0.0, 0.0};
-            int base = colbase(r0, n) + r;  // colbase(r0 + k) + r
-#pragma unroll
-            for (int k = 0; k < kTB; ++k) {
-              c[k & 3] = fma(K[base], ys[k], c[k & 3]);
-              base += n - (r0 + k) - 1;
-            }
-            y[t] -= (c[0] + c[1]) + (c[2] + c[3]);
-          }
-        }
-        __syncwarp();
-      }
-    }
-    // backward: L' x = y
-#pragma unroll
-    for (int blk = TM - 1; blk >= 0; --blk) {
-      if (blk < S.nblk) {
-        const int r0 = blk * kTB, nb = min(kTB, n - r0);
-        const double* X = S.X + (size_t)blk * kTB * kXL;
-        ys[lane] = y[blk];
-        __syncwarp();
-        const double* Xl = X + lane * kXL;  // X[k][lane], zero for k < lane
-        double a[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < kTB; ++k) a[k & 3] = fma(Xl[k], ys[k], a[k & 3]);
-        const double xb = lane < nb ? (a[0] + a[1]) + (a[2] + a[3]) : 0.0;
-        y[blk] = xb;
-        __syncwarp();
-        ys[lane] = xb;
-        __syncwarp();
-#pragma unroll
-        for (int t = 0; t < blk; ++t) {
-          const int r = lane + 32 * t;  // r < r0 <= n
-          const double* col = K + colbase(r, n) + r0;  // L[r0+k][r]
-          double c[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-          for (int k = 0; k < kTB; ++k)
-            if (k < nb) c[k & 3] = fma(col[k], ys[k], c[k & 3]);
-          y[t] -= (c[0] + c[1]) + (c[2] + c[3]);
-        }
-        __syncwarp();
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < TM; ++t) {
-      const int r = lane + 32 * t;
-      if (r < n) x[r] = y[t];
-    }
-  }
+  for (int r = threadIdx.x; r < S.nf; r += blockDim.x) S.yv[r] = b[r];
+  __syncthreads();
+  qpchol::solve_fwd<kQpThreads>(S.K, S.T, S.X, S.yv, nullptr);
+  qpchol::solve_bwd<kQpThreads>(S.K, S.T, S.X, S.yv);
+  for (int r = threadIdx.x; r < S.nf; r += blockDim.x) x[r] = S.yv[r];
   __syncthreads();
 }
 
@@ -630,11 +248,11 @@ __device__ void c_apply(const Qs& S, const double* xv, double* out) {
 // hu = H u: packed H over the kept variables (warp per pair of rows, every
 // lane issues all of its loads first: H may be in L2) plus the diagonal of
 // the eliminated ones.
-template <int TM>
 __device__ void h_apply(const Qs& S, const double* uv, double* out) {
   const int n = S.nf, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int r0 = wid; r0 < n; r0 += 2 * kQpWarps) {
     const int r1 = r0 + kQpWarps;
+    constexpr int TM = 8;  // n <= 256
     double h0[TM], h1[TM], uu[TM];
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
@@ -736,12 +354,11 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
     for (int b = 0; b < 4; ++b) {
       const int c = c0 + b;
       if (c >= n) continue;
-      double* col = S.K + colbase(c, n);
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int r = r0 + a;
         if (r < c || r >= n) continue;
-        col[r] = acc[a][b];
+        S.K[qpchol::gel(r, c)] = acc[a][b];
       }
     }
   }
@@ -757,9 +374,12 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
         const int r = S.colrows[q];
         dsum += S.w[r] * S.rval[r] * S.rval[r];
       }
-    const int dc = colbase(k, n) + k;
-    S.K[dc] = ((2.0 * S.Hp[dc] + diag_add) + dsum) + S.K[dc];
+    const int dc = qpchol::gel(k, k);
+    S.K[dc] = ((2.0 * S.Hp[colbase(k, n) + k] + diag_add) + dsum) + S.K[dc];
   }
+  // identity padding up to the tile size (last tile row)
+  for (int r = n + threadIdx.x / 8; r < 8 * S.T; r += blockDim.x / 8)
+    for (int c = (threadIdx.x & 7); c <= r; c += 8) S.K[qpchol::gel(r, c)] = r == c ? 1.0 : 0.0;
   return __syncthreads_and(ok ? 1 : 0) != 0;
 }
 
@@ -775,14 +395,13 @@ __device__ double max_step(const Qs& S, const double* x, const double* dx) {
 //   b_red = b_k - K_ke K_ee^{-1} b_e,  K_red x_k = b_red,
 //   x_e = (b_e - K_ek x_k) / K_ee,   K_ke = w_g a Cg_g (kept part).
 // Uses ytmp (reduced rhs / solution) and cf (per-row coefficients).
-template <int TM>
 __device__ void reduced_solve(Qs& S, const double* b, double* x) {
   double* yr = S.ytmp;
   double* coef = S.cf;
   if (S.ne == 0) {
     for (int k = threadIdx.x; k < S.nf; k += blockDim.x) yr[k] = b[S.kidx[k]];
     __syncthreads();
-    chol_solve<TM>(S, yr, yr);
+    chol_solve(S, yr, yr);
     for (int k = threadIdx.x; k < S.nf; k += blockDim.x) x[S.kidx[k]] = yr[k];
     __syncthreads();
     return;
@@ -798,7 +417,7 @@ __device__ void reduced_solve(Qs& S, const double* b, double* x) {
     yr[k] = s;
   }
   __syncthreads();
-  chol_solve<TM>(S, yr, yr);
+  chol_solve(S, yr, yr);
   for (int k = threadIdx.x; k < S.nf; k += blockDim.x) x[S.kidx[k]] = yr[k];
   // eliminated: one warp per eliminated variable
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -817,7 +436,6 @@ __device__ void reduced_solve(Qs& S, const double* b, double* x) {
 }
 
 // du, dlam, ds for complementarity target rcv (qpsolver.py:204-209)
-template <int TM>
 __device__ void kkt_step(Qs& S, const double* rcv) {
   for (int r = threadIdx.x; r < S.m; r += blockDim.x)
     S.t[r] = (rcv[r] + S.lam[r] * S.rp[r]) / S.s[r];
@@ -827,7 +445,7 @@ __device__ void kkt_step(Qs& S, const double* rcv) {
   for (int c = threadIdx.x; c < S.n; c += blockDim.x) S.rhs[c] = -S.rd[c] - S.ctl[c];
   __syncthreads();
   qmark(S, 10);
-  reduced_solve<TM>(S, S.rhs, S.du);
+  reduced_solve(S, S.rhs, S.du);
   qmark(S, 11);
   c_apply(S, S.du, S.t);  // C du
   __syncthreads();
@@ -844,9 +462,8 @@ struct Resid {
 };
 
 // residuals at (u, lam) (qpsolver.py:90-97); leaves r_dual in rd, C u in cu
-template <int TM>
 __device__ Resid residuals(Qs& S) {
-  h_apply<TM>(S, S.u, S.hu);
+  h_apply(S, S.u, S.hu);
   ct_apply(S, S.lam, S.ctl);
   c_apply(S, S.u, S.cu);
   __syncthreads();
@@ -868,7 +485,6 @@ __device__ Resid residuals(Qs& S) {
   return R;
 }
 
-template <int TM>
 __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[kQpWarps];
@@ -904,7 +520,6 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.ub = v; v += n;
     S.ctl = v; v += n;
     S.ytmp = v; v += n;
-    S.dinv = v; v += n;
     S.kee = v; v += n;
     S.hde = v; v += n;
     S.ea = v; v += n;
@@ -919,10 +534,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.tmp = v; v += m;
     S.w = v; v += m;
     S.lb = v; v += m;
-    S.rval = v; v += m;
-    S.wg = v; v += m;
-    S.ga = v; v += m;
-    S.cf = v;
+    S.rval = v;
     int* ip = (int*)(smem + L0.o_ints);
     S.rcol = ip;
     S.grow = ip + m;
@@ -977,6 +589,12 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   }
   __syncthreads();
   S.ng = sh_int[0];
+  {
+    double* gv = (double*)(smem + qp_layout(n, m, S.ng, false, false).o_gv);
+    S.wg = gv;
+    S.ga = gv + S.ng;
+    S.cf = gv + 2 * S.ng;
+  }
   // ---- eliminable variables: diagonal-only Hessian row, at most one general
   // row, and alone in that row (otherwise K_ee would not be diagonal)
   for (int c = wid; c < n; c += kQpWarps) {
@@ -1041,9 +659,14 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     const QpLayout LY = qp_layout(n, m, S.ng, h_smem, cg_smem, S.nf);
     S.K = (double*)(smem + LY.o_k);
     S.X = (double*)(smem + LY.o_x);
+    S.T = qpchol::tiles_for(S.nf);
+    S.scr = S.X + qpchol::xinv_doubles(S.nf);
+    S.dinv = S.scr + 64 * kQpWarps;
+    S.yv = S.dinv + 8 * S.T;
     S.Cg = cg_smem ? (double*)(smem + LY.o_cg) : gws + packed_size(n);
     S.Hp = h_smem ? (double*)(smem + LY.o_h) : gws;
   }
+  for (int t = tid; t < 8 * S.T; t += nt) S.yv[t] = 0.0;
   // general rows, column-permuted to the kept variables
   for (int t = tid; t < S.ng * S.nf; t += nt) {
     const int gi = t / S.nf, k = t - gi * S.nf;
@@ -1078,7 +701,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     for (int t = 0; t < 4 && !ok; ++t) {
       const double boost = t == 0 ? 0.0 : (t == 1 ? reg : (t == 2 ? reg * 1e3 : reg * 1e6));
       build_k(S, boost, false);
-      ok = chol_factor<TM>(S);
+      ok = chol_factor(S);
     }
     if (!ok) {
       for (int t = tid; t < n; t += nt) uo[t] = 0.0;
@@ -1092,8 +715,8 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     invert_diag_blocks(S);
     for (int t = tid; t < n; t += nt) S.rhs[t] = -S.g[t];
     __syncthreads();
-    chol_solve<TM>(S, S.rhs, S.u);
-    h_apply<TM>(S, S.u, S.hu);
+    chol_solve(S, S.rhs, S.u);
+    h_apply(S, S.u, S.hu);
     __syncthreads();
     double rs = 0.0;
     for (int c = tid; c < n; c += nt) rs = fmax(rs, fabs(2.0 * S.hu[c] + S.g[c]));
@@ -1127,7 +750,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
 
   qmark(S, 0);
   for (int it = 0; it < A.max_it; ++it) {
-    const Resid R = residuals<TM>(S);
+    const Resid R = residuals(S);
     qmark(S, 1);
     const double metric = fmax(fmax(R.rs / scale_g, R.rp), R.rc / fmax(comp_ref, 1e-300));
     if (metric < best_metric) {  // record_best (qpsolver.py:158-165)
@@ -1161,13 +784,13 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     __syncthreads();
     bool ok = build_k(S, reg, true);
     qmark(S, 3);
-    ok = ok && chol_factor<TM>(S);
+    ok = ok && chol_factor(S);
     qmark(S, 4);
     double boost = 0.0;
     for (int att = 1; att < 4 && !ok; ++att) {
       const double bump = boost == 0.0 ? fmax(reg * 1e3, 1e-12) : boost * 1e3;
       boost = bump;
-      ok = build_k(S, reg + boost, true) && chol_factor<TM>(S);
+      ok = build_k(S, reg + boost, true) && chol_factor(S);
     }
     if (!ok) {
       status = GM_QP_NUMERICAL_FAILURE;
@@ -1189,7 +812,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     for (int r = tid; r < m; r += nt) S.tmp[r] = -S.lam[r] * S.s[r];
     __syncthreads();
     qmark(S, 6);
-    kkt_step<TM>(S, S.tmp);
+    kkt_step(S, S.tmp);
     qmark(S, 7);
     const double ap = max_step(S, S.s, S.ds);
     const double ad = max_step(S, S.lam, S.dl);
@@ -1201,7 +824,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     for (int r = tid; r < m; r += nt) S.tmp[r] = -S.lam[r] * S.s[r] - S.dl[r] * S.ds[r] + sigma * mu;
     __syncthreads();
     qmark(S, 8);
-    kkt_step<TM>(S, S.tmp);
+    kkt_step(S, S.tmp);
     qmark(S, 7);
     const double alpha = fmin(tau * max_step(S, S.s, S.ds), tau * max_step(S, S.lam, S.dl));
     bool finite = true;
@@ -1224,7 +847,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     }
   }
   if (status < 0) {  // iteration cap (qpsolver.py:231-235)
-    const Resid R = residuals<TM>(S);
+    const Resid R = residuals(S);
     const double metric = fmax(fmax(R.rs / scale_g, R.rp), R.rc / fmax(comp_ref, 1e-300));
     if (metric < best_metric) {
       best_metric = metric;
@@ -1261,13 +884,9 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
 
 // Diagnostic kernel: factor a dense SPD A (n x n) with the solver's own
 // chol_factor / invert_diag_blocks / chol_solve and return L and A^{-1} b.
-template <int TM>
 __global__ void __launch_bounds__(kQpThreads, 1) k_chol_check(int n, const double* A, const double* b,
                                                                double* L, double* x, int* ok) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[kQpWarps];
-  __shared__ double pvbuf[32];
-  __shared__ double ysbuf[kTB];
   __shared__ int sh_int[4];
   Qs S;
   S.n = n;
@@ -1275,33 +894,36 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_chol_check(int n, const doubl
   S.ne = 0;
   S.m = 0;
   S.ng = 0;
-  S.nblk = (n + kTB - 1) / kTB;
-  S.red = red;
-  S.pv = pvbuf;
-  S.ys = ysbuf;
+  S.T = qpchol::tiles_for(n);
   S.flag = &sh_int[1];
   S.prof = false;
   const QpLayout L0 = qp_layout(n, 0, 0, false, false);
   double* v = (double*)(smem + L0.o_vec);
   S.rhs = v;
   S.du = v + n;
-  S.ctl = v + 2 * n;
-  S.ytmp = v + 3 * n;
-  S.dinv = v + 4 * n;
   S.K = (double*)(smem + L0.o_k);
   S.X = (double*)(smem + L0.o_x);
-  for (int c = threadIdx.x; c < n; c += blockDim.x)
-    for (int r = c; r < n; ++r) S.K[colbase(c, n) + r] = A[(int64_t)r * n + c];
+  S.scr = S.X + qpchol::xinv_doubles(n);
+  S.dinv = S.scr + 64 * kQpWarps;
+  S.yv = S.dinv + 8 * S.T;
+  for (int t = threadIdx.x; t < 8 * S.T; t += blockDim.x) S.yv[t] = 0.0;
+  for (int e = threadIdx.x; e < 64 * S.T * S.T; e += blockDim.x) {
+    const int r = e / (8 * S.T), c = e - r * (8 * S.T);
+    if (c > r) continue;
+    S.K[qpchol::gel(r, c)] = (r < n && c < n) ? A[(int64_t)r * n + c] : (r == c ? 1.0 : 0.0);
+  }
   for (int r = threadIdx.x; r < n; r += blockDim.x) S.rhs[r] = b[r];
   __syncthreads();
-  const bool good = chol_factor<TM>(S);
+  const bool good = chol_factor(S);
   if (threadIdx.x == 0) *ok = good ? 1 : 0;
   if (!good) return;
   invert_diag_blocks(S);
   __syncthreads();
-  for (int c = threadIdx.x; c < n; c += blockDim.x)
-    for (int r = 0; r < n; ++r) L[(int64_t)r * n + c] = r >= c ? S.K[colbase(c, n) + r] : 0.0;
-  chol_solve<TM>(S, S.rhs, S.du);
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int r = e / n, c = e - r * n;
+    L[e] = r >= c ? S.K[qpchol::gel(r, c)] : 0.0;
+  }
+  chol_solve(S, S.rhs, S.du);
   for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = S.du[r];
 }
 
@@ -1313,17 +935,11 @@ extern "C" int gm_chol_check(gm_ctx* ctx, int n, const double* A, const double* 
   if (rc) return rc;
   if (n < 1 || n > 256) return gm_fail(ctx, GM_ERR_CONFIG, "n must be in [1, 256]");
   const size_t sm = qp_layout(n, 0, 0, false, false).total;
-  const int tm = (n + 31) / 32;
-  auto launch = [&](auto kern) -> int {
-    GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    kern<<<1, kQpThreads, sm, (cudaStream_t)stream>>>(n, A, b, L, x, ok);
-    GM_LAUNCH_CHECK(ctx, "k_chol_check");
-    return GM_OK;
-  };
-  if (tm <= 2) return launch(k_chol_check<2>);
-  if (tm <= 4) return launch(k_chol_check<4>);
-  if (tm <= 5) return launch(k_chol_check<5>);
-  return launch(k_chol_check<8>);
+  if (sm > ctx->smem_optin) return gm_fail(ctx, GM_ERR_CONFIG, "matrix too large for the on-chip factorisation");
+  GM_CUDA(ctx, cudaFuncSetAttribute(k_chol_check, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_chol_check<<<1, kQpThreads, sm, (cudaStream_t)stream>>>(n, A, b, L, x, ok);
+  GM_LAUNCH_CHECK(ctx, "k_chol_check");
+  return GM_OK;
 }
 
 extern "C" int gm_qp_profile(int on) {
@@ -1379,16 +995,9 @@ extern "C" int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, co
   a.resid = resid;
   a.gws = gws;
   a.gws_stride = gws_stride;
-  const int tm = (n + 31) / 32;
-  auto launch = [&](auto kern) -> int {
-    GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
-    kern<<<B, kQpThreads, smem_bytes, (cudaStream_t)stream>>>(a);
-    GM_LAUNCH_CHECK(ctx, "k_solve_qp");
-    return GM_OK;
-  };
-  if (tm <= 2) return launch(k_solve_qp<2>);
-  if (tm <= 4) return launch(k_solve_qp<4>);
-  if (tm <= 5) return launch(k_solve_qp<5>);
-  if (tm <= 8) return launch(k_solve_qp<8>);
-  return gm_fail(ctx, GM_ERR_CONFIG, "QP with n > 256 variables is not supported by this build");
+  if (n > 256) return gm_fail(ctx, GM_ERR_CONFIG, "QP with n > 256 variables is not supported by this build");
+  GM_CUDA(ctx, cudaFuncSetAttribute(k_solve_qp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+  k_solve_qp<<<B, kQpThreads, smem_bytes, (cudaStream_t)stream>>>(a);
+  GM_LAUNCH_CHECK(ctx, "k_solve_qp");
+  return GM_OK;
 }
