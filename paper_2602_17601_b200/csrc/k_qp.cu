@@ -245,37 +245,73 @@ __device__ void c_apply(const Qs& S, const double* xv, double* out) {
   }
 }
 
-// hu = H u: packed H over the kept variables (warp per pair of rows, every
-// lane issues all of its loads first: H may be in L2) plus the diagonal of
-// the eliminated ones.
+// hu = H u over the kept variables (packed lower H, column major) plus the
+// diagonal of the eliminated ones.  One pass over the columns serves both
+// triangles: warp w takes columns c = w, w + NW, ...; lane-rows r >= c
+// (contiguous, conflict free) accumulate H[r][c] u_c into per-lane row
+// partials (lower part) and H[r][c] u_r into the column's sum (upper part,
+// r > c), 4 columns in flight so their warp reductions overlap.  Row
+// partials of the warps meet in the (free at this point) K tile region and
+// are added in a fixed order.  Call with all threads; out is complete after
+// the call's final barrier.
 __device__ void h_apply(const Qs& S, const double* uv, double* out) {
+  constexpr int TM = 8;  // n <= 256
   const int n = S.nf, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int r0 = wid; r0 < n; r0 += 2 * kQpWarps) {
-    const int r1 = r0 + kQpWarps;
-    constexpr int TM = 8;  // n <= 256
-    double h0[TM], h1[TM], uu[TM];
+  double* part = S.K;                      // NW x n row partials
+  double* colsum = S.K + kQpWarps * n;     // n upper-part sums
+  double uk[TM], acc[TM];
 #pragma unroll
-    for (int t = 0; t < TM; ++t) {
-      const int c = lane + 32 * t;
-      const bool live = c < n;
-      uu[t] = live ? uv[S.kidx[c]] : 0.0;
-      h0[t] = live ? (c <= r0 ? S.Hp[colbase(c, n) + r0] : S.Hp[colbase(r0, n) + c]) : 0.0;
-      h1[t] = (live && r1 < n) ? (c <= r1 ? S.Hp[colbase(c, n) + r1] : S.Hp[colbase(r1, n) + c]) : 0.0;
-    }
-    double s0 = 0.0, s1 = 0.0;
+  for (int t = 0; t < TM; ++t) {
+    const int r = lane + 32 * t;
+    uk[t] = r < n ? uv[S.kidx[r]] : 0.0;
+    acc[t] = 0.0;
+  }
+  for (int c0 = wid; c0 < n; c0 += 4 * kQpWarps) {
+    double cs[4];
 #pragma unroll
-    for (int t = 0; t < TM; ++t) {
-      s0 = fma(h0[t], uu[t], s0);
-      s1 = fma(h1[t], uu[t], s1);
+    for (int q = 0; q < 4; ++q) {
+      const int c = c0 + q * kQpWarps;
+      cs[q] = 0.0;
+      if (c < n) {
+        const double uc = uv[S.kidx[c]];
+        const double* col = S.Hp + colbase(c, n);
+#pragma unroll
+        for (int t = 0; t < TM; ++t) {
+          const int r = lane + 32 * t;
+          if (r >= c && r < n) {
+            const double h = col[r];
+            acc[t] = fma(h, uc, acc[t]);
+            if (r > c) cs[q] = fma(h, uk[t], cs[q]);
+          }
+        }
+      }
     }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cs[q] += __shfl_xor_sync(0xffffffffu, cs[q], o);
     if (lane == 0) {
-      out[S.kidx[r0]] = s0;
-      if (r1 < n) out[S.kidx[r1]] = s1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + q * kQpWarps;
+        if (c < n) colsum[c] = cs[q];
+      }
     }
   }
+#pragma unroll
+  for (int t = 0; t < TM; ++t) {
+    const int r = lane + 32 * t;
+    if (r < n) part[wid * n + r] = acc[t];
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    double v = colsum[r];
+#pragma unroll
+    for (int w = 0; w < kQpWarps; ++w) v += part[w * n + r];
+    out[S.kidx[r]] = v;
+  }
   for (int e = threadIdx.x; e < S.ne; e += blockDim.x) out[S.eidx[e]] = S.hde[e] * uv[S.eidx[e]];
+  __syncthreads();
 }
 
 // K = 2H + diag_add I + diag(sum_single w val^2) + Cg' W Cg  (qpsolver.py:178-184)
@@ -315,51 +351,35 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
     S.wg[gi] = wr;
   }
   __syncthreads();
-  const int nq = (n + 3) >> 2;
-  const int tiles = nq * (nq + 1) / 2;
-  for (int tt = threadIdx.x; tt < tiles; tt += blockDim.x) {
-    // column-major enumeration of lower tiles: column J holds nq - J tiles
-    const float q2 = 2.0f * nq + 1.0f;
-    int J = (int)((q2 - sqrtf(q2 * q2 - 8.0f * tt)) * 0.5f);
-    J = max(0, min(J, nq - 1));
-    while (J > 0 && J * nq - J * (J - 1) / 2 > tt) --J;
-    while ((J + 1) * nq - (J + 1) * J / 2 <= tt) ++J;
-    const int I = J + (tt - (J * nq - J * (J - 1) / 2));
-    const int r0 = 4 * I, c0 = 4 * J;
-    double acc[4][4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int c = c0 + b;
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int r = r0 + a;
-        acc[a][b] = (c < n && r > c && r < n) ? 2.0 * S.Hp[colbase(c, n) + r] : 0.0;
+  // lower 8x8 tiles of 2H + Cg' diag(wg) Cg on the fp64 tensor cores: the
+  // C fragment (row i, cols 2p, 2p+1) starts from 2H, ng/4 DMMAs add the
+  // general rows (A[i][g] = wg_g Cg[g][row], B[g][j] = Cg[g][col]), padding
+  // rows/cols (>= n) become the identity.  One warp per tile.
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int i = lane >> 2, p = lane & 3;
+    const int T = S.T, ntiles = T * (T + 1) / 2;
+    for (int tt = wid; tt < ntiles; tt += kQpWarps) {
+      int I = (int)((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);
+      while (I * (I + 1) / 2 > tt) --I;
+      while ((I + 1) * (I + 2) / 2 <= tt) ++I;
+      const int J = tt - I * (I + 1) / 2;
+      const int r = 8 * I + i, ca = 8 * J + 2 * p, cb = ca + 1;
+      // strictly lower entries start from 2H; the diagonal is completed below
+      double h0 = (r < n && ca < n && r > ca) ? 2.0 * S.Hp[colbase(ca, n) + r] : 0.0;
+      double h1 = (r < n && cb < n && r > cb) ? 2.0 * S.Hp[colbase(cb, n) + r] : 0.0;
+      const int rb = 8 * J + i;  // B operand column
+      for (int g0 = 0; g0 < ng; g0 += 4) {
+        const int g = g0 + p;
+        const double* cg = S.Cg + (int64_t)min(g, ng - 1) * S.n;
+        const double av = (g < ng && r < n) ? S.wg[g] * cg[r] : 0.0;
+        const double bv = (g < ng && rb < n) ? cg[rb] : 0.0;
+        qpchol::dmma884(h0, h1, av, bv);
       }
-    }
-    for (int gi = 0; gi < ng; ++gi) {
-      const double* cg = S.Cg + (int64_t)gi * S.n;
-      const double wgi = S.wg[gi];
-      double x[4], y[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        x[a] = r0 + a < n ? cg[r0 + a] * wgi : 0.0;
-        y[a] = c0 + a < n ? cg[c0 + a] : 0.0;
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
-    }
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int c = c0 + b;
-      if (c >= n) continue;
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int r = r0 + a;
-        if (r < c || r >= n) continue;
-        S.K[qpchol::gel(r, c)] = acc[a][b];
-      }
+      if (r >= n || ca >= n) h0 = r == ca ? 1.0 : 0.0;
+      if (r >= n || cb >= n) h1 = r == cb ? 1.0 : 0.0;
+      if (r >= ca) S.K[qpchol::gel(r, ca)] = h0;
+      if (r >= cb) S.K[qpchol::gel(r, cb)] = h1;
     }
   }
   __syncthreads();
@@ -377,9 +397,7 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
     const int dc = qpchol::gel(k, k);
     S.K[dc] = ((2.0 * S.Hp[colbase(k, n) + k] + diag_add) + dsum) + S.K[dc];
   }
-  // identity padding up to the tile size (last tile row)
-  for (int r = n + threadIdx.x / 8; r < 8 * S.T; r += blockDim.x / 8)
-    for (int c = (threadIdx.x & 7); c <= r; c += 8) S.K[qpchol::gel(r, c)] = r == c ? 1.0 : 0.0;
+
   return __syncthreads_and(ok ? 1 : 0) != 0;
 }
 
@@ -463,10 +481,14 @@ struct Resid {
 
 // residuals at (u, lam) (qpsolver.py:90-97); leaves r_dual in rd, C u in cu
 __device__ Resid residuals(Qs& S) {
+  qmark(S, 1);
   h_apply(S, S.u, S.hu);
+  qmark(S, 12);
   ct_apply(S, S.lam, S.ctl);
+  qmark(S, 13);
   c_apply(S, S.u, S.cu);
   __syncthreads();
+  qmark(S, 14);
   double a_rs = 0.0, a_rp = -INFINITY, a_rc = 0.0;
   for (int c = threadIdx.x; c < S.n; c += blockDim.x) {
     const double rd = (2.0 * S.hu[c] + S.g[c]) + S.ctl[c];
@@ -478,6 +500,7 @@ __device__ Resid residuals(Qs& S) {
     a_rp = fmax(a_rp, viol);
     a_rc = fmax(a_rc, fabs(S.lam[r] * viol));
   }
+  qmark(S, 15);
   Resid R;
   R.rs = block_reduce<0>(a_rs, S.red);
   R.rp = fmax(0.0, block_reduce<0>(a_rp, S.red));

@@ -8,7 +8,7 @@ from paper_2602_17601_b200 import _runtime
 from tests.golden_io import load
 names = ["setup", "residuals", "tests+best", "w+build_k", "cholesky", "inv_diag", "rp/mu+aff_rhs",
          "kkt(excl solve)", "steps/sigma", "update", "pre-solve", "chol_solve",
-         "[chol] lookahead(after bar)", "[chol] warp1 upd(after bar)", "[chol] panel+bar", "[chol] step total"]
+         "[res] h_apply", "[res] ct_apply", "[res] c_apply+bar", "[res] loops"]
 for case in sys.argv[1:] or ["cfg1_chain10"]:
     if case == "cfg3":
         from paper_2602_17601_b200 import workloads
