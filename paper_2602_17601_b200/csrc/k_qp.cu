@@ -359,27 +359,49 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int i = lane >> 2, p = lane & 3;
     const int T = S.T, ntiles = T * (T + 1) / 2;
-    for (int tt = wid; tt < ntiles; tt += kQpWarps) {
-      int I = (int)((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);
-      while (I * (I + 1) / 2 > tt) --I;
-      while ((I + 1) * (I + 2) / 2 <= tt) ++I;
-      const int J = tt - I * (I + 1) / 2;
-      const int r = 8 * I + i, ca = 8 * J + 2 * p, cb = ca + 1;
-      // strictly lower entries start from 2H; the diagonal is completed below
-      double h0 = (r < n && ca < n && r > ca) ? 2.0 * S.Hp[colbase(ca, n) + r] : 0.0;
-      double h1 = (r < n && cb < n && r > cb) ? 2.0 * S.Hp[colbase(cb, n) + r] : 0.0;
-      const int rb = 8 * J + i;  // B operand column
+    constexpr int U = 3;  // tiles in flight per warp
+    for (int t0 = wid; t0 < ntiles; t0 += U * kQpWarps) {
+      int r[U], ca[U], rb[U];
+      double h0[U], h1[U];
+      bool live[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int tt = t0 + u * kQpWarps;
+        live[u] = tt < ntiles;
+        int I = (int)((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);
+        while (I * (I + 1) / 2 > tt) --I;
+        while ((I + 1) * (I + 2) / 2 <= tt) ++I;
+        const int J = tt - I * (I + 1) / 2;
+        r[u] = 8 * I + i;
+        ca[u] = 8 * J + 2 * p;
+        rb[u] = 8 * J + i;  // B operand column
+        const int cb = ca[u] + 1;
+        // strictly lower entries start from 2H; the diagonal is completed below
+        h0[u] = (live[u] && r[u] < n && ca[u] < n && r[u] > ca[u]) ? 2.0 * S.Hp[colbase(ca[u], n) + r[u]] : 0.0;
+        h1[u] = (live[u] && r[u] < n && cb < n && r[u] > cb) ? 2.0 * S.Hp[colbase(cb, n) + r[u]] : 0.0;
+      }
       for (int g0 = 0; g0 < ng; g0 += 4) {
         const int g = g0 + p;
         const double* cg = S.Cg + (int64_t)min(g, ng - 1) * S.n;
-        const double av = (g < ng && r < n) ? S.wg[g] * cg[r] : 0.0;
-        const double bv = (g < ng && rb < n) ? cg[rb] : 0.0;
-        qpchol::dmma884(h0, h1, av, bv);
+        const double wgg = g < ng ? S.wg[g] : 0.0;
+        double av[U], bv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          av[u] = (g < ng && r[u] < n) ? wgg * cg[r[u]] : 0.0;
+          bv[u] = (g < ng && rb[u] < n) ? cg[rb[u]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) qpchol::dmma884(h0[u], h1[u], av[u], bv[u]);
       }
-      if (r >= n || ca >= n) h0 = r == ca ? 1.0 : 0.0;
-      if (r >= n || cb >= n) h1 = r == cb ? 1.0 : 0.0;
-      if (r >= ca) S.K[qpchol::gel(r, ca)] = h0;
-      if (r >= cb) S.K[qpchol::gel(r, cb)] = h1;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!live[u]) continue;
+        const int cb = ca[u] + 1;
+        if (r[u] >= n || ca[u] >= n) h0[u] = r[u] == ca[u] ? 1.0 : 0.0;
+        if (r[u] >= n || cb >= n) h1[u] = r[u] == cb ? 1.0 : 0.0;
+        if (r[u] >= ca[u]) S.K[qpchol::gel(r[u], ca[u])] = h0[u];
+        if (r[u] >= cb) S.K[qpchol::gel(r[u], cb)] = h1[u];
+      }
     }
   }
   __syncthreads();

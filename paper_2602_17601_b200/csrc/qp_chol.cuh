@@ -34,6 +34,11 @@ namespace qpchol {
 
 constexpr int kTS = 72;  // tile stride (doubles)
 
+// Pointers into shared memory that travel through structs / non-inlined
+// calls lose their address space and compile to generic LD/ST; asserting it
+// restores LDS/STS.
+#define QP_SMEM(p) __builtin_assume(__isShared(p))
+
 __device__ __forceinline__ int ti(int I, int J) { return ((I * (I + 1)) >> 1) + J; }
 __device__ __forceinline__ int eo(int r, int c) { return c * 8 + (r ^ ((c & 2) << 1)); }
 // element (R, C) with R >= C of the padded matrix
@@ -118,6 +123,7 @@ __device__ __forceinline__ void pair36(int l, int& a, int& b) {
 // the swizzle.
 template <int NU, int NB = 6>
 __device__ __forceinline__ void trailing_update(double* Kt, int T, int k, int uw, int lane) {
+  QP_SMEM(Kt);
   const int i = lane >> 2, p = lane & 3;
   int I = k + 2, J = k + 1;  // first tile after (k+1, k+1)
   auto adv = [&](int s) {
@@ -164,6 +170,9 @@ __device__ __forceinline__ void trailing_update(double* Kt, int T, int k, int uw
 // call; returns false (uniformly) on a failed pivot.
 template <int NT>
 __device__ __noinline__ bool factor(double* Kt, int T, double* dinv, int* flag, long long* prof = nullptr) {
+  QP_SMEM(Kt);
+  QP_SMEM(dinv);
+  QP_SMEM(flag);
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -293,6 +302,10 @@ __host__ __device__ inline int xinv_doubles(int n) { return superblocks_for(n) *
 // per-warp scratch tile to become a B operand).  scratch: NW * 64 doubles.
 template <int NT>
 __device__ __noinline__ void invert_superblocks(const double* Kt, int T, const double* dinv, double* X, double* scratch) {
+  QP_SMEM(Kt);
+  QP_SMEM(dinv);
+  QP_SMEM(X);
+  QP_SMEM(scratch);
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int t = tid; t < 8 * T; t += NT) {
@@ -356,6 +369,9 @@ __device__ __noinline__ void invert_superblocks(const double* Kt, int T, const d
 // stage: 32 doubles.  All NT threads call.
 template <int NT>
 __device__ __noinline__ void solve_fwd(const double* Kt, int T, const double* X, double* y, double* stage) {
+  QP_SMEM(Kt);
+  QP_SMEM(X);
+  QP_SMEM(y);
   const int tid = threadIdx.x, lane = tid & 31;
   const int NSB = (T + 3) >> 2, N8 = 8 * T;
   for (int s = 0; s < NSB; ++s) {
@@ -419,6 +435,9 @@ __device__ __noinline__ void solve_fwd(const double* Kt, int T, const double* X,
 // In-place backward solve L' x = x.
 template <int NT>
 __device__ __noinline__ void solve_bwd(const double* Kt, int T, const double* X, double* x) {
+  QP_SMEM(Kt);
+  QP_SMEM(X);
+  QP_SMEM(x);
   const int tid = threadIdx.x, lane = tid & 31;
   const int NSB = (T + 3) >> 2, N8 = 8 * T;
   for (int s = NSB - 1; s >= 0; --s) {
