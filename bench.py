@@ -39,6 +39,11 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "MPC step latency ms (linearize+condense+QP) & Hz at N nodes; solves/sec batched"
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from the round's
+# `ncu --set full` captures at cfg3 (profiles/r01/ncu_full_summary_v3.txt)
+NCU_TRAFFIC = {"k_solve_qp": 747008, "k_linearize": 1182464, "k_condense_fused": 35225344}
+# cfg3 linearize flops, psi-VJP formulation
+LIN_FLOPS_CFG3 = 1.53e9
 M_NODES, HORIZON = 1000, 20
 WORKLOAD = "cfg3: chain graph M=1000 nodes, horizon N=20, _scaling_problem recipe (paper 100 Hz headline)"
 
@@ -135,15 +140,23 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
-    def start(self):
+    def start(self, wait_s=5.0):
+        """Start sampling every 50 ms; returns once the first sample arrived
+        (nvidia-smi can take a second to come up) so the timed region that
+        follows is covered."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except (OSError, FileNotFoundError):
             self.proc = None
+            return
+        t0 = time.time()
+        while not self.lines and time.time() - t0 < wait_s:
+            time.sleep(0.02)
+        self.n0 = len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -227,7 +240,6 @@ def ours_arm(args, world, rank, local):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.3)
     step_ms, lin_ms, cond_ms, solve_ms = [], [], [], []
     if world > 1:
         torch.distributed.barrier()
@@ -294,6 +306,29 @@ def ours_arm(args, world, rank, local):
             "frac": (fl / (solve * 1e-3) / 1e12) / fp64_sm_peak, "traffic": None,
             "note": "latency-bound single-CTA fp64 IPM; peak = FP64 FMA rate of one SM at max clock"}
 
+    # HBM roofline of the Gamma recursion + H/g kernel (K-COND): compulsory
+    # bytes of the recursion (read stage n of Gamma once, write
+    # stage n+1 once, causal columns only, fp32) plus the A/B/c blocks
+    nx, nu = 6, 6
+    gam = 4.0 * M * nx * sum((1 + k * nu) + (1 + (k + 1) * nu) for k in range(N))
+    blocks = N * (M * nx * nx * 4 + int(topo.edge_count) * nx * nx * 4
+                  + M * nx * nu * 4 + M * nx * 8)
+    cond = float(np.mean(cond_ms))
+    hbm_peak = float(peaks.get("hbm_gbs") or 6449.1)
+    cond_gbs = (gam + blocks) / (cond * 1e-3) / 1e9
+    # K-LIN: algorithmic flops of the psi-VJP formulation, FP32 SIMT
+    lin = float(np.mean(lin_ms))
+    stages = {
+        "k_condense_fused": {"bound": "hbm", "achieved": cond_gbs, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": cond_gbs / hbm_peak, "algorithmic_bytes": gam + blocks,
+                             "traffic": NCU_TRAFFIC.get("k_condense_fused"),
+                             "note": "stage time incl. constraint rows/soft expansion; Gamma is L2-resident at cfg3"},
+        "k_linearize": {"bound": "fp32/fp64 SIMT", "ms": lin,
+                        "achieved": LIN_FLOPS_CFG3 / (lin * 1e-3) / 1e12 if (M, N) == (1000, 20) else None,
+                        "unit": "TFLOP/s", "traffic": NCU_TRAFFIC.get("k_linearize")},
+    }
+    roof["traffic"] = NCU_TRAFFIC.get("k_solve_qp")
+
     cpu = None
     if not args.no_cpu_baseline:
         cms = cpu_oracle_steps(M, N, args.cpu_steps, 1, 1)
@@ -321,6 +356,7 @@ def ours_arm(args, world, rank, local):
         "gpu_launch_mode": "CUDA graphs (3 replays/step)",
         "clocks": clk,
         "roofline": roof,
+        "roofline_stages": stages,
         "cpu_baseline": cpu,
     }
     print(json.dumps(out), flush=True)
@@ -370,7 +406,7 @@ def cfg4_arm(args, world, rank, local):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local); clocks.start(); time.sleep(0.3)
+    clocks = ClockSampler(local); clocks.start()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         res = run_step()
@@ -430,7 +466,7 @@ def cfg5_arm(args, world, rank, local):
         pm.step(x0, ls, li)
     dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local); clocks.start(); time.sleep(0.3)
+    clocks = ClockSampler(local); clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ms = []
     for _ in range(args.steps):

@@ -49,10 +49,12 @@ struct QpLayout {
 // m-vectors: d s lam cu rp t dl ds tmp w lb rval              (12)
 // ng-vectors (after the row classification): wg ga cf         (3)
 // nf: dimension of the factorised system, <= n.  K: lower 8x8 tiles of the
-// padded Schur matrix (qp_chol.cuh); X region: inverted diagonal
-// superblocks, per-warp scratch tiles, 1/diag(L) and the padded solve vector.
+// padded Schur matrix (qp_chol.cuh), overwritten by X = L^{-1} after the
+// factorisation; X region: inverted diagonal tiles, per-warp scratch tiles,
+// 1/diag(L), the padded solve vector and its staging copy.
 __host__ __device__ inline size_t xregion_doubles(int nf) {
-  return (size_t)qpchol::xinv_doubles(nf) + 64 * kQpWarps + 16 * (size_t)qpchol::tiles_for(nf);
+  const size_t T = qpchol::tiles_for(nf);
+  return T * qpchol::kTS + 64 * kQpWarps + 24 * T;
 }
 __host__ __device__ inline QpLayout qp_layout(int n, int m, int ng, bool h_smem, bool cg_smem, int nf = -1) {
   QpLayout L{};
@@ -160,12 +162,13 @@ __device__ double block_reduce(double v, double* red) {
 
 // ---------------------------------------------------------------------------
 // factorisation and solves (qp_chol.cuh): tiled Cholesky of the reduced Schur
-// matrix, inverted 32x32 diagonal superblocks, superblock triangular solves
+// matrix, X = L^{-1} in place, triangular solves as two parallel mat-vecs
 // ---------------------------------------------------------------------------
 // Packed lower triangle of H, column-major: element (r, c), r >= c, at
 // colbase(c, n) + r.
 __device__ __forceinline__ int colbase(int c, int n) { return c * n - ((c * (c + 1)) >> 1); }
 
+// Cholesky factor of the padded Schur matrix (qp_chol.cuh)
 __device__ __forceinline__ bool chol_factor(Qs& S) {
   if (S.T == 0) return true;  // every variable eliminated
   if (threadIdx.x == 0) *S.flag = 0;
@@ -175,17 +178,22 @@ __device__ __forceinline__ bool chol_factor(Qs& S) {
   return ok;
 }
 
+// L -> X = L^{-1} in place (the factor itself is not needed afterwards)
 __device__ __forceinline__ void invert_diag_blocks(Qs& S) {
-  qpchol::invert_superblocks<kQpThreads>(S.K, S.T, S.dinv, S.X, S.scr);
+  if (S.T == 0) return;
+  qpchol::invert_full<kQpThreads>(S.K, S.T, S.dinv, S.X, S.scr);
 }
 
-// x = K^{-1} b through the padded solve vector S.yv (padding stays zero);
-// b and x are shared nf-vectors (x may alias b).  Call with all threads.
+// x = K^{-1} b = X' (X b) through the padded solve vector S.yv (padding stays
+// zero); b and x are shared nf-vectors (x may alias b).  Call with all threads.
 __device__ void chol_solve(Qs& S, const double* b, double* x) {
   for (int r = threadIdx.x; r < S.nf; r += blockDim.x) S.yv[r] = b[r];
   __syncthreads();
-  qpchol::solve_fwd<kQpThreads>(S.K, S.T, S.X, S.yv, nullptr);
-  qpchol::solve_bwd<kQpThreads>(S.K, S.T, S.X, S.yv);
+  if (S.T > 0) {
+    double* tmp = S.yv + 8 * S.T;
+    qpchol::apply_x<kQpThreads>(S.K, S.T, S.yv, tmp);
+    qpchol::apply_xt<kQpThreads>(S.K, S.T, S.yv, tmp);
+  }
   for (int r = threadIdx.x; r < S.nf; r += blockDim.x) x[r] = S.yv[r];
   __syncthreads();
 }
@@ -705,13 +713,13 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.K = (double*)(smem + LY.o_k);
     S.X = (double*)(smem + LY.o_x);
     S.T = qpchol::tiles_for(S.nf);
-    S.scr = S.X + qpchol::xinv_doubles(S.nf);
+    S.scr = S.X + S.T * qpchol::kTS;
     S.dinv = S.scr + 64 * kQpWarps;
     S.yv = S.dinv + 8 * S.T;
     S.Cg = cg_smem ? (double*)(smem + LY.o_cg) : gws + packed_size(n);
     S.Hp = h_smem ? (double*)(smem + LY.o_h) : gws;
   }
-  for (int t = tid; t < 8 * S.T; t += nt) S.yv[t] = 0.0;
+  for (int t = tid; t < 16 * S.T; t += nt) S.yv[t] = 0.0;
   // general rows, column-permuted to the kept variables
   for (int t = tid; t < S.ng * S.nf; t += nt) {
     const int gi = t / S.nf, k = t - gi * S.nf;
@@ -948,10 +956,10 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_chol_check(int n, const doubl
   S.du = v + n;
   S.K = (double*)(smem + L0.o_k);
   S.X = (double*)(smem + L0.o_x);
-  S.scr = S.X + qpchol::xinv_doubles(n);
+  S.scr = S.X + S.T * qpchol::kTS;
   S.dinv = S.scr + 64 * kQpWarps;
   S.yv = S.dinv + 8 * S.T;
-  for (int t = threadIdx.x; t < 8 * S.T; t += blockDim.x) S.yv[t] = 0.0;
+  for (int t = threadIdx.x; t < 16 * S.T; t += blockDim.x) S.yv[t] = 0.0;
   for (int e = threadIdx.x; e < 64 * S.T * S.T; e += blockDim.x) {
     const int r = e / (8 * S.T), c = e - r * (8 * S.T);
     if (c > r) continue;
@@ -962,12 +970,13 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_chol_check(int n, const doubl
   const bool good = chol_factor(S);
   if (threadIdx.x == 0) *ok = good ? 1 : 0;
   if (!good) return;
-  invert_diag_blocks(S);
-  __syncthreads();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int r = e / n, c = e - r * n;
     L[e] = r >= c ? S.K[qpchol::gel(r, c)] : 0.0;
   }
+  __syncthreads();
+  invert_diag_blocks(S);
+  __syncthreads();
   chol_solve(S, S.rhs, S.du);
   for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = S.du[r];
 }

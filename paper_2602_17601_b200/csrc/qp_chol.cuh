@@ -4,10 +4,10 @@
 // Storage.  The n x n SPD matrix is padded to 8T x 8T (T = ceil(n/8)) with an
 // identity block and held as its lower 8x8 tiles (I >= J) in shared memory,
 // row-major tile order ti(I, J) = I(I+1)/2 + J, tile stride kTS doubles.
-// Inside a tile, element (r, c) sits at c*8 + (r ^ ((c & 2) << 1)): column
-// major with a 4-row swizzle on columns 2,3,6,7 so the DMMA fragment loads of
-// the trailing update hit distinct banks; kTS = 72 (a multiple of 8 but not
-// of 16) keeps row-per-thread accesses of consecutive tiles conflict free.
+// Inside a tile, element (r, c) sits at eo(r, c): column major with an XOR
+// row swizzle per column pair, so DMMA fragments, rows and columns are all
+// conflict free; kTS = 72 (a multiple of 8 but not of 16) keeps
+// row-per-thread accesses of consecutive tiles conflict free.
 //
 // Factorisation (right-looking, 8-column steps, look-ahead depth 1).  The
 // critical path of a small Cholesky is the chain of pivots: rsqrt of the
@@ -40,7 +40,11 @@ constexpr int kTS = 72;  // tile stride (doubles)
 #define QP_SMEM(p) __builtin_assume(__isShared(p))
 
 __device__ __forceinline__ int ti(int I, int J) { return ((I * (I + 1)) >> 1) + J; }
-__device__ __forceinline__ int eo(int r, int c) { return c * 8 + (r ^ ((c & 2) << 1)); }
+// in-tile offset of (r, c): column major, rows XOR-permuted by s(c) =
+// {0,0,4,4,2,2,6,6}[c] so that a column (fixed c), a row (fixed r), the DMMA
+// A/B fragments (rows 0..3 x cols 0..3 per half warp) and the transposed C
+// fragment pairs all hit distinct banks
+__device__ __forceinline__ int eo(int r, int c) { return c * 8 + (r ^ (((c & 2) << 1) | ((c & 4) >> 1))); }
 // element (R, C) with R >= C of the padded matrix
 __device__ __forceinline__ int gel(int R, int C) { return ti(R >> 3, C >> 3) * kTS + eo(R & 7, C & 7); }
 __host__ __device__ inline int tiles_for(int n) { return (n + 7) >> 3; }
@@ -174,6 +178,7 @@ __device__ __noinline__ bool factor(double* Kt, int T, double* dinv, int* flag, 
   QP_SMEM(dinv);
   QP_SMEM(flag);
   constexpr int NW = NT / 32;
+  constexpr int NU = NW - NW / 4;  // update warps (off warp 0's sub-partition)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (tid == 0) {
@@ -262,9 +267,7 @@ __device__ __noinline__ bool factor(double* Kt, int T, double* dinv, int* flag, 
       // Warps sharing warp 0's sub-partition (wid % 4 == 0) stay off the
       // FP64 pipe: a DMMA holds it ~16 cycles and would stall the pivot
       // chain's dependent DFMAs.
-#ifndef CHOL_SKIP_TRAIL
-      if ((wid & 3) != 0) trailing_update<NW - NW / 4>(Kt, T, k, wid - 1 - (wid >> 2), lane);
-#endif
+      if ((wid & 3) != 0) trailing_update<NU>(Kt, T, k, wid - 1 - (wid >> 2), lane);
       if (prof && lane == 0) pr[5] += clock64() - t0;
     }
     __syncthreads();
@@ -281,37 +284,29 @@ __device__ __noinline__ bool factor(double* Kt, int T, double* dinv, int* flag, 
 }
 
 // ---------------------------------------------------------------------------
-// Triangular solves through inverted 32 x 32 diagonal superblocks
+// Full inverse X = L^{-1} in place, and triangular solves as mat-vecs
 // ---------------------------------------------------------------------------
-// Superblock s covers tiles 4s..4s+3 (rows 32s..32s+31).  X holds, per
-// superblock, the 10 lower tiles of X_s = L_ss^{-1} (local tile index
-// ti(a, b), a >= b, same in-tile layout; the strict upper part of its
-// diagonal tiles is zero).  With X a solve is NSB = ceil(T/4) short steps:
-//   forward  y_s = X_s (b_s - sum_{c<s} L_sc y_c),
-//   backward x_s = X_s' (y_s - sum_{c>s} L_cs' x_c),
-// each a 32-term dot per row by one warp plus a parallel update of the
-// remaining rows.
-__host__ __device__ inline int superblocks_for(int n) { return (tiles_for(n) + 3) >> 2; }
-__host__ __device__ inline int xinv_doubles(int n) { return superblocks_for(n) * 10 * kTS; }
-
-// X_s tiles.  Phase 1: inverse of every diagonal 8x8 tile, one thread per
-// (tile, column), forward substitution with progressive accumulation.
-// Phase 2: off-diagonal tiles by levels d = a - b = 1, 2, 3:
-//   X(a, b) = -Linv_a * sum_{m=b}^{a-1} L(a, m) X(m, b),
-// one warp per tile on the fp64 tensor cores (the partial sum is staged in a
-// per-warp scratch tile to become a B operand).  scratch: NW * 64 doubles.
+// Row wavefront: after row I is processed, tile (I, I) holds Linv_I and tiles
+// (I, J < I) hold X_IJ = -Linv_I * sum_{K=J}^{I-1} L_IK X_KJ.  Row I only reads
+// row I of L (still intact) and the finished X rows above, so it can be
+// computed in place: all of the row's tiles are formed in registers (one warp
+// per tile, the K-sum split over two DMMA accumulator chains), then written
+// after a barrier.  The diagonal inverses are formed first for all rows (one
+// thread per (tile, column), forward substitution) in the scratch area D
+// (T tiles) and copied in with their row.  W: per-warp 64-double staging.
+// With X, each triangular solve is one parallel mat-vec instead of a chain.
 template <int NT>
-__device__ __noinline__ void invert_superblocks(const double* Kt, int T, const double* dinv, double* X, double* scratch) {
+__device__ __noinline__ void invert_full(double* Kt, int T, const double* dinv, double* D, double* W) {
   QP_SMEM(Kt);
   QP_SMEM(dinv);
-  QP_SMEM(X);
-  QP_SMEM(scratch);
+  QP_SMEM(D);
+  QP_SMEM(W);
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int t = tid; t < 8 * T; t += NT) {
     const int k = t >> 3, c = t & 7;
     const double* L = Kt + ti(k, k) * kTS;
-    double* Xt = X + ((k >> 2) * 10 + ti(k & 3, k & 3)) * kTS;
+    double* Xt = D + k * kTS;
     double x[8], acc[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -331,172 +326,128 @@ __device__ __noinline__ void invert_superblocks(const double* Kt, int T, const d
     for (int r = 0; r < 8; ++r) Xt[eo(r, c)] = x[r];
   }
   __syncthreads();
-  const int NSB = (T + 3) >> 2;
   const int i = lane >> 2, p = lane & 3;
-  double* W = scratch + wid * 64;
-  for (int d = 1; d < 4; ++d) {
-    // tasks: (superblock s, local column b) with b + d < min(4, T - 4s)
-    const int per = 4 - d;
-    for (int task = wid; task < NSB * per; task += NW) {
-      const int s = task / per, b = task - s * per, a = b + d;
-      if (4 * s + a >= T) continue;
-      double* Xs = X + s * 10 * kTS;
-      double w0 = 0.0, w1 = 0.0;
-      for (int m = b; m < a; ++m) {
-        const double* L = Kt + ti(4 * s + a, 4 * s + m) * kTS;  // A = L(a, m)
-        const double* Xm = Xs + ti(m, b) * kTS;                  // B = X(m, b)
+  double* Ws = W + wid * 64;
+  // row 0: only its diagonal
+  for (int e = tid; e < 64; e += NT) Kt[ti(0, 0) * kTS + e] = D[e];
+  for (int I = 1; I < T; ++I) {
+    constexpr int MAXR = 4;  // tiles per warp per row (T <= 32)
+    double x0[MAXR], x1[MAXR];
+    const double* Li = D + I * kTS;  // Linv_I
 #pragma unroll
-        for (int h = 0; h < 8; h += 4) dmma884(w0, w1, L[eo(i, p + h)], Xm[eo(p + h, i)]);
+    for (int u = 0; u < MAXR; ++u) {
+      const int J = wid + u * NW;
+      x0[u] = 0.0;
+      x1[u] = 0.0;
+      if (J < I) {
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        for (int K = J; K < I; K += 2) {
+          const double* L0 = Kt + ti(I, K) * kTS;
+          const double* X0 = Kt + ti(K, J) * kTS;
+#pragma unroll
+          for (int h = 0; h < 8; h += 4) dmma884(a0, a1, L0[eo(i, p + h)], X0[eo(p + h, i)]);
+          if (K + 1 < I) {
+            const double* L1 = Kt + ti(I, K + 1) * kTS;
+            const double* X1 = Kt + ti(K + 1, J) * kTS;
+#pragma unroll
+            for (int h = 0; h < 8; h += 4) dmma884(b0, b1, L1[eo(i, p + h)], X1[eo(p + h, i)]);
+          }
+        }
+        Ws[eo(i, 2 * p)] = a0 + b0;
+        Ws[eo(i, 2 * p + 1)] = a1 + b1;
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 8; h += 4) dmma884(x0[u], x1[u], -Li[eo(i, p + h)], Ws[eo(p + h, i)]);
+        __syncwarp();
       }
-      // W (C fragment: row i, cols 2p, 2p+1) -> scratch -> B fragments
-      W[eo(i, 2 * p)] = w0;
-      W[eo(i, 2 * p + 1)] = w1;
-      __syncwarp();
-      const double* La = Xs + ti(a, a) * kTS;  // Linv_a
-      double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-      for (int h = 0; h < 8; h += 4) dmma884(x0, x1, -La[eo(i, p + h)], W[eo(p + h, i)]);
-      double* Xab = Xs + ti(a, b) * kTS;
-      Xab[eo(i, 2 * p)] = x0;
-      Xab[eo(i, 2 * p + 1)] = x1;
-      __syncwarp();
     }
+    __syncthreads();  // row I of L fully read
+#pragma unroll
+    for (int u = 0; u < MAXR; ++u) {
+      const int J = wid + u * NW;
+      if (J < I) {
+        double* Xt = Kt + ti(I, J) * kTS;
+        Xt[eo(i, 2 * p)] = x0[u];
+        Xt[eo(i, 2 * p + 1)] = x1[u];
+      }
+    }
+    for (int e = tid; e < 64; e += NT) Kt[ti(I, I) * kTS + e] = Li[e];
     __syncthreads();
   }
 }
 
-// In-place forward solve L y = y (y: shared, 8T entries, padding zero).
-// stage: 32 doubles.  All NT threads call.
+// y <- X y (X = L^{-1} in Kt, lower): two threads per row, each over every
+// other tile of the row, 4 accumulators; the halves meet through a shuffle.
+// y: shared, 8T entries; tmp: 8T doubles.  All NT threads call.
 template <int NT>
-__device__ __noinline__ void solve_fwd(const double* Kt, int T, const double* X, double* y, double* stage) {
+__device__ __noinline__ void apply_x(const double* Kt, int T, double* y, double* tmp) {
   QP_SMEM(Kt);
-  QP_SMEM(X);
   QP_SMEM(y);
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int NSB = (T + 3) >> 2, N8 = 8 * T;
-  for (int s = 0; s < NSB; ++s) {
-    const int r0 = 32 * s, nb = min(32, N8 - r0);
-    if (tid < 32) {
-      const double* Xs = X + s * 10 * kTS;
-      double v = 0.0;
-      if (lane < nb) {
-        const int a = lane >> 3, r = lane & 7;
-        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-        for (int m = 0; m <= a; ++m) {
-          const double* Xt = Xs + ti(a, m) * kTS;
-          const double* yy = y + r0 + 8 * m;
-          c0 = fma(Xt[eo(r, 0)], yy[0], c0);
-          c1 = fma(Xt[eo(r, 1)], yy[1], c1);
-          c2 = fma(Xt[eo(r, 2)], yy[2], c2);
-          c3 = fma(Xt[eo(r, 3)], yy[3], c3);
-          c0 = fma(Xt[eo(r, 4)], yy[4], c0);
-          c1 = fma(Xt[eo(r, 5)], yy[5], c1);
-          c2 = fma(Xt[eo(r, 6)], yy[6], c2);
-          c3 = fma(Xt[eo(r, 7)], yy[7], c3);
-        }
-        v = (c0 + c1) + (c2 + c3);
+  QP_SMEM(tmp);
+  const int tid = threadIdx.x;
+  const int rows = 8 * T;
+  for (int t0 = 0; t0 < 2 * rows; t0 += NT) {
+    const int t = t0 + tid;
+    const bool live = t < 2 * rows;
+    const int r = live ? t >> 1 : 0, h = t & 1;
+    const int I = r >> 3, rr = r & 7;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+    if (live)
+      for (int J = h; J <= I; J += 2) {
+        const double* Xt = Kt + ti(I, J) * kTS;
+        const double* yy = y + 8 * J;
+        c0 = fma(Xt[eo(rr, 0)], yy[0], c0);
+        c1 = fma(Xt[eo(rr, 1)], yy[1], c1);
+        c2 = fma(Xt[eo(rr, 2)], yy[2], c2);
+        c3 = fma(Xt[eo(rr, 3)], yy[3], c3);
+        c0 = fma(Xt[eo(rr, 4)], yy[4], c0);
+        c1 = fma(Xt[eo(rr, 5)], yy[5], c1);
+        c2 = fma(Xt[eo(rr, 6)], yy[6], c2);
+        c3 = fma(Xt[eo(rr, 7)], yy[7], c3);
       }
-      __syncwarp();
-      if (lane < nb) y[r0 + lane] = v;
-    }
-    __syncthreads();
-    if (s + 1 == NSB) break;
-    // rows below: y_r -= L[r][r0 .. r0+31] y[r0 ..], two threads per row
-    const int rows = N8 - (r0 + 32);
-    for (int t0 = 0; t0 < 2 * rows; t0 += NT) {  // warp-uniform trip count (shuffle below)
-      const int t = t0 + tid;
-      const bool live = t < 2 * rows;
-      const int r = r0 + 32 + (live ? t >> 1 : 0), half = t & 1;
-      const int R = r >> 3, rr = r & 7;
-      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < 2 && live; ++mm) {
-        const int m = 4 * s + 2 * half + mm;
-        const double* Lt = Kt + ti(R, m) * kTS;
-        const double* yy = y + 8 * m;
-        c0 = fma(Lt[eo(rr, 0)], yy[0], c0);
-        c1 = fma(Lt[eo(rr, 1)], yy[1], c1);
-        c2 = fma(Lt[eo(rr, 2)], yy[2], c2);
-        c3 = fma(Lt[eo(rr, 3)], yy[3], c3);
-        c0 = fma(Lt[eo(rr, 4)], yy[4], c0);
-        c1 = fma(Lt[eo(rr, 5)], yy[5], c1);
-        c2 = fma(Lt[eo(rr, 6)], yy[6], c2);
-        c3 = fma(Lt[eo(rr, 7)], yy[7], c3);
-      }
-      double v = (c0 + c1) + (c2 + c3);
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if (live && !half) y[r] -= v;
-    }
-    __syncthreads();
+    double v = (c0 + c1) + (c2 + c3);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    if (live && !h) tmp[r] = v;
   }
-  (void)stage;
+  __syncthreads();
+  for (int r = tid; r < rows; r += NT) y[r] = tmp[r];
+  __syncthreads();
 }
 
-// In-place backward solve L' x = x.
+// y <- X' y: two threads per column c, each over every other tile row I >= C.
 template <int NT>
-__device__ __noinline__ void solve_bwd(const double* Kt, int T, const double* X, double* x) {
+__device__ __noinline__ void apply_xt(const double* Kt, int T, double* y, double* tmp) {
   QP_SMEM(Kt);
-  QP_SMEM(X);
-  QP_SMEM(x);
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int NSB = (T + 3) >> 2, N8 = 8 * T;
-  for (int s = NSB - 1; s >= 0; --s) {
-    const int r0 = 32 * s, nb = min(32, N8 - r0), na = (nb + 7) >> 3;
-    if (tid < 32) {
-      const double* Xs = X + s * 10 * kTS;
-      double v = 0.0;
-      if (lane < nb) {
-        const int b = lane >> 3, c = lane & 7;
-        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-        for (int m = b; m < na; ++m) {  // column c of X tiles (m, b)
-          const double* Xt = Xs + ti(m, b) * kTS;
-          const double* xx = x + r0 + 8 * m;
-          c0 = fma(Xt[eo(0, c)], xx[0], c0);
-          c1 = fma(Xt[eo(1, c)], xx[1], c1);
-          c2 = fma(Xt[eo(2, c)], xx[2], c2);
-          c3 = fma(Xt[eo(3, c)], xx[3], c3);
-          c0 = fma(Xt[eo(4, c)], xx[4], c0);
-          c1 = fma(Xt[eo(5, c)], xx[5], c1);
-          c2 = fma(Xt[eo(6, c)], xx[6], c2);
-          c3 = fma(Xt[eo(7, c)], xx[7], c3);
-        }
-        v = (c0 + c1) + (c2 + c3);
+  QP_SMEM(y);
+  QP_SMEM(tmp);
+  const int tid = threadIdx.x;
+  const int cols = 8 * T;
+  for (int t0 = 0; t0 < 2 * cols; t0 += NT) {
+    const int t = t0 + tid;
+    const bool live = t < 2 * cols;
+    const int c = live ? t >> 1 : 0, h = t & 1;
+    const int C = c >> 3, cc = c & 7;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+    if (live)
+      for (int I = C + h; I < T; I += 2) {
+        const double* Xt = Kt + ti(I, C) * kTS;
+        const double* yy = y + 8 * I;
+        c0 = fma(Xt[eo(0, cc)], yy[0], c0);
+        c1 = fma(Xt[eo(1, cc)], yy[1], c1);
+        c2 = fma(Xt[eo(2, cc)], yy[2], c2);
+        c3 = fma(Xt[eo(3, cc)], yy[3], c3);
+        c0 = fma(Xt[eo(4, cc)], yy[4], c0);
+        c1 = fma(Xt[eo(5, cc)], yy[5], c1);
+        c2 = fma(Xt[eo(6, cc)], yy[6], c2);
+        c3 = fma(Xt[eo(7, cc)], yy[7], c3);
       }
-      __syncwarp();
-      if (lane < nb) x[r0 + lane] = v;
-    }
-    __syncthreads();
-    if (s == 0) break;
-    // rows above: x_c -= sum_{r in superblock s} L[r][c] x_r, two threads per row
-    const int rows = r0;
-    for (int t0 = 0; t0 < 2 * rows; t0 += NT) {
-      const int t = t0 + tid;
-      const bool live = t < 2 * rows;
-      const int c = live ? t >> 1 : 0, half = t & 1;
-      const int C = c >> 3, cc = c & 7;
-      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < 2; ++mm) {
-        const int m = 4 * s + 2 * half + mm;
-        if (live && m < T) {
-          const double* Lt = Kt + ti(m, C) * kTS;
-          const double* xx = x + 8 * m;
-          c0 = fma(Lt[eo(0, cc)], xx[0], c0);
-          c1 = fma(Lt[eo(1, cc)], xx[1], c1);
-          c2 = fma(Lt[eo(2, cc)], xx[2], c2);
-          c3 = fma(Lt[eo(3, cc)], xx[3], c3);
-          c0 = fma(Lt[eo(4, cc)], xx[4], c0);
-          c1 = fma(Lt[eo(5, cc)], xx[5], c1);
-          c2 = fma(Lt[eo(6, cc)], xx[6], c2);
-          c3 = fma(Lt[eo(7, cc)], xx[7], c3);
-        }
-      }
-      double v = (c0 + c1) + (c2 + c3);
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if (live && !half) x[c] -= v;
-    }
-    __syncthreads();
+    double v = (c0 + c1) + (c2 + c3);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    if (live && !h) tmp[c] = v;
   }
+  __syncthreads();
+  for (int r = tid; r < cols; r += NT) y[r] = tmp[r];
+  __syncthreads();
 }
 
 }  // namespace qpchol

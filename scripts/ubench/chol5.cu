@@ -20,8 +20,9 @@ __global__ void __launch_bounds__(NT, 1) kfac(int n, const double* A, double* L,
   double* Kt = sm;
   double* dinv = sm + qpchol::tile_doubles(n);
   double* X = dinv + 8 * T;
-  double* scratch = X + qpchol::xinv_doubles(n);
+  double* scratch = X + T * qpchol::kTS;
   double* y = scratch + 64 * (NT / 32);
+  double* tmp = y + 8 * T;
   long long best = 1LL << 60;
   bool ok = true;
   for (int rep = 0; rep < reps; ++rep) {
@@ -40,14 +41,14 @@ __global__ void __launch_bounds__(NT, 1) kfac(int n, const double* A, double* L,
     __syncthreads();
   }
   const long long t2 = clock64();
-  qpchol::invert_superblocks<NT>(Kt, T, dinv, X, scratch);
+  qpchol::invert_full<NT>(Kt, T, dinv, X, scratch);
   const long long t3 = clock64();
   for (int r = threadIdx.x; r < 8 * T; r += NT) y[r] = r < n ? bvec[r] : 0.0;
   __syncthreads();
   const long long t4 = clock64();
-  qpchol::solve_fwd<NT>(Kt, T, X, y, nullptr);
+  qpchol::apply_x<NT>(Kt, T, y, tmp);
   const long long t5 = clock64();
-  qpchol::solve_bwd<NT>(Kt, T, X, y);
+  qpchol::apply_xt<NT>(Kt, T, y, tmp);
   const long long t6 = clock64();
   for (int r = threadIdx.x; r < n; r += NT) xout[r] = y[r];
   if (threadIdx.x == 0) {
@@ -128,7 +129,7 @@ int main(int argc, char** argv) {
       cudaMemset(dprof, 0, 64);
       cudaMemcpy(dA, A.data(), 8 * A.size(), cudaMemcpyHostToDevice);
       const int T = qpchol::tiles_for(n);
-      const size_t smem = 8 * (qpchol::tile_doubles(n) + 8 * T + qpchol::xinv_doubles(n) + 64 * (NT / 32) + 8 * T);
+      const size_t smem = 8 * (qpchol::tile_doubles(n) + 8 * T + T * qpchol::kTS + 64 * (NT / 32) + 16 * T);
       cudaFuncSetAttribute(kfac, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kfac<<<1, NT, smem>>>(n, dA, dL, dc, 5, dok, dprof, db, dx);
       cudaError_t e = cudaDeviceSynchronize();
