@@ -92,76 +92,94 @@ struct LinArgs {
   LinPlan plan;
 };
 
-// out[r][j] = act(sum_k in[r][k] W[j][k] + bias[j]); Wt is (K, Nout).  4 rows per
-// thread so each weight load feeds 4 FMAs; in[] reads are warp broadcasts.
-__device__ void fwd_layer(const double* in, int ldi, int R, int K, const double* __restrict__ Wt,
-                          const double* __restrict__ bias, int Nout, double* out, int ldo,
-                          uint8_t* mask, int ldm, bool relu) {
-  const int RG = (R + 3) >> 2;
-  for (int idx = threadIdx.x; idx < RG * Nout; idx += blockDim.x) {
-    const int j = idx % Nout;
-    const int r0 = (idx / Nout) << 2;
-    const double* x0 = in + (size_t)min(r0, R - 1) * ldi;
-    const double* x1 = in + (size_t)min(r0 + 1, R - 1) * ldi;
-    const double* x2 = in + (size_t)min(r0 + 2, R - 1) * ldi;
-    const double* x3 = in + (size_t)min(r0 + 3, R - 1) * ldi;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    for (int k = 0; k < K; ++k) {
-      const double w = __ldg(Wt + (size_t)k * Nout + j);
-      s0 = fma(x0[k], w, s0);
-      s1 = fma(x1[k], w, s1);
-      s2 = fma(x2[k], w, s2);
-      s3 = fma(x3[k], w, s3);
-    }
-    const double bj = __ldg(bias + j);
-    double s[4] = {s0 + bj, s1 + bj, s2 + bj, s3 + bj};
+// Register-tiled micro-GEMM shared by every layer:
+//   out[r][c] = epi(r, c, sum_k in[r][k] W[k][c]),  W row-major (K, N).
+// Each thread owns RT x CT outputs: per k it loads RT inputs (warp
+// broadcasts: neighbouring threads share rows) and CT weights (contiguous,
+// vector loads through L1), i.e. RT*CT FMAs per RT + CT loads.  N % CT == 0.
+template <typename T, int RT, int CT, typename Epi>
+__device__ __forceinline__ void tile_gemm(const T* in, int ldi, int R, int K, const T* __restrict__ W, int N,
+                                          Epi epi) {
+  const int CG = N / CT, RG = (R + RT - 1) / RT;
+  for (int idx = threadIdx.x; idx < RG * CG; idx += blockDim.x) {
+    const int c0 = (idx % CG) * CT;
+    const int r0 = (idx / CG) * RT;
+    const T* x[RT];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int r = r0 + t;
-      if (r < R) {
-        if (relu) {
-          const bool m = s[t] > 0.0;  // strict: derivative 0 at the kink (mlp.py:143)
-          mask[(size_t)r * ldm + j] = m;
-          out[(size_t)r * ldo + j] = m ? s[t] : 0.0;
-        } else {
-          out[(size_t)r * ldo + j] = s[t];
-        }
+    for (int t = 0; t < RT; ++t) x[t] = in + (size_t)min(r0 + t, R - 1) * ldi;
+    T acc[RT][CT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t)
+#pragma unroll
+      for (int u = 0; u < CT; ++u) acc[t][u] = T(0);
+    const T* wp = W + c0;
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+      T w[CT];
+#pragma unroll
+      for (int u = 0; u < CT; ++u) w[u] = __ldg(wp + u);
+      wp += N;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const T xv = x[t][k];
+#pragma unroll
+        for (int u = 0; u < CT; ++u) acc[t][u] = fma(xv, w[u], acc[t][u]);
       }
     }
+#pragma unroll
+    for (int t = 0; t < RT; ++t)
+      if (r0 + t < R)
+#pragma unroll
+        for (int u = 0; u < CT; ++u) epi(r0 + t, c0 + u, acc[t][u]);
   }
 }
 
+// Largest micro-tile that still gives every thread of the CTA an output
+// block (the per-CTA row counts are small: 32 nodes, ~64 edges, x n_p).
+template <typename T, typename Epi>
+__device__ __forceinline__ void gemm_dispatch(const T* in, int ldi, int R, int K, const T* __restrict__ W, int N,
+                                              Epi epi) {
+  const int nt = blockDim.x;
+  auto items = [&](int rt, int ct) { return ((R + rt - 1) / rt) * (N / ct); };
+  constexpr bool wide = sizeof(T) == 4;  // fp64 tiles capped at 2 x 4 (register budget)
+  if (wide && N % 8 == 0 && items(4, 8) >= nt)
+    tile_gemm<T, 4, 8>(in, ldi, R, K, W, N, epi);
+  else if (wide && N % 4 == 0 && items(4, 4) >= nt)
+    tile_gemm<T, 4, 4>(in, ldi, R, K, W, N, epi);
+  else if (N % 4 == 0 && items(2, 4) >= nt)
+    tile_gemm<T, 2, 4>(in, ldi, R, K, W, N, epi);
+  else if (N % 2 == 0 && items(2, 2) >= nt)
+    tile_gemm<T, 2, 2>(in, ldi, R, K, W, N, epi);
+  else if (N % 2 == 0)
+    tile_gemm<T, 1, 2>(in, ldi, R, K, W, N, epi);
+  else
+    tile_gemm<T, 1, 1>(in, ldi, R, K, W, N, epi);
+}
+
+// out[r][j] = act(sum_k in[r][k] W[j][k] + bias[j]); Wt is (K, Nout), fp64.
+__device__ void fwd_layer(const double* in, int ldi, int R, int K, const double* __restrict__ Wt,
+                          const double* __restrict__ bias, int Nout, double* out, int ldo,
+                          uint8_t* mask, int ldm, bool relu) {
+  gemm_dispatch<double>(in, ldi, R, K, Wt, Nout, [&](int r, int j, double s) {
+    s += __ldg(bias + j);
+    if (relu) {
+      const bool m = s > 0.0;  // strict: derivative 0 at the kink (mlp.py:143)
+      mask[(size_t)r * ldm + j] = m;
+      out[(size_t)r * ldo + j] = m ? s : 0.0;
+    } else {
+      out[(size_t)r * ldo + j] = s;
+    }
+  });
+}
+
 // out[r][kk] = (sum_j in[r][j] W[j][kk]) * mask[r / rows_per][kk]; W is (J, KK)
-// row-major (reference layout), so consecutive threads read consecutive kk.
+// row-major (reference layout), fp32.
 __device__ void bwd_layer(const float* in, int ldi, int R, int J, const float* __restrict__ W,
                           int KK, float* out, int ldo, const uint8_t* mask, int ldm, int rows_per) {
-  const int RG = (R + 3) >> 2;
-  for (int idx = threadIdx.x; idx < RG * KK; idx += blockDim.x) {
-    const int kk = idx % KK;
-    const int r0 = (idx / KK) << 2;
-    const float* x0 = in + (size_t)min(r0, R - 1) * ldi;
-    const float* x1 = in + (size_t)min(r0 + 1, R - 1) * ldi;
-    const float* x2 = in + (size_t)min(r0 + 2, R - 1) * ldi;
-    const float* x3 = in + (size_t)min(r0 + 3, R - 1) * ldi;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    for (int j = 0; j < J; ++j) {
-      const float w = __ldg(W + (size_t)j * KK + kk);
-      s0 = fmaf(x0[j], w, s0);
-      s1 = fmaf(x1[j], w, s1);
-      s2 = fmaf(x2[j], w, s2);
-      s3 = fmaf(x3[j], w, s3);
-    }
-    float s[4] = {s0, s1, s2, s3};
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int r = r0 + t;
-      if (r < R) {
-        float v = s[t];
-        if (mask && !mask[(size_t)(r / rows_per) * ldm + kk]) v = 0.f;
-        out[(size_t)r * ldo + kk] = v;
-      }
-    }
-  }
+  gemm_dispatch<float>(in, ldi, R, J, W, KK, [&](int r, int kk, float v) {
+    if (mask && !mask[(size_t)(r / rows_per) * ldm + kk]) v = 0.f;
+    out[(size_t)r * ldo + kk] = v;
+  });
 }
 
 __device__ inline int mask_off(const MlpView& m, int l) {  // column offset of hidden layer l
@@ -170,7 +188,7 @@ __device__ inline int mask_off(const MlpView& m, int l) {  // column offset of h
   return o;
 }
 
-__global__ void __launch_bounds__(kLinThreads) k_linearize(const LinArgs a) {
+__global__ void __launch_bounds__(kLinThreads, 3) k_linearize(const LinArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const LinPlan& pl = a.plan;
   const int nx = a.nx, nu = a.nu, n_p = a.n_p, n_m = a.n_m, nin = pl.nin;

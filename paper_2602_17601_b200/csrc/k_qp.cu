@@ -117,6 +117,7 @@ struct Qs {  // per-CTA views
   double *g, *u, *hu, *rd, *rhs, *du, *ub, *ctl, *ytmp, *dinv;
   double *d, *s, *lam, *cu, *rp, *t, *dl, *ds, *tmp, *w, *lb, *rval;
   int *rcol, *grow, *colptr, *colrows, *cstart;
+  const unsigned short* tij;  // lower tile (I, J) of linear index t, row major
   double* red;
   double* pv;  // 2 x 16 pivot-block factors (double buffered)
   double* ys;  // 32-entry staging vector of the triangular solves
@@ -359,6 +360,7 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
     S.wg[gi] = wr;
   }
   __syncthreads();
+  qmark(const_cast<Qs&>(S), 13);
   // lower 8x8 tiles of 2H + Cg' diag(wg) Cg on the fp64 tensor cores: the
   // C fragment (row i, cols 2p, 2p+1) starts from 2H, ng/4 DMMAs add the
   // general rows (A[i][g] = wg_g Cg[g][row], B[g][j] = Cg[g][col]), padding
@@ -376,10 +378,8 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
       for (int u = 0; u < U; ++u) {
         const int tt = t0 + u * kQpWarps;
         live[u] = tt < ntiles;
-        int I = (int)((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);
-        while (I * (I + 1) / 2 > tt) --I;
-        while ((I + 1) * (I + 2) / 2 <= tt) ++I;
-        const int J = tt - I * (I + 1) / 2;
+          const int ij = S.tij[min(tt, ntiles - 1)];  // (I << 8) | J, built once
+        const int I = ij >> 8, J = ij & 255;
         r[u] = 8 * I + i;
         ca[u] = 8 * J + 2 * p;
         rb[u] = 8 * J + i;  // B operand column
@@ -413,6 +413,7 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
     }
   }
   __syncthreads();
+  qmark(const_cast<Qs&>(S), 14);
   // diagonal (holds only the general-row term so far): (2H + reg) +
   // bincount(single rows) first, then the general-row term, as the
   // reference orders it
@@ -428,7 +429,9 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
     S.K[dc] = ((2.0 * S.Hp[colbase(k, n) + k] + diag_add) + dsum) + S.K[dc];
   }
 
-  return __syncthreads_and(ok ? 1 : 0) != 0;
+  const bool all_ok = __syncthreads_and(ok ? 1 : 0) != 0;
+  qmark(const_cast<Qs&>(S), 15);
+  return all_ok;
 }
 
 // largest step in [0, 1] with x + a dx > 0 (qpsolver.py:238-243)
@@ -515,10 +518,8 @@ __device__ Resid residuals(Qs& S) {
   h_apply(S, S.u, S.hu);
   qmark(S, 12);
   ct_apply(S, S.lam, S.ctl);
-  qmark(S, 13);
   c_apply(S, S.u, S.cu);
   __syncthreads();
-  qmark(S, 14);
   double a_rs = 0.0, a_rp = -INFINITY, a_rc = 0.0;
   for (int c = threadIdx.x; c < S.n; c += blockDim.x) {
     const double rd = (2.0 * S.hu[c] + S.g[c]) + S.ctl[c];
@@ -530,7 +531,6 @@ __device__ Resid residuals(Qs& S) {
     a_rp = fmax(a_rp, viol);
     a_rc = fmax(a_rc, fabs(S.lam[r] * viol));
   }
-  qmark(S, 15);
   Resid R;
   R.rs = block_reduce<0>(a_rs, S.red);
   R.rp = fmax(0.0, block_reduce<0>(a_rp, S.red));
@@ -720,6 +720,15 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.Hp = h_smem ? (double*)(smem + LY.o_h) : gws;
   }
   for (int t = tid; t < 16 * S.T; t += nt) S.yv[t] = 0.0;
+  {
+    __shared__ unsigned short tij[32 * 33 / 2];
+    for (int t = tid; t < S.T * (S.T + 1) / 2; t += nt) {
+      int I = 0;
+      while ((I + 1) * (I + 2) / 2 <= t) ++I;
+      tij[t] = (unsigned short)((I << 8) | (t - I * (I + 1) / 2));
+    }
+    S.tij = tij;
+  }
   // general rows, column-permuted to the kept variables
   for (int t = tid; t < S.ng * S.nf; t += nt) {
     const int gi = t / S.nf, k = t - gi * S.nf;
@@ -1022,7 +1031,7 @@ extern "C" int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, co
   if (!(s.tolerance > 0)) return gm_fail(ctx, GM_ERR_CONFIG, "tolerance must be positive");
   // vectors, the packed Schur matrix and the inverted diagonal blocks always
   // live on-chip; general rows, then packed H, go on-chip when room is left
-  const size_t cap = ctx->smem_optin - 1024;
+  const size_t cap = ctx->smem_optin - 2048;  // static shared arrays of the kernel
   const QpLayout base = qp_layout(n, m, 0, false, false);
   if (base.total > cap) return gm_fail(ctx, GM_ERR_CONFIG, "QP too large for the on-chip solver");
   const size_t smem_bytes = std::min(cap, qp_layout(n, m, m, true, true).total);

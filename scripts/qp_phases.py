@@ -8,7 +8,7 @@ from paper_2602_17601_b200 import _runtime
 from tests.golden_io import load
 names = ["setup", "residuals", "tests+best", "w+build_k", "cholesky", "inv_diag", "rp/mu+aff_rhs",
          "kkt(excl solve)", "steps/sigma", "update", "pre-solve", "chol_solve",
-         "[res] h_apply", "[res] ct_apply", "[res] c_apply+bar", "[res] loops"]
+         "[res] h_apply", "[res] ct+c_apply+loops / [bk] w,kee,wg", "[bk] tiles", "[bk] diag"]
 for case in sys.argv[1:] or ["cfg1_chain10"]:
     if case == "cfg3":
         from paper_2602_17601_b200 import workloads
