@@ -185,19 +185,32 @@ class StepPlan:
         self.status = e((1,), i32)
         self.iters = e((1,), i32)
         self.resid = e((1, 3), f64)
-        # static outputs
+        # static outputs; the four arrays a new MpcState keeps live in one
+        # buffer so the state is snapshotted with a single device copy
         self.cur = e((N + 1, M, nx), f64)
-        self.planned_states = e((M, N + 1, nx), f64)
-        self.planned_inputs = e((N, nu), f64)
-        self.next_states = e((N + 1, M, nx), f64)
-        self.next_inputs = e((N, nu), f64)
+        sizes = [M * (N + 1) * nx, N * nu, (N + 1) * M * nx, N * nu]
+        self.outbuf = e((sum(sizes),), f64)
+        self.out_views = self._carve(self.outbuf)
+        self.planned_states, self.planned_inputs, self.next_states, self.next_inputs = self.out_views
         self.u_applied = e((nu,), f64)
         self.summary = e((nu + 2,), f64)
         self.host_summary = torch.empty((nu + 2,), dtype=torch.float64, pin_memory=True)
         self.host_x = torch.empty((M, nx), dtype=torch.float64, pin_memory=True)
-        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        # external timing events: recorded as event nodes inside the step graph
+        self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
         self.graphs = None
+        self.graph = None
         self.settings_c = cfg.solver.as_c()
+
+    def _carve(self, buf):
+        M, N, nx, nu = self.M, self.N, self.nx, self.nu
+        sizes = [M * (N + 1) * nx, N * nu, (N + 1) * M * nx, N * nu]
+        shapes = [(M, N + 1, nx), (N, nu), (N + 1, M, nx), (N, nu)]
+        out, o = [], 0
+        for sz, sh in zip(sizes, shapes):
+            out.append(buf[o:o + sz].view(sh))
+            o += sz
+        return out
 
     # -- the three stage groups ------------------------------------------------
     def _linearize(self):
@@ -246,7 +259,12 @@ class StepPlan:
             else (self._condense, self._solve_finish)
 
     def capture(self):
-        """Record each stage group as a CUDA graph (after one eager run)."""
+        """Record the whole step as one CUDA graph (after one eager run):
+        measurement H2D from the pinned staging buffer, stage 0 of the
+        linearisation trajectory, the three stage groups bracketed by timing
+        event nodes, and the D2H of [u_applied, status, iterations] into
+        pinned memory -- one launch per control step.  The per-group graphs
+        are kept for eager-style replays (bench stage timing, launch counts)."""
         torch = self.eng.torch
         graphs = []
         for fn in self.groups():
@@ -255,26 +273,39 @@ class StepPlan:
                 fn()
             graphs.append(g)
         self.graphs = graphs
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.x_meas.copy_(self.host_x, non_blocking=True)
+            self.ls[0].copy_(self.x_meas)
+            self._issue(self.groups(), eager=True, timed=True)
+            self.host_summary.copy_(self.summary, non_blocking=True)
+        self.graph = g
 
-    def enqueue(self, timed=True):
-        """Issue one step on the current stream (graph replay if captured).
-        Events bracket linearize | condense | solve+epilogue for StepTiming."""
+    def _issue(self, groups, eager, timed):
         torch = self.eng.torch
         stream = torch.cuda.current_stream(self.eng.device)
         ev = self.events
-        groups = self.graphs if self.graphs is not None else self.groups()
         marks = [1, 2, 3] if len(groups) == 3 else [2, 3]
         if timed:
             ev[0].record(stream)
             if len(groups) == 2:
                 ev[1].record(stream)
         for g, mark in zip(groups, marks):
-            if self.graphs is not None:
-                g.replay()
-            else:
+            if eager:
                 g()
+            else:
+                g.replay()
             if timed:
                 ev[mark].record(stream)
+
+    def enqueue(self, timed=True):
+        """Issue the kernel chain of one step on the current stream (per-group
+        graph replay if captured, else eager).  Events bracket linearize |
+        condense | solve+epilogue for StepTiming."""
+        if self.graphs is not None:
+            self._issue(self.graphs, eager=False, timed=timed)
+        else:
+            self._issue(self.groups(), eager=True, timed=timed)
 
     def stage_ms(self):
         ev = self.events
@@ -336,9 +367,15 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
     stream = torch.cuda.current_stream(eng.device)
 
     # inputs: measurement, previous plan with x_measured at stage 0 (mpc.py:120-122)
-    _copy_in(plan.x_meas, x_measured.array, plan.host_x)
-    _copy_in(plan.ls, _field(state, "lin_states"))
-    plan.ls[0].copy_(plan.x_meas)
+    graphable = plan.use_graphs and cfg.sqp_iterations == 1
+    whole = graphable and plan.graph is not None
+    if whole:  # the step graph does the H2D from the pinned buffer and ls[0]
+        plan.host_x.numpy()[...] = np.asarray(x_measured.array, dtype=float).reshape(plan.host_x.shape)
+        _copy_in(plan.ls, _field(state, "lin_states"))
+    else:
+        _copy_in(plan.x_meas, x_measured.array, plan.host_x)
+        _copy_in(plan.ls, _field(state, "lin_states"))
+        plan.ls[0].copy_(plan.x_meas)
     _copy_in(plan.li, lin_in_prev)
     prev = _field(state, "last_applied")
     if prev is None:
@@ -360,12 +397,16 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
             for dst, src in zip((plan.a_self, plan.a_nbr, plan.b, plan.c), blocks):
                 if src.numel():
                     dst.view(-1)[: src.numel()].copy_(src.reshape(-1))
-        graphable = plan.use_graphs and cfg.sqp_iterations == 1
-        if graphable and plan.graphs is None and plan.runs >= 1:
-            plan.capture()
-        plan.enqueue()
+        if whole:
+            plan.graph.replay()
+        else:
+            if graphable and plan.graph is None and plan.runs >= 1:
+                # make sure the eager copies of this call are done before the
+                # capture's own side-stream work, then capture for later calls
+                plan.capture()
+            plan.enqueue()
+            plan.host_summary.copy_(plan.summary, non_blocking=True)
         plan.runs += 1
-        plan.host_summary.copy_(plan.summary, non_blocking=True)
         stream.synchronize()
         summ = plan.host_summary.numpy()
         status_code = int(summ[n_u])
@@ -391,10 +432,10 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
         last_applied = u_app.copy()
     else:
         last_applied = plan.u_applied.clone()
-    new_state = MpcState(lin_states=plan.next_states.clone(), lin_inputs=plan.next_inputs.clone(),
+    planned_states, planned_inputs, next_states, next_inputs = plan._carve(plan.outbuf.clone())
+    new_state = MpcState(lin_states=next_states, lin_inputs=next_inputs,
                          step_count=state.step_count + 1, last_applied=last_applied,
-                         planned_states=plan.planned_states.clone(),
-                         planned_inputs=plan.planned_inputs.clone(),
+                         planned_states=planned_states, planned_inputs=planned_inputs,
                          last_status=STATUS_BY_CODE[status_code], last_iterations=total_iters,
                          last_timing=timing, filtered_input=filtered)
     timing.total_ms = (time.perf_counter() - t_start) * 1e3
