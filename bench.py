@@ -486,7 +486,8 @@ def cfg5_arm(args, world, rank, local):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32/f64", "data": "synthetic",
             "config": {"workload": "cfg5: 2D mesh 400x250 = 100000 nodes, horizon 20",
-                       "parallelism": f"node partition x{world} (row slabs), NCCL halo per stage",
+                       "parallelism": (f"node partition x{world} (row slabs), NCCL halo per stage"
+                                       if world > 1 else "single GPU, fused persistent recursion + cost"),
                        "qp": {"status": st, "iterations": it}},
             "e2e": {"value": 1000.0 / m, "unit": "solves/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 64,

@@ -34,7 +34,10 @@
 
 namespace {
 
-constexpr int kQpThreads = 256;
+#ifndef QP_THREADS
+#define QP_THREADS 256
+#endif
+constexpr int kQpThreads = QP_THREADS;
 constexpr int kQpWarps = kQpThreads / 32;
 constexpr int kTB = 32;  // triangular-solve block
 

@@ -37,14 +37,22 @@ constexpr int kTS = 72;  // tile stride (doubles)
 // Pointers into shared memory that travel through structs / non-inlined
 // calls lose their address space and compile to generic LD/ST; asserting it
 // restores LDS/STS.
+#ifdef QP_NO_ASSUME
+#define QP_SMEM(p) ((void)0)
+#else
 #define QP_SMEM(p) __builtin_assume(__isShared(p))
+#endif
 
 __device__ __forceinline__ int ti(int I, int J) { return ((I * (I + 1)) >> 1) + J; }
 // in-tile offset of (r, c): column major, rows XOR-permuted by s(c) =
 // {0,0,4,4,2,2,6,6}[c] so that a column (fixed c), a row (fixed r), the DMMA
 // A/B fragments (rows 0..3 x cols 0..3 per half warp) and the transposed C
 // fragment pairs all hit distinct banks
+#ifdef QP_EO_OLD
+__device__ __forceinline__ int eo(int r, int c) { return c * 8 + (r ^ ((c & 2) << 1)); }
+#else
 __device__ __forceinline__ int eo(int r, int c) { return c * 8 + (r ^ (((c & 2) << 1) | ((c & 4) >> 1))); }
+#endif
 // element (R, C) with R >= C of the padded matrix
 __device__ __forceinline__ int gel(int R, int C) { return ti(R >> 3, C >> 3) * kTS + eo(R & 7, C & 7); }
 __host__ __device__ inline int tiles_for(int n) { return (n + 7) >> 3; }

@@ -259,8 +259,17 @@ class PartitionedMpc:
         ctx.call("gm_linearize", N, self.ls.data_ptr(), self.li.data_ptr(), self.a_self.data_ptr(),
                  self.a_nbr.data_ptr() if eng.E else None, self.b.data_ptr(), self.c.data_ptr(),
                  None, sp)
-        W = self.cond.gammas(self.a_self, self.a_nbr, self.b, self.c, self.x0)
-        self.cond.cost(ds, self.H0, self.g0)
+        if self.part.world == 1:
+            # nothing to exchange: the fused persistent recursion + cost kernel
+            # (K-COND) replaces the per-stage launches and the Gamma re-read
+            from .condensing import fused_device
+
+            W = self.cond.W
+            fused_device(eng, ds, self.a_self, self.a_nbr if eng.E else None, self.b, self.c,
+                         self.x0, W, self.cond.ld, N, self.H0, self.g0)
+        else:
+            W = self.cond.gammas(self.a_self, self.a_nbr, self.b, self.c, self.x0)
+            self.cond.cost(ds, self.H0, self.g0)
         if self.m0:
             rows_device(eng, ds, W, self.cond.ld, N, self.C0, self.d0)
             self.C0.mul_(self.row_mask[:, None])
