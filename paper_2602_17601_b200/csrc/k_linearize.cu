@@ -40,6 +40,9 @@ struct LinPlan {
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+// odd leading dimension for activation rows: rows read by different row
+// groups of a warp then fall into different banks
+__host__ __device__ inline int pld(int w) { return w | 1; }
 
 __host__ __device__ inline LinPlan make_plan(int TN, int EM, int nx, int nu, int n_p, int nin,
                                              int wpsi, int wphi, int hpsi, int hphi) {
@@ -52,8 +55,8 @@ __host__ __device__ inline LinPlan make_plan(int TN, int EM, int nx, int nu, int
   p.hpsi = hpsi;
   p.hphi = hphi;
   size_t o = 0;
-  const size_t f64ping = (size_t)max(EM * wpsi, TN * wphi);
-  const size_t f32ping = (size_t)max(TN * n_p * wphi, EM * n_p * wpsi);
+  const size_t f64ping = (size_t)max(EM * pld(wpsi), TN * pld(wphi));
+  const size_t f32ping = (size_t)max(TN * n_p * pld(wphi), EM * n_p * pld(wpsi));
   p.o_ef = o;    o = al16(o + sizeof(double) * EM * nx);
   p.o_z = o;     o = al16(o + sizeof(double) * TN * nin);
   p.o_p64a = o;  o = al16(o + sizeof(double) * f64ping);
@@ -241,10 +244,10 @@ __global__ void __launch_bounds__(kLinThreads, 3) k_linearize(const LinArgs a) {
       double* out = (l & 1) ? pb : pa;
       const bool relu = l < a.psi.L - 1;
       fwd_layer(cur, ldc, nE, a.psi.dims[l], a.psi.wt64[l], a.psi.b64[l], a.psi.dims[l + 1], out,
-                a.psi.dims[l + 1], relu ? mpsi + mask_off(a.psi, l) : nullptr, pl.hpsi, relu);
+                pld(a.psi.dims[l + 1]), relu ? mpsi + mask_off(a.psi, l) : nullptr, pl.hpsi, relu);
       __syncthreads();
       cur = out;
-      ldc = a.psi.dims[l + 1];
+      ldc = pld(a.psi.dims[l + 1]);
     }
     msg = cur;
     ldmsg = ldc;
@@ -267,12 +270,15 @@ __global__ void __launch_bounds__(kLinThreads, 3) k_linearize(const LinArgs a) {
       double* out = (l & 1) ? pb : pa;
       const bool relu = l < a.phi.L - 1;
       fwd_layer(cur, ldc, nN, a.phi.dims[l], a.phi.wt64[l], a.phi.b64[l], a.phi.dims[l + 1], out,
-                a.phi.dims[l + 1], relu ? mphi + mask_off(a.phi, l) : nullptr, pl.hphi, relu);
+                pld(a.phi.dims[l + 1]), relu ? mphi + mask_off(a.phi, l) : nullptr, pl.hphi, relu);
       __syncthreads();
       cur = out;
-      ldc = a.phi.dims[l + 1];
+      ldc = pld(a.phi.dims[l + 1]);
     }
-    dv = cur;  // (nN, n_p)
+    dv = cur;  // (nN, n_p), leading dimension ldv
+  }
+  const int ldv = pld(n_p);
+  {
   }
 
   // 4. f = step_array: v' = v + dv, p' = p + dt v' (gnn.py:157-158)
@@ -281,9 +287,9 @@ __global__ void __launch_bounds__(kLinThreads, 3) k_linearize(const LinArgs a) {
     const double* xi = Xp + (int64_t)(i0 + li) * nx;
     double val;
     if (k >= n_p) {
-      val = xi[k] + dv[li * n_p + (k - n_p)];
+      val = xi[k] + dv[li * ldv + (k - n_p)];
     } else {
-      const double v1 = xi[n_p + k] + dv[li * n_p + k];
+      const double v1 = xi[n_p + k] + dv[li * ldv + k];
       val = xi[k] + a.dt * v1;
     }
     fb[t] = val;
@@ -312,19 +318,20 @@ __global__ void __launch_bounds__(kLinThreads, 3) k_linearize(const LinArgs a) {
       for (int t = tid; t < R * wl; t += nt) {
         const int r = t / wl, j = t - r * wl;
         const int li = r / n_p, ro = r - li * n_p;
-        qa[t] = mphi[li * pl.hphi + mo + j] ? a.phi.w32[L - 1][ro * wl + j] : 0.f;
+        qa[r * pld(wl) + j] = mphi[li * pl.hphi + mo + j] ? a.phi.w32[L - 1][ro * wl + j] : 0.f;
       }
       __syncthreads();
       const float* cur = qa;
-      int ldc = wl;
+      int ldc = pld(wl);
       for (int l = L - 2; l >= 0; --l) {
         const int KK = a.phi.dims[l];
         float* out = (l == 0) ? jphi : ((cur == qa) ? qb : qa);
         const uint8_t* mk = (l >= 1) ? mphi + mask_off(a.phi, l - 1) : nullptr;
-        bwd_layer(cur, ldc, R, a.phi.dims[l + 1], a.phi.w32[l], KK, out, KK, mk, pl.hphi, n_p);
+        bwd_layer(cur, ldc, R, a.phi.dims[l + 1], a.phi.w32[l], KK, out, l == 0 ? KK : pld(KK), mk, pl.hphi,
+                  n_p);
         __syncthreads();
         cur = out;
-        ldc = KK;
+        ldc = pld(KK);
       }
     }
   }
@@ -338,19 +345,20 @@ __global__ void __launch_bounds__(kLinThreads, 3) k_linearize(const LinArgs a) {
       const int r = t / n_m, m = t - r * n_m;
       const int el = r / n_p, ro = r - el * n_p;
       const int li = a.dst[e0 + el] - i0;
-      qa[t] = jphi[(li * n_p + ro) * nin + nx + m];
+      qa[r * pld(n_m) + m] = jphi[(li * n_p + ro) * nin + nx + m];
     }
     __syncthreads();
     const float* cur = qa;
-    int ldc = n_m;
+    int ldc = pld(n_m);
     for (int l = L - 1; l >= 0; --l) {
       const int KK = a.psi.dims[l];
       float* out = (l == 0) ? Pe : ((cur == qa) ? qb : qa);
       const uint8_t* mk = (l >= 1) ? mpsi + mask_off(a.psi, l - 1) : nullptr;
-      bwd_layer(cur, ldc, R, a.psi.dims[l + 1], a.psi.w32[l], KK, out, KK, mk, pl.hpsi, n_p);
+      bwd_layer(cur, ldc, R, a.psi.dims[l + 1], a.psi.w32[l], KK, out, l == 0 ? KK : pld(KK), mk, pl.hpsi,
+                n_p);
       __syncthreads();
       cur = out;
-      ldc = KK;
+      ldc = pld(KK);
     }
   }
 
