@@ -118,6 +118,12 @@ int gm_set_node_range(gm_ctx* ctx, int64_t lo, int64_t hi);
 int gm_linearize(gm_ctx* ctx, int64_t P, const double* X, const double* U, float* a_self,
                  float* a_nbr, float* b, double* c, double* f_next, void* stream);
 
+/* Linearisation kernel selection: 0 = automatic (fused per-tile kernel for
+ * fewer than 200k node points, layer-wise GEMM chain above), 1 = always the
+ * fused kernel, 2 = always the layer-wise chain.  Both compute the same
+ * formulas; the switch exists for tests and benchmarks. */
+int gm_set_linearize_mode(gm_ctx* ctx, int mode);
+
 /* step_array only (gnn.py:153-159): f (P, M, nx) fp64. */
 int gm_step(gm_ctx* ctx, int64_t P, const double* X, const double* U, double* f, void* stream);
 

@@ -54,6 +54,7 @@ _SIGNATURES = {
     "gm_set_node_range": (c_int, [c_void_p, c_i64, c_i64]),
     "gm_linearize": (c_int, [c_void_p, c_i64, P, P, P, P, P, P, P, c_void_p]),
     "gm_step": (c_int, [c_void_p, c_i64, P, P, P, c_void_p]),
+    "gm_set_linearize_mode": (c_int, [c_void_p, c_int]),
     "gm_gamma_ld": (c_int, [c_int, c_int]),
     "gm_condense_gammas": (c_int, [c_void_p, c_int, c_int, P, P, P, P, P, P, c_int, c_void_p]),
     "gm_condense_gammas_stage": (c_int, [c_void_p, c_int, c_int, c_int, P, P, P, P, P, P, c_int,

@@ -29,6 +29,9 @@
 
 #include "common.cuh"
 
+int launch_linearize_layers(gm_ctx* ctx, int64_t P, const double* X, const double* U, float* a_self,
+                            float* a_nbr, float* b, double* c, double* f_next, void* stream);
+
 namespace {
 
 constexpr int kLinThreads = 256;
@@ -440,6 +443,15 @@ int launch_linearize(gm_ctx* ctx, int64_t P, const double* X, const double* U, f
   if (P < 0) return gm_fail(ctx, GM_ERR_CONFIG, "negative point count");
   const int64_t lo = ctx->node_lo, hi = gm_node_hi(ctx);
   if (P == 0 || hi <= lo) return GM_OK;
+  // Jacobians of large problems: layer-wise GEMM chain (k_linearize_layers.cu)
+  // unless phi is a single layer; the fused per-tile kernel below serves
+  // small problems, step_array (no Jacobian) and that corner case
+  // (latency-bound small problems -- cfg3's 20 K node points -- stay on the
+  // fused kernel: ~27 launches of small GEMMs cost more than one fused pass)
+  constexpr int64_t kLayerMinRows = 200000;
+  const bool big = P * (hi - lo) >= kLayerMinRows;
+  if (jac && ctx->phi.L >= 2 && ctx->psi.L >= 1 && (ctx->lin_mode == 2 || (ctx->lin_mode == 0 && big)))
+    return launch_linearize_layers(ctx, P, X, U, a_self, a_nbr, b, c, f_next, stream);
   const int nx = ctx->m_nx, nu = ctx->m_nu, n_p = ctx->n_p;
   const int nin = ctx->phi.dims[0];
   const int wpsi = ctx->psi.max_width(), wphi = ctx->phi.max_width();
@@ -503,6 +515,13 @@ int gm_linearize(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   if (!a_self || !b || !c || (ctx && ctx->E > 0 && !a_nbr))
     return gm_fail(ctx, GM_ERR_CONFIG, "null output buffer");
   return launch_linearize(ctx, P, X, U, a_self, a_nbr, b, c, f_next, 1, stream);
+}
+
+int gm_set_linearize_mode(gm_ctx* ctx, int mode) {
+  if (!ctx) return GM_ERR_CONFIG;
+  if (mode < 0 || mode > 2) return gm_fail(ctx, GM_ERR_CONFIG, "linearize mode must be 0, 1 or 2");
+  ctx->lin_mode = mode;
+  return GM_OK;
 }
 
 int gm_step(gm_ctx* ctx, int64_t P, const double* X, const double* U, double* f, void* stream) {

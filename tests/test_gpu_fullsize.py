@@ -27,11 +27,18 @@ def cfg3():
                 gx=gx, qp=qp, sol=sol, n0=n0)
 
 
-def test_cfg3_stages(cfg3):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_cfg3_stages(cfg3, mode):
+    """mode 1: fused per-tile linearisation, 2: layer-wise GEMM chain."""
     import paper_2602_17601_b200 as pkg
 
     c = cfg3
-    lin = pkg.linearize_trajectory(c["model"], c["topo"], c["states"], c["inputs"])
+    ctx = pkg.device.engine(c["topo"], c["model"]).ctx
+    ctx.call("gm_set_linearize_mode", mode)
+    try:
+        lin = pkg.linearize_trajectory(c["model"], c["topo"], c["states"], c["inputs"])
+    finally:
+        ctx.call("gm_set_linearize_mode", 0)
     for k in ("a_self", "a_nbr", "b"):
         assert rel(getattr(lin, k), getattr(c["lin"], k)) <= TOL, k
     assert np.max(np.abs(lin.c - c["lin"].c)) / np.max(np.abs(c["states"])) <= TOL

@@ -27,10 +27,20 @@ def pkg():
     return p
 
 
+def _set_lin_mode(pkg, cs, mode):
+    """Force the fused (1) or layer-wise (2) linearisation kernels; 0 = auto."""
+    pkg.device.engine(cs.topo, cs.model).ctx.call("gm_set_linearize_mode", mode)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("name", CASES)
-def test_linearize_matches_reference(pkg, name):
+def test_linearize_matches_reference(pkg, name, mode):
     cs = pipeline_case(name)
-    lin = pkg.linearize_trajectory(cs.model, cs.topo, cs.states, cs.inputs)
+    _set_lin_mode(pkg, cs, mode)
+    try:
+        lin = pkg.linearize_trajectory(cs.model, cs.topo, cs.states, cs.inputs)
+    finally:
+        _set_lin_mode(pkg, cs, 0)
     assert lin.on_device
     d = cs.d
     for k in ("a_self", "a_nbr", "b"):
@@ -39,12 +49,17 @@ def test_linearize_matches_reference(pkg, name):
     assert float(np.max(np.abs(lin.c - d["lin_c"]))) / xscale <= TOL
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("name", CASES)
-def test_affine_model_exact_at_point(pkg, name):
+def test_affine_model_exact_at_point(pkg, name, mode):
     """x+ = A x + sum A_nbr x_j + B u + c reproduces step_array (gnn.py:291-297)."""
     cs = pipeline_case(name)
     N = cs.inputs.shape[0]
-    lin = pkg.linearize_trajectory(cs.model, cs.topo, cs.states, cs.inputs)
+    _set_lin_mode(pkg, cs, mode)
+    try:
+        lin = pkg.linearize_trajectory(cs.model, cs.topo, cs.states, cs.inputs)
+    finally:
+        _set_lin_mode(pkg, cs, 0)
     X = cs.states[:N]
     f = pkg.step_array(cs.model, cs.topo, X, cs.inputs)
     rec = np.einsum("kiab,kib->kia", lin.a_self, X) + np.einsum("kiab,kb->kia", lin.b, cs.inputs) + lin.c
