@@ -33,7 +33,7 @@ enum { kFwdHidden = 0, kFwdLast = 1, kBwd = 2 };
 // out[r][c] = epi(sum_k in[r][k] W[k][c]), W (K, N) row-major.  Block: BR rows
 // x all N columns; thread (rg, cg) owns rows rg*RT.., columns cg*CT..
 template <typename T, int RT, int CT, int MODE>
-__global__ void __launch_bounds__(kLT) k_layer(const T* __restrict__ in, int ldi, int64_t R, int K,
+__global__ void __launch_bounds__(kLT) k_layer(const T* __restrict__ in, int ldi, int R, int K,
                                                const T* __restrict__ W, int N, const T* __restrict__ bias,
                                                T* __restrict__ out, int ldo, uint8_t* __restrict__ mask,
                                                int ldm, int rows_per) {
@@ -42,12 +42,13 @@ __global__ void __launch_bounds__(kLT) k_layer(const T* __restrict__ in, int ldi
   const int CG = N / CT, RGB = kLT / CG, BR = RGB * RT, ldx = BR + 1;
   T* Ws = (T*)sm;      // K x N
   T* Xs = Ws + K * N;  // K x ldx: transposed input tile
-  const int64_t rb = (int64_t)blockIdx.x * BR;
+  const int rb = blockIdx.x * BR;
   for (int t = tid; t < K * N; t += kLT) Ws[t] = W[t];
+#pragma unroll 8
   for (int t = tid; t < BR * K; t += kLT) {
     const int r = t / K, k = t - r * K;
-    const int64_t gr = rb + r;
-    Xs[k * ldx + r] = gr < R ? in[gr * ldi + k] : T(0);
+    const int gr = rb + r;
+    Xs[k * ldx + r] = gr < R ? in[(int64_t)gr * ldi + k] : T(0);
   }
   __syncthreads();
   const int cg = tid % CG, rg = tid / CG;
@@ -72,8 +73,9 @@ __global__ void __launch_bounds__(kLT) k_layer(const T* __restrict__ in, int ldi
   }
 #pragma unroll
   for (int t = 0; t < RT; ++t) {
-    const int64_t r = rb + rl + t;
+    const int r = rb + rl + t;
     if (r >= R) break;
+    const int mrow = MODE == kBwd ? r / rows_per : r;
 #pragma unroll
     for (int u = 0; u < CT; ++u) {
       const int c = c0 + u;
@@ -81,14 +83,14 @@ __global__ void __launch_bounds__(kLT) k_layer(const T* __restrict__ in, int ldi
       if constexpr (MODE == kFwdHidden) {
         v += bias[c];
         const bool m = v > T(0);  // strict: derivative 0 at the kink (mlp.py:143)
-        mask[r * ldm + c] = m;
+        mask[(int64_t)r * ldm + c] = m;
         v = m ? v : T(0);
       } else if constexpr (MODE == kFwdLast) {
         v += bias[c];
       } else {
-        if (mask && !mask[(r / rows_per) * ldm + c]) v = T(0);
+        if (mask && !mask[(int64_t)mrow * ldm + c]) v = T(0);
       }
-      out[r * ldo + c] = v;
+      out[(int64_t)r * ldo + c] = v;
     }
   }
 }
@@ -97,13 +99,14 @@ template <typename T, int RT, int MODE>
 int launch_layer(gm_ctx* ctx, const T* in, int ldi, int64_t R, int K, const T* W, int N, const T* bias,
                  T* out, int ldo, uint8_t* mask, int ldm, int rows_per, cudaStream_t st) {
   if (R <= 0) return GM_OK;
+  if (R >= (int64_t(1) << 31)) return gm_fail(ctx, GM_ERR_CONFIG, "too many rows for one layer launch");
   auto go = [&](auto kern, int CT) -> int {
     const int CG = N / CT, BR = (kLT / CG) * RT;
     const size_t smem = sizeof(T) * ((size_t)K * N + (size_t)K * (BR + 1));
     if (smem > ctx->smem_optin) return gm_fail(ctx, GM_ERR_CONFIG, "layer too wide for the layer GEMM");
     GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (R + BR - 1) / BR;
-    kern<<<(unsigned)blocks, kLT, smem, st>>>(in, ldi, R, K, W, N, bias, out, ldo, mask, ldm, rows_per);
+    kern<<<(unsigned)blocks, kLT, smem, st>>>(in, ldi, (int)R, K, W, N, bias, out, ldo, mask, ldm, rows_per);
     GM_LAUNCH_CHECK(ctx, "k_layer");
     return GM_OK;
   };
@@ -114,17 +117,17 @@ int launch_layer(gm_ctx* ctx, const T* in, int ldi, int64_t R, int K, const T* W
 
 struct LinDims {
   int M, nx, nu, n_p, n_m, nin, lo, nN, e0, nE;
-  int64_t P, Rn, Re;
+  int P, Rn, Re;  // every element count below stays < 2^31 (host check)
 };
 
 // edge features e = (x_dst - x_src) / s_x over all (point, owned edge)
 __global__ void k_lin_edges(const LinDims d, const int* __restrict__ dst, const int* __restrict__ src,
                             const double* __restrict__ X, const double* __restrict__ norm, double* ef) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= d.Re * d.nx) return;
-  const int64_t re = t / d.nx;
+  const int re = t / d.nx;
   const int k = (int)(t - re * d.nx);
-  const int64_t p = re / d.nE;
+  const int p = re / d.nE;
   const int e = d.e0 + (int)(re - p * d.nE);
   const double* Xp = X + p * (int64_t)d.M * d.nx;
   ef[t] = (Xp[(int64_t)dst[e] * d.nx + k] - Xp[(int64_t)src[e] * d.nx + k]) / norm[d.nx + k];
@@ -134,11 +137,11 @@ __global__ void k_lin_edges(const LinDims d, const int* __restrict__ dst, const 
 __global__ void k_lin_z(const LinDims d, const int* __restrict__ ptr, const double* __restrict__ X,
                         const double* __restrict__ U, const double* __restrict__ norm,
                         const double* __restrict__ msg, int ldmsg, double* z) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= d.Rn * d.nin) return;
-  const int64_t rn = t / d.nin;
+  const int rn = t / d.nin;
   const int k = (int)(t - rn * d.nin);
-  const int64_t p = rn / d.nN;
+  const int p = rn / d.nN;
   const int i = d.lo + (int)(rn - p * d.nN);
   const int nx = d.nx;
   double v;
@@ -158,11 +161,11 @@ __global__ void k_lin_z(const LinDims d, const int* __restrict__ ptr, const doub
 // f = step_array: v' = v + dv, p' = p + dt v' (gnn.py:157-158)
 __global__ void k_lin_f(const LinDims d, double dt, const double* __restrict__ X,
                         const double* __restrict__ dv, int ldv, double* f, double* f_next) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= d.Rn * d.nx) return;
-  const int64_t rn = t / d.nx;
+  const int rn = t / d.nx;
   const int k = (int)(t - rn * d.nx);
-  const int64_t p = rn / d.nN;
+  const int p = rn / d.nN;
   const int i = d.lo + (int)(rn - p * d.nN);
   const double* xi = X + (p * d.M + i) * d.nx;
   const int n_p = d.n_p;
@@ -180,11 +183,11 @@ __global__ void k_lin_f(const LinDims d, double dt, const double* __restrict__ X
 // phi Jacobian seed: row (node, ro) = W_L[ro] masked by the node's last hidden layer
 __global__ void k_lin_seed_phi(const LinDims d, const float* __restrict__ wL, int wl,
                                const uint8_t* __restrict__ mphi, int hphi, int mo, float* q, int ldq) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= d.Rn * d.n_p * wl) return;
-  const int64_t r = t / wl;
+  const int r = t / wl;
   const int j = (int)(t - r * wl);
-  const int64_t rn = r / d.n_p;
+  const int rn = r / d.n_p;
   const int ro = (int)(r - rn * d.n_p);
   q[r * ldq + j] = mphi[rn * hphi + mo + j] ? wL[ro * wl + j] : 0.f;
 }
@@ -192,27 +195,27 @@ __global__ void k_lin_seed_phi(const LinDims d, const float* __restrict__ wL, in
 // psi VJP seed: row (edge, ro) = J_m of the edge's destination node
 __global__ void k_lin_seed_psi(const LinDims d, const int* __restrict__ dst, const float* __restrict__ jphi,
                                float* q, int ldq) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= d.Re * d.n_p * d.n_m) return;
-  const int64_t r = t / d.n_m;
+  const int r = t / d.n_m;
   const int m = (int)(t - r * d.n_m);
-  const int64_t re = r / d.n_p;
+  const int re = r / d.n_p;
   const int ro = (int)(r - re * d.n_p);
-  const int64_t p = re / d.nE;
+  const int p = re / d.nE;
   const int e = d.e0 + (int)(re - p * d.nE);
-  const int64_t rn = p * d.nN + (dst[e] - d.lo);
+  const int rn = p * d.nN + (dst[e] - d.lo);
   q[r * ldq + m] = jphi[(rn * d.n_p + ro) * d.nin + d.nx + m];
 }
 
 // a_nbr blocks of every (point, owned edge) (gnn.py:266, :282-285)
 __global__ void k_lin_nbr(const LinDims d, float dtf, const double* __restrict__ norm,
                           const float* __restrict__ Pe, int E, float* a_nbr) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int nx = d.nx, n_p = d.n_p;
   if (t >= d.Re * n_p * nx) return;
-  const int64_t re = t / (n_p * nx);
+  const int re = t / (n_p * nx);
   const int rem = (int)(t - re * n_p * nx), r = rem / nx, cc = rem - r * nx;
-  const int64_t p = re / d.nE;
+  const int p = re / d.nE;
   const int e = d.e0 + (int)(re - p * d.nE);
   const float inv_sx = (float)(1.0 / norm[nx + cc]);
   const float jv = -Pe[(re * n_p + r) * nx + cc] * inv_sx;
@@ -225,12 +228,12 @@ __global__ void k_lin_nbr(const LinDims d, float dtf, const double* __restrict__
 __global__ void k_lin_self(const LinDims d, float dtf, const int* __restrict__ ptr,
                            const double* __restrict__ norm, const float* __restrict__ jphi,
                            const float* __restrict__ Pe, float* a_self, float* b) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int nx = d.nx, nu = d.nu, n_p = d.n_p, w = nx + nu;
   if (t >= d.Rn * n_p * w) return;
-  const int64_t rn = t / (n_p * w);
+  const int rn = t / (n_p * w);
   const int rem = (int)(t - rn * n_p * w), r = rem / w, cc = rem - r * w;
-  const int64_t p = rn / d.nN;
+  const int p = rn / d.nN;
   const int i = d.lo + (int)(rn - p * d.nN);
   const float* jr = jphi + (rn * n_p + r) * d.nin;
   if (cc < nx) {
@@ -256,12 +259,12 @@ __global__ void k_lin_c(const LinDims d, int E, const int* __restrict__ ptr, con
                         const double* __restrict__ X, const double* __restrict__ U, const double* __restrict__ f,
                         const float* __restrict__ a_self, const float* __restrict__ a_nbr,
                         const float* __restrict__ b, double* c) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int nx = d.nx, nu = d.nu;
   if (t >= d.Rn * nx) return;
-  const int64_t rn = t / nx;
+  const int rn = t / nx;
   const int r = (int)(t - rn * nx);
-  const int64_t p = rn / d.nN;
+  const int p = rn / d.nN;
   const int i = d.lo + (int)(rn - p * d.nN);
   const double* Xp = X + p * (int64_t)d.M * nx;
   const double* xi = Xp + (int64_t)i * nx;
@@ -284,10 +287,10 @@ inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
-// Layer-wise linearisation over P points (owned node range); same contract
-// as gm_linearize.  Returns GM_OK or an error code.
-int launch_linearize_layers(gm_ctx* ctx, int64_t P, const double* X, const double* U, float* a_self,
-                            float* a_nbr, float* b, double* c, double* f_next, void* stream) {
+namespace {
+
+int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float* a_self, float* a_nbr,
+                 float* b, double* c, double* f_next, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t lo = ctx->node_lo, hi = gm_node_hi(ctx);
   LinDims d{};
@@ -301,9 +304,9 @@ int launch_linearize_layers(gm_ctx* ctx, int64_t P, const double* X, const doubl
   d.nN = (int)(hi - lo);
   d.e0 = (int)ctx->h_ptr[lo];
   d.nE = (int)(ctx->h_ptr[hi] - ctx->h_ptr[lo]);
-  d.P = P;
-  d.Rn = P * d.nN;
-  d.Re = P * d.nE;
+  d.P = (int)P;  // chunked by the caller: every element count fits in int
+  d.Rn = (int)(P * (hi - lo));
+  d.Re = (int)(P * (ctx->h_ptr[hi] - ctx->h_ptr[lo]));
   const MlpView psi = ctx->psi.view(), phi = ctx->phi.view();
   const int wpsi = ctx->psi.max_width(), wphi = ctx->phi.max_width();
   const int hpsi = ctx->psi.hidden_sum(), hphi = ctx->phi.hidden_sum();
@@ -436,5 +439,36 @@ int launch_linearize_layers(gm_ctx* ctx, int64_t P, const double* X, const doubl
   k_lin_c<<<grid_for(d.Rn * nx), 256, 0, st>>>(d, (int)ctx->E, ctx->d_ptr, ctx->d_src, X, U, fb, a_self, a_nbr,
                                                b, c);
   GM_LAUNCH_CHECK(ctx, "k_lin_c");
+  return GM_OK;
+}
+
+// largest per-point element count of any intermediate buffer
+int64_t per_point_elements(const gm_ctx* ctx) {
+  const int64_t nN = gm_node_hi(ctx) - ctx->node_lo;
+  const int64_t nE = ctx->h_ptr[gm_node_hi(ctx)] - ctx->h_ptr[ctx->node_lo];
+  const int64_t wpsi = pld(ctx->psi.max_width()), wphi = pld(ctx->phi.max_width()), n_p = ctx->n_p;
+  const int64_t nin = ctx->phi.dims[0];
+  int64_t m = std::max({nE * n_p * wpsi, nN * n_p * wphi, nN * n_p * nin, nE * wpsi, nN * wphi,
+                        (int64_t)nE * ctx->psi.hidden_sum(), (int64_t)nN * ctx->phi.hidden_sum()});
+  return std::max<int64_t>(m, 1);
+}
+
+}  // namespace
+
+// Layer-wise linearisation over P points (owned node range); same contract
+// as gm_linearize.  Points are processed in chunks so every buffer index fits
+// in 32 bits and the workspace stays below ~2^30 elements per buffer.
+int launch_linearize_layers(gm_ctx* ctx, int64_t P, const double* X, const double* U, float* a_self,
+                            float* a_nbr, float* b, double* c, double* f_next, void* stream) {
+  const int64_t M = ctx->M, E = ctx->E;
+  const int nx = ctx->m_nx, nu = ctx->m_nu;
+  const int64_t chunk = std::max<int64_t>(1, (int64_t(1) << 30) / per_point_elements(ctx));
+  for (int64_t p0 = 0; p0 < P; p0 += chunk) {
+    const int64_t np = std::min(chunk, P - p0);
+    const int rc = layers_chunk(ctx, np, X + p0 * M * nx, U + p0 * nu, a_self + p0 * M * nx * nx,
+                                a_nbr ? a_nbr + p0 * E * nx * nx : nullptr, b + p0 * M * nx * nu, c + p0 * M * nx,
+                                f_next ? f_next + p0 * M * nx : nullptr, stream);
+    if (rc) return rc;
+  }
   return GM_OK;
 }
