@@ -52,8 +52,7 @@ __global__ void __launch_bounds__(kLT) k_layer(const T* __restrict__ in, int ldi
   }
   __syncthreads();
   const int cg = tid % CG, rg = tid / CG;
-  if (rg >= RGB) return;
-  const int c0 = cg * CT, rl = rg * RT;
+  const int c0 = cg * CT, rl = min(rg, RGB - 1) * RT;  // idle threads (rg >= RGB) shadow the last group
   T acc[RT][CT];
 #pragma unroll
   for (int t = 0; t < RT; ++t)
@@ -71,27 +70,42 @@ __global__ void __launch_bounds__(kLT) k_layer(const T* __restrict__ in, int ldi
 #pragma unroll
       for (int u = 0; u < CT; ++u) acc[t][u] = fma(x[t], w[u], acc[t][u]);
   }
+  // epilogue into a row-major output tile in shared memory (the input tile is
+  // dead), then coalesced row-contiguous stores of values and mask bytes
+  __syncthreads();
+  const int ldt = N + 1;
+  T* Os = Xs;                                            // BR x ldt
+  uint8_t* Ms = (uint8_t*)(Xs + (size_t)BR * ldt);        // BR x N (hidden layers)
+  if (rg < RGB) {
 #pragma unroll
-  for (int t = 0; t < RT; ++t) {
-    const int r = rb + rl + t;
-    if (r >= R) break;
-    const int mrow = MODE == kBwd ? r / rows_per : r;
+    for (int t = 0; t < RT; ++t) {
+      const int rloc = rl + t;
+      const int r = rb + rloc;
+      const int mrow = MODE == kBwd ? r / rows_per : r;
 #pragma unroll
-    for (int u = 0; u < CT; ++u) {
-      const int c = c0 + u;
-      T v = acc[t][u];
-      if constexpr (MODE == kFwdHidden) {
-        v += bias[c];
-        const bool m = v > T(0);  // strict: derivative 0 at the kink (mlp.py:143)
-        mask[(int64_t)r * ldm + c] = m;
-        v = m ? v : T(0);
-      } else if constexpr (MODE == kFwdLast) {
-        v += bias[c];
-      } else {
-        if (mask && !mask[(int64_t)mrow * ldm + c]) v = T(0);
+      for (int u = 0; u < CT; ++u) {
+        const int c = c0 + u;
+        T v = acc[t][u];
+        if constexpr (MODE == kFwdHidden) {
+          v += bias[c];
+          const bool m = v > T(0);  // strict: derivative 0 at the kink (mlp.py:143)
+          Ms[rloc * N + c] = m;
+          v = m ? v : T(0);
+        } else if constexpr (MODE == kFwdLast) {
+          v += bias[c];
+        } else {
+          if (mask && r < R && !mask[(int64_t)mrow * ldm + c]) v = T(0);
+        }
+        Os[rloc * ldt + c] = v;
       }
-      out[(int64_t)r * ldo + c] = v;
     }
+  }
+  __syncthreads();
+  const int rows = min(BR, R - rb);
+  for (int t = tid; t < rows * N; t += kLT) {
+    const int rloc = t / N, c = t - rloc * N;
+    out[(int64_t)(rb + rloc) * ldo + c] = Os[rloc * ldt + c];
+    if constexpr (MODE == kFwdHidden) mask[(int64_t)(rb + rloc) * ldm + c] = Ms[rloc * N + c];
   }
 }
 
@@ -102,7 +116,9 @@ int launch_layer(gm_ctx* ctx, const T* in, int ldi, int64_t R, int K, const T* W
   if (R >= (int64_t(1) << 31)) return gm_fail(ctx, GM_ERR_CONFIG, "too many rows for one layer launch");
   auto go = [&](auto kern, int CT) -> int {
     const int CG = N / CT, BR = (kLT / CG) * RT;
-    const size_t smem = sizeof(T) * ((size_t)K * N + (size_t)K * (BR + 1));
+    const size_t tile_in = sizeof(T) * (size_t)K * (BR + 1);
+    const size_t tile_out = sizeof(T) * (size_t)BR * (N + 1) + (size_t)BR * N;
+    const size_t smem = sizeof(T) * (size_t)K * N + ((std::max(tile_in, tile_out) + 15) & ~size_t(15));
     if (smem > ctx->smem_optin) return gm_fail(ctx, GM_ERR_CONFIG, "layer too wide for the layer GEMM");
     GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (R + BR - 1) / BR;
