@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=8, help="oracle steps for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-l2-flush", action="store_true")
-    ap.add_argument("--workload", choices=["cfg3", "cfg4", "cfg5"], default="cfg3",
+    ap.add_argument("--workload", choices=["cfg2", "cfg3", "cfg4", "cfg5"], default="cfg3",
                     help="cfg3 (default, headline latency); cfg4: 4096 instances of M=200 "
                          "sharded over ranks; cfg5: 400x250 mesh, node-partitioned over ranks")
     ap.add_argument("--batch", type=int, default=4096, help="cfg4 total instances")
@@ -456,6 +456,91 @@ def cfg4_arm(args, world, rank, local):
         torch.distributed.destroy_process_group()
 
 
+def cfg2_arm(args, world, rank, local):
+    """Closed-loop tracking, chain M=100 (BASELINE cfg2): ChainConfig(100),
+    settled 3 s, end effector on a 0.04 m / 8 s circle around its settled
+    position, default TrackingWeights, random-init GNN (no training data),
+    horizon 20.  A step = one controller step (mpc_step) + one plant period
+    (device kernel); the state stays on the device, per step x_ref (H2D) and
+    [u, status, iterations] (D2H) cross.  Replicas at N>1 (no collective)."""
+    import torch
+
+    import paper_2602_17601_b200 as pkg
+    from paper_2602_17601_b200.graph import chain_topology
+    from paper_2602_17601_b200.tracking import (TrackingWeights, circle_reference,
+                                                 run_closed_loop_device, tracking_spec_provider)
+    from paper_2602_17601_b200.trunk import ChainConfig, DevicePlant
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    M, N = 100, 20
+    pc = ChainConfig(node_count=M)
+    topo = chain_topology(M)
+    model = pkg.init_model(3, 6, 0.01, np.random.default_rng(0), out_scale=0.05)
+    plant = DevicePlant(pc, topo)
+    x0 = plant.settle(3.0)
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+    center = x0[-1, :3].cpu().numpy()
+    prov = tracking_spec_provider(topo, cfg, pkg.SystemState(x0.cpu().numpy()),
+                                  circle_reference(0.04, 8.0, center), TrackingWeights(), pc.n_u, pc.u_max)
+    run_closed_loop_device(plant, model, topo, prov, x0, args.warmup, cfg)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local); clocks.start()
+    t0 = time.perf_counter()
+    log = run_closed_loop_device(plant, model, topo, prov, x0, args.steps, cfg)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) / args.steps * 1e3
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    tm = log.timings.mean(axis=0)
+    cpu = None
+    if not args.no_cpu_baseline:
+        from threadpoolctl import threadpool_limits
+
+        from oracle import ref_port as O
+        P = O.trunk_params(M)
+        specs = O.tracking_specs(topo, N, 0.01, x0.cpu().numpy(), O.circle_ref(0.04, 8.0, center), 6, 8.0)
+        n_cpu = max(2, min(args.cpu_steps, 6))
+        with threadpool_limits(limits=1):
+            c0 = time.perf_counter()
+            O.closed_loop(model, topo, P, specs, x0.cpu().numpy(), n_cpu, N)
+            cms = (time.perf_counter() - c0) / n_cpu * 1e3
+        cpu = {"value": 1000.0 / cms, "unit": "steps/s", "cores": 1, "kind": "port",
+               "sample": f"{n_cpu} closed-loop steps (oracle mpc_step + numpy plant) at M={M}, N={N}, "
+                         "BLAS pinned to 1 thread", "ms_per_step": cms}
+    print(json.dumps({
+        "metric": METRIC, "value": world * 1000.0 / ms, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "hz": 1000.0 / ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic (random-init GNN, trunk plant)",
+        "config": {"workload": "cfg2: closed-loop tracking, soft-trunk-like chain M=100, horizon 20",
+                   "plant": "trunk.py chain on the device (10 substeps)", "reference": "circle r=0.04 m, T=8 s",
+                   "parallelism": f"independent closed loop per GPU x{world}",
+                   "optimal_fraction": log.optimal_fraction(),
+                   "mean_qp_iterations": float(np.mean(log.iterations))},
+        "stage_ms": {"linearize": float(tm[0]), "condense": float(tm[1]), "solve_and_epilogue": float(tm[2]),
+                     "mpc_step_total": float(tm[3])},
+        "e2e": {"value": world * 1000.0 / ms, "unit": "steps/s", "ms_per_step": ms,
+                "h2d_bytes_per_step": M * (N + 1) * 6 * 8, "d2h_bytes_per_step": (6 + 2) * 8,
+                "path": "tracking.run_closed_loop_device (public API, wall clock)"},
+        "clocks": clk, "cpu_baseline": cpu}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def cfg5_arm(args, world, rank, local):
     """400x250 mesh (1e5 nodes), N=20, node-partitioned over ranks with a
     per-stage NCCL halo exchange and an all-reduce of H and g."""
@@ -521,7 +606,9 @@ def main():
     if args.impl == "reference":
         reference_arm(args, world, rank)
         return
-    if args.workload == "cfg4":
+    if args.workload == "cfg2":
+        cfg2_arm(args, world, rank, local)
+    elif args.workload == "cfg4":
         cfg4_arm(args, world, rank, local)
     elif args.workload == "cfg5":
         cfg5_arm(args, world, rank, local)

@@ -229,6 +229,19 @@ int gm_mpc_finish(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const d
                   double* planned_states, double* planned_inputs, double* next_states,
                   double* next_inputs, double* u_applied, double* summary, void* stream);
 
+/* ---- cfg2 plant: trunk.py chain (trunk.py:116-160) ------------------------ */
+/* One controller period (substeps semi-implicit Euler substeps of dt_sim) of B
+ * chain plants with M nodes: X, Xout (B, M, 6) fp64 [p | v], U (B, nu) fp64
+ * tendon tensions (clipped to [0, u_max] when clip != 0, trunk.py:152),
+ * rest (M, 3) rest positions, fmap (M, 3, nu) tendon force map (device);
+ * gravity (3) is a HOST array.
+ * *bad (device int) is set to 1 when a state becomes non-finite (the
+ * reference raises FloatingPointError, trunk.py:158-159). */
+int gm_trunk_step(gm_ctx* ctx, int B, int M, int nu, int substeps, double dt_sim, double mass,
+                  double k, double c, double kb, double rest_len, const double* gravity,
+                  const double* rest, const double* fmap, double u_max, int clip, const double* X,
+                  const double* U, double* Xout, int32_t* bad, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

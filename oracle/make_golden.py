@@ -34,6 +34,47 @@ def _ref():
     return rc, rex, rg, rgr, rmlp, rm, rq
 
 
+def cfg2_closed_loop():
+    """Closed-loop tracking with the reference's own plant, provider and
+    run_closed_loop (cfg2 stack, reduced: M=10 nodes, N=10, 6 steps after a
+    0.5 s settle; circle r=0.04 m, period 8 s around the settled tip), plus
+    single plant steps at random states / inputs."""
+    sys.path.insert(0, str(REF))
+    import gnnmpc.experiments as rex
+    import gnnmpc.gnn as rg
+    import gnnmpc.graph as rgr
+    import gnnmpc.mpc as rm
+    import gnnmpc.references as rr
+    import gnnmpc.trunk as rt
+
+    out = {}
+    M, N, steps = 10, 10, 6
+    pc = rt.ChainConfig(node_count=M)
+    x0 = rt.settle(pc, 0.5)
+    topo = rgr.chain_topology(M)
+    model = rg.init_model(3, 6, 0.01, np.random.default_rng(3), n_m=16, psi_hidden=(32, 32),
+                          phi_hidden=(64, 64), out_scale=0.05)
+    cfg = rm.MpcConfig(horizon=N, dt=0.01)
+    center = x0.array[-1, :3].copy()
+    ref = rr.circle_reference(0.04, 8.0, center)
+    prov = rex.tracking_spec_provider(topo, cfg, x0, ref, rex.TrackingWeights(), pc.n_u, pc.u_max)
+    log = rm.run_closed_loop(rex.make_plant_step(pc), model, topo, prov, x0, steps, cfg)
+    _model_arrays("m_", model, out)
+    out["x0"] = x0.array
+    out["center"] = center
+    out["states"] = log.states
+    out["inputs"] = log.inputs
+    out["iterations"] = log.iterations
+    out["statuses"] = np.array([s.value for s in log.statuses])
+    rng = np.random.default_rng(7)
+    arr = x0.array + 0.01 * rng.standard_normal((M, 6))
+    u = rng.uniform(-1.0, 9.0, 6)
+    out["plant_in"] = arr
+    out["plant_u"] = u
+    out["plant_out"] = rt.step_state_array(pc, arr, u)
+    np.savez_compressed(OUT / "cfg2_closed_loop.npz", **out)
+
+
 def _model_arrays(prefix, model, out):
     for name, mlp in (("psi", model.psi), ("phi", model.phi)):
         out[f"{prefix}{name}_dims"] = np.asarray(mlp.layer_dims)
@@ -265,4 +306,7 @@ def main():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "cfg2":
+        cfg2_closed_loop()
+        raise SystemExit(0)
     main()

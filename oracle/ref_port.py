@@ -583,3 +583,124 @@ def mpc_step(model, topo, spec, x_measured, lin_states, lin_inputs, horizon, war
         timings.update(tm)
     return dict(u_applied=u_app, lin_states=ns, lin_inputs=ni, planned_states=planned_states,
                 planned_inputs=planned_inputs, status=status, iterations=iters)
+
+
+# --------------------------------------------------------------------------
+# chain plant (trunk.py) and closed-loop tracking (experiments.py, mpc.py)
+# -- the environment of BASELINE cfg2, used to check the device closed loop
+# --------------------------------------------------------------------------
+
+def trunk_params(node_count, node_mass=0.08, coupling_stiffness=300.0, coupling_damping=2.0,
+                 bend_stiffness=25.0, rest_length=0.15, gravity=(0.0, 0.0, -9.81), u_max=8.0,
+                 dt_sim=1e-3, dt=0.01):
+    """ChainConfig defaults (trunk.py:23-73) as a dict; six horizontal tendons
+    60 degrees apart, each attached to every moving node (trunk.py:51-61)."""
+    angles = np.deg2rad([0, 60, 120, 180, 240, 300])
+    dirs = np.stack([np.cos(angles), np.sin(angles), np.zeros(6)], axis=1)
+    M = node_count
+    fmap = np.zeros((M, 3, 6))
+    for t in range(6):  # tendon_force_map (trunk.py:96-104)
+        for i in range(1, M):
+            fmap[i, :, t] = (1.0 / (M - 1)) * dirs[t]
+    rest = np.zeros((M, 3))
+    rest[:, 2] = -rest_length * np.arange(M)
+    return dict(M=M, m=node_mass, k=coupling_stiffness, c=coupling_damping, kb=bend_stiffness,
+                L=rest_length, g=np.asarray(gravity, dtype=float), u_max=u_max, dt_sim=dt_sim, dt=dt,
+                substeps=int(round(dt / dt_sim)), fmap=fmap, rest=rest)
+
+
+def trunk_accelerations(P, p, v, u):
+    """Net force / mass (trunk.py:116-135)."""
+    f = np.broadcast_to(P["m"] * P["g"], p.shape).copy()
+    delta = p[1:] - p[:-1]
+    length = np.maximum(np.linalg.norm(delta, axis=-1, keepdims=True), 1e-12)
+    axial = P["k"] * (length - P["L"]) * (delta / length)
+    damp = P["c"] * (v[1:] - v[:-1])
+    f[1:] -= axial + damp
+    f[:-1] += axial + damp
+    f[1:] -= P["kb"] * (p[1:] - P["rest"][1:])
+    f += P["fmap"] @ u
+    return f / P["m"]
+
+
+def trunk_step(P, arr, u, clip_inputs=True):
+    """step_state_array (trunk.py:148-160) for one (M, 6) state."""
+    u = np.asarray(u, dtype=float)
+    if clip_inputs:
+        u = np.clip(u, 0.0, P["u_max"])
+    p = arr[:, :3].copy()
+    v = arr[:, 3:].copy()
+    for _ in range(P["substeps"]):
+        a = trunk_accelerations(P, p, v, u)
+        v = v + P["dt_sim"] * a
+        v[0] = 0.0
+        p = p + P["dt_sim"] * v
+        p[0] = P["rest"][0]
+    return np.concatenate([p, v], axis=-1)
+
+
+def circle_ref(radius, period, center):
+    """references.py:12-30."""
+    center = np.asarray(center, dtype=float)
+    om = 2.0 * np.pi / period
+
+    def ref(t):
+        ang = om * np.asarray(t, dtype=float)
+        pos = np.stack([radius * np.cos(ang), radius * np.sin(ang), np.zeros_like(ang)], -1) + center
+        vel = np.stack([-radius * om * np.sin(ang), radius * om * np.cos(ang), np.zeros_like(ang)], -1)
+        return pos, vel
+
+    return ref
+
+
+class _Spec:
+    """Plain OCP container with the fields condense_ocp reads."""
+
+    def __init__(self, topology, horizon, q, x_ref, r, u_ref, input_constraints, state_constraints):
+        self.topology, self.horizon = topology, horizon
+        self.q, self.x_ref, self.r, self.u_ref = q, x_ref, r, u_ref
+        self.input_constraints, self.state_constraints = input_constraints, state_constraints
+
+
+def tracking_specs(topo, horizon, dt, rest_arr, ref, n_u, u_max, q_pos=(500.0, 500.0, 100.0),
+                   q_vel=(0.5, 0.5, 0.5), r_diag=2e-4):
+    """tracking_spec_provider (experiments.py:107-139) with default
+    TrackingWeights (experiments.py:90-104): t -> spec."""
+    M, N = topo.node_count, horizon
+    target = M - 1
+    q = np.zeros((M, N + 1, 6, 6))
+    q[target, :] = np.diag(np.concatenate([q_pos, q_vel]))
+    r = np.tile(np.eye(n_u) * r_diag, (N, 1, 1))
+    u_ref = np.zeros((N, n_u))
+    box = (np.vstack([np.eye(n_u), -np.eye(n_u)]), np.concatenate([np.full(n_u, u_max), np.zeros(n_u)]))
+    x_base = np.tile(rest_arr[:, None, :], (1, N + 1, 1))
+    offs = np.arange(N + 1) * dt
+
+    def spec(t):
+        x_ref = x_base.copy()
+        pos, vel = ref(t * dt + offs)
+        x_ref[target, :, :3] = pos
+        x_ref[target, :, 3:] = vel
+        return _Spec(topo, N, q, x_ref, r, u_ref, [box] * N, [])
+
+    return spec
+
+
+def closed_loop(model, topo, P, specs, x0, n_steps, horizon):
+    """run_closed_loop (mpc.py:224-264) with the chain plant; returns states
+    (n_steps+1, M, 6), inputs (n_steps, n_u), statuses, iterations."""
+    n_u = 6
+    ls = np.tile(x0, (horizon + 1, 1, 1))
+    li = np.zeros((horizon, n_u))
+    x = np.array(x0, dtype=float)
+    states, inputs, statuses, iters = [x.copy()], [], [], []
+    last = None
+    for t in range(n_steps):
+        res = mpc_step(model, topo, specs(t), x, ls, li, horizon, last_applied=last)
+        ls, li, last = res["lin_states"], res["lin_inputs"], res["u_applied"]
+        inputs.append(res["u_applied"])
+        statuses.append(res["status"])
+        iters.append(res["iterations"])
+        x = trunk_step(P, x, res["u_applied"])
+        states.append(x.copy())
+    return np.stack(states), np.stack(inputs), statuses, np.asarray(iters)

@@ -55,6 +55,9 @@ _SIGNATURES = {
     "gm_linearize": (c_int, [c_void_p, c_i64, P, P, P, P, P, P, P, c_void_p]),
     "gm_step": (c_int, [c_void_p, c_i64, P, P, P, c_void_p]),
     "gm_set_linearize_mode": (c_int, [c_void_p, c_int]),
+    "gm_trunk_step": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_double, c_double, c_double,
+                              c_double, c_double, c_double, P, P, P, c_double, c_int, P, P, P, P,
+                              c_void_p]),
     "gm_gamma_ld": (c_int, [c_int, c_int]),
     "gm_condense_gammas": (c_int, [c_void_p, c_int, c_int, P, P, P, P, P, P, c_int, c_void_p]),
     "gm_condense_gammas_stage": (c_int, [c_void_p, c_int, c_int, c_int, P, P, P, P, P, P, c_int,

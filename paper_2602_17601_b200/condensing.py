@@ -273,7 +273,23 @@ class DeviceSpec:
 
 def device_spec(eng, spec, nx: int, nu: int) -> DeviceSpec:
     """Device copy of ``spec``; cached per engine for frozen specs
-    (``OcpSpec.freeze``), rebuilt on every call otherwise."""
+    (``OcpSpec.freeze``), rebuilt on every call otherwise.  Specs produced by a
+    tracking provider (``tracking.tracking_spec_provider``) share frozen cost /
+    constraint arrays and carry the provider's static token: their upload is
+    cached under the token and only x_ref is copied in on each call."""
+    token = getattr(spec, "_static_token", None)
+    if token is not None:
+        key = ("spec-token", id(token), nx, nu)
+        hit = eng.cache.get(key)
+        if hit is not None and hit[0]() is token:
+            ds = hit[1]
+            src = eng.torch.from_numpy(np.ascontiguousarray(spec.x_ref, dtype=np.float64))
+            ds.x_ref.copy_(src.reshape(ds.x_ref.shape))
+            return ds
+        ds = DeviceSpec(eng, spec, nx, nu)
+        eng.cache[key] = (weakref.ref(token), ds)
+        weakref.finalize(token, eng.cache.pop, key, None)
+        return ds
     if not getattr(spec, "_frozen", False):
         return DeviceSpec(eng, spec, nx, nu)
     key = ("spec", id(spec), nx, nu)

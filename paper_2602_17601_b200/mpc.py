@@ -323,7 +323,9 @@ def get_plan(eng, spec, N, nx, nu, cfg, gnn) -> StepPlan:
     plan = eng.cache.get(key)
     if plan is None or plan.ds is not ds:
         plan = StepPlan(eng, ds, N, nx, nu, cfg, gnn)
-        plan.use_graphs = getattr(spec, "_frozen", False)  # only frozen specs are replayable
+        # replayable: frozen specs, and tracking specs whose only moving part
+        # (x_ref) is refreshed in place in the plan's device spec
+        plan.use_graphs = getattr(spec, "_frozen", False) or getattr(spec, "_static_token", None) is not None
         plan.runs = 0
         eng.cache[key] = plan
     return plan
@@ -361,14 +363,18 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
     torch = eng.torch
     lin_in_prev = _field(state, "lin_inputs")
     n_u = int(lin_in_prev.shape[1])
-    nx = int(np.asarray(x_measured.array).shape[1])
+    x_arr = x_measured.array
+    x_on_device = hasattr(x_arr, "data_ptr") and not isinstance(x_arr, np.ndarray)
+    nx = int(x_arr.shape[1])
     eng.set_dims(nx, n_u)
     plan = get_plan(eng, spec, N, nx, n_u, cfg, gnn)
     stream = torch.cuda.current_stream(eng.device)
 
     # inputs: measurement, previous plan with x_measured at stage 0 (mpc.py:120-122)
     graphable = plan.use_graphs and cfg.sqp_iterations == 1
-    whole = graphable and plan.graph is not None
+    # the whole-step graph reads the measurement from the pinned host buffer;
+    # a device-resident measurement goes through the per-group graphs
+    whole = graphable and plan.graph is not None and not x_on_device
     if whole:  # the step graph does the H2D from the pinned buffer and ls[0]
         plan.host_x.numpy()[...] = np.asarray(x_measured.array, dtype=float).reshape(plan.host_x.shape)
         _copy_in(plan.ls, _field(state, "lin_states"))

@@ -115,3 +115,35 @@ def test_hand_known_answers():
     t3 = chain_topology(3)
     assert t3.edges == [(0, 1), (1, 0), (1, 2), (2, 1)]
     assert t3.closed_neighbors(1) == (1, 0, 2)
+
+
+def _cfg2():
+    from tests.golden_io import model_from
+
+    d = load("cfg2_closed_loop")
+    model = model_from(d, "m_")
+    from paper_2602_17601_b200.graph import chain_topology
+
+    return d, model, chain_topology(d["x0"].shape[0])
+
+
+def test_oracle_plant_matches_reference():
+    """trunk.py step_state_array (one controller period, 10 substeps)."""
+    d, _, _ = _cfg2()
+    P = O.trunk_params(d["x0"].shape[0])
+    out = O.trunk_step(P, d["plant_in"], d["plant_u"])
+    assert np.max(np.abs(out - d["plant_out"])) <= 1e-12
+
+
+def test_oracle_closed_loop_matches_reference():
+    """run_closed_loop with the reference's tracking provider and plant (cfg2
+    stack at M=10, N=10, 6 steps)."""
+    d, model, topo = _cfg2()
+    M = d["x0"].shape[0]
+    P = O.trunk_params(M)
+    specs = O.tracking_specs(topo, 10, 0.01, d["x0"], O.circle_ref(0.04, 8.0, d["center"]), 6, 8.0)
+    states, inputs, statuses, iters = O.closed_loop(model, topo, P, specs, d["x0"], 6, 10)
+    assert [s for s in statuses] == [str(s) for s in d["statuses"]]
+    assert np.array_equal(iters, d["iterations"])
+    assert np.max(np.abs(inputs - d["inputs"])) <= 1e-7
+    assert np.max(np.abs(states - d["states"])) <= 1e-9
