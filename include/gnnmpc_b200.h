@@ -159,6 +159,10 @@ int gm_condense_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, cons
  * fully written.  Requires the whole node range (gm_set_node_range unset);
  * shapes outside the fused kernel's instantiations run the two-kernel path.
  * One launch per context at a time (per-context stage counters). */
+/* Node reduction of H in gm_condense_fused: 0 = auto (tcgen05 3xTF32
+ * tensor-core kernel when N*nu <= 128, else the SIMT kernel), 1 = always the
+ * SIMT (register-tiled fp32 FMA) kernel.  For tests and benchmarks. */
+int gm_set_condense_mode(gm_ctx* ctx, int mode);
 int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_nbr,
                       const float* b, const double* c, const double* x0, float* gamma, int ld,
                       const double* q, int64_t q_stride, const double* x_ref, int64_t xref_stride,
@@ -203,6 +207,10 @@ int gm_qp_phase_cycles(unsigned long long* out);
  * failed.  Used by the tests to check the factorisation in isolation. */
 int gm_chol_check(gm_ctx* ctx, int n, const double* A, const double* b, double* L, double* x,
                   int32_t* ok, void* stream);
+/* Diagnostics: known-answer check of the tcgen05 3xTF32 Gram product used by
+ * K-COND's H accumulation: S (P, P) = G' Q for G, Q (K, P) fp32 row-major,
+ * P <= 128 (one CTA, TMEM accumulator). */
+int gm_gram_check(gm_ctx* ctx, int K, int P, const float* G, const float* Q, float* S, void* stream);
 
 /* ---- reconstruct_states (condensing.py:409-416) ------------------------ */
 /* u (B, ldu) fp64 (first N*nu used); x (B, M, N+1, nx) fp64. */

@@ -67,6 +67,7 @@ struct gm_ctx {
   int* d_dst = nullptr;
   int64_t node_lo = 0, node_hi = -1;
   int lin_mode = 0;  // gm_set_linearize_mode
+  int cond_mode = 0;  // gm_set_condense_mode
   // model
   bool has_model = false;
   int n_p = 0, n_m = 0;

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Context, graph index construction and model upload.
 //
 // Graph: GraphTopology validation (graph.py:35-54) and the index tables of
@@ -82,6 +83,12 @@ int gm_create(gm_ctx** out, int device) {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     c->smem_optin = (size_t)optin;
+  }
+  // benchmark/profiling overrides of the kernel-variant switches
+  if (const char* v = getenv("GM_CONDENSE_MODE")) c->cond_mode = atoi(v) == 1 ? 1 : 0;
+  if (const char* v = getenv("GM_LINEARIZE_MODE")) {
+    const int m = atoi(v);
+    c->lin_mode = (m >= 0 && m <= 2) ? m : 0;
   }
   *out = c;
   return GM_OK;

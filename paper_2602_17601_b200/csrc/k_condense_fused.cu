@@ -33,6 +33,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "umma.cuh"
 
 namespace {
 
@@ -368,6 +369,297 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// K-COND on the tensor cores (n0 = N*nu <= 128): the same persistent stage
+// wavefront and the same fp32 Gamma recursion as k_condense_fused, but the
+// node reduction of H -- per work item of SC nodes a rank-(SC*nx) update
+//     H += G' (Qs G),   G = stage-k Gamma_u rows of the item (SC*nx x n0)
+// -- runs as tcgen05.mma kind::tf32 in 3xTF32 form (umma.cuh) into one
+// 128 x 128 fp32 accumulator in TMEM per CTA.  The recursion writes its rows
+// straight into the K-major operand buffers (hi/lo split), one elected thread
+// issues 3 * KC/8 MMAs of N = round16(k*nu) columns (causality: only the first
+// k*nu columns are live at stage k) and commits to an mbarrier; the g update
+// (fp64, SIMT) runs while the tensor core works.  At the end the accumulator
+// is read back with tcgen05.ld into the same per-CTA pair-ordered partials
+// the SIMT kernel writes, so the fixed-order fp64 reduction is shared.
+// ---------------------------------------------------------------------------
+template <int NX, int NU>
+__global__ void __launch_bounds__(256, 1) k_condense_tc(const FusedArgs a) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  const int N = a.N, ld = a.ld, SC = a.sc, M = a.M;
+  const int n0 = N * NU, XC = N * NU;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5;
+  const int64_t bi = blockIdx.x / a.splits;
+  const int split = (int)(blockIdx.x % a.splits);
+  const int nb = split * a.per, ne = min(M, nb + a.per);
+  const int nn = ne - nb;
+  const int nsub = (nn + SC - 1) / SC;
+  const int emax = SC * (a.dslot - 1) > 0 ? SC * (a.dslot - 1) : 1;
+  const int KC = ((SC * NX + 7) / 8) * 8;               // K rows per item, MMA-padded
+  const uint32_t sbo = (uint32_t)(KC / 4) * 128u;        // 8-row group stride
+  const size_t bufb = 16 * (size_t)sbo;                  // 128-row operand buffer
+  int* flags = a.flags + bi * a.splits;
+  const int64_t stage_stride = (int64_t)NX * ld;
+  const int64_t node_stride = (int64_t)(N + 1) * stage_stride;
+  float* Wb = a.W + bi * (int64_t)M * node_stride;
+
+  const size_t sbytes = stage_bytes<NX, NU>(SC, emax);
+  unsigned char* ops = smraw + ((2 * sbytes + 127) & ~size_t(127));
+  unsigned char* g_hi = ops;
+  unsigned char* g_lo = ops + bufb;
+  unsigned char* q_hi = ops + 2 * bufb;
+  unsigned char* q_lo = ops + 3 * bufb;
+  float* Qs = (float*)(ops + 4 * bufb);                  // SC x NX*NX  (Q + Q')/2
+  float* gx = Qs + SC * NX * NX;                         // SC x NX     Gamma_x rows
+  double* wv = (double*)(((uintptr_t)(gx + SC * NX) + 15) & ~(uintptr_t)15);  // SC x NX
+  double* gs = wv + SC * NX;                             // n0
+  uint64_t* mbar = (uint64_t*)(gs + n0);
+  uint32_t* tslot = (uint32_t*)(mbar + 1);
+  int* nptr = (int*)(tslot + 2);                         // nn + 1
+
+  if (warp == 0) umma::tmem_alloc<128>(tslot);
+  if (tid == 32) umma::mbar_init(mbar, 1);
+  for (int t = tid; t <= nn; t += nt) nptr[t] = a.ptr[nb + t];
+  for (int t = tid; t < (int)(4 * bufb / 16); t += nt) ((float4*)ops)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int t = tid; t < n0; t += nt) gs[t] = 0.0;
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tslot;
+  uint32_t phase = 0;
+  bool pending = false, issued = false;
+
+  auto prefetch = [&](int j) {
+    const int n = j / nsub, s0 = nb + (j % nsub) * SC;
+    const int sc = min(SC, ne - s0), k = n + 1;
+    const Stage<NX, NU> S = stage_at<NX, NU>(smraw + (j & 1) * sbytes, SC, emax);
+    const int64_t pstage = bi * N + n;
+    const int eb = nptr[s0 - nb], ee = nptr[s0 - nb + sc];
+    const int nE = ee - eb;
+    const float* gas = a.a_self + (pstage * M + s0) * NX * NX;
+    for (int t = tid; t < sc * NX * NX; t += nt) cp_async4(S.as + t, gas + t);
+    if (nE > 0) {
+      const float* gan = a.a_nbr + (pstage * a.E + eb) * NX * NX;
+      for (int t = tid; t < nE * NX * NX; t += nt) cp_async4(S.an + t, gan + t);
+      for (int t = tid; t < nE; t += nt) cp_async4(S.src + t, a.src + eb + t);
+    }
+    const float* gb = a.b + (pstage * M + s0) * NX * NU;
+    for (int t = tid; t < sc * NX * NU; t += nt) cp_async4(S.bb + t, gb + t);
+    const double* gc = a.c + (pstage * M + s0) * NX;
+    for (int t = tid; t < sc * NX; t += nt) cp_async8(S.cc + t, gc + t);
+    for (int t = tid; t < sc * NX * NX; t += nt) {
+      const int li = t / (NX * NX), e = t - li * NX * NX;
+      cp_async8(S.qd + t, a.q + bi * a.q_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX * NX + e);
+    }
+    for (int t = tid; t < sc * NX; t += nt) {
+      const int li = t / NX, e = t - li * NX;
+      cp_async8(S.xd + t, a.xref + bi * a.xref_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX + e);
+    }
+    cp_async_commit();
+  };
+  const int items = N * nsub;
+  if (items > 0) prefetch(0);
+
+  // stage 0: Gamma_u = 0, Gamma_x = x0 (condensing.py:205-206)
+  for (int t = tid; t < nn * NX * ld; t += nt) {
+    const int li = t / (NX * ld), rem = t - li * NX * ld, r = rem / ld, col = rem - r * ld;
+    Wb[(int64_t)(nb + li) * node_stride + rem] =
+        (col == XC) ? (float)a.x0[(bi * M + nb + li) * NX + r] : 0.f;
+  }
+  const int d0 = a.dep_ptr[split], d1 = a.dep_ptr[split + 1];
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(&flags[split], 1);
+  }
+
+  for (int j = 0; j < items; ++j) {
+    const int n = j / nsub, sub = j % nsub;
+    const int s0 = nb + sub * SC, sc = min(SC, ne - s0);
+    const int k = n + 1;
+    const int live = n * NU;
+    const Stage<NX, NU> S = stage_at<NX, NU>(smraw + (j & 1) * sbytes, SC, emax);
+    if (sub == 0) {
+      for (int d = d0 + tid; d < d1; d += nt) {
+        const int* f = &flags[a.dep[d]];
+        while (ld_acquire(f) < k) __nanosleep(32);
+      }
+    }
+    cp_async_wait_all();
+    if (pending) {  // the previous item's MMAs still read the operand buffers
+      umma::mbar_wait(mbar, phase);
+      phase ^= 1;
+      pending = false;
+      umma::fence_after();
+    }
+    __syncthreads();
+    if (j + 1 < items) prefetch(j + 1);
+    for (int t = tid; t < sc * NX * NX; t += nt) {
+      const int li = t / (NX * NX), e = t - li * NX * NX, r = e / NX, cc = e - r * NX;
+      const double* Qk = S.qd + li * NX * NX;
+      Qs[t] = (float)(0.5 * (Qk[r * NX + cc] + Qk[cc * NX + r]));
+    }
+    const int ebase = nptr[s0 - nb];
+    // Gamma rows of stage k (condensing.py:213-224); rows of padding nodes
+    // (li >= sc) are zero in the operand buffers
+    for (int t = tid; t < SC * ld; t += nt) {
+      const int li = t / ld, col = t - li * ld;
+      const int i = s0 + li;
+      float r6[NX];
+#pragma unroll
+      for (int r = 0; r < NX; ++r) r6[r] = 0.f;
+      if (li < sc) {
+        if (col < live || col == XC) {
+          const int el0 = nptr[i - nb] - ebase, deg = nptr[i - nb + 1] - nptr[i - nb];
+          const float* Wn = Wb + (int64_t)n * stage_stride + col;
+          for (int s = 0; s <= deg; s += 4) {
+            float w[4][NX];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int ss = s + u;
+              if (ss <= deg) {
+                const int jn = ss == 0 ? i : S.src[el0 + ss - 1];
+                const float* Wj = Wn + (int64_t)jn * node_stride;
+#pragma unroll
+                for (int qq = 0; qq < NX; ++qq) w[u][qq] = __ldcg(Wj + (int64_t)qq * ld);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int ss = s + u;
+              if (ss <= deg) {
+                const float* As = ss == 0 ? S.as + li * NX * NX : S.an + (el0 + ss - 1) * NX * NX;
+#pragma unroll
+                for (int r = 0; r < NX; ++r)
+#pragma unroll
+                  for (int qq = 0; qq < NX; ++qq) r6[r] = fmaf(As[r * NX + qq], w[u][qq], r6[r]);
+              }
+            }
+          }
+          if (col == XC) {
+#pragma unroll
+            for (int r = 0; r < NX; ++r) r6[r] += (float)S.cc[li * NX + r];
+          }
+        } else if (col >= live && col < live + NU) {
+#pragma unroll
+          for (int r = 0; r < NX; ++r) r6[r] = S.bb[(li * NX + r) * NU + (col - live)];
+        }
+        float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + col;
+#pragma unroll
+        for (int r = 0; r < NX; ++r) Wo[(int64_t)r * ld] = r6[r];
+      }
+      if (col < n0) {
+#pragma unroll
+        for (int r = 0; r < NX; ++r) umma::put_split(g_hi, g_lo, col, li * NX + r, sbo, r6[r]);
+      } else if (col == XC) {
+#pragma unroll
+        for (int r = 0; r < NX; ++r) gx[li * NX + r] = r6[r];
+      }
+    }
+    __syncthreads();
+    if (sub == nsub - 1 && tid == 0) {  // all of this CTA's stage-k rows are out
+      __threadfence();
+      st_release(&flags[split], k + 1);
+    }
+    // Qs G on the live columns of stage k -> B operand; w = 2 Q Gamma_x - 2 Q x_ref
+    const int lk = k * NU;
+    for (int t = tid; t < SC * lk; t += nt) {
+      const int li = t / lk, col = t - li * lk;
+      float gcol[NX];
+#pragma unroll
+      for (int qq = 0; qq < NX; ++qq) {
+        const uint32_t o = umma::kmajor_offset(col, li * NX + qq, sbo);
+        gcol[qq] = *(const float*)(g_hi + o) + *(const float*)(g_lo + o);
+      }
+      const float* Qn = Qs + li * NX * NX;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) {
+        float s = 0.f;
+        if (li < sc) {
+#pragma unroll
+          for (int qq = 0; qq < NX; ++qq) s = fmaf(Qn[r * NX + qq], gcol[qq], s);
+        }
+        umma::put_split(q_hi, q_lo, col, li * NX + r, sbo, s);
+      }
+    }
+    for (int t = tid; t < sc * NX; t += nt) {
+      const int li = t / NX, r = t - li * NX;
+      const double* Qk = S.qd + li * NX * NX + r * NX;
+      const double* xr = S.xd + li * NX;
+      double qg = 0.0, qx = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < NX; ++qq) {
+        qg += Qk[qq] * (double)gx[li * NX + qq];
+        qx += Qk[qq] * xr[qq];
+      }
+      wv[t] = 2.0 * qg + (-2.0 * qx);
+    }
+    umma::fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      umma::fence_after();
+      // TMEM is not zeroed by tcgen05.alloc: the first MMA (accumulate = 0)
+      // spans every column ever used so later, wider ones add onto zeros
+      const int Nm = max(16, (((issued ? lk : n0) + 15) / 16) * 16);
+      umma::gram_3xtf32(tmem, g_hi, g_lo, sbo, q_hi, q_lo, sbo, KC / 8, umma::idesc_tf32(128, Nm), issued);
+      umma::commit(mbar);
+    }
+    pending = true;
+    issued = true;
+    // g (fp64) while the tensor core runs; operand buffers are only read
+    for (int cidx = tid; cidx < lk; cidx += nt) {
+      double s = gs[cidx];
+      for (int li = 0; li < sc; ++li)
+#pragma unroll
+        for (int r = 0; r < NX; ++r) {
+          const uint32_t o = umma::kmajor_offset(cidx, li * NX + r, sbo);
+          const float gv = *(const float*)(g_hi + o) + *(const float*)(g_lo + o);
+          s += (double)gv * wv[li * NX + r];
+        }
+      gs[cidx] = s;
+    }
+    __syncthreads();
+  }
+  if (pending) {
+    umma::mbar_wait(mbar, phase);
+    umma::fence_after();
+  }
+
+  // partials: TMEM row m = p*nu + u, column c = q*nu + v -> pair (p, q), p <= q
+  const int PU = a.npairs * NU * NU;
+  float* P = a.partH + (bi * a.splits + split) * (int64_t)PU;
+  {
+    const int m = (warp & 3) * 32 + (tid & 31);
+    const int cbeg = (warp >> 2) * 64;
+    const int p = m / NU, u = m - p * NU;
+    for (int c0 = cbeg; c0 < cbeg + 64; c0 += 16) {
+      float v[16];
+      umma::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
+      if (m < n0) {
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int c = c0 + jj;
+          const int q = c / NU, vv = c - q * NU;
+          if (c < n0 && p <= q) P[(q * (q + 1) / 2 + p) * NU * NU + u * NU + vv] = issued ? v[jj] : 0.f;
+        }
+      }
+    }
+  }
+  for (int t = tid; t < n0; t += nt) a.partg[(bi * a.splits + split) * n0 + t] = gs[t];
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<128>(tmem);
+  if (tid == 0) {
+    __threadfence();
+    int* done = a.flags + (int64_t)gridDim.x;
+    if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
+      for (int s = 0; s < (int)gridDim.x; ++s) a.flags[s] = 0;
+      *done = 0;
+      __threadfence();
+    }
+  }
+}
+
 struct PairReduceArgs {
   int nu, n0, npairs, splits, groups;
   const float* partH;
@@ -456,6 +748,32 @@ __global__ void k_pair_reduce2(const PairReduceArgs a) {
 
 using FusedKernel = void (*)(const FusedArgs);
 
+FusedKernel pick_tc_kernel(int nx, int nu) {
+  if (nx == 6 && nu == 6) return k_condense_tc<6, 6>;
+  if (nx == 6 && nu == 3) return k_condense_tc<6, 3>;
+  if (nx == 6 && nu == 2) return k_condense_tc<6, 2>;
+  if (nx == 6 && nu == 1) return k_condense_tc<6, 1>;
+  if (nx == 4 && nu == 2) return k_condense_tc<4, 2>;
+  if (nx == 2 && nu == 1) return k_condense_tc<2, 1>;
+  return nullptr;
+}
+
+// shared memory of k_condense_tc (same carve-up as the kernel)
+size_t tc_smem(int SC, int nx, int nu, int dslot, int n0, int64_t per) {
+  const int emax = SC * (dslot - 1) > 0 ? SC * (dslot - 1) : 1;
+  size_t st = sizeof(double) * ((size_t)SC * nx * 2 + (size_t)SC * nx * nx) +
+              sizeof(float) * ((size_t)SC * nx * nx + (size_t)emax * nx * nx + (size_t)SC * nx * nu) +
+              sizeof(int) * (size_t)emax;
+  st = (st + 15) & ~size_t(15);
+  const int KC = ((SC * nx + 7) / 8) * 8;
+  const size_t bufb = 16 * (size_t)(KC / 4) * 128;
+  size_t b = ((2 * st + 127) & ~size_t(127)) + 4 * bufb;
+  b += sizeof(float) * ((size_t)SC * nx * nx + (size_t)SC * nx);
+  b = (b + 15) & ~size_t(15);
+  b += sizeof(double) * ((size_t)SC * nx + n0) + 8 + 8;
+  return b + sizeof(int) * (size_t)(per + 1) + 16;
+}
+
 FusedKernel pick_kernel(int nx, int nu) {
   if (nx == 6 && nu == 6) return k_condense_fused<6, 6>;
   if (nx == 6 && nu == 3) return k_condense_fused<6, 3>;
@@ -522,6 +840,13 @@ int ensure_flags(gm_ctx* ctx, int64_t n) {
 
 extern "C" {
 
+int gm_set_condense_mode(gm_ctx* ctx, int mode) {
+  if (!ctx) return GM_ERR_CONFIG;
+  if (mode < 0 || mode > 1) return gm_fail(ctx, GM_ERR_CONFIG, "condense mode must be 0 or 1");
+  ctx->cond_mode = mode;
+  return GM_OK;
+}
+
 int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_nbr,
                       const float* b, const double* c, const double* x0, float* gamma, int ld,
                       const double* q, int64_t q_stride, const double* x_ref, int64_t xref_stride,
@@ -537,7 +862,10 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   const int nx = ctx->nx, nu = ctx->n_u, n0 = N * nu;
   const int npairs = N * (N + 1) / 2;
   const int dslot = (int)ctx->dmax + 1;
-  FusedKernel kern = pick_kernel(nx, nu);
+  // tensor-core H (k_condense_tc) whenever the H accumulator fits one
+  // 128 x 128 TMEM tile; gm_set_condense_mode forces either kernel
+  FusedKernel tck = (n0 <= 128 && ctx->cond_mode != 1) ? pick_tc_kernel(nx, nu) : nullptr;
+  FusedKernel kern = tck ? tck : pick_kernel(nx, nu);
   const bool whole = ctx->node_lo == 0 && gm_node_hi(ctx) == ctx->M;
   // node partition: one CTA per SM, all co-resident (the stage waits need it)
   const int64_t M = ctx->M;
@@ -547,9 +875,12 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
     const int64_t want = std::max<int64_t>(1, slots / B);
     per = (M + want - 1) / want;
   }
-  int SC = 16;
-  while (SC > 1 && fused_smem(SC, nx, nu, ld, dslot, n0, per) > kFusedSmemBudget) SC >>= 1;
-  const size_t sm = fused_smem(SC, nx, nu, ld, dslot, n0, per);
+  int SC = tck ? 8 : 16;
+  auto smem_of = [&](int sc_) {
+    return tck ? tc_smem(sc_, nx, nu, dslot, n0, per) : fused_smem(sc_, nx, nu, ld, dslot, n0, per);
+  };
+  while (SC > 1 && smem_of(SC) > kFusedSmemBudget) SC >>= 1;
+  const size_t sm = smem_of(SC);
   if (!kern || !whole || npairs > 256 || sm > kFusedSmemBudget) {
     // shapes outside the fused kernel's instantiations: the two-kernel path
     rc = gm_condense_gammas(ctx, B, N, a_self, a_nbr, b, c, x0, gamma, ld, stream);
