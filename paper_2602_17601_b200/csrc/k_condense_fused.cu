@@ -38,6 +38,7 @@
 namespace {
 
 constexpr int kFusedSmemBudget = 160 * 1024;
+constexpr int kTcThreads = 512;  // k_condense_tc block size (16 warps: latency hiding for the neighbour loads)
 
 struct FusedArgs {
   int M, E, N, ld, per, splits, sc, npairs, dslot;
@@ -378,13 +379,18 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
 // 128 x 128 fp32 accumulator in TMEM per CTA.  The recursion writes its rows
 // straight into the K-major operand buffers (hi/lo split), one elected thread
 // issues 3 * KC/8 MMAs of N = round16(k*nu) columns (causality: only the first
-// k*nu columns are live at stage k) and commits to an mbarrier; the g update
-// (fp64, SIMT) runs while the tensor core works.  At the end the accumulator
+// k*nu columns are live at stage k) and commits to an mbarrier.  g rides on
+// the tensor core too: a 16-row B operand whose row 0 is w = 2 Q Gamma_x -
+// 2 Q x_ref accumulates sum G' w into TMEM column 128 (fp32 per CTA, fp64
+// fixed-order reduction).  Latency hiding: within a stage the next item's
+// first neighbour rows are loaded into registers while the current item's
+// operands are built, and each thread waits for the previous item's MMAs
+// only right before it overwrites an operand buffer.  At the end the accumulator
 // is read back with tcgen05.ld into the same per-CTA pair-ordered partials
 // the SIMT kernel writes, so the fixed-order fp64 reduction is shared.
 // ---------------------------------------------------------------------------
 template <int NX, int NU>
-__global__ void __launch_bounds__(256, 1) k_condense_tc(const FusedArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   const int N = a.N, ld = a.ld, SC = a.sc, M = a.M;
   const int n0 = N * NU, XC = N * NU;
@@ -409,7 +415,9 @@ __global__ void __launch_bounds__(256, 1) k_condense_tc(const FusedArgs a) {
   unsigned char* g_lo = ops + bufb;
   unsigned char* q_hi = ops + 2 * bufb;
   unsigned char* q_lo = ops + 3 * bufb;
-  float* Qs = (float*)(ops + 4 * bufb);                  // SC x NX*NX  (Q + Q')/2
+  unsigned char* w_hi = ops + 4 * bufb;                  // 16-row B operand: row 0 = g weights
+  unsigned char* w_lo = w_hi + 2 * sbo;
+  float* Qs = (float*)(w_lo + 2 * sbo);                  // SC x NX*NX  (Q + Q')/2
   float* gx = Qs + SC * NX * NX;                         // SC x NX     Gamma_x rows
   double* wv = (double*)(((uintptr_t)(gx + SC * NX) + 15) & ~(uintptr_t)15);  // SC x NX
   double* gs = wv + SC * NX;                             // n0
@@ -417,17 +425,29 @@ __global__ void __launch_bounds__(256, 1) k_condense_tc(const FusedArgs a) {
   uint32_t* tslot = (uint32_t*)(mbar + 1);
   int* nptr = (int*)(tslot + 2);                         // nn + 1
 
-  if (warp == 0) umma::tmem_alloc<128>(tslot);
+  if (warp == 0) umma::tmem_alloc<256>(tslot);  // H in columns [0, 128), g in column 128
   if (tid == 32) umma::mbar_init(mbar, 1);
   for (int t = tid; t <= nn; t += nt) nptr[t] = a.ptr[nb + t];
-  for (int t = tid; t < (int)(4 * bufb / 16); t += nt) ((float4*)ops)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int t = tid; t < n0; t += nt) gs[t] = 0.0;
+  for (int t = tid; t < (int)((4 * bufb + 4 * sbo) / 16); t += nt) ((float4*)ops)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tslot;
   uint32_t phase = 0;
   bool pending = false, issued = false;
+  float wpre[5][NX];
+  bool pre_ok = false;
+  // per-thread wait for the previous item's MMAs (they read the operand
+  // buffers) just before this thread first overwrites them, so the tensor
+  // core overlaps the neighbour loads and FMAs of the next item
+  auto operands_free = [&]() {
+    if (pending) {
+      umma::mbar_wait(mbar, phase);
+      phase ^= 1;
+      pending = false;
+      umma::fence_after();
+    }
+  };
 
   auto prefetch = [&](int j) {
     const int n = j / nsub, s0 = nb + (j % nsub) * SC;
@@ -486,12 +506,6 @@ __global__ void __launch_bounds__(256, 1) k_condense_tc(const FusedArgs a) {
       }
     }
     cp_async_wait_all();
-    if (pending) {  // the previous item's MMAs still read the operand buffers
-      umma::mbar_wait(mbar, phase);
-      phase ^= 1;
-      pending = false;
-      umma::fence_after();
-    }
     __syncthreads();
     if (j + 1 < items) prefetch(j + 1);
     for (int t = tid; t < sc * NX * NX; t += nt) {
@@ -500,60 +514,105 @@ __global__ void __launch_bounds__(256, 1) k_condense_tc(const FusedArgs a) {
       Qs[t] = (float)(0.5 * (Qk[r * NX + cc] + Qk[cc * NX + r]));
     }
     const int ebase = nptr[s0 - nb];
-    // Gamma rows of stage k (condensing.py:213-224); rows of padding nodes
-    // (li >= sc) are zero in the operand buffers
-    for (int t = tid; t < SC * ld; t += nt) {
-      const int li = t / ld, col = t - li * ld;
+    // (R1) the live Gamma_u columns and Gamma_x of stage k (condensing.py:213-
+    // 224): one (node, column) per thread over the closed neighbourhood, all
+    // neighbour loads of a node issued before the FMAs (one L2/DRAM round
+    // trip for deg < 5); work spread over live columns only
+    const int lw = live + 1;
+    for (int t = tid, it = 0; t < sc * lw; t += nt, ++it) {
+      const int li = t / lw, cc = t - li * lw;
+      const int col = cc < live ? cc : XC;
       const int i = s0 + li;
       float r6[NX];
 #pragma unroll
       for (int r = 0; r < NX; ++r) r6[r] = 0.f;
-      if (li < sc) {
-        if (col < live || col == XC) {
-          const int el0 = nptr[i - nb] - ebase, deg = nptr[i - nb + 1] - nptr[i - nb];
-          const float* Wn = Wb + (int64_t)n * stage_stride + col;
-          for (int s = 0; s <= deg; s += 4) {
-            float w[4][NX];
+      const int el0 = nptr[i - nb] - ebase, deg = nptr[i - nb + 1] - nptr[i - nb];
+      const float* Wn = Wb + (int64_t)n * stage_stride + col;
+      for (int s = 0; s <= deg; s += 5) {
+        float w[5][NX];
+        if (s == 0 && it == 0 && pre_ok) {  // loaded during the previous item
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int ss = s + u;
-              if (ss <= deg) {
-                const int jn = ss == 0 ? i : S.src[el0 + ss - 1];
-                const float* Wj = Wn + (int64_t)jn * node_stride;
+          for (int u = 0; u < 5; ++u)
 #pragma unroll
-                for (int qq = 0; qq < NX; ++qq) w[u][qq] = __ldcg(Wj + (int64_t)qq * ld);
-              }
-            }
+            for (int qq = 0; qq < NX; ++qq) w[u][qq] = wpre[u][qq];
+        } else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int ss = s + u;
-              if (ss <= deg) {
-                const float* As = ss == 0 ? S.as + li * NX * NX : S.an + (el0 + ss - 1) * NX * NX;
+          for (int u = 0; u < 5; ++u) {
+            const int ss = s + u;
+            if (ss <= deg) {
+              const int jn = ss == 0 ? i : S.src[el0 + ss - 1];
+              const float* Wj = Wn + (int64_t)jn * node_stride;
 #pragma unroll
-                for (int r = 0; r < NX; ++r)
-#pragma unroll
-                  for (int qq = 0; qq < NX; ++qq) r6[r] = fmaf(As[r * NX + qq], w[u][qq], r6[r]);
-              }
+              for (int qq = 0; qq < NX; ++qq) w[u][qq] = __ldcg(Wj + (int64_t)qq * ld);
             }
           }
-          if (col == XC) {
-#pragma unroll
-            for (int r = 0; r < NX; ++r) r6[r] += (float)S.cc[li * NX + r];
-          }
-        } else if (col >= live && col < live + NU) {
-#pragma unroll
-          for (int r = 0; r < NX; ++r) r6[r] = S.bb[(li * NX + r) * NU + (col - live)];
         }
-        float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + col;
 #pragma unroll
-        for (int r = 0; r < NX; ++r) Wo[(int64_t)r * ld] = r6[r];
+        for (int u = 0; u < 5; ++u) {
+          const int ss = s + u;
+          if (ss <= deg) {
+            // block rows as 8-byte shared loads (broadcast within the warp)
+            const float2* A2 =
+                (const float2*)(ss == 0 ? S.as + li * NX * NX : S.an + (el0 + ss - 1) * NX * NX);
+#pragma unroll
+            for (int r = 0; r < NX; ++r)
+#pragma unroll
+              for (int qq = 0; qq < NX; qq += 2) {
+                const float2 v = A2[(r * NX + qq) / 2];
+                r6[r] = fmaf(v.x, w[u][qq], r6[r]);
+                r6[r] = fmaf(v.y, w[u][qq + 1], r6[r]);
+              }
+          }
+        }
       }
-      if (col < n0) {
+      if (col == XC) {
 #pragma unroll
-        for (int r = 0; r < NX; ++r) umma::put_split(g_hi, g_lo, col, li * NX + r, sbo, r6[r]);
-      } else if (col == XC) {
+        for (int r = 0; r < NX; ++r) r6[r] += (float)S.cc[li * NX + r];
+      }
+      float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + col;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) Wo[(int64_t)r * ld] = r6[r];
+      operands_free();
+      if (col < n0) {
+        umma::putn_split<NX>(g_hi, g_lo, col, li * NX, sbo, r6);
+      } else {
 #pragma unroll
         for (int r = 0; r < NX; ++r) gx[li * NX + r] = r6[r];
+      }
+    }
+    // (R2) block n <- B_n, every other column zero (global rows only: the
+    // operand buffers hold zeros beyond the live columns already)
+    operands_free();
+    const int nz = ld - lw;
+    for (int t = tid; t < sc * nz; t += nt) {
+      const int li = t / nz, cc = t - li * nz;
+      int col = live + cc;
+      if (col >= XC) ++col;
+      const int i = s0 + li;
+      float r6[NX];
+      const bool isb = col < live + NU;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) r6[r] = isb ? S.bb[(li * NX + r) * NU + (col - live)] : 0.f;
+      float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + col;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) Wo[(int64_t)r * ld] = r6[r];
+      if (isb) umma::putn_split<NX>(g_hi, g_lo, col, li * NX, sbo, r6);
+    }
+    // padding nodes of a short last chunk: zero K rows
+    for (int t = tid; t < (SC - sc) * live; t += nt) {
+      const int li = sc + t / live, col = t - (t / live) * live;
+      float z[NX];
+#pragma unroll
+      for (int r = 0; r < NX; ++r) z[r] = 0.f;
+      umma::putn_split<NX>(g_hi, g_lo, col, li * NX, sbo, z);
+    }
+    if (sc < SC) {
+      for (int t = tid; t < (SC - sc) * NU; t += nt) {
+        const int li = sc + t / NU, col = live + t % NU;
+        float z[NX];
+#pragma unroll
+        for (int r = 0; r < NX; ++r) z[r] = 0.f;
+        umma::putn_split<NX>(g_hi, g_lo, col, li * NX, sbo, z);
       }
     }
     __syncthreads();
@@ -561,16 +620,36 @@ __global__ void __launch_bounds__(256, 1) k_condense_tc(const FusedArgs a) {
       __threadfence();
       st_release(&flags[split], k + 1);
     }
+    // register prefetch of the next item's first (node, column) neighbour
+    // rows (same stage: its dependencies are already met), in flight while
+    // this item's B operand is built and its MMAs run
+    pre_ok = false;
+    if (sub + 1 < nsub) {
+      const int s0n = s0 + SC, scn = min(SC, ne - s0n);
+      if (tid < scn * lw) {
+        const int li = tid / lw, cc = tid - li * lw;
+        const int col = cc < live ? cc : XC;
+        const int i = s0n + li;
+        const int e0 = nptr[i - nb], deg = nptr[i - nb + 1] - e0;
+        const float* Wn = Wb + (int64_t)n * stage_stride + col;
+#pragma unroll
+        for (int u = 0; u < 5; ++u) {
+          if (u <= deg) {
+            const int jn = u == 0 ? i : __ldg(a.src + e0 + u - 1);
+            const float* Wj = Wn + (int64_t)jn * node_stride;
+#pragma unroll
+            for (int qq = 0; qq < NX; ++qq) wpre[u][qq] = __ldcg(Wj + (int64_t)qq * ld);
+          }
+        }
+        pre_ok = true;
+      }
+    }
     // Qs G on the live columns of stage k -> B operand; w = 2 Q Gamma_x - 2 Q x_ref
     const int lk = k * NU;
     for (int t = tid; t < SC * lk; t += nt) {
       const int li = t / lk, col = t - li * lk;
-      float gcol[NX];
-#pragma unroll
-      for (int qq = 0; qq < NX; ++qq) {
-        const uint32_t o = umma::kmajor_offset(col, li * NX + qq, sbo);
-        gcol[qq] = *(const float*)(g_hi + o) + *(const float*)(g_lo + o);
-      }
+      float gcol[NX], o[NX];
+      umma::getn<NX>(g_hi, g_lo, col, li * NX, sbo, gcol);
       const float* Qn = Qs + li * NX * NX;
 #pragma unroll
       for (int r = 0; r < NX; ++r) {
@@ -579,45 +658,43 @@ __global__ void __launch_bounds__(256, 1) k_condense_tc(const FusedArgs a) {
 #pragma unroll
           for (int qq = 0; qq < NX; ++qq) s = fmaf(Qn[r * NX + qq], gcol[qq], s);
         }
-        umma::put_split(q_hi, q_lo, col, li * NX + r, sbo, s);
+        o[r] = s;
       }
+      umma::putn_split<NX>(q_hi, q_lo, col, li * NX, sbo, o);
     }
-    for (int t = tid; t < sc * NX; t += nt) {
+    // g weights w = 2 Q Gamma_x - 2 Q x_ref (fp64, condensing.py:388) as row 0
+    // of the 16-row B operand: a second MMA chain accumulates g = sum G' w
+    for (int t = tid; t < SC * NX; t += nt) {
       const int li = t / NX, r = t - li * NX;
-      const double* Qk = S.qd + li * NX * NX + r * NX;
-      const double* xr = S.xd + li * NX;
-      double qg = 0.0, qx = 0.0;
+      double wr = 0.0;
+      if (li < sc) {
+        const double* Qk = S.qd + li * NX * NX + r * NX;
+        const double* xr = S.xd + li * NX;
+        double qg = 0.0, qx = 0.0;
 #pragma unroll
-      for (int qq = 0; qq < NX; ++qq) {
-        qg += Qk[qq] * (double)gx[li * NX + qq];
-        qx += Qk[qq] * xr[qq];
+        for (int qq = 0; qq < NX; ++qq) {
+          qg += Qk[qq] * (double)gx[li * NX + qq];
+          qx += Qk[qq] * xr[qq];
+        }
+        wr = 2.0 * qg + (-2.0 * qx);
       }
-      wv[t] = 2.0 * qg + (-2.0 * qx);
+      umma::put_split(w_hi, w_lo, 0, t, sbo, (float)wr);
     }
     umma::fence_async_smem();
     __syncthreads();
     if (tid == 0) {
       umma::fence_after();
-      // TMEM is not zeroed by tcgen05.alloc: the first MMA (accumulate = 0)
-      // spans every column ever used so later, wider ones add onto zeros
+      // H: N = the live columns of stage k (TMEM is not zeroed by
+      // tcgen05.alloc: the first MMA, accumulate = 0, spans every column
+      // used later); g: N = 16 from the w operand into TMEM column 128
       const int Nm = max(16, (((issued ? lk : n0) + 15) / 16) * 16);
       umma::gram_3xtf32(tmem, g_hi, g_lo, sbo, q_hi, q_lo, sbo, KC / 8, umma::idesc_tf32(128, Nm), issued);
+      umma::gram_3xtf32(tmem + 128, g_hi, g_lo, sbo, w_hi, w_lo, sbo, KC / 8, umma::idesc_tf32(128, 16),
+                        issued);
       umma::commit(mbar);
     }
     pending = true;
     issued = true;
-    // g (fp64) while the tensor core runs; operand buffers are only read
-    for (int cidx = tid; cidx < lk; cidx += nt) {
-      double s = gs[cidx];
-      for (int li = 0; li < sc; ++li)
-#pragma unroll
-        for (int r = 0; r < NX; ++r) {
-          const uint32_t o = umma::kmajor_offset(cidx, li * NX + r, sbo);
-          const float gv = *(const float*)(g_hi + o) + *(const float*)(g_lo + o);
-          s += (double)gv * wv[li * NX + r];
-        }
-      gs[cidx] = s;
-    }
     __syncthreads();
   }
   if (pending) {
@@ -630,9 +707,10 @@ __global__ void __launch_bounds__(256, 1) k_condense_tc(const FusedArgs a) {
   float* P = a.partH + (bi * a.splits + split) * (int64_t)PU;
   {
     const int m = (warp & 3) * 32 + (tid & 31);
-    const int cbeg = (warp >> 2) * 64;
+    const int cw = 128 / (nt / 128);  // columns per warp quadruple
+    const int cbeg = (warp >> 2) * cw;
     const int p = m / NU, u = m - p * NU;
-    for (int c0 = cbeg; c0 < cbeg + 64; c0 += 16) {
+    for (int c0 = cbeg; c0 < cbeg + cw; c0 += 16) {
       float v[16];
       umma::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
       if (m < n0) {
@@ -645,10 +723,15 @@ __global__ void __launch_bounds__(256, 1) k_condense_tc(const FusedArgs a) {
       }
     }
   }
-  for (int t = tid; t < n0; t += nt) a.partg[(bi * a.splits + split) * n0 + t] = gs[t];
+  if (warp < 4) {
+    float v[16];
+    const int m = warp * 32 + (tid & 31);
+    umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + 128u, v);
+    if (m < n0) a.partg[(bi * a.splits + split) * n0 + m] = issued ? (double)v[0] : 0.0;
+  }
   umma::fence_before();
   __syncthreads();
-  if (warp == 0) umma::tmem_free<128>(tmem);
+  if (warp == 0) umma::tmem_free<256>(tmem);
   if (tid == 0) {
     __threadfence();
     int* done = a.flags + (int64_t)gridDim.x;
@@ -767,7 +850,7 @@ size_t tc_smem(int SC, int nx, int nu, int dslot, int n0, int64_t per) {
   st = (st + 15) & ~size_t(15);
   const int KC = ((SC * nx + 7) / 8) * 8;
   const size_t bufb = 16 * (size_t)(KC / 4) * 128;
-  size_t b = ((2 * st + 127) & ~size_t(127)) + 4 * bufb;
+  size_t b = ((2 * st + 127) & ~size_t(127)) + 4 * bufb + 4 * (size_t)(KC / 4) * 128;
   b += sizeof(float) * ((size_t)SC * nx * nx + (size_t)SC * nx);
   b = (b + 15) & ~size_t(15);
   b += sizeof(double) * ((size_t)SC * nx + n0) + 8 + 8;
@@ -891,7 +974,8 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   cudaStream_t st = (cudaStream_t)stream;
   GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int occ = 0;
-  GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, sm));
+  const int threads = tck ? kTcThreads : 256;
+  GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, sm));
   if (occ < 1) return gm_fail(ctx, GM_ERR_CONFIG, "fused condensing kernel does not fit an SM");
   const int splits = (int)((M + per - 1) / per);
   rc = ensure_deps(ctx, per, splits);
@@ -934,7 +1018,7 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   a.partH = (float*)scr;
   a.partg = (double*)(scr + up(pH));
   a.flags = ctx->d_flags;
-  kern<<<(unsigned)grid, 256, sm, st>>>(a);
+  kern<<<(unsigned)grid, (unsigned)threads, sm, st>>>(a);
   GM_LAUNCH_CHECK(ctx, "k_condense_fused");
   PairReduceArgs ra{};
   ra.nu = nu;

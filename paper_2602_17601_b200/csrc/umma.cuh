@@ -136,6 +136,85 @@ __device__ __forceinline__ void put_split(unsigned char* hi_buf, unsigned char* 
   *(float*)(lo_buf + o) = x - h;
 }
 
+// NX consecutive K positions k0 .. k0+NX-1 of operand row r (k0 = li * NX),
+// split into hi / lo, with 16- / 8-byte stores (a warp over consecutive rows
+// then writes whole 128-B core-matrix rows: no bank conflicts)
+template <int NX>
+__device__ __forceinline__ void putn_split(unsigned char* hb, unsigned char* lb, int r, int k0,
+                                           uint32_t sbo, const float* x) {
+  float h[NX], l[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    h[i] = tf32_hi(x[i]);
+    l[i] = x[i] - h[i];
+  }
+  const uint32_t base = (uint32_t)(r >> 3) * sbo + (uint32_t)(r & 7) * 16u + (uint32_t)(k0 >> 2) * 128u;
+  if constexpr (NX == 6) {
+    if ((k0 & 3) == 0) {
+      *(float4*)(hb + base) = make_float4(h[0], h[1], h[2], h[3]);
+      *(float2*)(hb + base + 128) = make_float2(h[4], h[5]);
+      *(float4*)(lb + base) = make_float4(l[0], l[1], l[2], l[3]);
+      *(float2*)(lb + base + 128) = make_float2(l[4], l[5]);
+    } else {
+      *(float2*)(hb + base + 8) = make_float2(h[0], h[1]);
+      *(float4*)(hb + base + 128) = make_float4(h[2], h[3], h[4], h[5]);
+      *(float2*)(lb + base + 8) = make_float2(l[0], l[1]);
+      *(float4*)(lb + base + 128) = make_float4(l[2], l[3], l[4], l[5]);
+    }
+  } else if constexpr (NX == 4) {
+    *(float4*)(hb + base) = make_float4(h[0], h[1], h[2], h[3]);
+    *(float4*)(lb + base) = make_float4(l[0], l[1], l[2], l[3]);
+  } else if constexpr (NX == 2) {
+    *(float2*)(hb + base + (k0 & 3) * 4) = make_float2(h[0], h[1]);
+    *(float2*)(lb + base + (k0 & 3) * 4) = make_float2(l[0], l[1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      const uint32_t o = kmajor_offset(r, k0 + i, sbo);
+      *(float*)(hb + o) = h[i];
+      *(float*)(lb + o) = l[i];
+    }
+  }
+}
+
+// x = hi + lo (exact fp32) of NX consecutive K positions of operand row r
+template <int NX>
+__device__ __forceinline__ void getn(const unsigned char* hb, const unsigned char* lb, int r, int k0,
+                                     uint32_t sbo, float* x) {
+  const uint32_t base = (uint32_t)(r >> 3) * sbo + (uint32_t)(r & 7) * 16u + (uint32_t)(k0 >> 2) * 128u;
+  if constexpr (NX == 6) {
+    float4 a, b, c, d;
+    float2 e, f;
+    if ((k0 & 3) == 0) {
+      a = *(const float4*)(hb + base);
+      b = *(const float4*)(lb + base);
+      e = *(const float2*)(hb + base + 128);
+      f = *(const float2*)(lb + base + 128);
+      x[0] = a.x + b.x; x[1] = a.y + b.y; x[2] = a.z + b.z; x[3] = a.w + b.w;
+      x[4] = e.x + f.x; x[5] = e.y + f.y;
+    } else {
+      e = *(const float2*)(hb + base + 8);
+      f = *(const float2*)(lb + base + 8);
+      c = *(const float4*)(hb + base + 128);
+      d = *(const float4*)(lb + base + 128);
+      x[0] = e.x + f.x; x[1] = e.y + f.y;
+      x[2] = c.x + d.x; x[3] = c.y + d.y; x[4] = c.z + d.z; x[5] = c.w + d.w;
+    }
+  } else if constexpr (NX == 4) {
+    const float4 a = *(const float4*)(hb + base), b = *(const float4*)(lb + base);
+    x[0] = a.x + b.x; x[1] = a.y + b.y; x[2] = a.z + b.z; x[3] = a.w + b.w;
+  } else if constexpr (NX == 2) {
+    const float2 a = *(const float2*)(hb + base + (k0 & 3) * 4), b = *(const float2*)(lb + base + (k0 & 3) * 4);
+    x[0] = a.x + b.x; x[1] = a.y + b.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      const uint32_t o = kmajor_offset(r, k0 + i, sbo);
+      x[i] = *(const float*)(hb + o) + *(const float*)(lb + o);
+    }
+  }
+}
+
 // D[m][n] += sum_k A(m, k) B(n, k) over ksteps x 8 columns of K, 3xTF32.
 // A and B buffers: K-major (see top), SBO sbo_a / sbo_b, 128-B LBO.
 // Called by ONE thread.

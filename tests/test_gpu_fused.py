@@ -93,7 +93,7 @@ def _check(ref, outs, n0, nu, N, tol=2e-6):
         assert np.max(np.abs(Hf - Hr)) <= tol * scale
         assert np.array_equal(Hf, np.swapaxes(Hf, 1, 2))  # exactly symmetric
         gr, gf = g1.cpu().numpy(), g2.cpu().numpy()
-        assert np.max(np.abs(gf - gr)) <= 2e-6 * max(1.0, np.max(np.abs(gr)))
+        assert np.max(np.abs(gf - gr)) <= tol * max(1.0, np.max(np.abs(gr)))
     # bitwise reproducible across launches
     for W2, H2, g2 in outs[1:]:
         assert torch_equal(H2, outs[0][1]) and torch_equal(g2, outs[0][2])
@@ -118,7 +118,8 @@ def torch_equal(a, b):
 def test_fused_matches_two_kernel_path(graph, N, nx, nu, B, mode):
     """mode 0: tcgen05 3xTF32 H (k_condense_tc), 1: SIMT fp32 H (k_condense_fused).
     Gamma is bitwise identical in both; H agrees with the fp32 SIMT K-HG to
-    fp32 round-off (3xTF32 drops the lo*lo term, ~2^-22 relative)."""
+    fp32 round-off (3xTF32 drops the lo*lo term, ~2^-22 relative); in mode 0
+    g is accumulated in fp32 on the tensor core too (fp64 in the SIMT kernel)."""
     from paper_2602_17601_b200.graph import GraphTopology, chain_topology, mesh_topology
 
     if graph == "chain1000":
