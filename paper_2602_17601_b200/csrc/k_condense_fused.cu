@@ -30,6 +30,7 @@
 // Numerics equal the two-kernel path: the same fp32 Gamma recursion (c rounded
 // once to fp32, as K-REC), fp32 partial sums, fp64 reduction.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "common.cuh"
@@ -42,6 +43,7 @@ constexpr int kTcThreads = 512;  // k_condense_tc block size (16 warps: latency 
 
 struct FusedArgs {
   int M, E, N, ld, per, splits, sc, npairs, dslot;
+  int reg_prefetch;  // k_condense_tc: register prefetch of the next item's neighbour rows
   const int* ptr;
   const int* src;
   const int* dep_ptr;
@@ -624,7 +626,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     // rows (same stage: its dependencies are already met), in flight while
     // this item's B operand is built and its MMAs run
     pre_ok = false;
-    if (sub + 1 < nsub) {
+    if (a.reg_prefetch && sub + 1 < nsub) {
       const int s0n = s0 + SC, scn = min(SC, ne - s0n);
       if (tid < scn * lw) {
         const int li = tid / lw, cc = tid - li * lw;
@@ -1018,6 +1020,10 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   a.partH = (float*)scr;
   a.partg = (double*)(scr + up(pH));
   a.flags = ctx->d_flags;
+  {
+    const char* v = getenv("GM_TC_PREFETCH");
+    a.reg_prefetch = v ? atoi(v) : 1;
+  }
   kern<<<(unsigned)grid, (unsigned)threads, sm, st>>>(a);
   GM_LAUNCH_CHECK(ctx, "k_condense_fused");
   PairReduceArgs ra{};
