@@ -41,7 +41,10 @@ sys.path.insert(0, str(ROOT))
 METRIC = "MPC step latency ms (linearize+condense+QP) & Hz at N nodes; solves/sec batched"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the round's
 # `ncu --set full` captures at cfg3 (profiles/r01/ncu_full_summary_v3.txt)
-NCU_TRAFFIC = {"k_solve_qp": 747008, "k_linearize": 1182464, "k_condense_fused": 35225344}
+NCU_TRAFFIC = {"k_solve_qp": 751616, "k_linearize": 1213440, "k_condense_tc": 32530688}
+# sm__pipe_tensor_cycles_active (% of peak, active cycles) of K-COND's tcgen05
+# H/g accumulation from the same capture
+NCU_TENSOR_PCT = {"k_condense_tc": 4.79}
 # cfg3 linearize flops, psi-VJP formulation
 LIN_FLOPS_CFG3 = 1.53e9
 M_NODES, HORIZON = 1000, 20
@@ -301,10 +304,11 @@ def ours_arm(args, world, rank, local):
     ng = plan.ds.ns + (plan.ds.rows.n_st)  # general (multi-nonzero) rows: the soft rows
     fl = qp_flops(n, m, ng, iters)
     fp64_sm_peak = 64 * 2 * smax / 1e12  # one CTA on one SM: 64 DFMA/clk
-    roof = {"kernel": "k_solve_qp (+k_finish)", "bound": "fp64-one-SM",
+    roof = {"kernel": "k_solve_qp (+k_finish)", "bound": "tensor",
             "achieved": fl / (solve * 1e-3) / 1e12, "peak": fp64_sm_peak, "unit": "TFLOP/s",
             "frac": (fl / (solve * 1e-3) / 1e12) / fp64_sm_peak, "traffic": None,
-            "note": "latency-bound single-CTA fp64 IPM; peak = FP64 FMA rate of one SM at max clock"}
+            "note": "single-CTA fp64 IPM (Schur build and Cholesky updates on fp64 DMMA); peak = the fp64 "
+                    "tensor/FMA rate of the ONE SM it runs on at max clock (64 DFMA/clk); latency-bound"}
 
     # HBM roofline of the Gamma recursion + H/g kernel (K-COND): compulsory
     # bytes of the recursion (read stage n of Gamma once, write
@@ -316,13 +320,22 @@ def ours_arm(args, world, rank, local):
     cond = float(np.mean(cond_ms))
     hbm_peak = float(peaks.get("hbm_gbs") or 6449.1)
     cond_gbs = (gam + blocks) / (cond * 1e-3) / 1e9
+    # H on the tensor cores: causal Gram flops x3 (3xTF32) against
+    # the dense tf32 peak
+    hfl = M * sum(2 * nx * nx * k * nu + 2 * nx * (k * nu) ** 2 for k in range(1, N + 1))
+    tf32_peak = float(peaks.get("tf32_tflops") or 1100.0)
     # K-LIN: algorithmic flops of the psi-VJP formulation, FP32 SIMT
     lin = float(np.mean(lin_ms))
     stages = {
-        "k_condense_fused": {"bound": "hbm", "achieved": cond_gbs, "peak": hbm_peak, "unit": "GB/s",
-                             "frac": cond_gbs / hbm_peak, "algorithmic_bytes": gam + blocks,
-                             "traffic": NCU_TRAFFIC.get("k_condense_fused"),
-                             "note": "stage time incl. constraint rows/soft expansion; Gamma is L2-resident at cfg3"},
+        "k_condense_tc": {"bound": "hbm", "achieved": cond_gbs, "peak": hbm_peak, "unit": "GB/s",
+                          "frac": cond_gbs / hbm_peak, "algorithmic_bytes": gam + blocks,
+                          "traffic": NCU_TRAFFIC.get("k_condense_tc"),
+                          "h_tensor": {"algorithmic_flops": hfl, "issued_tf32_flops": 3 * hfl,
+                                       "achieved_tflops": 3 * hfl / (cond * 1e-3) / 1e12,
+                                       "peak_tflops": tf32_peak,
+                                       "tensor_pipe_pct_ncu": NCU_TENSOR_PCT.get("k_condense_tc")},
+                          "note": "stage time incl. constraint rows/soft expansion; Gamma is L2-resident at cfg3; "
+                                  "H and g accumulate on tcgen05 (3xTF32) inside the recursion kernel"},
         "k_linearize": {"bound": "fp32/fp64 SIMT", "ms": lin,
                         "achieved": LIN_FLOPS_CFG3 / (lin * 1e-3) / 1e12 if (M, N) == (1000, 20) else None,
                         "unit": "TFLOP/s", "traffic": NCU_TRAFFIC.get("k_linearize")},
