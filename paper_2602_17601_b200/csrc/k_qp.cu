@@ -191,15 +191,7 @@ __device__ __forceinline__ void invert_diag_blocks(Qs& S) {
 // x = K^{-1} b = X' (X b) through the padded solve vector S.yv (padding stays
 // zero); b and x are shared nf-vectors (x may alias b).  Call with all threads.
 __device__ void chol_solve(Qs& S, const double* b, double* x) {
-  for (int r = threadIdx.x; r < S.nf; r += blockDim.x) S.yv[r] = b[r];
-  __syncthreads();
-  if (S.T > 0) {
-    double* tmp = S.yv + 8 * S.T;
-    qpchol::apply_x<kQpThreads>(S.K, S.T, S.yv, tmp);
-    qpchol::apply_xt<kQpThreads>(S.K, S.T, S.yv, tmp);
-  }
-  for (int r = threadIdx.x; r < S.nf; r += blockDim.x) x[r] = S.yv[r];
-  __syncthreads();
+  if (S.T > 0) qpchol::solve_xxt<kQpThreads>(S.K, S.T, S.nf, b, x, S.yv + 8 * S.T);
 }
 
 // ---------------------------------------------------------------------------
@@ -473,18 +465,31 @@ __device__ void reduced_solve(Qs& S, const double* b, double* x) {
   __syncthreads();
   chol_solve(S, yr, yr);
   for (int k = threadIdx.x; k < S.nf; k += blockDim.x) x[S.kidx[k]] = yr[k];
-  // eliminated: one warp per eliminated variable
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int e = wid; e < S.ne; e += kQpWarps) {
-    const int gi = S.egi[e];
+  // eliminated: one 8-lane group per eliminated variable, all groups at once
+  constexpr int G = 8;
+  const int lg = threadIdx.x & (G - 1);
+  for (int e0 = 0; e0 < S.ne; e0 += kQpThreads / G) {
+    const int e = e0 + (int)threadIdx.x / G;
+    const bool live = e < S.ne;
+    const int gi = live ? S.egi[e] : -1;
     double s = 0.0;
     if (gi >= 0) {
       const double* row = S.Cg + (int64_t)gi * S.n;
-      for (int k = lane; k < S.nf; k += 32) s = fma(row[k], yr[k], s);
-      s = warp_sum(s);
-      s *= S.w[S.grow[gi]] * S.ea[e];
+      double s1 = 0.0;
+      int k = lg;
+      for (; k + G < S.nf; k += 2 * G) {
+        s = fma(row[k], yr[k], s);
+        s1 = fma(row[k + G], yr[k + G], s1);
+      }
+      if (k < S.nf) s = fma(row[k], yr[k], s);
+      s += s1;
     }
-    if (lane == 0) x[S.eidx[e]] = (b[S.eidx[e]] - s) / S.kee[e];
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (live && lg == 0) {
+      if (gi >= 0) s *= S.w[S.grow[gi]] * S.ea[e];
+      x[S.eidx[e]] = (b[S.eidx[e]] - s) / S.kee[e];
+    }
   }
   __syncthreads();
 }

@@ -384,77 +384,148 @@ __device__ __noinline__ void invert_full(double* Kt, int T, const double* dinv, 
   }
 }
 
-// y <- X y (X = L^{-1} in Kt, lower): two threads per row, each over every
-// other tile of the row, 4 accumulators; the halves meet through a shuffle.
+// y <- X y (X = L^{-1} in Kt, lower).  One warp per tile row-block I
+// (blocks dealt in mirrored pairs w, 2NW-1-w, ... so every warp sums about
+// the same number of tiles); lane (rr, cq) owns row rr and columns 2cq, 2cq+1
+// of each tile, two independent FMA chains, then a 4-lane shuffle reduce.
+// The two column loads alternate order by cq parity so a warp's first loads
+// fall on 16 different bank pairs (2 wavefronts, the minimum).
 // y: shared, 8T entries; tmp: 8T doubles.  All NT threads call.
 template <int NT>
 __device__ __noinline__ void apply_x(const double* Kt, int T, double* y, double* tmp) {
   QP_SMEM(Kt);
   QP_SMEM(y);
   QP_SMEM(tmp);
-  const int tid = threadIdx.x;
-  const int rows = 8 * T;
-  for (int t0 = 0; t0 < 2 * rows; t0 += NT) {
-    const int t = t0 + tid;
-    const bool live = t < 2 * rows;
-    const int r = live ? t >> 1 : 0, h = t & 1;
-    const int I = r >> 3, rr = r & 7;
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-    if (live)
-      for (int J = h; J <= I; J += 2) {
-        const double* Xt = Kt + ti(I, J) * kTS;
-        const double* yy = y + 8 * J;
-        c0 = fma(Xt[eo(rr, 0)], yy[0], c0);
-        c1 = fma(Xt[eo(rr, 1)], yy[1], c1);
-        c2 = fma(Xt[eo(rr, 2)], yy[2], c2);
-        c3 = fma(Xt[eo(rr, 3)], yy[3], c3);
-        c0 = fma(Xt[eo(rr, 4)], yy[4], c0);
-        c1 = fma(Xt[eo(rr, 5)], yy[5], c1);
-        c2 = fma(Xt[eo(rr, 6)], yy[6], c2);
-        c3 = fma(Xt[eo(rr, 7)], yy[7], c3);
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int rr = lane >> 2, cq = lane & 3;
+  const int ca = 2 * cq + (cq & 1), cb = 2 * cq + 1 - (cq & 1);
+  for (int base = 0; base < T; base += 2 * NW) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int I = h == 0 ? base + wid : base + 2 * NW - 1 - wid;
+      if (I >= T) continue;
+      double s0 = 0.0, s1 = 0.0;
+      const double* Xt = Kt + ti(I, 0) * kTS;
+      for (int J = 0; J <= I; ++J, Xt += kTS) {
+        s0 = fma(Xt[eo(rr, ca)], y[8 * J + ca], s0);
+        s1 = fma(Xt[eo(rr, cb)], y[8 * J + cb], s1);
       }
-    double v = (c0 + c1) + (c2 + c3);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    if (live && !h) tmp[r] = v;
+      double v = s0 + s1;
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (cq == 0) tmp[8 * I + rr] = v;
+    }
   }
   __syncthreads();
-  for (int r = tid; r < rows; r += NT) y[r] = tmp[r];
+  for (int r = threadIdx.x; r < 8 * T; r += NT) y[r] = tmp[r];
   __syncthreads();
 }
 
-// y <- X' y: two threads per column c, each over every other tile row I >= C.
+// y <- X' y: one warp per tile column-block C (mirrored pairs as above);
+// lane (cc, rq) owns column cc and rows 2rq, 2rq+1 of each tile (I, C), I >= C.
 template <int NT>
 __device__ __noinline__ void apply_xt(const double* Kt, int T, double* y, double* tmp) {
   QP_SMEM(Kt);
   QP_SMEM(y);
   QP_SMEM(tmp);
-  const int tid = threadIdx.x;
-  const int cols = 8 * T;
-  for (int t0 = 0; t0 < 2 * cols; t0 += NT) {
-    const int t = t0 + tid;
-    const bool live = t < 2 * cols;
-    const int c = live ? t >> 1 : 0, h = t & 1;
-    const int C = c >> 3, cc = c & 7;
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-    if (live)
-      for (int I = C + h; I < T; I += 2) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int cc = lane >> 2, rq = lane & 3;
+  for (int base = 0; base < T; base += 2 * NW) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int C = h == 0 ? base + wid : base + 2 * NW - 1 - wid;
+      if (C >= T) continue;
+      double s0 = 0.0, s1 = 0.0;
+      for (int I = C; I < T; ++I) {
         const double* Xt = Kt + ti(I, C) * kTS;
-        const double* yy = y + 8 * I;
-        c0 = fma(Xt[eo(0, cc)], yy[0], c0);
-        c1 = fma(Xt[eo(1, cc)], yy[1], c1);
-        c2 = fma(Xt[eo(2, cc)], yy[2], c2);
-        c3 = fma(Xt[eo(3, cc)], yy[3], c3);
-        c0 = fma(Xt[eo(4, cc)], yy[4], c0);
-        c1 = fma(Xt[eo(5, cc)], yy[5], c1);
-        c2 = fma(Xt[eo(6, cc)], yy[6], c2);
-        c3 = fma(Xt[eo(7, cc)], yy[7], c3);
+        s0 = fma(Xt[eo(2 * rq, cc)], y[8 * I + 2 * rq], s0);
+        s1 = fma(Xt[eo(2 * rq + 1, cc)], y[8 * I + 2 * rq + 1], s1);
       }
-    double v = (c0 + c1) + (c2 + c3);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    if (live && !h) tmp[c] = v;
+      double v = s0 + s1;
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (rq == 0) tmp[8 * C + cc] = v;
+    }
   }
   __syncthreads();
-  for (int r = tid; r < cols; r += NT) y[r] = tmp[r];
+  for (int r = threadIdx.x; r < 8 * T; r += NT) y[r] = tmp[r];
+  __syncthreads();
+}
+
+// x = X' (X b) = K^{-1} b in one call: two barrier-separated mat-vec phases,
+// no staging copies.  Phase 1 (tmp = X b) and phase 2 (x = X' tmp) use the
+// warp-per-tile-block scheme of apply_x / apply_xt with the tile loop
+// unrolled by two (four independent FMA chains).  b: nf entries (padding rows
+// read as zero); x may alias b; tmp: 8T doubles.  All NT threads call.
+template <int NT>
+__device__ __noinline__ void solve_xxt(const double* Kt, int T, int nf, const double* b, double* x,
+                                       double* tmp) {
+  QP_SMEM(Kt);
+  QP_SMEM(tmp);
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  {
+    const int rr = lane >> 2, cq = lane & 3;
+    const int ca = 2 * cq + (cq & 1), cb = 2 * cq + 1 - (cq & 1);
+    for (int base = 0; base < T; base += 2 * NW) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int I = h == 0 ? base + wid : base + 2 * NW - 1 - wid;
+        if (I >= T) continue;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        const double* Xt = Kt + ti(I, 0) * kTS;
+        int J = 0;
+        for (; J + 1 <= I; J += 2, Xt += 2 * kTS) {
+          const int ja = 8 * J + ca, jb = 8 * J + cb;
+          s0 = fma(Xt[eo(rr, ca)], ja < nf ? b[ja] : 0.0, s0);
+          s1 = fma(Xt[eo(rr, cb)], jb < nf ? b[jb] : 0.0, s1);
+          s2 = fma(Xt[kTS + eo(rr, ca)], ja + 8 < nf ? b[ja + 8] : 0.0, s2);
+          s3 = fma(Xt[kTS + eo(rr, cb)], jb + 8 < nf ? b[jb + 8] : 0.0, s3);
+        }
+        if (J == I) {
+          const int ja = 8 * J + ca, jb = 8 * J + cb;
+          s0 = fma(Xt[eo(rr, ca)], ja < nf ? b[ja] : 0.0, s0);
+          s1 = fma(Xt[eo(rr, cb)], jb < nf ? b[jb] : 0.0, s1);
+        }
+        double v = (s0 + s1) + (s2 + s3);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (cq == 0) tmp[8 * I + rr] = v;
+      }
+    }
+  }
+  __syncthreads();
+  {
+    const int cc = lane >> 2, rq = lane & 3;
+    for (int base = 0; base < T; base += 2 * NW) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int C = h == 0 ? base + wid : base + 2 * NW - 1 - wid;
+        if (C >= T) continue;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int I = C;
+        for (; I + 1 < T; I += 2) {
+          const double* X0 = Kt + ti(I, C) * kTS;
+          const double* X1 = Kt + ti(I + 1, C) * kTS;
+          s0 = fma(X0[eo(2 * rq, cc)], tmp[8 * I + 2 * rq], s0);
+          s1 = fma(X0[eo(2 * rq + 1, cc)], tmp[8 * I + 2 * rq + 1], s1);
+          s2 = fma(X1[eo(2 * rq, cc)], tmp[8 * I + 8 + 2 * rq], s2);
+          s3 = fma(X1[eo(2 * rq + 1, cc)], tmp[8 * I + 9 + 2 * rq], s3);
+        }
+        if (I < T) {
+          const double* X0 = Kt + ti(I, C) * kTS;
+          s0 = fma(X0[eo(2 * rq, cc)], tmp[8 * I + 2 * rq], s0);
+          s1 = fma(X0[eo(2 * rq + 1, cc)], tmp[8 * I + 2 * rq + 1], s1);
+        }
+        double v = (s0 + s1) + (s2 + s3);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (rq == 0 && 8 * C + cc < nf) x[8 * C + cc] = v;
+      }
+    }
+  }
   __syncthreads();
 }
 
