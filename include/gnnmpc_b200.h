@@ -120,7 +120,9 @@ int gm_linearize(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
 
 /* Linearisation kernel selection: 0 = automatic (fused per-tile kernel for
  * fewer than 200k node points, layer-wise GEMM chain above), 1 = always the
- * fused kernel, 2 = always the layer-wise chain.  Both compute the same
+ * fused kernel, 2 = always the layer-wise chain (Jacobian chains fused per row
+ * for the reference architecture), 3 = layer-wise with one launch per
+ * Jacobian layer.  Both compute the same
  * formulas; the switch exists for tests and benchmarks. */
 int gm_set_linearize_mode(gm_ctx* ctx, int mode);
 

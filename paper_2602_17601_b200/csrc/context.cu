@@ -88,7 +88,7 @@ int gm_create(gm_ctx** out, int device) {
   if (const char* v = getenv("GM_CONDENSE_MODE")) c->cond_mode = atoi(v) == 1 ? 1 : 0;
   if (const char* v = getenv("GM_LINEARIZE_MODE")) {
     const int m = atoi(v);
-    c->lin_mode = (m >= 0 && m <= 2) ? m : 0;
+    c->lin_mode = (m >= 0 && m <= 3) ? m : 0;
   }
   *out = c;
   return GM_OK;

@@ -10,25 +10,86 @@
 
 namespace {
 
-__device__ __forceinline__ double planned_entry(const float* W, int ld, int N, int nx, int nu,
-                                                int64_t gi, int k, int a, const double* u) {
-  const float* row = W + ((gi * (N + 1) + k) * nx + a) * (int64_t)ld;
-  // only the causal columns [0, k*nu) can be non-zero
-  double s = 0.0;
-  const int live = k * nu;
-  for (int c = 0; c < live; ++c) s = fma((double)row[c], u[c], s);
-  return s + (double)row[N * nu];
+// Planned-state rows of node gi at stage k, (Gamma_u u + Gamma_x)[a] for
+// a < nx, by one warp: lane l reads the 16-byte column chunks l*4 + 128 j of
+// each row (coalesced 512-B rows; only chunks holding causal columns
+// [0, k*nu) or the Gamma_x column), the loads of up to 8 rows are issued
+// before any arithmetic, and each row's partial sums meet in a fixed-order
+// butterfly (bitwise reproducible).  Lane a < nx returns row a.
+__device__ __forceinline__ double warp_rows(const float* W, int ld, int N, int nx, int nu, int64_t gi, int k,
+                                            const double* u, int lane) {
+  const float* rows = W + ((gi * (N + 1) + k) * nx) * (int64_t)ld;
+  const int live = k * nu, xc = N * nu;
+  double mine = 0.0;
+  for (int a0 = 0; a0 < nx; a0 += 8) {
+    double s[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] = 0.0;
+    for (int c0 = lane * 4; c0 < ld; c0 += 128) {
+      if (c0 >= live && (xc < c0 || xc >= c0 + 4)) continue;
+      double coef[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + j;
+        coef[j] = c < live ? u[c] : (c == xc ? 1.0 : 0.0);
+      }
+      float4 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (a0 + q < nx) v[q] = __ldcs(reinterpret_cast<const float4*>(rows + (int64_t)(a0 + q) * ld + c0));
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (a0 + q < nx) {
+          s[q] = fma((double)v[q].x, coef[0], s[q]);
+          s[q] = fma((double)v[q].y, coef[1], s[q]);
+          s[q] = fma((double)v[q].z, coef[2], s[q]);
+          s[q] = fma((double)v[q].w, coef[3], s[q]);
+        }
+    }
+    // reduce-scatter butterfly: after the xor-16/8/4 levels lane l holds a
+    // partial of row 4*b4 + 2*b3 + b2 (b = bits of l) summed over 8 lanes,
+    // the xor-2/1 levels finish it: lane 4a holds row a (9 exchanges for 8
+    // rows instead of 40)
+    const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+    double t4[4], t2[2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double send = h4 ? s[q] : s[q + 4];
+      const double keep = h4 ? s[q + 4] : s[q];
+      t4[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double send = h3 ? t4[q] : t4[q + 2];
+      const double keep = h3 ? t4[q + 2] : t4[q];
+      t2[q] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    double v;
+    {
+      const double send = h2 ? t2[0] : t2[1];
+      const double keep = h2 ? t2[1] : t2[0];
+      v = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    const double got = __shfl_sync(0xffffffffu, v, (4 * (lane - a0)) & 31);
+    if (lane >= a0 && lane < a0 + 8) mine = got;
+  }
+  return mine;
 }
 
-__global__ void k_reconstruct(const float* W, int ld, int M, int N, int nx, int nu,
-                              const double* u, int ldu, double* x, int64_t total) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int a = (int)(t % nx);
-    const int k = (int)((t / nx) % (N + 1));
-    const int64_t gi = t / ((int64_t)nx * (N + 1));
+// one warp per (node, stage) item, items in Gamma's memory order
+__global__ void __launch_bounds__(256, 3) k_reconstruct(const float* W, int ld, int M, int N, int nx, int nu,
+                              const double* u, int ldu, double* x, int64_t items) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = w0; w < items; w += nw) {
+    const int k = (int)(w % (N + 1));
+    const int64_t gi = w / (N + 1);
     const int64_t bi = gi / M;
-    x[t] = planned_entry(W, ld, N, nx, nu, gi, k, a, u + bi * ldu);
+    const double v = warp_rows(W, ld, N, nx, nu, gi, k, u + bi * ldu, lane);
+    if (lane < nx) x[(gi * (N + 1) + k) * nx + lane] = v;
   }
 }
 
@@ -59,28 +120,31 @@ __device__ __forceinline__ bool solved(int st) {
 
 // state entries: (1-a) lin + a planned (mpc.py:396-398), or the fallback plan
 // when the solve failed (mpc.py:415-418).
-__global__ void k_finish_states(const FinishArgs A, int64_t total) {
+__global__ void __launch_bounds__(256, 3) k_finish_states(const FinishArgs A, int64_t items) {
   const int M = A.M, N = A.N, nx = A.nx;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int a = (int)(t % nx);
-    const int i = (int)((t / nx) % M);
-    const int k = (int)((t / ((int64_t)nx * M)) % (N + 1));
-    const int64_t bi = t / ((int64_t)nx * M * (N + 1));
-    double v;
-    if (solved(A.status[bi])) {
-      const double p = planned_entry(A.W, A.ld, N, nx, A.nu, bi * M + i, k, a, A.u + bi * A.ldu);
-      v = (1.0 - A.damp) * A.lin_states[t] + A.damp * p;
-    } else {
-      v = A.fb_states[t];
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = w0; w < items; w += nw) {  // (bi, i, k): Gamma's memory order
+    const int k = (int)(w % (N + 1));
+    const int64_t gi = w / (N + 1);
+    const int i = (int)(gi % M);
+    const int64_t bi = gi / M;
+    const bool ok = solved(A.status[bi]);
+    double p = 0.0;
+    if (ok) p = warp_rows(A.W, A.ld, N, nx, A.nu, gi, k, A.u + bi * A.ldu, lane);
+    if (lane < nx) {
+      const int a = lane;
+      const int64_t t = ((bi * (N + 1) + k) * M + i) * nx + a;
+      const double v = ok ? (1.0 - A.damp) * A.lin_states[t] + A.damp * p : A.fb_states[t];
+      if (A.cur_states) A.cur_states[t] = v;
+      // planned_states (M, N+1, nx) = lin_states.transpose(1, 0, 2)   (mpc.py:407)
+      A.planned_states[((bi * M + i) * (N + 1) + k) * nx + a] = v;
+      // _shift (mpc.py:90-99): s[k-1] = s[k] for k >= 1, s[N] = s[N]
+      const int64_t base = bi * (int64_t)(N + 1) * M * nx;
+      if (k >= 1) A.next_states[base + ((int64_t)(k - 1) * M + i) * nx + a] = v;
+      if (k == N) A.next_states[base + ((int64_t)N * M + i) * nx + a] = v;
     }
-    if (A.cur_states) A.cur_states[t] = v;
-    // planned_states (M, N+1, nx) = lin_states.transpose(1, 0, 2)   (mpc.py:407)
-    A.planned_states[((bi * M + i) * (N + 1) + k) * nx + a] = v;
-    // _shift (mpc.py:90-99): s[k-1] = s[k] for k >= 1, s[N] = s[N]
-    const int64_t base = bi * (int64_t)(N + 1) * M * nx;
-    if (k >= 1) A.next_states[base + ((int64_t)(k - 1) * M + i) * nx + a] = v;
-    if (k == N) A.next_states[base + ((int64_t)N * M + i) * nx + a] = v;
   }
 }
 
@@ -129,11 +193,12 @@ int gm_reconstruct_states(gm_ctx* ctx, int B, int N, const float* gamma, int ld,
   int rc = gm_need_device(ctx);
   if (rc) return rc;
   if (ctx->M < 1 || ctx->nx < 1) return gm_fail(ctx, GM_ERR_CONFIG, "graph/dimensions not set");
-  const int64_t total = (int64_t)B * ctx->M * (N + 1) * ctx->nx;
-  if (total == 0) return GM_OK;
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8 * ctx->sm_count);
+  if (ld % 4 != 0 || ((uintptr_t)gamma & 15)) return gm_fail(ctx, GM_ERR_CONFIG, "gamma rows must be 16-byte aligned (ld % 4 == 0)");
+  const int64_t items = (int64_t)B * ctx->M * (N + 1);
+  if (items == 0) return GM_OK;
+  const int blocks = (int)std::min<int64_t>((items + 7) / 8, 16 * ctx->sm_count);
   k_reconstruct<<<blocks, 256, 0, (cudaStream_t)stream>>>(gamma, ld, (int)ctx->M, N, ctx->nx,
-                                                          ctx->n_u, u, ldu, x, total);
+                                                          ctx->n_u, u, ldu, x, items);
   GM_LAUNCH_CHECK(ctx, "k_reconstruct");
   return GM_OK;
 }
@@ -149,6 +214,7 @@ int gm_mpc_finish(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const d
   if (rc) return rc;
   if (ctx->M < 1 || ctx->nx < 1) return gm_fail(ctx, GM_ERR_CONFIG, "graph/dimensions not set");
   if (B == 0) return GM_OK;
+  if (ld % 4 != 0 || ((uintptr_t)gamma & 15)) return gm_fail(ctx, GM_ERR_CONFIG, "gamma rows must be 16-byte aligned (ld % 4 == 0)");
   FinishArgs a{};
   a.M = (int)ctx->M;
   a.N = N;
@@ -176,9 +242,9 @@ int gm_mpc_finish(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const d
   a.u_applied = u_applied;
   a.summary = summary;
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t total = (int64_t)B * (N + 1) * ctx->M * ctx->nx;
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8 * ctx->sm_count);
-  k_finish_states<<<blocks, 256, 0, st>>>(a, total);
+  const int64_t items = (int64_t)B * (N + 1) * ctx->M;
+  const int blocks = (int)std::min<int64_t>((items + 7) / 8, 16 * ctx->sm_count);
+  k_finish_states<<<blocks, 256, 0, st>>>(a, items);
   GM_LAUNCH_CHECK(ctx, "k_finish_states");
   const int64_t ti = (int64_t)B * N * ctx->n_u;
   k_finish_inputs<<<(int)std::max<int64_t>(1, std::min<int64_t>((ti + 255) / 256, 1024)), 256, 0, st>>>(a, B);

@@ -450,7 +450,7 @@ int launch_linearize(gm_ctx* ctx, int64_t P, const double* X, const double* U, f
   // fused kernel: ~27 launches of small GEMMs cost more than one fused pass)
   constexpr int64_t kLayerMinRows = 200000;
   const bool big = P * (hi - lo) >= kLayerMinRows;
-  if (jac && ctx->phi.L >= 2 && ctx->psi.L >= 1 && (ctx->lin_mode == 2 || (ctx->lin_mode == 0 && big)))
+  if (jac && ctx->phi.L >= 2 && ctx->psi.L >= 1 && (ctx->lin_mode >= 2 || (ctx->lin_mode == 0 && big)))
     return launch_linearize_layers(ctx, P, X, U, a_self, a_nbr, b, c, f_next, stream);
   const int nx = ctx->m_nx, nu = ctx->m_nu, n_p = ctx->n_p;
   const int nin = ctx->phi.dims[0];
@@ -519,7 +519,7 @@ int gm_linearize(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
 
 int gm_set_linearize_mode(gm_ctx* ctx, int mode) {
   if (!ctx) return GM_ERR_CONFIG;
-  if (mode < 0 || mode > 2) return gm_fail(ctx, GM_ERR_CONFIG, "linearize mode must be 0, 1 or 2");
+  if (mode < 0 || mode > 3) return gm_fail(ctx, GM_ERR_CONFIG, "linearize mode must be 0, 1, 2 or 3");
   ctx->lin_mode = mode;
   return GM_OK;
 }

@@ -297,6 +297,237 @@ __global__ void k_lin_c(const LinDims d, int E, const int* __restrict__ ptr, con
   c[(p * d.M + i) * nx + r] = s;
 }
 
+// ---------------------------------------------------------------------------
+// Fused backward Jacobian chains (fp32): seed + every layer of the phi
+// Jacobian (mlp_jacobian, mlp.py:132-145) and of the psi VJP, ONE launch each,
+// one row per thread held in registers.  The layer-by-layer GEMMs above
+// stream every intermediate row block through HBM (at the 1e5-node mesh the
+// psi rows alone are 24 M x 32 floats per layer); here the only traffic is
+// the seed, the mask bytes and the final rows.  Weights sit in shared memory
+// and are read as warp-broadcast 16-/8-byte vectors (4 or 2 FMAs per load).
+// Same per-row formulas and fp32 products as k_layer (summation order within
+// a dot product differs).  Instantiated for the reference architecture
+// (psi [6,32,32,16], phi [28,64,64,3]); other shapes use the layer path.
+// ---------------------------------------------------------------------------
+constexpr int kJT = 128;
+
+// o[c] = (mask[c] ?) sum_k v[k] W[k][c],  W (K, N) row-major in shared memory
+template <int K, int N, bool MASK>
+__device__ __forceinline__ void chain_layer(const float (&v)[K], float (&o)[N], const float* Ws,
+                                            const uint8_t* mrow) {
+  constexpr int VW = (N % 4 == 0) ? 4 : 2;
+  static_assert(N % VW == 0, "layer width must be even");
+#pragma unroll
+  for (int c0 = 0; c0 < N; c0 += VW) {
+    float a[VW];
+#pragma unroll
+    for (int u = 0; u < VW; ++u) a[u] = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if constexpr (VW == 4) {
+        const float4 w = *reinterpret_cast<const float4*>(Ws + k * N + c0);
+        a[0] = fmaf(v[k], w.x, a[0]);
+        a[1] = fmaf(v[k], w.y, a[1]);
+        a[2] = fmaf(v[k], w.z, a[2]);
+        a[3] = fmaf(v[k], w.w, a[3]);
+      } else {
+        const float2 w = *reinterpret_cast<const float2*>(Ws + k * N + c0);
+        a[0] = fmaf(v[k], w.x, a[0]);
+        a[1] = fmaf(v[k], w.y, a[1]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < VW; ++u) o[c0 + u] = a[u];
+  }
+  if constexpr (MASK) {
+#pragma unroll
+    for (int c0 = 0; c0 < N; c0 += 16) {
+      const uint4 mv = *reinterpret_cast<const uint4*>(mrow + c0);
+      const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (c0 + u < N && ((mw[u >> 2] >> (8 * (u & 3))) & 0xffu) == 0) o[c0 + u] = 0.f;
+    }
+  }
+}
+
+// phi Jacobian rows (point, ro): seed W_{L-1}[ro] masked by the last hidden
+// layer, then layers L-2 .. 0 (L = 3): out (Rn*n_p, D0) = jphi
+template <int D0, int D1, int D2>
+__global__ void __launch_bounds__(kJT) k_jac_phi(int Rj, int n_p, const float* __restrict__ w2,
+                                                 const float* __restrict__ w1, const float* __restrict__ w0,
+                                                 const uint8_t* __restrict__ mphi, int hphi,
+                                                 float* __restrict__ out) {
+  __shared__ __align__(16) float s2[4 * D2];  // n_p <= 4 rows of W_2 (D3 x D2)
+  __shared__ __align__(16) float s1[D2 * D1];
+  __shared__ __align__(16) float s0[D1 * D0];
+  for (int t = threadIdx.x; t < n_p * D2; t += kJT) s2[t] = w2[t];
+  for (int t = threadIdx.x; t < D2 * D1; t += kJT) s1[t] = w1[t];
+  for (int t = threadIdx.x; t < D1 * D0; t += kJT) s0[t] = w0[t];
+  __syncthreads();
+  for (int r = blockIdx.x * kJT + threadIdx.x; r < Rj; r += gridDim.x * kJT) {
+    const int pr = r / n_p, ro = r - pr * n_p;
+    const uint8_t* mp = mphi + (int64_t)pr * hphi;
+    float v[D2];
+#pragma unroll
+    for (int c0 = 0; c0 < D2; c0 += 16) {
+      const uint4 mv = *reinterpret_cast<const uint4*>(mp + D1 + c0);  // mask of hidden layer 1
+      const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (c0 + u < D2) v[c0 + u] = ((mw[u >> 2] >> (8 * (u & 3))) & 0xffu) ? s2[ro * D2 + c0 + u] : 0.f;
+    }
+    float h[D1];
+    chain_layer<D2, D1, true>(v, h, s1, mp);  // mask of hidden layer 0
+    float o[D0];
+    chain_layer<D1, D0, false>(h, o, s0, nullptr);
+    float* dst = out + (int64_t)r * D0;
+#pragma unroll
+    for (int c = 0; c < D0; c += 2) *reinterpret_cast<float2*>(dst + c) = make_float2(o[c], o[c + 1]);
+  }
+}
+
+// psi VJP rows (point, edge, ro): seed J_m of the destination node (from
+// jphi), then layers L-1 .. 0 (L = 3): out (Re*n_p, D0) = Pe
+template <int D0, int D1, int D2, int D3>
+__global__ void __launch_bounds__(kJT) k_jac_psi(const LinDims d, const int* __restrict__ dst,
+                                                 const float* __restrict__ jphi, const float* __restrict__ w2,
+                                                 const float* __restrict__ w1, const float* __restrict__ w0,
+                                                 const uint8_t* __restrict__ mpsi, int hpsi,
+                                                 float* __restrict__ out) {
+  __shared__ __align__(16) float s2[D3 * D2];
+  __shared__ __align__(16) float s1[D2 * D1];
+  __shared__ __align__(16) float s0[D1 * D0];
+  for (int t = threadIdx.x; t < D3 * D2; t += kJT) s2[t] = w2[t];
+  for (int t = threadIdx.x; t < D2 * D1; t += kJT) s1[t] = w1[t];
+  for (int t = threadIdx.x; t < D1 * D0; t += kJT) s0[t] = w0[t];
+  __syncthreads();
+  const int n_p = d.n_p, Rv = d.Re * n_p;
+  for (int r = blockIdx.x * kJT + threadIdx.x; r < Rv; r += gridDim.x * kJT) {
+    const int re = r / n_p, ro = r - re * n_p;
+    const int p = re / d.nE;
+    const int e = d.e0 + (re - p * d.nE);
+    const int rn = p * d.nN + (__ldg(dst + e) - d.lo);
+    const float* js = jphi + ((int64_t)rn * n_p + ro) * d.nin + d.nx;
+    float v[D3];
+#pragma unroll
+    for (int m = 0; m < D3; ++m) v[m] = __ldg(js + m);
+    const uint8_t* mp = mpsi + (int64_t)re * hpsi;
+    float h2[D2];
+    chain_layer<D3, D2, true>(v, h2, s2, mp + D1);  // mask of hidden layer 1
+    float h1[D1];
+    chain_layer<D2, D1, true>(h2, h1, s1, mp);       // mask of hidden layer 0
+    float o[D0];
+    chain_layer<D1, D0, false>(h1, o, s0, nullptr);
+    float* dp = out + (int64_t)r * D0;
+#pragma unroll
+    for (int c = 0; c < D0; c += 2) *reinterpret_cast<float2*>(dp + c) = make_float2(o[c], o[c + 1]);
+  }
+}
+
+// Fused forward chains (fp64): every layer of psi (6-32-32-16) over
+// (point, edge) rows and of phi (28-64-64-3) over (point, node) rows in ONE
+// launch each, one row per thread.  The last hidden layer is produced in
+// chunks of 16 units and folded straight into the output layer, so neither
+// hidden vector round-trips through memory; ReLU masks (strict, mlp.py:143)
+// are written as bytes in the layout the Jacobian chains read.  Same fp64
+// formulas as k_layer (summation order within a dot product differs).
+template <int K, int CH>
+__device__ __forceinline__ void fwd_chunk(const double (&v)[K], const double* Ws, int N, int c0,
+                                          const double* bs, double (&a)[CH]) {
+#pragma unroll
+  for (int u = 0; u < CH; ++u) a[u] = bs[c0 + u];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+#pragma unroll
+    for (int u = 0; u < CH; u += 2) {
+      const double2 w = *reinterpret_cast<const double2*>(Ws + k * N + c0 + u);
+      a[u] = fma(v[k], w.x, a[u]);
+      a[u + 1] = fma(v[k], w.y, a[u + 1]);
+    }
+  }
+}
+
+template <int CH>
+__device__ __forceinline__ void relu_mask16(double (&a)[CH], uint8_t* mdst) {
+  static_assert(CH == 16, "mask chunks are 16 bytes");
+  uint32_t mw[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int u = 0; u < CH; ++u) {
+    const bool m = a[u] > 0.0;
+    if (!m) a[u] = 0.0;
+    mw[u >> 2] |= (m ? 1u : 0u) << (8 * (u & 3));
+  }
+  *reinterpret_cast<uint4*>(mdst) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+}
+
+// rows of in (R, D0) -> hidden D1 (mask) -> hidden D2 (mask) -> out (R, D3)
+template <int D0, int D1, int D2, int D3>
+__global__ void __launch_bounds__(kJT) k_fwd_chain(int R, const double* __restrict__ in, int ldi,
+                                                   const double* __restrict__ w0, const double* __restrict__ b0,
+                                                   const double* __restrict__ w1, const double* __restrict__ b1,
+                                                   const double* __restrict__ w2, const double* __restrict__ b2,
+                                                   uint8_t* __restrict__ mask, int hmask, double* __restrict__ out,
+                                                   int ldo) {
+  extern __shared__ __align__(16) double fs[];
+  double* s0 = fs;                 // D0 x D1
+  double* s1 = s0 + D0 * D1;       // D1 x D2
+  double* s2 = s1 + D1 * D2;       // D2 x D3
+  double* sb0 = s2 + D2 * D3;      // D1
+  double* sb1 = sb0 + D1;          // D2
+  double* sb2 = sb1 + D2;          // D3
+  for (int t = threadIdx.x; t < D0 * D1; t += kJT) s0[t] = w0[t];
+  for (int t = threadIdx.x; t < D1 * D2; t += kJT) s1[t] = w1[t];
+  for (int t = threadIdx.x; t < D2 * D3; t += kJT) s2[t] = w2[t];
+  for (int t = threadIdx.x; t < D1; t += kJT) sb0[t] = b0[t];
+  for (int t = threadIdx.x; t < D2; t += kJT) sb1[t] = b1[t];
+  for (int t = threadIdx.x; t < D3; t += kJT) sb2[t] = b2[t];
+  __syncthreads();
+  for (int r = blockIdx.x * kJT + threadIdx.x; r < R; r += gridDim.x * kJT) {
+    uint8_t* mr = mask + (int64_t)r * hmask;
+    double h[D1];
+    {
+      double x[D0];
+      const double* xr = in + (int64_t)r * ldi;
+#pragma unroll
+      for (int k = 0; k < D0; ++k) x[k] = __ldg(xr + k);
+#pragma unroll
+      for (int c0 = 0; c0 < D1; c0 += 16) {
+        double a[16];
+        fwd_chunk<D0, 16>(x, s0, D1, c0, sb0, a);
+        relu_mask16<16>(a, mr + c0);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) h[c0 + u] = a[u];
+      }
+    }
+    double o[D3];
+#pragma unroll
+    for (int j = 0; j < D3; ++j) o[j] = sb2[j];
+#pragma unroll
+    for (int c0 = 0; c0 < D2; c0 += 16) {
+      double a[16];
+      fwd_chunk<D1, 16>(h, s1, D2, c0, sb1, a);
+      relu_mask16<16>(a, mr + D1 + c0);
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+#pragma unroll
+        for (int j = 0; j < D3; ++j) o[j] = fma(a[u], s2[(c0 + u) * D3 + j], o[j]);
+    }
+    double* orow = out + (int64_t)r * ldo;
+#pragma unroll
+    for (int j = 0; j < D3; ++j) orow[j] = o[j];
+  }
+}
+
+template <int D0, int D1, int D2, int D3>
+size_t fwd_chain_smem() {
+  return sizeof(double) * (size_t)(D0 * D1 + D1 * D2 + D2 * D3 + D1 + D2 + D3);
+}
+
+inline unsigned chain_grid(int64_t rows, int sms) {
+  return (unsigned)std::min<int64_t>((rows + kJT - 1) / kJT, (int64_t)sms * 16);
+}
+
 inline unsigned grid_for(int64_t n) { return (unsigned)((n + 255) / 256); }
 inline int pld(int w) { return w | 1; }
 inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -364,7 +595,24 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   // psi forward over every (point, owned edge)
   const double* msg = nullptr;
   int ldmsg = 0;
-  if (d.Re > 0) {
+  // the reference architecture (psi 6-32-32-16, phi 28-64-64-3) runs its
+  // forward passes and Jacobian chains as fused per-row kernels; mode 3 keeps
+  // one launch per layer
+  const bool fused = phi.L == 3 && psi.L == 3 && n_p <= 4 && phi.dims[0] == 28 && phi.dims[1] == 64 &&
+                     phi.dims[2] == 64 && phi.dims[3] == n_p && psi.dims[0] == 6 && psi.dims[1] == 32 &&
+                     psi.dims[2] == 32 && psi.dims[3] == 16 && d.n_m == 16 && nx == 6 && d.nin == 28 &&
+                     hphi == 128 && hpsi == 64 && n_p == 3 && ctx->lin_mode != 3;
+  if (d.Re > 0 && fused) {
+    k_lin_edges<<<grid_for(d.Re * nx), 256, 0, st>>>(d, ctx->d_dst, ctx->d_src, X, ctx->d_norm, ef);
+    GM_LAUNCH_CHECK(ctx, "k_lin_edges");
+    const size_t sm = fwd_chain_smem<6, 32, 32, 16>();
+    k_fwd_chain<6, 32, 32, 16><<<chain_grid(d.Re, ctx->sm_count), kJT, sm, st>>>(
+        d.Re, ef, nx, psi.wt64[0], psi.b64[0], psi.wt64[1], psi.b64[1], psi.wt64[2], psi.b64[2], mpsi, hpsi, ha,
+        pld(16));
+    GM_LAUNCH_CHECK(ctx, "k_fwd_chain");
+    msg = ha;
+    ldmsg = pld(16);
+  } else if (d.Re > 0) {
     k_lin_edges<<<grid_for(d.Re * nx), 256, 0, st>>>(d, ctx->d_dst, ctx->d_src, X, ctx->d_norm, ef);
     GM_LAUNCH_CHECK(ctx, "k_lin_edges");
     const double* cur = ef;
@@ -392,7 +640,17 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   double* pbuf[2] = {(msg == ha) ? hb : ha, (msg == ha) ? ha : hb};
   const double* cur = z;
   int ldc = d.nin;
-  for (int l = 0; l < phi.L; ++l) {
+  if (fused) {
+    const size_t sm = fwd_chain_smem<28, 64, 64, 3>();
+    GM_CUDA(ctx, cudaFuncSetAttribute(k_fwd_chain<28, 64, 64, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_fwd_chain<28, 64, 64, 3><<<chain_grid(d.Rn, ctx->sm_count), kJT, sm, st>>>(
+        d.Rn, z, d.nin, phi.wt64[0], phi.b64[0], phi.wt64[1], phi.b64[1], phi.wt64[2], phi.b64[2], mphi, hphi,
+        pbuf[0], pld(3));
+    GM_LAUNCH_CHECK(ctx, "k_fwd_chain");
+    cur = pbuf[0];
+    ldc = pld(3);
+  }
+  for (int l = 0; l < (fused ? 0 : phi.L); ++l) {
     double* outp = pbuf[l & 1];
     const int N = phi.dims[l + 1];
     const bool relu = l < phi.L - 1;
@@ -411,7 +669,11 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   if (phi.L == 1) {
     return gm_fail(ctx, GM_ERR_CONFIG, "single-layer phi is handled by the fused kernel");
   }
-  {
+  if (fused) {
+    k_jac_phi<28, 64, 64><<<chain_grid(Rj, ctx->sm_count), kJT, 0, st>>>((int)Rj, n_p, phi.w32[2], phi.w32[1],
+                                                                         phi.w32[0], mphi, hphi, jphi);
+    GM_LAUNCH_CHECK(ctx, "k_jac_phi");
+  } else {
     const int L = phi.L, wl = phi.dims[L - 1];
     k_lin_seed_phi<<<grid_for(Rj * wl), 256, 0, st>>>(d, phi.w32[L - 1], wl, mphi, hphi, mask_off(phi, L - 2), qa,
                                                       pld(wl));
@@ -431,7 +693,13 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   }
   // psi VJP seeded with J_m[dst], n_p rows per edge
   const int64_t Rv = d.Re * n_p;
-  if (d.Re > 0) {
+  if (d.Re > 0 && fused) {
+    k_jac_psi<6, 32, 32, 16><<<chain_grid(Rv, ctx->sm_count), kJT, 0, st>>>(d, ctx->d_dst, jphi, psi.w32[2],
+                                                                           psi.w32[1], psi.w32[0], mpsi, hpsi, Pe);
+    GM_LAUNCH_CHECK(ctx, "k_jac_psi");
+    k_lin_nbr<<<grid_for(Rv * nx), 256, 0, st>>>(d, (float)ctx->dt, ctx->d_norm, Pe, (int)ctx->E, a_nbr);
+    GM_LAUNCH_CHECK(ctx, "k_lin_nbr");
+  } else if (d.Re > 0) {
     k_lin_seed_psi<<<grid_for(Rv * d.n_m), 256, 0, st>>>(d, ctx->d_dst, jphi, qa, pld(d.n_m));
     GM_LAUNCH_CHECK(ctx, "k_lin_seed_psi");
     const float* qc = qa;

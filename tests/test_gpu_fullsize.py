@@ -27,7 +27,7 @@ def cfg3():
                 gx=gx, qp=qp, sol=sol, n0=n0)
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 def test_cfg3_stages(cfg3, mode):
     """mode 1: fused per-tile linearisation, 2: layer-wise GEMM chain."""
     import paper_2602_17601_b200 as pkg
