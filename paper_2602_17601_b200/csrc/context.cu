@@ -85,7 +85,10 @@ int gm_create(gm_ctx** out, int device) {
     c->smem_optin = (size_t)optin;
   }
   // benchmark/profiling overrides of the kernel-variant switches
-  if (const char* v = getenv("GM_CONDENSE_MODE")) c->cond_mode = atoi(v) == 1 ? 1 : 0;
+  if (const char* v = getenv("GM_CONDENSE_MODE")) {
+    const int m = atoi(v);
+    c->cond_mode = (m >= 0 && m <= 2) ? m : 0;
+  }
   if (const char* v = getenv("GM_LINEARIZE_MODE")) {
     const int m = atoi(v);
     c->lin_mode = (m >= 0 && m <= 3) ? m : 0;

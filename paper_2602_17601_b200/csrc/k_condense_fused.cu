@@ -82,6 +82,11 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
                "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
 // ---------------------------------------------------------------------------
 template <int NX, int NU>
 __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a) {
-  extern __shared__ __align__(1024) unsigned char smraw[];
+  extern __shared__ __align__(16) unsigned char smraw[];
   const int N = a.N, ld = a.ld, SC = a.sc, M = a.M;
   const int n0 = N * NU, XC = N * NU;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5;
@@ -451,6 +456,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     }
   };
 
+  // stage operands of item j: 16-byte cp.async for every contiguous segment
+  // (a_self, a_nbr, b, c of the chunk; Q and x_ref per node), 4-byte for the
+  // edge sources
   auto prefetch = [&](int j) {
     const int n = j / nsub, s0 = nb + (j % nsub) * SC;
     const int sc = min(SC, ne - s0), k = n + 1;
@@ -458,24 +466,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     const int64_t pstage = bi * N + n;
     const int eb = nptr[s0 - nb], ee = nptr[s0 - nb + sc];
     const int nE = ee - eb;
-    const float* gas = a.a_self + (pstage * M + s0) * NX * NX;
-    for (int t = tid; t < sc * NX * NX; t += nt) cp_async4(S.as + t, gas + t);
+    constexpr int A4 = NX * NX / 4, C2 = NX / 2;  // 16-byte units per node / edge
+    static_assert((NX * NX) % 4 == 0 && NX % 2 == 0, "16-byte staging");
+    const float4* gas = (const float4*)(a.a_self + (pstage * M + s0) * NX * NX);
+    for (int t = tid; t < sc * A4; t += nt) cp_async16((float4*)S.as + t, gas + t);
     if (nE > 0) {
-      const float* gan = a.a_nbr + (pstage * a.E + eb) * NX * NX;
-      for (int t = tid; t < nE * NX * NX; t += nt) cp_async4(S.an + t, gan + t);
+      const float4* gan = (const float4*)(a.a_nbr + (pstage * a.E + eb) * NX * NX);
+      for (int t = tid; t < nE * A4; t += nt) cp_async16((float4*)S.an + t, gan + t);
       for (int t = tid; t < nE; t += nt) cp_async4(S.src + t, a.src + eb + t);
     }
-    const float* gb = a.b + (pstage * M + s0) * NX * NU;
-    for (int t = tid; t < sc * NX * NU; t += nt) cp_async4(S.bb + t, gb + t);
-    const double* gc = a.c + (pstage * M + s0) * NX;
-    for (int t = tid; t < sc * NX; t += nt) cp_async8(S.cc + t, gc + t);
-    for (int t = tid; t < sc * NX * NX; t += nt) {
-      const int li = t / (NX * NX), e = t - li * NX * NX;
-      cp_async8(S.qd + t, a.q + bi * a.q_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX * NX + e);
+    if constexpr ((NX * NU) % 4 == 0) {
+      const float4* gb = (const float4*)(a.b + (pstage * M + s0) * NX * NU);
+      for (int t = tid; t < sc * (NX * NU / 4); t += nt) cp_async16((float4*)S.bb + t, gb + t);
+    } else {
+      const float* gb = a.b + (pstage * M + s0) * NX * NU;
+      for (int t = tid; t < sc * NX * NU; t += nt) cp_async4(S.bb + t, gb + t);
     }
-    for (int t = tid; t < sc * NX; t += nt) {
-      const int li = t / NX, e = t - li * NX;
-      cp_async8(S.xd + t, a.xref + bi * a.xref_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX + e);
+    const double2* gc = (const double2*)(a.c + (pstage * M + s0) * NX);
+    for (int t = tid; t < sc * C2; t += nt) cp_async16((double2*)S.cc + t, gc + t);
+    constexpr int Q2 = NX * NX / 2;
+    for (int t = tid; t < sc * Q2; t += nt) {
+      const int li = t / Q2, e = t - li * Q2;
+      const double2* gq = (const double2*)(a.q + bi * a.q_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX * NX);
+      cp_async16((double2*)S.qd + t, gq + e);
+    }
+    for (int t = tid; t < sc * C2; t += nt) {
+      const int li = t / C2, e = t - li * C2;
+      const double2* gx = (const double2*)(a.xref + bi * a.xref_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX);
+      cp_async16((double2*)S.xd + t, gx + e);
     }
     cp_async_commit();
   };
@@ -553,17 +571,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
         for (int u = 0; u < 5; ++u) {
           const int ss = s + u;
           if (ss <= deg) {
-            // block rows as 8-byte shared loads (broadcast within the warp)
-            const float2* A2 =
-                (const float2*)(ss == 0 ? S.as + li * NX * NX : S.an + (el0 + ss - 1) * NX * NX);
+            // block as 16-byte shared loads (broadcast within the warp),
+            // consumed two rows at a time to bound register pressure
+            const float4* A4 =
+                (const float4*)(ss == 0 ? S.as + li * NX * NX : S.an + (el0 + ss - 1) * NX * NX);
+            if constexpr ((2 * NX) % 4 == 0) {
 #pragma unroll
-            for (int r = 0; r < NX; ++r)
+              for (int r = 0; r < NX; r += 2) {
+                float ab[2 * NX];
 #pragma unroll
-              for (int qq = 0; qq < NX; qq += 2) {
-                const float2 v = A2[(r * NX + qq) / 2];
-                r6[r] = fmaf(v.x, w[u][qq], r6[r]);
-                r6[r] = fmaf(v.y, w[u][qq + 1], r6[r]);
+                for (int e = 0; e < 2 * NX / 4; ++e) {
+                  const float4 v = A4[(r * NX) / 4 + e];
+                  ab[4 * e] = v.x;
+                  ab[4 * e + 1] = v.y;
+                  ab[4 * e + 2] = v.z;
+                  ab[4 * e + 3] = v.w;
+                }
+#pragma unroll
+                for (int qq = 0; qq < NX; ++qq) {
+                  r6[r] = fmaf(ab[qq], w[u][qq], r6[r]);
+                  r6[r + 1] = fmaf(ab[NX + qq], w[u][qq], r6[r + 1]);
+                }
               }
+            } else {
+              const float* Af = (const float*)A4;
+#pragma unroll
+              for (int r = 0; r < NX; ++r)
+#pragma unroll
+                for (int qq = 0; qq < NX; ++qq) r6[r] = fmaf(Af[r * NX + qq], w[u][qq], r6[r]);
+            }
           }
         }
       }
@@ -652,15 +688,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
       const int li = t / lk, col = t - li * lk;
       float gcol[NX], o[NX];
       umma::getn<NX>(g_hi, g_lo, col, li * NX, sbo, gcol);
-      const float* Qn = Qs + li * NX * NX;
+      const float4* Qn4 = (const float4*)(Qs + li * NX * NX);
 #pragma unroll
-      for (int r = 0; r < NX; ++r) {
-        float s = 0.f;
-        if (li < sc) {
+      for (int r = 0; r < NX; ++r) o[r] = 0.f;
+      if (li < sc) {
 #pragma unroll
-          for (int qq = 0; qq < NX; ++qq) s = fmaf(Qn[r * NX + qq], gcol[qq], s);
+        for (int e = 0; e < NX * NX / 4; ++e) {
+          const float4 q4 = Qn4[e];
+          const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int idx = 4 * e + u, r = idx / NX, qq = idx % NX;
+            o[r] = fmaf(qv[u], gcol[qq], o[r]);
+          }
         }
-        o[r] = s;
       }
       umma::putn_split<NX>(q_hi, q_lo, col, li * NX, sbo, o);
     }
@@ -927,7 +968,7 @@ extern "C" {
 
 int gm_set_condense_mode(gm_ctx* ctx, int mode) {
   if (!ctx) return GM_ERR_CONFIG;
-  if (mode < 0 || mode > 1) return gm_fail(ctx, GM_ERR_CONFIG, "condense mode must be 0 or 1");
+  if (mode < 0 || mode > 2) return gm_fail(ctx, GM_ERR_CONFIG, "condense mode must be 0, 1 or 2");
   ctx->cond_mode = mode;
   return GM_OK;
 }
@@ -966,7 +1007,7 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   };
   while (SC > 1 && smem_of(SC) > kFusedSmemBudget) SC >>= 1;
   const size_t sm = smem_of(SC);
-  if (!kern || !whole || npairs > 256 || sm > kFusedSmemBudget) {
+  if (!kern || !whole || npairs > 256 || sm > kFusedSmemBudget || ctx->cond_mode == 2) {
     // shapes outside the fused kernel's instantiations: the two-kernel path
     rc = gm_condense_gammas(ctx, B, N, a_self, a_nbr, b, c, x0, gamma, ld, stream);
     if (rc) return rc;
