@@ -31,6 +31,7 @@
 // once to fp32, as K-REC), fp32 partial sums, fp64 reduction.
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cmath>
 
 #include "common.cuh"
@@ -993,20 +994,51 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   FusedKernel tck = (n0 <= 128 && ctx->cond_mode != 1) ? pick_tc_kernel(nx, nu) : nullptr;
   FusedKernel kern = tck ? tck : pick_kernel(nx, nu);
   const bool whole = ctx->node_lo == 0 && gm_node_hi(ctx) == ctx->M;
-  // node partition: one CTA per SM, all co-resident (the stage waits need it)
-  const int64_t M = ctx->M;
-  const int64_t slots = ctx->sm_count;
-  int64_t per = M;
-  if (B < slots) {
-    const int64_t want = std::max<int64_t>(1, slots / B);
-    per = (M + want - 1) / want;
+  // node partition: cps CTAs per SM, all co-resident (the stage waits need
+  // it).  k_condense_tc: threads x SC (nodes per item) x CTAs per SM,
+  // default 512 x 8 x 1; GM_TC_CFG="threads,sc,cps" overrides (the
+  // occupancy query decides how many CTAs per SM are really co-resident)
+  int tc_threads = kTcThreads, tc_sc = 8, cps = 1;
+  if (tck) {
+    if (const char* v = getenv("GM_TC_CFG")) {
+      int t0 = 0, s0 = 0, c0 = 0;
+      if (sscanf(v, "%d,%d,%d", &t0, &s0, &c0) == 3 && t0 >= 128 && t0 <= kTcThreads && t0 % 128 == 0 &&
+          s0 >= 2 && s0 <= 16 && c0 >= 1 && c0 <= 4) {
+        tc_threads = t0;
+        tc_sc = s0;
+        cps = c0;
+      }
+    }
   }
-  int SC = tck ? 8 : 16;
-  auto smem_of = [&](int sc_) {
-    return tck ? tc_smem(sc_, nx, nu, dslot, n0, per) : fused_smem(sc_, nx, nu, ld, dslot, n0, per);
-  };
-  while (SC > 1 && smem_of(SC) > kFusedSmemBudget) SC >>= 1;
-  const size_t sm = smem_of(SC);
+  const int64_t M = ctx->M;
+  const int threads = tck ? tc_threads : 256;
+  int64_t per = M;
+  int SC = 16;
+  size_t sm = 0;
+  int occ = 0;
+  // partition for `cps` co-resident CTAs per SM; if the occupancy query
+  // grants fewer, repartition for what it grants (nptr, and so the shared
+  // memory size, depends on the partition)
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const int64_t slots = (int64_t)ctx->sm_count * cps;
+    per = M;
+    if (B < slots) {
+      const int64_t want = std::max<int64_t>(1, slots / B);
+      per = (M + want - 1) / want;
+    }
+    SC = tck ? tc_sc : 16;
+    auto smem_of = [&](int sc_) {
+      return tck ? tc_smem(sc_, nx, nu, dslot, n0, per) : fused_smem(sc_, nx, nu, ld, dslot, n0, per);
+    };
+    while (SC > 1 && smem_of(SC) > kFusedSmemBudget) SC >>= 1;
+    sm = smem_of(SC);
+    if (!kern || !whole || npairs > 256 || sm > kFusedSmemBudget || ctx->cond_mode == 2) break;
+    GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, sm));
+    if (occ < 1) return gm_fail(ctx, GM_ERR_CONFIG, "fused condensing kernel does not fit an SM");
+    if (occ >= cps) break;
+    cps = occ;
+  }
   if (!kern || !whole || npairs > 256 || sm > kFusedSmemBudget || ctx->cond_mode == 2) {
     // shapes outside the fused kernel's instantiations: the two-kernel path
     rc = gm_condense_gammas(ctx, B, N, a_self, a_nbr, b, c, x0, gamma, ld, stream);
@@ -1015,16 +1047,14 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
                             u_ref, uref_stride, H, g, 0, stream);
   }
   cudaStream_t st = (cudaStream_t)stream;
-  GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  int occ = 0;
-  const int threads = tck ? kTcThreads : 256;
-  GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, sm));
-  if (occ < 1) return gm_fail(ctx, GM_ERR_CONFIG, "fused condensing kernel does not fit an SM");
   const int splits = (int)((M + per - 1) / per);
   rc = ensure_deps(ctx, per, splits);
   if (rc) return rc;
   const int64_t grid = (int64_t)B * splits;
-  if (splits > 1 && grid > slots * occ) return gm_fail(ctx, GM_ERR_CONFIG, "fused condensing grid not co-resident");
+  if (splits > 1 && grid > (int64_t)ctx->sm_count * occ)
+    return gm_fail(ctx, GM_ERR_CONFIG,
+                   "fused condensing grid not co-resident (" + std::to_string(grid) + " CTAs, " +
+                       std::to_string(occ) + " per SM, " + std::to_string(sm) + " B shared)");
   rc = ensure_flags(ctx, grid + 1);
   if (rc) return rc;
   const int groups = std::min(splits, 16);
@@ -1064,6 +1094,15 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   {
     const char* v = getenv("GM_TC_PREFETCH");
     a.reg_prefetch = v ? atoi(v) : 1;
+  }
+  if (getenv("GM_TC_DEBUG")) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    fprintf(stderr,
+            "k_condense: tc=%d threads=%d SC=%d per=%lld splits=%d grid=%lld occ=%d smem=%zu regs=%d static=%zu "
+            "maxthr=%d\n",
+            tck != nullptr, threads, SC, (long long)per, splits, (long long)grid, occ, sm, fa.numRegs,
+            fa.sharedSizeBytes, fa.maxThreadsPerBlock);
   }
   kern<<<(unsigned)grid, (unsigned)threads, sm, st>>>(a);
   GM_LAUNCH_CHECK(ctx, "k_condense_fused");
