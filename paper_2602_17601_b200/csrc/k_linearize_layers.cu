@@ -389,12 +389,16 @@ __global__ void __launch_bounds__(kJT) k_jac_phi(int Rj, int n_p, const float* _
 
 // psi VJP rows (point, edge, ro): seed J_m of the destination node (from
 // jphi), then layers L-1 .. 0 (L = 3): out (Re*n_p, D0) = Pe
+// The epilogue also writes the row's part of the a_nbr block of its (point,
+// edge): Jv_nbr = -Jpsi / s_x, position rows dt * Jv_nbr, velocity rows
+// Jv_nbr (gnn.py:266, :282-285).
 template <int D0, int D1, int D2, int D3>
 __global__ void __launch_bounds__(kJT) k_jac_psi(const LinDims d, const int* __restrict__ dst,
                                                  const float* __restrict__ jphi, const float* __restrict__ w2,
                                                  const float* __restrict__ w1, const float* __restrict__ w0,
                                                  const uint8_t* __restrict__ mpsi, int hpsi,
-                                                 float* __restrict__ out) {
+                                                 float* __restrict__ out, float dtf, const double* __restrict__ norm,
+                                                 int E, float* __restrict__ a_nbr) {
   __shared__ __align__(16) float s2[D3 * D2];
   __shared__ __align__(16) float s1[D2 * D1];
   __shared__ __align__(16) float s0[D1 * D0];
@@ -422,6 +426,14 @@ __global__ void __launch_bounds__(kJT) k_jac_psi(const LinDims d, const int* __r
     float* dp = out + (int64_t)r * D0;
 #pragma unroll
     for (int c = 0; c < D0; c += 2) *reinterpret_cast<float2*>(dp + c) = make_float2(o[c], o[c + 1]);
+    float* blk = a_nbr + ((int64_t)p * E + e) * D0 * D0;
+#pragma unroll
+    for (int c = 0; c < D0; c += 2) {
+      const float j0 = -o[c] * (float)(1.0 / __ldg(norm + D0 + c));
+      const float j1 = -o[c + 1] * (float)(1.0 / __ldg(norm + D0 + c + 1));
+      *reinterpret_cast<float2*>(blk + ro * D0 + c) = make_float2(dtf * j0, dtf * j1);
+      *reinterpret_cast<float2*>(blk + (n_p + ro) * D0 + c) = make_float2(j0, j1);
+    }
   }
 }
 
@@ -461,9 +473,59 @@ __device__ __forceinline__ void relu_mask16(double (&a)[CH], uint8_t* mdst) {
   *reinterpret_cast<uint4*>(mdst) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
 }
 
-// rows of in (R, D0) -> hidden D1 (mask) -> hidden D2 (mask) -> out (R, D3)
-template <int D0, int D1, int D2, int D3>
-__global__ void __launch_bounds__(kJT) k_fwd_chain(int R, const double* __restrict__ in, int ldi,
+// input rows of the fused forward chains, formed on the fly (no HBM round
+// trip): psi rows are the edge features e = (x_dst - x_src) / s_x of one
+// (point, edge) (gnn.py:133-135), phi rows are z = [(x - mu_x)/s_x,
+// sum of the node's in-edge messages (edge order), (u - mu_u)/s_u]
+// (gnn.py:136-149)
+struct EdgeRows {
+  LinDims d;
+  const int* dst;
+  const int* src;
+  const double* X;
+  const double* norm;
+  __device__ __forceinline__ void operator()(int re, double* x) const {
+    const int p = re / d.nE;
+    const int e = d.e0 + (re - p * d.nE);
+    const double* Xp = X + (int64_t)p * d.M * d.nx;
+    const double* xd = Xp + (int64_t)__ldg(dst + e) * d.nx;
+    const double* xs = Xp + (int64_t)__ldg(src + e) * d.nx;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) x[k] = (__ldg(xd + k) - __ldg(xs + k)) / __ldg(norm + d.nx + k);
+  }
+};
+struct NodeRows {
+  LinDims d;
+  const int* ptr;
+  const double* X;
+  const double* U;
+  const double* norm;
+  const double* msg;
+  int ldmsg;
+  __device__ __forceinline__ void operator()(int rn, double* x) const {
+    const int p = rn / d.nN;
+    const int i = d.lo + (rn - p * d.nN);
+    const int nx = 6, nm = 16, nu = 6;
+    const double* xi = X + ((int64_t)p * d.M + i) * nx;
+#pragma unroll
+    for (int k = 0; k < nx; ++k) x[k] = (__ldg(xi + k) - __ldg(norm + k)) / __ldg(norm + nx + k);
+#pragma unroll
+    for (int m = 0; m < nm; ++m) x[nx + m] = 0.0;
+    for (int e = __ldg(ptr + i); e < __ldg(ptr + i + 1); ++e) {
+      const double* mr = msg + ((int64_t)p * d.nE + (e - d.e0)) * ldmsg;
+#pragma unroll
+      for (int m = 0; m < nm; ++m) x[nx + m] += mr[m];
+    }
+    const double* up = U + (int64_t)p * nu;
+#pragma unroll
+    for (int j = 0; j < nu; ++j)
+      x[nx + nm + j] = (__ldg(up + j) - __ldg(norm + 2 * nx + j)) / __ldg(norm + 2 * nx + nu + j);
+  }
+};
+
+// rows (R, D0) -> hidden D1 (mask) -> hidden D2 (mask) -> out (R, D3)
+template <int D0, int D1, int D2, int D3, typename Rows>
+__global__ void __launch_bounds__(kJT) k_fwd_chain(int R, const Rows rows,
                                                    const double* __restrict__ w0, const double* __restrict__ b0,
                                                    const double* __restrict__ w1, const double* __restrict__ b1,
                                                    const double* __restrict__ w2, const double* __restrict__ b2,
@@ -488,9 +550,7 @@ __global__ void __launch_bounds__(kJT) k_fwd_chain(int R, const double* __restri
     double h[D1];
     {
       double x[D0];
-      const double* xr = in + (int64_t)r * ldi;
-#pragma unroll
-      for (int k = 0; k < D0; ++k) x[k] = __ldg(xr + k);
+      rows(r, x);
 #pragma unroll
       for (int c0 = 0; c0 < D1; c0 += 16) {
         double a[16];
@@ -603,11 +663,10 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
                      psi.dims[2] == 32 && psi.dims[3] == 16 && d.n_m == 16 && nx == 6 && d.nin == 28 &&
                      hphi == 128 && hpsi == 64 && n_p == 3 && ctx->lin_mode != 3;
   if (d.Re > 0 && fused) {
-    k_lin_edges<<<grid_for(d.Re * nx), 256, 0, st>>>(d, ctx->d_dst, ctx->d_src, X, ctx->d_norm, ef);
-    GM_LAUNCH_CHECK(ctx, "k_lin_edges");
     const size_t sm = fwd_chain_smem<6, 32, 32, 16>();
+    const EdgeRows rows{d, ctx->d_dst, ctx->d_src, X, ctx->d_norm};
     k_fwd_chain<6, 32, 32, 16><<<chain_grid(d.Re, ctx->sm_count), kJT, sm, st>>>(
-        d.Re, ef, nx, psi.wt64[0], psi.b64[0], psi.wt64[1], psi.b64[1], psi.wt64[2], psi.b64[2], mpsi, hpsi, ha,
+        d.Re, rows, psi.wt64[0], psi.b64[0], psi.wt64[1], psi.b64[1], psi.wt64[2], psi.b64[2], mpsi, hpsi, ha,
         pld(16));
     GM_LAUNCH_CHECK(ctx, "k_fwd_chain");
     msg = ha;
@@ -633,8 +692,10 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
     msg = cur;
     ldmsg = ldc;
   }
-  k_lin_z<<<grid_for(d.Rn * d.nin), 256, 0, st>>>(d, ctx->d_ptr, X, U, ctx->d_norm, msg, ldmsg, z);
-  GM_LAUNCH_CHECK(ctx, "k_lin_z");
+  if (!fused) {
+    k_lin_z<<<grid_for(d.Rn * d.nin), 256, 0, st>>>(d, ctx->d_ptr, X, U, ctx->d_norm, msg, ldmsg, z);
+    GM_LAUNCH_CHECK(ctx, "k_lin_z");
+  }
   // phi forward over every (point, owned node); the output buffer must not
   // alias msg (ha/hb hold it), so phi starts in the buffer psi did not end in
   double* pbuf[2] = {(msg == ha) ? hb : ha, (msg == ha) ? ha : hb};
@@ -642,9 +703,11 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   int ldc = d.nin;
   if (fused) {
     const size_t sm = fwd_chain_smem<28, 64, 64, 3>();
-    GM_CUDA(ctx, cudaFuncSetAttribute(k_fwd_chain<28, 64, 64, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    GM_CUDA(ctx, cudaFuncSetAttribute(k_fwd_chain<28, 64, 64, 3, NodeRows>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const NodeRows rows{d, ctx->d_ptr, X, U, ctx->d_norm, msg, ldmsg};
     k_fwd_chain<28, 64, 64, 3><<<chain_grid(d.Rn, ctx->sm_count), kJT, sm, st>>>(
-        d.Rn, z, d.nin, phi.wt64[0], phi.b64[0], phi.wt64[1], phi.b64[1], phi.wt64[2], phi.b64[2], mphi, hphi,
+        d.Rn, rows, phi.wt64[0], phi.b64[0], phi.wt64[1], phi.b64[1], phi.wt64[2], phi.b64[2], mphi, hphi,
         pbuf[0], pld(3));
     GM_LAUNCH_CHECK(ctx, "k_fwd_chain");
     cur = pbuf[0];
@@ -694,11 +757,10 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   // psi VJP seeded with J_m[dst], n_p rows per edge
   const int64_t Rv = d.Re * n_p;
   if (d.Re > 0 && fused) {
-    k_jac_psi<6, 32, 32, 16><<<chain_grid(Rv, ctx->sm_count), kJT, 0, st>>>(d, ctx->d_dst, jphi, psi.w32[2],
-                                                                           psi.w32[1], psi.w32[0], mpsi, hpsi, Pe);
+    k_jac_psi<6, 32, 32, 16><<<chain_grid(Rv, ctx->sm_count), kJT, 0, st>>>(
+        d, ctx->d_dst, jphi, psi.w32[2], psi.w32[1], psi.w32[0], mpsi, hpsi, Pe, (float)ctx->dt, ctx->d_norm,
+        (int)ctx->E, a_nbr);
     GM_LAUNCH_CHECK(ctx, "k_jac_psi");
-    k_lin_nbr<<<grid_for(Rv * nx), 256, 0, st>>>(d, (float)ctx->dt, ctx->d_norm, Pe, (int)ctx->E, a_nbr);
-    GM_LAUNCH_CHECK(ctx, "k_lin_nbr");
   } else if (d.Re > 0) {
     k_lin_seed_psi<<<grid_for(Rv * d.n_m), 256, 0, st>>>(d, ctx->d_dst, jphi, qa, pld(d.n_m));
     GM_LAUNCH_CHECK(ctx, "k_lin_seed_psi");
