@@ -162,8 +162,10 @@ int gm_condense_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, cons
  * shapes outside the fused kernel's instantiations run the two-kernel path.
  * One launch per context at a time (per-context stage counters). */
 /* Node reduction of H in gm_condense_fused: 0 = auto (tcgen05 3xTF32
- * tensor-core kernel when N*nu <= 128, else the SIMT kernel), 1 = always the
- * SIMT (register-tiled fp32 FMA) kernel.  For tests and benchmarks. */
+ * tensor-core kernel when N*nu <= 128 and B*M >= 512, else the SIMT kernel),
+ * 1 = always the SIMT (register-tiled fp32 FMA) kernel, 2 = the two-kernel
+ * path (per-stage K-REC launches + K-HG), 3 = always the tcgen05 kernel.
+ * For tests and benchmarks. */
 int gm_set_condense_mode(gm_ctx* ctx, int mode);
 int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_nbr,
                       const float* b, const double* c, const double* x0, float* gamma, int ld,

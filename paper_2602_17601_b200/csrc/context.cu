@@ -87,7 +87,7 @@ int gm_create(gm_ctx** out, int device) {
   // benchmark/profiling overrides of the kernel-variant switches
   if (const char* v = getenv("GM_CONDENSE_MODE")) {
     const int m = atoi(v);
-    c->cond_mode = (m >= 0 && m <= 2) ? m : 0;
+    c->cond_mode = (m >= 0 && m <= 3) ? m : 0;
   }
   if (const char* v = getenv("GM_LINEARIZE_MODE")) {
     const int m = atoi(v);

@@ -969,7 +969,7 @@ extern "C" {
 
 int gm_set_condense_mode(gm_ctx* ctx, int mode) {
   if (!ctx) return GM_ERR_CONFIG;
-  if (mode < 0 || mode > 2) return gm_fail(ctx, GM_ERR_CONFIG, "condense mode must be 0, 1 or 2");
+  if (mode < 0 || mode > 3) return gm_fail(ctx, GM_ERR_CONFIG, "condense mode must be 0, 1, 2 or 3");
   ctx->cond_mode = mode;
   return GM_OK;
 }
@@ -991,7 +991,11 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   const int dslot = (int)ctx->dmax + 1;
   // tensor-core H (k_condense_tc) whenever the H accumulator fits one
   // 128 x 128 TMEM tile; gm_set_condense_mode forces either kernel
-  FusedKernel tck = (n0 <= 128 && ctx->cond_mode != 1) ? pick_tc_kernel(nx, nu) : nullptr;
+  // (auto mode: from ~512 node rows up; below that, the per-item MMA issue /
+  // commit / wait round trip costs more than the SIMT products it replaces:
+  // cfg2, M = 100, 0.18 ms tc vs 0.10 ms SIMT; cfg3, M = 1000, equal)
+  const bool tc_ok = ctx->cond_mode == 0 ? (int64_t)B * ctx->M >= 512 : ctx->cond_mode == 3;
+  FusedKernel tck = (n0 <= 128 && tc_ok) ? pick_tc_kernel(nx, nu) : nullptr;
   FusedKernel kern = tck ? tck : pick_kernel(nx, nu);
   const bool whole = ctx->node_lo == 0 && gm_node_hi(ctx) == ctx->M;
   // node partition: cps CTAs per SM, all co-resident (the stage waits need

@@ -297,11 +297,13 @@ class PartitionedMpc:
                  None, self.planned_states.data_ptr(), self.planned_inputs.data_ptr(),
                  self.next_states.data_ptr(), self.next_inputs.data_ptr(),
                  self.u_applied.data_ptr(), self.summary.data_ptr(), sp)
-        # owned node rows of the plan are valid here: replicate, then shift
-        gather_owned(self.part, self.planned_states)
-        ps = self.planned_states.transpose(0, 1)  # (N+1, M, nx)
-        self.next_states[:N].copy_(ps[1:])
-        self.next_states[N].copy_(ps[N])
+        if self.part.world > 1:
+            # owned node rows of the plan are valid here: replicate, then shift
+            # (at world size 1 gm_mpc_finish already wrote the whole shift)
+            gather_owned(self.part, self.planned_states)
+            ps = self.planned_states.transpose(0, 1)  # (N+1, M, nx)
+            self.next_states[:N].copy_(ps[1:])
+            self.next_states[N].copy_(ps[N])
         ctx.call("gm_set_node_range", 0, eng.M)
         summ = self.summary.cpu().numpy()
         return summ[:nu].copy(), int(summ[nu]), int(summ[nu + 1])
