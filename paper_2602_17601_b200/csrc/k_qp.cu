@@ -177,7 +177,11 @@ __device__ __forceinline__ bool chol_factor(Qs& S) {
   if (S.T == 0) return true;  // every variable eliminated
   if (threadIdx.x == 0) *S.flag = 0;
   __syncthreads();
+#ifdef QP_CHOL_SYNC
   const bool ok = qpchol::factor<kQpThreads>(S.K, S.T, S.dinv, S.flag);
+#else
+  const bool ok = qpchol::factor_la<kQpThreads>(S.K, S.T, S.dinv, S.flag);
+#endif
   __syncthreads();
   return ok;
 }

@@ -291,6 +291,189 @@ __device__ __noinline__ bool factor(double* Kt, int T, double* dinv, int* flag, 
   return !*flag;
 }
 
+// One tile of a rank-8 trailing update: C_IJ -= P_I P_J' (P_X = tile (X, k)),
+// transposed-C DMMA form of trailing_update.  One warp.
+__device__ __forceinline__ void update_tile(double* Kt, int k, int I, int J, int lane) {
+  QP_SMEM(Kt);
+  const int i = lane >> 2, p = lane & 3;
+  const double* PI = Kt + ti(I, k) * kTS;
+  const double* PJ = Kt + ti(J, k) * kTS;
+  const int off = ti(I, J) * kTS + eo(2 * p, i);
+  double2 cv = *reinterpret_cast<const double2*>(Kt + off);
+  dmma884(cv.x, cv.y, -PJ[eo(i, p)], PI[eo(i, p)]);
+  dmma884(cv.x, cv.y, -PJ[eo(i, p + 4)], PI[eo(i, p + 4)]);
+  *reinterpret_cast<double2*>(Kt + off) = cv;
+}
+
+// trailing_update without the look-ahead tiles (k+1, k+1), (k+2, k+1) and
+// (k+2, k+2): columns J = k+1 and k+2 start at row k+3
+template <int NU, int NB = 6>
+__device__ __forceinline__ void trailing_update_la(double* Kt, int T, int k, int uw, int lane) {
+  QP_SMEM(Kt);
+  const int i = lane >> 2, p = lane & 3;
+  auto col_start = [&](int J) { return J <= k + 2 ? k + 3 : J; };
+  int J = k + 1, I = col_start(k + 1);
+  auto adv = [&](int s) {
+    I += s;
+    while (J < T && I >= T) {
+      const int o = I - T;
+      ++J;
+      I = col_start(J) + o;
+    }
+  };
+  adv(uw);
+  while (J < T) {
+    int off[NB], cnt = 0;
+    double a0[NB], a1[NB], b0[NB], b1[NB];
+    double2 cv[NB];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      if (J < T) {
+        const double* PI = Kt + ti(I, k) * kTS;
+        const double* PJ = Kt + ti(J, k) * kTS;
+        off[u] = ti(I, J) * kTS + eo(2 * p, i);
+        a0[u] = -PJ[eo(i, p)];
+        a1[u] = -PJ[eo(i, p + 4)];
+        b0[u] = PI[eo(i, p)];
+        b1[u] = PI[eo(i, p + 4)];
+        cv[u] = *reinterpret_cast<const double2*>(Kt + off[u]);
+        ++cnt;
+        adv(NU);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u)
+      if (u < cnt) dmma884(cv[u].x, cv[u].y, a0[u], b0[u]);
+#pragma unroll
+    for (int u = 0; u < NB; ++u)
+      if (u < cnt) dmma884(cv[u].x, cv[u].y, a1[u], b1[u]);
+#pragma unroll
+    for (int u = 0; u < NB; ++u)
+      if (u < cnt) *reinterpret_cast<double2*>(Kt + off[u]) = cv[u];
+  }
+}
+
+// Factorisation with a software-pipelined look-ahead (replaces the
+// CTA-wide barrier that ended every step of `factor`).  Warp 0 owns the
+// pivot chain: at step k it forms panel (k+1, k), E = A(k+1,k+1) - P P' and
+// factors it (lane 0).  It needs only tiles (k+1, k) and (k+1, k+1) from the
+// previous trailing update, so update warp 0 refreshes those two first and
+// signals warp 0 on named barrier 2; the rest of the trailing update overlaps
+// warp 0's next pivot step.  Named barriers:
+//   1  (NT):  warp 0 arrives after panel (k+1, k); the others sync after
+//             their panel rows -> every column-k panel is final
+//   2  (64):  update warp 0 arrives after tiles (k+2, k+1), (k+2, k+2);
+//             warp 0 syncs before step k+1
+//   3/4 (NT, by step parity): warp 0 arrives after factoring tile (k+1, k+1);
+//             the others sync at the start of step k+1 (all of them have
+//             finished trailing(k) by then, and L_{k+1,k+1} is published).
+//             Parity alternation keeps warp 0, which may run one step ahead,
+//             from arriving twice on an open barrier phase.
+// No early exit inside the loop (the phases must stay balanced): a failed
+// pivot raises *flag and the factorisation runs to the end.
+template <int NT>
+__device__ __noinline__ bool factor_la(double* Kt, int T, double* dinv, int* flag) {
+  QP_SMEM(Kt);
+  QP_SMEM(dinv);
+  QP_SMEM(flag);
+  constexpr int NW = NT / 32;
+  constexpr int NU = NW - NW / 4;  // update warps (off warp 0's sub-partition)
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    double a[8][8], d[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c <= r; ++c) a[r][c] = Kt[eo(r, c)];
+    if (!factor8(a, d)) *flag = 1;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      dinv[r] = d[r];
+#pragma unroll
+      for (int c = 0; c <= r; ++c) Kt[eo(r, c)] = a[r][c];
+    }
+  }
+  __syncthreads();
+  if (wid == 0) {
+    for (int k = 0; k + 1 < T; ++k) {
+      if (k >= 1) bar_sync(2, 64);  // tiles (k+1, k), (k+1, k+1) refreshed
+      const double* Lkk = Kt + ti(k, k) * kTS;
+      const double* dk = dinv + 8 * k;
+      double* P = Kt + ti(k + 1, k) * kTS;
+      if (lane < 8) {
+        double w[8];
+        load_row(P, lane, w);
+        panel_row(Lkk, dk, w);
+        store_row(P, lane, w);
+      }
+      __syncwarp();
+      __threadfence_block();
+      bar_arrive(1, NT);
+      double* Dt = Kt + ti(k + 1, k + 1) * kTS;
+      {
+        int ra, ca, rb, cb;
+        pair36(lane, ra, ca);
+        pair36(32 + (lane & 3), rb, cb);
+        double x0 = Dt[eo(ra, ca)], x1 = 0.0, y0 = Dt[eo(rb, cb)], y1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          x0 = fma(-P[eo(ra, q)], P[eo(ca, q)], x0);
+          x1 = fma(-P[eo(ra, q + 1)], P[eo(ca, q + 1)], x1);
+          y0 = fma(-P[eo(rb, q)], P[eo(cb, q)], y0);
+          y1 = fma(-P[eo(rb, q + 1)], P[eo(cb, q + 1)], y1);
+        }
+        Dt[eo(ra, ca)] = x0 + x1;
+        if (lane < 4) Dt[eo(rb, cb)] = y0 + y1;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        double a[8][8], d[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c <= r; ++c) a[r][c] = Dt[eo(r, c)];
+        if (!factor8(a, d)) *flag = 1;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          dinv[8 * (k + 1) + r] = d[r];
+#pragma unroll
+          for (int c = 0; c <= r; ++c) Dt[eo(r, c)] = a[r][c];
+        }
+      }
+      __syncwarp();
+      __threadfence_block();
+      bar_arrive(3 + (k & 1), NT);
+    }
+  } else {
+    const int uw = ((wid & 3) != 0) ? wid - 1 - (wid >> 2) : -1;  // trailing-update rank
+    for (int k = 0; k + 1 < T; ++k) {
+      if (k >= 1) bar_sync(3 + ((k - 1) & 1), NT);  // L_kk published, trailing(k-1) done
+      const double* Lkk = Kt + ti(k, k) * kTS;
+      const double* dk = dinv + 8 * k;
+      const int rows = 8 * (T - k - 2);
+      for (int t = tid - 32; t < rows; t += NT - 32) {
+        double* P = Kt + ti(k + 2 + (t >> 3), k) * kTS;
+        double w[8];
+        load_row(P, t & 7, w);
+        panel_row(Lkk, dk, w);
+        store_row(P, t & 7, w);
+      }
+      bar_sync(1, NT);
+      if (uw == 0 && k + 2 < T) {  // the look-ahead tiles of warp 0's next step
+        update_tile(Kt, k, k + 2, k + 1, lane);
+        update_tile(Kt, k, k + 2, k + 2, lane);
+        __syncwarp();
+        __threadfence_block();
+        bar_arrive(2, 64);
+      }
+      if (uw >= 0) trailing_update_la<NU>(Kt, T, k, uw, lane);
+    }
+    if (T >= 2) bar_sync(3 + ((T - 2) & 1), NT);  // consume warp 0's last arrival
+  }
+  __syncthreads();
+  return !*flag;
+}
+
 // ---------------------------------------------------------------------------
 // Full inverse X = L^{-1} in place, and triangular solves as mat-vecs
 // ---------------------------------------------------------------------------
