@@ -202,8 +202,9 @@ int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, const double*
                 int32_t* iterations, double* resid, void* stream);
 
 /* Diagnostics: per-phase cycle accounting of K-QP (block 0).  gm_qp_profile(1)
- * enables and zeroes the counters; gm_qp_phase_cycles copies 16 counters
- * (synchronous). */
+ * enables and zeroes the counters (2: counters 13-15 account the Cholesky
+ * pivot chain instead of the Schur build); gm_qp_phase_cycles copies 16
+ * counters (synchronous). */
 int gm_qp_profile(int on);
 int gm_qp_phase_cycles(unsigned long long* out);
 /* Diagnostics: factor a dense SPD matrix A (n x n, row-major, device) with

@@ -104,6 +104,9 @@ struct QpArgs {
 // gm_qp_phase_cycles(); enabled by gm_qp_profile(1)
 __device__ unsigned long long g_qp_prof[16];
 __device__ int g_qp_prof_on;
+// 1: the K-QP profile's slots 13-15 account the Cholesky pivot chain instead
+// of the Schur-build phases (diagnostics)
+__device__ int g_qp_chol_split;
 
 struct Qs {  // per-CTA views
   // n: variables; nf: variables kept in the factorised (reduced) system.
@@ -180,7 +183,8 @@ __device__ __forceinline__ bool chol_factor(Qs& S) {
 #ifdef QP_CHOL_SYNC
   const bool ok = qpchol::factor<kQpThreads>(S.K, S.T, S.dinv, S.flag);
 #else
-  const bool ok = qpchol::factor_la<kQpThreads>(S.K, S.T, S.dinv, S.flag);
+  const bool ok = qpchol::factor_la<kQpThreads>(S.K, S.T, S.dinv, S.flag,
+                                                (S.prof && g_qp_chol_split) ? g_qp_prof + 13 : nullptr);
 #endif
   __syncthreads();
   return ok;
@@ -359,7 +363,7 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
     S.wg[gi] = wr;
   }
   __syncthreads();
-  qmark(const_cast<Qs&>(S), 13);
+  if (!g_qp_chol_split) qmark(const_cast<Qs&>(S), 13);
   // lower 8x8 tiles of 2H + Cg' diag(wg) Cg on the fp64 tensor cores: the
   // C fragment (row i, cols 2p, 2p+1) starts from 2H, ng/4 DMMAs add the
   // general rows (A[i][g] = wg_g Cg[g][row], B[g][j] = Cg[g][col]), padding
@@ -412,7 +416,7 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
     }
   }
   __syncthreads();
-  qmark(const_cast<Qs&>(S), 14);
+  if (!g_qp_chol_split) qmark(const_cast<Qs&>(S), 14);
   // diagonal (holds only the general-row term so far): (2H + reg) +
   // bincount(single rows) first, then the general-row term, as the
   // reference orders it
@@ -429,7 +433,7 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
   }
 
   const bool all_ok = __syncthreads_and(ok ? 1 : 0) != 0;
-  qmark(const_cast<Qs&>(S), 15);
+  if (!g_qp_chol_split) qmark(const_cast<Qs&>(S), 15);
   return all_ok;
 }
 
@@ -1018,7 +1022,10 @@ extern "C" int gm_chol_check(gm_ctx* ctx, int n, const double* A, const double* 
 }
 
 extern "C" int gm_qp_profile(int on) {
+  const int split = on == 2 ? 1 : 0;
+  on = on != 0 ? 1 : 0;
   cudaMemcpyToSymbol(g_qp_prof_on, &on, sizeof(int));
+  cudaMemcpyToSymbol(g_qp_chol_split, &split, sizeof(int));
   unsigned long long z[16] = {0};
   cudaMemcpyToSymbol(g_qp_prof, z, sizeof(z));
   return GM_OK;

@@ -372,7 +372,8 @@ __device__ __forceinline__ void trailing_update_la(double* Kt, int T, int k, int
 // No early exit inside the loop (the phases must stay balanced): a failed
 // pivot raises *flag and the factorisation runs to the end.
 template <int NT>
-__device__ __noinline__ bool factor_la(double* Kt, int T, double* dinv, int* flag) {
+__device__ __noinline__ bool factor_la(double* Kt, int T, double* dinv, int* flag,
+                                       unsigned long long* prof = nullptr) {
   QP_SMEM(Kt);
   QP_SMEM(dinv);
   QP_SMEM(flag);
@@ -395,8 +396,14 @@ __device__ __noinline__ bool factor_la(double* Kt, int T, double* dinv, int* fla
   }
   __syncthreads();
   if (wid == 0) {
+    // optional pivot-chain accounting (prof[0..2]: look-ahead wait, panel + E,
+    // 8x8 factor + publish), lane 0 of block 0
+    const bool pf = prof && lane == 0;
+    long long c0 = 0, c1 = 0, c2 = 0;
     for (int k = 0; k + 1 < T; ++k) {
+      if (pf) c0 = clock64();
       if (k >= 1) bar_sync(2, 64);  // tiles (k+1, k), (k+1, k+1) refreshed
+      if (pf) c1 = clock64();
       const double* Lkk = Kt + ti(k, k) * kTS;
       const double* dk = dinv + 8 * k;
       double* P = Kt + ti(k + 1, k) * kTS;
@@ -426,6 +433,7 @@ __device__ __noinline__ bool factor_la(double* Kt, int T, double* dinv, int* fla
         if (lane < 4) Dt[eo(rb, cb)] = y0 + y1;
       }
       __syncwarp();
+      if (pf) c2 = clock64();
       if (lane == 0) {
         double a[8][8], d[8];
 #pragma unroll
@@ -443,6 +451,12 @@ __device__ __noinline__ bool factor_la(double* Kt, int T, double* dinv, int* fla
       __syncwarp();
       __threadfence_block();
       bar_arrive(3 + (k & 1), NT);
+      if (pf) {
+        const long long c3 = clock64();
+        atomicAdd(prof + 0, (unsigned long long)(c1 - c0));
+        atomicAdd(prof + 1, (unsigned long long)(c2 - c1));
+        atomicAdd(prof + 2, (unsigned long long)(c3 - c2));
+      }
     }
   } else {
     const int uw = ((wid & 3) != 0) ? wid - 1 - (wid >> 2) : -1;  // trailing-update rank

@@ -9,7 +9,9 @@ from tests.golden_io import load
 names = ["setup", "residuals", "tests+best", "w+build_k", "cholesky", "inv_diag", "rp/mu+aff_rhs",
          "kkt(excl solve)", "steps/sigma", "update", "pre-solve", "chol_solve",
          "[res] h_apply", "[res] ct+c_apply+loops / [bk] w,kee,wg", "[bk] tiles", "[bk] diag"]
-for case in sys.argv[1:] or ["cfg1_chain10"]:
+if "--chol" in sys.argv:  # slots 13-15: the Cholesky pivot chain (warp 0)
+    names[13:16] = ["[chol] look-ahead wait", "[chol] panel + E", "[chol] factor8 + publish"]
+for case in [a for a in sys.argv[1:] if not a.startswith("--")] or ["cfg1_chain10"]:
     if case == "cfg3":
         from paper_2602_17601_b200 import workloads
         from oracle import ref_port as O
@@ -22,7 +24,7 @@ for case in sys.argv[1:] or ["cfg1_chain10"]:
     p = pkg.QpProblem(H, g, C, d)
     s = pkg.solve_qp(p)
     L = _runtime.lib()
-    L.gm_qp_profile(1)
+    L.gm_qp_profile(2 if "--chol" in sys.argv else 1)
     s = pkg.solve_qp(p)
     out = np.zeros(16, dtype=np.uint64)
     L.gm_qp_phase_cycles(out.ctypes.data)
