@@ -112,6 +112,11 @@ void gm_count_launch();
     if (_e != cudaSuccess) return gm_cuda_check((ctx), _e, what); \
   } while (0)
 
+// K-HG on tcgen05 (k_condense_fused.cu); 1 = shape not handled
+int gm_tc_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const double* q, int64_t q_stride,
+               const double* x_ref, int64_t xref_stride, const double* r, int64_t r_stride, const double* u_ref,
+               int64_t uref_stride, double* H, double* g, int partial, void* stream);
+
 static inline int64_t gm_node_hi(const gm_ctx* c) { return c->node_hi < 0 ? c->M : c->node_hi; }
 
 static inline int gm_ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

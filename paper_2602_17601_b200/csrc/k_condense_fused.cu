@@ -45,6 +45,8 @@ constexpr int kTcThreads = 512;  // k_condense_tc block size (16 warps: latency 
 struct FusedArgs {
   int M, E, N, ld, per, splits, sc, npairs, dslot;
   int reg_prefetch;  // k_condense_tc: register prefetch of the next item's neighbour rows
+  int rec;           // k_condense_tc: 1 = run the recursion (K-COND), 0 = read Gamma (K-HG on tcgen05)
+  int lo, hi;        // node range of the launch (k_condense_tc)
   const int* ptr;
   const int* src;
   const int* dep_ptr;
@@ -405,14 +407,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5;
   const int64_t bi = blockIdx.x / a.splits;
   const int split = (int)(blockIdx.x % a.splits);
-  const int nb = split * a.per, ne = min(M, nb + a.per);
+  const int nb = a.lo + split * a.per, ne = min(a.hi, nb + a.per);
+  const bool rec = a.rec != 0;
   const int nn = ne - nb;
   const int nsub = (nn + SC - 1) / SC;
   const int emax = SC * (a.dslot - 1) > 0 ? SC * (a.dslot - 1) : 1;
   const int KC = ((SC * NX + 7) / 8) * 8;               // K rows per item, MMA-padded
   const uint32_t sbo = (uint32_t)(KC / 4) * 128u;        // 8-row group stride
   const size_t bufb = 16 * (size_t)sbo;                  // 128-row operand buffer
-  int* flags = a.flags + bi * a.splits;
+  int* flags = rec ? a.flags + bi * a.splits : nullptr;
   const int64_t stage_stride = (int64_t)NX * ld;
   const int64_t node_stride = (int64_t)(N + 1) * stage_stride;
   float* Wb = a.W + bi * (int64_t)M * node_stride;
@@ -469,6 +472,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     const int nE = ee - eb;
     constexpr int A4 = NX * NX / 4, C2 = NX / 2;  // 16-byte units per node / edge
     static_assert((NX * NX) % 4 == 0 && NX % 2 == 0, "16-byte staging");
+    if (rec) {
     const float4* gas = (const float4*)(a.a_self + (pstage * M + s0) * NX * NX);
     for (int t = tid; t < sc * A4; t += nt) cp_async16((float4*)S.as + t, gas + t);
     if (nE > 0) {
@@ -485,6 +489,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     }
     const double2* gc = (const double2*)(a.c + (pstage * M + s0) * NX);
     for (int t = tid; t < sc * C2; t += nt) cp_async16((double2*)S.cc + t, gc + t);
+    }
     constexpr int Q2 = NX * NX / 2;
     for (int t = tid; t < sc * Q2; t += nt) {
       const int li = t / Q2, e = t - li * Q2;
@@ -502,14 +507,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
   if (items > 0) prefetch(0);
 
   // stage 0: Gamma_u = 0, Gamma_x = x0 (condensing.py:205-206)
-  for (int t = tid; t < nn * NX * ld; t += nt) {
+  for (int t = tid; rec && t < nn * NX * ld; t += nt) {
     const int li = t / (NX * ld), rem = t - li * NX * ld, r = rem / ld, col = rem - r * ld;
     Wb[(int64_t)(nb + li) * node_stride + rem] =
         (col == XC) ? (float)a.x0[(bi * M + nb + li) * NX + r] : 0.f;
   }
-  const int d0 = a.dep_ptr[split], d1 = a.dep_ptr[split + 1];
+  const int d0 = rec ? a.dep_ptr[split] : 0, d1 = rec ? a.dep_ptr[split + 1] : 0;
   __syncthreads();
-  if (tid == 0) {
+  if (rec && tid == 0) {
     __threadfence();
     st_release(&flags[split], 1);
   }
@@ -520,7 +525,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     const int k = n + 1;
     const int live = n * NU;
     const Stage<NX, NU> S = stage_at<NX, NU>(smraw + (j & 1) * sbytes, SC, emax);
-    if (sub == 0) {
+    if (rec && sub == 0) {
       for (int d = d0 + tid; d < d1; d += nt) {
         const int* f = &flags[a.dep[d]];
         while (ld_acquire(f) < k) __nanosleep(32);
@@ -539,14 +544,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     // 224): one (node, column) per thread over the closed neighbourhood, all
     // neighbour loads of a node issued before the FMAs (one L2/DRAM round
     // trip for deg < 5); work spread over live columns only
-    const int lw = live + 1;
+    // without the recursion (K-HG on tcgen05) the rows are read from Gamma:
+    // the live columns, the B block and Gamma_x of stage k
+    const int nlive = rec ? live : live + NU;
+    const int lw = nlive + 1;
     for (int t = tid, it = 0; t < sc * lw; t += nt, ++it) {
       const int li = t / lw, cc = t - li * lw;
-      const int col = cc < live ? cc : XC;
+      const int col = cc < nlive ? cc : XC;
       const int i = s0 + li;
       float r6[NX];
 #pragma unroll
       for (int r = 0; r < NX; ++r) r6[r] = 0.f;
+      if (!rec) {
+        const float* Wr = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + col;
+#pragma unroll
+        for (int r = 0; r < NX; ++r) r6[r] = __ldcg(Wr + (int64_t)r * ld);
+      } else {
       const int el0 = nptr[i - nb] - ebase, deg = nptr[i - nb + 1] - nptr[i - nb];
       const float* Wn = Wb + (int64_t)n * stage_stride + col;
       for (int s = 0; s <= deg; s += 5) {
@@ -611,6 +624,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
       float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + col;
 #pragma unroll
       for (int r = 0; r < NX; ++r) Wo[(int64_t)r * ld] = r6[r];
+      }
       operands_free();
       if (col < n0) {
         umma::putn_split<NX>(g_hi, g_lo, col, li * NX, sbo, r6);
@@ -622,7 +636,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     // (R2) block n <- B_n, every other column zero (global rows only: the
     // operand buffers hold zeros beyond the live columns already)
     operands_free();
-    const int nz = ld - lw;
+    const int nz = rec ? ld - lw : 0;
     for (int t = tid; t < sc * nz; t += nt) {
       const int li = t / nz, cc = t - li * nz;
       int col = live + cc;
@@ -655,7 +669,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
       }
     }
     __syncthreads();
-    if (sub == nsub - 1 && tid == 0) {  // all of this CTA's stage-k rows are out
+    if (rec && sub == nsub - 1 && tid == 0) {  // all of this CTA's stage-k rows are out
       __threadfence();
       st_release(&flags[split], k + 1);
     }
@@ -663,7 +677,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     // rows (same stage: its dependencies are already met), in flight while
     // this item's B operand is built and its MMAs run
     pre_ok = false;
-    if (a.reg_prefetch && sub + 1 < nsub) {
+    if (rec && a.reg_prefetch && sub + 1 < nsub) {
       const int s0n = s0 + SC, scn = min(SC, ne - s0n);
       if (tid < scn * lw) {
         const int li = tid / lw, cc = tid - li * lw;
@@ -776,7 +790,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
   umma::fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_free<256>(tmem);
-  if (tid == 0) {
+  if (rec && tid == 0) {
     __threadfence();
     int* done = a.flags + (int64_t)gridDim.x;
     if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
@@ -965,6 +979,87 @@ int ensure_flags(gm_ctx* ctx, int64_t n) {
 
 }  // namespace
 
+// K-HG on the tensor cores: the cost part of condense_ocp over the node range
+// [node_lo, node_hi) from a Gamma produced elsewhere (per-stage K-REC, the
+// partitioned driver): k_condense_tc without the recursion, split-K over node
+// ranges (no co-residency requirement), then the shared fixed-order fp64
+// reduction.  partial != 0 leaves out R-bar / r_lin (added by one rank only).
+// Returns 1 (not handled) when the shape has no tensor-core instantiation.
+int gm_tc_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const double* q, int64_t q_stride,
+               const double* x_ref, int64_t xref_stride, const double* r, int64_t r_stride, const double* u_ref,
+               int64_t uref_stride, double* H, double* g, int partial, void* stream) {
+  const int nx = ctx->nx, nu = ctx->n_u, n0 = N * nu;
+  const int npairs = N * (N + 1) / 2;
+  const int64_t lo = ctx->node_lo, hi = gm_node_hi(ctx), nodes = hi - lo;
+  FusedKernel kern = (n0 <= 128) ? pick_tc_kernel(nx, nu) : nullptr;
+  if (!kern || nodes < 1 || (ld % 4) != 0 || ((uintptr_t)gamma & 15) || ((uintptr_t)q & 15) ||
+      ((uintptr_t)x_ref & 15) || (q_stride % 2) != 0 || (xref_stride % 2) != 0)
+    return 1;
+  const int SC = 8;
+  const int64_t want = std::max<int64_t>(1, (2 * (int64_t)ctx->sm_count + B - 1) / B);
+  const int64_t per = std::max<int64_t>(SC, (nodes + want - 1) / want);
+  const int splits = (int)((nodes + per - 1) / per);
+  const int dslot = (int)ctx->dmax + 1;
+  const size_t sm = tc_smem(SC, nx, nu, dslot, n0, per);
+  if (sm > kFusedSmemBudget) return 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const int64_t grid = (int64_t)B * splits;
+  const int groups = std::min(splits, 16);
+  const int PU = npairs * nu * nu;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t pH = sizeof(float) * (size_t)grid * PU, pg = sizeof(double) * (size_t)grid * n0;
+  const size_t tH = sizeof(double) * (size_t)B * groups * PU, tg = sizeof(double) * (size_t)B * groups * n0;
+  char* scr = (char*)gm_scratch(ctx, up(pH) + up(pg) + up(tH) + tg + 256);
+  if (!scr) return gm_fail(ctx, GM_ERR_CUDA, "scratch allocation failed");
+  FusedArgs a{};
+  a.M = (int)ctx->M;
+  a.E = (int)ctx->E;
+  a.N = N;
+  a.ld = ld;
+  a.per = (int)per;
+  a.splits = splits;
+  a.sc = SC;
+  a.npairs = npairs;
+  a.dslot = dslot;
+  a.ptr = ctx->d_ptr;
+  a.src = ctx->d_src;
+  a.W = const_cast<float*>(gamma);
+  a.q = q;
+  a.q_stride = q_stride;
+  a.xref = x_ref;
+  a.xref_stride = xref_stride;
+  a.partH = (float*)scr;
+  a.partg = (double*)(scr + up(pH));
+  a.rec = 0;
+  a.lo = (int)lo;
+  a.hi = (int)hi;
+  kern<<<(unsigned)grid, (unsigned)kTcThreads, sm, st>>>(a);
+  GM_LAUNCH_CHECK(ctx, "k_condense_tc(cost)");
+  PairReduceArgs ra{};
+  ra.nu = nu;
+  ra.n0 = n0;
+  ra.npairs = npairs;
+  ra.splits = splits;
+  ra.groups = groups;
+  ra.partH = a.partH;
+  ra.partg = a.partg;
+  ra.tmpH = (double*)(scr + up(pH) + up(pg));
+  ra.tmpg = (double*)(scr + up(pH) + up(pg) + up(tH));
+  ra.r = partial ? nullptr : r;
+  ra.r_stride = r_stride;
+  ra.uref = u_ref;
+  ra.uref_stride = uref_stride;
+  ra.H = H;
+  ra.g = g;
+  const unsigned eb = (unsigned)gm_ceil_div(std::max(PU, n0), 256);
+  k_pair_reduce1<<<dim3(eb, (unsigned)groups, (unsigned)B), 256, 0, st>>>(ra);
+  GM_LAUNCH_CHECK(ctx, "k_pair_reduce1");
+  k_pair_reduce2<<<dim3(eb, (unsigned)B), 256, 0, st>>>(ra);
+  GM_LAUNCH_CHECK(ctx, "k_pair_reduce2");
+  return GM_OK;
+}
+
 extern "C" {
 
 int gm_set_condense_mode(gm_ctx* ctx, int mode) {
@@ -1095,6 +1190,9 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   a.partH = (float*)scr;
   a.partg = (double*)(scr + up(pH));
   a.flags = ctx->d_flags;
+  a.rec = 1;
+  a.lo = 0;
+  a.hi = (int)M;
   {
     const char* v = getenv("GM_TC_PREFETCH");
     a.reg_prefetch = v ? atoi(v) : 1;

@@ -37,7 +37,7 @@ def _run(topo, N, nx, nu, B, seed, reps=2, graph=False, mode=0):
 
     eng = dev.engine(topo)
     eng.set_dims(nx, nu)
-    eng.ctx.call("gm_set_condense_mode", mode)
+    eng.ctx.call("gm_set_condense_mode", 1)  # the reference: SIMT K-REC + K-HG
     M = topo.node_count
     ld = lib().gm_gamma_ld(N, nu)
     arrs = _problem(topo, N, nx, nu, B, seed)
@@ -54,6 +54,7 @@ def _run(topo, N, nx, nu, B, seed, reps=2, graph=False, mode=0):
     eng.ctx.call("gm_condense_cost", B, N, W1.data_ptr(), ld, q.data_ptr(), 0, xref.data_ptr(),
                  M * (N + 1) * nx, r.data_ptr(), 0, uref.data_ptr(), 0, H1.data_ptr(),
                  g1.data_ptr(), 0, sp)
+    eng.ctx.call("gm_set_condense_mode", mode)
     W2 = eng.zeros((B, M, N + 1, nx, ld), np.float32) + 7.0  # fully overwritten
     H2 = eng.zeros((B, n0, n0), np.float64)
     g2 = eng.zeros((B, n0), np.float64)
@@ -146,3 +147,58 @@ def test_fused_graph_replay(mode):
     topo = mesh_topology(30, 20)
     ref, outs = _run(topo, 10, 6, 6, 1, seed=3, reps=3, graph=True, mode=mode)
     _check(ref, outs, 60, 6, 10, tol=2e-6 if mode == 1 else 1e-5)
+
+
+@pytest.mark.parametrize("graph,N,nx,nu,B,rng_,partial", [
+    ("chain1000", 20, 6, 6, 1, None, 0),
+    ("chain1000", 20, 6, 6, 2, None, 0),
+    ("chain1000", 20, 6, 6, 1, (300, 700), 1),
+    ("chain1000", 20, 6, 6, 1, (0, 517), 0),
+    ("mesh", 12, 6, 3, 1, None, 0),
+    ("mesh", 7, 4, 2, 2, (40, 391), 1),
+])
+def test_cost_tensor_core_matches_simt(graph, N, nx, nu, B, rng_, partial):
+    """K-HG (cost part of condense_ocp, condensing.py:376-389) on tcgen05
+    (k_condense_tc without the recursion, mode 3) against the SIMT K-HG
+    (mode 1) on the same Gamma, over the whole graph and over node ranges
+    as the partitioned driver uses them, with and without R-bar (partial)."""
+    import torch
+
+    from paper_2602_17601_b200 import device as dev
+    from paper_2602_17601_b200._runtime import lib
+    from paper_2602_17601_b200.graph import chain_topology, mesh_topology
+
+    topo = chain_topology(1000) if graph == "chain1000" else mesh_topology(23, 17)
+    eng = dev.engine(topo)
+    eng.set_dims(nx, nu)
+    M = topo.node_count
+    ld = lib().gm_gamma_ld(N, nu)
+    arrs = _problem(topo, N, nx, nu, B, 7)
+    a_self, a_nbr, b, c, x0, q, xref, r, uref = [
+        eng.h2d(x, np.float32 if x.dtype == np.float32 else np.float64) for x in arrs]
+    n0 = N * nu
+    sp = eng.stream_ptr()
+    W = eng.zeros((B, M, N + 1, nx, ld), np.float32)
+    eng.ctx.call("gm_set_condense_mode", 1)
+    eng.ctx.call("gm_condense_gammas", B, N, a_self.data_ptr(), a_nbr.data_ptr() if eng.E else None,
+                 b.data_ptr(), c.data_ptr(), x0.data_ptr(), W.data_ptr(), ld, sp)
+    out = {}
+    try:
+        if rng_ is not None:
+            eng.ctx.call("gm_set_node_range", rng_[0], rng_[1])
+        for mode in (1, 3):
+            eng.ctx.call("gm_set_condense_mode", mode)
+            H = eng.zeros((B, n0, n0), np.float64)
+            g = eng.zeros((B, n0), np.float64)
+            eng.ctx.call("gm_condense_cost", B, N, W.data_ptr(), ld, q.data_ptr(), 0, xref.data_ptr(),
+                         M * (N + 1) * nx, r.data_ptr(), 0, uref.data_ptr(), 0, H.data_ptr(), g.data_ptr(),
+                         partial, sp)
+            torch.cuda.synchronize()
+            out[mode] = (H.cpu().numpy(), g.cpu().numpy())
+    finally:
+        eng.ctx.call("gm_set_node_range", 0, M)
+        eng.ctx.call("gm_set_condense_mode", 0)
+    (Hs, gs), (Ht, gt) = out[1], out[3]
+    assert np.max(np.abs(Ht - Hs)) <= 1e-5 * np.max(np.abs(Hs))
+    assert np.array_equal(Ht, np.swapaxes(Ht, 1, 2))
+    assert np.max(np.abs(gt - gs)) <= 1e-5 * max(1.0, np.max(np.abs(gs)))
