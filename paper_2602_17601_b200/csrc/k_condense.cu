@@ -31,7 +31,7 @@ namespace {
 // K-REC
 // ---------------------------------------------------------------------------
 struct RecArgs {
-  int M, E, N, nx, nu, ld, n, lo, nodes;
+  int M, E, N, nx, nu, ld, n, lo, nodes, B;
   const int* ptr;
   const int* src;
   const float* a_self;
@@ -111,6 +111,102 @@ __global__ void __launch_bounds__(128) k_gamma_stage(const RecArgs a) {
   }
 }
 
+// K-REC, warp form (nx = 6, 16-byte aligned rows): one warp per (instance,
+// node), lane l owns the column chunks 4l + 128 j of all six rows, so every
+// neighbour row is one coalesced 512-byte float4 sweep and each lane keeps
+// 6 x 4 accumulators; the node's 6x6 blocks are staged once per warp in
+// shared memory (no CTA barrier) and read as broadcast vectors.  Chunks with
+// no causal column skip the neighbour loads.  Per-column FMA order is that of
+// k_gamma_stage (neighbour slot, then state index), so Gamma is bitwise
+// identical to it and to the fused K-COND.
+constexpr int kRecWarps = 8;
+__global__ void __launch_bounds__(32 * kRecWarps) k_gamma_stage_w6(const RecArgs a, int dmax) {
+  constexpr int NX = 6;
+  extern __shared__ __align__(16) float rsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t wg = (int64_t)blockIdx.x * kRecWarps + warp;
+  const int nu = a.nu, ld = a.ld, N = a.N, n = a.n;
+  const int64_t bi = wg / a.nodes;
+  if (bi >= a.B) return;
+  const int i = a.lo + (int)(wg - bi * a.nodes);
+  const int64_t gi = bi * a.M + i;
+  const int XC = N * nu;
+  const int64_t stage_stride = (int64_t)NX * ld;
+  const int64_t node_stride = (int64_t)(N + 1) * stage_stride;
+  if (n < 0) {  // stage 0: Gamma_u = 0, Gamma_x = x0 (condensing.py:205-206)
+    float* Wo = a.W + gi * node_stride;
+    for (int c0 = lane * 4; c0 < ld; c0 += 128)
+#pragma unroll
+      for (int r = 0; r < NX; ++r) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float x = (float)a.x0[gi * NX + r];
+        if (c0 == XC) v.x = x;
+        if (c0 + 1 == XC) v.y = x;
+        if (c0 + 2 == XC) v.z = x;
+        if (c0 + 3 == XC) v.w = x;
+        *reinterpret_cast<float4*>(Wo + (int64_t)r * ld + c0) = v;
+      }
+    return;
+  }
+  const int e0 = a.ptr[i], deg = a.ptr[i + 1] - e0;
+  float* As = rsm + warp * ((dmax + 2) * NX * NX);  // (1+deg) A blocks, then B (nx x nu)
+  float* Bs = As + (dmax + 1) * NX * NX;
+  const int64_t pstage = bi * N + n;
+  for (int t = lane; t < (1 + deg) * NX * NX; t += 32) {
+    const int s = t / (NX * NX), q = t - s * NX * NX;
+    As[t] = s == 0 ? a.a_self[(pstage * a.M + i) * NX * NX + q] : a.a_nbr[(pstage * a.E + e0 + s - 1) * NX * NX + q];
+  }
+  for (int t = lane; t < NX * nu; t += 32) Bs[t] = a.b[(pstage * a.M + i) * NX * nu + t];
+  __syncwarp();
+  const int live = n * nu;
+  float* Wo = a.W + gi * node_stride + (int64_t)(n + 1) * stage_stride;
+  for (int c0 = lane * 4; c0 < ld; c0 += 128) {
+    float acc[NX][4];
+#pragma unroll
+    for (int r = 0; r < NX; ++r)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[r][e] = 0.f;
+    if (c0 < live || (XC >= c0 && XC < c0 + 4)) {
+      for (int s = 0; s <= deg; ++s) {
+        const int j = s == 0 ? i : __ldg(a.src + e0 + s - 1);
+        const float* Wj = a.W + (bi * a.M + j) * node_stride + (int64_t)n * stage_stride + c0;
+        float4 w[NX];
+#pragma unroll
+        for (int q = 0; q < NX; ++q) w[q] = __ldcg(reinterpret_cast<const float4*>(Wj + (int64_t)q * ld));
+        const float* A = As + s * NX * NX;
+#pragma unroll
+        for (int q = 0; q < NX; ++q)
+#pragma unroll
+          for (int r = 0; r < NX; ++r) {
+            const float ar = A[r * NX + q];
+            acc[r][0] = fmaf(ar, w[q].x, acc[r][0]);
+            acc[r][1] = fmaf(ar, w[q].y, acc[r][1]);
+            acc[r][2] = fmaf(ar, w[q].z, acc[r][2]);
+            acc[r][3] = fmaf(ar, w[q].w, acc[r][3]);
+          }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NX; ++r) {
+      float o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int col = c0 + e;
+        if (col < live) {
+          o[e] = acc[r][e];
+        } else if (col == XC) {
+          o[e] = acc[r][e] + (float)a.c[pstage * a.M * NX + (int64_t)i * NX + r];
+        } else if (col < live + nu) {
+          o[e] = Bs[r * nu + (col - live)];
+        } else {
+          o[e] = 0.f;
+        }
+      }
+      *reinterpret_cast<float4*>(Wo + (int64_t)r * ld + c0) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 int rec_stage(gm_ctx* ctx, int B, int N, int n, const float* a_self, const float* a_nbr,
               const float* b, const double* c, const double* x0, float* W, int ld,
               cudaStream_t st) {
@@ -132,8 +228,16 @@ int rec_stage(gm_ctx* ctx, int B, int N, int n, const float* a_self, const float
   a.c = c;
   a.x0 = x0;
   a.W = W;
+  a.B = B;
   const int64_t blocks = (int64_t)B * a.nodes;
   if (blocks == 0) return GM_OK;
+  if (a.nx == 6 && ld % 4 == 0 && ((uintptr_t)W & 15) == 0 && ctx->cond_mode != 1) {
+    const int dmax = (int)ctx->dmax;
+    const size_t smw = sizeof(float) * (size_t)kRecWarps * (dmax + 2) * 36;
+    k_gamma_stage_w6<<<(unsigned)((blocks + kRecWarps - 1) / kRecWarps), 32 * kRecWarps, smw, st>>>(a, dmax);
+    GM_LAUNCH_CHECK(ctx, "k_gamma_stage_w6");
+    return GM_OK;
+  }
   const size_t sm = sizeof(float) * ((1 + ctx->dmax) * a.nx * a.nx + a.nx * a.nu + a.nx) +
                     sizeof(int) * (ctx->dmax + 1) + 16;
   if (a.nx <= 2)

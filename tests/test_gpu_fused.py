@@ -115,10 +115,11 @@ def torch_equal(a, b):
     ("chain37", 5, 2, 1, 1),
     ("chain37", 6, 3, 2, 1),   # not instantiated: two-kernel fallback inside the call
 ])
-@pytest.mark.parametrize("mode", [3, 1, 0])
+@pytest.mark.parametrize("mode", [3, 1, 0, 2])
 def test_fused_matches_two_kernel_path(graph, N, nx, nu, B, mode):
     """mode 3: tcgen05 3xTF32 H (k_condense_tc), 1: SIMT fp32 H (k_condense_fused),
-    0: automatic choice.
+    0: automatic choice, 2: two-kernel path (warp-per-node K-REC + tensor-core
+    K-HG) against the SIMT reference (per-node-CTA K-REC + SIMT K-HG).
     Gamma is bitwise identical in both; H agrees with the fp32 SIMT K-HG to
     fp32 round-off (3xTF32 drops the lo*lo term, ~2^-22 relative); on the tcgen05 path
     g is accumulated in fp32 on the tensor core too (fp64 in the SIMT kernel)."""
