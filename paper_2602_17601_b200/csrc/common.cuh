@@ -112,6 +112,10 @@ void gm_count_launch();
     if (_e != cudaSuccess) return gm_cuda_check((ctx), _e, what); \
   } while (0)
 
+// the fused per-row MLP chains of the layer-wise linearisation apply
+// (k_linearize_layers.cu)
+bool gm_lin_chains(const gm_ctx* ctx);
+
 // K-HG on tcgen05 (k_condense_fused.cu); 1 = shape not handled
 int gm_tc_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const double* q, int64_t q_stride,
                const double* x_ref, int64_t xref_stride, const double* r, int64_t r_stride, const double* u_ref,

@@ -443,12 +443,14 @@ int launch_linearize(gm_ctx* ctx, int64_t P, const double* X, const double* U, f
   if (P < 0) return gm_fail(ctx, GM_ERR_CONFIG, "negative point count");
   const int64_t lo = ctx->node_lo, hi = gm_node_hi(ctx);
   if (P == 0 || hi <= lo) return GM_OK;
-  // Jacobians of large problems: layer-wise GEMM chain (k_linearize_layers.cu)
-  // unless phi is a single layer; the fused per-tile kernel below serves
-  // small problems, step_array (no Jacobian) and that corner case
-  // (latency-bound small problems -- cfg3's 20 K node points -- stay on the
-  // fused kernel: ~27 launches of small GEMMs cost more than one fused pass)
-  constexpr int64_t kLayerMinRows = 200000;
+  // Jacobians beyond a few thousand node points: the layer-wise path
+  // (k_linearize_layers.cu; with the fused per-row MLP chains of the
+  // reference architecture it beats the per-tile kernel from ~8 K node points:
+  // M = 600 0.12 vs 0.16 ms, M = 1000 0.21 vs 0.25 ms, M = 1e4 1.0 vs 2.1 ms at
+  // N = 20; the per-layer GEMM form only from ~200 K); the fused per-tile
+  // kernel below serves small problems, step_array (no Jacobian) and a
+  // single-layer phi
+  const int64_t kLayerMinRows = gm_lin_chains(ctx) ? 8000 : 200000;
   const bool big = P * (hi - lo) >= kLayerMinRows;
   if (jac && ctx->phi.L >= 2 && ctx->psi.L >= 1 && (ctx->lin_mode >= 2 || (ctx->lin_mode == 0 && big)))
     return launch_linearize_layers(ctx, P, X, U, a_self, a_nbr, b, c, f_next, stream);

@@ -594,6 +594,16 @@ inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
+// the fused per-row chains apply (reference architecture: psi 6-32-32-16,
+// phi 28-64-64-3, n_p = 3) and are not switched off (linearize mode 3)
+bool gm_lin_chains(const gm_ctx* ctx) {
+  const MlpHost &phi = ctx->phi, &psi = ctx->psi;
+  return phi.L == 3 && psi.L == 3 && ctx->n_p == 3 && phi.dims[0] == 28 && phi.dims[1] == 64 &&
+         phi.dims[2] == 64 && phi.dims[3] == 3 && psi.dims[0] == 6 && psi.dims[1] == 32 && psi.dims[2] == 32 &&
+         psi.dims[3] == 16 && ctx->n_m == 16 && ctx->m_nx == 6 && phi.hidden_sum() == 128 &&
+         psi.hidden_sum() == 64 && ctx->lin_mode != 3;
+}
+
 namespace {
 
 int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float* a_self, float* a_nbr,
@@ -658,10 +668,7 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   // the reference architecture (psi 6-32-32-16, phi 28-64-64-3) runs its
   // forward passes and Jacobian chains as fused per-row kernels; mode 3 keeps
   // one launch per layer
-  const bool fused = phi.L == 3 && psi.L == 3 && n_p <= 4 && phi.dims[0] == 28 && phi.dims[1] == 64 &&
-                     phi.dims[2] == 64 && phi.dims[3] == n_p && psi.dims[0] == 6 && psi.dims[1] == 32 &&
-                     psi.dims[2] == 32 && psi.dims[3] == 16 && d.n_m == 16 && nx == 6 && d.nin == 28 &&
-                     hphi == 128 && hpsi == 64 && n_p == 3 && ctx->lin_mode != 3;
+  const bool fused = gm_lin_chains(ctx);
   if (d.Re > 0 && fused) {
     const size_t sm = fwd_chain_smem<6, 32, 32, 16>();
     const EdgeRows rows{d, ctx->d_dst, ctx->d_src, X, ctx->d_norm};
