@@ -59,7 +59,10 @@ __host__ __device__ inline size_t xregion_doubles(int nf) {
   const size_t T = qpchol::tiles_for(nf);
   return T * qpchol::kTS + 64 * kQpWarps + 24 * T;
 }
-__host__ __device__ inline QpLayout qp_layout(int n, int m, int ng, bool h_smem, bool cg_smem, int nf = -1) {
+// gv_smem = false: the three ng-vectors live in the global workspace (many
+// general rows), so they take no shared memory
+__host__ __device__ inline QpLayout qp_layout(int n, int m, int ng, bool h_smem, bool cg_smem, int nf = -1,
+                                              bool gv_smem = true) {
   QpLayout L{};
   if (nf < 0) nf = n;
   size_t o = 0;
@@ -68,7 +71,7 @@ __host__ __device__ inline QpLayout qp_layout(int n, int m, int ng, bool h_smem,
   L.o_ints = o;  // rcol(m) grow(m) colptr(n+1) colrows(m) cstart(n+1) kidx(n) eidx(n) egi(n) ge(m) elig(n)
   o = qal(o + sizeof(int) * (4 * (size_t)m + 6 * (size_t)n + 2 + 8));
   L.o_gv = o;
-  o = qal(o + sizeof(double) * 3 * (size_t)ng);
+  if (gv_smem) o = qal(o + sizeof(double) * 3 * (size_t)ng);
   L.o_k = o;
   o = qal(o + sizeof(double) * (size_t)qpchol::tile_doubles(nf));
   L.o_x = o;
@@ -658,8 +661,12 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   }
   __syncthreads();
   S.ng = sh_int[0];
+  // the ng-vectors (and with them everything placed after them) go on-chip
+  // only when the base layout with them still fits; else to the workspace
+  const bool gv_smem = qp_layout(n, m, S.ng, false, false).total <= A.smem_bytes;
   {
-    double* gv = (double*)(smem + qp_layout(n, m, S.ng, false, false).o_gv);
+    double* gv = gv_smem ? (double*)(smem + qp_layout(n, m, S.ng, false, false).o_gv)
+                         : gws + packed_size(n) + (int64_t)m * n;
     S.wg = gv;
     S.ga = gv + S.ng;
     S.cf = gv + 2 * S.ng;
@@ -723,9 +730,9 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   S.ne = sh_int[3];
   S.nblk = (S.nf + kTB - 1) / kTB;
   {
-    const bool cg_smem = qp_layout(n, m, S.ng, false, true, S.nf).total <= A.smem_bytes;
-    const bool h_smem = qp_layout(n, m, S.ng, true, cg_smem, S.nf).total <= A.smem_bytes;
-    const QpLayout LY = qp_layout(n, m, S.ng, h_smem, cg_smem, S.nf);
+    const bool cg_smem = qp_layout(n, m, S.ng, false, true, S.nf, gv_smem).total <= A.smem_bytes;
+    const bool h_smem = qp_layout(n, m, S.ng, true, cg_smem, S.nf, gv_smem).total <= A.smem_bytes;
+    const QpLayout LY = qp_layout(n, m, S.ng, h_smem, cg_smem, S.nf, gv_smem);
     S.K = (double*)(smem + LY.o_k);
     S.X = (double*)(smem + LY.o_x);
     S.T = qpchol::tiles_for(S.nf);
@@ -1054,7 +1061,7 @@ extern "C" int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, co
   const QpLayout base = qp_layout(n, m, 0, false, false);
   if (base.total > cap) return gm_fail(ctx, GM_ERR_CONFIG, "QP too large for the on-chip solver");
   const size_t smem_bytes = std::min(cap, qp_layout(n, m, m, true, true).total);
-  const int64_t gws_stride = packed_size(n) + (int64_t)m * n;
+  const int64_t gws_stride = packed_size(n) + (int64_t)m * n + 3 * (int64_t)m;
   double* gws = (double*)gm_scratch(ctx, sizeof(double) * (size_t)gws_stride * B);
   if (!gws) return gm_fail(ctx, GM_ERR_CUDA, "QP workspace allocation failed");
   QpArgs a{};

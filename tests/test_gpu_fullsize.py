@@ -70,3 +70,51 @@ def test_cfg3_mpc_step_u0(cfg3):
     scale = max(1.0, float(np.max(np.abs(ref["u_applied"]))))
     assert float(np.max(np.abs(u.u - ref["u_applied"]))) / scale <= TOL
     assert rel(st1.planned_inputs, ref["planned_inputs"]) <= TOL
+
+
+def test_many_state_constraints_at_scale():
+    """state constraints on many nodes make the QP's general
+    rows dominate (m >> 280).  Chain M=400, N=20, hard rows on every 20th
+    node at every stage (one upper bound on the height z, one lower bound on
+    the lateral position x, the second one active for a few nodes):
+    m = 240 box + 800 general rows, n = 120.  condense_ocp's constraint rows
+    and the mpc_step input against the CPU oracle (condensing.py:263-282,
+    qpsolver.py:112-243); the general rows no longer fit on chip and stream
+    from the QP workspace."""
+    import paper_2602_17601_b200 as pkg
+    from oracle import ref_port as O
+    from paper_2602_17601_b200 import workloads
+    from paper_2602_17601_b200.condensing import OcpSpec, StateConstraint
+
+    M, N = 400, 20
+    topo, model, states, inputs, spec0 = workloads.scaling_problem(M, N, 0.01, 3)
+    rows = []
+    for node in range(0, M, 20):
+        cz = np.zeros((2, 6))
+        cz[0, 2] = 1.0    # z <= z0 + 0.05
+        cz[1, 0] = -1.0   # x >= x0 + (0.002 on a few nodes: active)
+        for k in range(1, N + 1):
+            x0 = states[0][node]
+            d = np.array([x0[2] + 0.05, -(x0[0] + (0.002 if node % 100 == 0 else -0.05))])
+            rows.append(StateConstraint(node, k, cz, d, soft=False))
+    spec = OcpSpec(topo, N, spec0.q, spec0.x_ref, spec0.r, spec0.u_ref, spec0.input_constraints, rows)
+
+    lin = O.linearize_trajectory(model, topo, states, inputs)
+    qref = O.condense_ocp(spec, lin, states[0])
+    linb = pkg.linearize_trajectory(model, topo, states, inputs)
+    qb = pkg.condense_ocp(spec, linb, states[0])
+    assert qb.c.shape == qref.c.shape and qb.c.shape[0] == 240 + 2 * 20 * N
+    assert rel(qb.c, qref.c) <= TOL
+    assert rel(qb.d, qref.d) <= TOL
+
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+    x = pkg.SystemState(states[0])
+    st = pkg.mpc_init(x, cfg, 6)
+    st.lin_states = np.concatenate([states, states[-1:]], axis=0)
+    st.lin_inputs = inputs
+    u, st1 = pkg.mpc_step(model, topo, spec, x, st, cfg)
+    ref = O.mpc_step(model, topo, spec, states[0], st.lin_states, st.lin_inputs, N)
+    assert st1.last_status.value == ref["status"]
+    if ref["status"] == "optimal":
+        scale = max(1.0, float(np.max(np.abs(ref["u_applied"]))))
+        assert float(np.max(np.abs(u.u - ref["u_applied"]))) / scale <= TOL
