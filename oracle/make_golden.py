@@ -13,12 +13,13 @@ nothing in here reimplements the algorithm.
 
 from __future__ import annotations
 
+import os
 import sys
 from pathlib import Path
 
 import numpy as np
 
-REF = Path("/root/reference/pkg/src")
+REF = Path(os.environ.get("GNNMPC_REF", "/root/reference/pkg/src"))
 OUT = Path(__file__).resolve().parents[1] / "tests" / "golden"
 
 
@@ -73,6 +74,57 @@ def cfg2_closed_loop():
     out["plant_u"] = u
     out["plant_out"] = rt.step_state_array(pc, arr, u)
     np.savez_compressed(OUT / "cfg2_closed_loop.npz", **out)
+
+
+def obstacle_provider():
+    """The reference's obstacle_spec_provider (experiments.py:186-238) on a
+    settled M=12 chain, N=10, evaluated at several times with no state and
+    with predicted trajectories pushed towards the sphere: the OCP arrays and
+    every emitted soft half-space row (node, stage, row, bound, rho)."""
+    sys.path.insert(0, str(REF))
+    import gnnmpc.experiments as rex
+    import gnnmpc.graph as rgr
+    import gnnmpc.mpc as rm
+    import gnnmpc.trunk as rt
+
+    out = {}
+    M, N = 12, 10
+    pc = rt.ChainConfig(node_count=M)
+    x0 = rt.settle(pc, 0.5)
+    topo = rgr.chain_topology(M)
+    cfg = rm.MpcConfig(horizon=N, dt=0.01)
+    tip = x0.array[-1, :3].copy()
+    mid = 0.5 * (x0.array[-1, :3] + x0.array[-2, :3])
+    scen = rex.ObstacleScenario(target_point=mid + np.array([0.05, 0.0, 0.0]),
+                                approach_from=np.array([1.0, 0.0, 0.0]), constrained_nodes=(M - 1, M - 2, 5),
+                                start_distance=0.3, approach_time=2.0, hold_time=1.0, retreat_time=2.0,
+                                start_delay=0.2)
+    prov = rex.obstacle_spec_provider(topo, cfg, x0, scen, rex.TrackingWeights(), pc.n_u, pc.u_max)
+    rng = np.random.default_rng(11)
+    out["x0"] = x0.array
+    out["tip"] = tip
+    cases = []
+    for t in (0, 50, 150, 230, 300, 420):
+        for with_state in (False, True):
+            st = None
+            if with_state:
+                pred = np.repeat(x0.array[None], N + 1, axis=0) + 0.01 * rng.standard_normal((N + 1, M, 6))
+                pred[:, :, 0] += np.linspace(0.0, 0.03, N + 1)[:, None]
+                st = rm.MpcState(lin_states=pred, lin_inputs=np.zeros((N, pc.n_u)))
+                out[f"pred_{t}"] = pred
+            spec = prov(t, st)
+            key = f"{t}_{int(with_state)}"
+            cases.append(key)
+            out[f"nodes_{key}"] = np.array([c.node for c in spec.state_constraints], dtype=np.int64)
+            out[f"stages_{key}"] = np.array([c.stage for c in spec.state_constraints], dtype=np.int64)
+            out[f"rows_{key}"] = np.array([c.c for c in spec.state_constraints]).reshape(-1, 6)
+            out[f"bounds_{key}"] = np.array([c.d for c in spec.state_constraints]).reshape(-1)
+            out[f"soft_{key}"] = np.array([c.soft for c in spec.state_constraints], dtype=bool)
+            out[f"rho_{key}"] = np.array([[c.rho1, c.rho2] for c in spec.state_constraints]).reshape(-1, 2)
+            out["q"], out["x_ref"], out["r"], out["u_ref"] = spec.q, spec.x_ref, spec.r, spec.u_ref
+    out["cases"] = np.array(cases)
+    out["centers"] = scen.center(np.arange(0, 6.0, 0.01))
+    np.savez_compressed(OUT / "obstacle_provider.npz", **out)
 
 
 def _model_arrays(prefix, model, out):
@@ -308,5 +360,8 @@ def main():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "cfg2":
         cfg2_closed_loop()
+        raise SystemExit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "obstacle":
+        obstacle_provider()
         raise SystemExit(0)
     main()

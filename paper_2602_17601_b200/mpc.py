@@ -317,15 +317,22 @@ def get_plan(eng, spec, N, nx, nu, cfg, gnn) -> StepPlan:
 
     ds = device_spec(eng, spec, nx, nu)
     s = cfg.solver
-    key = ("plan", id(ds), N, nx, nu, gnn, bool(cfg.warm_start), float(cfg.sqp_damping),
+    # replayable: frozen specs, and tracking specs whose only moving part
+    # (x_ref) is refreshed in place in the plan's device spec; their plans are
+    # keyed by the cached device spec.  Specs rebuilt on every call (not
+    # frozen, e.g. with moving constraint rows) share one eagerly enqueued plan
+    # per row layout, re-pointed at the new device spec (no per-call buffers)
+    replay = getattr(spec, "_frozen", False) or getattr(spec, "_static_token", None) is not None
+    ident = id(ds) if replay else ("rows", ds.rows.m0, ds.ns)
+    key = ("plan", ident, N, nx, nu, gnn, bool(cfg.warm_start), float(cfg.sqp_damping),
            cfg.fallback, float(s.tolerance), int(s.max_iterations), float(s.regularization),
            float(s.fraction_to_boundary))
     plan = eng.cache.get(key)
+    if plan is not None and not replay:
+        plan.ds = ds
     if plan is None or plan.ds is not ds:
         plan = StepPlan(eng, ds, N, nx, nu, cfg, gnn)
-        # replayable: frozen specs, and tracking specs whose only moving part
-        # (x_ref) is refreshed in place in the plan's device spec
-        plan.use_graphs = getattr(spec, "_frozen", False) or getattr(spec, "_static_token", None) is not None
+        plan.use_graphs = replay
         plan.runs = 0
         eng.cache[key] = plan
     return plan

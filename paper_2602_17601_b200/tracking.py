@@ -156,3 +156,105 @@ def run_tracking_device(plant_cfg: ChainConfig, model, mpc_cfg: MpcConfig, ee_re
     t0 = time.perf_counter()
     log = run_closed_loop_device(plant, model, topo, provider, x0, n_steps, mpc_cfg)
     return log, time.perf_counter() - t0
+
+
+@dataclass
+class ObstacleScenario:
+    """A sphere approaching a target point along a line, holding, then
+    retreating (``experiments.py:142-183``)."""
+
+    target_point: np.ndarray
+    approach_from: np.ndarray
+    radius: float = 0.05
+    margin: float = 0.01
+    start_distance: float = 0.5
+    approach_time: float = 4.0
+    hold_time: float = 3.0
+    retreat_time: float = 4.0
+    start_delay: float = 1.0
+    constrained_nodes: tuple = ()
+    activation_factor: float = 2.5
+    rho1: float = 1e3
+    rho2: float = 1e4
+
+    def center(self, t):
+        """Sphere centre at time(s) t (``experiments.py:162-179``)."""
+        t = np.asarray(t, dtype=float)
+        d0 = self.start_distance
+        t1 = self.start_delay
+        t2 = t1 + self.approach_time
+        t3 = t2 + self.hold_time
+        t4 = t3 + self.retreat_time
+        dist = np.where(t < t1, d0,
+                        np.where(t < t2, d0 * (t2 - t) / self.approach_time,
+                                 np.where(t < t3, 0.0, np.where(t < t4, d0 * (t - t3) / self.retreat_time, d0))))
+        return np.asarray(self.target_point, dtype=float) + dist[..., None] * np.asarray(self.approach_from,
+                                                                                      dtype=float)
+
+    @property
+    def total_time(self) -> float:
+        return self.start_delay + self.approach_time + self.hold_time + self.retreat_time
+
+
+def obstacle_spec_provider(topo, cfg: MpcConfig, rest_state: SystemState, scenario: ObstacleScenario,
+                           weights: TrackingWeights, n_u: int, u_max: float):
+    """Rest-pose regulation plus time-varying avoidance half-spaces
+    (``experiments.py:186-238``): per constrained node and stage k = 1..N, a
+    soft row -n^T p <= -(r + margin) - n^T c_k when the predicted position is
+    within activation range of the sphere, n the unit vector from the centre
+    to the prediction.  The predictions are the controller's own shifted plan
+    (``MpcState.lin_states``); only the constrained nodes' positions are read
+    back from the device.""" 
+    from .condensing import StateConstraint
+
+    M = topo.node_count
+    N = cfg.horizon
+    q = np.zeros((M, N + 1, 6, 6))
+    diag = np.zeros(6)
+    diag[:3] = weights.q_pos
+    diag[3:] = weights.q_vel
+    q[:, :] = np.diag(diag)
+    r = np.tile(np.eye(n_u) * weights.r_diag, (N, 1, 1))
+    u_ref = np.zeros((N, n_u))
+    input_cons = [stage_input_box(n_u, 0.0, u_max)] * N
+    rest_arr = np.asarray(rest_state.array, dtype=float)
+    x_ref = np.tile(rest_arr[:, None, :], (1, N + 1, 1))
+    for a in (q, r, u_ref, x_ref):
+        a.flags.writeable = False
+    r_active = scenario.activation_factor * (scenario.radius + scenario.margin)
+    r_con = scenario.radius + scenario.margin
+    stage_offsets = np.arange(N + 1) * cfg.dt
+    nodes = tuple(int(i) for i in scenario.constrained_nodes)
+
+    def predicted(mpc_state):
+        """(N+1 or 1, len(nodes), 3) predicted positions of the constrained nodes."""
+        if mpc_state is None:
+            return rest_arr[None, nodes, :3]
+        ls = mpc_state.lin_states
+        if hasattr(ls, "data_ptr") and not isinstance(ls, np.ndarray):
+            return ls[:, list(nodes), :3].cpu().numpy()
+        ls = np.asarray(ls, dtype=float)
+        return ls[:, nodes, :3] if ls.ndim == 3 else ls[None, nodes, :3]
+
+    def provider(t: int, mpc_state) -> OcpSpec:
+        pred = predicted(mpc_state)
+        centers = scenario.center(t * cfg.dt + stage_offsets)  # (N+1, 3)
+        cons = []
+        for k in range(1, N + 1):
+            for a, node in enumerate(nodes):
+                p_hat = pred[min(k, len(pred) - 1), a]
+                rel = p_hat - centers[k]
+                dist = float(np.linalg.norm(rel))
+                if dist > r_active:
+                    continue
+                n_hat = rel / max(dist, 1e-9)
+                row = np.zeros((1, 6))
+                row[0, :3] = -n_hat
+                bound = np.array([-r_con - float(n_hat @ centers[k])])
+                cons.append(StateConstraint(node, k, row, bound, soft=True, rho1=scenario.rho1,
+                                            rho2=scenario.rho2))
+        # the constraint rows change every step: no static token (device_spec
+        # rebuilds the device copy), unlike the tracking provider
+        return OcpSpec(topo, N, q, x_ref, r, u_ref, input_cons, cons)
+
+    return provider
