@@ -194,15 +194,34 @@ __device__ __forceinline__ bool chol_factor(Qs& S) {
 }
 
 // L -> X = L^{-1} in place (the factor itself is not needed afterwards)
+// Two solve strategies per IPM iteration: (default) X = L^{-1} formed in
+// place once (23 K cycles at cfg3), then every K^{-1} b is two parallel
+// mat-vecs (~9 K per solve); (QP_SOLVE_SUBST) only the diagonal-tile
+// inverses (1.8 K) and single-warp blocked substitution (~24 K per solve,
+// measured: the 15-step chain of shuffle reductions and 23-cycle fp64 FMAs
+// loses to the inverse at two solves per factorisation).
+#ifndef QP_SOLVE_SUBST
 __device__ __forceinline__ void invert_diag_blocks(Qs& S) {
   if (S.T == 0) return;
   qpchol::invert_full<kQpThreads>(S.K, S.T, S.dinv, S.X, S.scr);
 }
+#else
+// inverses of the diagonal tiles of L (into the X region); L stays in K
+__device__ __forceinline__ void invert_diag_blocks(Qs& S) {
+  if (S.T == 0) return;
+  qpchol::diag_inverses<kQpThreads>(S.K, S.T, S.dinv, S.X);
+  __syncthreads();
+}
+#endif
 
 // x = K^{-1} b = X' (X b) through the padded solve vector S.yv (padding stays
 // zero); b and x are shared nf-vectors (x may alias b).  Call with all threads.
 __device__ void chol_solve(Qs& S, const double* b, double* x) {
+#ifndef QP_SOLVE_SUBST
   if (S.T > 0) qpchol::solve_xxt<kQpThreads>(S.K, S.T, S.nf, b, x, S.yv + 8 * S.T);
+#else
+  if (S.T > 0) qpchol::solve_llt<kQpThreads>(S.K, S.X, S.T, S.nf, b, x, S.yv);
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -726,4 +726,104 @@ __device__ __noinline__ void solve_xxt(const double* Kt, int T, int nf, const do
   __syncthreads();
 }
 
+// Inverses of the diagonal tiles only, D_k = L_kk^{-1} (lower), one thread
+// per (tile, column): the first phase of invert_full.
+template <int NT>
+__device__ __noinline__ void diag_inverses(const double* Kt, int T, const double* dinv, double* D) {
+  QP_SMEM(Kt);
+  QP_SMEM(dinv);
+  QP_SMEM(D);
+  for (int t = threadIdx.x; t < 8 * T; t += NT) {
+    const int k = t >> 3, c = t & 7;
+    const double* L = Kt + ti(k, k) * kTS;
+    double* Xt = D + k * kTS;
+    double x[8], acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      x[r] = 0.0;
+      acc[r] = 0.0;
+    }
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      if (p == c) x[p] = dinv[8 * k + p];
+      if (p > c) x[p] = -dinv[8 * k + p] * acc[p];
+      if (p >= c) {
+#pragma unroll
+        for (int r = p + 1; r < 8; ++r) acc[r] = fma(L[eo(r, p)], x[p], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) Xt[eo(r, c)] = x[r];
+  }
+}
+
+// x = K^{-1} b = L^{-T} L^{-1} b by blocked substitution in ONE warp (the
+// caller's other warps wait at the closing barrier): right-looking, so the
+// chain per 8-row block is one 8x8 mat-vec with the diagonal-tile inverse D
+// (lane (r, cq): two FMAs + a 4-lane shuffle reduce) followed by the update
+// of the remaining rows by that block (independent 8-FMA rows, two chains
+// each).  No inverse of L is formed.  b: nf entries (padding reads as zero);
+// x may alias b; s: 8T doubles of shared scratch.  All NT threads call.
+template <int NT>
+__device__ __noinline__ void solve_llt(const double* Kt, const double* D, int T, int nf, const double* b,
+                                       double* x, double* s) {
+  QP_SMEM(Kt);
+  QP_SMEM(D);
+  QP_SMEM(s);
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    const int rr = lane >> 2, cq = lane & 3;
+    for (int t = lane; t < 8 * T; t += 32) s[t] = t < nf ? b[t] : 0.0;
+    __syncwarp();
+    // forward: L y = b (y overwrites s block by block)
+    for (int J = 0; J < T; ++J) {
+      const double* Dj = D + J * kTS;
+      double v = fma(Dj[eo(rr, 2 * cq)], s[8 * J + 2 * cq], Dj[eo(rr, 2 * cq + 1)] * s[8 * J + 2 * cq + 1]);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      __syncwarp();
+      if (cq == 0) s[8 * J + rr] = v;
+      __syncwarp();
+      for (int row = 8 * (J + 1) + lane; row < 8 * T; row += 32) {
+        const double* Lt = Kt + ti(row >> 3, J) * kTS;
+        const int r = row & 7;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; c += 2) {
+          a0 = fma(Lt[eo(r, c)], s[8 * J + c], a0);
+          a1 = fma(Lt[eo(r, c + 1)], s[8 * J + c + 1], a1);
+        }
+        s[row] -= a0 + a1;
+      }
+      __syncwarp();
+    }
+    // backward: L^T x = y (x overwrites s block by block, from the last)
+    for (int J = T - 1; J >= 0; --J) {
+      const double* Dj = D + J * kTS;
+      // x_J[c] = sum_{r >= c} D_J[r][c] t_J[r]; lane (cc = rr, rq = cq)
+      double v = fma(Dj[eo(2 * cq, rr)], s[8 * J + 2 * cq], Dj[eo(2 * cq + 1, rr)] * s[8 * J + 2 * cq + 1]);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      __syncwarp();
+      if (cq == 0) s[8 * J + rr] = v;
+      __syncwarp();
+      // t_K[c] -= sum_r L_JK[r][c] x_J[r] for every column of the blocks K < J
+      for (int col = lane; col < 8 * J; col += 32) {
+        const double* Lt = Kt + ti(J, col >> 3) * kTS;
+        const int c = col & 7;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int r = 0; r < 8; r += 2) {
+          a0 = fma(Lt[eo(r, c)], s[8 * J + r], a0);
+          a1 = fma(Lt[eo(r + 1, c)], s[8 * J + r + 1], a1);
+        }
+        s[col] -= a0 + a1;
+      }
+      __syncwarp();
+    }
+    for (int t = lane; t < nf; t += 32) x[t] = s[t];
+  }
+  __syncthreads();
+}
+
 }  // namespace qpchol
