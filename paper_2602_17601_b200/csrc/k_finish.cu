@@ -5,6 +5,7 @@
 // read on the device, the damped update / fallback policy / shift are applied
 // and the successor trajectory is written in one elementwise pass.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -148,6 +149,96 @@ __global__ void __launch_bounds__(256, 3) k_finish_states(const FinishArgs A, in
   }
 }
 
+// Fixed-order butterfly of warp_rows for 8 row partials: lane a < 8 returns
+// row a (bitwise the same sums as warp_rows' single-chunk case).
+__device__ __forceinline__ double butterfly8(const double (&s)[8], int lane) {
+  const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+  double t4[4], t2[2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double send = h4 ? s[q] : s[q + 4];
+    const double keep = h4 ? s[q + 4] : s[q];
+    t4[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const double send = h3 ? t4[q] : t4[q + 2];
+    const double keep = h3 ? t4[q + 2] : t4[q];
+    t2[q] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double v;
+  {
+    const double send = h2 ? t2[0] : t2[1];
+    const double keep = h2 ? t2[1] : t2[0];
+    v = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return __shfl_sync(0xffffffffu, v, (4 * lane) & 31);
+}
+
+// k_finish_states for nx = NX <= 8 and ld <= 128 (one 16-byte column chunk
+// per lane and row): software-pipelined, the Gamma rows (and u coefficients)
+// of the warp's next item are loaded before the current item is reduced, so
+// two items' rows are in flight per warp.  Same sums in the same order as
+// warp_rows (bitwise identical results).
+template <int NX>
+__global__ void __launch_bounds__(256, 3) k_finish_states_pipe(const FinishArgs A, int64_t items) {
+  const int M = A.M, N = A.N, ld = A.ld, nu = A.nu;
+  const int lane = threadIdx.x & 31, c0 = lane * 4, xc = N * nu;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  float4 v[NX];
+  double coef[4];
+  auto fetch = [&](int64_t w) {
+    const int k = (int)(w % (N + 1));
+    const int64_t gi = w / (N + 1);
+    const int64_t bi = gi / M;
+    const int live = k * nu;
+    const bool act = solved(A.status[bi]) && c0 < ld && (c0 < live || (xc >= c0 && xc < c0 + 4));
+    const float* rows = A.W + ((gi * (N + 1) + k) * NX) * (int64_t)ld + c0;
+    const double* u = A.u + bi * A.ldu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + j;
+      coef[j] = !act ? 0.0 : (c < live ? u[c] : (c == xc ? 1.0 : 0.0));
+    }
+#pragma unroll
+    for (int q = 0; q < NX; ++q)
+      v[q] = act ? __ldcs(reinterpret_cast<const float4*>(rows + (int64_t)q * ld)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  if (w0 < items) fetch(w0);
+  for (int64_t w = w0; w < items; w += nw) {
+    double s[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NX; ++q) {
+      s[q] = fma((double)v[q].x, coef[0], s[q]);
+      s[q] = fma((double)v[q].y, coef[1], s[q]);
+      s[q] = fma((double)v[q].z, coef[2], s[q]);
+      s[q] = fma((double)v[q].w, coef[3], s[q]);
+    }
+    if (w + nw < items) fetch(w + nw);
+    const double p = butterfly8(s, lane);
+    const int k = (int)(w % (N + 1));
+    const int64_t gi = w / (N + 1);
+    const int i = (int)(gi % M);
+    const int64_t bi = gi / M;
+    if (lane < NX) {
+      const bool ok = solved(A.status[bi]);
+      const int a = lane;
+      const int64_t t = ((bi * (N + 1) + k) * M + i) * NX + a;
+      const double x = ok ? (1.0 - A.damp) * A.lin_states[t] + A.damp * p : A.fb_states[t];
+      if (A.cur_states) A.cur_states[t] = x;
+      A.planned_states[((bi * M + i) * (N + 1) + k) * NX + a] = x;
+      const int64_t base = bi * (int64_t)(N + 1) * M * NX;
+      if (k >= 1) A.next_states[base + ((int64_t)(k - 1) * M + i) * NX + a] = x;
+      if (k == N) A.next_states[base + ((int64_t)N * M + i) * NX + a] = x;
+    }
+  }
+}
+
 __global__ void k_finish_inputs(const FinishArgs A, int B) {
   const int N = A.N, nu = A.nu;
   const int64_t total = (int64_t)B * N * nu;
@@ -244,7 +335,18 @@ int gm_mpc_finish(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const d
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t items = (int64_t)B * (N + 1) * ctx->M;
   const int blocks = (int)std::min<int64_t>((items + 7) / 8, 16 * ctx->sm_count);
-  k_finish_states<<<blocks, 256, 0, st>>>(a, items);
+  // nx = 6, ld <= 128: the pipelined kernel (B200, ncu: cfg5 2.15 -> 1.46 ms,
+  // cfg4 4.38 -> 2.97 ms per launch; batching 2 or 4 items per warp at lower
+  // occupancy measured slower, 2.93 / 5.18 ms at cfg5).  GM_FIN_MODE=0 forces
+  // the generic kernel (measurement override).
+  static const int fin_mode = [] {
+    const char* e = std::getenv("GM_FIN_MODE");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (ctx->nx == 6 && ld <= 128 && fin_mode != 0)
+    k_finish_states_pipe<6><<<blocks, 256, 0, st>>>(a, items);
+  else
+    k_finish_states<<<blocks, 256, 0, st>>>(a, items);
   GM_LAUNCH_CHECK(ctx, "k_finish_states");
   const int64_t ti = (int64_t)B * N * ctx->n_u;
   k_finish_inputs<<<(int)std::max<int64_t>(1, std::min<int64_t>((ti + 255) / 256, 1024)), 256, 0, st>>>(a, B);
