@@ -91,7 +91,7 @@ int gm_create(gm_ctx** out, int device) {
   }
   if (const char* v = getenv("GM_LINEARIZE_MODE")) {
     const int m = atoi(v);
-    c->lin_mode = (m >= 0 && m <= 3) ? m : 0;
+    c->lin_mode = (m >= 0 && m <= 4) ? m : 0;
   }
   *out = c;
   return GM_OK;

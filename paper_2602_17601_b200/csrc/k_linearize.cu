@@ -521,7 +521,7 @@ int gm_linearize(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
 
 int gm_set_linearize_mode(gm_ctx* ctx, int mode) {
   if (!ctx) return GM_ERR_CONFIG;
-  if (mode < 0 || mode > 3) return gm_fail(ctx, GM_ERR_CONFIG, "linearize mode must be 0, 1, 2 or 3");
+  if (mode < 0 || mode > 4) return gm_fail(ctx, GM_ERR_CONFIG, "linearize mode must be 0 .. 4");
   ctx->lin_mode = mode;
   return GM_OK;
 }

@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "umma.cuh"
 
 namespace {
 
@@ -387,6 +388,151 @@ __global__ void __launch_bounds__(kJT) k_jac_phi(int Rj, int n_p, const float* _
   }
 }
 
+// phi Jacobian rows on the tensor cores (tcgen05, 3xTF32): the same chain as
+// k_jac_phi, as two GEMMs per 128-row tile,
+//   V1 = (V0 W_1) .* mask_0    (128 x D2) x (D2 x D1),  V0 = seed rows
+//   O  = V1 W_0                (128 x D1) x (D1 x D0),  D0 padded to 32
+// with W_1, W_0 resident in shared memory as K-major B operands (hi/lo
+// halves), the A tile staged by its 128 threads (thread t = row t = TMEM
+// lane t), fp32 accumulation in TMEM, read back with tcgen05.ld.  Two CTAs
+// per SM overlap one tile's staging with the other's MMAs.
+constexpr int kJTC = 128;
+template <int D0, int D1, int D2>
+struct JacPhiTc {
+  static constexpr int N0 = 32;                            // padded layer-0 output width
+  static constexpr uint32_t SBO_A = (D2 / 4) * 128;        // A: 128 rows x K = 64
+  static constexpr uint32_t SBO_1 = (D2 / 4) * 128;        // B1: D1 rows x K = D2
+  static constexpr uint32_t SBO_0 = (D1 / 4) * 128;        // B0: N0 rows x K = D1
+  static constexpr size_t A_BYTES = 16 * (size_t)SBO_A;
+  static constexpr size_t B1_BYTES = (D1 / 8) * (size_t)SBO_1;
+  static constexpr size_t B0_BYTES = (N0 / 8) * (size_t)SBO_0;
+  static constexpr size_t SMEM = 2 * (A_BYTES + B1_BYTES + B0_BYTES) + 16;
+};
+
+template <int D0, int D1, int D2>
+__global__ void __launch_bounds__(kJTC, 2) k_jac_phi_tc(int Rj, int n_p, const float* __restrict__ w2,
+                                                        const float* __restrict__ w1, const float* __restrict__ w0,
+                                                        const uint8_t* __restrict__ mphi, int hphi,
+                                                        float* __restrict__ out) {
+  using T = JacPhiTc<D0, D1, D2>;
+  static_assert(D1 == 64 && D2 == 64 && D0 <= T::N0 && D0 % 4 == 0, "tile shapes for phi 28-64-64");
+  extern __shared__ __align__(128) unsigned char smj[];
+  unsigned char* a_hi = smj;
+  unsigned char* a_lo = a_hi + T::A_BYTES;
+  unsigned char* b1_hi = a_lo + T::A_BYTES;
+  unsigned char* b1_lo = b1_hi + T::B1_BYTES;
+  unsigned char* b0_hi = b1_lo + T::B1_BYTES;
+  unsigned char* b0_lo = b0_hi + T::B0_BYTES;
+  uint64_t* mbar = (uint64_t*)(b0_lo + T::B0_BYTES);
+  uint32_t* tslot = (uint32_t*)(mbar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  // B operands: B1(n, k) = W_1[k][n] (W_1 is (D2 out, D1 in)), B0(n, k) = W_0[k][n]
+  for (int t = tid; t < D2 * D1; t += kJTC) umma::put_split(b1_hi, b1_lo, t % D1, t / D1, T::SBO_1, w1[t]);
+  for (int t = tid; t < T::N0 * D1; t += kJTC) {
+    const int k = t / T::N0, n = t - k * T::N0;
+    umma::put_split(b0_hi, b0_lo, n, k, T::SBO_0, n < D0 ? w0[k * D0 + n] : 0.f);
+  }
+  if (warp == 0) umma::tmem_alloc<128>(tslot);  // V1 in columns [0, 64), O in [64, 96)
+  if (tid == 32) umma::mbar_init(mbar, 1);
+  umma::fence_async_smem();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  uint32_t phase = 0;
+  const uint32_t rowoff = (uint32_t)(tid >> 3) * T::SBO_A + (uint32_t)(tid & 7) * 16u;
+  for (int64_t tile = blockIdx.x; tile * kJTC < Rj; tile += gridDim.x) {
+    const int64_t r = tile * kJTC + tid;
+    const bool valid = r < Rj;
+    const int pr = valid ? (int)(r / n_p) : 0, ro = valid ? (int)(r - (int64_t)pr * n_p) : 0;
+    const uint8_t* mp = mphi + (int64_t)pr * hphi;
+    // seed: row ro of W_2 masked by hidden layer 1
+#pragma unroll
+    for (int c0 = 0; c0 < D2; c0 += 16) {
+      uint4 mv = make_uint4(0u, 0u, 0u, 0u);
+      if (valid) mv = *reinterpret_cast<const uint4*>(mp + D1 + c0);
+      const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(w2 + ro * D2 + c0 + 4 * q));
+        const float x[4] = {(mw[q] & 0xffu) ? w.x : 0.f, (mw[q] & 0xff00u) ? w.y : 0.f,
+                            (mw[q] & 0xff0000u) ? w.z : 0.f, (mw[q] & 0xff000000u) ? w.w : 0.f};
+        float h[4], l[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          h[u] = umma::tf32_hi(x[u]);
+          l[u] = x[u] - h[u];
+        }
+        const uint32_t o = rowoff + (uint32_t)((c0 + 4 * q) >> 2) * 128u;
+        *(float4*)(a_hi + o) = make_float4(h[0], h[1], h[2], h[3]);
+        *(float4*)(a_lo + o) = make_float4(l[0], l[1], l[2], l[3]);
+      }
+    }
+    umma::fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      umma::fence_after();
+      umma::gram_3xtf32(tmem, a_hi, a_lo, T::SBO_A, b1_hi, b1_lo, T::SBO_1, D2 / 8, umma::idesc_tf32(128, D1),
+                        false);
+      umma::commit(mbar);
+    }
+    umma::mbar_wait(mbar, phase);
+    phase ^= 1;
+    umma::fence_after();
+    // V1 .* mask of hidden layer 0 -> A (the first GEMM has consumed it)
+#pragma unroll
+    for (int c0 = 0; c0 < D1; c0 += 16) {
+      float v[16];
+      umma::tmem_ld16(lane_base + (uint32_t)c0, v);
+      uint4 mv = make_uint4(0u, 0u, 0u, 0u);
+      if (valid) mv = *reinterpret_cast<const uint4*>(mp + c0);
+      const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float h[4], l[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float x = ((mw[q] >> (8 * u)) & 0xffu) ? v[4 * q + u] : 0.f;
+          h[u] = umma::tf32_hi(x);
+          l[u] = x - h[u];
+        }
+        const uint32_t o = rowoff + (uint32_t)((c0 + 4 * q) >> 2) * 128u;
+        *(float4*)(a_hi + o) = make_float4(h[0], h[1], h[2], h[3]);
+        *(float4*)(a_lo + o) = make_float4(l[0], l[1], l[2], l[3]);
+      }
+    }
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      umma::fence_after();
+      umma::gram_3xtf32(tmem + 64, a_hi, a_lo, T::SBO_A, b0_hi, b0_lo, T::SBO_0, D1 / 8,
+                        umma::idesc_tf32(128, T::N0), false);
+      umma::commit(mbar);
+    }
+    umma::mbar_wait(mbar, phase);
+    phase ^= 1;
+    umma::fence_after();
+    float o0[16], o1[16];
+    umma::tmem_ld16(lane_base + 64u, o0);
+    umma::tmem_ld16(lane_base + 80u, o1);
+    if (valid) {
+      float4* dst = reinterpret_cast<float4*>(out + r * D0);
+#pragma unroll
+      for (int q = 0; q < D0 / 4; ++q) {
+        const int c = 4 * q;
+        const float x0 = c < 16 ? o0[c] : o1[c - 16], x1 = c + 1 < 16 ? o0[c + 1] : o1[c - 15];
+        const float x2 = c + 2 < 16 ? o0[c + 2] : o1[c - 14], x3 = c + 3 < 16 ? o0[c + 3] : o1[c - 13];
+        dst[q] = make_float4(x0, x1, x2, x3);
+      }
+    }
+    umma::fence_before();  // this tile's TMEM reads precede the next tile's MMAs
+  }
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<128>(tmem);
+}
+
 // psi VJP rows (point, edge, ro): seed J_m of the destination node (from
 // jphi), then layers L-1 .. 0 (L = 3): out (Re*n_p, D0) = Pe
 // The epilogue also writes the row's part of the a_nbr block of its (point,
@@ -739,7 +885,21 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   if (phi.L == 1) {
     return gm_fail(ctx, GM_ERR_CONFIG, "single-layer phi is handled by the fused kernel");
   }
-  if (fused) {
+  // tcgen05 phi Jacobian unless linearize mode 4 (per-row SIMT chain) is set
+  if (fused && ctx->lin_mode != 4 && n_p <= 4) {
+    using T = JacPhiTc<28, 64, 64>;
+    static bool attr = false;
+    if (!attr) {
+      GM_CUDA(ctx, cudaFuncSetAttribute(k_jac_phi_tc<28, 64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)T::SMEM));
+      attr = true;
+    }
+    const int64_t tiles = (Rj + kJTC - 1) / kJTC;
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, 2 * (int64_t)ctx->sm_count);
+    k_jac_phi_tc<28, 64, 64><<<grid, kJTC, T::SMEM, st>>>((int)Rj, n_p, phi.w32[2], phi.w32[1], phi.w32[0], mphi,
+                                                          hphi, jphi);
+    GM_LAUNCH_CHECK(ctx, "k_jac_phi_tc");
+  } else if (fused) {
     k_jac_phi<28, 64, 64><<<chain_grid(Rj, ctx->sm_count), kJT, 0, st>>>((int)Rj, n_p, phi.w32[2], phi.w32[1],
                                                                          phi.w32[0], mphi, hphi, jphi);
     GM_LAUNCH_CHECK(ctx, "k_jac_phi");

@@ -28,12 +28,13 @@ def pkg():
 
 
 def _set_lin_mode(pkg, cs, mode):
-    """Force the fused (1), layer-wise with fused Jacobian chains (2) or fully
-    layer-wise (3) linearisation kernels; 0 = auto."""
+    """Force the fused (1), layer-wise with fused Jacobian chains and the phi
+    Jacobian on tcgen05 (2), fully layer-wise (3) or layer-wise with the SIMT
+    phi Jacobian chain (4) linearisation kernels; 0 = auto."""
     pkg.device.engine(cs.topo, cs.model).ctx.call("gm_set_linearize_mode", mode)
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
 @pytest.mark.parametrize("name", CASES)
 def test_linearize_matches_reference(pkg, name, mode):
     cs = pipeline_case(name)
@@ -50,7 +51,7 @@ def test_linearize_matches_reference(pkg, name, mode):
     assert float(np.max(np.abs(lin.c - d["lin_c"]))) / xscale <= TOL
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
 @pytest.mark.parametrize("name", CASES)
 def test_affine_model_exact_at_point(pkg, name, mode):
     """x+ = A x + sum A_nbr x_j + B u + c reproduces step_array (gnn.py:291-297)."""
