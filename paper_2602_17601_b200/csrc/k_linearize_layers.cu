@@ -533,6 +533,163 @@ __global__ void __launch_bounds__(kJTC, 2) k_jac_phi_tc(int Rj, int n_p, const f
   if (warp == 0) umma::tmem_free<128>(tmem);
 }
 
+// psi VJP rows on the tensor cores (tcgen05, 3xTF32): the chain of k_jac_psi
+// as three GEMMs per 128-row tile (K = 16, 32, 32; N = 32, 32, 16 with D0 = 6
+// padded), weights resident as K-major B operands, masks applied between the
+// GEMMs from TMEM, the same a_nbr epilogue.  48 KB of shared memory and 128
+// TMEM columns per CTA: four CTAs per SM overlap staging and MMAs.
+template <int D0, int D1, int D2, int D3>
+struct JacPsiTc {
+  static constexpr int N0 = 16;                             // padded output width
+  static constexpr uint32_t SBO_A = 8 * 128;                // A: 128 rows x K <= 32
+  static constexpr uint32_t SBO_2 = (D3 / 4) * 128;         // B2: D2 rows x K = D3
+  static constexpr uint32_t SBO_1 = (D2 / 4) * 128;         // B1: D1 rows x K = D2
+  static constexpr uint32_t SBO_0 = (D1 / 4) * 128;         // B0: N0 rows x K = D1
+  static constexpr size_t A_BYTES = 16 * (size_t)SBO_A;
+  static constexpr size_t B2_BYTES = (D2 / 8) * (size_t)SBO_2;
+  static constexpr size_t B1_BYTES = (D1 / 8) * (size_t)SBO_1;
+  static constexpr size_t B0_BYTES = (N0 / 8) * (size_t)SBO_0;
+  static constexpr size_t SMEM = 2 * (A_BYTES + B2_BYTES + B1_BYTES + B0_BYTES) + 16;
+};
+
+// A row (thread t) <- x[0..W) masked by bytes m (or unmasked), hi/lo split
+template <int W>
+__device__ __forceinline__ void stage_row(unsigned char* hi, unsigned char* lo, uint32_t rowoff, const float* x,
+                                          const uint8_t* m) {
+#pragma unroll
+  for (int c0 = 0; c0 < W; c0 += 16) {
+    uint4 mv = make_uint4(~0u, ~0u, ~0u, ~0u);
+    if (m) mv = *reinterpret_cast<const uint4*>(m + c0);
+    const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float h[4], l[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float v = ((mw[q] >> (8 * u)) & 0xffu) ? x[c0 + 4 * q + u] : 0.f;
+        h[u] = umma::tf32_hi(v);
+        l[u] = v - h[u];
+      }
+      const uint32_t o = rowoff + (uint32_t)((c0 + 4 * q) >> 2) * 128u;
+      *(float4*)(hi + o) = make_float4(h[0], h[1], h[2], h[3]);
+      *(float4*)(lo + o) = make_float4(l[0], l[1], l[2], l[3]);
+    }
+  }
+}
+
+template <int D0, int D1, int D2, int D3>
+__global__ void __launch_bounds__(kJTC, 4) k_jac_psi_tc(const LinDims d, const int* __restrict__ dst,
+                                                        const float* __restrict__ jphi, const float* __restrict__ w2,
+                                                        const float* __restrict__ w1, const float* __restrict__ w0,
+                                                        const uint8_t* __restrict__ mpsi, int hpsi,
+                                                        float* __restrict__ out, float dtf,
+                                                        const double* __restrict__ norm, int E,
+                                                        float* __restrict__ a_nbr) {
+  using T = JacPsiTc<D0, D1, D2, D3>;
+  static_assert(D3 == 16 && D2 == 32 && D1 == 32 && D0 <= T::N0 && D0 % 2 == 0, "tile shapes for psi 6-32-32-16");
+  extern __shared__ __align__(128) unsigned char smj[];
+  unsigned char* a_hi = smj;
+  unsigned char* a_lo = a_hi + T::A_BYTES;
+  unsigned char* b2_hi = a_lo + T::A_BYTES;
+  unsigned char* b2_lo = b2_hi + T::B2_BYTES;
+  unsigned char* b1_hi = b2_lo + T::B2_BYTES;
+  unsigned char* b1_lo = b1_hi + T::B1_BYTES;
+  unsigned char* b0_hi = b1_lo + T::B1_BYTES;
+  unsigned char* b0_lo = b0_hi + T::B0_BYTES;
+  uint64_t* mbar = (uint64_t*)(b0_lo + T::B0_BYTES);
+  uint32_t* tslot = (uint32_t*)(mbar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  // B(n, k) = W_l[k][n] (W_l is (out, in) row-major)
+  for (int t = tid; t < D3 * D2; t += kJTC) umma::put_split(b2_hi, b2_lo, t % D2, t / D2, T::SBO_2, w2[t]);
+  for (int t = tid; t < D2 * D1; t += kJTC) umma::put_split(b1_hi, b1_lo, t % D1, t / D1, T::SBO_1, w1[t]);
+  for (int t = tid; t < T::N0 * D1; t += kJTC) {
+    const int k = t / T::N0, n = t - k * T::N0;
+    umma::put_split(b0_hi, b0_lo, n, k, T::SBO_0, n < D0 ? w0[k * D0 + n] : 0.f);
+  }
+  if (warp == 0) umma::tmem_alloc<128>(tslot);  // h2 in [0, 32), h1 in [32, 64), o in [64, 80)
+  if (tid == 32) umma::mbar_init(mbar, 1);
+  umma::fence_async_smem();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  uint32_t phase = 0;
+  const uint32_t rowoff = (uint32_t)(tid >> 3) * T::SBO_A + (uint32_t)(tid & 7) * 16u;
+  const int n_p = d.n_p;
+  const int64_t Rv = (int64_t)d.Re * n_p;
+  auto gemm = [&](uint32_t col, const unsigned char* bh, const unsigned char* bl, uint32_t sbo_b, int K, int N) {
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      umma::fence_after();
+      umma::gram_3xtf32(tmem + col, a_hi, a_lo, T::SBO_A, bh, bl, sbo_b, K / 8, umma::idesc_tf32(128, N), false);
+      umma::commit(mbar);
+    }
+    umma::mbar_wait(mbar, phase);
+    phase ^= 1;
+    umma::fence_after();
+  };
+  for (int64_t tile = blockIdx.x; tile * kJTC < Rv; tile += gridDim.x) {
+    const int64_t r = tile * kJTC + tid;
+    const bool valid = r < Rv;
+    const int64_t re = valid ? r / n_p : 0;
+    const int ro = valid ? (int)(r - re * n_p) : 0;
+    const int p = (int)(re / d.nE);
+    const int e = d.e0 + (int)(re - (int64_t)p * d.nE);
+    const uint8_t* mp = mpsi + re * hpsi;
+    float v[D3];
+    if (valid) {
+      const int rn = p * d.nN + (__ldg(dst + e) - d.lo);
+      const float2* js = reinterpret_cast<const float2*>(jphi + ((int64_t)rn * n_p + ro) * d.nin + d.nx);
+#pragma unroll
+      for (int m = 0; m < D3 / 2; ++m) {
+        const float2 x = __ldg(js + m);
+        v[2 * m] = x.x;
+        v[2 * m + 1] = x.y;
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < D3; ++m) v[m] = 0.f;
+    }
+    stage_row<D3>(a_hi, a_lo, rowoff, v, nullptr);
+    gemm(0, b2_hi, b2_lo, T::SBO_2, D3, D2);
+    {
+      float h[D2];
+      umma::tmem_ld16(lane_base + 0u, *reinterpret_cast<float(*)[16]>(h));
+      umma::tmem_ld16(lane_base + 16u, *reinterpret_cast<float(*)[16]>(h + 16));
+      stage_row<D2>(a_hi, a_lo, rowoff, h, valid ? mp + D1 : nullptr);  // mask of hidden layer 1
+    }
+    gemm(32, b1_hi, b1_lo, T::SBO_1, D2, D1);
+    {
+      float h[D1];
+      umma::tmem_ld16(lane_base + 32u, *reinterpret_cast<float(*)[16]>(h));
+      umma::tmem_ld16(lane_base + 48u, *reinterpret_cast<float(*)[16]>(h + 16));
+      stage_row<D1>(a_hi, a_lo, rowoff, h, valid ? mp : nullptr);  // mask of hidden layer 0
+    }
+    gemm(64, b0_hi, b0_lo, T::SBO_0, D1, T::N0);
+    float o[16];
+    umma::tmem_ld16(lane_base + 64u, o);
+    if (valid) {
+      float* dp = out + r * D0;
+#pragma unroll
+      for (int c = 0; c < D0; c += 2) *reinterpret_cast<float2*>(dp + c) = make_float2(o[c], o[c + 1]);
+      float* blk = a_nbr + ((int64_t)p * E + e) * D0 * D0;
+#pragma unroll
+      for (int c = 0; c < D0; c += 2) {
+        const float j0 = -o[c] * (float)(1.0 / __ldg(norm + D0 + c));
+        const float j1 = -o[c + 1] * (float)(1.0 / __ldg(norm + D0 + c + 1));
+        *reinterpret_cast<float2*>(blk + ro * D0 + c) = make_float2(dtf * j0, dtf * j1);
+        *reinterpret_cast<float2*>(blk + (n_p + ro) * D0 + c) = make_float2(j0, j1);
+      }
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<128>(tmem);
+}
+
 // psi VJP rows (point, edge, ro): seed J_m of the destination node (from
 // jphi), then layers L-1 .. 0 (L = 3): out (Re*n_p, D0) = Pe
 // The epilogue also writes the row's part of the a_nbr block of its (point,
@@ -923,7 +1080,21 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   }
   // psi VJP seeded with J_m[dst], n_p rows per edge
   const int64_t Rv = d.Re * n_p;
-  if (d.Re > 0 && fused) {
+  if (d.Re > 0 && fused && ctx->lin_mode != 4 && n_p <= 4) {
+    using T = JacPsiTc<6, 32, 32, 16>;
+    static bool attr = false;
+    if (!attr) {
+      GM_CUDA(ctx, cudaFuncSetAttribute(k_jac_psi_tc<6, 32, 32, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)T::SMEM));
+      attr = true;
+    }
+    const int64_t tiles = (Rv + kJTC - 1) / kJTC;
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, 4 * (int64_t)ctx->sm_count);
+    k_jac_psi_tc<6, 32, 32, 16><<<grid, kJTC, T::SMEM, st>>>(d, ctx->d_dst, jphi, psi.w32[2], psi.w32[1],
+                                                              psi.w32[0], mpsi, hpsi, Pe, (float)ctx->dt,
+                                                              ctx->d_norm, (int)ctx->E, a_nbr);
+    GM_LAUNCH_CHECK(ctx, "k_jac_psi_tc");
+  } else if (d.Re > 0 && fused) {
     k_jac_psi<6, 32, 32, 16><<<chain_grid(Rv, ctx->sm_count), kJT, 0, st>>>(
         d, ctx->d_dst, jphi, psi.w32[2], psi.w32[1], psi.w32[0], mpsi, hpsi, Pe, (float)ctx->dt, ctx->d_norm,
         (int)ctx->E, a_nbr);
