@@ -641,42 +641,110 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.X = (double*)(smem + L0.o_x);
   }
 
-  // ---- classify rows (qpsolver.py:100-109): single-nonzero vs general
-  for (int r = wid; r < m; r += kQpWarps) {
-    const double* Cr = C + (int64_t)r * n;
-    int cnt = 0, first = n;
-    double fval = 0.0;
-    for (int c0 = 0; c0 < n; c0 += 32) {
-      const int c = c0 + lane;
-      const double v = c < n ? Cr[c] : 0.0;
-      const unsigned bal = __ballot_sync(0xffffffffu, v != 0.0);
-      cnt += __popc(bal);
-      if (bal && first == n) {
-        const int src = __ffs(bal) - 1;
-        first = c0 + src;
-        fval = __shfl_sync(0xffffffffu, v, src);
+  // ---- classify rows (qpsolver.py:100-109): single-nonzero vs general.
+  // Setup runs once per solve; every pass below is a flat, independent-load
+  // sweep or a warp-wide ballot/match compaction (no single-thread loops over
+  // m or n: they cost ~100 us of L2/shared latency per solve).
+  // Pass 1 over C: per-row nonzero count (rcol) and first nonzero column
+  // (grow), by shared atomics.
+  for (int r = tid; r < m; r += nt) {
+    S.rcol[r] = 0;
+    S.grow[r] = n;
+  }
+  for (int c = tid; c <= n; c += nt) {
+    S.colptr[c] = 0;
+    S.cstart[c] = c * n - (c * (c - 1)) / 2;
+  }
+  for (int c = tid; c < n; c += nt) S.elig[c] = m > 0 ? 1 : 0;
+  __syncthreads();
+  {
+    const int64_t mn = (int64_t)m * n;
+    for (int64_t t0 = tid; t0 < mn; t0 += 8 * (int64_t)nt) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t t = t0 + (int64_t)j * nt;
+        v[j] = t < mn ? __ldg(C + t) : 0.0;
       }
-    }
-    if (lane == 0) {
-      S.rcol[r] = cnt == 1 ? first : -1;
-      S.rval[r] = cnt == 1 ? fval : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (v[j] != 0.0) {
+          const int64_t t = t0 + (int64_t)j * nt;
+          const int r = (int)(t / n), c = (int)(t - (int64_t)r * n);
+          atomicAdd(&S.rcol[r], 1);
+          atomicMin(&S.grow[r], c);
+        }
     }
   }
-  for (int c = tid; c <= n; c += nt) S.cstart[c] = c * n - (c * (c - 1)) / 2;
+  // Pass over H: the scale reference max|H| (qpsolver.py:124) and the
+  // eliminable-variable test below (no off-diagonal Hessian entry in the row)
+  double hmax_loc = 0.0;
+  {
+    const int64_t nn2 = (int64_t)n * n;
+    for (int64_t t0 = tid; t0 < nn2; t0 += 8 * (int64_t)nt) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t t = t0 + (int64_t)j * nt;
+        v[j] = t < nn2 ? __ldg(H + t) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        hmax_loc = fmax(hmax_loc, fabs(v[j]));
+        if (v[j] != 0.0) {
+          const int64_t t = t0 + (int64_t)j * nt;
+          const int r = (int)(t / n), c = (int)(t - (int64_t)r * n);
+          if (r != c) S.elig[r] = 0;
+        }
+      }
+    }
+  }
   __syncthreads();
-  if (tid == 0) {
+  for (int r = tid; r < m; r += nt) {
+    const int cnt = S.rcol[r], first = S.grow[r];
+    S.rcol[r] = cnt == 1 ? first : -1;
+    S.rval[r] = cnt == 1 ? C[(int64_t)r * n + first] : 0.0;
+    if (cnt == 1) atomicAdd(&S.colptr[first + 1], 1);
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const unsigned lt = (1u << lane) - 1u;
+    // general rows, ascending
     int ng = 0;
-    for (int r = 0; r < m; ++r)
-      if (S.rcol[r] < 0) S.grow[ng++] = r;
-    for (int c = 0; c <= n; ++c) S.colptr[c] = 0;
-    for (int r = 0; r < m; ++r)
-      if (S.rcol[r] >= 0) S.colptr[S.rcol[r] + 1]++;
-    for (int c = 0; c < n; ++c) S.colptr[c + 1] += S.colptr[c];
-    for (int r = 0; r < m; ++r)  // counting sort: ascending row order per column
-      if (S.rcol[r] >= 0) S.colrows[S.colptr[S.rcol[r]]++] = r;
-    for (int c = n; c > 0; --c) S.colptr[c] = S.colptr[c - 1];
-    S.colptr[0] = 0;
-    sh_int[0] = ng;
+    for (int r0 = 0; r0 < m; r0 += 32) {
+      const int r = r0 + lane;
+      const bool gen = r < m && S.rcol[r] < 0;
+      const unsigned bg = __ballot_sync(0xffffffffu, gen);
+      if (gen) S.grow[ng + __popc(bg & lt)] = r;
+      ng += __popc(bg);
+    }
+    // column starts: exclusive prefix of the per-column counts in colptr[c + 1]
+    int run = 0;
+    for (int c0 = 0; c0 <= n; c0 += 32) {
+      const int c = c0 + lane;
+      int v = c <= n ? S.colptr[c] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (c <= n) S.colptr[c] = run + v;
+      run += __shfl_sync(0xffffffffu, v, 31);
+    }
+    __syncwarp();
+    // stable counting sort (ascending rows per column); running offsets in kidx
+    for (int c = lane; c < n; c += 32) S.kidx[c] = S.colptr[c];
+    __syncwarp();
+    for (int r0 = 0; r0 < m; r0 += 32) {
+      const int r = r0 + lane;
+      const int c = r < m ? S.rcol[r] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, c);
+      if (c >= 0) S.colrows[S.kidx[c] + __popc(peers & lt)] = r;
+      __syncwarp();
+      if (c >= 0 && (peers & lt) == 0) S.kidx[c] += __popc(peers);
+      __syncwarp();
+    }
+    if (lane == 0) sh_int[0] = ng;
   }
   __syncthreads();
   S.ng = sh_int[0];
@@ -690,16 +758,9 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.ga = gv + S.ng;
     S.cf = gv + 2 * S.ng;
   }
-  // ---- eliminable variables: diagonal-only Hessian row, at most one general
-  // row, and alone in that row (otherwise K_ee would not be diagonal)
-  for (int c = wid; c < n; c += kQpWarps) {
-    const double* Hr = H + (int64_t)c * n;
-    bool off = false;
-    for (int c2 = lane; c2 < n; c2 += 32) off |= (c2 != c && Hr[c2] != 0.0);
-    off = __any_sync(0xffffffffu, off);
-    if (lane == 0) S.elig[c] = (m > 0 && !off) ? 1 : 0;
-  }
-  __syncthreads();
+  // ---- eliminable variables: diagonal-only Hessian row (elig, from the H
+  // pass), at most one general row, and alone in that row (otherwise K_ee
+  // would not be diagonal)
   for (int c = tid; c < n; c += nt) {
     if (!S.elig[c]) { S.egi[c] = -1; continue; }
     int cnt = 0, gs = -1;
@@ -708,41 +769,50 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.egi[c] = gs;  // temporarily indexed by column
     if (cnt > 1) S.elig[c] = 0;
   }
+  for (int gi = tid; gi < S.ng; gi += nt) S.ge[gi] = 0;
   __syncthreads();
-  for (int gi = tid; gi < S.ng; gi += nt) {  // rows meeting several candidates keep them all
-    int cnt = 0;
-    for (int c = 0; c < n; ++c) cnt += (S.elig[c] && S.egi[c] == gi) ? 1 : 0;
-    S.ge[gi] = cnt;
-  }
+  for (int c = tid; c < n; c += nt)  // rows meeting several candidates keep them all
+    if (S.elig[c] && S.egi[c] >= 0) atomicAdd(&S.ge[S.egi[c]], 1);
   __syncthreads();
   for (int c = tid; c < n; c += nt)
     if (S.elig[c] && S.egi[c] >= 0 && S.ge[S.egi[c]] > 1) S.elig[c] = 0;
   __syncthreads();
-  if (tid == 0) {
+  if (wid == 0) {
+    const unsigned lt = (1u << lane) - 1u;
+    for (int gi = lane; gi < S.ng; gi += 32) S.ge[gi] = -1;
+    __syncwarp();
     int nf = 0, ne = 0;
-    for (int gi = 0; gi < S.ng; ++gi) S.ge[gi] = -1;
-    for (int c = 0; c < n; ++c) {
-      if (S.elig[c]) {
-        const int gs = S.egi[c];
-        S.eidx[ne] = c;
-        S.hde[ne] = H[(int64_t)c * n + c];
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const int c = c0 + lane;
+      const bool el = c < n && S.elig[c] != 0;
+      const int gs = el ? S.egi[c] : -1;
+      const unsigned be = __ballot_sync(0xffffffffu, el);
+      const unsigned bk = __ballot_sync(0xffffffffu, c < n && !el);
+      if (el) {
+        const int e = ne + __popc(be & lt);
+        S.eidx[e] = c;
+        S.hde[e] = H[(int64_t)c * n + c];
         if (gs >= 0) {
           const double a = C[(int64_t)S.grow[gs] * n + c];
-          S.ge[gs] = ne;
+          S.ge[gs] = e;
           S.ga[gs] = a;
-          S.ea[ne] = a;
+          S.ea[e] = a;
         } else {
-          S.ea[ne] = 0.0;
+          S.ea[e] = 0.0;
         }
-        S.elig[ne] = gs;  // egi by eliminated index, staged (egi is column-indexed here)
-        ++ne;
-      } else {
-        S.kidx[nf++] = c;
+        S.elig[e] = gs;  // egi by eliminated index, staged (e <= c: slots already read)
+      } else if (c < n) {
+        S.kidx[nf + __popc(bk & lt)] = c;
       }
+      ne += __popc(be);
+      nf += __popc(bk);
+      __syncwarp();
     }
-    for (int e = 0; e < ne; ++e) S.egi[e] = S.elig[e];
-    sh_int[2] = nf;
-    sh_int[3] = ne;
+    for (int e = lane; e < ne; e += 32) S.egi[e] = S.elig[e];
+    if (lane == 0) {
+      sh_int[2] = nf;
+      sh_int[3] = ne;
+    }
   }
   __syncthreads();
   S.nf = sh_int[2];
@@ -786,8 +856,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   __syncthreads();
 
   // scale references (qpsolver.py:124-127)
-  double hmax = 0.0, gmax = 0.0;
-  for (int t = tid; t < n * n; t += nt) hmax = fmax(hmax, fabs(H[t]));
+  double hmax = hmax_loc, gmax = 0.0;
   for (int t = tid; t < n; t += nt) gmax = fmax(gmax, fabs(S.g[t]));
   hmax = block_reduce<0>(hmax, red);
   gmax = block_reduce<0>(gmax, red);
