@@ -337,7 +337,7 @@ def ours_arm(args, world, rank, local):
                           "note": "stage time incl. constraint rows/soft expansion; Gamma is L2-resident at cfg3; "
                                   "H and g accumulate on tcgen05 (3xTF32) inside the recursion kernel"},
         "linearize": {"bound": "fp32/fp64 SIMT", "ms": lin,
-                      "kernels": "k_fwd_chain (psi, phi; fp64), k_jac_phi, k_jac_psi (fp32), k_lin_self, k_lin_c, k_lin_f",
+                      "kernels": "k_fwd_chain (psi, phi; fp64), k_jac_phi_tc, k_jac_psi_tc (tcgen05 3xTF32), k_lin_self, k_lin_c, k_lin_f",
                         "achieved": LIN_FLOPS_CFG3 / (lin * 1e-3) / 1e12 if (M, N) == (1000, 20) else None,
                         "unit": "TFLOP/s", "traffic": NCU_TRAFFIC.get("linearize")},
     }
