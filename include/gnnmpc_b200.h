@@ -121,9 +121,10 @@ int gm_linearize(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
 /* Linearisation kernel selection: 0 = automatic (fused per-tile kernel for
  * fewer than 8k node points with the reference architecture, layer-wise
  * chain above), 1 = always the fused kernel, 2 = always the layer-wise chain
- * (Jacobian chains fused per row for the reference architecture, the phi
- * Jacobian on tcgen05), 3 = layer-wise with one launch per Jacobian layer,
- * 4 = as 2 with the phi Jacobian as a per-row SIMT chain.  All compute the
+ * (forward and Jacobian chains fused per row for the reference
+ * architecture: forward passes on fp64 DMMA, Jacobian chains on tcgen05),
+ * 3 = layer-wise with one launch per layer, 4 = as 2 with every chain as a
+ * per-row SIMT kernel.  All compute the
  * same formulas; the switch exists for tests and benchmarks. */
 int gm_set_linearize_mode(gm_ctx* ctx, int mode);
 

@@ -826,6 +826,168 @@ struct NodeRows {
   }
 };
 
+// The same fp64 forward chain on the fp64 tensor cores (DMMA, mma.sync
+// m8n8k4 f64: tcgen05 has no fp64 kind).  One warp per 8-row tile: lanes
+// 0..7 form the input rows into a per-warp shared tile, each layer is
+// (D_in/4) x (D_out/8) DMMAs with the weights pre-arranged in shared memory
+// in B-fragment order (one conflict-free 8-byte load per DMMA), bias in the
+// accumulator, ReLU + mask bytes applied on the C fragment and the hidden row
+// re-staged as the next layer's A tile; mask bytes leave through a per-warp
+// staging buffer as 16-byte stores.  Accumulators take 16 registers instead of
+// the 64-double hidden row of k_fwd_chain (244 registers, 12.5 % occupancy).
+constexpr int kFMT = 256;
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+template <int D0, int D1, int D2, int D3>
+struct FwdMma {
+  static constexpr int K0 = (D0 + 3) / 4 * 4;               // padded input width
+  static constexpr int N3 = (D3 + 7) / 8 * 8;               // padded output width
+  static constexpr int S0 = K0 | 4, SH = (D1 > D2 ? D1 : D2) | 4;  // row strides (bank spread)
+  static constexpr int HM = D1 + D2;                        // mask bytes per row
+  static constexpr int F0 = K0 * D1, F1 = D1 * D2, F2 = D2 * N3;   // B-fragment doubles
+  static constexpr int WARP_D = 8 * S0 + 8 * SH;            // per-warp doubles
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(F0 + F1 + F2 + D1 + D2 + N3 + (kFMT / 32) * WARP_D) +
+                                 (size_t)(kFMT / 32) * 8 * HM;
+};
+// B fragment order: Bf[(s * NT + j) * 32 + l] = W^T[4s + l % 4][8j + l / 4]
+__device__ __forceinline__ void frag_fill(double* bf, const double* wt, int K, int N, int KP, int NP) {
+  const int NT = NP / 8;
+  for (int t = threadIdx.x; t < KP * NP; t += blockDim.x) {
+    const int l = t & 31, sj = t >> 5, s4 = sj / NT, j = sj - s4 * NT;
+    const int k = 4 * s4 + (l & 3), n = 8 * j + (l >> 2);
+    bf[t] = (k < K && n < N) ? wt[k * N + n] : 0.0;
+  }
+}
+template <int D0, int D1, int D2, int D3, typename Rows>
+__global__ void __launch_bounds__(kFMT) k_fwd_chain_mma(int R, const Rows rows,
+                                                        const double* __restrict__ w0, const double* __restrict__ b0,
+                                                        const double* __restrict__ w1, const double* __restrict__ b1,
+                                                        const double* __restrict__ w2, const double* __restrict__ b2,
+                                                        uint8_t* __restrict__ mask, int hmask,
+                                                        double* __restrict__ out, int ldo) {
+  using T = FwdMma<D0, D1, D2, D3>;
+  static_assert(D1 % 8 == 0 && D2 % 8 == 0 && T::HM % 16 == 0, "hidden widths: multiples of 8, masks of 16 B");
+  extern __shared__ __align__(16) double fm[];
+  double* bf0 = fm;
+  double* bf1 = bf0 + T::F0;
+  double* bf2 = bf1 + T::F1;
+  double* sb0 = bf2 + T::F2;
+  double* sb1 = sb0 + D1;
+  double* sb2 = sb1 + D2;
+  double* wbase = sb2 + T::N3;
+  frag_fill(bf0, w0, D0, D1, T::K0, D1);
+  frag_fill(bf1, w1, D1, D2, D1, D2);
+  frag_fill(bf2, w2, D2, D3, D2, T::N3);
+  for (int t = threadIdx.x; t < D1; t += kFMT) sb0[t] = b0[t];
+  for (int t = threadIdx.x; t < D2; t += kFMT) sb1[t] = b1[t];
+  for (int t = threadIdx.x; t < T::N3; t += kFMT) sb2[t] = t < D3 ? b2[t] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* xs = wbase + wid * T::WARP_D;
+  double* hs = xs + 8 * T::S0;
+  uint8_t* ms = reinterpret_cast<uint8_t*>(wbase + (kFMT / 32) * T::WARP_D) + wid * 8 * T::HM;
+  const int gr = lane >> 2, gc = lane & 3;
+  const int64_t nwarps = (int64_t)gridDim.x * (kFMT / 32);
+  for (int64_t tile = (int64_t)blockIdx.x * (kFMT / 32) + wid; tile * 8 < R; tile += nwarps) {
+    const int r0 = (int)(tile * 8);
+    if (lane < 8) {
+      double x[D0];
+      if (r0 + lane < R) {
+        rows(r0 + lane, x);
+      } else {
+#pragma unroll
+        for (int k = 0; k < D0; ++k) x[k] = 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < T::K0; ++k) xs[lane * T::S0 + k] = k < D0 ? x[k] : 0.0;
+    }
+    __syncwarp();
+    // layer 0 -> hs (ReLU), mask bytes [0, D1)
+    {
+      double acc[D1 / 8][2];
+#pragma unroll
+      for (int j = 0; j < D1 / 8; ++j) {
+        acc[j][0] = sb0[8 * j + 2 * gc];
+        acc[j][1] = sb0[8 * j + 2 * gc + 1];
+      }
+#pragma unroll
+      for (int s4 = 0; s4 < T::K0 / 4; ++s4) {
+        const double a = xs[gr * T::S0 + 4 * s4 + gc];
+#pragma unroll
+        for (int j = 0; j < D1 / 8; ++j) dmma_f64(acc[j][0], acc[j][1], a, bf0[(s4 * (D1 / 8) + j) * 32 + lane]);
+      }
+#pragma unroll
+      for (int j = 0; j < D1 / 8; ++j) {
+        const int c = 8 * j + 2 * gc;
+        const bool m0 = acc[j][0] > 0.0, m1 = acc[j][1] > 0.0;
+        *reinterpret_cast<double2*>(hs + gr * T::SH + c) = make_double2(m0 ? acc[j][0] : 0.0, m1 ? acc[j][1] : 0.0);
+        *reinterpret_cast<uint16_t*>(ms + gr * T::HM + c) = (uint16_t)((m0 ? 1u : 0u) | (m1 ? 256u : 0u));
+      }
+    }
+    __syncwarp();
+    // layer 1 -> hs (ReLU), mask bytes [D1, D1 + D2)
+    {
+      double acc[D2 / 8][2];
+#pragma unroll
+      for (int j = 0; j < D2 / 8; ++j) {
+        acc[j][0] = sb1[8 * j + 2 * gc];
+        acc[j][1] = sb1[8 * j + 2 * gc + 1];
+      }
+#pragma unroll
+      for (int s4 = 0; s4 < D1 / 4; ++s4) {
+        const double a = hs[gr * T::SH + 4 * s4 + gc];
+#pragma unroll
+        for (int j = 0; j < D2 / 8; ++j) dmma_f64(acc[j][0], acc[j][1], a, bf1[(s4 * (D2 / 8) + j) * 32 + lane]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < D2 / 8; ++j) {
+        const int c = 8 * j + 2 * gc;
+        const bool m0 = acc[j][0] > 0.0, m1 = acc[j][1] > 0.0;
+        *reinterpret_cast<double2*>(hs + gr * T::SH + c) = make_double2(m0 ? acc[j][0] : 0.0, m1 ? acc[j][1] : 0.0);
+        *reinterpret_cast<uint16_t*>(ms + gr * T::HM + D1 + c) = (uint16_t)((m0 ? 1u : 0u) | (m1 ? 256u : 0u));
+      }
+    }
+    __syncwarp();
+    // output layer
+    {
+      double acc[T::N3 / 8][2];
+#pragma unroll
+      for (int j = 0; j < T::N3 / 8; ++j) {
+        acc[j][0] = sb2[8 * j + 2 * gc];
+        acc[j][1] = sb2[8 * j + 2 * gc + 1];
+      }
+#pragma unroll
+      for (int s4 = 0; s4 < D2 / 4; ++s4) {
+        const double a = hs[gr * T::SH + 4 * s4 + gc];
+#pragma unroll
+        for (int j = 0; j < T::N3 / 8; ++j)
+          dmma_f64(acc[j][0], acc[j][1], a, bf2[(s4 * (T::N3 / 8) + j) * 32 + lane]);
+      }
+      if (r0 + gr < R) {
+        double* orow = out + (int64_t)(r0 + gr) * ldo;
+#pragma unroll
+        for (int j = 0; j < T::N3 / 8; ++j)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int c = 8 * j + 2 * gc + q;
+            if (c < D3) orow[c] = acc[j][q];
+          }
+      }
+    }
+    // mask rows (contiguous 8 x HM bytes, hmask == HM) as 16-byte stores
+    constexpr int V = 8 * T::HM / 16;
+    const int valid = min(8, R - r0);
+    for (int v = lane; v < V; v += 32)
+      if (v * 16 < valid * T::HM)
+        reinterpret_cast<uint4*>(mask + (int64_t)r0 * hmask)[v] = reinterpret_cast<const uint4*>(ms)[v];
+    __syncwarp();
+  }
+}
+
 // rows (R, D0) -> hidden D1 (mask) -> hidden D2 (mask) -> out (R, D3)
 template <int D0, int D1, int D2, int D3, typename Rows>
 __global__ void __launch_bounds__(kJT) k_fwd_chain(int R, const Rows rows,
@@ -975,10 +1137,22 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   if (d.Re > 0 && fused) {
     const size_t sm = fwd_chain_smem<6, 32, 32, 16>();
     const EdgeRows rows{d, ctx->d_dst, ctx->d_src, X, ctx->d_norm};
+    if (ctx->lin_mode != 4 && hpsi == FwdMma<6, 32, 32, 16>::HM) {
+      using F = FwdMma<6, 32, 32, 16>;
+      GM_CUDA(ctx, cudaFuncSetAttribute(k_fwd_chain_mma<6, 32, 32, 16, EdgeRows>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM));
+      const unsigned grid = (unsigned)std::min<int64_t>((d.Re + 8 * (kFMT / 32) - 1) / (8 * (kFMT / 32)),
+                                                        (int64_t)ctx->sm_count * 8);
+      k_fwd_chain_mma<6, 32, 32, 16><<<grid, kFMT, F::SMEM, st>>>(d.Re, rows, psi.wt64[0], psi.b64[0], psi.wt64[1],
+                                                                  psi.b64[1], psi.wt64[2], psi.b64[2], mpsi, hpsi,
+                                                                  ha, pld(16));
+      GM_LAUNCH_CHECK(ctx, "k_fwd_chain_mma");
+    } else {
     k_fwd_chain<6, 32, 32, 16><<<chain_grid(d.Re, ctx->sm_count), kJT, sm, st>>>(
         d.Re, rows, psi.wt64[0], psi.b64[0], psi.wt64[1], psi.b64[1], psi.wt64[2], psi.b64[2], mpsi, hpsi, ha,
         pld(16));
     GM_LAUNCH_CHECK(ctx, "k_fwd_chain");
+    }
     msg = ha;
     ldmsg = pld(16);
   } else if (d.Re > 0) {
@@ -1016,10 +1190,22 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
     GM_CUDA(ctx, cudaFuncSetAttribute(k_fwd_chain<28, 64, 64, 3, NodeRows>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const NodeRows rows{d, ctx->d_ptr, X, U, ctx->d_norm, msg, ldmsg};
+    if (ctx->lin_mode != 4 && hphi == FwdMma<28, 64, 64, 3>::HM) {
+      using F = FwdMma<28, 64, 64, 3>;
+      GM_CUDA(ctx, cudaFuncSetAttribute(k_fwd_chain_mma<28, 64, 64, 3, NodeRows>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM));
+      const unsigned grid = (unsigned)std::min<int64_t>((d.Rn + 8 * (kFMT / 32) - 1) / (8 * (kFMT / 32)),
+                                                        (int64_t)ctx->sm_count * 2);
+      k_fwd_chain_mma<28, 64, 64, 3><<<grid, kFMT, F::SMEM, st>>>(d.Rn, rows, phi.wt64[0], phi.b64[0], phi.wt64[1],
+                                                                  phi.b64[1], phi.wt64[2], phi.b64[2], mphi, hphi,
+                                                                  pbuf[0], pld(3));
+      GM_LAUNCH_CHECK(ctx, "k_fwd_chain_mma");
+    } else {
     k_fwd_chain<28, 64, 64, 3><<<chain_grid(d.Rn, ctx->sm_count), kJT, sm, st>>>(
         d.Rn, rows, phi.wt64[0], phi.b64[0], phi.wt64[1], phi.b64[1], phi.wt64[2], phi.b64[2], mphi, hphi,
         pbuf[0], pld(3));
     GM_LAUNCH_CHECK(ctx, "k_fwd_chain");
+    }
     cur = pbuf[0];
     ldc = pld(3);
   }
@@ -1042,7 +1228,7 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
   if (phi.L == 1) {
     return gm_fail(ctx, GM_ERR_CONFIG, "single-layer phi is handled by the fused kernel");
   }
-  // tcgen05 phi Jacobian unless linearize mode 4 (per-row SIMT chain) is set
+  // tcgen05 phi Jacobian unless linearize mode 4 (per-row SIMT chains) is set
   if (fused && ctx->lin_mode != 4 && n_p <= 4) {
     using T = JacPhiTc<28, 64, 64>;
     static bool attr = false;

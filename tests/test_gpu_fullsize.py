@@ -30,8 +30,8 @@ def cfg3():
 @pytest.mark.parametrize("mode", [1, 2, 3, 4])
 def test_cfg3_stages(cfg3, mode):
     """mode 1: fused per-tile linearisation, 2: layer-wise with fused chains
-    (phi Jacobian on tcgen05), 3: per-layer GEMM chain, 4: as 2 with the SIMT
-    phi Jacobian."""
+    (forward on fp64 DMMA, Jacobians on tcgen05), 3: per-layer GEMM chain,
+    4: as 2 with the per-row SIMT chains."""
     import paper_2602_17601_b200 as pkg
 
     c = cfg3

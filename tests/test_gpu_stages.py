@@ -28,9 +28,9 @@ def pkg():
 
 
 def _set_lin_mode(pkg, cs, mode):
-    """Force the fused (1), layer-wise with fused Jacobian chains and the phi
-    Jacobian on tcgen05 (2), fully layer-wise (3) or layer-wise with the SIMT
-    phi Jacobian chain (4) linearisation kernels; 0 = auto."""
+    """Force the fused (1), layer-wise with fused chains (2: forward on fp64
+    DMMA, Jacobians on tcgen05), fully layer-wise (3) or layer-wise with the
+    per-row SIMT chains (4) linearisation kernels; 0 = auto."""
     pkg.device.engine(cs.topo, cs.model).ctx.call("gm_set_linearize_mode", mode)
 
 
