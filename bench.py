@@ -40,8 +40,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "MPC step latency ms (linearize+condense+QP) & Hz at N nodes; solves/sec batched"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the round's
-# `ncu --set full` captures at cfg3 (profiles/r01/ncu_full_summary_v7.txt)
-NCU_TRAFFIC = {"k_solve_qp": 757248, "linearize": None, "k_condense_tc": 39062528}
+# `ncu --set full` captures at cfg3 (profiles/r01/ncu_full_summary_v8.txt)
+NCU_TRAFFIC = {"k_solve_qp": 757760, "linearize": None, "k_condense_tc": 38191616}
 # sm__pipe_tensor_cycles_active (% of peak, active cycles) of K-COND's tcgen05
 # H/g accumulation from the same capture
 NCU_TENSOR_PCT = {"k_condense_tc": 4.62}
