@@ -44,7 +44,9 @@ METRIC = "MPC step latency ms (linearize+condense+QP) & Hz at N nodes; solves/se
 NCU_TRAFFIC = {"k_solve_qp": 757760, "linearize": None, "k_condense_tc": 38191616}
 # sm__pipe_tensor_cycles_active (% of peak, active cycles) of K-COND's tcgen05
 # H/g accumulation from the same capture
-NCU_TENSOR_PCT = {"k_condense_tc": 4.62}
+NCU_TENSOR_PCT = {"k_condense_tc": 4.62,
+                  # cfg3 (v8 / v7 captures): fp64 DMMA forward chain, tcgen05 Jacobians
+                  "linearize": {"k_fwd_chain_mma<phi>": 30.5, "k_jac_phi_tc": 8.4, "k_jac_psi_tc": 6.3}}
 # cfg3 linearize flops, psi-VJP formulation
 LIN_FLOPS_CFG3 = 1.53e9
 M_NODES, HORIZON = 1000, 20
@@ -336,10 +338,14 @@ def ours_arm(args, world, rank, local):
                                        "tensor_pipe_pct_ncu": NCU_TENSOR_PCT.get("k_condense_tc")},
                           "note": "stage time incl. constraint rows/soft expansion; Gamma is L2-resident at cfg3; "
                                   "H and g accumulate on tcgen05 (3xTF32) inside the recursion kernel"},
-        "linearize": {"bound": "fp32/fp64 SIMT", "ms": lin,
-                      "kernels": "k_fwd_chain (psi, phi; fp64), k_jac_phi_tc, k_jac_psi_tc (tcgen05 3xTF32), k_lin_self, k_lin_c, k_lin_f",
-                        "achieved": LIN_FLOPS_CFG3 / (lin * 1e-3) / 1e12 if (M, N) == (1000, 20) else None,
-                        "unit": "TFLOP/s", "traffic": NCU_TRAFFIC.get("linearize")},
+        "linearize": {"bound": "tensor (fp64 DMMA forward, tcgen05 3xTF32 Jacobians)", "ms": lin,
+                      "kernels": "k_fwd_chain_mma (psi, phi; fp64 DMMA), k_jac_phi_tc, k_jac_psi_tc (tcgen05 "
+                                 "3xTF32), k_lin_self, k_lin_c, k_lin_f",
+                      "achieved": LIN_FLOPS_CFG3 / (lin * 1e-3) / 1e12 if (M, N) == (1000, 20) else None,
+                      "unit": "TFLOP/s", "traffic": NCU_TRAFFIC.get("linearize"),
+                      "tensor_pipe_pct_ncu": NCU_TENSOR_PCT.get("linearize"),
+                      "note": "stage of 6 short launches (~0.12 ms at cfg3): launch/tail-bound; tensor pipe "
+                              "activity per kernel from ncu in tensor_pipe_pct_ncu"},
     }
     roof["traffic"] = NCU_TRAFFIC.get("k_solve_qp")
 
