@@ -190,10 +190,18 @@ __global__ void __launch_bounds__(256, 3) k_finish_states_pipe(const FinishArgs 
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   float4 v[NX];
   double coef[4];
+  // item -> (instance, node, stage) in 32-bit unsigned arithmetic (the host
+  // launches this kernel only for items < 2^31): the 64-bit divisions they
+  // replace were ~100 instructions each and bounded the kernel on issue
+  const unsigned N1 = (unsigned)(N + 1), Mu = (unsigned)M;
+  unsigned fk = 0, fgi = 0;
   auto fetch = [&](int64_t w) {
-    const int k = (int)(w % (N + 1));
-    const int64_t gi = w / (N + 1);
-    const int64_t bi = gi / M;
+    const unsigned wu = (unsigned)w;
+    fgi = wu / N1;
+    fk = wu - fgi * N1;
+    const int k = (int)fk;
+    const int64_t gi = fgi;
+    const int64_t bi = fgi / Mu;
     const int live = k * nu;
     const bool act = solved(A.status[bi]) && c0 < ld && (c0 < live || (xc >= c0 && xc < c0 + 4));
     const float* rows = A.W + ((gi * (N + 1) + k) * NX) * (int64_t)ld + c0;
@@ -219,12 +227,12 @@ __global__ void __launch_bounds__(256, 3) k_finish_states_pipe(const FinishArgs 
       s[q] = fma((double)v[q].z, coef[2], s[q]);
       s[q] = fma((double)v[q].w, coef[3], s[q]);
     }
+    const int k = (int)fk;
+    const unsigned gu = fgi, bu = gu / Mu;
+    const int64_t gi = gu, bi = bu;
+    const int i = (int)(gu - bu * Mu);
     if (w + nw < items) fetch(w + nw);
     const double p = butterfly8(s, lane);
-    const int k = (int)(w % (N + 1));
-    const int64_t gi = w / (N + 1);
-    const int i = (int)(gi % M);
-    const int64_t bi = gi / M;
     if (lane < NX) {
       const bool ok = solved(A.status[bi]);
       const int a = lane;
@@ -343,7 +351,7 @@ int gm_mpc_finish(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const d
     const char* e = std::getenv("GM_FIN_MODE");
     return e ? std::atoi(e) : -1;
   }();
-  if (ctx->nx == 6 && ld <= 128 && fin_mode != 0)
+  if (ctx->nx == 6 && ld <= 128 && fin_mode != 0 && items < (int64_t(1) << 31))
     k_finish_states_pipe<6><<<blocks, 256, 0, st>>>(a, items);
   else
     k_finish_states<<<blocks, 256, 0, st>>>(a, items);
