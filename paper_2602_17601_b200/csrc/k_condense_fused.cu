@@ -399,6 +399,29 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
 // is read back with tcgen05.ld into the same per-CTA pair-ordered partials
 // the SIMT kernel writes, so the fixed-order fp64 reduction is shared.
 // ---------------------------------------------------------------------------
+// Division by a per-item runtime divisor d >= 1 through its fp32 reciprocal
+// and one correction step: exact for 0 <= t < 2^22 (every dividend below is
+// a (node, column) index of one item, < 16 x 129).  ~6 instructions instead
+// of the ~20 of an integer division; the item loops issue several per item.
+struct FDiv {
+  int d;
+  float r;
+};
+__device__ __forceinline__ FDiv fdiv_make(int d) { return FDiv{d, d > 0 ? __frcp_rn((float)d) : 0.f}; }
+__device__ __forceinline__ int fdiv(const FDiv& f, int t, int& rem) {
+  int q = __float2int_rz(__int2float_rn(t) * f.r);
+  int r = t - q * f.d;
+  if (r < 0) {
+    --q;
+    r += f.d;
+  } else if (r >= f.d) {
+    ++q;
+    r -= f.d;
+  }
+  rem = r;
+  return q;
+}
+
 template <int NX, int NU>
 __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -463,8 +486,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
   // stage operands of item j: 16-byte cp.async for every contiguous segment
   // (a_self, a_nbr, b, c of the chunk; Q and x_ref per node), 4-byte for the
   // edge sources
-  auto prefetch = [&](int j) {
-    const int n = j / nsub, s0 = nb + (j % nsub) * SC;
+  auto prefetch = [&](int j, int n, int sub) {
+    const int s0 = nb + sub * SC;
     const int sc = min(SC, ne - s0), k = n + 1;
     const Stage<NX, NU> S = stage_at<NX, NU>(smraw + (j & 1) * sbytes, SC, emax);
     const int64_t pstage = bi * N + n;
@@ -504,13 +527,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     cp_async_commit();
   };
   const int items = N * nsub;
-  if (items > 0) prefetch(0);
+  if (items > 0) prefetch(0, 0, 0);
 
   // stage 0: Gamma_u = 0, Gamma_x = x0 (condensing.py:205-206)
-  for (int t = tid; rec && t < nn * NX * ld; t += nt) {
-    const int li = t / (NX * ld), rem = t - li * NX * ld, r = rem / ld, col = rem - r * ld;
-    Wb[(int64_t)(nb + li) * node_stride + rem] =
-        (col == XC) ? (float)a.x0[(bi * M + nb + li) * NX + r] : 0.f;
+  for (int row = warp; rec && row < nn * NX; row += nt >> 5) {
+    const int li = row / NX, r = row - li * NX;
+    float* Wr0 = Wb + (int64_t)(nb + li) * node_stride + (int64_t)r * ld;
+    const float x0v = (float)a.x0[(bi * M + nb + li) * NX + r];
+    for (int col = tid & 31; col < ld; col += 32) Wr0[col] = (col == XC) ? x0v : 0.f;
   }
   const int d0 = rec ? a.dep_ptr[split] : 0, d1 = rec ? a.dep_ptr[split + 1] : 0;
   __syncthreads();
@@ -519,8 +543,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     st_release(&flags[split], 1);
   }
 
-  for (int j = 0; j < items; ++j) {
-    const int n = j / nsub, sub = j % nsub;
+  for (int j = 0, n = 0, sub = 0; j < items; ++j, n += (sub + 1 == nsub), sub = (sub + 1 == nsub) ? 0 : sub + 1) {
     const int s0 = nb + sub * SC, sc = min(SC, ne - s0);
     const int k = n + 1;
     const int live = n * NU;
@@ -533,7 +556,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     }
     cp_async_wait_all();
     __syncthreads();
-    if (j + 1 < items) prefetch(j + 1);
+    if (j + 1 < items) prefetch(j + 1, sub + 1 == nsub ? n + 1 : n, sub + 1 == nsub ? 0 : sub + 1);
     for (int t = tid; t < sc * NX * NX; t += nt) {
       const int li = t / (NX * NX), e = t - li * NX * NX, r = e / NX, cc = e - r * NX;
       const double* Qk = S.qd + li * NX * NX;
@@ -548,8 +571,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     // the live columns, the B block and Gamma_x of stage k
     const int nlive = rec ? live : live + NU;
     const int lw = nlive + 1;
+    const FDiv flw = fdiv_make(lw);
     for (int t = tid, it = 0; t < sc * lw; t += nt, ++it) {
-      const int li = t / lw, cc = t - li * lw;
+      int cc;
+      const int li = fdiv(flw, t, cc);
       const int col = cc < nlive ? cc : XC;
       const int i = s0 + li;
       float r6[NX];
@@ -637,8 +662,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     // operand buffers hold zeros beyond the live columns already)
     operands_free();
     const int nz = rec ? ld - lw : 0;
+    const FDiv fnz = fdiv_make(nz);
     for (int t = tid; t < sc * nz; t += nt) {
-      const int li = t / nz, cc = t - li * nz;
+      int cc;
+      const int li = fdiv(fnz, t, cc);
       int col = live + cc;
       if (col >= XC) ++col;
       const int i = s0 + li;
@@ -680,7 +707,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     if (rec && a.reg_prefetch && sub + 1 < nsub) {
       const int s0n = s0 + SC, scn = min(SC, ne - s0n);
       if (tid < scn * lw) {
-        const int li = tid / lw, cc = tid - li * lw;
+        int cc;
+        const int li = fdiv(flw, tid, cc);
         const int col = cc < live ? cc : XC;
         const int i = s0n + li;
         const int e0 = nptr[i - nb], deg = nptr[i - nb + 1] - e0;
@@ -699,8 +727,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     }
     // Qs G on the live columns of stage k -> B operand; w = 2 Q Gamma_x - 2 Q x_ref
     const int lk = k * NU;
+    const FDiv flk = fdiv_make(lk);
     for (int t = tid; t < SC * lk; t += nt) {
-      const int li = t / lk, col = t - li * lk;
+      int col;
+      const int li = fdiv(flk, t, col);
       float gcol[NX], o[NX];
       umma::getn<NX>(g_hi, g_lo, col, li * NX, sbo, gcol);
       const float4* Qn4 = (const float4*)(Qs + li * NX * NX);
