@@ -783,7 +783,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_condense_tc(const FusedArgs a
     }
     pending = true;
     issued = true;
-    __syncthreads();
+    // no barrier here: the next item's loop-top barrier orders the MMA issue
+    // before any operand rewrite (each thread also waits on the mbarrier)
   }
   if (pending) {
     umma::mbar_wait(mbar, phase);
