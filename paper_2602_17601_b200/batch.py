@@ -112,17 +112,18 @@ class BatchedMpc:
         self.settings_c = cfg.solver.as_c()
         self.graph = None
 
-    def load(self, x_measured, lin_states, lin_inputs, x_ref):
+    def load(self, x_measured, lin_states, lin_inputs, x_ref, non_blocking: bool = False):
         """Copy the step's inputs (numpy or tensors) into the device buffers:
         x_measured (B, M, nx), lin_states (B, N+1, M, nx), lin_inputs (B, N, nu),
-        x_ref (B, M, N+1, nx)."""
+        x_ref (B, M, N+1, nx).  ``non_blocking`` makes copies from pinned host
+        tensors asynchronous on the current stream (WavePipeline)."""
         torch = self.eng.torch
         for dst, src in ((self.x0, x_measured), (self.X, lin_states), (self.U, lin_inputs),
                          (self.xref, x_ref)):
             if isinstance(src, np.ndarray):
                 dst.copy_(torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64)))
             else:
-                dst.copy_(src)
+                dst.copy_(src, non_blocking=non_blocking)
         self.X[:, 0].copy_(self.x0)  # measurement at stage 0 (mpc.py:120-122)
 
     def enqueue(self):
@@ -181,3 +182,66 @@ class BatchedMpc:
                            status=[STATUS_BY_CODE[int(s)] for s in summ[:, nu]],
                            iterations=summ[:, nu + 1].astype(int),
                            next_states=self.next_states, next_inputs=self.next_inputs)
+
+
+class WavePipeline:
+    """A batch run as back-to-back waves of :class:`BatchedMpc`, each wave's
+    host->device input copy overlapped with the previous wave's kernels.
+
+    Two BatchedMpc buffer sets per wave size alternate: wave w's inputs are
+    copied on a side stream into the set wave w-1 is not using (after that
+    set's previous wave has finished), the compute stream waits for the copy,
+    runs the wave and queues the D2H of its summary into a per-wave pinned
+    buffer; one host synchronisation per :meth:`step`.  Results equal
+    ``[BatchedMpc.step(*inp) for inp in inputs]`` wave by wave (same kernels
+    on the same data); ``next_states`` / ``next_inputs`` are device copies
+    owned by the result."""
+
+    def __init__(self, model, topo, spec, cfg: MpcConfig, sizes, device=None):
+        self.sizes = [int(n) for n in sizes]
+        self.sets = {n: [BatchedMpc(model, topo, spec, cfg, n, device) for _ in range(2)]
+                     for n in sorted(set(self.sizes))}
+        first = next(iter(self.sets.values()))[0]
+        self.torch = torch = first.eng.torch
+        self.device = first.eng.device
+        self.nu = first.nu
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.summ = [torch.empty((n, self.nu + 2), dtype=torch.float64).pin_memory() for n in self.sizes]
+        self.done = {}
+
+    def step(self, inputs) -> list:
+        """inputs: one (x_measured, lin_states, lin_inputs, x_ref) tuple of
+        pinned host tensors per wave, shaped for that wave's size."""
+        torch = self.torch
+        if len(inputs) != len(self.sizes):
+            raise ValueError(f"expected {len(self.sizes)} waves of inputs, got {len(inputs)}")
+        cs = torch.cuda.current_stream(self.device)
+        turn = {n: 0 for n in self.sets}
+        nexts = []
+        for w, (n, inp) in enumerate(zip(self.sizes, inputs)):
+            bm = self.sets[n][turn[n] & 1]
+            turn[n] += 1
+            with torch.cuda.stream(self.copy_stream):
+                prev = self.done.get(id(bm))
+                if prev is not None:
+                    self.copy_stream.wait_event(prev)  # the set's previous wave is finished
+                bm.load(*inp, non_blocking=True)
+                loaded = torch.cuda.Event()
+                loaded.record(self.copy_stream)
+            cs.wait_event(loaded)
+            bm.enqueue()
+            self.summ[w].copy_(bm.summary, non_blocking=True)
+            nexts.append((bm.next_states.clone(), bm.next_inputs.clone()))
+            done = torch.cuda.Event()
+            done.record(cs)
+            self.done[id(bm)] = done
+        cs.synchronize()
+        out = []
+        for w, (ns, ni) in enumerate(nexts):
+            summ = self.summ[w].numpy()
+            nu = self.nu
+            out.append(BatchResult(u_applied=summ[:, :nu].copy(),
+                                   status=[STATUS_BY_CODE[int(s)] for s in summ[:, nu]],
+                                   iterations=summ[:, nu + 1].astype(int),
+                                   next_states=ns, next_inputs=ni))
+        return out

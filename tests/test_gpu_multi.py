@@ -44,6 +44,43 @@ def test_batched_step_matches_oracle_per_instance():
         assert np.max(np.abs(nxt[b] - ref["lin_states"])) / np.max(np.abs(ref["lin_states"])) <= 1e-4
 
 
+def test_wave_pipeline_matches_batched_step():
+    """WavePipeline (H2D of wave w on a side stream under wave w-1's kernels)
+    gives the same per-wave results as BatchedMpc.step, over two passes so
+    both buffer sets of each size are reused."""
+    import torch
+
+    import paper_2602_17601_b200 as pkg
+    from paper_2602_17601_b200 import workloads
+    from paper_2602_17601_b200.batch import BatchedMpc, WavePipeline
+
+    M, N = 12, 8
+    sizes = [3, 3, 2, 3]
+    topo, model, _, _, spec = workloads.scaling_problem(M, N, 0.01, 0)
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+    waves, i0 = [], 0
+    for n in sizes:
+        xs, ls, li, xr = [], [], [], []
+        for b in range(i0, i0 + n):
+            st, inp = workloads.batch_instance(b, M, N)
+            xs.append(st[0])
+            ls.append(np.concatenate([st, st[-1:]], axis=0))
+            li.append(inp)
+            xr.append(np.repeat(st[0][:, None, :], N + 1, axis=1))
+        waves.append(tuple(torch.from_numpy(np.stack(v)).pin_memory() for v in (xs, ls, li, xr)))
+        i0 += n
+    ref = [BatchedMpc(model, topo, spec, cfg, n).step(*w) for n, w in zip(sizes, waves)]
+    pipe = WavePipeline(model, topo, spec, cfg, sizes)
+    for _ in range(2):
+        got = pipe.step(waves)
+        for r, g in zip(ref, got):
+            assert [s.value for s in g.status] == [s.value for s in r.status]
+            np.testing.assert_array_equal(g.iterations, r.iterations)
+            np.testing.assert_array_equal(g.u_applied, r.u_applied)
+            np.testing.assert_array_equal(g.next_states.cpu().numpy(), r.next_states.cpu().numpy())
+            np.testing.assert_array_equal(g.next_inputs.cpu().numpy(), r.next_inputs.cpu().numpy())
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
