@@ -288,7 +288,12 @@ __device__ void c_apply(const Qs& S, const double* xv, double* out) {
 // partials of the warps meet in the (free at this point) K tile region and
 // are added in a fixed order.  Call with all threads; out is complete after
 // the call's final barrier.
+__device__ void h_apply_rows(const Qs& S, const double* uv, double* out);
 __device__ void h_apply(const Qs& S, const double* uv, double* out) {
+  if (__isShared(S.Hp) && S.nf <= (int)blockDim.x) {
+    h_apply_rows(S, uv, out);
+    return;
+  }
   constexpr int TM = 8;  // n <= 256
   const int n = S.nf, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* part = S.K;                      // NW x n row partials
@@ -343,6 +348,39 @@ __device__ void h_apply(const Qs& S, const double* uv, double* out) {
 #pragma unroll
     for (int w = 0; w < kQpWarps; ++w) v += part[w * n + r];
     out[S.kidx[r]] = v;
+  }
+  for (int e = threadIdx.x; e < S.ne; e += blockDim.x) out[S.eidx[e]] = S.hde[e] * uv[S.eidx[e]];
+  __syncthreads();
+}
+
+// out = H u with packed H on chip: one thread per kept row r, the row read
+// as column r's lower part below the diagonal (H[c][r], consecutive rows ->
+// consecutive words) and column r itself above it, four independent
+// accumulators; no shuffles or cross-warp partials (the warp-per-column form
+// above is for H left in global memory, where it batches the L2 round trips).
+__device__ void h_apply_rows(const Qs& S, const double* uv, double* out) {
+  const int n = S.nf, r = threadIdx.x;
+  const double* Hp = S.Hp;
+  QP_SMEM(Hp);
+  if (r < n) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int c = 0;
+    for (; c + 3 < r; c += 4) {
+      a0 = fma(Hp[colbase(c, n) + r], uv[S.kidx[c]], a0);
+      a1 = fma(Hp[colbase(c + 1, n) + r], uv[S.kidx[c + 1]], a1);
+      a2 = fma(Hp[colbase(c + 2, n) + r], uv[S.kidx[c + 2]], a2);
+      a3 = fma(Hp[colbase(c + 3, n) + r], uv[S.kidx[c + 3]], a3);
+    }
+    for (; c < r; ++c) a0 = fma(Hp[colbase(c, n) + r], uv[S.kidx[c]], a0);
+    const double* colr = Hp + colbase(r, n);
+    for (; c + 3 < n; c += 4) {
+      a0 = fma(colr[c], uv[S.kidx[c]], a0);
+      a1 = fma(colr[c + 1], uv[S.kidx[c + 1]], a1);
+      a2 = fma(colr[c + 2], uv[S.kidx[c + 2]], a2);
+      a3 = fma(colr[c + 3], uv[S.kidx[c + 3]], a3);
+    }
+    for (; c < n; ++c) a0 = fma(colr[c], uv[S.kidx[c]], a0);
+    out[S.kidx[r]] = (a0 + a1) + (a2 + a3);
   }
   for (int e = threadIdx.x; e < S.ne; e += blockDim.x) out[S.eidx[e]] = S.hde[e] * uv[S.eidx[e]];
   __syncthreads();
