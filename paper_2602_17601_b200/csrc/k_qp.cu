@@ -290,7 +290,7 @@ __device__ void c_apply(const Qs& S, const double* xv, double* out) {
 // the call's final barrier.
 __device__ void h_apply_rows(const Qs& S, const double* uv, double* out);
 __device__ void h_apply(const Qs& S, const double* uv, double* out) {
-  if (__isShared(S.Hp) && S.nf <= (int)blockDim.x) {
+  if (__isShared(S.Hp) && S.nf <= (int)blockDim.x && uv != out) {
     h_apply_rows(S, uv, out);
     return;
   }
@@ -362,26 +362,37 @@ __device__ void h_apply_rows(const Qs& S, const double* uv, double* out) {
   const int n = S.nf, r = threadIdx.x;
   const double* Hp = S.Hp;
   QP_SMEM(Hp);
+  // kept part of u gathered into out (out != uv; rewritten below) so the
+  // row loops read it directly instead of through kidx
+  double* uk = out;
+  double uv_r = 0.0;
+  if (r < n) uv_r = uv[S.kidx[r]];
+  __syncthreads();
+  if (r < n) uk[r] = uv_r;
+  __syncthreads();
+  double acc = 0.0;
   if (r < n) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int c = 0;
     for (; c + 3 < r; c += 4) {
-      a0 = fma(Hp[colbase(c, n) + r], uv[S.kidx[c]], a0);
-      a1 = fma(Hp[colbase(c + 1, n) + r], uv[S.kidx[c + 1]], a1);
-      a2 = fma(Hp[colbase(c + 2, n) + r], uv[S.kidx[c + 2]], a2);
-      a3 = fma(Hp[colbase(c + 3, n) + r], uv[S.kidx[c + 3]], a3);
+      a0 = fma(Hp[colbase(c, n) + r], uk[c], a0);
+      a1 = fma(Hp[colbase(c + 1, n) + r], uk[c + 1], a1);
+      a2 = fma(Hp[colbase(c + 2, n) + r], uk[c + 2], a2);
+      a3 = fma(Hp[colbase(c + 3, n) + r], uk[c + 3], a3);
     }
-    for (; c < r; ++c) a0 = fma(Hp[colbase(c, n) + r], uv[S.kidx[c]], a0);
+    for (; c < r; ++c) a0 = fma(Hp[colbase(c, n) + r], uk[c], a0);
     const double* colr = Hp + colbase(r, n);
     for (; c + 3 < n; c += 4) {
-      a0 = fma(colr[c], uv[S.kidx[c]], a0);
-      a1 = fma(colr[c + 1], uv[S.kidx[c + 1]], a1);
-      a2 = fma(colr[c + 2], uv[S.kidx[c + 2]], a2);
-      a3 = fma(colr[c + 3], uv[S.kidx[c + 3]], a3);
+      a0 = fma(colr[c], uk[c], a0);
+      a1 = fma(colr[c + 1], uk[c + 1], a1);
+      a2 = fma(colr[c + 2], uk[c + 2], a2);
+      a3 = fma(colr[c + 3], uk[c + 3], a3);
     }
-    for (; c < n; ++c) a0 = fma(colr[c], uv[S.kidx[c]], a0);
-    out[S.kidx[r]] = (a0 + a1) + (a2 + a3);
+    for (; c < n; ++c) a0 = fma(colr[c], uk[c], a0);
+    acc = (a0 + a1) + (a2 + a3);
   }
+  __syncthreads();
+  if (r < n) out[S.kidx[r]] = acc;
   for (int e = threadIdx.x; e < S.ne; e += blockDim.x) out[S.eidx[e]] = S.hde[e] * uv[S.eidx[e]];
   __syncthreads();
 }
