@@ -15,8 +15,10 @@ instance from the same initial controller state (identical work every step):
              the kernels, D2H of [u_applied, status, iterations], wall clock.
 * roofline   the dominant kernel (per-launch CUDA-event time inside the timed
              region) against its hardware ceiling.
-* cpu_baseline / --impl reference: the CPU oracle port of the reference path
-  (oracle/ref_port.py; the reference is pure Python and is not on the GPU box).
+* cpu_baseline / --impl reference: the reference's own CPU path -- the
+  unmodified package installed in baseline/_ref (pip --target), called
+  through its public mpc_step; the oracle port (oracle/ref_port.py) only when
+  that install is missing.
 
 Multi-GPU (torchrun): every rank solves its own independent instance (weak
 scaling, no data-path collective); timing is max over ranks.
@@ -110,22 +112,76 @@ def cpu_oracle_steps(M, N, steps, warmup, threads):
     return float(np.mean(times)) * 1e3
 
 
+def import_reference():
+    """The unmodified reference package installed in baseline/_ref (pip
+    --target), or None when it is not there."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "gnnmpc" / "mpc.py").exists():
+        return None
+    sys.path.insert(0, str(ref))
+    try:
+        import gnnmpc.experiments as rex
+        import gnnmpc.graph as rgr
+        import gnnmpc.mpc as rm
+    finally:
+        sys.path.remove(str(ref))
+    return rex, rgr, rm
+
+
+def reference_steps(M, N, steps, warmup, threads):
+    """Stock reference mpc_step (gnnmpc.mpc, mpc.py:102-200) on the
+    reference's own _scaling_problem (experiments.py:465-489), from the same
+    initial controller state every step (the work of our arm's step).
+    Returns (ms per step, status, iterations)."""
+    from threadpoolctl import threadpool_limits
+
+    rex, rgr, rm = import_reference()
+    topo, model, states, inputs, spec = rex._scaling_problem(M, N, 0.01, 0)
+    cfg = rm.MpcConfig(horizon=N, dt=0.01, threads=threads)
+    x = rgr.SystemState(states[0])
+    st0 = rm.mpc_init(x, cfg, 6)
+    times = []
+    with threadpool_limits(limits=threads):
+        for k in range(warmup + steps):
+            t0 = time.perf_counter()
+            u, st1 = rm.mpc_step(model, topo, spec, x, st0, cfg)
+            dt = time.perf_counter() - t0
+            if k >= warmup:
+                times.append(dt)
+    return float(np.mean(times)) * 1e3, st1.last_status.value, st1.last_iterations
+
+
 def reference_arm(args, world, rank):
+    """The reference's own CPU implementation of the path, timed on the host
+    cores: the unmodified package from baseline/_ref through its public
+    mpc_step (BLAS threads = condense threads = all cores); the oracle port
+    only if the install is missing.  Rank 0 alone runs at N>1."""
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    ms = cpu_oracle_steps(args.nodes, args.horizon, args.steps, args.warmup, cores)
+    M, N = args.nodes, args.horizon
+    if import_reference() is not None:
+        ms, status, iters = reference_steps(M, N, args.steps, args.warmup, cores)
+        kind = "reference"
+        what = (f"{args.steps} calls of the unmodified reference gnnmpc.mpc.mpc_step "
+                f"(baseline/_ref) after {args.warmup} warm-up, M={M}, N={N}, "
+                f"_scaling_problem seed 0, BLAS threads = condense threads = {cores}")
+    else:
+        ms = cpu_oracle_steps(M, N, args.steps, args.warmup, cores)
+        status, iters = None, None
+        kind = "port"
+        what = (f"{args.steps} oracle mpc_step calls (after {args.warmup} warm-up) at M={M}, "
+                f"N={N}, BLAS threads = condense threads = {cores} (baseline/_ref missing)")
     v = 1000.0 / ms
     out = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "nodes": args.nodes,
-                                        "horizon": args.horizon, "parallelism": "host cores"},
-        "cpu_baseline": {"value": v, "unit": "solves/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} oracle mpc_step calls (after {args.warmup} "
-                                   f"warm-up) at M={args.nodes}, N={args.horizon}, BLAS threads "
-                                   f"= condense threads = {cores}"},
+        "data": "synthetic", "config": {"workload": WORKLOAD, "nodes": M, "horizon": N,
+                                        "parallelism": "host cores",
+                                        "qp": {"status": status, "iterations": iters}},
+        "cpu_baseline": {"value": v, "unit": "solves/s", "cores": cores, "kind": kind,
+                         "sample": what},
         "e2e": {"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -351,9 +407,14 @@ def ours_arm(args, world, rank, local):
 
     cpu = None
     if not args.no_cpu_baseline:
-        cms = cpu_oracle_steps(M, N, args.cpu_steps, 1, 1)
-        cpu = {"value": 1000.0 / cms, "unit": "solves/s", "cores": 1, "kind": "port",
-               "sample": f"{args.cpu_steps} oracle mpc_step calls at M={M}, N={N} (1 warm-up), "
+        if import_reference() is not None:
+            cms = reference_steps(M, N, args.cpu_steps, 1, 1)[0]
+            kind, who = "reference", "unmodified reference gnnmpc.mpc.mpc_step (baseline/_ref)"
+        else:
+            cms = cpu_oracle_steps(M, N, args.cpu_steps, 1, 1)
+            kind, who = "port", "oracle mpc_step (baseline/_ref missing)"
+        cpu = {"value": 1000.0 / cms, "unit": "solves/s", "cores": 1, "kind": kind,
+               "sample": f"{args.cpu_steps} calls of the {who} at M={M}, N={N} (1 warm-up), "
                          "BLAS pinned to 1 thread (reference protocol experiments.py:492-528)",
                "ms_per_step": cms}
     out = {
@@ -586,10 +647,12 @@ def cfg5_arm(args, world, rank, local):
     topo, model, states, inputs, spec = workloads.mesh_problem(400, 250, N, 0.01, 0)
     spec.freeze()
     cfg = pkg.MpcConfig(horizon=N, dt=0.01)
-    pm = PartitionedMpc(model, topo, spec, cfg, partition_nodes(topo, world, rank))
-    ls = torch.from_numpy(np.concatenate([states, states[-1:]], 0)).to(dev)
+    part = partition_nodes(topo, world, rank)
+    pm = PartitionedMpc(model, topo, spec, cfg, part)
+    loc = part.local_nodes  # owned + halo nodes of this rank
+    ls = torch.from_numpy(np.concatenate([states, states[-1:]], 0)[:, loc]).to(dev)
     li = torch.from_numpy(inputs).to(dev)
-    x0 = torch.from_numpy(states[0]).to(dev)
+    x0 = torch.from_numpy(states[0][loc]).to(dev)
     for _ in range(args.warmup):
         pm.step(x0, ls, li)
     dist.barrier()

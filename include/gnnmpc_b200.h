@@ -100,6 +100,15 @@ int gm_set_model(gm_ctx* ctx, int n_p, int n_u, int n_m, double dt,
                  const double* state_mean, const double* state_scale,
                  const double* input_mean, const double* input_scale);
 
+/* Model generation: incremented by gm_set_model whenever the device weight
+ * buffers are reallocated (layer dims changed) or a scalar baked into kernel
+ * arguments (n_p, n_u, n_m, dt) changed.  Parameter edits with unchanged dims
+ * are copied into the existing buffers and keep the generation, so captured
+ * CUDA graphs stay valid and read the new weights; a host that captured
+ * graphs must drop them when the generation moves.  Buffers are never freed
+ * under a captured graph (retired until gm_destroy). */
+int64_t gm_model_generation(const gm_ctx* ctx);
+
 /* State / input dimensions used by the condensing entry points when the
  * linearisation was not produced by gm_linearize (set_model sets both). */
 int gm_set_dims(gm_ctx* ctx, int nx, int nu);
@@ -243,6 +252,21 @@ int gm_mpc_finish(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const d
                   const double* u_prev, int has_prev, double* cur_states,
                   double* planned_states, double* planned_inputs, double* next_states,
                   double* next_inputs, double* u_applied, double* summary, void* stream);
+
+/* ---- node-partitioned recursion: halo pack / unpack (multi-GPU) ------- */
+/* Strided row gather / scatter for the per-stage halo exchange of the
+ * node-partitioned Gamma recursion (the reference's node-chunk pool,
+ * condensing.py:208-227, generalised to row slabs over devices).
+ * gather: dst (n_outer, n_idx, row_bytes) contiguous <- src rows at
+ *   src + o*outer_stride_bytes + idx[i]*row_stride_bytes;
+ * scatter: the inverse.  idx (n_idx) int32 device; all sizes and addresses
+ * multiples of 8 bytes. */
+int gm_gather_rows(gm_ctx* ctx, const void* src, void* dst, const int32_t* idx, int n_idx,
+                   int64_t row_bytes, int64_t row_stride_bytes, int n_outer,
+                   int64_t outer_stride_bytes, void* stream);
+int gm_scatter_rows(gm_ctx* ctx, const void* src, void* dst, const int32_t* idx, int n_idx,
+                    int64_t row_bytes, int64_t row_stride_bytes, int n_outer,
+                    int64_t outer_stride_bytes, void* stream);
 
 /* ---- cfg2 plant: trunk.py chain (trunk.py:116-160) ------------------------ */
 /* One controller period (substeps semi-implicit Euler substeps of dt_sim) of B

@@ -357,9 +357,198 @@ def main():
         print(f.name, f.stat().st_size)
 
 
+def _ref_mesh(rgr, rows, cols):
+    """4-neighbour grid as a reference GraphTopology (id = r*cols + c,
+    in-neighbours ascending: up, left, right, down)."""
+    nbrs = []
+    for r in range(rows):
+        for c in range(cols):
+            ns = []
+            if r > 0: ns.append((r - 1) * cols + c)
+            if c > 0: ns.append(r * cols + c - 1)
+            if c < cols - 1: ns.append(r * cols + c + 1)
+            if r < rows - 1: ns.append((r + 1) * cols + c)
+            nbrs.append(tuple(ns))
+    return rgr.GraphTopology(rows * cols, tuple(nbrs), 4)
+
+
+def _ref_mesh_problem(rc, rg, rgr, rows, cols, N, dt, seed):
+    """The cfg5 recipe (workloads.mesh_problem) built from reference objects:
+    _scaling_problem's draws (experiments.py:465-489) on a mesh graph."""
+    rng = np.random.default_rng(seed)
+    topo = _ref_mesh(rgr, rows, cols)
+    M = rows * cols
+    model = rg.init_model(3, 6, dt, rng, n_m=16, psi_hidden=(32, 32), phi_hidden=(64, 64),
+                          out_scale=0.05)
+    ids = np.arange(M)
+    states = np.zeros((N, M, 6))
+    states[:, :, 0] = 0.15 * (ids % cols)
+    states[:, :, 2] = -0.15 * (ids // cols)
+    states += 0.01 * rng.standard_normal(states.shape)
+    inputs = rng.uniform(0.0, 4.0, size=(N, 6))
+    q = np.zeros((M, N + 1, 6, 6))
+    q[:, :] = np.diag(np.concatenate([np.full(3, 1.0), np.full(3, 0.1)]))
+    x_ref = states[0][:, None, :].repeat(N + 1, axis=1)
+    row = np.zeros((1, 6))
+    row[0, 2] = 1.0
+    scons = [rc.StateConstraint(M - 1, k, row, np.array([1.0]), soft=True) for k in range(1, N + 1)]
+    spec = rc.OcpSpec(topo, N, q, x_ref, np.tile(np.eye(6) * 1e-2, (N, 1, 1)), np.zeros((N, 6)),
+                      [rc.stage_input_box(6, 0.0, 8.0)] * N, scons)
+    return topo, model, states, inputs, spec
+
+
+def _mpc_seq(rm, rgr, model, topo, specs, x0s, cfg, prefix, out):
+    """Run the reference mpc_step over a sequence of (spec, measurement) and
+    record every step's outputs (mpc.py:102-200)."""
+    st = rm.mpc_init(rgr.SystemState(x0s[0]), cfg, specs[0].r.shape[-1])
+    for t, (spec, x) in enumerate(zip(specs, x0s)):
+        u, st = rm.mpc_step(model, topo, spec, rgr.SystemState(x), st, cfg)
+        p = f"{prefix}{t}_"
+        out[p + "u"] = u.u
+        out[p + "lin_states"] = st.lin_states
+        out[p + "lin_inputs"] = st.lin_inputs
+        out[p + "planned_states"] = st.planned_states
+        out[p + "planned_inputs"] = st.planned_inputs
+        out[p + "last_applied"] = st.last_applied
+        out[p + "filtered"] = (st.filtered_input if st.filtered_input is not None
+                               else np.zeros(0))
+        out[p + "meta"] = np.array([["optimal", "max_iterations", "primal_infeasible",
+                                     "numerical_failure"].index(st.last_status.value),
+                                    st.last_iterations])
+    out[prefix + "steps"] = np.array(len(specs))
+
+
+def round2():
+    """Round-2 fixtures: mesh graphs (degree 4) through the whole pipeline,
+    the mpc_step branches (SQP loop, damping, input filter, both fallback
+    policies), the iteration-cap best iterate and batched same-shape QPs."""
+    rc, rex, rg, rgr, rmlp, rm, rq = _ref()
+    OUT.mkdir(parents=True, exist_ok=True)
+
+    # mesh 6x5 (M=30, E=98), N=6, the cfg5 recipe
+    out = {}
+    topo, model, states, inputs, spec = _ref_mesh_problem(rc, rg, rgr, 6, 5, 6, 0.01, 1)
+    out["states"], out["inputs"] = states, inputs
+    out["mesh"] = np.array([6, 5])
+    _model_arrays("", model, out)
+    _spec_arrays("", spec, out)
+    _pipeline("", model, topo, spec, states, inputs, states[0], out, rc, rg, rq, rm, rgr)
+    np.savez_compressed(OUT / "mesh6x5.npz", **out)
+
+    # P3-style mesh 4x4: random biases + normalisation (c != 0), hard and soft
+    # state rows on interior (degree-4) nodes
+    out = {}
+    rng = np.random.default_rng(91)
+    topo = _ref_mesh(rgr, 4, 4)
+    M, N = 16, 5
+    model = rg.init_model(3, 6, 0.02, rng, n_m=8, psi_hidden=(16, 12), phi_hidden=(24, 20),
+                          out_scale=0.3)
+    for mlp in (model.psi, model.phi):
+        for b in mlp.biases:
+            b[...] = 0.2 * rng.standard_normal(b.shape)
+    model.normalization = rg.Normalization(0.1 * rng.standard_normal(6), rng.random(6) + 0.5,
+                                           rng.standard_normal(6), rng.random(6) + 0.5)
+    states = 0.3 * rng.standard_normal((N + 1, M, 6))
+    inputs = rng.standard_normal((N, 6))
+    q = np.tile(np.diag(rng.random(6) + 0.1), (M, N + 1, 1, 1))
+    spec = rc.OcpSpec(topo, N, q, 0.1 * rng.standard_normal((M, N + 1, 6)),
+                      np.tile(np.eye(6) * 0.5, (N, 1, 1)), np.zeros((N, 6)),
+                      [rc.stage_input_box(6, -1.0, 1.0)] * N,
+                      [rc.StateConstraint(5, 3, rng.standard_normal((2, 6)), np.array([0.5, 0.2])),
+                       rc.StateConstraint(10, N, np.eye(6)[:1], np.array([0.1]), soft=True,
+                                          rho1=10.0, rho2=100.0)])
+    out["states"], out["inputs"] = states, inputs
+    out["mesh"] = np.array([4, 4])
+    _model_arrays("", model, out)
+    _spec_arrays("", spec, out)
+    _pipeline("", model, topo, spec, states, inputs, states[0], out, rc, rg, rq, rm, rgr)
+    np.savez_compressed(OUT / "mesh_p3.npz", **out)
+
+    # mpc_step branches on the cfg1 recipe (chain M=10, N=10)
+    out = {}
+    topo, model, states, inputs, spec = rex._scaling_problem(10, 10, 0.01, 0)
+    _model_arrays("", model, out)
+    _spec_arrays("", spec, out)
+    out["states"], out["inputs"] = states, inputs
+    N = 10
+    rng = np.random.default_rng(13)
+    xs = [states[0] + 0.002 * rng.standard_normal(states[0].shape) for _ in range(3)]
+    out["x_seq"] = np.stack(xs)
+    # a spec whose QP is primal infeasible: hard rows z <= -100 and -z <= -100
+    # on node 0 at stage 1 (contradictory), on top of the feasible spec
+    bad_rows = np.zeros((2, 6))
+    bad_rows[0, 2], bad_rows[1, 2] = 1.0, -1.0
+    bad = rc.OcpSpec(topo, N, spec.q, spec.x_ref, spec.r, spec.u_ref, spec.input_constraints,
+                     list(spec.state_constraints)
+                     + [rc.StateConstraint(0, 1, bad_rows, np.array([-100.0, -100.0]))])
+    out["bad_row_c"], out["bad_row_d"] = bad_rows, np.array([-100.0, -100.0])
+    cases = {
+        "sqp2": (rm.MpcConfig(horizon=N, dt=0.01, sqp_iterations=2), [spec] * 2),
+        "damp": (rm.MpcConfig(horizon=N, dt=0.01, sqp_damping=0.5), [spec] * 2),
+        "sqp2damp": (rm.MpcConfig(horizon=N, dt=0.01, sqp_iterations=2, sqp_damping=0.5),
+                     [spec] * 2),
+        "filter": (rm.MpcConfig(horizon=N, dt=0.01, input_filter_tau=0.05), [spec] * 3),
+        "fbhold": (rm.MpcConfig(horizon=N, dt=0.01), [spec, bad, spec]),
+        "fbzero": (rm.MpcConfig(horizon=N, dt=0.01, fallback="zero-input"), [spec, bad, spec]),
+        "fbfirst": (rm.MpcConfig(horizon=N, dt=0.01), [bad, spec]),
+        "coldstart": (rm.MpcConfig(horizon=N, dt=0.01, warm_start=False), [spec] * 2),
+    }
+    for name, (cfg, specs) in cases.items():
+        _mpc_seq(rm, rgr, model, topo, specs, xs[: len(specs)], cfg, name + "_", out)
+    out["cases"] = np.array(list(cases))
+    np.savez_compressed(OUT / "mpc_branches.npz", **out)
+
+    # QP: best iterate at the iteration cap (tests/test_qpsolver.py:127-134),
+    # batched same-shape problems, the infeasible KAT (:119-124)
+    out = {}
+    rng = np.random.default_rng(21)
+    k = 0
+    for cap in (1, 2, 3, 5):
+        for _ in range(3):
+            n, m = int(rng.integers(2, 7)), int(rng.integers(1, 9))
+            A = rng.standard_normal((n, n))
+            H = A @ A.T + np.eye(n) * (0.1 + rng.random())
+            g = rng.standard_normal(n)
+            C = rng.standard_normal((m, n))
+            d = C @ rng.standard_normal(n) + rng.random(m) + 0.05
+            sol = rq.solve_qp(rq.QpProblem(H, g, C, d), rq.SolverSettings(max_iterations=cap))
+            p = f"cap{k}_"
+            out[p + "H"], out[p + "g"], out[p + "C"], out[p + "d"] = H, g, C, d
+            out[p + "u"], out[p + "duals"] = sol.u, sol.duals
+            out[p + "meta"] = np.array([["optimal", "max_iterations", "primal_infeasible",
+                                         "numerical_failure"].index(sol.status.value),
+                                        sol.iterations, cap])
+            k += 1
+    for t in range(8):
+        n, m = 5, 7
+        A = rng.standard_normal((n, n))
+        H = A @ A.T + np.eye(n) * (0.1 + rng.random())
+        g = rng.standard_normal(n)
+        C = rng.standard_normal((m, n))
+        d = C @ rng.standard_normal(n) + rng.random(m) + 0.05
+        sol = rq.solve_qp(rq.QpProblem(H, g, C, d))
+        p = f"b{t}_"
+        out[p + "H"], out[p + "g"], out[p + "C"], out[p + "d"] = H, g, C, d
+        out[p + "u"], out[p + "duals"] = sol.u, sol.duals
+        out[p + "meta"] = np.array([["optimal", "max_iterations", "primal_infeasible",
+                                     "numerical_failure"].index(sol.status.value), sol.iterations])
+    sol = rq.solve_qp(rq.QpProblem(np.array([[1.0]]), np.zeros(1), np.array([[1.0], [-1.0]]),
+                                   np.array([-1.0, -2.0])))
+    out["infeas_u"] = sol.u
+    out["infeas_meta"] = np.array([["optimal", "max_iterations", "primal_infeasible",
+                                    "numerical_failure"].index(sol.status.value), sol.iterations,
+                                   sol.primal_infeas])
+    np.savez_compressed(OUT / "qp_round2.npz", **out)
+    for f in ("mesh6x5", "mesh_p3", "mpc_branches", "qp_round2"):
+        print(f, (OUT / f"{f}.npz").stat().st_size)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "cfg2":
         cfg2_closed_loop()
+        raise SystemExit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "round2":
+        round2()
         raise SystemExit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "obstacle":
         obstacle_provider()

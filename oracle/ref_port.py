@@ -521,7 +521,7 @@ def shift(states, inputs):
 
 def mpc_step(model, topo, spec, x_measured, lin_states, lin_inputs, horizon, warm_start=True,
              solver=None, sqp_iterations=1, sqp_damping=1.0, threads=1, fallback="hold-previous-input",
-             last_applied=None, timings=None):
+             last_applied=None, timings=None, input_filter_tau=None, filtered_input=None, dt=None):
     """One RTI control step (mpc.py:102-200), state passed as plain arrays.
 
     Returns dict(u_applied, lin_states, lin_inputs, planned_states,
@@ -578,11 +578,18 @@ def mpc_step(model, topo, spec, x_measured, lin_states, lin_inputs, horizon, war
         li = np.array(lin_inputs, dtype=float, copy=True)
     planned_states = ls.transpose(1, 0, 2).copy()
     planned_inputs = li.copy()
+    filtered = filtered_input
+    if input_filter_tau is not None:  # first-order input smoothing (mpc.py:178-183)
+        alpha = dt / (input_filter_tau + dt)
+        prev = np.asarray(filtered, dtype=float) if filtered is not None else u_app
+        u_app = prev + alpha * (u_app - prev)
+        filtered = u_app.copy()
     ns, ni = shift(ls, li)
     if timings is not None:
         timings.update(tm)
     return dict(u_applied=u_app, lin_states=ns, lin_inputs=ni, planned_states=planned_states,
-                planned_inputs=planned_inputs, status=status, iterations=iters)
+                planned_inputs=planned_inputs, status=status, iterations=iters,
+                filtered_input=filtered)
 
 
 # --------------------------------------------------------------------------

@@ -50,6 +50,7 @@ _SIGNATURES = {
     "gm_graph_tables": (c_int, [c_void_p, P, P, P, P, P]),
     "gm_set_model": (c_int, [c_void_p, c_int, c_int, c_int, c_double, c_int, P, P, P, c_int, P, P,
                              P, P, P, P, P]),
+    "gm_model_generation": (c_i64, [c_void_p]),
     "gm_set_dims": (c_int, [c_void_p, c_int, c_int]),
     "gm_set_node_range": (c_int, [c_void_p, c_i64, c_i64]),
     "gm_linearize": (c_int, [c_void_p, c_i64, P, P, P, P, P, P, P, c_void_p]),
@@ -77,6 +78,8 @@ _SIGNATURES = {
     "gm_chol_check": (c_int, [c_void_p, c_int, P, P, P, P, P, c_void_p]),
     "gm_set_condense_mode": (c_int, [c_void_p, c_int]),
     "gm_gram_check": (c_int, [c_void_p, c_int, c_int, P, P, P, c_void_p]),
+    "gm_gather_rows": (c_int, [c_void_p, P, P, P, c_int, c_i64, c_i64, c_int, c_i64, c_void_p]),
+    "gm_scatter_rows": (c_int, [c_void_p, P, P, P, c_int, c_i64, c_i64, c_int, c_i64, c_void_p]),
     "gm_reconstruct_states": (c_int, [c_void_p, c_int, c_int, P, c_int, P, c_int, P, c_void_p]),
     "gm_mpc_finish": (c_int, [c_void_p, c_int, c_int, P, c_int, P, c_int, P, P, P, P, P, P, c_double,
                               c_int, P, c_int, P, P, P, P, P, P, P, c_void_p]),

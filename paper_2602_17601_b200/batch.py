@@ -24,8 +24,9 @@ import numpy as np
 from . import device as _dev
 from ._runtime import lib
 from .condensing import spec_rows
+from .errors import ConfigurationError
 from .mpc import MpcConfig
-from .qpsolver import STATUS_BY_CODE
+from .qpsolver import STATUS_BY_CODE, settings_c
 
 
 def shard_range(n_items: int, world: int, rank: int) -> tuple[int, int]:
@@ -52,6 +53,11 @@ class BatchedMpc:
     each instance's own initial state as its reference)."""
 
     def __init__(self, model, topo, spec, cfg: MpcConfig, B: int, device=None):
+        if cfg.sqp_iterations != 1 or cfg.input_filter_tau is not None:
+            # the batched step is the RTI step (one QP per instance per call);
+            # the SQP loop and the input filter are per-instance host logic of
+            # mpc_step (mpc.py:129-183) -- use mpc_step for those
+            raise ConfigurationError("BatchedMpc supports sqp_iterations == 1 and no input filter")
         self.eng = eng = _dev.engine(topo, model, device)
         self.model, self.topo, self.spec, self.cfg, self.B = model, topo, spec, cfg, B
         torch = eng.torch
@@ -108,18 +114,28 @@ class BatchedMpc:
         self.next_inputs = e((B, N, nu), f64)
         self.u_applied = e((B, nu), f64)
         self.u_prev = eng.zeros((B, nu), f64)
+        self.has_prev = 0
         self.summary = e((B, nu + 2), f64)
-        self.settings_c = cfg.solver.as_c()
+        self.settings_c = settings_c(cfg.solver)
         self.graph = None
 
-    def load(self, x_measured, lin_states, lin_inputs, x_ref, non_blocking: bool = False):
+    def load(self, x_measured, lin_states, lin_inputs, x_ref, non_blocking: bool = False,
+             last_applied=None):
         """Copy the step's inputs (numpy or tensors) into the device buffers:
         x_measured (B, M, nx), lin_states (B, N+1, M, nx), lin_inputs (B, N, nu),
-        x_ref (B, M, N+1, nx).  ``non_blocking`` makes copies from pinned host
-        tensors asynchronous on the current stream (WavePipeline)."""
+        x_ref (B, M, N+1, nx), and optionally last_applied (B, nu) -- each
+        instance's previously applied input, held by the 'hold-previous-input'
+        fallback (mpc.py:167-170); without it the fallback applies zeros, as
+        the reference does when ``state.last_applied is None``.
+        ``non_blocking`` makes copies from pinned host tensors asynchronous on
+        the current stream (WavePipeline)."""
         torch = self.eng.torch
-        for dst, src in ((self.x0, x_measured), (self.X, lin_states), (self.U, lin_inputs),
-                         (self.xref, x_ref)):
+        pairs = [(self.x0, x_measured), (self.X, lin_states), (self.U, lin_inputs),
+                 (self.xref, x_ref)]
+        self.has_prev = 0 if last_applied is None else 1
+        if last_applied is not None:
+            pairs.append((self.u_prev, last_applied))
+        for dst, src in pairs:
             if isinstance(src, np.ndarray):
                 dst.copy_(torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64)))
             else:
@@ -168,13 +184,13 @@ class BatchedMpc:
                  self.status.data_ptr(), self.iters.data_ptr(), self.X.data_ptr(),
                  self.U.data_ptr(), self.X.data_ptr(), self.U.data_ptr(),
                  float(self.cfg.sqp_damping),
-                 0 if self.cfg.fallback == "hold-previous-input" else 1, self.u_prev.data_ptr(), 1,
-                 None, self.planned_states.data_ptr(), self.planned_inputs.data_ptr(),
+                 0 if self.cfg.fallback == "hold-previous-input" else 1, self.u_prev.data_ptr(),
+                 self.has_prev, None, self.planned_states.data_ptr(), self.planned_inputs.data_ptr(),
                  self.next_states.data_ptr(), self.next_inputs.data_ptr(),
                  self.u_applied.data_ptr(), self.summary.data_ptr(), sp)
 
-    def step(self, x_measured, lin_states, lin_inputs, x_ref) -> BatchResult:
-        self.load(x_measured, lin_states, lin_inputs, x_ref)
+    def step(self, x_measured, lin_states, lin_inputs, x_ref, last_applied=None) -> BatchResult:
+        self.load(x_measured, lin_states, lin_inputs, x_ref, last_applied=last_applied)
         self.enqueue()
         summ = self.summary.cpu().numpy()
         nu = self.nu

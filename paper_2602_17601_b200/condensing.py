@@ -249,11 +249,23 @@ def spec_rows(spec, nx: int, nu: int) -> SpecRows:
 class DeviceSpec:
     """Everything of an OcpSpec the device path reads, uploaded once."""
 
-    def __init__(self, eng, spec, nx: int, nu: int):
+    def __init__(self, eng, spec, nx: int, nu: int, local_nodes=None, node_map=None):
+        """``local_nodes`` (global ids, ascending) / ``node_map`` (global id ->
+        local id, -1 elsewhere) restrict the per-node arrays to one rank's
+        local nodes of a node partition (partition.py); the constraint rows
+        keep the global order (sorted by global node id) with each state
+        row's node mapped to its local id (rows of non-local nodes point at
+        local node 0 and are masked by the caller)."""
         f64, i32 = np.float64, np.int32
         self.rows = rows = spec_rows(spec, nx, nu)
-        self.q = eng.h2d(spec.q, f64)
-        self.x_ref = eng.h2d(spec.x_ref, f64)
+        q, x_ref = spec.q, spec.x_ref
+        if local_nodes is not None:
+            q, x_ref = np.asarray(q)[local_nodes], np.asarray(x_ref)[local_nodes]
+            if rows.n_st:
+                loc = np.asarray(node_map)[rows.st_node]
+                rows.st_node = np.where(loc >= 0, loc, 0).astype(np.int32)
+        self.q = eng.h2d(q, f64)
+        self.x_ref = eng.h2d(x_ref, f64)
         self.r = eng.h2d(spec.r, f64)
         self.u_ref = eng.h2d(spec.u_ref, f64)
         self.in_stage = eng.h2d(rows.in_stage, i32) if rows.n_in else None

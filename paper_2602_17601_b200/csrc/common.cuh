@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -76,6 +77,8 @@ struct gm_ctx {
   double dt = 0;
   MlpHost psi, phi;
   double* d_norm = nullptr;  // state_mean(nx) state_scale(nx) input_mean(nu) input_scale(nu)
+  int64_t norm_len = 0;
+  int64_t model_gen = 0;  // bumped when weight buffers / baked scalars change (gm_model_generation)
   // scratch (grown on demand, stream-ordered use only)
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -116,10 +119,12 @@ void gm_count_launch();
 // (k_linearize_layers.cu)
 bool gm_lin_chains(const gm_ctx* ctx);
 
-// K-HG on tcgen05 (k_condense_fused.cu); 1 = shape not handled
-int gm_tc_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const double* q, int64_t q_stride,
-               const double* x_ref, int64_t xref_stride, const double* r, int64_t r_stride, const double* u_ref,
-               int64_t uref_stride, double* H, double* g, int partial, void* stream);
+// K-HG through the fused kernels without the recursion (k_condense_fused.cu):
+// tc != 0 tcgen05, else SIMT; returns 1 when the shape is not handled
+int gm_fused_cost(gm_ctx* ctx, int tc, int B, int N, const float* gamma, int ld, const double* q,
+                  int64_t q_stride, const double* x_ref, int64_t xref_stride, const double* r,
+                  int64_t r_stride, const double* u_ref, int64_t uref_stride, double* H, double* g,
+                  int partial, void* stream);
 
 static inline int64_t gm_node_hi(const gm_ctx* c) { return c->node_hi < 0 ? c->M : c->node_hi; }
 

@@ -228,20 +228,25 @@ int gm_set_node_range(gm_ctx* ctx, int64_t lo, int64_t hi) {
   return GM_OK;
 }
 
+// Upload one MLP.  When the layer dims are unchanged the new parameters are
+// copied into the existing device buffers, so CUDA graphs captured with these
+// pointers (mpc.py StepPlan) read the new weights.  Otherwise the old buffers
+// are retired (kept alive until gm_destroy, never freed under a captured
+// graph) and *realloc is set: the caller bumps the model generation so the
+// host drops every captured graph.
 static int upload_mlp(gm_ctx* ctx, MlpHost& m, int L, const int32_t* dims, const double* w,
-                      const double* b) {
+                      const double* b, bool* realloc) {
   if (L < 1 || L > GM_MAX_LAYERS)
     return gm_fail(ctx, GM_ERR_CONFIG, "MLP needs 1.." + std::to_string(GM_MAX_LAYERS) + " layers");
-  free_mlp(m);
-  m.L = L;
-  m.dims.assign(dims, dims + L + 1);
-  m.w_off.assign(L, 0);
-  m.b_off.assign(L, 0);
+  for (int l = 0; l < L; ++l)
+    if (dims[l] < 1 || dims[l + 1] < 1) return gm_fail(ctx, GM_ERR_CONFIG, "layer dims must be >= 1");
+  const bool same = m.d_wt64 && m.L == L && (int)m.dims.size() == L + 1 &&
+                    std::equal(m.dims.begin(), m.dims.end(), dims);
+  std::vector<int64_t> w_off(L, 0), b_off(L, 0);
   int64_t wn = 0, bn = 0;
   for (int l = 0; l < L; ++l) {
-    if (dims[l] < 1 || dims[l + 1] < 1) return gm_fail(ctx, GM_ERR_CONFIG, "layer dims must be >= 1");
-    m.w_off[l] = wn;
-    m.b_off[l] = bn;
+    w_off[l] = wn;
+    b_off[l] = bn;
     wn += (int64_t)dims[l] * dims[l + 1];
     bn += dims[l + 1];
   }
@@ -249,18 +254,33 @@ static int upload_mlp(gm_ctx* ctx, MlpHost& m, int L, const int32_t* dims, const
   std::vector<float> w32(wn);
   for (int l = 0; l < L; ++l) {
     const int in = dims[l], out = dims[l + 1];
-    const double* Wl = w + m.w_off[l];  // (out, in) row-major
+    const double* Wl = w + w_off[l];  // (out, in) row-major
     for (int o = 0; o < out; ++o)
       for (int k = 0; k < in; ++k) {
         double v = Wl[(int64_t)o * in + k];
         if (!std::isfinite(v)) return gm_fail(ctx, GM_ERR_CONFIG, "parameters must be finite");
-        wt[m.w_off[l] + (int64_t)k * out + o] = v;
-        w32[m.w_off[l] + (int64_t)o * in + k] = (float)v;
+        wt[w_off[l] + (int64_t)k * out + o] = v;
+        w32[w_off[l] + (int64_t)o * in + k] = (float)v;
       }
   }
-  GM_CUDA(ctx, cudaMalloc(&m.d_wt64, sizeof(double) * wn));
-  GM_CUDA(ctx, cudaMalloc(&m.d_w32, sizeof(float) * wn));
-  GM_CUDA(ctx, cudaMalloc(&m.d_b64, sizeof(double) * bn));
+  if (!same) {
+    if (m.d_wt64) {
+      ctx->retired.push_back(m.d_wt64);
+      ctx->retired.push_back(m.d_w32);
+      ctx->retired.push_back(m.d_b64);
+    }
+    m.d_wt64 = nullptr;
+    m.d_w32 = nullptr;
+    m.d_b64 = nullptr;
+    m.L = L;
+    m.dims.assign(dims, dims + L + 1);
+    m.w_off = w_off;
+    m.b_off = b_off;
+    GM_CUDA(ctx, cudaMalloc(&m.d_wt64, sizeof(double) * wn));
+    GM_CUDA(ctx, cudaMalloc(&m.d_w32, sizeof(float) * wn));
+    GM_CUDA(ctx, cudaMalloc(&m.d_b64, sizeof(double) * bn));
+    *realloc = true;
+  }
   GM_CUDA(ctx, cudaMemcpy(m.d_wt64, wt.data(), sizeof(double) * wn, cudaMemcpyHostToDevice));
   GM_CUDA(ctx, cudaMemcpy(m.d_w32, w32.data(), sizeof(float) * wn, cudaMemcpyHostToDevice));
   GM_CUDA(ctx, cudaMemcpy(m.d_b64, b, sizeof(double) * bn, cudaMemcpyHostToDevice));
@@ -287,19 +307,30 @@ int gm_set_model(gm_ctx* ctx, int n_p, int n_u, int n_m, double dt, int psi_laye
     if (!(state_scale[k] > 0)) return gm_fail(ctx, GM_ERR_CONFIG, "normalization scales must be positive");
   for (int k = 0; k < n_u; ++k)
     if (!(input_scale[k] > 0)) return gm_fail(ctx, GM_ERR_CONFIG, "normalization scales must be positive");
-  rc = upload_mlp(ctx, ctx->psi, psi_layers, psi_dims, psi_w, psi_b);
+  // kernels of captured graphs may still read the buffers updated in place
+  GM_CUDA(ctx, cudaDeviceSynchronize());
+  // scalars are kernel arguments baked into captured graphs: any change
+  // invalidates them like a reallocation does
+  bool realloc = !ctx->has_model || ctx->n_p != n_p || ctx->n_m != n_m || ctx->m_nu != n_u ||
+                 ctx->dt != dt;
+  rc = upload_mlp(ctx, ctx->psi, psi_layers, psi_dims, psi_w, psi_b, &realloc);
   if (rc) return rc;
-  rc = upload_mlp(ctx, ctx->phi, phi_layers, phi_dims, phi_w, phi_b);
+  rc = upload_mlp(ctx, ctx->phi, phi_layers, phi_dims, phi_w, phi_b, &realloc);
   if (rc) return rc;
   std::vector<double> norm(2 * nx + 2 * n_u);
   std::memcpy(norm.data(), state_mean, sizeof(double) * nx);
   std::memcpy(norm.data() + nx, state_scale, sizeof(double) * nx);
   std::memcpy(norm.data() + 2 * nx, input_mean, sizeof(double) * n_u);
   std::memcpy(norm.data() + 2 * nx + n_u, input_scale, sizeof(double) * n_u);
-  cudaFree(ctx->d_norm);
-  ctx->d_norm = nullptr;
-  GM_CUDA(ctx, cudaMalloc(&ctx->d_norm, sizeof(double) * norm.size()));
+  if (!ctx->d_norm || ctx->norm_len != (int64_t)norm.size()) {
+    if (ctx->d_norm) ctx->retired.push_back(ctx->d_norm);
+    ctx->d_norm = nullptr;
+    GM_CUDA(ctx, cudaMalloc(&ctx->d_norm, sizeof(double) * norm.size()));
+    ctx->norm_len = (int64_t)norm.size();
+    realloc = true;
+  }
   GM_CUDA(ctx, cudaMemcpy(ctx->d_norm, norm.data(), sizeof(double) * norm.size(), cudaMemcpyHostToDevice));
+  if (realloc) ++ctx->model_gen;
   ctx->n_p = n_p;
   ctx->n_m = n_m;
   ctx->m_nx = nx;
@@ -310,6 +341,8 @@ int gm_set_model(gm_ctx* ctx, int n_p, int n_u, int n_m, double dt, int psi_laye
   ctx->has_model = true;
   return GM_OK;
 }
+
+int64_t gm_model_generation(const gm_ctx* ctx) { return ctx ? ctx->model_gen : -1; }
 
 int gm_set_dims(gm_ctx* ctx, int nx, int nu) {
   if (!ctx) return GM_ERR_CONFIG;

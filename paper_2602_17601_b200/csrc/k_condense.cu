@@ -705,16 +705,14 @@ int gm_condense_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, cons
   int rc = check_dims(ctx, B, N, ld);
   if (rc) return rc;
   if (B == 0) return GM_OK;
-  // tensor-core K-HG (tcgen05 3xTF32) for B * nodes >= 512 or when forced;
-  // gm_set_condense_mode(1) keeps the SIMT kernel below
+  // K-HG through the fused condensing kernel without its recursion: the
+  // SIMT one (fp32 FMA, round-to-nearest) by default, the tcgen05 3xTF32 one
+  // when forced (gm_set_condense_mode(3)); the per-tile kernel below for
+  // shapes without an instantiation
   {
-    const int64_t nodes_ = gm_node_hi(ctx) - ctx->node_lo;
-    const bool tc = ctx->cond_mode == 3 || (ctx->cond_mode != 1 && (int64_t)B * nodes_ >= 512);
-    if (tc) {
-      rc = gm_tc_cost(ctx, B, N, gamma, ld, q, q_stride, x_ref, xref_stride, r, r_stride, u_ref, uref_stride, H,
-                      g, partial, stream);
-      if (rc != 1) return rc;
-    }
+    rc = gm_fused_cost(ctx, ctx->cond_mode == 3, B, N, gamma, ld, q, q_stride, x_ref, xref_stride,
+                       r, r_stride, u_ref, uref_stride, H, g, partial, stream);
+    if (rc != 1) return rc;
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int nx = ctx->nx, nu = ctx->n_u;

@@ -137,11 +137,12 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t bi = blockIdx.x / a.splits;
   const int split = (int)(blockIdx.x % a.splits);
-  const int nb = split * a.per, ne = min(M, nb + a.per);
+  const bool rec = a.rec != 0;  // 0: read Gamma of [lo, hi) instead of producing it (K-HG)
+  const int nb = a.lo + split * a.per, ne = min(a.hi, nb + a.per);
   const int nn = ne - nb;
   const int nsub = (nn + SC - 1) / SC;
   const int emax = SC * (a.dslot - 1) > 0 ? SC * (a.dslot - 1) : 1;
-  int* flags = a.flags + bi * a.splits;
+  int* flags = rec ? a.flags + bi * a.splits : nullptr;
   const int64_t stage_stride = (int64_t)NX * ld;
   const int64_t node_stride = (int64_t)(N + 1) * stage_stride;
   float* Wb = a.W + bi * (int64_t)M * node_stride;
@@ -178,17 +179,19 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
     const int64_t pstage = bi * N + n;
     const int eb = nptr[s0 - nb], ee = nptr[s0 - nb + sc];
     const int nE = ee - eb;
-    const float* gas = a.a_self + (pstage * M + s0) * NX * NX;
-    for (int t = tid; t < sc * NX * NX; t += nt) cp_async4(S.as + t, gas + t);
-    if (nE > 0) {
-      const float* gan = a.a_nbr + (pstage * a.E + eb) * NX * NX;
-      for (int t = tid; t < nE * NX * NX; t += nt) cp_async4(S.an + t, gan + t);
-      for (int t = tid; t < nE; t += nt) cp_async4(S.src + t, a.src + eb + t);
+    if (rec) {
+      const float* gas = a.a_self + (pstage * M + s0) * NX * NX;
+      for (int t = tid; t < sc * NX * NX; t += nt) cp_async4(S.as + t, gas + t);
+      if (nE > 0) {
+        const float* gan = a.a_nbr + (pstage * a.E + eb) * NX * NX;
+        for (int t = tid; t < nE * NX * NX; t += nt) cp_async4(S.an + t, gan + t);
+        for (int t = tid; t < nE; t += nt) cp_async4(S.src + t, a.src + eb + t);
+      }
+      const float* gb = a.b + (pstage * M + s0) * NX * NU;
+      for (int t = tid; t < sc * NX * NU; t += nt) cp_async4(S.bb + t, gb + t);
+      const double* gc = a.c + (pstage * M + s0) * NX;
+      for (int t = tid; t < sc * NX; t += nt) cp_async8(S.cc + t, gc + t);
     }
-    const float* gb = a.b + (pstage * M + s0) * NX * NU;
-    for (int t = tid; t < sc * NX * NU; t += nt) cp_async4(S.bb + t, gb + t);
-    const double* gc = a.c + (pstage * M + s0) * NX;
-    for (int t = tid; t < sc * NX; t += nt) cp_async8(S.cc + t, gc + t);
     for (int t = tid; t < sc * NX * NX; t += nt) {
       const int li = t / (NX * NX), e = t - li * NX * NX;
       cp_async8(S.qd + t, a.q + bi * a.q_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX * NX + e);
@@ -203,14 +206,15 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
   if (items > 0) prefetch(0);
 
   // stage 0: Gamma_u = 0, Gamma_x = x0 (condensing.py:205-206)
-  for (int t = tid; t < nn * NX * ld; t += nt) {
-    const int li = t / (NX * ld), rem = t - li * NX * ld, r = rem / ld, col = rem - r * ld;
-    Wb[(int64_t)(nb + li) * node_stride + rem] =
-        (col == XC) ? (float)a.x0[(bi * M + nb + li) * NX + r] : 0.f;
-  }
-  const int d0 = a.dep_ptr[split], d1 = a.dep_ptr[split + 1];
+  if (rec)
+    for (int t = tid; t < nn * NX * ld; t += nt) {
+      const int li = t / (NX * ld), rem = t - li * NX * ld, r = rem / ld, col = rem - r * ld;
+      Wb[(int64_t)(nb + li) * node_stride + rem] =
+          (col == XC) ? (float)a.x0[(bi * M + nb + li) * NX + r] : 0.f;
+    }
+  const int d0 = rec ? a.dep_ptr[split] : 0, d1 = rec ? a.dep_ptr[split + 1] : 0;
   __syncthreads();
-  if (tid == 0) {
+  if (rec && tid == 0) {
     __threadfence();
     st_release(&flags[split], 1);
   }
@@ -237,10 +241,19 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
       Qs[t] = (float)(0.5 * (Qk[r * NX + cc] + Qk[cc * NX + r]));
     }
     const int ebase = nptr[s0 - nb];
+    if (!rec) {
+      // K-HG: the stage-k rows (causal columns + Gamma_x) come from Gamma
+      const int lk1 = k * NU;
+      for (int t = tid; t < sc * NX * ld; t += nt) {
+        const int li = t / (NX * ld), rem = t - li * NX * ld, col = rem % ld;
+        if (col < lk1 || col == XC)
+          Gc[t] = __ldcg(Wb + (int64_t)(s0 + li) * node_stride + (int64_t)k * stage_stride + rem);
+      }
+    }
     // Gamma rows of stage k (condensing.py:213-224), same per-column
     // recursion and FMA order as K-REC: live columns and Gamma_x via the
     // closed neighbourhood, block n <- B_n, zero elsewhere
-    for (int t = tid; t < sc * ld; t += nt) {
+    for (int t = tid; rec && t < sc * ld; t += nt) {
       const int li = t / ld, col = t - li * ld;
       const int i = s0 + li;
       float r6[NX];
@@ -290,7 +303,7 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
       }
     }
     __syncthreads();
-    if (sub == nsub - 1 && tid == 0) {  // all of this CTA's stage-k rows are out
+    if (rec && sub == nsub - 1 && tid == 0) {  // all of this CTA's stage-k rows are out
       __threadfence();
       st_release(&flags[split], k + 1);
     }
@@ -369,7 +382,7 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
   for (int t = tid; t < n0; t += nt) a.partg[(bi * a.splits + split) * n0 + t] = gs[t];
   // the last CTA out resets the stage counters for the next launch
   __syncthreads();
-  if (tid == 0) {
+  if (rec && tid == 0) {
     __threadfence();
     int* done = a.flags + (int64_t)gridDim.x;
     if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
@@ -1010,28 +1023,38 @@ int ensure_flags(gm_ctx* ctx, int64_t n) {
 
 }  // namespace
 
-// K-HG on the tensor cores: the cost part of condense_ocp over the node range
-// [node_lo, node_hi) from a Gamma produced elsewhere (per-stage K-REC, the
-// partitioned driver): k_condense_tc without the recursion, split-K over node
+// K-HG: the cost part of condense_ocp over the node range [node_lo, node_hi)
+// from a Gamma produced elsewhere (per-stage K-REC, the partitioned driver):
+// the fused kernel without the recursion (a.rec = 0), split-K over node
 // ranges (no co-residency requirement), then the shared fixed-order fp64
-// reduction.  partial != 0 leaves out R-bar / r_lin (added by one rank only).
-// Returns 1 (not handled) when the shape has no tensor-core instantiation.
-int gm_tc_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const double* q, int64_t q_stride,
-               const double* x_ref, int64_t xref_stride, const double* r, int64_t r_stride, const double* u_ref,
-               int64_t uref_stride, double* H, double* g, int partial, void* stream) {
+// reduction.  tc != 0 selects k_condense_tc (tcgen05 3xTF32 H), else the SIMT
+// k_condense_fused (fp32 FMA with round-to-nearest accumulation: the tensor
+// core accumulator truncates).  partial != 0 leaves out
+// R-bar / r_lin (added by one rank only).  Returns 1 (not handled) when the
+// shape has no instantiation.
+int gm_fused_cost(gm_ctx* ctx, int tc, int B, int N, const float* gamma, int ld, const double* q,
+                  int64_t q_stride, const double* x_ref, int64_t xref_stride, const double* r,
+                  int64_t r_stride, const double* u_ref, int64_t uref_stride, double* H, double* g,
+                  int partial, void* stream) {
   const int nx = ctx->nx, nu = ctx->n_u, n0 = N * nu;
   const int npairs = N * (N + 1) / 2;
   const int64_t lo = ctx->node_lo, hi = gm_node_hi(ctx), nodes = hi - lo;
-  FusedKernel kern = (n0 <= 128) ? pick_tc_kernel(nx, nu) : nullptr;
+  FusedKernel kern = tc ? ((n0 <= 128) ? pick_tc_kernel(nx, nu) : nullptr)
+                        : (npairs <= 256 ? pick_kernel(nx, nu) : nullptr);
   if (!kern || nodes < 1 || (ld % 4) != 0 || ((uintptr_t)gamma & 15) || ((uintptr_t)q & 15) ||
       ((uintptr_t)x_ref & 15) || (q_stride % 2) != 0 || (xref_stride % 2) != 0)
     return 1;
-  const int SC = 8;
+  const int dslot = (int)ctx->dmax + 1;
+  int SC = tc ? 8 : 16;
+  const int threads = tc ? kTcThreads : 256;
   const int64_t want = std::max<int64_t>(1, (2 * (int64_t)ctx->sm_count + B - 1) / B);
   const int64_t per = std::max<int64_t>(SC, (nodes + want - 1) / want);
+  auto smem_of = [&](int sc_) {
+    return tc ? tc_smem(sc_, nx, nu, dslot, n0, per) : fused_smem(sc_, nx, nu, ld, dslot, n0, per);
+  };
+  while (!tc && SC > 1 && smem_of(SC) > kFusedSmemBudget) SC >>= 1;
   const int splits = (int)((nodes + per - 1) / per);
-  const int dslot = (int)ctx->dmax + 1;
-  const size_t sm = tc_smem(SC, nx, nu, dslot, n0, per);
+  const size_t sm = smem_of(SC);
   if (sm > kFusedSmemBudget) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   GM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -1065,8 +1088,8 @@ int gm_tc_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const doub
   a.rec = 0;
   a.lo = (int)lo;
   a.hi = (int)hi;
-  kern<<<(unsigned)grid, (unsigned)kTcThreads, sm, st>>>(a);
-  GM_LAUNCH_CHECK(ctx, "k_condense_tc(cost)");
+  kern<<<(unsigned)grid, (unsigned)threads, sm, st>>>(a);
+  GM_LAUNCH_CHECK(ctx, tc ? "k_condense_tc(cost)" : "k_condense_fused(cost)");
   PairReduceArgs ra{};
   ra.nu = nu;
   ra.n0 = n0;
@@ -1120,7 +1143,11 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   // (auto mode: from ~512 node rows up; below that, the per-item MMA issue /
   // commit / wait round trip costs more than the SIMT products it replaces:
   // cfg2, M = 100, 0.18 ms tc vs 0.10 ms SIMT; cfg3, M = 1000, equal)
-  const bool tc_ok = ctx->cond_mode == 0 ? (int64_t)B * ctx->M >= 512 : ctx->cond_mode == 3;
+  // Auto mode keeps H on the SIMT kernel: the tcgen05 accumulator truncates
+  // on every add, so at 10^4 nodes the 3xTF32 H drifts to ~7e-5 relative
+  // (u to ~1.5e-4) where the fp32 FMA kernel stays at ~2e-6 (DESIGN.md 4,
+  // scripts/diag_precision.py); gm_set_condense_mode(3) selects tcgen05
+  const bool tc_ok = ctx->cond_mode == 3;
   FusedKernel tck = (n0 <= 128 && tc_ok) ? pick_tc_kernel(nx, nu) : nullptr;
   FusedKernel kern = tck ? tck : pick_kernel(nx, nu);
   const bool whole = ctx->node_lo == 0 && gm_node_hi(ctx) == ctx->M;
@@ -1237,7 +1264,25 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
             tck != nullptr, threads, SC, (long long)per, splits, (long long)grid, occ, sm, fa.numRegs,
             fa.sharedSizeBytes, fa.maxThreadsPerBlock);
   }
-  kern<<<(unsigned)grid, (unsigned)threads, sm, st>>>(a);
+  if (splits > 1) {
+    // CTAs of one instance spin on each other's stage flags: launch
+    // cooperatively so the driver guarantees co-residency (or fails the
+    // launch loudly) even when other work shares the SMs
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)grid);
+    lc.blockDim = dim3((unsigned)threads);
+    lc.dynamicSmemBytes = sm;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    GM_CUDA(ctx, cudaLaunchKernelEx(&lc, kern, a));
+  } else {
+    // one CTA per instance: no inter-CTA waits, any grid size
+    kern<<<(unsigned)grid, (unsigned)threads, sm, st>>>(a);
+  }
   GM_LAUNCH_CHECK(ctx, "k_condense_fused");
   PairReduceArgs ra{};
   ra.nu = nu;

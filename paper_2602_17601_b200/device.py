@@ -85,12 +85,28 @@ class Engine:
         hd, hw, hb = flat(model.phi)
         stats = [np.ascontiguousarray(a, dtype=float) for a in
                  (nrm.state_mean, nrm.state_scale, nrm.input_mean, nrm.input_scale)]
+        from ._runtime import lib
+
+        gen = lib().gm_model_generation(self.ctx.handle)
+        self._model_fp = None  # a failed upload leaves no valid binding
         self.ctx.call("gm_set_model", int(model.n_p), int(model.n_u), int(model.n_m), float(model.dt),
                       len(model.psi.weights), pd.ctypes.data, pw.ctypes.data, pb.ctypes.data,
                       len(model.phi.weights), hd.ctypes.data, hw.ctypes.data, hb.ctypes.data,
                       *[s.ctypes.data for s in stats])
+        if lib().gm_model_generation(self.ctx.handle) != gen:
+            # weight buffers moved (layer dims changed) or a scalar baked into
+            # kernel arguments changed: every captured step graph is stale.
+            # Same-shape parameter edits are copied in place by gm_set_model
+            # and keep the graphs valid.
+            self.drop_graphs()
         self._model_fp = fp
         self._dims = (2 * int(model.n_p), int(model.n_u))
+
+    def drop_graphs(self):
+        """Forget every captured CUDA graph of this engine (StepPlans are
+        re-captured on their next use)."""
+        for key in [k for k in self.cache if isinstance(k, tuple) and k and k[0] == "plan"]:
+            self.cache.pop(key, None)
 
     def set_dims(self, nx: int, nu: int):
         if self._dims != (nx, nu):
@@ -118,11 +134,18 @@ class Engine:
         return self.torch.cuda.current_stream(self.device).cuda_stream
 
 
+def device_index(device=None) -> int:
+    """CUDA device ordinal of ``device`` (None: the current device)."""
+    torch = require_cuda()
+    if device is None:
+        return torch.cuda.current_device()
+    idx = device.index if hasattr(device, "index") else device
+    return torch.cuda.current_device() if idx is None else int(idx)
+
+
 def engine(topo, model=None, device=None) -> Engine:
     """Cached engine for (device, topology); binds ``model`` if given."""
-    torch = require_cuda()
-    dev = torch.cuda.current_device() if device is None else int(
-        device.index if hasattr(device, "index") else device)
+    dev = device_index(device)
     key = (dev, id(topo))
     with _lock:
         eng = _engines.get(key)

@@ -22,6 +22,7 @@ NumPy views are materialised lazily when a caller reads them.
 from __future__ import annotations
 
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -31,7 +32,7 @@ from ._runtime import lib
 from .condensing import fused_device, lin_blocks, rows_device
 from .gnn import LinearizedDynamics, linearize_device
 from .graph import InputVector, SystemState, Trajectory
-from .qpsolver import STATUS_BY_CODE, QpStatus, SolverSettings
+from .qpsolver import STATUS_BY_CODE, QpStatus, SolverSettings, settings_c
 
 
 @dataclass
@@ -200,7 +201,7 @@ class StepPlan:
         self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
         self.graphs = None
         self.graph = None
-        self.settings_c = cfg.solver.as_c()
+        self.settings_c = settings_c(cfg.solver)
 
     def _carve(self, buf):
         M, N, nx, nu = self.M, self.N, self.nx, self.nu
@@ -312,6 +313,9 @@ class StepPlan:
         return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])
 
 
+_MAX_PLANS = 16
+
+
 def get_plan(eng, spec, N, nx, nu, cfg, gnn) -> StepPlan:
     from .condensing import device_spec
 
@@ -335,6 +339,16 @@ def get_plan(eng, spec, N, nx, nu, cfg, gnn) -> StepPlan:
         plan.use_graphs = replay
         plan.runs = 0
         eng.cache[key] = plan
+        if replay:
+            # the plan lives as long as the spec (or the provider token) it
+            # was built for: its buffers and graphs go when the owner goes
+            owner = getattr(spec, "_static_token", None)
+            weakref.finalize(owner if owner is not None else spec, eng.cache.pop, key, None)
+        # bound the number of live plans per engine (each owns a Gamma array
+        # and captured graphs): evict the oldest beyond _MAX_PLANS
+        plans = [k for k in eng.cache if isinstance(k, tuple) and k and k[0] == "plan"]
+        for k in plans[:-_MAX_PLANS]:
+            eng.cache.pop(k, None)
     return plan
 
 

@@ -79,8 +79,14 @@ class SolverSettings:
             raise ValueError("tolerance must be positive")
 
     def as_c(self) -> QpSettingsC:
-        return QpSettingsC(float(self.tolerance), int(self.max_iterations),
-                           float(self.regularization), float(self.fraction_to_boundary))
+        return settings_c(self)
+
+
+def settings_c(s) -> QpSettingsC:
+    """The C struct of any SolverSettings-like object (ours or the
+    reference's, qpsolver.py:66-76)."""
+    return QpSettingsC(float(s.tolerance), int(s.max_iterations), float(s.regularization),
+                       float(s.fraction_to_boundary))
 
 
 @dataclass
@@ -107,7 +113,7 @@ def solve_qp_device(eng, H, g, C, d, warm, settings: SolverSettings, B: int = 1)
     st = eng.empty((B,), np.int32)
     it = eng.empty((B,), np.int32)
     rs = eng.empty((B, 3), np.float64)
-    cs = settings.as_c()
+    cs = settings_c(settings)
     eng.ctx.call("gm_solve_qp", B, n, m, H.data_ptr(), g.data_ptr(),
                  C.data_ptr() if C.numel() else None, d.data_ptr() if d.numel() else None,
                  warm.data_ptr() if warm is not None else None, ctypes.byref(cs), u.data_ptr(),

@@ -11,7 +11,7 @@ import numpy as np
 
 from paper_2602_17601_b200.condensing import OcpSpec, StateConstraint
 from paper_2602_17601_b200.gnn import GnnModel, LinearizedDynamics, Normalization
-from paper_2602_17601_b200.graph import GraphTopology, chain_topology
+from paper_2602_17601_b200.graph import GraphTopology, chain_topology, mesh_topology
 from paper_2602_17601_b200.mlp import MlpParams
 
 DIR = Path(__file__).resolve().parent / "golden"
@@ -64,11 +64,12 @@ def spec_from(d, topo, prefix=""):
 
 
 def pipeline_case(name):
-    """A full-pipeline fixture (cfg1 / P3 / P4) as objects + expected arrays."""
+    """A full-pipeline fixture (cfg1 / P3 / P4 chains, mesh6x5 / mesh_p3
+    4-neighbour grids) as objects + expected arrays."""
     d = load(name)
     model = model_from(d)
     M = d["states"].shape[1]
-    topo = chain_topology(M)
+    topo = mesh_topology(*(int(v) for v in d["mesh"])) if "mesh" in d else chain_topology(M)
     spec = spec_from(d, topo)
     return SimpleNamespace(d=d, model=model, topo=topo, spec=spec, states=d["states"],
                            inputs=d["inputs"], x0=d["states"][0])
@@ -111,3 +112,48 @@ def rel(a, b):
     if b.size == 0:
         return 0.0
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def mpc_branch_cases():
+    """mpc_step sequences of the reference under non-default MpcConfig
+    branches (oracle/make_golden.py round2): returns (model, topo, spec,
+    bad_spec, x_seq, {case: [step dicts]})."""
+    d = load("mpc_branches")
+    model = model_from(d)
+    M = d["states"].shape[1]
+    topo = chain_topology(M)
+    spec = spec_from(d, topo)
+    bad = OcpSpec(topo, spec.horizon, spec.q, spec.x_ref, spec.r, spec.u_ref,
+                  spec.input_constraints,
+                  list(spec.state_constraints) + [StateConstraint(0, 1, d["bad_row_c"], d["bad_row_d"])])
+    cases = {}
+    for c in d["cases"]:
+        c = str(c)
+        steps = []
+        for t in range(int(d[c + "_steps"])):
+            p = f"{c}_{t}_"
+            steps.append({k: d[p + k] for k in ("u", "lin_states", "lin_inputs", "planned_states",
+                                                "planned_inputs", "last_applied", "filtered", "meta")})
+        cases[c] = steps
+    return SimpleNamespace(model=model, topo=topo, spec=spec, bad=bad, x_seq=d["x_seq"], cases=cases)
+
+
+def qp_round2():
+    d = load("qp_round2")
+
+    def get(prefix):
+        out, t = [], 0
+        while f"{prefix}{t}_H" in d:
+            p = f"{prefix}{t}_"
+            out.append(SimpleNamespace(H=d[p + "H"], g=d[p + "g"], C=d[p + "C"], d=d[p + "d"],
+                                       u=d[p + "u"], duals=d[p + "duals"],
+                                       status=STATUS[int(d[p + "meta"][0])],
+                                       iterations=int(d[p + "meta"][1]),
+                                       cap=int(d[p + "meta"][2]) if d[p + "meta"].size > 2 else 50))
+            t += 1
+        return out
+
+    return SimpleNamespace(cap=get("cap"), batch=get("b"), infeas_u=d["infeas_u"],
+                           infeas_status=STATUS[int(d["infeas_meta"][0])],
+                           infeas_iterations=int(d["infeas_meta"][1]),
+                           infeas_primal=float(d["infeas_meta"][2]))

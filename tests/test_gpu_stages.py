@@ -9,15 +9,20 @@ Tolerances (fp32 stages vs the fp64 reference):
   u* through the whole pipeline        max|du| / max(1, max|u|) <= 1e-4
 """
 
+from types import SimpleNamespace
+
 import numpy as np
 import pytest
 
-from tests.golden_io import STATUS, pipeline_case, random_condense_cases, random_qps, rel
+from tests.golden_io import (STATUS, mpc_branch_cases, pipeline_case, qp_round2,
+                             random_condense_cases, random_qps, rel)
 
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-4
-CASES = ["cfg1_chain10", "p3_biases_norm", "p4_interior"]
+# chains (cfg1 recipe, P3 biases + normalisation, P4 interior QP) and
+# 4-neighbour meshes (cfg5 recipe 6x5, P3-style 4x4 with hard + soft rows)
+CASES = ["cfg1_chain10", "p3_biases_norm", "p4_interior", "mesh6x5", "mesh_p3"]
 
 
 @pytest.fixture(scope="module")
@@ -160,13 +165,30 @@ def test_random_qps(pkg):
 
 
 def test_qp_batched_matches_single(pkg):
-    qs = [q for q in random_qps() if q.H.shape[0] == 3 and q.C.shape[0] == 4]
-    if len(qs) < 2:
-        pytest.skip("fixture has too few same-shape QPs")
+    """Eight same-shape reference QPs (n=5, m=7) in one batched launch (one
+    CTA each) against the reference's solutions and the single-QP path."""
+    qs = qp_round2().batch
     sols = pkg.solve_qp_batched(np.stack([q.H for q in qs]), np.stack([q.g for q in qs]),
                                 np.stack([q.C for q in qs]), np.stack([q.d for q in qs]))
-    for q, s in zip(qs, sols):
-        assert np.max(np.abs(s.u - q.u)) <= 1e-6
+    for t, (q, s) in enumerate(zip(qs, sols)):
+        assert s.status.value == q.status, t
+        assert abs(s.iterations - q.iterations) <= 1, t
+        assert np.max(np.abs(s.u - q.u)) <= 1e-6, t
+        one = pkg.solve_qp(pkg.QpProblem(q.H, q.g, q.C, q.d))
+        assert np.array_equal(one.u, s.u) and one.iterations == s.iterations, t
+
+
+def test_qp_best_iterate_at_cap(pkg):
+    """The iteration cap returns the best iterate found (qpsolver.py:231-235,
+    reference tests/test_qpsolver.py:127-134): caps 1, 2, 3, 5 against the
+    reference's own returned iterate."""
+    for t, q in enumerate(qp_round2().cap):
+        s = pkg.solve_qp(pkg.QpProblem(q.H, q.g, q.C, q.d),
+                         pkg.SolverSettings(max_iterations=q.cap))
+        assert s.status.value == q.status, (t, s.status, q.status)
+        assert s.iterations == q.iterations, t
+        assert np.all(np.isfinite(s.u))
+        assert np.max(np.abs(s.u - q.u)) <= 1e-9 * max(1.0, np.max(np.abs(q.u))), t
 
 
 def test_qp_known_answers(pkg):
@@ -177,8 +199,13 @@ def test_qp_known_answers(pkg):
     assert abs(s.u[0] - 0.5) <= 1e-7 and abs(s.duals[0] - 1.0) <= 1e-6
     s = pkg.solve_qp(pkg.QpProblem(np.array([[1.0]]), np.zeros(1), np.array([[1.0], [-1.0]]),
                                    np.array([-1.0, -2.0])))
-    assert s.status in (pkg.QpStatus.PRIMAL_INFEASIBLE, pkg.QpStatus.MAX_ITERATIONS)
-    assert s.primal_infeas > 1e-3
+    # the reference returns PRIMAL_INFEASIBLE after 6 iterations with the best
+    # iterate u = 0 (fixture qp_round2, qpsolver.py:163-165)
+    q2 = qp_round2()
+    assert s.status.value == q2.infeas_status == "primal_infeasible"
+    assert s.iterations == q2.infeas_iterations
+    assert np.array_equal(s.u, q2.infeas_u)
+    assert abs(s.primal_infeas - q2.infeas_primal) <= 1e-12
 
 
 @pytest.mark.parametrize("name", CASES)
@@ -269,3 +296,126 @@ def test_plugin_linearizer_and_reference_style_state(pkg):
     sol = O.solve_qp(H, g, C, d, warm_start=np.zeros(H.shape[0]))
     assert st1.last_status.value == sol.status
     assert np.max(np.abs(u.u - sol.u[:6])) <= 1e-4 * max(1.0, np.max(np.abs(sol.u)))
+
+
+# ---------------------------------------------------------------------------
+# mpc_step branches (reference mpc.py:129-200): SQP loop, damping, input
+# filter, cold start, both fallback policies (forced primal-infeasible QP)
+# ---------------------------------------------------------------------------
+BRANCH_CFG = {"sqp2": dict(sqp_iterations=2), "damp": dict(sqp_damping=0.5),
+              "sqp2damp": dict(sqp_iterations=2, sqp_damping=0.5),
+              "filter": dict(input_filter_tau=0.05), "fbhold": {},
+              "fbzero": dict(fallback="zero-input"), "fbfirst": {}, "coldstart": dict(warm_start=False)}
+BRANCH_SPECS = {"fbhold": ("spec", "bad", "spec"), "fbzero": ("spec", "bad", "spec"),
+                "fbfirst": ("bad", "spec")}
+
+
+@pytest.mark.parametrize("case", sorted(BRANCH_CFG))
+def test_mpc_step_branches_match_reference(pkg, case):
+    bc = mpc_branch_cases()
+    steps = bc.cases[case]
+    N = bc.spec.horizon
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01, **BRANCH_CFG[case])
+    names = BRANCH_SPECS.get(case, ("spec",) * len(steps))
+    st = pkg.mpc_init(pkg.SystemState(bc.x_seq[0]), cfg, 6)
+    prev_applied = None
+    for t, ref in enumerate(steps):
+        u, st = pkg.mpc_step(bc.model, bc.topo, getattr(bc, names[t]), pkg.SystemState(bc.x_seq[t]),
+                             st, cfg)
+        info = (case, t)
+        assert st.last_status.value == STATUS[int(ref["meta"][0])], info
+        assert abs(st.last_iterations - int(ref["meta"][1])) <= cfg.sqp_iterations, info
+        scale = max(1.0, float(np.max(np.abs(ref["u"]))))
+        assert float(np.max(np.abs(u.u - ref["u"]))) / scale <= TOL, info
+        assert float(np.max(np.abs(st.last_applied - ref["last_applied"]))) / scale <= TOL, info
+        assert rel(st.lin_states, ref["lin_states"]) <= TOL, info
+        assert float(np.max(np.abs(st.lin_inputs - ref["lin_inputs"]))) / scale <= TOL, info
+        assert rel(st.planned_states, ref["planned_states"]) <= TOL, info
+        assert float(np.max(np.abs(st.planned_inputs - ref["planned_inputs"]))) / scale <= TOL, info
+        if ref["filtered"].size:
+            assert float(np.max(np.abs(st.filtered_input - ref["filtered"]))) / scale <= TOL, info
+        if STATUS[int(ref["meta"][0])] == "primal_infeasible":
+            # the fallback input is exact: this controller's own held input
+            # (hold-previous-input after a solved step) or zeros
+            expect = prev_applied if (cfg.fallback == "hold-previous-input"
+                                      and prev_applied is not None) else np.zeros(6)
+            assert np.array_equal(u.u, expect), info
+        prev_applied = np.array(st.last_applied)
+
+
+# ---------------------------------------------------------------------------
+# known-answer tests of the reference suite on the GPU path
+# ---------------------------------------------------------------------------
+
+def test_relu_subgradient_zero_at_kink(pkg):
+    """Pre-activations exactly 0 take derivative 0 (mlp.py:143 strict > 0,
+    reference tests/test_mlp.py:84-90): zero biases, zero normalisation mean
+    and the all-zero linearisation point make every pre-activation of psi and
+    phi exactly 0, so every Jacobian vanishes and A = [[I, dt I],[0, I]],
+    A_nbr = 0, B = 0 exactly, for every linearisation kernel."""
+    rng = np.random.default_rng(8)
+    topo = pkg.chain_topology(5)
+    model = pkg.init_model(3, 6, 0.02, rng, n_m=16, psi_hidden=(32, 32), phi_hidden=(64, 64))
+    N = 3
+    expect = np.block([[np.eye(3), 0.02 * np.eye(3)], [np.zeros((3, 3)), np.eye(3)]])
+    for mode in (1, 2, 3, 4):
+        _set_lin_mode(pkg, SimpleNamespace(topo=topo, model=model), mode)
+        try:
+            lin = pkg.linearize_trajectory(model, topo, np.zeros((N, 5, 6)), np.zeros((N, 6)))
+        finally:
+            _set_lin_mode(pkg, SimpleNamespace(topo=topo, model=model), 0)
+        # blocks are stored in fp32: exactly the fp32 rounding of the expectation
+        e32 = expect.astype(np.float32).astype(float)
+        assert np.array_equal(lin.a_self, np.broadcast_to(e32, lin.a_self.shape)), mode
+        assert not np.any(lin.a_nbr) and not np.any(lin.b) and not np.any(lin.c), mode
+    # just above the kink the derivative is 1 (the reference's J_pos case):
+    # a point with every pre-activation > 0 must give non-zero Jacobians
+    lin = pkg.linearize_trajectory(model, topo, np.full((N, 5, 6), 1e-3), np.full((N, 6), 1e-3))
+    assert np.any(lin.b)
+
+
+def test_linearize_zero_network_blocks(pkg):
+    """All-zero weights (reference tests/test_gnn.py:157-166): A = [[I, dt I],
+    [0, I]], B = 0, c = 0, A_nbr = 0 at any point."""
+    from paper_2602_17601_b200.mlp import MlpParams
+
+    rng = np.random.default_rng(2)
+    m0 = pkg.init_model(2, 3, 0.04, rng, n_m=4, psi_hidden=(6,), phi_hidden=(6,))
+
+    def zero(mlp):
+        return MlpParams(list(mlp.layer_dims), [np.zeros_like(W) for W in mlp.weights],
+                         [np.zeros_like(b) for b in mlp.biases])
+
+    model = pkg.GnnModel(zero(m0.psi), zero(m0.phi), 0.04, 2, 3, 4, m0.normalization)
+    topo = pkg.chain_topology(3)
+    lin = pkg.linearize_trajectory(model, topo, np.ones((1, 3, 4)), np.zeros((1, 3)))
+    expected = np.block([[np.eye(2), 0.04 * np.eye(2)], [np.zeros((2, 2)), np.eye(2)]])
+    e32 = expected.astype(np.float32).astype(float)  # blocks are stored in fp32
+    for i in range(3):
+        assert np.array_equal(lin.a_self[0, i], e32)
+        assert not np.any(lin.b[0, i])
+        # c = f - A x - B u in fp64 from the stored fp32 blocks: fp32(dt) * x
+        # leaves ~1e-9 (the reference test's own check is allclose(c, 0))
+        assert np.allclose(lin.c[0, i], 0)
+    assert not np.any(lin.a_nbr)
+
+
+def test_single_node_ignores_edge_function(pkg):
+    """A single node has no edges, so psi never enters (reference
+    tests/test_gnn.py:75-84): step_array and the linearisation are bitwise
+    independent of the psi weights."""
+    rng = np.random.default_rng(4)
+    topo = pkg.chain_topology(1)
+    m1 = pkg.init_model(2, 3, 0.02, rng, n_m=4, psi_hidden=(6,), phi_hidden=(6,))
+    m2 = m1.copy()
+    for w in m2.psi.weights:
+        w[...] = rng.standard_normal(w.shape)
+    x = rng.standard_normal((2, 1, 4))
+    u = rng.standard_normal((2, 3))
+    f1 = pkg.step_array(m1, topo, x, u)
+    f2 = pkg.step_array(m2, topo, x, u)
+    assert np.array_equal(f1, f2)
+    l1 = pkg.linearize_trajectory(m1, topo, x, u)
+    l2 = pkg.linearize_trajectory(m2, topo, x, u)
+    for k in ("a_self", "b", "c"):
+        assert np.array_equal(getattr(l1, k), getattr(l2, k)), k

@@ -7,10 +7,18 @@ import numpy as np
 import pytest
 
 from oracle import ref_port as O
-from tests.golden_io import (STATUS, load, pipeline_case, random_condense_cases, random_qps, rel,
-                             topo_from_ptr)
+from tests.golden_io import (STATUS, load, mpc_branch_cases, pipeline_case, qp_round2,
+                             random_condense_cases, random_qps, rel, topo_from_ptr)
 
-CASES = ["cfg1_chain10", "p3_biases_norm", "p4_interior"]
+CASES = ["cfg1_chain10", "p3_biases_norm", "p4_interior", "mesh6x5", "mesh_p3"]
+
+# MpcConfig of each reference branch sequence (oracle/make_golden.py round2)
+BRANCH_CFG = {"sqp2": dict(sqp_iterations=2), "damp": dict(sqp_damping=0.5),
+              "sqp2damp": dict(sqp_iterations=2, sqp_damping=0.5),
+              "filter": dict(input_filter_tau=0.05), "fbhold": {},
+              "fbzero": dict(fallback="zero-input"), "fbfirst": {}, "coldstart": dict(warm_start=False)}
+BRANCH_SPECS = {"fbhold": ("spec", "bad", "spec"), "fbzero": ("spec", "bad", "spec"),
+                "fbfirst": ("bad", "spec")}
 
 
 @pytest.mark.parametrize("name", CASES)
@@ -147,3 +155,44 @@ def test_oracle_closed_loop_matches_reference():
     assert np.array_equal(iters, d["iterations"])
     assert np.max(np.abs(inputs - d["inputs"])) <= 1e-7
     assert np.max(np.abs(states - d["states"])) <= 1e-9
+
+
+@pytest.mark.parametrize("case", sorted(BRANCH_CFG))
+def test_oracle_mpc_branches_match_reference(case):
+    """The oracle's mpc_step under the SQP loop, damping, input filter,
+    cold start and both fallback policies equals the reference's
+    (mpc.py:129-200)."""
+    bc = mpc_branch_cases()
+    steps = bc.cases[case]
+    kw = dict(BRANCH_CFG[case])
+    N = bc.spec.horizon
+    tau = kw.pop("input_filter_tau", None)
+    warm = kw.pop("warm_start", True)
+    names = BRANCH_SPECS.get(case, ("spec",) * len(steps))
+    ls, li = np.tile(bc.x_seq[0], (N + 1, 1, 1)), np.zeros((N, 6))
+    last, filt = None, None
+    for t, ref in enumerate(steps):
+        spec = getattr(bc, names[t])
+        out = O.mpc_step(bc.model, bc.topo, spec, bc.x_seq[t], ls, li, N, warm_start=warm,
+                         last_applied=last, input_filter_tau=tau, filtered_input=filt, dt=0.01, **kw)
+        assert out["status"] == STATUS[int(ref["meta"][0])], (case, t)
+        assert out["iterations"] == int(ref["meta"][1]), (case, t)
+        assert np.max(np.abs(out["u_applied"] - ref["u"])) <= 1e-8, (case, t)
+        assert np.max(np.abs(out["lin_states"] - ref["lin_states"])) <= 1e-9, (case, t)
+        assert np.max(np.abs(out["lin_inputs"] - ref["lin_inputs"])) <= 1e-8, (case, t)
+        assert np.max(np.abs(out["planned_states"] - ref["planned_states"])) <= 1e-9, (case, t)
+        ls, li, last, filt = out["lin_states"], out["lin_inputs"], out["u_applied"], out["filtered_input"]
+
+
+def test_oracle_qp_round2_fixtures():
+    """Best iterate at the iteration cap (tests/test_qpsolver.py:127-134),
+    same-shape batches, the infeasible KAT (:119-124)."""
+    q2 = qp_round2()
+    for t, q in enumerate(q2.cap + q2.batch):
+        sol = O.solve_qp(q.H, q.g, q.C, q.d, max_iterations=q.cap)
+        assert sol.status == q.status and sol.iterations == q.iterations, t
+        assert np.max(np.abs(sol.u - q.u)) <= 1e-9, t
+    sol = O.solve_qp(np.array([[1.0]]), np.zeros(1), np.array([[1.0], [-1.0]]), np.array([-1.0, -2.0]))
+    assert sol.status == q2.infeas_status == "primal_infeasible"
+    assert sol.iterations == q2.infeas_iterations
+    assert np.array_equal(sol.u, q2.infeas_u)
