@@ -184,6 +184,22 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
                       const double* r, int64_t r_stride, const double* u_ref, int64_t uref_stride,
                       double* H, double* g, void* stream);
 
+/* ---- per-node condensing (condensing.py:231-243, :285-295, :334-360) --- */
+/* local_hessian_gradient for every node of the node range [lo, hi) of every
+ * instance: H (B, nodes, n0, n0) = sum_k Gu_k' Qs_k Gu_k (Qs = (Q + Q')/2,
+ * i.e. the reference's symmetrised 0.5 (h + h')) and g (B, nodes, n0) =
+ * sum_k Gu_k' (2 Q_k Gx_k + q_lin_k), fp64, from the fp32 work array (all
+ * N+1 stages, all n0 columns).  q (B, M, N+1, nx, nx), q_lin (B, M, N+1, nx)
+ * fp64 device, per-instance strides in elements (0 broadcasts). */
+int gm_node_hessians(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const double* q,
+                     int64_t q_stride, const double* q_lin, int64_t qlin_stride, double* H,
+                     double* g, void* stream);
+/* assemble_qp's node sum (condensing.py:344-355): dst (B, len) = base (B,
+ * len, may be NULL) + sum_{i < count} src (B, count, len), ascending i, fp64;
+ * sym_n > 0 (len = sym_n^2) returns the symmetrised 0.5 (S + S'). */
+int gm_sum_nodes(gm_ctx* ctx, int B, int count, int len, int sym_n, const double* src,
+                 const double* base, double* dst, void* stream);
+
 /* Constraint rows (condensing.py:263-282, :312-323), per instance:
  * rows [0, n_in) are input rows: row k has coefficients in_c (nu) at
  * column block in_stage[k]; rows [n_in, n_in+n_st) are state rows:
@@ -267,6 +283,20 @@ int gm_gather_rows(gm_ctx* ctx, const void* src, void* dst, const int32_t* idx, 
 int gm_scatter_rows(gm_ctx* ctx, const void* src, void* dst, const int32_t* idx, int n_idx,
                     int64_t row_bytes, int64_t row_stride_bytes, int n_outer,
                     int64_t outer_stride_bytes, void* stream);
+
+/* ---- batched training gradients (training.py:99-150) ------------------ */
+/* Number of model parameters (psi weights, psi biases, phi weights, phi
+ * biases), the length of gm_loss_gradients' grads; -1 without a model. */
+int gm_param_count(const gm_ctx* ctx);
+/* loss_gradients for a batch of B records with the context's model and
+ * graph, fp64: X, Xn (B, M, nx), U (B, nu), weights (M, nx) (the diagonal of
+ * O per node, training.py:_weight_grid) device.  loss (1) device receives
+ * sum(W r^2)/B + l2 |p|^2; grads (gm_param_count) device, in the order of
+ * training.py:_params: every psi weight matrix (out, in) row-major, psi
+ * biases, phi weights, phi biases.  Deterministic (fixed-order sums). */
+int gm_loss_gradients(gm_ctx* ctx, int B, const double* X, const double* U, const double* Xn,
+                      const double* weights, double l2_lambda, double* loss, double* grads,
+                      void* stream);
 
 /* ---- cfg2 plant: trunk.py chain (trunk.py:116-160) ------------------------ */
 /* One controller period (substeps semi-implicit Euler substeps of dt_sim) of B

@@ -543,12 +543,96 @@ def round2():
         print(f, (OUT / f"{f}.npz").stat().st_size)
 
 
+def local_condense():
+    """Per-node condensing of the reference (condensing.py:231-360):
+    condense_local + assemble_qp on P2-family random instances (degree <= 2,
+    constraints, soft rows) and on the P3-style mesh, every node's h, g and
+    rows plus the assembled QP."""
+    rc, rex, rg, rgr, rmlp, rm, rq = _ref()
+    out = {}
+    rng = np.random.default_rng(17)
+    for t in range(6):
+        spec, lin, x0 = random_instance(rng, rc, rg, rgr, with_constraints=(t % 3 != 2))
+        p = f"c{t}_"
+        out[p + "nbr_ptr"] = np.concatenate([[0], np.cumsum([len(n) for n in lin.topology.in_neighbors])])
+        out[p + "nbr_list"] = np.array([j for ns in lin.topology.in_neighbors for j in ns], dtype=np.int64)
+        for k in ("a_self", "a_nbr", "b", "c"):
+            out[p + k] = getattr(lin, k)
+        out[p + "x0"] = x0
+        _spec_arrays(p, spec, out)
+        locs = rc.condense_local(spec, lin, x0)
+        out[p + "h"] = np.stack([lc.h for lc in locs])
+        out[p + "g"] = np.stack([lc.g for lc in locs])
+        out[p + "rows"] = np.array([lc.c_rows.shape[0] for lc in locs])
+        n0 = spec.horizon * spec.n_u
+        out[p + "c_rows"] = np.concatenate([lc.c_rows for lc in locs]) if locs else np.zeros((0, n0))
+        out[p + "d_rows"] = np.concatenate([lc.d_rows for lc in locs])
+        qa = rc.assemble_qp(spec, locs)
+        for k in ("h", "g", "c", "d", "soft", "rho1", "rho2"):
+            out[p + "qa_" + k] = getattr(qa, k)
+        # the single-node API on node 0's maps and cost
+        cost = rc.cost_to_standard_form(spec)
+        h0, g0 = rc.local_hessian_gradient(locs[0].gamma_u, locs[0].gamma_x, cost.q_blocks[0],
+                                           cost.q_lin[0])
+        out[p + "lhg_h"], out[p + "lhg_g"] = h0, g0
+    np.savez_compressed(OUT / "local_condense.npz", **out)
+    print("local_condense", (OUT / "local_condense.npz").stat().st_size)
+
+
+def training_grads():
+    """The reference's loss_gradients (training.py:99-150) on three
+    instances: the reference FD test's tiny model (chain 2, l2 1e-3), the
+    cfg architecture on a chain of 5, and a 3x3 mesh with random biases and
+    normalisation; batch losses and every gradient."""
+    sys.path.insert(0, str(REF))
+    import gnnmpc.gnn as rg
+    import gnnmpc.graph as rgr
+    import gnnmpc.training as rt
+
+    out = {}
+    rng = np.random.default_rng(2)
+    cases = []
+    m = rg.init_model(1, 2, 0.05, rng, n_m=3, psi_hidden=(5,), phi_hidden=(6,))
+    cases.append(("fd", rgr.chain_topology(2), m, 6, np.array([2.0, 0.5]), 1e-3))
+    m = rg.init_model(3, 6, 0.01, rng, n_m=16, psi_hidden=(32, 32), phi_hidden=(64, 64), out_scale=0.05)
+    cases.append(("cfg", rgr.chain_topology(5), m, 16, None, 1e-6))
+    m = rg.init_model(3, 6, 0.02, rng, n_m=8, psi_hidden=(16, 12), phi_hidden=(24, 20), out_scale=0.3)
+    for mlp in (m.psi, m.phi):
+        for b in mlp.biases:
+            b[...] = 0.2 * rng.standard_normal(b.shape)
+    m.normalization = rg.Normalization(0.1 * rng.standard_normal(6), rng.random(6) + 0.5,
+                                       rng.standard_normal(6), rng.random(6) + 0.5)
+    cases.append(("mesh", _ref_mesh(rgr, 3, 3), m, 9, np.linspace(0.5, 2.0, 6), 0.0))
+    names = []
+    for name, topo, model, B, w, lam in cases:
+        M, nx = topo.node_count, 2 * model.n_p
+        X = rng.standard_normal((B, M, nx)) * 0.3
+        U = rng.standard_normal((B, model.n_u))
+        Xn = X + 0.05 * rng.standard_normal((B, M, nx))
+        W = rt._weight_grid(w, M, nx)
+        L, grads = rt.loss_gradients(model, topo, X, U, Xn, W, lam)
+        p = name + "_"
+        _model_arrays(p + "m_", model, out)
+        out[p + "nbr_ptr"] = np.concatenate([[0], np.cumsum([len(n) for n in topo.in_neighbors])])
+        out[p + "nbr_list"] = np.array([j for ns in topo.in_neighbors for j in ns], dtype=np.int64)
+        out[p + "X"], out[p + "U"], out[p + "Xn"], out[p + "W"] = X, U, Xn, W
+        out[p + "lam"] = np.array(lam)
+        out[p + "loss"] = np.array(L)
+        out[p + "grads"] = np.concatenate([g.ravel() for g in grads])
+        names.append(name)
+    out["cases"] = np.array(names)
+    np.savez_compressed(OUT / "training_grads.npz", **out)
+    print("training_grads", (OUT / "training_grads.npz").stat().st_size)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "cfg2":
         cfg2_closed_loop()
         raise SystemExit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "round2":
         round2()
+        local_condense()
+        training_grads()
         raise SystemExit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "obstacle":
         obstacle_provider()

@@ -127,6 +127,56 @@ def _forward_parts(model, topo, X, U):
     return ef, agg, z, mlp_apply(model.phi, z)
 
 
+# --------------------------------------------------------------------------
+# training gradients (training.py:99-150)
+# --------------------------------------------------------------------------
+
+def _mlp_backward(params, x, g_out):
+    """Reverse mode of mlp_apply (mlp.py:110-129): weight / bias gradients
+    summed over the batch and the input gradient."""
+    _, pres = mlp_apply(params, x, keep_pre=True)
+    n = len(params.weights)
+    acts = [x] + [np.maximum(z, 0.0) for z in pres[:-1]]
+    gw, gb = [None] * n, [None] * n
+    g = g_out
+    for l in range(n - 1, -1, -1):
+        if l != n - 1:
+            g = g * (pres[l] > 0.0)
+        gf = g.reshape(-1, g.shape[-1])
+        gw[l] = gf.T @ acts[l].reshape(-1, acts[l].shape[-1])
+        gb[l] = gf.sum(axis=0)
+        g = g @ params.weights[l]
+    return gw, gb, g
+
+
+def loss_gradients(model, topo, X, U, Xn, weights, l2_lambda):
+    """Batch loss sum(W r^2)/B + lambda |p|^2 and its gradient, order psi W,
+    psi b, phi W, phi b (training.py:99-150)."""
+    B, n_p = X.shape[0], model.n_p
+    dst, src, gather = edge_lists(topo)
+    ef, agg, z, dv = _forward_parts(model, topo, X, U)
+    v1 = X[..., n_p:] + dv
+    p1 = X[..., :n_p] + model.dt * v1
+    r = np.concatenate([p1, v1], axis=-1) - Xn
+    loss = float(np.sum(weights * r * r) / B)
+    gp = 2.0 * weights * r / B
+    g_dv = gp[..., n_p:] + model.dt * gp[..., :n_p]
+    gw_phi, gb_phi, g_z = _mlp_backward(model.phi, z, g_dv)
+    if dst.size:
+        nx = X.shape[-1]
+        g_msg = g_z[..., nx:nx + model.n_m][..., dst, :]
+        gw_psi, gb_psi, _ = _mlp_backward(model.psi, ef, g_msg)
+    else:
+        gw_psi = [np.zeros_like(W) for W in model.psi.weights]
+        gb_psi = [np.zeros_like(b) for b in model.psi.biases]
+    grads = gw_psi + gb_psi + gw_phi + gb_phi
+    if l2_lambda > 0:
+        params = model.psi.weights + model.psi.biases + model.phi.weights + model.phi.biases
+        grads = [g + 2.0 * l2_lambda * p for g, p in zip(grads, params)]
+        loss += l2_lambda * sum(float(np.sum(p * p)) for p in params)
+    return loss, grads
+
+
 def step_array(model, topo, X, U):
     """One model step, velocity first then position (gnn.py:153-159)."""
     n_p = model.n_p
@@ -328,6 +378,50 @@ def condense_ocp(spec, lin, x0, threads=1, gammas=None):
     return SimpleNamespace(h=0.5 * (H + H.T), g=g, c=np.vstack(Cs), d=np.concatenate(ds),
                            soft=np.concatenate(soft), rho1=np.concatenate(r1),
                            rho2=np.concatenate(r2))
+
+
+def local_hessian_gradient(gamma_u, gamma_x, q_blocks, q_lin):
+    """One node's symmetrised Hessian and gradient (condensing.py:231-243):
+    h = sum_k Gu_k' Q_k Gu_k over all N+1 stages, g = sum_k Gu_k' w_k with
+    w_k = 2 Q_k Gx_k + q_lin_k."""
+    h = np.zeros((gamma_u.shape[-1],) * 2)
+    g = np.zeros(gamma_u.shape[-1])
+    for k in range(gamma_u.shape[0]):
+        G = gamma_u[k]
+        h += G.T @ (q_blocks[k] @ G)
+        g += G.T @ (2.0 * q_blocks[k] @ gamma_x[k] + q_lin[k])
+    return 0.5 * (h + h.T), g
+
+
+def condense_local(spec, lin, x0):
+    """Per-node (node, h, g, rows) after the recursion (condensing.py:285-295)."""
+    q_lin, _ = standard_form(spec)
+    gu, gx = condense_gammas(lin, x0)
+    n_cols = spec.horizon * spec.r.shape[-1]
+    out = []
+    for i in range(spec.topology.node_count):
+        h, g = local_hessian_gradient(gu[i], gx[i], spec.q[i], q_lin[i])
+        rows = node_rows(spec, i, gu[i], gx[i], n_cols)
+        out.append(SimpleNamespace(node=i, gamma_u=gu[i], gamma_x=gx[i], h=h, g=g, c_rows=rows[0],
+                                   d_rows=rows[1], soft=rows[2], rho1=rows[3], rho2=rows[4]))
+    return out
+
+
+def assemble_qp(spec, locals_):
+    """R-bar plus the node contributions in list order, symmetrised; input
+    rows then each node's rows (condensing.py:334-360)."""
+    H, g = r_bar(spec)
+    g = g.copy()
+    for lc in locals_:
+        H = H + lc.h
+        g = g + lc.g
+    cu, du = input_rows(spec)
+    return SimpleNamespace(
+        h=0.5 * (H + H.T), g=g, c=np.vstack([cu] + [lc.c_rows for lc in locals_]),
+        d=np.concatenate([du] + [lc.d_rows for lc in locals_]),
+        soft=np.concatenate([np.zeros(cu.shape[0], dtype=bool)] + [lc.soft for lc in locals_]),
+        rho1=np.concatenate([np.zeros(cu.shape[0])] + [lc.rho1 for lc in locals_]),
+        rho2=np.concatenate([np.zeros(cu.shape[0])] + [lc.rho2 for lc in locals_]))
 
 
 def expand_soft_constraints(qp):

@@ -16,8 +16,9 @@ from .gnn import (GnnModel, LinearizedDynamics, Normalization, gnn_step, init_mo
                   step_array)
 from .mlp import MlpParams, mlp_init
 from .qpsolver import QpProblem, QpSolution, QpStatus, SolverSettings, solve_qp, solve_qp_batched
-from .condensing import (CondensedQp, OcpSpec, StateConstraint, condense_gammas, condense_ocp,
-                         cost_to_standard_form, expand_soft_constraints, reconstruct_states,
+from .condensing import (CondensedQp, LocalCondensed, OcpSpec, StateConstraint, assemble_qp,
+                         condense_gammas, condense_local, condense_ocp, cost_to_standard_form,
+                         expand_soft_constraints, local_hessian_gradient, reconstruct_states,
                          stage_input_box)
 from .mpc import (ClosedLoopLog, MpcConfig, MpcState, StepTiming, mpc_init, mpc_step,
                   run_closed_loop)

@@ -69,6 +69,11 @@ _SIGNATURES = {
                                   c_i64, P, c_i64, P, c_i64, P, P, c_void_p]),
     "gm_constraint_rows": (c_int, [c_void_p, c_int, c_int, P, c_int, c_int, P, P, P, c_int, P, P,
                                    P, P, P, P, c_void_p]),
+    "gm_node_hessians": (c_int, [c_void_p, c_int, c_int, P, c_int, P, c_i64, P, c_i64, P, P,
+                                 c_void_p]),
+    "gm_sum_nodes": (c_int, [c_void_p, c_int, c_int, c_int, c_int, P, P, P, c_void_p]),
+    "gm_param_count": (c_int, [c_void_p]),
+    "gm_loss_gradients": (c_int, [c_void_p, c_int, P, P, P, P, c_double, P, P, c_void_p]),
     "gm_expand_soft": (c_int, [c_void_p, c_int, c_int, c_int, P, P, P, P, c_int, P, P, P, P, P, P,
                                P, c_void_p]),
     "gm_solve_qp": (c_int, [c_void_p, c_int, c_int, c_int, P, P, P, P, P,

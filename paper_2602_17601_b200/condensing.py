@@ -31,7 +31,8 @@ from .graph import GraphTopology, chain_topology
 __all__ = [
     "ConfigurationError", "StateConstraint", "OcpSpec", "stage_input_box", "StandardFormCost",
     "cost_to_standard_form", "CondensedQp", "condense_gammas", "condense_ocp",
-    "reconstruct_states", "expand_soft_constraints", "min_eig_sym",
+    "reconstruct_states", "expand_soft_constraints", "min_eig_sym", "local_hessian_gradient",
+    "LocalCondensed", "condense_local", "assemble_qp",
 ]
 
 
@@ -527,3 +528,162 @@ def reconstruct_states(gamma_u, gamma_x, u) -> np.ndarray:
                  eng.stream_ptr())
     out = x.cpu().numpy()
     return out[0] if single else out
+
+
+# ---------------------------------------------------------------------------
+# per-node condensing (condensing.py:231-360): each node's H^i, g^i and
+# constraint rows, and their assembly -- the paper's Eqs. (16)-(17)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class LocalCondensed:
+    """One node's condensed quantities (``condensing.py:246-260``)."""
+
+    node: int
+    gamma_u: np.ndarray  # (N+1, n_state, N*n_u)
+    gamma_x: np.ndarray  # (N+1, n_state)
+    h: np.ndarray  # (N*n_u, N*n_u)
+    g: np.ndarray  # (N*n_u,)
+    c_rows: np.ndarray  # (rows, N*n_u)
+    d_rows: np.ndarray  # (rows,)
+    soft: np.ndarray  # (rows,) bool
+    rho1: np.ndarray  # (rows,)
+    rho2: np.ndarray  # (rows,)
+    # device copies of every node's (h, g) of the condense_local call that
+    # produced this node, and its index there (assemble_qp sums on the device
+    # without re-uploading)
+    _dev: tuple | None = field(default=None, repr=False, compare=False)
+
+
+def node_hessians_device(eng, W, ld, N, q, q_lin):
+    """K-NHG: per-node (H^i, g^i) of every node of the engine's graph on the
+    device: H (M, n0, n0), g (M, n0) fp64 tensors."""
+    nu = eng._dims[1] if eng._dims else None
+    n0 = N * nu
+    H = eng.empty((eng.M, n0, n0), np.float64)
+    g = eng.empty((eng.M, n0), np.float64)
+    eng.ctx.call("gm_node_hessians", 1, N, W.data_ptr(), ld, q.data_ptr(), 0, q_lin.data_ptr(), 0,
+                 H.data_ptr(), g.data_ptr(), eng.stream_ptr())
+    return H, g
+
+
+def local_hessian_gradient(gamma_u, gamma_x, q_blocks, q_lin):
+    """One node's Hessian and gradient contribution (``condensing.py:231-243``):
+    ``0.5 (h + h')`` with ``h = sum_k Gu_k' Q_k Gu_k`` and
+    ``g = sum_k Gu_k' (2 Q_k Gx_k + q_lin_k)``, on the GPU (K-NHG).
+    gamma_u (N+1, n_state, N*n_u), gamma_x (N+1, n_state), q_blocks
+    (N+1, n_state, n_state), q_lin (N+1, n_state)."""
+    gu = np.asarray(gamma_u, dtype=float)
+    gx = np.asarray(gamma_x, dtype=float)
+    S1, nx, n0 = gu.shape
+    N = S1 - 1
+    if N < 1 or n0 % N:
+        raise ConfigurationError("gamma_u must be (N+1, n_state, N*n_u) with N >= 1")
+    nu = n0 // N
+    if gx.shape != (S1, nx):
+        raise ConfigurationError("gamma_x must be (N+1, n_state)")
+    eng = _dev.engine(_qp_topo)
+    eng.set_dims(nx, nu)
+    W, ld = _upload_gammas(eng, gu[None], gx[None], N, nx, nu)
+    q = eng.h2d(np.asarray(q_blocks, dtype=float).reshape(1, S1, nx, nx), np.float64)
+    ql = eng.h2d(np.asarray(q_lin, dtype=float).reshape(1, S1, nx), np.float64)
+    H, g = node_hessians_device(eng, W, ld, N, q, ql)
+    return H[0].cpu().numpy(), g[0].cpu().numpy()
+
+
+def condense_local(spec, lin, x0) -> list:
+    """Per-node condensing (``condensing.py:285-295``): the Gamma recursion
+    (K-REC), every node's cost contribution (K-NHG) and its state-constraint
+    rows mapped to input space (K-CON), all on the GPU."""
+    topo = spec.topology
+    N, nx, nu = spec.horizon, spec.n_state, spec.n_u
+    M, n0 = topo.node_count, N * nu
+    eng = _dev.engine(topo)
+    eng.set_dims(nx, nu)
+    blocks = lin_blocks(lin, eng)
+    x0d = eng.h2d(np.asarray(x0, dtype=float).reshape(M, nx), np.float64)
+    W, ld = gammas_device(eng, blocks, x0d, N, nx, nu)
+    cost = cost_to_standard_form(spec)
+    q = eng.h2d(spec.q, np.float64)
+    ql = eng.h2d(cost.q_lin, np.float64)
+    Hd, gd = node_hessians_device(eng, W, ld, N, q, ql)
+    rows = spec_rows(spec, nx, nu)
+    C = d = None
+    if rows.n_st:
+        f64, i32 = np.float64, np.int32
+        Cd = eng.empty((rows.n_st, n0), f64)
+        dd = eng.empty((rows.n_st,), f64)
+        # keep the uploads referenced until the kernel is enqueued (a bare
+        # .data_ptr() of a temporary lets the allocator hand its block to the
+        # next upload)
+        sn, ss = eng.h2d(rows.st_node, i32), eng.h2d(rows.st_stage, i32)
+        sc, sd = eng.h2d(rows.st_c, f64), eng.h2d(rows.st_d, f64)
+        eng.ctx.call("gm_constraint_rows", 1, N, W.data_ptr(), ld, 0, None, None, None, rows.n_st,
+                     sn.data_ptr(), ss.data_ptr(), sc.data_ptr(), sd.data_ptr(),
+                     Cd.data_ptr(), dd.data_ptr(), eng.stream_ptr())
+        C, d = Cd.cpu().numpy(), dd.cpu().numpy()
+    gu, gx = _materialise(W, N, nu)
+    H, g = Hd.cpu().numpy(), gd.cpu().numpy()
+    # state rows are grouped by node ascending, stage ascending (spec_rows),
+    # exactly the per-node order of _node_constraint_rows (:263-282)
+    st_node = rows.st_node
+    bounds = np.searchsorted(st_node, np.arange(M + 1)) if rows.n_st else np.zeros(M + 1, int)
+    soft_st, r1_st, r2_st = (rows.soft[rows.n_in:], rows.rho1[rows.n_in:], rows.rho2[rows.n_in:])
+    out = []
+    for i in range(M):
+        a, b = int(bounds[i]), int(bounds[i + 1])
+        if b > a:
+            cr, dr = C[a:b].copy(), d[a:b].copy()
+        else:
+            cr, dr = np.zeros((0, n0)), np.zeros(0)
+        out.append(LocalCondensed(i, gu[i], gx[i], H[i], g[i], cr, dr, soft_st[a:b].copy(),
+                                  r1_st[a:b].copy(), r2_st[a:b].copy(), _dev=(Hd, gd, i)))
+    return out
+
+
+def assemble_qp(spec, locals_) -> CondensedQp:
+    """Sum the per-node cost contributions in ascending list order on the
+    device (R-bar first, then each node's h, g; symmetrised) and stack the
+    constraint rows: input rows first, then each node's block
+    (``condensing.py:334-360``)."""
+    N, nu = spec.horizon, spec.n_u
+    n0 = N * nu
+    cost = cost_to_standard_form(spec)
+    rb = np.zeros((n0, n0))
+    for k in range(N):
+        rb[k * nu:(k + 1) * nu, k * nu:(k + 1) * nu] = cost.r_blocks[k]
+    r_lin = cost.r_lin.reshape(-1)
+    eng = _dev.engine(_qp_topo)
+    locs = list(locals_)
+    src = locs[0]._dev if locs and locs[0]._dev is not None else None
+    same = src is not None and all(lc._dev is not None and lc._dev[0] is src[0]
+                                   and lc._dev[2] == k for k, lc in enumerate(locs)) \
+        and src[0].shape[0] == len(locs)
+    if same and src[0].device == eng.device:
+        Hs, gs = src[0], src[1]
+    else:  # arbitrary LocalCondensed lists: upload their (h, g)
+        Hs = eng.h2d(np.stack([np.asarray(lc.h, dtype=float) for lc in locs])
+                     if locs else np.zeros((0, n0, n0)), np.float64)
+        gs = eng.h2d(np.stack([np.asarray(lc.g, dtype=float) for lc in locs])
+                     if locs else np.zeros((0, n0)), np.float64)
+    H = eng.empty((n0, n0), np.float64)
+    g = eng.empty((n0,), np.float64)
+    count = len(locs)
+    rbd, rld = eng.h2d(rb, np.float64), eng.h2d(r_lin, np.float64)
+    eng.ctx.call("gm_sum_nodes", 1, count, n0 * n0, n0, Hs.data_ptr() if count else None,
+                 rbd.data_ptr(), H.data_ptr(), eng.stream_ptr())
+    eng.ctx.call("gm_sum_nodes", 1, count, n0, 0, gs.data_ptr() if count else None,
+                 rld.data_ptr(), g.data_ptr(), eng.stream_ptr())
+    rows = spec_rows(spec, spec.n_state, nu)
+    cu = np.zeros((rows.n_in, n0))
+    for r in range(rows.n_in):
+        k = rows.in_stage[r]
+        cu[r, k * nu:(k + 1) * nu] = rows.in_c[r]
+    c_all = [cu] + [np.asarray(lc.c_rows, dtype=float).reshape(-1, n0) for lc in locs]
+    d_all = [rows.in_d] + [np.asarray(lc.d_rows, dtype=float) for lc in locs]
+    soft = [np.zeros(rows.n_in, dtype=bool)] + [np.asarray(lc.soft, dtype=bool) for lc in locs]
+    rho1 = [np.zeros(rows.n_in)] + [np.asarray(lc.rho1, dtype=float) for lc in locs]
+    rho2 = [np.zeros(rows.n_in)] + [np.asarray(lc.rho2, dtype=float) for lc in locs]
+    return CondensedQp(h=H.cpu().numpy(), g=g.cpu().numpy(), c=np.vstack(c_all),
+                       d=np.concatenate(d_all), soft=np.concatenate(soft),
+                       rho1=np.concatenate(rho1), rho2=np.concatenate(rho2))

@@ -157,3 +157,36 @@ def qp_round2():
                            infeas_status=STATUS[int(d["infeas_meta"][0])],
                            infeas_iterations=int(d["infeas_meta"][1]),
                            infeas_primal=float(d["infeas_meta"][2]))
+
+
+def local_condense_cases():
+    """Reference condense_local / assemble_qp outputs (oracle/make_golden.py
+    local_condense)."""
+    d = load("local_condense")
+    out, t = [], 0
+    while f"c{t}_a_self" in d:
+        p = f"c{t}_"
+        topo = topo_from_ptr(d[p + "nbr_ptr"], d[p + "nbr_list"], 2)
+        N = d[p + "a_self"].shape[0]
+        lin = LinearizedDynamics(topo, N, d[p + "a_self"], d[p + "a_nbr"], d[p + "b"], d[p + "c"])
+        out.append(SimpleNamespace(
+            topo=topo, lin=lin, spec=spec_from(d, topo, p), x0=d[p + "x0"], h=d[p + "h"],
+            g=d[p + "g"], rows=d[p + "rows"], c_rows=d[p + "c_rows"], d_rows=d[p + "d_rows"],
+            qa={k: d[p + "qa_" + k] for k in ("h", "g", "c", "d", "soft", "rho1", "rho2")},
+            lhg_h=d[p + "lhg_h"], lhg_g=d[p + "lhg_g"]))
+        t += 1
+    return out
+
+
+def training_cases():
+    """Reference loss_gradients outputs (oracle/make_golden.py training_grads)."""
+    d = load("training_grads")
+    out = []
+    for name in d["cases"]:
+        p = str(name) + "_"
+        topo = topo_from_ptr(d[p + "nbr_ptr"], d[p + "nbr_list"])
+        out.append(SimpleNamespace(name=str(name), topo=topo, model=model_from(d, p + "m_"),
+                                   X=d[p + "X"], U=d[p + "U"], Xn=d[p + "Xn"], W=d[p + "W"],
+                                   lam=float(d[p + "lam"]), loss=float(d[p + "loss"]),
+                                   grads=d[p + "grads"]))
+    return out

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from oracle import ref_port as O
-from tests.golden_io import (STATUS, load, mpc_branch_cases, pipeline_case, qp_round2,
+from tests.golden_io import (STATUS, load, local_condense_cases, training_cases, mpc_branch_cases, pipeline_case, qp_round2,
                              random_condense_cases, random_qps, rel, topo_from_ptr)
 
 CASES = ["cfg1_chain10", "p3_biases_norm", "p4_interior", "mesh6x5", "mesh_p3"]
@@ -196,3 +196,28 @@ def test_oracle_qp_round2_fixtures():
     assert sol.status == q2.infeas_status == "primal_infeasible"
     assert sol.iterations == q2.infeas_iterations
     assert np.array_equal(sol.u, q2.infeas_u)
+
+
+def test_oracle_local_condensing_matches_reference():
+    """condense_local / local_hessian_gradient / assemble_qp restated
+    (condensing.py:231-360) against the reference's own outputs."""
+    for t, cs in enumerate(local_condense_cases()):
+        locs = O.condense_local(cs.spec, cs.lin, cs.x0)
+        assert np.max(np.abs(np.stack([lc.h for lc in locs]) - cs.h)) <= 1e-12, t
+        assert np.max(np.abs(np.stack([lc.g for lc in locs]) - cs.g)) <= 1e-12, t
+        qa = O.assemble_qp(cs.spec, locs)
+        for k in ("h", "g", "c", "d"):
+            assert np.max(np.abs(getattr(qa, k) - cs.qa[k]), initial=0.0) <= 1e-12, (t, k)
+        assert np.array_equal(qa.soft, cs.qa["soft"])
+        q_lin, _ = O.standard_form(cs.spec)
+        h0, g0 = O.local_hessian_gradient(locs[0].gamma_u, locs[0].gamma_x, cs.spec.q[0], q_lin[0])
+        assert np.max(np.abs(h0 - cs.lhg_h)) <= 1e-12 and np.max(np.abs(g0 - cs.lhg_g)) <= 1e-12
+
+
+def test_oracle_loss_gradients_match_reference():
+    """training.py:99-150 restated, against the reference's own values."""
+    for cs in training_cases():
+        L, grads = O.loss_gradients(cs.model, cs.topo, cs.X, cs.U, cs.Xn, cs.W, cs.lam)
+        flat = np.concatenate([g.ravel() for g in grads])
+        assert abs(L - cs.loss) <= 1e-12 * max(1.0, abs(cs.loss)), cs.name
+        assert np.max(np.abs(flat - cs.grads)) <= 1e-12 * max(1.0, np.max(np.abs(cs.grads))), cs.name
