@@ -142,12 +142,20 @@ class BatchedMpc:
                 dst.copy_(src, non_blocking=non_blocking)
         self.X[:, 0].copy_(self.x0)  # measurement at stage 0 (mpc.py:120-122)
 
-    def enqueue(self):
-        """All stages for all B instances on the current stream, no host sync."""
+    def enqueue(self, events=None):
+        """All stages for all B instances on the current stream, no host sync.
+        ``events`` (5 torch.cuda.Event, optional) are recorded on the stream
+        around K-LIN | K-COND (+ rows, soft) | K-QP | K-RS for stage timing."""
         eng, B, N, nx, nu = self.eng, self.B, self.N, self.nx, self.nu
         ctx, sp = eng.ctx, eng.stream_ptr()
         E = eng.E
         M = eng.M
+
+        def mark(i):
+            if events is not None:
+                events[i].record()
+
+        mark(0)
         # K-LIN over B*N points: linearise along the first N states of each instance
         Xlin = self.X[:, :N]  # (B, N, M, nx) view, contiguous per instance block
         if not Xlin.is_contiguous():
@@ -155,6 +163,7 @@ class BatchedMpc:
         ctx.call("gm_linearize", B * N, Xlin.data_ptr(), self.U.data_ptr(), self.a_self.data_ptr(),
                  self.a_nbr.data_ptr() if E else None, self.b.data_ptr(), self.c.data_ptr(), None,
                  sp)
+        mark(1)
         # K-COND: Gamma recursion + H/g reduction in one persistent kernel
         ctx.call("gm_condense_fused", B, N, self.a_self.data_ptr(),
                  self.a_nbr.data_ptr() if E else None, self.b.data_ptr(), self.c.data_ptr(),
@@ -172,6 +181,7 @@ class BatchedMpc:
                      self.C0.data_ptr(), self.d0.data_ptr(), self.ns, self.idx.data_ptr(),
                      self.rho1.data_ptr(), self.rho2.data_ptr(), self.H.data_ptr(),
                      self.g.data_ptr(), self.C.data_ptr(), self.d.data_ptr(), sp)
+        mark(2)
         warm = None
         if self.cfg.warm_start:
             self.warm[:, : N * nu].copy_(self.U.reshape(B, N * nu))
@@ -180,6 +190,7 @@ class BatchedMpc:
                  self.C.data_ptr() if self.m else None, self.d.data_ptr() if self.m else None,
                  warm, ctypes.byref(self.settings_c), self.u.data_ptr(), self.lam.data_ptr(),
                  self.status.data_ptr(), self.iters.data_ptr(), self.resid.data_ptr(), sp)
+        mark(3)
         ctx.call("gm_mpc_finish", B, N, self.W.data_ptr(), self.ld, self.u.data_ptr(), self.n,
                  self.status.data_ptr(), self.iters.data_ptr(), self.X.data_ptr(),
                  self.U.data_ptr(), self.X.data_ptr(), self.U.data_ptr(),
@@ -188,6 +199,7 @@ class BatchedMpc:
                  self.has_prev, None, self.planned_states.data_ptr(), self.planned_inputs.data_ptr(),
                  self.next_states.data_ptr(), self.next_inputs.data_ptr(),
                  self.u_applied.data_ptr(), self.summary.data_ptr(), sp)
+        mark(4)
 
     def step(self, x_measured, lin_states, lin_inputs, x_ref, last_applied=None) -> BatchResult:
         self.load(x_measured, lin_states, lin_inputs, x_ref, last_applied=last_applied)

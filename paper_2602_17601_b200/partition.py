@@ -424,19 +424,28 @@ class PartitionedMpc:
         nu = self.nu
         return summ[:nu].copy(), int(summ[nu]), int(summ[nu + 1])
 
-    def enqueue(self):
+    def enqueue(self, events=None):
         """The whole step on the current stream; host synchronisation only
-        inside the transport's collectives."""
+        inside the transport's collectives.  ``events`` (5 torch.cuda.Event,
+        optional) bracket K-LIN | condensing incl. exchanges and all-reduce |
+        K-QP | K-RS."""
         from .condensing import fused_device, rows_device
 
         eng, N, nu, ds = self.eng, self.N, self.nu, self.ds
         ctx, sp = eng.ctx, eng.stream_ptr()
         lo, hi = self.own
         a_nbr = self.a_nbr.data_ptr() if eng.E else None
+
+        def mark(i):
+            if events is not None:
+                events[i].record()
+
         try:
             ctx.call("gm_set_node_range", lo, hi)
+            mark(0)
             ctx.call("gm_linearize", N, self.ls.data_ptr(), self.li.data_ptr(),
                      self.a_self.data_ptr(), a_nbr, self.b.data_ptr(), self.c.data_ptr(), None, sp)
+            mark(1)
             if self.part.world == 1:
                 # nothing to exchange: the fused persistent recursion + cost
                 # kernel (K-COND) replaces the per-stage launches
@@ -469,6 +478,7 @@ class PartitionedMpc:
                      self.C0.data_ptr(), self.d0.data_ptr(), self.ns, ds.idx.data_ptr(),
                      ds.rho1.data_ptr(), ds.rho2.data_ptr(), self.H.data_ptr(), self.g.data_ptr(),
                      self.C.data_ptr(), self.d.data_ptr(), sp)
+        mark(2)
         warm = None
         if self.cfg.warm_start:
             self.warm[: N * nu].copy_(self.li.reshape(-1))
@@ -477,6 +487,7 @@ class PartitionedMpc:
                  self.C.data_ptr() if self.m else None, self.d.data_ptr() if self.m else None, warm,
                  self._ctypes.byref(self.settings_c), self.u.data_ptr(), self.lam.data_ptr(),
                  self.status.data_ptr(), self.iters.data_ptr(), self.resid.data_ptr(), sp)
+        mark(3)
         # every local node's Gamma rows are valid (halo rows exchanged), so the
         # plan and its shift are formed for owned + halo nodes here
         ctx.call("gm_mpc_finish", 1, N, self.W.data_ptr(), self.ld, self.u.data_ptr(), self.n,
@@ -487,6 +498,7 @@ class PartitionedMpc:
                  self.has_prev, None, self.planned_states.data_ptr(),
                  self.planned_inputs.data_ptr(), self.next_states.data_ptr(),
                  self.next_inputs.data_ptr(), self.u_applied.data_ptr(), self.summary.data_ptr(), sp)
+        mark(4)
 
     def _stage(self, n):
         eng = self.eng
