@@ -172,10 +172,14 @@ int gm_condense_cost(gm_ctx* ctx, int B, int N, const float* gamma, int ld, cons
  * fully written.  Requires the whole node range (gm_set_node_range unset);
  * shapes outside the fused kernel's instantiations run the two-kernel path.
  * One launch per context at a time (per-context stage counters). */
-/* Node reduction of H in gm_condense_fused: 0 = auto (tcgen05 3xTF32
- * tensor-core kernel when N*nu <= 128 and B*M >= 512, else the SIMT kernel),
- * 1 = always the SIMT (register-tiled fp32 FMA) kernel, 2 = the two-kernel
- * path (per-stage K-REC launches + K-HG), 3 = always the tcgen05 kernel.
+/* Kernel selection of gm_condense_fused: 0 = auto (nx = nu = 6 with 8-node
+ * items fitting shared memory: the TMA-staged kernel k_condense_tma, else the
+ * SIMT fused kernel; H and g always in fp32 FMA with round-to-nearest
+ * accumulation), 1 = always the SIMT fused kernel (per-thread neighbour
+ * loads), 2 = the two-kernel path (per-stage K-REC launches + K-HG),
+ * 3 = the tcgen05 3xTF32 H kernel (opt-in: the tensor-core accumulator
+ * truncates on every add, ~7e-5 relative H error at 10^4 nodes).  The same
+ * switch selects K-HG in gm_condense_cost (3: tcgen05, else SIMT).
  * For tests and benchmarks. */
 int gm_set_condense_mode(gm_ctx* ctx, int mode);
 int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_nbr,

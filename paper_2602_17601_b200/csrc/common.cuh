@@ -92,6 +92,13 @@ struct gm_ctx {
   int64_t dep_per = -1;
   int* d_dep_ptr = nullptr;
   int* d_dep = nullptr;
+  // K-COND TMA variant: per node chunk of `cu_sc` nodes, its unique
+  // closed-neighbourhood nodes (cu_ptr / cu_nodes) and each (node, slot)'s
+  // index into them (cu_slot, 255 = none)
+  int cu_sc = 0, cu_umax = 0;
+  int* d_cu_ptr = nullptr;
+  int* d_cu_nodes = nullptr;
+  unsigned char* d_cu_slot = nullptr;
 };
 
 // error helpers -------------------------------------------------------------

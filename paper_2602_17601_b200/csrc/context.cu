@@ -109,6 +109,9 @@ void gm_destroy(gm_ctx* ctx) {
     cudaFree(ctx->d_flags);
     cudaFree(ctx->d_dep_ptr);
     cudaFree(ctx->d_dep);
+    cudaFree(ctx->d_cu_ptr);
+    cudaFree(ctx->d_cu_nodes);
+    cudaFree(ctx->d_cu_slot);
     for (void* p : ctx->retired) cudaFree(p);
     free_mlp(ctx->psi);
     free_mlp(ctx->phi);
@@ -182,6 +185,12 @@ int gm_set_graph(gm_ctx* ctx, int64_t node_count, int64_t neighbor_bound, const 
   if (ctx->d_dep) ctx->retired.push_back(ctx->d_dep);
   ctx->d_dep_ptr = ctx->d_dep = nullptr;
   ctx->dep_per = -1;
+  if (ctx->d_cu_ptr) ctx->retired.push_back(ctx->d_cu_ptr);
+  if (ctx->d_cu_nodes) ctx->retired.push_back(ctx->d_cu_nodes);
+  if (ctx->d_cu_slot) ctx->retired.push_back(ctx->d_cu_slot);
+  ctx->d_cu_ptr = ctx->d_cu_nodes = nullptr;
+  ctx->d_cu_slot = nullptr;
+  ctx->cu_sc = 0;
   GM_CUDA(ctx, cudaMalloc(&ctx->d_ptr, sizeof(int) * (node_count + 1)));
   GM_CUDA(ctx, cudaMalloc(&ctx->d_src, sizeof(int) * src32.size()));
   GM_CUDA(ctx, cudaMalloc(&ctx->d_dst, sizeof(int) * dst32.size()));

@@ -34,6 +34,9 @@
 #include <cstdio>
 #include <cmath>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "umma.cuh"
 
@@ -64,6 +67,11 @@ struct FusedArgs {
   float* partH;   // (B, splits, npairs * nu * nu)
   double* partg;  // (B, splits, n0)
   int* flags;     // (B * splits) stage counters, then one completion counter
+  // k_condense_tma: unique closed-neighbourhood nodes per SC-node chunk
+  const int* cu_ptr;
+  const int* cu_nodes;
+  const unsigned char* cu_slot;
+  int umax;
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -387,6 +395,345 @@ __global__ void __launch_bounds__(256, 1) k_condense_fused(const FusedArgs a) {
     int* done = a.flags + (int64_t)gridDim.x;
     if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
       for (int s = 0; s < (int)gridDim.x; ++s) a.flags[s] = 0;
+      *done = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K-COND with TMA-staged Gamma tiles (nx = nu = 6, the reference
+// architecture; the default fused path).  Same work items, stage flags,
+// FMA order and fp32 round-to-nearest H accumulation as k_condense_fused,
+// but the neighbour Gamma rows of an item no longer come from per-thread
+// global loads (the measured bottleneck: long-scoreboard stalls at 8 warps
+// per SM, ncu profiles/r02): thread 0 stages them with the tensor memory
+// accelerator, cp.async.bulk.tensor.2d over the work array viewed as a
+// (rows = B*M*(N+1)*6, cols = ld) fp32 matrix, box 6 rows x 32 columns = one
+// node-stage block of one 32-column chunk.  Per item only the chunks holding
+// live Gamma_u columns and the Gamma_x column are loaded, once per UNIQUE
+// node of the item's closed neighbourhood (host tables per SC-node chunk:
+// a chain chunk of 8 nodes reads 10 node rows instead of 24 per-edge rows),
+// into a double-buffered shared ring completed on an mbarrier
+// (complete_tx).  Within a stage the next item's tiles are in flight while
+// the current item computes; the first item of a stage waits for them.
+// Ordering: generic stores of Gamma (own CTA: after a CTA barrier; other
+// CTAs: their release + our acquire of the stage flag) are made visible to
+// the async proxy by fence.proxy.async.global before each issue.
+// The recursion then runs from shared memory: one thread per (node, 4
+// columns), float4 tile reads (conflict free), A blocks broadcast.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          umma::smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(umma::smem_u32(mbar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(umma::smem_u32(mbar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+constexpr int kTileBytes = 6 * 32 * 4;  // one (node, stage, 32-column chunk) box
+
+template <int SC>
+__global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, const __grid_constant__ CUtensorMap tm) {
+  constexpr int NX = 6, NU = 6;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int N = a.N, ld = a.ld, M = a.M;
+  const int n0 = N * NU, XC = N * NU;
+  const int NCH = ld / 32;  // 32-column chunks per row
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t bi = blockIdx.x / a.splits;
+  const int split = (int)(blockIdx.x % a.splits);
+  const int nb = split * a.per, ne = min(M, nb + a.per);
+  const int nn = ne - nb;
+  const int nsub = (nn + SC - 1) / SC;
+  const int chunk0 = nb / SC;  // per is a multiple of SC
+  const int emax = SC * (a.dslot - 1) > 0 ? SC * (a.dslot - 1) : 1;
+  int* flags = a.flags + bi * a.splits;
+  const int64_t stage_stride = (int64_t)NX * ld;
+  const int64_t node_stride = (int64_t)(N + 1) * stage_stride;
+  float* Wb = a.W + bi * (int64_t)M * node_stride;
+
+  // shared memory: neighbour tile ring (2 x umax x NCH tiles) | 2 block
+  // stages | Gc | QGc | Qs | wv | gs | nptr | mbarriers
+  const size_t ring = (size_t)a.umax * NCH * kTileBytes;
+  float* nbuf0 = reinterpret_cast<float*>(smraw);
+  float* nbuf1 = reinterpret_cast<float*>(smraw + ring);
+  unsigned char* sbase = smraw + 2 * ring;
+  const size_t sbytes = stage_bytes<NX, NU>(SC, emax);
+  float* Gc = (float*)(sbase + 2 * sbytes);
+  float* QGc = Gc + (int64_t)SC * NX * ld;
+  float* Qs = QGc + (int64_t)SC * NX * ld;
+  double* wv = (double*)(((uintptr_t)(Qs + SC * NX * NX) + 15) & ~(uintptr_t)15);
+  double* gs = wv + SC * NX;
+  int* nptr = (int*)(gs + n0);
+  // the CTA's chunk tables, staged once: unique-node offsets / ids and the
+  // (node, slot) -> unique index map (no dependent global loads per item)
+  const int nchk = (a.per + SC - 1) / SC;
+  int* cptr = nptr + a.per + 1;                 // nchk + 1
+  int* cnod = cptr + nchk + 1;                  // nchk * umax
+  unsigned char* cslot = (unsigned char*)(cnod + nchk * a.umax);  // nchk * SC * dslot
+  uint64_t* mb = (uint64_t*)(((uintptr_t)(cslot + nchk * SC * a.dslot) + 7) & ~(uintptr_t)7);
+
+  for (int t = tid; t <= nn; t += nt) nptr[t] = a.ptr[nb + t];
+  {
+    const int c0p = a.cu_ptr[chunk0];
+    for (int t = tid; t <= nsub; t += nt) cptr[t] = a.cu_ptr[chunk0 + t] - c0p;
+    for (int t = tid; t < a.cu_ptr[chunk0 + nsub] - c0p; t += nt) cnod[t] = a.cu_nodes[c0p + t];
+    for (int t = tid; t < nsub * SC * a.dslot; t += nt) cslot[t] = a.cu_slot[(int64_t)chunk0 * SC * a.dslot + t];
+  }
+  int bq = (int)((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f);
+  while ((bq + 1) * (bq + 2) / 2 <= tid) ++bq;
+  while (bq * (bq + 1) / 2 > tid) --bq;
+  const int bp = tid - bq * (bq + 1) / 2;
+  const bool owner = tid < a.npairs;
+  float acc[NU][NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u)
+#pragma unroll
+    for (int v = 0; v < NU; ++v) acc[u][v] = 0.f;
+  for (int t = tid; t < n0; t += nt) gs[t] = 0.0;
+  if (tid == 0) {
+    umma::mbar_init(&mb[0], 1);
+    umma::mbar_init(&mb[1], 1);
+  }
+  __syncthreads();
+
+  auto prefetch = [&](int j) {  // A / B / c / Q / x_ref blocks of item j (cp.async)
+    const int n = j / nsub, s0 = nb + (j % nsub) * SC;
+    const int sc = min(SC, ne - s0), k = n + 1;
+    const Stage<NX, NU> S = stage_at<NX, NU>(sbase + (j & 1) * sbytes, SC, emax);
+    const int64_t pstage = bi * N + n;
+    const int eb = nptr[s0 - nb], ee = nptr[s0 - nb + sc];
+    const int nE = ee - eb;
+    const float* gas = a.a_self + (pstage * M + s0) * NX * NX;
+    for (int t = tid; t < sc * NX * NX; t += nt) cp_async4(S.as + t, gas + t);
+    if (nE > 0) {
+      const float* gan = a.a_nbr + (pstage * a.E + eb) * NX * NX;
+      for (int t = tid; t < nE * NX * NX; t += nt) cp_async4(S.an + t, gan + t);
+    }
+    const float* gb = a.b + (pstage * M + s0) * NX * NU;
+    for (int t = tid; t < sc * NX * NU; t += nt) cp_async4(S.bb + t, gb + t);
+    const double* gc = a.c + (pstage * M + s0) * NX;
+    for (int t = tid; t < sc * NX; t += nt) cp_async8(S.cc + t, gc + t);
+    for (int t = tid; t < sc * NX * NX; t += nt) {
+      const int li = t / (NX * NX), e = t - li * NX * NX;
+      cp_async8(S.qd + t, a.q + bi * a.q_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX * NX + e);
+    }
+    for (int t = tid; t < sc * NX; t += nt) {
+      const int li = t / NX, e = t - li * NX;
+      cp_async8(S.xd + t, a.xref + bi * a.xref_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX + e);
+    }
+    cp_async_commit();
+  };
+  // warp 0: TMA tiles of item j (stage n rows of its unique neighbours),
+  // one lane per unique node
+  const int lane = tid & 31;
+  auto issue_tiles = [&](int j) {
+    const int n = j / nsub, sub = j % nsub;
+    const int u0 = cptr[sub], U = cptr[sub + 1] - u0;
+    const int nlive = (NU * n + 31) / 32, xch = XC / 32;
+    const int nch = nlive + (xch >= nlive ? 1 : 0);
+    float* dst = (j & 1) ? nbuf1 : nbuf0;
+    uint64_t* bar = &mb[j & 1];
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(U * nch * kTileBytes));
+    __syncwarp();
+    for (int u = lane; u < U; u += 32) {
+      const int row = (int)(((bi * M + cnod[u0 + u]) * (N + 1) + n) * NX);
+      fence_proxy_async_global();
+      for (int ch = 0; ch < nlive; ++ch) tma_load_2d(dst + (u * NCH + ch) * (kTileBytes / 4), &tm, ch * 32, row, bar);
+      if (xch >= nlive) tma_load_2d(dst + (u * NCH + xch) * (kTileBytes / 4), &tm, xch * 32, row, bar);
+    }
+  };
+  const int items = N * nsub;
+  if (items > 0) prefetch(0);
+
+  // stage 0: Gamma_u = 0, Gamma_x = x0 (condensing.py:205-206)
+  for (int t = tid; t < nn * NX * ld; t += nt) {
+    const int li = t / (NX * ld), rem = t - li * NX * ld, r = rem / ld, col = rem - r * ld;
+    Wb[(int64_t)(nb + li) * node_stride + rem] = (col == XC) ? (float)a.x0[(bi * M + nb + li) * NX + r] : 0.f;
+  }
+  const int d0 = a.dep_ptr[split], d1 = a.dep_ptr[split + 1];
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(&flags[split], 1);
+  }
+
+  for (int j = 0; j < items; ++j) {
+    const int n = j / nsub, sub = j % nsub;
+    const int s0 = nb + sub * SC, sc = min(SC, ne - s0);
+    const int k = n + 1;
+    const int live = n * NU;
+    const Stage<NX, NU> S = stage_at<NX, NU>(sbase + (j & 1) * sbytes, SC, emax);
+    if (sub == 0) {
+      for (int d = d0 + tid; d < d1; d += nt) {
+        const int* f = &flags[a.dep[d]];
+        while (ld_acquire(f) < k) __nanosleep(32);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (tid < 32) {
+      if (sub == 0) issue_tiles(j);  // first item of a stage: its rows just became final
+      if (j + 1 < items && (j + 1) / nsub == n) issue_tiles(j + 1);  // in flight under item j
+    }
+    if (j + 1 < items) prefetch(j + 1);
+    for (int t = tid; t < sc * NX * NX; t += nt) {
+      const int li = t / (NX * NX), e = t - li * NX * NX, r = e / NX, cc = e - r * NX;
+      const double* Qk = S.qd + li * NX * NX;
+      Qs[t] = (float)(0.5 * (Qk[r * NX + cc] + Qk[cc * NX + r]));
+    }
+    umma::mbar_wait(&mb[j & 1], (uint32_t)((j >> 1) & 1));
+    const float* nbuf = (j & 1) ? nbuf1 : nbuf0;
+    const int ebase = nptr[s0 - nb];
+    const unsigned char* slot = cslot + sub * SC * a.dslot;
+    // Gamma rows of stage k: one thread per (node, 4 columns); per column the
+    // FMA order of K-REC (closed neighbourhood in slot order, rows, then the
+    // 6 products), then c on Gamma_x, B on block n, zeros elsewhere
+    const int G4 = ld / 4;
+    for (int t = tid; t < sc * G4; t += nt) {
+      const int li = t / G4, c0 = (t - li * G4) * 4;
+      const int i = s0 + li;
+      float r6[NX][4];
+#pragma unroll
+      for (int r = 0; r < NX; ++r)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) r6[r][e] = 0.f;
+      const bool xin = c0 <= XC && XC < c0 + 4;
+      if (c0 < live || xin) {
+        const int el0 = nptr[i - nb] - ebase, deg = nptr[i - nb + 1] - nptr[i - nb];
+        for (int ss = 0; ss <= deg; ++ss) {
+          const int u = slot[li * a.dslot + ss];
+          const float* g = nbuf + (u * NCH + (c0 >> 5)) * (kTileBytes / 4) + (c0 & 31);
+          float4 w[NX];
+#pragma unroll
+          for (int qq = 0; qq < NX; ++qq) w[qq] = *reinterpret_cast<const float4*>(g + qq * 32);
+          const float* As = ss == 0 ? S.as + li * NX * NX : S.an + (el0 + ss - 1) * NX * NX;
+#pragma unroll
+          for (int r = 0; r < NX; ++r)
+#pragma unroll
+            for (int qq = 0; qq < NX; ++qq) {
+              const float av = As[r * NX + qq];
+              r6[r][0] = fmaf(av, w[qq].x, r6[r][0]);
+              r6[r][1] = fmaf(av, w[qq].y, r6[r][1]);
+              r6[r][2] = fmaf(av, w[qq].z, r6[r][2]);
+              r6[r][3] = fmaf(av, w[qq].w, r6[r][3]);
+            }
+        }
+        if (xin) {
+#pragma unroll
+          for (int r = 0; r < NX; ++r)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (c0 + e == XC) r6[r][e] += (float)S.cc[li * NX + r];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int col = c0 + e;
+        const bool rec_col = col < live || col == XC;
+        const bool b_col = col >= live && col < live + NU;
+#pragma unroll
+        for (int r = 0; r < NX; ++r)
+          r6[r][e] = rec_col ? r6[r][e] : (b_col ? S.bb[(li * NX + r) * NU + (col - live)] : 0.f);
+      }
+      float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + c0;
+      float* Gs = Gc + (int64_t)li * NX * ld + c0;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) {
+        const float4 v = make_float4(r6[r][0], r6[r][1], r6[r][2], r6[r][3]);
+        *reinterpret_cast<float4*>(Wo + (int64_t)r * ld) = v;
+        *reinterpret_cast<float4*>(Gs + (int64_t)r * ld) = v;
+      }
+    }
+    __syncthreads();
+    if (sub == nsub - 1 && tid == 0) {
+      __threadfence();
+      st_release(&flags[split], k + 1);
+    }
+    // Qs G on the live columns of stage k, and w = 2 Q Gamma_x - 2 Q x_ref
+    const int lk = k * NU;
+    for (int t = tid; t < sc * lk; t += nt) {
+      const int li = t / lk, col = t - li * lk;
+      const float* Gs = Gc + (int64_t)li * NX * ld + col;
+      float gcol[NX];
+#pragma unroll
+      for (int qq = 0; qq < NX; ++qq) gcol[qq] = Gs[(int64_t)qq * ld];
+      const float* Qn = Qs + li * NX * NX;
+      float* Os = QGc + (int64_t)li * NX * ld + col;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) {
+        float sacc = 0.f;
+#pragma unroll
+        for (int qq = 0; qq < NX; ++qq) sacc = fmaf(Qn[r * NX + qq], gcol[qq], sacc);
+        Os[(int64_t)r * ld] = sacc;
+      }
+    }
+    for (int t = tid; t < sc * NX; t += nt) {
+      const int li = t / NX, r = t - li * NX;
+      const double* Qk = S.qd + li * NX * NX + r * NX;
+      const double* xr = S.xd + li * NX;
+      const float* gx = Gc + (int64_t)li * NX * ld + XC;
+      double qg = 0.0, qx = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < NX; ++qq) {
+        qg += Qk[qq] * (double)gx[(int64_t)qq * ld];
+        qx += Qk[qq] * xr[qq];
+      }
+      wv[t] = 2.0 * qg + (-2.0 * qx);
+    }
+    __syncthreads();
+    if (owner && bq < k) {
+      for (int li = 0; li < sc; ++li) {
+#pragma unroll
+        for (int r = 0; r < NX; ++r) {
+          const float* gp = Gc + ((int64_t)li * NX + r) * ld + bp * NU;
+          const float* gq = QGc + ((int64_t)li * NX + r) * ld + bq * NU;
+          const float2 x01 = *reinterpret_cast<const float2*>(gp), x23 = *reinterpret_cast<const float2*>(gp + 2),
+                       x45 = *reinterpret_cast<const float2*>(gp + 4);
+          const float2 y01 = *reinterpret_cast<const float2*>(gq), y23 = *reinterpret_cast<const float2*>(gq + 2),
+                       y45 = *reinterpret_cast<const float2*>(gq + 4);
+          const float x[NU] = {x01.x, x01.y, x23.x, x23.y, x45.x, x45.y};
+          const float y[NU] = {y01.x, y01.y, y23.x, y23.y, y45.x, y45.y};
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int v = 0; v < NU; ++v) acc[u][v] = fmaf(x[u], y[v], acc[u][v]);
+        }
+      }
+    }
+    for (int cidx = tid; cidx < lk; cidx += nt) {
+      double sg = gs[cidx];
+      for (int li = 0; li < sc; ++li)
+#pragma unroll
+        for (int r = 0; r < NX; ++r) sg += (double)Gc[((int64_t)li * NX + r) * ld + cidx] * wv[li * NX + r];
+      gs[cidx] = sg;
+    }
+    __syncthreads();
+  }
+
+  const int PU = a.npairs * NU * NU;
+  float* P = a.partH + (bi * a.splits + split) * (int64_t)PU;
+  if (owner) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u)
+#pragma unroll
+      for (int v = 0; v < NU; ++v) P[tid * NU * NU + u * NU + v] = acc[u][v];
+  }
+  for (int t = tid; t < n0; t += nt) a.partg[(bi * a.splits + split) * n0 + t] = gs[t];
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    int* done = a.flags + (int64_t)gridDim.x;
+    if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
+      for (int s2 = 0; s2 < (int)gridDim.x; ++s2) a.flags[s2] = 0;
       *done = 0;
       __threadfence();
     }
@@ -1021,6 +1368,238 @@ int ensure_flags(gm_ctx* ctx, int64_t n) {
   return GM_OK;
 }
 
+// ---- K-COND TMA variant: host side -----------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return (EncodeTiledFn)p;
+  }();
+  return fn;
+}
+
+// unique closed-neighbourhood nodes of every SC-node chunk (ascending ids)
+// and each (node, slot)'s index into them; slot 0 = self, then the in-edges
+// in CSR (edge) order
+int ensure_chunks(gm_ctx* ctx, int SC) {
+  if (ctx->cu_sc == SC && ctx->d_cu_ptr) return GM_OK;
+  const int64_t M = ctx->M;
+  const int dslot = (int)ctx->dmax + 1;
+  if (dslot > 255) return 1;
+  const int64_t nch = (M + SC - 1) / SC;
+  std::vector<int> cptr(nch + 1, 0), cnodes;
+  std::vector<unsigned char> slot((size_t)nch * SC * dslot, 255);
+  int umax = 0;
+  std::vector<int> u;
+  for (int64_t c = 0; c < nch; ++c) {
+    const int64_t lo = c * SC, hi = std::min<int64_t>(M, lo + SC);
+    u.clear();
+    for (int64_t i = lo; i < hi; ++i) {
+      u.push_back((int)i);
+      for (int64_t e = ctx->h_ptr[i]; e < ctx->h_ptr[i + 1]; ++e) u.push_back((int)ctx->h_src[e]);
+    }
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    if ((int)u.size() > 255) return 1;
+    umax = std::max(umax, (int)u.size());
+    auto idx = [&](int node) { return (unsigned char)(std::lower_bound(u.begin(), u.end(), node) - u.begin()); };
+    for (int64_t i = lo; i < hi; ++i) {
+      unsigned char* sl = slot.data() + ((size_t)c * SC + (i - lo)) * dslot;
+      sl[0] = idx((int)i);
+      for (int64_t e = ctx->h_ptr[i]; e < ctx->h_ptr[i + 1]; ++e) sl[1 + (e - ctx->h_ptr[i])] = idx((int)ctx->h_src[e]);
+    }
+    cnodes.insert(cnodes.end(), u.begin(), u.end());
+    cptr[c + 1] = (int)cnodes.size();
+  }
+  if (ctx->d_cu_ptr) ctx->retired.push_back(ctx->d_cu_ptr);
+  if (ctx->d_cu_nodes) ctx->retired.push_back(ctx->d_cu_nodes);
+  if (ctx->d_cu_slot) ctx->retired.push_back(ctx->d_cu_slot);
+  ctx->d_cu_ptr = ctx->d_cu_nodes = nullptr;
+  ctx->d_cu_slot = nullptr;
+  GM_CUDA(ctx, cudaMalloc(&ctx->d_cu_ptr, sizeof(int) * cptr.size()));
+  GM_CUDA(ctx, cudaMalloc(&ctx->d_cu_nodes, sizeof(int) * cnodes.size()));
+  GM_CUDA(ctx, cudaMalloc(&ctx->d_cu_slot, slot.size()));
+  GM_CUDA(ctx, cudaMemcpy(ctx->d_cu_ptr, cptr.data(), sizeof(int) * cptr.size(), cudaMemcpyHostToDevice));
+  GM_CUDA(ctx, cudaMemcpy(ctx->d_cu_nodes, cnodes.data(), sizeof(int) * cnodes.size(), cudaMemcpyHostToDevice));
+  GM_CUDA(ctx, cudaMemcpy(ctx->d_cu_slot, slot.data(), slot.size(), cudaMemcpyHostToDevice));
+  ctx->cu_sc = SC;
+  ctx->cu_umax = umax;
+  return GM_OK;
+}
+
+size_t tma_smem(int SC, int umax, int ld, int dslot, int n0, int64_t per) {
+  const int emax = SC * (dslot - 1) > 0 ? SC * (dslot - 1) : 1;
+  size_t b = 2 * (size_t)umax * (ld / 32) * kTileBytes;
+  b += 2 * stage_bytes<6, 6>(SC, emax);
+  b += sizeof(float) * ((size_t)2 * SC * 6 * ld + (size_t)SC * 36);
+  b = (b + 15) & ~size_t(15);
+  b += sizeof(double) * ((size_t)SC * 6 + n0);
+  b += sizeof(int) * (size_t)(per + 1);
+  const size_t nchk = (size_t)((per + SC - 1) / SC);
+  b += sizeof(int) * (nchk + 1 + nchk * umax) + nchk * SC * dslot;
+  b = (b + 7) & ~size_t(7);
+  return b + 2 * sizeof(uint64_t) + 16;
+}
+
+int launch_pair_reduce(gm_ctx* ctx, int B, int nu, int n0, int npairs, int splits, int groups, float* partH,
+                       double* partg, double* tmpH, double* tmpg, const double* r, int64_t r_stride,
+                       const double* u_ref, int64_t uref_stride, double* H, double* g, cudaStream_t st);
+
+// 1 = not applicable (shape, tables, smem), else a GM_ code
+int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_nbr, const float* b,
+                 const double* c, const double* x0, float* gamma, int ld, const double* q, int64_t q_stride,
+                 const double* x_ref, int64_t xref_stride, const double* r, int64_t r_stride,
+                 const double* u_ref, int64_t uref_stride, double* H, double* g, void* stream) {
+  const int nu = 6, n0 = N * nu, npairs = N * (N + 1) / 2;
+  if (ctx->nx != 6 || ctx->n_u != 6 || npairs > 256 || ld % 32 != 0 || n0 >= ld || ((uintptr_t)gamma & 15))
+    return 1;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return 1;
+  const int64_t M = ctx->M;
+  const int dslot = (int)ctx->dmax + 1;
+  const size_t budget = std::min<size_t>(ctx->smem_optin, 227 * 1024) - 2048;
+  int SC = 0;
+  int64_t per = 0;
+  // SC = 8 only: with 4-node items (what a 4-neighbour mesh fits into shared
+  // memory: 26 unique rows per 8-node item) the per-item overheads outweigh
+  // the staging (cfg5: 30 ms vs 21 ms for the per-thread-load kernel), so
+  // such graphs keep k_condense_fused
+  for (int sc_try : {8}) {
+    const int64_t slots = ctx->sm_count;
+    int64_t p = M;
+    if (B < slots) {
+      const int64_t want = std::max<int64_t>(1, slots / B);
+      p = (M + want - 1) / want;
+    }
+    p = (p + sc_try - 1) / sc_try * sc_try;
+    int rc = ensure_chunks(ctx, sc_try);
+    if (rc) return rc;
+    if (tma_smem(sc_try, ctx->cu_umax, ld, dslot, n0, p) <= budget) {
+      SC = sc_try;
+      per = p;
+      break;
+    }
+  }
+  if (!SC) return 1;
+  FusedKernel kern = SC == 8 ? (FusedKernel) nullptr : nullptr;
+  (void)kern;
+  const size_t sm = tma_smem(SC, ctx->cu_umax, ld, dslot, n0, per);
+  auto kfn = SC == 8 ? k_condense_tma<8> : k_condense_tma<4>;
+  GM_CUDA(ctx, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int occ = 0;
+  GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 256, sm));
+  if (occ < 1) return 1;
+  const int splits = (int)((M + per - 1) / per);
+  const int64_t grid = (int64_t)B * splits;
+  if (splits > 1 && grid > (int64_t)ctx->sm_count * occ) return 1;
+  int rc = ensure_deps(ctx, per, splits);
+  if (rc) return rc;
+  rc = ensure_flags(ctx, grid + 1);
+  if (rc) return rc;
+  // the work array as a (B*M*(N+1)*6, ld) fp32 matrix, 6 x 32 boxes
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)B * M * (N + 1) * 6};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {32, 6};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)gamma, dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return 1;
+  const int groups = std::min(splits, 16);
+  const int PU = npairs * nu * nu;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t pH = sizeof(float) * (size_t)grid * PU, pg = sizeof(double) * (size_t)grid * n0;
+  const size_t tH = sizeof(double) * (size_t)B * groups * PU, tg = sizeof(double) * (size_t)B * groups * n0;
+  char* scr = (char*)gm_scratch(ctx, up(pH) + up(pg) + up(tH) + tg + 256);
+  if (!scr) return gm_fail(ctx, GM_ERR_CUDA, "scratch allocation failed");
+  FusedArgs a{};
+  a.M = (int)M;
+  a.E = (int)ctx->E;
+  a.N = N;
+  a.ld = ld;
+  a.per = (int)per;
+  a.splits = splits;
+  a.sc = SC;
+  a.npairs = npairs;
+  a.dslot = dslot;
+  a.ptr = ctx->d_ptr;
+  a.src = ctx->d_src;
+  a.dep_ptr = ctx->d_dep_ptr;
+  a.dep = ctx->d_dep;
+  a.a_self = a_self;
+  a.a_nbr = a_nbr;
+  a.b = b;
+  a.c = c;
+  a.x0 = x0;
+  a.W = gamma;
+  a.q = q;
+  a.q_stride = q_stride;
+  a.xref = x_ref;
+  a.xref_stride = xref_stride;
+  a.partH = (float*)scr;
+  a.partg = (double*)(scr + up(pH));
+  a.flags = ctx->d_flags;
+  a.rec = 1;
+  a.lo = 0;
+  a.hi = (int)M;
+  a.cu_ptr = ctx->d_cu_ptr;
+  a.cu_nodes = ctx->d_cu_nodes;
+  a.cu_slot = ctx->d_cu_slot;
+  a.umax = ctx->cu_umax;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)grid);
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = sm;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = splits > 1 ? 1 : 0;  // stage waits across CTAs need co-residency
+  GM_CUDA(ctx, cudaLaunchKernelEx(&lc, kfn, a, tm));
+  GM_LAUNCH_CHECK(ctx, "k_condense_tma");
+  return launch_pair_reduce(ctx, B, nu, n0, npairs, splits, groups, a.partH, a.partg,
+                            (double*)(scr + up(pH) + up(pg)), (double*)(scr + up(pH) + up(pg) + up(tH)), r,
+                            r_stride, u_ref, uref_stride, H, g, st);
+}
+
+int launch_pair_reduce(gm_ctx* ctx, int B, int nu, int n0, int npairs, int splits, int groups, float* partH,
+                       double* partg, double* tmpH, double* tmpg, const double* r, int64_t r_stride,
+                       const double* u_ref, int64_t uref_stride, double* H, double* g, cudaStream_t st) {
+  PairReduceArgs ra{};
+  ra.nu = nu;
+  ra.n0 = n0;
+  ra.npairs = npairs;
+  ra.splits = splits;
+  ra.groups = groups;
+  ra.partH = partH;
+  ra.partg = partg;
+  ra.tmpH = tmpH;
+  ra.tmpg = tmpg;
+  ra.r = r;
+  ra.r_stride = r_stride;
+  ra.uref = u_ref;
+  ra.uref_stride = uref_stride;
+  ra.H = H;
+  ra.g = g;
+  const int PU = npairs * nu * nu;
+  const unsigned eb = (unsigned)gm_ceil_div(std::max(PU, n0), 256);
+  k_pair_reduce1<<<dim3(eb, (unsigned)groups, (unsigned)B), 256, 0, st>>>(ra);
+  GM_LAUNCH_CHECK(ctx, "k_pair_reduce1");
+  k_pair_reduce2<<<dim3(eb, (unsigned)B), 256, 0, st>>>(ra);
+  GM_LAUNCH_CHECK(ctx, "k_pair_reduce2");
+  return GM_OK;
+}
+
 }  // namespace
 
 // K-HG: the cost part of condense_ocp over the node range [node_lo, node_hi)
@@ -1135,6 +1714,15 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   if (B < 0 || N < 1) return gm_fail(ctx, GM_ERR_CONFIG, "need B >= 0 and horizon >= 1");
   if (ld < N * ctx->n_u + 1) return gm_fail(ctx, GM_ERR_CONFIG, "gamma leading dimension too small");
   if (B == 0) return GM_OK;
+  // default (mode 0): the TMA-staged kernel for the reference architecture
+  if (ctx->cond_mode == 0 && ctx->node_lo == 0 && gm_node_hi(ctx) == ctx->M) {
+    static const bool no_tma = std::getenv("GM_NO_TMA") != nullptr;  // measurement override
+    if (!no_tma) {
+      rc = condense_tma(ctx, B, N, a_self, a_nbr, b, c, x0, gamma, ld, q, q_stride, x_ref, xref_stride, r,
+                        r_stride, u_ref, uref_stride, H, g, stream);
+      if (rc != 1) return rc;
+    }
+  }
   const int nx = ctx->nx, nu = ctx->n_u, n0 = N * nu;
   const int npairs = N * (N + 1) / 2;
   const int dslot = (int)ctx->dmax + 1;

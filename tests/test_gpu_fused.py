@@ -114,11 +114,14 @@ def torch_equal(a, b):
     ("random", 9, 6, 2, 1),
     ("chain37", 5, 2, 1, 1),
     ("chain37", 6, 3, 2, 1),   # not instantiated: two-kernel fallback inside the call
+    ("mesh", 12, 6, 6, 1),     # mode 0: TMA-staged kernel, 4-neighbour mesh
+    ("random", 9, 6, 6, 2),    # mode 0: TMA-staged kernel, irregular degree <= 5
+    ("chain37", 20, 6, 6, 3),  # mode 0: M not a multiple of the node chunk
 ])
 @pytest.mark.parametrize("mode", [3, 1, 0, 2])
 def test_fused_matches_two_kernel_path(graph, N, nx, nu, B, mode):
     """mode 3: tcgen05 3xTF32 H (k_condense_tc), 1: SIMT fp32 H (k_condense_fused),
-    0: automatic choice, 2: two-kernel path (warp-per-node K-REC + tensor-core
+    0: automatic choice (nx = nu = 6: the TMA-staged k_condense_tma), 2: two-kernel path (warp-per-node K-REC + tensor-core
     K-HG) against the SIMT reference (per-node-CTA K-REC + SIMT K-HG).
     Gamma is bitwise identical in both; H agrees with the fp32 SIMT K-HG to
     fp32 round-off (3xTF32 drops the lo*lo term, ~2^-22 relative); on the tcgen05 path
@@ -138,16 +141,16 @@ def test_fused_matches_two_kernel_path(graph, N, nx, nu, B, mode):
                 for i in range(M)]
         topo = GraphTopology(M, tuple(tuple(n) for n in nbrs), 8)
     ref, outs = _run(topo, N, nx, nu, B, seed=11, reps=3, mode=mode)
-    _check(ref, outs, N * nu, nu, N, tol=2e-6 if mode == 1 else 1e-5)
+    _check(ref, outs, N * nu, nu, N, tol=2e-6 if mode in (0, 1) else 1e-5)
 
 
-@pytest.mark.parametrize("mode", [3, 1])
+@pytest.mark.parametrize("mode", [3, 1, 0])
 def test_fused_graph_replay(mode):
     from paper_2602_17601_b200.graph import mesh_topology
 
     topo = mesh_topology(30, 20)
     ref, outs = _run(topo, 10, 6, 6, 1, seed=3, reps=3, graph=True, mode=mode)
-    _check(ref, outs, 60, 6, 10, tol=2e-6 if mode == 1 else 1e-5)
+    _check(ref, outs, 60, 6, 10, tol=2e-6 if mode in (0, 1) else 1e-5)
 
 
 @pytest.mark.parametrize("graph,N,nx,nu,B,rng_,partial", [
