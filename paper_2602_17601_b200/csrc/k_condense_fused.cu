@@ -479,7 +479,10 @@ __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, cons
   int* cptr = nptr + a.per + 1;                 // nchk + 1
   int* cnod = cptr + nchk + 1;                  // nchk * umax
   unsigned char* cslot = (unsigned char*)(cnod + nchk * a.umax);  // nchk * SC * dslot
-  uint64_t* mb = (uint64_t*)(((uintptr_t)(cslot + nchk * SC * a.dslot) + 7) & ~(uintptr_t)7);
+  // H accumulator of the CTA (block pairs x 36, fp32): stage partials are
+  // folded in once per stage
+  float* Hacc = (float*)(((uintptr_t)(cslot + nchk * SC * a.dslot) + 15) & ~(uintptr_t)15);
+  uint64_t* mb = (uint64_t*)(Hacc + a.npairs * NU * NU);
 
   for (int t = tid; t <= nn; t += nt) nptr[t] = a.ptr[nb + t];
   {
@@ -488,17 +491,21 @@ __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, cons
     for (int t = tid; t < a.cu_ptr[chunk0 + nsub] - c0p; t += nt) cnod[t] = a.cu_nodes[c0p + t];
     for (int t = tid; t < nsub * SC * a.dslot; t += nt) cslot[t] = a.cu_slot[(int64_t)chunk0 * SC * a.dslot + t];
   }
-  int bq = (int)((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f);
-  while ((bq + 1) * (bq + 2) / 2 <= tid) ++bq;
-  while (bq * (bq + 1) / 2 > tid) --bq;
-  const int bp = tid - bq * (bq + 1) / 2;
-  const bool owner = tid < a.npairs;
+  // H work of a stage is balanced over all threads: at stage k the
+  // npk = k(k+1)/2 live block pairs get R = 256 / npk threads each, thread
+  // (pair pp = tid % npk, slice sl = tid / npk) summing the rows
+  // sl, sl + R, ... of every item of the stage in registers; the slices are
+  // folded into Hacc in a fixed order at the end of the stage
+  int bq = 0, bp = 0, pp = 0, sl = 0, R = 1;
+  bool hact = false;
+  const bool balance = nsub >= 4;  // (a CTA with 1-3 items per stage folds too often)
   float acc[NU][NU];
 #pragma unroll
   for (int u = 0; u < NU; ++u)
 #pragma unroll
     for (int v = 0; v < NU; ++v) acc[u][v] = 0.f;
   for (int t = tid; t < n0; t += nt) gs[t] = 0.0;
+  for (int t = tid; t < a.npairs * NU * NU; t += nt) Hacc[t] = 0.f;
   if (tid == 0) {
     umma::mbar_init(&mb[0], 1);
     umma::mbar_init(&mb[1], 1);
@@ -577,6 +584,22 @@ __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, cons
         const int* f = &flags[a.dep[d]];
         while (ld_acquire(f) < k) __nanosleep(32);
       }
+      const int npk = k * (k + 1) / 2;
+      if (balance) {
+        R = max(1, min(SC * NX, nt / npk));
+        pp = tid % npk;
+        sl = tid / npk;
+        hact = sl < R;
+      } else {  // few items per stage: fixed pair ownership, no folds
+        R = 1;
+        pp = tid;
+        sl = 0;
+        hact = tid < npk;
+      }
+      bq = (int)((sqrtf(8.f * pp + 1.f) - 1.f) * 0.5f);
+      while ((bq + 1) * (bq + 2) / 2 <= pp) ++bq;
+      while (bq * (bq + 1) / 2 > pp) --bq;
+      bp = pp - bq * (bq + 1) / 2;
     }
     cp_async_wait_all();
     __syncthreads();
@@ -690,12 +713,11 @@ __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, cons
       wv[t] = 2.0 * qg + (-2.0 * qx);
     }
     __syncthreads();
-    if (owner && bq < k) {
-      for (int li = 0; li < sc; ++li) {
-#pragma unroll
-        for (int r = 0; r < NX; ++r) {
-          const float* gp = Gc + ((int64_t)li * NX + r) * ld + bp * NU;
-          const float* gq = QGc + ((int64_t)li * NX + r) * ld + bq * NU;
+    if (hact) {
+      for (int row = sl; row < sc * NX; row += R) {
+        {
+          const float* gp = Gc + (int64_t)row * ld + bp * NU;
+          const float* gq = QGc + (int64_t)row * ld + bq * NU;
           const float2 x01 = *reinterpret_cast<const float2*>(gp), x23 = *reinterpret_cast<const float2*>(gp + 2),
                        x45 = *reinterpret_cast<const float2*>(gp + 4);
           const float2 y01 = *reinterpret_cast<const float2*>(gq), y23 = *reinterpret_cast<const float2*>(gq + 2),
@@ -716,12 +738,40 @@ __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, cons
         for (int r = 0; r < NX; ++r) sg += (double)Gc[((int64_t)li * NX + r) * ld + cidx] * wv[li * NX + r];
       gs[cidx] = sg;
     }
-    __syncthreads();
+    // (no barrier here: the next item's loop-top barrier orders these reads
+    // of Gc / QGc before its recursion overwrites them)
+    if (balance && sub == nsub - 1) {
+      // fold the stage's slices into Hacc (Gc / QGc are free until the
+      // next item's recursion): stage in shared memory, then each pair's
+      // owner adds its R slices in slice order
+      __syncthreads();
+      float* stg = Gc;
+      if (hact) {
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+#pragma unroll
+          for (int v = 0; v < NU; ++v) {
+            stg[tid * NU * NU + u * NU + v] = acc[u][v];
+            acc[u][v] = 0.f;
+          }
+      }
+      __syncthreads();
+      const int npk = k * (k + 1) / 2;
+      for (int t = tid; t < npk * NU * NU; t += nt) {
+        const int p2 = t / (NU * NU), e = t - p2 * NU * NU;
+        float hs = Hacc[t];
+        for (int s2 = 0; s2 < R; ++s2) hs += stg[(p2 + s2 * npk) * NU * NU + e];
+        Hacc[t] = hs;
+      }
+      __syncthreads();
+    }
   }
 
   const int PU = a.npairs * NU * NU;
   float* P = a.partH + (bi * a.splits + split) * (int64_t)PU;
-  if (owner) {
+  if (balance) {
+    for (int t = tid; t < PU; t += nt) P[t] = Hacc[t];
+  } else if (tid < a.npairs) {
 #pragma unroll
     for (int u = 0; u < NU; ++u)
 #pragma unroll
@@ -1444,7 +1494,9 @@ size_t tma_smem(int SC, int umax, int ld, int dslot, int n0, int64_t per) {
   b += sizeof(int) * (size_t)(per + 1);
   const size_t nchk = (size_t)((per + SC - 1) / SC);
   b += sizeof(int) * (nchk + 1 + nchk * umax) + nchk * SC * dslot;
-  b = (b + 7) & ~size_t(7);
+  b = (b + 15) & ~size_t(15);
+  const int N = n0 / 6;
+  b += sizeof(float) * (size_t)(N * (N + 1) / 2) * 36;  // Hacc
   return b + 2 * sizeof(uint64_t) + 16;
 }
 
@@ -1458,7 +1510,10 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
                  const double* x_ref, int64_t xref_stride, const double* r, int64_t r_stride,
                  const double* u_ref, int64_t uref_stride, double* H, double* g, void* stream) {
   const int nu = 6, n0 = N * nu, npairs = N * (N + 1) / 2;
-  if (ctx->nx != 6 || ctx->n_u != 6 || npairs > 256 || ld % 32 != 0 || n0 >= ld || ((uintptr_t)gamma & 15))
+  // ld >= 96: the per-stage H fold stages 256 x 36 floats in the Gc / QGc
+  // buffers (2 x 8 nodes x 6 rows x ld floats)
+  if (ctx->nx != 6 || ctx->n_u != 6 || npairs > 256 || ld % 32 != 0 || ld < 96 || n0 >= ld ||
+      ((uintptr_t)gamma & 15))
     return 1;
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return 1;
