@@ -49,9 +49,13 @@ METRIC = "MPC step latency ms (linearize+condense+QP) & Hz at N nodes; solves/se
 # dram__bytes_read.sum + dram__bytes_write.sum per launch, from this round's
 # `ncu --set full` captures (profiles/r02/ncu_*); None where not captured
 NCU_TRAFFIC = {
-    "cfg3": {"k_solve_qp": 757760, "linearize": None, "k_condense_fused": None},
-    "cfg4": {"k_condense_fused": None},
-    "cfg5": {"k_condense_fused": None},
+    # cfg3: profiles/r02/ncu_kernels_cfg3.txt (linearize = the 6 K-LIN
+    # launches of one step; k_solve_qp: the round-1 capture, kernel unchanged)
+    "cfg3": {"k_solve_qp": 757760, "linearize": 42511616, "k_condense_fused": 35475200},
+    # cfg4: one 1024-instance wave of k_condense_tma (profiles/r02/ncu_kernels_cond.txt)
+    "cfg4": {"k_condense_fused": 25940555000},
+    # cfg5: k_condense_fused (the mesh keeps the per-thread-load kernel)
+    "cfg5": {"k_condense_fused": 23642548000},
 }
 M_NODES, HORIZON = 1000, 20
 WORKLOAD = "cfg3: chain graph M=1000 nodes, horizon N=20, _scaling_problem recipe (paper 100 Hz headline)"

@@ -1770,7 +1770,10 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   if (ld < N * ctx->n_u + 1) return gm_fail(ctx, GM_ERR_CONFIG, "gamma leading dimension too small");
   if (B == 0) return GM_OK;
   // default (mode 0): the TMA-staged kernel for the reference architecture
-  if (ctx->cond_mode == 0 && ctx->node_lo == 0 && gm_node_hi(ctx) == ctx->M) {
+  // from 512 node rows (below, e.g. cfg2 at M = 100, the per-stage tile
+  // issue / wait latency of a one-item-per-stage CTA costs more than the
+  // staging saves: 0.20 vs 0.10 ms)
+  if (ctx->cond_mode == 0 && ctx->node_lo == 0 && gm_node_hi(ctx) == ctx->M && (int64_t)B * ctx->M >= 512) {
     static const bool no_tma = std::getenv("GM_NO_TMA") != nullptr;  // measurement override
     if (!no_tma) {
       rc = condense_tma(ctx, B, N, a_self, a_nbr, b, c, x0, gamma, ld, q, q_stride, x_ref, xref_stride, r,
