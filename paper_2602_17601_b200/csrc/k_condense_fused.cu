@@ -440,7 +440,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 
 constexpr int kTileBytes = 6 * 32 * 4;  // one (node, stage, 32-column chunk) box
 
-template <int SC>
+template <int SC, int CPS, int GW, bool DB>
 __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, const __grid_constant__ CUtensorMap tm) {
   constexpr int NX = 6, NU = 6;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -462,10 +462,16 @@ __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, cons
 
   // shared memory: neighbour tile ring (2 x umax x NCH tiles) | 2 block
   // stages | Gc | QGc | Qs | wv | gs | nptr | mbarriers
-  const size_t ring = (size_t)a.umax * NCH * kTileBytes;
+  // passes of CPS 32-column chunks: slot p holds chunks [CPS p, CPS p + CPS)
+  // of an item's unique neighbour rows; slot p's k-th fill is item k.  DB
+  // (one pass): two slots alternating by item instead, the next item's tiles
+  // issued as the current item starts
+  const int npass = (NCH + CPS - 1) / CPS;
+  const size_t ring = (size_t)a.umax * CPS * kTileBytes;
+  const int nslot = DB ? 2 : npass;
   float* nbuf0 = reinterpret_cast<float*>(smraw);
   float* nbuf1 = reinterpret_cast<float*>(smraw + ring);
-  unsigned char* sbase = smraw + 2 * ring;
+  unsigned char* sbase = smraw + nslot * ring;
   const size_t sbytes = stage_bytes<NX, NU>(SC, emax);
   float* Gc = (float*)(sbase + 2 * sbytes);
   float* QGc = Gc + (int64_t)SC * NX * ld;
@@ -539,23 +545,29 @@ __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, cons
     }
     cp_async_commit();
   };
-  // warp 0: TMA tiles of item j (stage n rows of its unique neighbours),
-  // one lane per unique node
+  // warp 0: TMA tiles of half h of item j (stage n rows of its unique
+  // neighbours, the live chunks among {2h, 2h+1}), one lane per unique node;
+  // a half without live chunks still completes its phase (expect_tx 0)
   const int lane = tid & 31;
-  auto issue_tiles = [&](int j) {
+  auto issue_half = [&](int j, int h) {
     const int n = j / nsub, sub = j % nsub;
     const int u0 = cptr[sub], U = cptr[sub + 1] - u0;
     const int nlive = (NU * n + 31) / 32, xch = XC / 32;
-    const int nch = nlive + (xch >= nlive ? 1 : 0);
-    float* dst = (j & 1) ? nbuf1 : nbuf0;
-    uint64_t* bar = &mb[j & 1];
-    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(U * nch * kTileBytes));
+    const int cb = CPS * h, ceo = min(CPS * h + CPS, NCH);
+    int cnt = 0;
+    for (int ch = cb; ch < ceo; ++ch) cnt += (ch < nlive || ch == xch) ? 1 : 0;
+    const int slotw = DB ? (j & 1) : h;
+    float* dst = slotw ? nbuf1 : nbuf0;
+    uint64_t* bar = &mb[slotw];
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(U * cnt * kTileBytes));
     __syncwarp();
+    if (cnt == 0) return;
     for (int u = lane; u < U; u += 32) {
       const int row = (int)(((bi * M + cnod[u0 + u]) * (N + 1) + n) * NX);
       fence_proxy_async_global();
-      for (int ch = 0; ch < nlive; ++ch) tma_load_2d(dst + (u * NCH + ch) * (kTileBytes / 4), &tm, ch * 32, row, bar);
-      if (xch >= nlive) tma_load_2d(dst + (u * NCH + xch) * (kTileBytes / 4), &tm, xch * 32, row, bar);
+      for (int ch = cb; ch < ceo; ++ch)
+        if (ch < nlive || ch == xch)
+          tma_load_2d(dst + (u * CPS + (ch - cb)) * (kTileBytes / 4), &tm, ch * 32, row, bar);
     }
   };
   const int items = N * nsub;
@@ -604,8 +616,12 @@ __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, cons
     cp_async_wait_all();
     __syncthreads();
     if (tid < 32) {
-      if (sub == 0) issue_tiles(j);  // first item of a stage: its rows just became final
-      if (j + 1 < items && (j + 1) / nsub == n) issue_tiles(j + 1);  // in flight under item j
+      if (sub == 0) issue_half(j, 0);  // first item of a stage: its rows just became final
+      if (DB) {
+        if (j + 1 < items && (j + 1) / nsub == n) issue_half(j + 1, 0);  // in flight under item j
+      } else {
+        for (int h = 1; h < npass; ++h) issue_half(j, h);
+      }
     }
     if (j + 1 < items) prefetch(j + 1);
     for (int t = tid; t < sc * NX * NX; t += nt) {
@@ -613,70 +629,103 @@ __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, cons
       const double* Qk = S.qd + li * NX * NX;
       Qs[t] = (float)(0.5 * (Qk[r * NX + cc] + Qk[cc * NX + r]));
     }
-    umma::mbar_wait(&mb[j & 1], (uint32_t)((j >> 1) & 1));
-    const float* nbuf = (j & 1) ? nbuf1 : nbuf0;
     const int ebase = nptr[s0 - nb];
     const unsigned char* slot = cslot + sub * SC * a.dslot;
-    // Gamma rows of stage k: one thread per (node, 4 columns); per column the
-    // FMA order of K-REC (closed neighbourhood in slot order, rows, then the
-    // 6 products), then c on Gamma_x, B on block n, zeros elsewhere
-    const int G4 = ld / 4;
-    for (int t = tid; t < sc * G4; t += nt) {
-      const int li = t / G4, c0 = (t - li * G4) * 4;
-      const int i = s0 + li;
-      float r6[NX][4];
-#pragma unroll
-      for (int r = 0; r < NX; ++r)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) r6[r][e] = 0.f;
-      const bool xin = c0 <= XC && XC < c0 + 4;
-      if (c0 < live || xin) {
-        const int el0 = nptr[i - nb] - ebase, deg = nptr[i - nb + 1] - nptr[i - nb];
-        for (int ss = 0; ss <= deg; ++ss) {
-          const int u = slot[li * a.dslot + ss];
-          const float* g = nbuf + (u * NCH + (c0 >> 5)) * (kTileBytes / 4) + (c0 & 31);
-          float4 w[NX];
-#pragma unroll
-          for (int qq = 0; qq < NX; ++qq) w[qq] = *reinterpret_cast<const float4*>(g + qq * 32);
-          const float* As = ss == 0 ? S.as + li * NX * NX : S.an + (el0 + ss - 1) * NX * NX;
-#pragma unroll
-          for (int r = 0; r < NX; ++r)
-#pragma unroll
-            for (int qq = 0; qq < NX; ++qq) {
-              const float av = As[r * NX + qq];
-              r6[r][0] = fmaf(av, w[qq].x, r6[r][0]);
-              r6[r][1] = fmaf(av, w[qq].y, r6[r][1]);
-              r6[r][2] = fmaf(av, w[qq].z, r6[r][2]);
-              r6[r][3] = fmaf(av, w[qq].w, r6[r][3]);
-            }
-        }
-        if (xin) {
-#pragma unroll
-          for (int r = 0; r < NX; ++r)
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (c0 + e == XC) r6[r][e] += (float)S.cc[li * NX + r];
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int col = c0 + e;
-        const bool rec_col = col < live || col == XC;
-        const bool b_col = col >= live && col < live + NU;
+    // Gamma rows of stage k, one half (64 columns) at a time: one thread per
+    // (node, 2 columns); per column the FMA order of K-REC (closed
+    // neighbourhood in slot order, rows, then the 6 products), then c on
+    // Gamma_x, B on block n, zeros elsewhere
+#pragma unroll 1
+    for (int h = 0; h < npass; ++h) {
+      const int cb0 = 32 * CPS * h, ncol = min(32 * CPS, ld - cb0);
+      const int slotr = DB ? (j & 1) : h;
+      umma::mbar_wait(&mb[slotr], (uint32_t)(DB ? ((j >> 1) & 1) : (j & 1)));
+      const float* nbuf = slotr ? nbuf1 : nbuf0;
+      const int G2 = ncol / GW;
+      for (int t = tid; t < sc * G2; t += nt) {
+        const int li = t / G2, c0 = cb0 + (t - li * G2) * GW;
+        const int i = s0 + li;
+        float r6[NX][GW];
 #pragma unroll
         for (int r = 0; r < NX; ++r)
-          r6[r][e] = rec_col ? r6[r][e] : (b_col ? S.bb[(li * NX + r) * NU + (col - live)] : 0.f);
-      }
-      float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + c0;
-      float* Gs = Gc + (int64_t)li * NX * ld + c0;
 #pragma unroll
-      for (int r = 0; r < NX; ++r) {
-        const float4 v = make_float4(r6[r][0], r6[r][1], r6[r][2], r6[r][3]);
-        *reinterpret_cast<float4*>(Wo + (int64_t)r * ld) = v;
-        *reinterpret_cast<float4*>(Gs + (int64_t)r * ld) = v;
+          for (int e = 0; e < GW; ++e) r6[r][e] = 0.f;
+        const bool xin = c0 <= XC && XC < c0 + GW;
+        if (c0 < live || xin) {
+          const int el0 = nptr[i - nb] - ebase, deg = nptr[i - nb + 1] - nptr[i - nb];
+          for (int ss = 0; ss <= deg; ++ss) {
+            const int u = slot[li * a.dslot + ss];
+            const float* g = nbuf + (u * CPS + ((c0 >> 5) - CPS * h)) * (kTileBytes / 4) + (c0 & 31);
+            float w[NX][GW];
+#pragma unroll
+            for (int qq = 0; qq < NX; ++qq) {
+              if (GW == 4) {
+                const float4 v = *reinterpret_cast<const float4*>(g + qq * 32);
+                w[qq][0] = v.x;
+                w[qq][GW > 1 ? 1 : 0] = v.y;
+                w[qq][GW > 2 ? 2 : 0] = v.z;
+                w[qq][GW > 3 ? 3 : 0] = v.w;
+              } else {
+                const float2 v = *reinterpret_cast<const float2*>(g + qq * 32);
+                w[qq][0] = v.x;
+                w[qq][GW > 1 ? 1 : 0] = v.y;
+              }
+            }
+            const float4* A4 = reinterpret_cast<const float4*>(ss == 0 ? S.as + li * NX * NX
+                                                                      : S.an + (el0 + ss - 1) * NX * NX);
+            float av[NX * NX];
+#pragma unroll
+            for (int q4 = 0; q4 < NX * NX / 4; ++q4) {
+              const float4 v4 = A4[q4];
+              av[4 * q4] = v4.x;
+              av[4 * q4 + 1] = v4.y;
+              av[4 * q4 + 2] = v4.z;
+              av[4 * q4 + 3] = v4.w;
+            }
+#pragma unroll
+            for (int r = 0; r < NX; ++r)
+#pragma unroll
+              for (int qq = 0; qq < NX; ++qq)
+#pragma unroll
+                for (int e = 0; e < GW; ++e) r6[r][e] = fmaf(av[r * NX + qq], w[qq][e], r6[r][e]);
+          }
+          if (xin) {
+#pragma unroll
+            for (int r = 0; r < NX; ++r)
+#pragma unroll
+              for (int e = 0; e < GW; ++e)
+                if (c0 + e == XC) r6[r][e] += (float)S.cc[li * NX + r];
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < GW; ++e) {
+          const int col = c0 + e;
+          const bool rec_col = col < live || col == XC;
+          const bool b_col = col >= live && col < live + NU;
+#pragma unroll
+          for (int r = 0; r < NX; ++r)
+            r6[r][e] = rec_col ? r6[r][e] : (b_col ? S.bb[(li * NX + r) * NU + (col - live)] : 0.f);
+        }
+        float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + c0;
+        float* Gs = Gc + (int64_t)li * NX * ld + c0;
+#pragma unroll
+        for (int r = 0; r < NX; ++r) {
+          if (GW == 4) {
+            const float4 v = make_float4(r6[r][0], r6[r][GW > 1 ? 1 : 0], r6[r][GW > 2 ? 2 : 0],
+                                         r6[r][GW > 3 ? 3 : 0]);
+            *reinterpret_cast<float4*>(Wo + (int64_t)r * ld) = v;
+            *reinterpret_cast<float4*>(Gs + (int64_t)r * ld) = v;
+          } else {
+            const float2 v = make_float2(r6[r][0], r6[r][GW > 1 ? 1 : 0]);
+            *reinterpret_cast<float2*>(Wo + (int64_t)r * ld) = v;
+            *reinterpret_cast<float2*>(Gs + (int64_t)r * ld) = v;
+          }
+        }
       }
+      __syncthreads();  // the slot of pass h is free again
+      if (!DB && h == 0 && tid < 32 && j + 1 < items && (j + 1) / nsub == n)
+        issue_half(j + 1, 0);  // the next item's first pass, in flight under this item
     }
-    __syncthreads();
     if (sub == nsub - 1 && tid == 0) {
       __threadfence();
       st_release(&flags[split], k + 1);
@@ -1484,9 +1533,10 @@ int ensure_chunks(gm_ctx* ctx, int SC) {
   return GM_OK;
 }
 
-size_t tma_smem(int SC, int umax, int ld, int dslot, int n0, int64_t per) {
+size_t tma_smem(int SC, int CPS, bool DB, int umax, int ld, int dslot, int n0, int64_t per) {
   const int emax = SC * (dslot - 1) > 0 ? SC * (dslot - 1) : 1;
-  size_t b = 2 * (size_t)umax * (ld / 32) * kTileBytes;
+  const int npass = (ld / 32 + CPS - 1) / CPS;
+  size_t b = (size_t)(DB ? 2 : npass) * umax * CPS * kTileBytes;
   b += 2 * stage_bytes<6, 6>(SC, emax);
   b += sizeof(float) * ((size_t)2 * SC * 6 * ld + (size_t)SC * 36);
   b = (b + 15) & ~size_t(15);
@@ -1520,33 +1570,46 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
   const int64_t M = ctx->M;
   const int dslot = (int)ctx->dmax + 1;
   const size_t budget = std::min<size_t>(ctx->smem_optin, 227 * 1024) - 2048;
-  int SC = 0;
-  int64_t per = 0;
-  // SC = 8 only: with 4-node items (what a 4-neighbour mesh fits into shared
-  // memory: 26 unique rows per 8-node item) the per-item overheads outweigh
-  // the staging (cfg5: 30 ms vs 21 ms for the per-thread-load kernel), so
-  // such graphs keep k_condense_fused
-  for (int sc_try : {8}) {
-    const int64_t slots = ctx->sm_count;
-    int64_t p = M;
-    if (B < slots) {
-      const int64_t want = std::max<int64_t>(1, slots / B);
-      p = (M + want - 1) / want;
-    }
-    p = (p + sc_try - 1) / sc_try * sc_try;
-    int rc = ensure_chunks(ctx, sc_try);
-    if (rc) return rc;
-    if (tma_smem(sc_try, ctx->cu_umax, ld, dslot, n0, p) <= budget) {
-      SC = sc_try;
-      per = p;
+  // 8-node items (with 4-node items the per-item overheads outweigh the
+  // staging: cfg5 30 ms vs 21 ms for the per-thread-load kernel).  Tile
+  // passes: all 4 chunks of an item in one pass (4-column thread groups) when
+  // that fits shared memory, else two passes of 2 chunks (2-column groups):
+  // a chain item has 10 unique rows (1 pass, 31 KB of tiles), a mesh item 26
+  // (80 KB in 1 pass).  GM_TMA_CPS=14|4|2 forces a variant (measurement
+  // override: 14 = one pass double-buffered).
+  constexpr int SC = 8;
+  int64_t per = M;
+  if (B < ctx->sm_count) {
+    const int64_t want = std::max<int64_t>(1, ctx->sm_count / B);
+    per = (M + want - 1) / want;
+  }
+  per = (per + SC - 1) / SC * SC;
+  int rc0 = ensure_chunks(ctx, SC);
+  if (rc0) return rc0;
+  static const int cps_env = [] {
+    const char* v = std::getenv("GM_TMA_CPS");
+    return v ? std::atoi(v) : 0;
+  }();
+  // variants in order of preference: one pass double-buffered by item
+  // (chains), one pass single-buffered (meshes), two passes of 2 chunks
+  struct Var {
+    int cps;
+    bool db;
+    void (*fn)(const FusedArgs, const CUtensorMap);
+  };
+  const Var vars[3] = {{4, true, k_condense_tma<8, 4, 4, true>},
+                       {4, false, k_condense_tma<8, 4, 4, false>},
+                       {2, false, k_condense_tma<8, 2, 2, false>}};
+  const Var* var = nullptr;
+  for (const Var& v : vars)
+    if ((cps_env == 0 || cps_env == v.cps + (v.db ? 10 : 0)) &&
+        tma_smem(SC, v.cps, v.db, ctx->cu_umax, ld, dslot, n0, per) <= budget) {
+      var = &v;
       break;
     }
-  }
-  if (!SC) return 1;
-  FusedKernel kern = SC == 8 ? (FusedKernel) nullptr : nullptr;
-  (void)kern;
-  const size_t sm = tma_smem(SC, ctx->cu_umax, ld, dslot, n0, per);
-  auto kfn = SC == 8 ? k_condense_tma<8> : k_condense_tma<4>;
+  if (!var) return 1;
+  const size_t sm = tma_smem(SC, var->cps, var->db, ctx->cu_umax, ld, dslot, n0, per);
+  auto kfn = var->fn;
   GM_CUDA(ctx, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int occ = 0;
   GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 256, sm));
