@@ -387,6 +387,7 @@ def cfg3_leg(args, world, rank, local, dev):
     M, N = args.nodes, args.horizon
     topo, model, states, inputs, spec = problem(M, N)
     spec.freeze()
+    model.freeze()  # a deployed controller's fixed weights: checked by identity, not re-hashed per step
     cfg = pkg.MpcConfig(horizon=N, dt=0.01)
     x0 = states[0]
     xs = pkg.SystemState(x0)
@@ -492,6 +493,7 @@ def cfg3_leg(args, world, rank, local, dev):
         "data": "synthetic",
         "config": {"workload": WORKLOAD, "nodes": M, "horizon": N, "instances_per_gpu": 1,
                    "parallelism": f"independent instance per GPU x{world}",
+                   "model": "random-init weights, frozen (GnnModel.freeze); spec frozen (OcpSpec.freeze)",
                    "l2": "flushed (256 MiB write) between timed steps" if not args.no_l2_flush
                    else "not flushed", "qp": {"n": n, "m": m, "status": status, "iterations": iters}},
         "stage_ms": {"linearize": lin, "condense": cond, "solve_and_epilogue": solve},

@@ -12,6 +12,7 @@ in the native library.
 from __future__ import annotations
 
 import threading
+import weakref
 from collections import OrderedDict
 
 import numpy as np
@@ -64,14 +65,20 @@ class Engine:
         from ._runtime import lib
         self.dmax = int(lib().gm_max_degree(self.ctx.handle))
         self._model_fp = None
+        self._frozen_ref = None
         self._dims = None
         self.lock = threading.RLock()
         self.cache = {}  # workspace / uploaded-constant cache (see mpc.py, condensing.py)
 
     # -- bindings -----------------------------------------------------------
     def bind_model(self, model):
+        frozen = getattr(model, "_frozen", None)
+        if frozen is not None and self._frozen_ref is not None and self._frozen_ref() is model \
+                and frozen == (id(model.psi), id(model.phi), id(model.normalization), model.dt):
+            return  # same frozen model object, nothing can have changed
         fp = _model_fingerprint(model)
         if fp == self._model_fp:
+            self._frozen_ref = weakref.ref(model) if frozen is not None else None
             return
         nrm = model.normalization
 
@@ -100,6 +107,7 @@ class Engine:
             # and keep the graphs valid.
             self.drop_graphs()
         self._model_fp = fp
+        self._frozen_ref = weakref.ref(model) if frozen is not None else None
         self._dims = (2 * int(model.n_p), int(model.n_u))
 
     def drop_graphs(self):

@@ -73,6 +73,23 @@ class GnnModel:
     def n_state(self) -> int:
         return 2 * self.n_p
 
+    def freeze(self) -> "GnnModel":
+        """Make the parameters immutable (arrays read-only, layer lists
+        tuples).  A frozen model is re-checked by identity instead of by a
+        byte fingerprint of its ~8 k parameters on every ``mpc_step`` (the
+        reference reads the arrays on every call; an unfrozen model keeps
+        that semantics, in-place edits included)."""
+        for mlp in (self.psi, self.phi):
+            for a in list(mlp.weights) + list(mlp.biases):
+                a.flags.writeable = False
+            mlp.weights = tuple(mlp.weights)
+            mlp.biases = tuple(mlp.biases)
+        nrm = self.normalization
+        for a in (nrm.state_mean, nrm.state_scale, nrm.input_mean, nrm.input_scale):
+            a.flags.writeable = False
+        object.__setattr__(self, "_frozen", (id(self.psi), id(self.phi), id(nrm), self.dt))
+        return self
+
     def copy(self) -> "GnnModel":
         nrm = self.normalization
         return GnnModel(self.psi.copy(), self.phi.copy(), self.dt, self.n_p, self.n_u, self.n_m,

@@ -118,3 +118,22 @@ def test_error_mapping():
         c.check(_runtime.GM_ERR_NUMERIC, "x")
     with pytest.raises(RuntimeError):
         c.check(_runtime.GM_ERR_CUDA, "x")
+
+
+def test_frozen_model_is_immutable():
+    """GnnModel.freeze (the engine then checks the model by identity instead
+    of re-hashing its parameters per step): arrays read-only, layer lists
+    tuples, copies unfrozen."""
+    import numpy as np
+    import pytest
+
+    import paper_2602_17601_b200 as pkg
+
+    m = pkg.init_model(3, 6, 0.01, np.random.default_rng(0)).freeze()
+    with pytest.raises(ValueError):
+        m.psi.weights[0][0, 0] = 1.0
+    with pytest.raises(TypeError):
+        m.phi.weights[0] = np.zeros_like(m.phi.weights[0])
+    c = m.copy()
+    c.psi.weights[0][0, 0] = 1.0
+    assert not hasattr(c, "_frozen")
