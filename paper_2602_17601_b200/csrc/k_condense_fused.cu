@@ -839,6 +839,433 @@ __global__ void __launch_bounds__(256, 1) k_condense_tma(const FusedArgs a, cons
   }
 }
 
+__device__ __forceinline__ void qpb_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void qpb_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// K-COND, warp-specialised pipeline (the default TMA kernel).  Per item the
+// round-1/2 kernels run recursion -> QG -> H/g back to back on all warps
+// with CTA barriers between them (ncu: ~40 % of warp samples at barriers,
+// more warps per SM gave nothing).  Here warps 0-3 (group R) produce item j
+// -- TMA tiles, recursion (Gamma rows to W and to the double-buffered Gc),
+// Qs, QG, w -- while warps 4-7 (group H) fold item j-1 into H and g.  The
+// groups hand items over through named barriers per Gc/QGc buffer
+// (FULL: R arrives, H syncs; EMPTY: H arrives, R syncs two items later);
+// each group syncs internally on its own named barrier.  Numerics are those
+// of k_condense_tma (same per-column FMA order, fp32 H accumulation folded
+// into the CTA accumulator once per stage in a fixed order, fp64 g).
+// ---------------------------------------------------------------------------
+template <int SC, int CPS, int GW, bool DB>
+__global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, const __grid_constant__ CUtensorMap tm) {
+  constexpr int NX = 6, NU = 6;
+  constexpr int GT = 128;  // threads per group
+  constexpr int BAR_R = 1, BAR_H = 2, BAR_FULL = 3, BAR_EMPTY = 5;  // FULL / EMPTY: + buffer
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int N = a.N, ld = a.ld, M = a.M;
+  const int n0 = N * NU, XC = N * NU;
+  const int NCH = ld / 32;
+  const int tid = threadIdx.x;
+  const bool grpR = tid < GT;
+  const int gt = grpR ? tid : tid - GT;  // thread index within the group
+  const int64_t bi = blockIdx.x / a.splits;
+  const int split = (int)(blockIdx.x % a.splits);
+  const int nb = split * a.per, ne = min(M, nb + a.per);
+  const int nn = ne - nb;
+  const int nsub = (nn + SC - 1) / SC;
+  const int chunk0 = nb / SC;
+  const int emax = SC * (a.dslot - 1) > 0 ? SC * (a.dslot - 1) : 1;
+  int* flags = a.flags + bi * a.splits;
+  const int64_t stage_stride = (int64_t)NX * ld;
+  const int64_t node_stride = (int64_t)(N + 1) * stage_stride;
+  float* Wb = a.W + bi * (int64_t)M * node_stride;
+
+  // shared memory: tile ring | 2 block stages | 2 x (Gc, QGc) | Qs | 2 x wv |
+  // gs | nptr | chunk tables | Hacc | mbarriers
+  const int npass = (NCH + CPS - 1) / CPS;
+  const size_t ring = (size_t)a.umax * CPS * kTileBytes;
+  const int nslot = DB ? 2 : npass;
+  float* nbuf0 = reinterpret_cast<float*>(smraw);
+  float* nbuf1 = reinterpret_cast<float*>(smraw + ring);
+  unsigned char* sbase = smraw + nslot * ring;
+  const size_t sbytes = stage_bytes<NX, NU>(SC, emax);
+  const int64_t gsz = (int64_t)SC * NX * ld;
+  float* Gc2 = (float*)(sbase + 2 * sbytes);  // buffer b: Gc = Gc2 + 2 b gsz, QGc = Gc + gsz
+  float* Qs2 = Gc2 + 4 * gsz;  // 2 x SC*NX*NX
+  double* wv2 = (double*)(((uintptr_t)(Qs2 + 2 * SC * NX * NX) + 15) & ~(uintptr_t)15);  // 2 x SC*NX
+  double* gs = wv2 + 2 * SC * NX;
+  int* nptr = (int*)(gs + n0);
+  const int nchk = (a.per + SC - 1) / SC;
+  int* cptr = nptr + a.per + 1;
+  int* cnod = cptr + nchk + 1;
+  unsigned char* cslot = (unsigned char*)(cnod + nchk * a.umax);
+  float* Hacc = (float*)(((uintptr_t)(cslot + nchk * SC * a.dslot) + 15) & ~(uintptr_t)15);
+  uint64_t* mb = (uint64_t*)(Hacc + a.npairs * NU * NU);
+
+  for (int t = tid; t <= nn; t += 256) nptr[t] = a.ptr[nb + t];
+  {
+    const int c0p = a.cu_ptr[chunk0];
+    for (int t = tid; t <= nsub; t += 256) cptr[t] = a.cu_ptr[chunk0 + t] - c0p;
+    for (int t = tid; t < a.cu_ptr[chunk0 + nsub] - c0p; t += 256) cnod[t] = a.cu_nodes[c0p + t];
+    for (int t = tid; t < nsub * SC * a.dslot; t += 256) cslot[t] = a.cu_slot[(int64_t)chunk0 * SC * a.dslot + t];
+  }
+  for (int t = tid; t < n0; t += 256) gs[t] = 0.0;
+  for (int t = tid; t < a.npairs * NU * NU; t += 256) Hacc[t] = 0.f;
+  if (tid == 0) {
+    umma::mbar_init(&mb[0], 1);
+    umma::mbar_init(&mb[1], 1);
+  }
+  const int items = N * nsub;
+  // stage 0: Gamma_u = 0, Gamma_x = x0 (condensing.py:205-206)
+  for (int t = tid; t < nn * NX * ld; t += 256) {
+    const int li = t / (NX * ld), rem = t - li * NX * ld, r = rem / ld, col = rem - r * ld;
+    Wb[(int64_t)(nb + li) * node_stride + rem] = (col == XC) ? (float)a.x0[(bi * M + nb + li) * NX + r] : 0.f;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(&flags[split], 1);
+  }
+
+  if (grpR) {
+    // ===================== group R: tiles, recursion, QG =====================
+    const int lane = tid & 31;
+    auto prefetch = [&](int j) {
+      const int n = j / nsub, s0 = nb + (j % nsub) * SC;
+      const int sc = min(SC, ne - s0), k = n + 1;
+      const Stage<NX, NU> S = stage_at<NX, NU>(sbase + (j & 1) * sbytes, SC, emax);
+      const int64_t pstage = bi * N + n;
+      const int eb = nptr[s0 - nb], ee = nptr[s0 - nb + sc];
+      const int nE = ee - eb;
+      const float* gas = a.a_self + (pstage * M + s0) * NX * NX;
+      for (int t = gt; t < sc * NX * NX; t += GT) cp_async4(S.as + t, gas + t);
+      if (nE > 0) {
+        const float* gan = a.a_nbr + (pstage * a.E + eb) * NX * NX;
+        for (int t = gt; t < nE * NX * NX; t += GT) cp_async4(S.an + t, gan + t);
+      }
+      const float* gb = a.b + (pstage * M + s0) * NX * NU;
+      for (int t = gt; t < sc * NX * NU; t += GT) cp_async4(S.bb + t, gb + t);
+      const double* gc = a.c + (pstage * M + s0) * NX;
+      for (int t = gt; t < sc * NX; t += GT) cp_async8(S.cc + t, gc + t);
+      for (int t = gt; t < sc * NX * NX; t += GT) {
+        const int li = t / (NX * NX), e = t - li * NX * NX;
+        cp_async8(S.qd + t, a.q + bi * a.q_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX * NX + e);
+      }
+      for (int t = gt; t < sc * NX; t += GT) {
+        const int li = t / NX, e = t - li * NX;
+        cp_async8(S.xd + t, a.xref + bi * a.xref_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX + e);
+      }
+      cp_async_commit();
+    };
+    auto issue_half = [&](int j, int h) {  // warp 0
+      const int n = j / nsub, sub = j % nsub;
+      const int u0 = cptr[sub], U = cptr[sub + 1] - u0;
+      const int nlive = (NU * n + 31) / 32, xch = XC / 32;
+      const int cb = CPS * h, ceo = min(CPS * h + CPS, NCH);
+      int cnt = 0;
+      for (int ch = cb; ch < ceo; ++ch) cnt += (ch < nlive || ch == xch) ? 1 : 0;
+      const int slotw = DB ? (j & 1) : h;
+      float* dst = slotw ? nbuf1 : nbuf0;
+      uint64_t* bar = &mb[slotw];
+      if (lane == 0) mbar_expect_tx(bar, (uint32_t)(U * cnt * kTileBytes));
+      __syncwarp();
+      if (cnt == 0) return;
+      for (int u = lane; u < U; u += 32) {
+        const int row = (int)(((bi * M + cnod[u0 + u]) * (N + 1) + n) * NX);
+        fence_proxy_async_global();
+        for (int ch = cb; ch < ceo; ++ch)
+          if (ch < nlive || ch == xch)
+            tma_load_2d(dst + (u * CPS + (ch - cb)) * (kTileBytes / 4), &tm, ch * 32, row, bar);
+      }
+    };
+    const int d0 = a.dep_ptr[split], d1 = a.dep_ptr[split + 1];
+    if (items > 0) prefetch(0);
+    for (int j = 0; j < items; ++j) {
+      const int n = j / nsub, sub = j % nsub;
+      const int s0 = nb + sub * SC, sc = min(SC, ne - s0);
+      const int k = n + 1, live = n * NU, b = j & 1;
+      const Stage<NX, NU> S = stage_at<NX, NU>(sbase + (j & 1) * sbytes, SC, emax);
+      float* Gc = Gc2 + 2 * b * gsz;
+      double* wv = wv2 + b * SC * NX;
+      if (sub == 0)
+        for (int d = d0 + gt; d < d1; d += GT) {
+          const int* f = &flags[a.dep[d]];
+          while (ld_acquire(f) < k) __nanosleep(32);
+        }
+      cp_async_wait_all();
+      qpb_sync(BAR_R, GT);  // blocks of item j in; the previous recursion left the tile slots
+      if (tid < 32) {
+        if (sub == 0) issue_half(j, 0);
+        if (DB) {
+          if (j + 1 < items && (j + 1) / nsub == n) issue_half(j + 1, 0);
+        } else {
+          for (int h = 1; h < npass; ++h) issue_half(j, h);
+        }
+      }
+      if (j + 1 < items) prefetch(j + 1);
+      if (j >= 2) qpb_sync(BAR_EMPTY + b, 256);  // group H is done with buffer b (item j-2)
+      float* Qs = Qs2 + b * SC * NX * NX;
+      for (int t = gt; t < sc * NX * NX; t += GT) {
+        const int li = t / (NX * NX), e = t - li * NX * NX, r = e / NX, cc = e - r * NX;
+        const double* Qk = S.qd + li * NX * NX;
+        Qs[t] = (float)(0.5 * (Qk[r * NX + cc] + Qk[cc * NX + r]));
+      }
+      const int ebase = nptr[s0 - nb];
+      const unsigned char* slot = cslot + sub * SC * a.dslot;
+#pragma unroll 1
+      for (int h = 0; h < npass; ++h) {
+        const int cb0 = 32 * CPS * h, ncol = min(32 * CPS, ld - cb0);
+        const int slotr = DB ? (j & 1) : h;
+        umma::mbar_wait(&mb[slotr], (uint32_t)(DB ? ((j >> 1) & 1) : (j & 1)));
+        const float* nbuf = slotr ? nbuf1 : nbuf0;
+        const int G2 = ncol / GW;
+        for (int t = gt; t < sc * G2; t += GT) {
+          const int li = t / G2, c0 = cb0 + (t - li * G2) * GW;
+          const int i = s0 + li;
+          float r6[NX][GW];
+#pragma unroll
+          for (int r = 0; r < NX; ++r)
+#pragma unroll
+            for (int e = 0; e < GW; ++e) r6[r][e] = 0.f;
+          const bool xin = c0 <= XC && XC < c0 + GW;
+          if (c0 < live || xin) {
+            const int el0 = nptr[i - nb] - ebase, deg = nptr[i - nb + 1] - nptr[i - nb];
+            for (int ss = 0; ss <= deg; ++ss) {
+              const int u = slot[li * a.dslot + ss];
+              const float* g = nbuf + (u * CPS + ((c0 >> 5) - CPS * h)) * (kTileBytes / 4) + (c0 & 31);
+              float w[NX][GW];
+#pragma unroll
+              for (int qq = 0; qq < NX; ++qq) {
+                if (GW == 4) {
+                  const float4 v = *reinterpret_cast<const float4*>(g + qq * 32);
+                  w[qq][0] = v.x;
+                  w[qq][GW > 1 ? 1 : 0] = v.y;
+                  w[qq][GW > 2 ? 2 : 0] = v.z;
+                  w[qq][GW > 3 ? 3 : 0] = v.w;
+                } else {
+                  const float2 v = *reinterpret_cast<const float2*>(g + qq * 32);
+                  w[qq][0] = v.x;
+                  w[qq][GW > 1 ? 1 : 0] = v.y;
+                }
+              }
+              const float4* A4 = reinterpret_cast<const float4*>(ss == 0 ? S.as + li * NX * NX
+                                                                        : S.an + (el0 + ss - 1) * NX * NX);
+              float av[NX * NX];
+#pragma unroll
+              for (int q4 = 0; q4 < NX * NX / 4; ++q4) {
+                const float4 v4 = A4[q4];
+                av[4 * q4] = v4.x;
+                av[4 * q4 + 1] = v4.y;
+                av[4 * q4 + 2] = v4.z;
+                av[4 * q4 + 3] = v4.w;
+              }
+#pragma unroll
+              for (int r = 0; r < NX; ++r)
+#pragma unroll
+                for (int qq = 0; qq < NX; ++qq)
+#pragma unroll
+                  for (int e = 0; e < GW; ++e) r6[r][e] = fmaf(av[r * NX + qq], w[qq][e], r6[r][e]);
+            }
+            if (xin) {
+#pragma unroll
+              for (int r = 0; r < NX; ++r)
+#pragma unroll
+                for (int e = 0; e < GW; ++e)
+                  if (c0 + e == XC) r6[r][e] += (float)S.cc[li * NX + r];
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < GW; ++e) {
+            const int col = c0 + e;
+            const bool rec_col = col < live || col == XC;
+            const bool b_col = col >= live && col < live + NU;
+#pragma unroll
+            for (int r = 0; r < NX; ++r)
+              r6[r][e] = rec_col ? r6[r][e] : (b_col ? S.bb[(li * NX + r) * NU + (col - live)] : 0.f);
+          }
+          float* Wo = Wb + (int64_t)i * node_stride + (int64_t)k * stage_stride + c0;
+          float* Gs = Gc + (int64_t)li * NX * ld + c0;
+#pragma unroll
+          for (int r = 0; r < NX; ++r) {
+            if (GW == 4) {
+              const float4 v = make_float4(r6[r][0], r6[r][GW > 1 ? 1 : 0], r6[r][GW > 2 ? 2 : 0],
+                                           r6[r][GW > 3 ? 3 : 0]);
+              *reinterpret_cast<float4*>(Wo + (int64_t)r * ld) = v;
+              *reinterpret_cast<float4*>(Gs + (int64_t)r * ld) = v;
+            } else {
+              const float2 v = make_float2(r6[r][0], r6[r][GW > 1 ? 1 : 0]);
+              *reinterpret_cast<float2*>(Wo + (int64_t)r * ld) = v;
+              *reinterpret_cast<float2*>(Gs + (int64_t)r * ld) = v;
+            }
+          }
+        }
+        qpb_sync(BAR_R, GT);  // Gamma rows of the pass written; its tile slot is free again
+        if (!DB && h == 0 && tid < 32 && j + 1 < items && (j + 1) / nsub == n) issue_half(j + 1, 0);
+      }
+      if (sub == nsub - 1 && gt == 0) {
+        __threadfence();
+        st_release(&flags[split], k + 1);
+      }
+      for (int t = gt; t < sc * NX; t += GT) {
+        const int li = t / NX, r = t - li * NX;
+        const double* Qk = S.qd + li * NX * NX + r * NX;
+        const double* xr = S.xd + li * NX;
+        const float* gx = Gc + (int64_t)li * NX * ld + XC;
+        double qg = 0.0, qx = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < NX; ++qq) {
+          qg += Qk[qq] * (double)gx[(int64_t)qq * ld];
+          qx += Qk[qq] * xr[qq];
+        }
+        wv[t] = 2.0 * qg + (-2.0 * qx);
+      }
+      __threadfence_block();
+      qpb_arrive(BAR_FULL + b, 256);  // item j -> group H
+    }
+    // consume group H's last EMPTY arrivals (balanced barrier phases)
+    for (int j = max(items, 2); j < items + 2; ++j) qpb_sync(BAR_EMPTY + (j & 1), 256);
+  } else {
+    // ===================== group H: H and g =====================
+    // stage k: npk = k(k+1)/2 live block pairs over 128 threads: npk <= 128
+    // -> R = 128 / npk row slices per pair; npk > 128 -> two pairs per thread
+    float acc0[NU][NU], acc1[NU][NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u)
+#pragma unroll
+      for (int v = 0; v < NU; ++v) acc0[u][v] = acc1[u][v] = 0.f;
+    int R = 1, sl = 0, bp0 = 0, bq0 = 0, bp1 = 0, bq1 = 0;
+    bool h0 = false, h1 = false;
+    auto pair_of = [](int p, int& bp, int& bq) {
+      bq = (int)((sqrtf(8.f * p + 1.f) - 1.f) * 0.5f);
+      while ((bq + 1) * (bq + 2) / 2 <= p) ++bq;
+      while (bq * (bq + 1) / 2 > p) --bq;
+      bp = p - bq * (bq + 1) / 2;
+    };
+    for (int j = 0; j < items; ++j) {
+      const int n = j / nsub, sub = j % nsub;
+      const int s0 = nb + sub * SC, sc = min(SC, ne - s0);
+      const int k = n + 1, b = j & 1, npk = k * (k + 1) / 2;
+      float* Gc = Gc2 + 2 * b * gsz;
+      float* QGc = Gc + gsz;
+      const double* wv = wv2 + b * SC * NX;
+      if (sub == 0) {
+        if (npk <= GT) {
+          R = max(1, min(SC * NX, GT / npk));
+          sl = gt / npk;
+          h0 = sl < R;
+          h1 = false;
+          pair_of(gt % npk, bp0, bq0);
+        } else {
+          R = 1;
+          sl = 0;
+          h0 = true;
+          h1 = gt + GT < npk;
+          pair_of(gt, bp0, bq0);
+          pair_of(min(gt + GT, npk - 1), bp1, bq1);
+        }
+      }
+      qpb_sync(BAR_FULL + b, 256);  // item j from group R
+      // Qs G on the live columns of stage k (group H: balances the groups)
+      {
+        const int lk = k * NU;
+        const float* Qs = Qs2 + b * SC * NX * NX;
+        for (int t = gt; t < sc * lk; t += GT) {
+          const int li = t / lk, col = t - li * lk;
+          const float* Gs = Gc + (int64_t)li * NX * ld + col;
+          float gcol[NX];
+#pragma unroll
+          for (int qq = 0; qq < NX; ++qq) gcol[qq] = Gs[(int64_t)qq * ld];
+          const float* Qn = Qs + li * NX * NX;
+          float* Os = QGc + (int64_t)li * NX * ld + col;
+#pragma unroll
+          for (int r = 0; r < NX; ++r) {
+            float sacc = 0.f;
+#pragma unroll
+            for (int qq = 0; qq < NX; ++qq) sacc = fmaf(Qn[r * NX + qq], gcol[qq], sacc);
+            Os[(int64_t)r * ld] = sacc;
+          }
+        }
+        qpb_sync(BAR_H, GT);
+      }
+      auto hrow = [&](int bp, int bq, float (&acc)[NU][NU]) {
+        for (int row = sl; row < sc * NX; row += R) {
+          const float* gp = Gc + (int64_t)row * ld + bp * NU;
+          const float* gq = QGc + (int64_t)row * ld + bq * NU;
+          const float2 x01 = *reinterpret_cast<const float2*>(gp), x23 = *reinterpret_cast<const float2*>(gp + 2),
+                       x45 = *reinterpret_cast<const float2*>(gp + 4);
+          const float2 y01 = *reinterpret_cast<const float2*>(gq), y23 = *reinterpret_cast<const float2*>(gq + 2),
+                       y45 = *reinterpret_cast<const float2*>(gq + 4);
+          const float x[NU] = {x01.x, x01.y, x23.x, x23.y, x45.x, x45.y};
+          const float y[NU] = {y01.x, y01.y, y23.x, y23.y, y45.x, y45.y};
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int v = 0; v < NU; ++v) acc[u][v] = fmaf(x[u], y[v], acc[u][v]);
+        }
+      };
+      if (h0) hrow(bp0, bq0, acc0);
+      if (h1) hrow(bp1, bq1, acc1);
+      const int lk = k * NU;
+      for (int cidx = gt; cidx < lk; cidx += GT) {
+        double sg = gs[cidx];
+        for (int li = 0; li < sc; ++li)
+#pragma unroll
+          for (int r = 0; r < NX; ++r) sg += (double)Gc[((int64_t)li * NX + r) * ld + cidx] * wv[li * NX + r];
+        gs[cidx] = sg;
+      }
+      if (sub == nsub - 1) {
+        // fold the stage into Hacc through this buffer (group R does not
+        // touch it before our EMPTY arrival): slot gt <- acc0, gt + 128 <- acc1
+        float* stg = Gc;
+        qpb_sync(BAR_H, GT);  // every H thread is done reading buffer b
+        if (h0)
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int v = 0; v < NU; ++v) {
+              stg[gt * NU * NU + u * NU + v] = acc0[u][v];
+              acc0[u][v] = 0.f;
+            }
+        if (h1)
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int v = 0; v < NU; ++v) {
+              stg[(gt + GT) * NU * NU + u * NU + v] = acc1[u][v];
+              acc1[u][v] = 0.f;
+            }
+        qpb_sync(BAR_H, GT);
+        for (int t = gt; t < npk * NU * NU; t += GT) {
+          const int p2 = t / (NU * NU), e = t - p2 * NU * NU;
+          float hs = Hacc[t];
+          for (int s2 = 0; s2 < R; ++s2) hs += stg[(p2 + s2 * npk) * NU * NU + e];
+          Hacc[t] = hs;
+        }
+        qpb_sync(BAR_H, GT);
+      }
+      qpb_arrive(BAR_EMPTY + b, 256);  // buffer b back to group R
+    }
+  }
+  __syncthreads();
+  const int PU = a.npairs * NU * NU;
+  float* P = a.partH + (bi * a.splits + split) * (int64_t)PU;
+  for (int t = tid; t < PU; t += 256) P[t] = Hacc[t];
+  for (int t = tid; t < n0; t += 256) a.partg[(bi * a.splits + split) * n0 + t] = gs[t];
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    int* done = a.flags + (int64_t)gridDim.x;
+    if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
+      for (int s2 = 0; s2 < (int)gridDim.x; ++s2) a.flags[s2] = 0;
+      *done = 0;
+      __threadfence();
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K-COND on the tensor cores (n0 = N*nu <= 128): the same persistent stage
 // wavefront and the same fp32 Gamma recursion as k_condense_fused, but the
@@ -1533,14 +1960,14 @@ int ensure_chunks(gm_ctx* ctx, int SC) {
   return GM_OK;
 }
 
-size_t tma_smem(int SC, int CPS, bool DB, int umax, int ld, int dslot, int n0, int64_t per) {
+size_t tma_smem(int SC, int CPS, bool DB, int umax, int ld, int dslot, int n0, int64_t per, bool pipe = false) {
   const int emax = SC * (dslot - 1) > 0 ? SC * (dslot - 1) : 1;
   const int npass = (ld / 32 + CPS - 1) / CPS;
   size_t b = (size_t)(DB ? 2 : npass) * umax * CPS * kTileBytes;
   b += 2 * stage_bytes<6, 6>(SC, emax);
-  b += sizeof(float) * ((size_t)2 * SC * 6 * ld + (size_t)SC * 36);
+  b += sizeof(float) * ((size_t)(pipe ? 4 : 2) * SC * 6 * ld + (size_t)(pipe ? 2 : 1) * SC * 36);
   b = (b + 15) & ~size_t(15);
-  b += sizeof(double) * ((size_t)SC * 6 + n0);
+  b += sizeof(double) * ((size_t)(pipe ? 2 : 1) * SC * 6 + n0);
   b += sizeof(int) * (size_t)(per + 1);
   const size_t nchk = (size_t)((per + SC - 1) / SC);
   b += sizeof(int) * (nchk + 1 + nchk * umax) + nchk * SC * dslot;
@@ -1595,20 +2022,29 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
   struct Var {
     int cps;
     bool db;
+    bool pipe;
     void (*fn)(const FusedArgs, const CUtensorMap);
   };
-  const Var vars[3] = {{4, true, k_condense_tma<8, 4, 4, true>},
-                       {4, false, k_condense_tma<8, 4, 4, false>},
-                       {2, false, k_condense_tma<8, 2, 2, false>}};
+  // the warp-specialised pipeline first (GM_TMA_PIPE=0 skips it)
+  static const int pipe_env = [] {
+    const char* v = std::getenv("GM_TMA_PIPE");
+    return v ? std::atoi(v) : 1;
+  }();
+  const Var vars[6] = {{4, true, true, k_condense_tmap<8, 4, 4, true>},
+                       {4, false, true, k_condense_tmap<8, 4, 4, false>},
+                       {2, false, true, k_condense_tmap<8, 2, 2, false>},
+                       {4, true, false, k_condense_tma<8, 4, 4, true>},
+                       {4, false, false, k_condense_tma<8, 4, 4, false>},
+                       {2, false, false, k_condense_tma<8, 2, 2, false>}};
   const Var* var = nullptr;
   for (const Var& v : vars)
-    if ((cps_env == 0 || cps_env == v.cps + (v.db ? 10 : 0)) &&
-        tma_smem(SC, v.cps, v.db, ctx->cu_umax, ld, dslot, n0, per) <= budget) {
+    if ((cps_env == 0 || cps_env == v.cps + (v.db ? 10 : 0)) && (pipe_env != 0 || !v.pipe) &&
+        tma_smem(SC, v.cps, v.db, ctx->cu_umax, ld, dslot, n0, per, v.pipe) <= budget) {
       var = &v;
       break;
     }
   if (!var) return 1;
-  const size_t sm = tma_smem(SC, var->cps, var->db, ctx->cu_umax, ld, dslot, n0, per);
+  const size_t sm = tma_smem(SC, var->cps, var->db, ctx->cu_umax, ld, dslot, n0, per, var->pipe);
   auto kfn = var->fn;
   GM_CUDA(ctx, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int occ = 0;
