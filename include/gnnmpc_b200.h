@@ -238,6 +238,12 @@ int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, const double*
  * counters (synchronous). */
 int gm_qp_profile(int on);
 int gm_qp_phase_cycles(unsigned long long* out);
+/* Diagnostics: per-stage cycle accounting of the pipelined K-COND (CTA 0):
+ * 32 stages x 8 counters (group R item / empty-wait / flag-wait / tile-wait,
+ * group H full-wait / busy / fold, items).  gm_cond_profile(1) enables and
+ * zeroes; gm_cond_phase_cycles copies 256 counters (synchronous). */
+int gm_cond_profile(int on);
+int gm_cond_phase_cycles(unsigned long long* out);
 /* Diagnostics: factor a dense SPD matrix A (n x n, row-major, device) with
  * K-QP's own Cholesky and solve A x = b; L (n x n) lower, ok = 0 when a pivot
  * failed.  Used by the tests to check the factorisation in isolation. */

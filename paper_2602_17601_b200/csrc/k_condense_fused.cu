@@ -72,6 +72,8 @@ struct FusedArgs {
   const int* cu_nodes;
   const unsigned char* cu_slot;
   int umax;
+  int qg_r8;  // k_condense_tmap: eighths of the Qs*G columns done by the recursion group
+  int al16;   // every block base 16-byte aligned: 16-byte cp.async for the item blocks
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -859,10 +861,25 @@ __device__ __forceinline__ void qpb_arrive(int id, int n) {
 // of k_condense_tma (same per-column FMA order, fp32 H accumulation folded
 // into the CTA accumulator once per stage in a fixed order, fp64 g).
 // ---------------------------------------------------------------------------
-template <int SC, int CPS, int GW, bool DB>
-__global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, const __grid_constant__ CUtensorMap tm) {
+// optional per-stage cycle accounting of k_condense_tmap (CTA 0; one thread
+// per group): per stage k (< 32) 8 counters -- [0] group R item time, [1] R
+// waiting for buffer EMPTY, [2] R waiting on neighbour stage flags, [3] R
+// waiting for its TMA tiles, [4] group H waiting for FULL, [5] H busy, [6] H
+// stage fold, [7] items; [8..11] R: blocks-in barrier + issue, Qs, recursion
+// passes, flag + w; [12..15] H: Qs*G + barrier, H rows, g, rest.
+// gm_cond_profile(1) enables + zeroes.
+__device__ unsigned long long g_cond_prof[32 * 24];
+__device__ int g_cond_prof_on;
+__device__ __forceinline__ long long cprof_clock(bool on) { return on ? clock64() : 0; }
+__device__ __forceinline__ void cprof_add(bool on, int k, int slot, long long v) {
+  if (on && k < 32) atomicAdd(&g_cond_prof[k * 24 + slot], (unsigned long long)v);
+}
+
+template <int SC, int CPS, int GW, bool DB, int GH>
+__global__ void __launch_bounds__(128 + GH, 1) k_condense_tmap(const FusedArgs a, const __grid_constant__ CUtensorMap tm) {
   constexpr int NX = 6, NU = 6;
-  constexpr int GT = 128;  // threads per group
+  constexpr int GT = 128;       // group R threads (group H: GH)
+  constexpr int NT = GT + GH;
   constexpr int BAR_R = 1, BAR_H = 2, BAR_FULL = 3, BAR_EMPTY = 5;  // FULL / EMPTY: + buffer
   extern __shared__ __align__(128) unsigned char smraw[];
   const int N = a.N, ld = a.ld, M = a.M;
@@ -905,22 +922,22 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
   float* Hacc = (float*)(((uintptr_t)(cslot + nchk * SC * a.dslot) + 15) & ~(uintptr_t)15);
   uint64_t* mb = (uint64_t*)(Hacc + a.npairs * NU * NU);
 
-  for (int t = tid; t <= nn; t += 256) nptr[t] = a.ptr[nb + t];
+  for (int t = tid; t <= nn; t += NT) nptr[t] = a.ptr[nb + t];
   {
     const int c0p = a.cu_ptr[chunk0];
-    for (int t = tid; t <= nsub; t += 256) cptr[t] = a.cu_ptr[chunk0 + t] - c0p;
-    for (int t = tid; t < a.cu_ptr[chunk0 + nsub] - c0p; t += 256) cnod[t] = a.cu_nodes[c0p + t];
-    for (int t = tid; t < nsub * SC * a.dslot; t += 256) cslot[t] = a.cu_slot[(int64_t)chunk0 * SC * a.dslot + t];
+    for (int t = tid; t <= nsub; t += NT) cptr[t] = a.cu_ptr[chunk0 + t] - c0p;
+    for (int t = tid; t < a.cu_ptr[chunk0 + nsub] - c0p; t += NT) cnod[t] = a.cu_nodes[c0p + t];
+    for (int t = tid; t < nsub * SC * a.dslot; t += NT) cslot[t] = a.cu_slot[(int64_t)chunk0 * SC * a.dslot + t];
   }
-  for (int t = tid; t < n0; t += 256) gs[t] = 0.0;
-  for (int t = tid; t < a.npairs * NU * NU; t += 256) Hacc[t] = 0.f;
+  for (int t = tid; t < n0; t += NT) gs[t] = 0.0;
+  for (int t = tid; t < a.npairs * NU * NU; t += NT) Hacc[t] = 0.f;
   if (tid == 0) {
     umma::mbar_init(&mb[0], 1);
     umma::mbar_init(&mb[1], 1);
   }
   const int items = N * nsub;
   // stage 0: Gamma_u = 0, Gamma_x = x0 (condensing.py:205-206)
-  for (int t = tid; t < nn * NX * ld; t += 256) {
+  for (int t = tid; t < nn * NX * ld; t += NT) {
     const int li = t / (NX * ld), rem = t - li * NX * ld, r = rem / ld, col = rem - r * ld;
     Wb[(int64_t)(nb + li) * node_stride + rem] = (col == XC) ? (float)a.x0[(bi * M + nb + li) * NX + r] : 0.f;
   }
@@ -930,9 +947,30 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
     st_release(&flags[split], 1);
   }
 
+  // QGc = Qs Gc on flattened (node, column) indices [t0, t1) of the live columns
+  auto qg_cols = [&](const float* Gc, const float* Qs, float* QGc, int lk, int t0, int t1) {
+    for (int t = t0 + gt; t < t1; t += (grpR ? GT : GH)) {
+      const int li = t / lk, col = t - li * lk;
+      const float* Gs = Gc + (int64_t)li * NX * ld + col;
+      float gcol[NX];
+#pragma unroll
+      for (int qq = 0; qq < NX; ++qq) gcol[qq] = Gs[(int64_t)qq * ld];
+      const float* Qn = Qs + li * NX * NX;
+      float* Os = QGc + (int64_t)li * NX * ld + col;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) {
+        float sacc = 0.f;
+#pragma unroll
+        for (int qq = 0; qq < NX; ++qq) sacc = fmaf(Qn[r * NX + qq], gcol[qq], sacc);
+        Os[(int64_t)r * ld] = sacc;
+      }
+    }
+  };
+
   if (grpR) {
-    // ===================== group R: tiles, recursion, QG =====================
+    // ===================== group R: tiles, recursion, part of QG =====================
     const int lane = tid & 31;
+    const bool pf = g_cond_prof_on && blockIdx.x == 0 && gt == 0;
     auto prefetch = [&](int j) {
       const int n = j / nsub, s0 = nb + (j % nsub) * SC;
       const int sc = min(SC, ne - s0), k = n + 1;
@@ -940,6 +978,28 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
       const int64_t pstage = bi * N + n;
       const int eb = nptr[s0 - nb], ee = nptr[s0 - nb + sc];
       const int nE = ee - eb;
+      if (a.al16) {  // 16-byte units: A 9 per node / edge, B 9, c 3, Q 18, x_ref 3
+        const char* gas = (const char*)(a.a_self + (pstage * M + s0) * NX * NX);
+        for (int t = gt; t < sc * 9; t += GT) cp_async16((char*)S.as + 16 * t, gas + 16 * t);
+        const char* gan = (const char*)(a.a_nbr + (pstage * a.E + eb) * NX * NX);
+        for (int t = gt; t < nE * 9; t += GT) cp_async16((char*)S.an + 16 * t, gan + 16 * t);
+        const char* gb = (const char*)(a.b + (pstage * M + s0) * NX * NU);
+        for (int t = gt; t < sc * 9; t += GT) cp_async16((char*)S.bb + 16 * t, gb + 16 * t);
+        const char* gc = (const char*)(a.c + (pstage * M + s0) * NX);
+        for (int t = gt; t < sc * 3; t += GT) cp_async16((char*)S.cc + 16 * t, gc + 16 * t);
+        for (int t = gt; t < sc * 18; t += GT) {
+          const int li = t / 18, e = t - li * 18;
+          cp_async16((char*)(S.qd + li * NX * NX) + 16 * e,
+                     (const char*)(a.q + bi * a.q_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX * NX) + 16 * e);
+        }
+        for (int t = gt; t < sc * 3; t += GT) {
+          const int li = t / 3, e = t - li * 3;
+          cp_async16((char*)(S.xd + li * NX) + 16 * e,
+                     (const char*)(a.xref + bi * a.xref_stride + ((int64_t)(s0 + li) * (N + 1) + k) * NX) + 16 * e);
+        }
+        cp_async_commit();
+        return;
+      }
       const float* gas = a.a_self + (pstage * M + s0) * NX * NX;
       for (int t = gt; t < sc * NX * NX; t += GT) cp_async4(S.as + t, gas + t);
       if (nE > 0) {
@@ -960,7 +1020,9 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
       }
       cp_async_commit();
     };
-    auto issue_half = [&](int j, int h) {  // warp 0
+    // tiles of item j, pass h: called by every group-R thread; unique node u
+    // goes to warp u % 4 (lane u / 4), so the four warps issue in parallel
+    auto issue_half = [&](int j, int h) {
       const int n = j / nsub, sub = j % nsub;
       const int u0 = cptr[sub], U = cptr[sub + 1] - u0;
       const int nlive = (NU * n + 31) / 32, xch = XC / 32;
@@ -970,15 +1032,17 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
       const int slotw = DB ? (j & 1) : h;
       float* dst = slotw ? nbuf1 : nbuf0;
       uint64_t* bar = &mb[slotw];
-      if (lane == 0) mbar_expect_tx(bar, (uint32_t)(U * cnt * kTileBytes));
-      __syncwarp();
+      // one box of 6 rows x 32*CPS columns per unique node (the tensor map
+      // of this kernel): dead columns ride along (zeros in W)
+      // (complete_tx may precede the expect: the tx-count goes transiently
+      // negative, the phase still needs gt 0's single arrival)
+      if (gt == 0) mbar_expect_tx(bar, cnt ? (uint32_t)(U * CPS * kTileBytes) : 0u);
       if (cnt == 0) return;
-      for (int u = lane; u < U; u += 32) {
+      const int ub = (gt & 31) * 4 + (gt >> 5);
+      if (ub < U) fence_proxy_async_global();
+      for (int u = ub; u < U; u += GT) {
         const int row = (int)(((bi * M + cnod[u0 + u]) * (N + 1) + n) * NX);
-        fence_proxy_async_global();
-        for (int ch = cb; ch < ceo; ++ch)
-          if (ch < nlive || ch == xch)
-            tma_load_2d(dst + (u * CPS + (ch - cb)) * (kTileBytes / 4), &tm, ch * 32, row, bar);
+        tma_load_2d(dst + u * CPS * (kTileBytes / 4), &tm, cb * 32, row, bar);
       }
     };
     const int d0 = a.dep_ptr[split], d1 = a.dep_ptr[split + 1];
@@ -990,14 +1054,21 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
       const Stage<NX, NU> S = stage_at<NX, NU>(sbase + (j & 1) * sbytes, SC, emax);
       float* Gc = Gc2 + 2 * b * gsz;
       double* wv = wv2 + b * SC * NX;
+      const long long pt0 = cprof_clock(pf);
       if (sub == 0)
         for (int d = d0 + gt; d < d1; d += GT) {
           const int* f = &flags[a.dep[d]];
           while (ld_acquire(f) < k) __nanosleep(32);
         }
+      cprof_add(pf, k, 2, cprof_clock(pf) - pt0);
+      const long long pq0 = cprof_clock(pf);
       cp_async_wait_all();
+      const long long pq1 = cprof_clock(pf);
+      cprof_add(pf, k, 16, pq1 - pq0);
       qpb_sync(BAR_R, GT);  // blocks of item j in; the previous recursion left the tile slots
-      if (tid < 32) {
+      const long long pq2 = cprof_clock(pf);
+      cprof_add(pf, k, 17, pq2 - pq1);
+      {
         if (sub == 0) issue_half(j, 0);
         if (DB) {
           if (j + 1 < items && (j + 1) / nsub == n) issue_half(j + 1, 0);
@@ -1005,8 +1076,14 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
           for (int h = 1; h < npass; ++h) issue_half(j, h);
         }
       }
+      const long long pq3 = cprof_clock(pf);
+      cprof_add(pf, k, 18, pq3 - pq2);
       if (j + 1 < items) prefetch(j + 1);
-      if (j >= 2) qpb_sync(BAR_EMPTY + b, 256);  // group H is done with buffer b (item j-2)
+      const long long pt1 = cprof_clock(pf);
+      cprof_add(pf, k, 19, pt1 - pq3);
+      cprof_add(pf, k, 8, pt1 - pt0);
+      if (j >= 2) qpb_sync(BAR_EMPTY + b, NT);  // group H is done with buffer b (item j-2)
+      cprof_add(pf, k, 1, cprof_clock(pf) - pt1);
       float* Qs = Qs2 + b * SC * NX * NX;
       for (int t = gt; t < sc * NX * NX; t += GT) {
         const int li = t / (NX * NX), e = t - li * NX * NX, r = e / NX, cc = e - r * NX;
@@ -1015,11 +1092,15 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
       }
       const int ebase = nptr[s0 - nb];
       const unsigned char* slot = cslot + sub * SC * a.dslot;
+      const long long pt3 = cprof_clock(pf);
+      cprof_add(pf, k, 9, pt3 - pt1);
 #pragma unroll 1
       for (int h = 0; h < npass; ++h) {
         const int cb0 = 32 * CPS * h, ncol = min(32 * CPS, ld - cb0);
         const int slotr = DB ? (j & 1) : h;
+        const long long pt2 = cprof_clock(pf);
         umma::mbar_wait(&mb[slotr], (uint32_t)(DB ? ((j >> 1) & 1) : (j & 1)));
+        cprof_add(pf, k, 3, cprof_clock(pf) - pt2);
         const float* nbuf = slotr ? nbuf1 : nbuf0;
         const int G2 = ncol / GW;
         for (int t = gt; t < sc * G2; t += GT) {
@@ -1035,18 +1116,18 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
             const int el0 = nptr[i - nb] - ebase, deg = nptr[i - nb + 1] - nptr[i - nb];
             for (int ss = 0; ss <= deg; ++ss) {
               const int u = slot[li * a.dslot + ss];
-              const float* g = nbuf + (u * CPS + ((c0 >> 5) - CPS * h)) * (kTileBytes / 4) + (c0 & 31);
+              const float* g = nbuf + u * CPS * (kTileBytes / 4) + (c0 - 32 * CPS * h);
               float w[NX][GW];
 #pragma unroll
               for (int qq = 0; qq < NX; ++qq) {
                 if (GW == 4) {
-                  const float4 v = *reinterpret_cast<const float4*>(g + qq * 32);
+                  const float4 v = *reinterpret_cast<const float4*>(g + qq * 32 * CPS);
                   w[qq][0] = v.x;
                   w[qq][GW > 1 ? 1 : 0] = v.y;
                   w[qq][GW > 2 ? 2 : 0] = v.z;
                   w[qq][GW > 3 ? 3 : 0] = v.w;
                 } else {
-                  const float2 v = *reinterpret_cast<const float2*>(g + qq * 32);
+                  const float2 v = *reinterpret_cast<const float2*>(g + qq * 32 * CPS);
                   w[qq][0] = v.x;
                   w[qq][GW > 1 ? 1 : 0] = v.y;
                 }
@@ -1103,11 +1184,17 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
           }
         }
         qpb_sync(BAR_R, GT);  // Gamma rows of the pass written; its tile slot is free again
-        if (!DB && h == 0 && tid < 32 && j + 1 < items && (j + 1) / nsub == n) issue_half(j + 1, 0);
+        if (!DB && h == 0 && j + 1 < items && (j + 1) / nsub == n) issue_half(j + 1, 0);
       }
+      const long long pt4 = cprof_clock(pf);
+      cprof_add(pf, k, 10, pt4 - pt3);
       if (sub == nsub - 1 && gt == 0) {
         __threadfence();
         st_release(&flags[split], k + 1);
+      }
+      {
+        const int nq = sc * k * NU;
+        qg_cols(Gc, Qs, Gc + gsz, k * NU, 0, nq * a.qg_r8 / 8);
       }
       for (int t = gt; t < sc * NX; t += GT) {
         const int li = t / NX, r = t - li * NX;
@@ -1123,10 +1210,13 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
         wv[t] = 2.0 * qg + (-2.0 * qx);
       }
       __threadfence_block();
-      qpb_arrive(BAR_FULL + b, 256);  // item j -> group H
+      qpb_arrive(BAR_FULL + b, NT);  // item j -> group H
+      cprof_add(pf, k, 11, cprof_clock(pf) - pt4);
+      cprof_add(pf, k, 0, cprof_clock(pf) - pt0);
+      cprof_add(pf, k, 7, 1);
     }
     // consume group H's last EMPTY arrivals (balanced barrier phases)
-    for (int j = max(items, 2); j < items + 2; ++j) qpb_sync(BAR_EMPTY + (j & 1), 256);
+    for (int j = max(items, 2); j < items + 2; ++j) qpb_sync(BAR_EMPTY + (j & 1), NT);
   } else {
     // ===================== group H: H and g =====================
     // stage k: npk = k(k+1)/2 live block pairs over 128 threads: npk <= 128
@@ -1152,8 +1242,8 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
       float* QGc = Gc + gsz;
       const double* wv = wv2 + b * SC * NX;
       if (sub == 0) {
-        if (npk <= GT) {
-          R = max(1, min(SC * NX, GT / npk));
+        if (npk <= GH) {
+          R = max(1, min(SC * NX, GH / npk));
           sl = gt / npk;
           h0 = sl < R;
           h1 = false;
@@ -1162,34 +1252,24 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
           R = 1;
           sl = 0;
           h0 = true;
-          h1 = gt + GT < npk;
+          h1 = gt + GH < npk;
           pair_of(gt, bp0, bq0);
-          pair_of(min(gt + GT, npk - 1), bp1, bq1);
+          pair_of(min(gt + GH, npk - 1), bp1, bq1);
         }
       }
-      qpb_sync(BAR_FULL + b, 256);  // item j from group R
+      const bool pf = g_cond_prof_on && blockIdx.x == 0 && gt == 0;
+      const long long ph0 = cprof_clock(pf);
+      qpb_sync(BAR_FULL + b, NT);  // item j from group R
+      const long long ph1 = cprof_clock(pf);
+      cprof_add(pf, k, 4, ph1 - ph0);
       // Qs G on the live columns of stage k (group H: balances the groups)
       {
-        const int lk = k * NU;
-        const float* Qs = Qs2 + b * SC * NX * NX;
-        for (int t = gt; t < sc * lk; t += GT) {
-          const int li = t / lk, col = t - li * lk;
-          const float* Gs = Gc + (int64_t)li * NX * ld + col;
-          float gcol[NX];
-#pragma unroll
-          for (int qq = 0; qq < NX; ++qq) gcol[qq] = Gs[(int64_t)qq * ld];
-          const float* Qn = Qs + li * NX * NX;
-          float* Os = QGc + (int64_t)li * NX * ld + col;
-#pragma unroll
-          for (int r = 0; r < NX; ++r) {
-            float sacc = 0.f;
-#pragma unroll
-            for (int qq = 0; qq < NX; ++qq) sacc = fmaf(Qn[r * NX + qq], gcol[qq], sacc);
-            Os[(int64_t)r * ld] = sacc;
-          }
-        }
-        qpb_sync(BAR_H, GT);
+        const int nq = sc * k * NU;
+        qg_cols(Gc, Qs2 + b * SC * NX * NX, QGc, k * NU, nq * a.qg_r8 / 8, nq);
+        qpb_sync(BAR_H, GH);
       }
+      const long long ph3 = cprof_clock(pf);
+      cprof_add(pf, k, 12, ph3 - ph1);
       auto hrow = [&](int bp, int bq, float (&acc)[NU][NU]) {
         for (int row = sl; row < sc * NX; row += R) {
           const float* gp = Gc + (int64_t)row * ld + bp * NU;
@@ -1208,19 +1288,23 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
       };
       if (h0) hrow(bp0, bq0, acc0);
       if (h1) hrow(bp1, bq1, acc1);
+      const long long ph4 = cprof_clock(pf);
+      cprof_add(pf, k, 13, ph4 - ph3);
       const int lk = k * NU;
-      for (int cidx = gt; cidx < lk; cidx += GT) {
+      for (int cidx = gt; cidx < lk; cidx += GH) {
         double sg = gs[cidx];
         for (int li = 0; li < sc; ++li)
 #pragma unroll
           for (int r = 0; r < NX; ++r) sg += (double)Gc[((int64_t)li * NX + r) * ld + cidx] * wv[li * NX + r];
         gs[cidx] = sg;
       }
+      const long long ph2 = cprof_clock(pf);
+      cprof_add(pf, k, 14, ph2 - ph4);
       if (sub == nsub - 1) {
         // fold the stage into Hacc through this buffer (group R does not
         // touch it before our EMPTY arrival): slot gt <- acc0, gt + 128 <- acc1
         float* stg = Gc;
-        qpb_sync(BAR_H, GT);  // every H thread is done reading buffer b
+        qpb_sync(BAR_H, GH);  // every H thread is done reading buffer b
         if (h0)
 #pragma unroll
           for (int u = 0; u < NU; ++u)
@@ -1234,26 +1318,28 @@ __global__ void __launch_bounds__(256, 1) k_condense_tmap(const FusedArgs a, con
           for (int u = 0; u < NU; ++u)
 #pragma unroll
             for (int v = 0; v < NU; ++v) {
-              stg[(gt + GT) * NU * NU + u * NU + v] = acc1[u][v];
+              stg[(gt + GH) * NU * NU + u * NU + v] = acc1[u][v];
               acc1[u][v] = 0.f;
             }
-        qpb_sync(BAR_H, GT);
-        for (int t = gt; t < npk * NU * NU; t += GT) {
+        qpb_sync(BAR_H, GH);
+        for (int t = gt; t < npk * NU * NU; t += GH) {
           const int p2 = t / (NU * NU), e = t - p2 * NU * NU;
           float hs = Hacc[t];
           for (int s2 = 0; s2 < R; ++s2) hs += stg[(p2 + s2 * npk) * NU * NU + e];
           Hacc[t] = hs;
         }
-        qpb_sync(BAR_H, GT);
+        qpb_sync(BAR_H, GH);
       }
-      qpb_arrive(BAR_EMPTY + b, 256);  // buffer b back to group R
+      qpb_arrive(BAR_EMPTY + b, NT);  // buffer b back to group R
+      cprof_add(pf, k, 5, cprof_clock(pf) - ph1);
+      cprof_add(pf, k, 6, cprof_clock(pf) - ph2);
     }
   }
   __syncthreads();
   const int PU = a.npairs * NU * NU;
   float* P = a.partH + (bi * a.splits + split) * (int64_t)PU;
-  for (int t = tid; t < PU; t += 256) P[t] = Hacc[t];
-  for (int t = tid; t < n0; t += 256) a.partg[(bi * a.splits + split) * n0 + t] = gs[t];
+  for (int t = tid; t < PU; t += NT) P[t] = Hacc[t];
+  for (int t = tid; t < n0; t += NT) a.partg[(bi * a.splits + split) * n0 + t] = gs[t];
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -2024,21 +2110,34 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
     bool db;
     bool pipe;
     void (*fn)(const FusedArgs, const CUtensorMap);
+    int threads;
   };
   // the warp-specialised pipeline first (GM_TMA_PIPE=0 skips it)
   static const int pipe_env = [] {
     const char* v = std::getenv("GM_TMA_PIPE");
     return v ? std::atoi(v) : 1;
   }();
-  const Var vars[6] = {{4, true, true, k_condense_tmap<8, 4, 4, true>},
-                       {4, false, true, k_condense_tmap<8, 4, 4, false>},
-                       {2, false, true, k_condense_tmap<8, 2, 2, false>},
-                       {4, true, false, k_condense_tma<8, 4, 4, true>},
-                       {4, false, false, k_condense_tma<8, 4, 4, false>},
-                       {2, false, false, k_condense_tma<8, 2, 2, false>}};
+  // pipeline group H size: 256 threads (GM_TMA_GH=128: 128); the fold of a
+  // stage stages max(GH, npk) 6x6 pairs in the 2 * SC*6*ld floats of a buffer
+  static const int gh_env = [] {
+    const char* v = std::getenv("GM_TMA_GH");
+    return v ? std::atoi(v) : 256;
+  }();
+  const Var vars[9] = {{4, true, true, k_condense_tmap<8, 4, 4, true, 256>, 384},
+                       {4, false, true, k_condense_tmap<8, 4, 4, false, 256>, 384},
+                       {2, false, true, k_condense_tmap<8, 2, 2, false, 256>, 384},
+                       {4, true, true, k_condense_tmap<8, 4, 4, true, 128>, 256},
+                       {4, false, true, k_condense_tmap<8, 4, 4, false, 128>, 256},
+                       {2, false, true, k_condense_tmap<8, 2, 2, false, 128>, 256},
+                       {4, true, false, k_condense_tma<8, 4, 4, true>, 256},
+                       {4, false, false, k_condense_tma<8, 4, 4, false>, 256},
+                       {2, false, false, k_condense_tma<8, 2, 2, false>, 256}};
+  const int npk_max = N * (N + 1) / 2;
   const Var* var = nullptr;
   for (const Var& v : vars)
     if ((cps_env == 0 || cps_env == v.cps + (v.db ? 10 : 0)) && (pipe_env != 0 || !v.pipe) &&
+        (!v.pipe || (v.threads - 128 == gh_env && npk_max <= 2 * (v.threads - 128) &&
+                     36 * std::max(v.threads - 128, npk_max) <= 2 * SC * 6 * ld)) &&
         tma_smem(SC, v.cps, v.db, ctx->cu_umax, ld, dslot, n0, per, v.pipe) <= budget) {
       var = &v;
       break;
@@ -2048,7 +2147,7 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
   auto kfn = var->fn;
   GM_CUDA(ctx, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int occ = 0;
-  GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 256, sm));
+  GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, var->threads, sm));
   if (occ < 1) return 1;
   const int splits = (int)((M + per - 1) / per);
   const int64_t grid = (int64_t)B * splits;
@@ -2061,7 +2160,9 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
   CUtensorMap tm;
   const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)B * M * (N + 1) * 6};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  const cuuint32_t box[2] = {32, 6};
+  // box: one 32-column chunk (k_condense_tma), or the whole pass of 32*CPS
+  // columns (k_condense_tmap: one TMA per unique node and pass)
+  const cuuint32_t box[2] = {var->pipe ? (cuuint32_t)(32 * var->cps) : 32u, 6};
   const cuuint32_t estr[2] = {1, 1};
   if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)gamma, dims, strides, box, estr,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -2108,10 +2209,20 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
   a.cu_nodes = ctx->d_cu_nodes;
   a.cu_slot = ctx->d_cu_slot;
   a.umax = ctx->cu_umax;
+  // Qs*Gamma split between the pipeline's groups (measured: all in group H, 0/8, is fastest)
+  static const int qg_env = [] {
+    const char* v = std::getenv("GM_TMA_QGR");
+    return v ? std::max(0, std::min(8, std::atoi(v))) : 0;
+  }();
+  a.qg_r8 = qg_env;
+  a.al16 = ((((uintptr_t)a_self | (uintptr_t)a_nbr | (uintptr_t)b | (uintptr_t)c | (uintptr_t)q |
+              (uintptr_t)x_ref) & 15) == 0 && (q_stride % 2) == 0 && (xref_stride % 2) == 0)
+               ? 1
+               : 0;
   cudaStream_t st = (cudaStream_t)stream;
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3((unsigned)grid);
-  lc.blockDim = dim3(256);
+  lc.blockDim = dim3((unsigned)var->threads);
   lc.dynamicSmemBytes = sm;
   lc.stream = st;
   cudaLaunchAttribute attr[1];
@@ -2454,3 +2565,16 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
 }
 
 }  // extern "C"
+
+extern "C" int gm_cond_profile(int on) {
+  on = on != 0 ? 1 : 0;
+  cudaMemcpyToSymbol(g_cond_prof_on, &on, sizeof(int));
+  static const unsigned long long z[32 * 24] = {0};
+  cudaMemcpyToSymbol(g_cond_prof, z, sizeof(z));
+  return GM_OK;
+}
+
+extern "C" int gm_cond_phase_cycles(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_cond_prof, sizeof(unsigned long long) * 32 * 24) == cudaSuccess ? GM_OK
+                                                                                                    : GM_ERR_CUDA;
+}
