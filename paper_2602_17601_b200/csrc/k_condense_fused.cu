@@ -74,6 +74,7 @@ struct FusedArgs {
   int umax;
   int qg_r8;  // k_condense_tmap: eighths of the Qs*G columns done by the recursion group
   int al16;   // every block base 16-byte aligned: 16-byte cp.async for the item blocks
+  int hacc_gl;  // k_condense_tmap: H accumulator in the global partial (shared memory too small)
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -901,7 +902,9 @@ __global__ void __launch_bounds__(128 + GH, 1) k_condense_tmap(const FusedArgs a
   float* Wb = a.W + bi * (int64_t)M * node_stride;
 
   // shared memory: tile ring | 2 block stages | 2 x (Gc, QGc) | Qs | 2 x wv |
-  // gs | nptr | chunk tables | Hacc | mbarriers
+  // gs | nptr | chunk tables | Hacc | mbarriers.  When shared memory is
+  // short (meshes), Hacc is the CTA's fp32 partial in global memory instead
+  // (folded once per stage, L2-resident)
   const int npass = (NCH + CPS - 1) / CPS;
   const size_t ring = (size_t)a.umax * CPS * kTileBytes;
   const int nslot = DB ? 2 : npass;
@@ -919,8 +922,10 @@ __global__ void __launch_bounds__(128 + GH, 1) k_condense_tmap(const FusedArgs a
   int* cptr = nptr + a.per + 1;
   int* cnod = cptr + nchk + 1;
   unsigned char* cslot = (unsigned char*)(cnod + nchk * a.umax);
-  float* Hacc = (float*)(((uintptr_t)(cslot + nchk * SC * a.dslot) + 15) & ~(uintptr_t)15);
-  uint64_t* mb = (uint64_t*)(Hacc + a.npairs * NU * NU);
+  float* Hs = (float*)(((uintptr_t)(cslot + nchk * SC * a.dslot) + 15) & ~(uintptr_t)15);
+  uint64_t* mb = (uint64_t*)(a.hacc_gl ? Hs : Hs + a.npairs * NU * NU);
+  float* const P = a.partH + (bi * a.splits + split) * (int64_t)(a.npairs * NU * NU);
+  float* Hacc = a.hacc_gl ? P : Hs;
 
   for (int t = tid; t <= nn; t += NT) nptr[t] = a.ptr[nb + t];
   {
@@ -1336,9 +1341,8 @@ __global__ void __launch_bounds__(128 + GH, 1) k_condense_tmap(const FusedArgs a
     }
   }
   __syncthreads();
-  const int PU = a.npairs * NU * NU;
-  float* P = a.partH + (bi * a.splits + split) * (int64_t)PU;
-  for (int t = tid; t < PU; t += NT) P[t] = Hacc[t];
+  if (!a.hacc_gl)
+    for (int t = tid; t < a.npairs * NU * NU; t += NT) P[t] = Hacc[t];
   for (int t = tid; t < n0; t += NT) a.partg[(bi * a.splits + split) * n0 + t] = gs[t];
   __syncthreads();
   if (tid == 0) {
@@ -2046,7 +2050,8 @@ int ensure_chunks(gm_ctx* ctx, int SC) {
   return GM_OK;
 }
 
-size_t tma_smem(int SC, int CPS, bool DB, int umax, int ld, int dslot, int n0, int64_t per, bool pipe = false) {
+size_t tma_smem(int SC, int CPS, bool DB, int umax, int ld, int dslot, int n0, int64_t per, bool pipe = false,
+                bool hacc_smem = true) {
   const int emax = SC * (dslot - 1) > 0 ? SC * (dslot - 1) : 1;
   const int npass = (ld / 32 + CPS - 1) / CPS;
   size_t b = (size_t)(DB ? 2 : npass) * umax * CPS * kTileBytes;
@@ -2059,7 +2064,7 @@ size_t tma_smem(int SC, int CPS, bool DB, int umax, int ld, int dslot, int n0, i
   b += sizeof(int) * (nchk + 1 + nchk * umax) + nchk * SC * dslot;
   b = (b + 15) & ~size_t(15);
   const int N = n0 / 6;
-  b += sizeof(float) * (size_t)(N * (N + 1) / 2) * 36;  // Hacc
+  if (hacc_smem) b += sizeof(float) * (size_t)(N * (N + 1) / 2) * 36;  // Hacc
   return b + 2 * sizeof(uint64_t) + 16;
 }
 
@@ -2138,12 +2143,16 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
     if ((cps_env == 0 || cps_env == v.cps + (v.db ? 10 : 0)) && (pipe_env != 0 || !v.pipe) &&
         (!v.pipe || (v.threads - 128 == gh_env && npk_max <= 2 * (v.threads - 128) &&
                      36 * std::max(v.threads - 128, npk_max) <= 2 * SC * 6 * ld)) &&
-        tma_smem(SC, v.cps, v.db, ctx->cu_umax, ld, dslot, n0, per, v.pipe) <= budget) {
+        tma_smem(SC, v.cps, v.db, ctx->cu_umax, ld, dslot, n0, per, v.pipe, !v.pipe) <= budget) {
       var = &v;
       break;
     }
   if (!var) return 1;
-  const size_t sm = tma_smem(SC, var->cps, var->db, ctx->cu_umax, ld, dslot, n0, per, var->pipe);
+  // the pipeline keeps its H accumulator on chip when that fits (chains),
+  // else in its global partial (meshes: 26-row tile ring)
+  const bool hacc_smem =
+      !var->pipe || tma_smem(SC, var->cps, var->db, ctx->cu_umax, ld, dslot, n0, per, true, true) <= budget;
+  const size_t sm = tma_smem(SC, var->cps, var->db, ctx->cu_umax, ld, dslot, n0, per, var->pipe, hacc_smem);
   auto kfn = var->fn;
   GM_CUDA(ctx, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int occ = 0;
@@ -2215,6 +2224,7 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
     return v ? std::max(0, std::min(8, std::atoi(v))) : 0;
   }();
   a.qg_r8 = qg_env;
+  a.hacc_gl = hacc_smem ? 0 : 1;
   a.al16 = ((((uintptr_t)a_self | (uintptr_t)a_nbr | (uintptr_t)b | (uintptr_t)c | (uintptr_t)q |
               (uintptr_t)x_ref) & 15) == 0 && (q_stride % 2) == 0 && (xref_stride % 2) == 0)
                ? 1
