@@ -876,10 +876,10 @@ __device__ __forceinline__ void cprof_add(bool on, int k, int slot, long long v)
   if (on && k < 32) atomicAdd(&g_cond_prof[k * 24 + slot], (unsigned long long)v);
 }
 
-template <int SC, int CPS, int GW, bool DB, int GH>
-__global__ void __launch_bounds__(128 + GH, 1) k_condense_tmap(const FusedArgs a, const __grid_constant__ CUtensorMap tm) {
+template <int SC, int CPS, int GW, bool DB, int GH, int GR = 128>
+__global__ void __launch_bounds__(GR + GH, 1) k_condense_tmap(const FusedArgs a, const __grid_constant__ CUtensorMap tm) {
   constexpr int NX = 6, NU = 6;
-  constexpr int GT = 128;       // group R threads (group H: GH)
+  constexpr int GT = GR;        // group R threads (group H: GH)
   constexpr int NT = GT + GH;
   constexpr int BAR_R = 1, BAR_H = 2, BAR_FULL = 3, BAR_EMPTY = 5;  // FULL / EMPTY: + buffer
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -1026,7 +1026,7 @@ __global__ void __launch_bounds__(128 + GH, 1) k_condense_tmap(const FusedArgs a
       cp_async_commit();
     };
     // tiles of item j, pass h: called by every group-R thread; unique node u
-    // goes to warp u % 4 (lane u / 4), so the four warps issue in parallel
+    // goes to warp u % (GR/32), so the group's warps issue in parallel
     auto issue_half = [&](int j, int h) {
       const int n = j / nsub, sub = j % nsub;
       const int u0 = cptr[sub], U = cptr[sub + 1] - u0;
@@ -1043,7 +1043,7 @@ __global__ void __launch_bounds__(128 + GH, 1) k_condense_tmap(const FusedArgs a
       // negative, the phase still needs gt 0's single arrival)
       if (gt == 0) mbar_expect_tx(bar, cnt ? (uint32_t)(U * CPS * kTileBytes) : 0u);
       if (cnt == 0) return;
-      const int ub = (gt & 31) * 4 + (gt >> 5);
+      const int ub = (gt & 31) * (GT / 32) + (gt >> 5);
       if (ub < U) fence_proxy_async_global();
       for (int u = ub; u < U; u += GT) {
         const int row = (int)(((bi * M + cnod[u0 + u]) * (N + 1) + n) * NX);
@@ -1271,6 +1271,7 @@ __global__ void __launch_bounds__(128 + GH, 1) k_condense_tmap(const FusedArgs a
       {
         const int nq = sc * k * NU;
         qg_cols(Gc, Qs2 + b * SC * NX * NX, QGc, k * NU, nq * a.qg_r8 / 8, nq);
+        cprof_add(pf, k, 21, cprof_clock(pf) - ph1);
         qpb_sync(BAR_H, GH);
       }
       const long long ph3 = cprof_clock(pf);
@@ -2116,6 +2117,7 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
     bool pipe;
     void (*fn)(const FusedArgs, const CUtensorMap);
     int threads;
+    int gr = 128;  // pipeline: recursion group size
   };
   // the warp-specialised pipeline first (GM_TMA_PIPE=0 skips it)
   static const int pipe_env = [] {
@@ -2124,10 +2126,13 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
   }();
   // pipeline group H size: 256 threads (GM_TMA_GH=128: 128); the fold of a
   // stage stages max(GH, npk) 6x6 pairs in the 2 * SC*6*ld floats of a buffer
+  // (a 256-thread recursion group with 128 H threads measured slower on
+  // both chains and meshes: cfg4 22.9 vs 20.8 ms, cfg5 11.8 vs 11.2 ms)
   static const int gh_env = [] {
     const char* v = std::getenv("GM_TMA_GH");
     return v ? std::atoi(v) : 256;
   }();
+  const int gr_want = 128;
   const Var vars[9] = {{4, true, true, k_condense_tmap<8, 4, 4, true, 256>, 384},
                        {4, false, true, k_condense_tmap<8, 4, 4, false, 256>, 384},
                        {2, false, true, k_condense_tmap<8, 2, 2, false, 256>, 384},
@@ -2141,8 +2146,8 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
   const Var* var = nullptr;
   for (const Var& v : vars)
     if ((cps_env == 0 || cps_env == v.cps + (v.db ? 10 : 0)) && (pipe_env != 0 || !v.pipe) &&
-        (!v.pipe || (v.threads - 128 == gh_env && npk_max <= 2 * (v.threads - 128) &&
-                     36 * std::max(v.threads - 128, npk_max) <= 2 * SC * 6 * ld)) &&
+        (!v.pipe || (v.gr == gr_want && v.threads - v.gr == gh_env && npk_max <= 2 * (v.threads - v.gr) &&
+                     36 * std::max(v.threads - v.gr, npk_max) <= 2 * SC * 6 * ld)) &&
         tma_smem(SC, v.cps, v.db, ctx->cu_umax, ld, dslot, n0, per, v.pipe, !v.pipe) <= budget) {
       var = &v;
       break;
