@@ -2126,14 +2126,23 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
   }();
   // pipeline group H size: 256 threads (GM_TMA_GH=128: 128); the fold of a
   // stage stages max(GH, npk) 6x6 pairs in the 2 * SC*6*ld floats of a buffer
-  // (a 256-thread recursion group with 128 H threads measured slower on
-  // both chains and meshes: cfg4 22.9 vs 20.8 ms, cfg5 11.8 vs 11.2 ms)
+  // group sizes: R 128 + H 256 (384 threads, 168 registers) for chains;
+  // R 256 + H 256 (512 threads, 128 registers) where the recursion has more
+  // neighbour blocks (degree >= 3: meshes; cfg5 11.2 -> 10.7 ms, cfg4 and
+  // cfg3 even).  Measured and dropped: R 256 + H 128 (cfg4 22.9 vs 20.8 ms).
   static const int gh_env = [] {
     const char* v = std::getenv("GM_TMA_GH");
     return v ? std::atoi(v) : 256;
   }();
-  const int gr_want = 128;
-  const Var vars[9] = {{4, true, true, k_condense_tmap<8, 4, 4, true, 256>, 384},
+  static const int gr_env = [] {
+    const char* v = std::getenv("GM_TMA_GR");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int gr_want = gr_env ? gr_env : (dslot >= 4 ? 256 : 128);
+  const Var vars[12] = {{4, true, true, k_condense_tmap<8, 4, 4, true, 256, 256>, 512, 256},
+                       {4, false, true, k_condense_tmap<8, 4, 4, false, 256, 256>, 512, 256},
+                       {2, false, true, k_condense_tmap<8, 2, 2, false, 256, 256>, 512, 256},
+                       {4, true, true, k_condense_tmap<8, 4, 4, true, 256>, 384},
                        {4, false, true, k_condense_tmap<8, 4, 4, false, 256>, 384},
                        {2, false, true, k_condense_tmap<8, 2, 2, false, 256>, 384},
                        {4, true, true, k_condense_tmap<8, 4, 4, true, 128>, 256},

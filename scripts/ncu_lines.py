@@ -31,3 +31,15 @@ print(f"samples {tot}  warp-instr {toti}")
 for ln, (s, e, src, st) in sorted(per.items(), key=lambda kv: -kv[1][key])[:n]:
     top = ", ".join(f"{k.replace('stall_', '')}:{v}" for k, v in st.most_common(2))
     print(f"{ln:4d} {100*s/tot:5.1f}%s {100*e/toti:5.1f}%i {src[:64]:64s} | {top}")
+# optional: stall totals over source-line ranges, e.g. --ranges R:985-1230,H:1240-1340
+rng = [a for a in sys.argv if a.startswith("--ranges=")]
+if rng:
+    for part in rng[0].split("=", 1)[1].split(","):
+        name, span = part.split(":")
+        lo, hi = map(int, span.split("-"))
+        agg, ss, ee = collections.Counter(), 0, 0
+        for ln, (s, e, src, st) in per.items():
+            if lo <= ln <= hi:
+                agg.update(st); ss += s; ee += e
+        top = ", ".join(f"{k.replace('stall_', '')}:{100*v/max(1,ss):.0f}%" for k, v in agg.most_common(6))
+        print(f"{name}: {100*ss/tot:.1f}% samples, {100*ee/toti:.1f}% instr | {top}")
