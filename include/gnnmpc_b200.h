@@ -278,6 +278,21 @@ int gm_mpc_finish(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const d
                   const double* u_prev, int has_prev, double* cur_states,
                   double* planned_states, double* planned_inputs, double* next_states,
                   double* next_inputs, double* u_applied, double* summary, void* stream);
+/* Same epilogue with the planned states formed by linear rollout instead of
+ * from Gamma: p_0 = x0, p_{n+1}(i) = A_self p_n(i) + sum_e A_e p_n(src e) +
+ * B_n(i) u_n + c_n(i), which equals Gamma_u u + Gamma_x (reference
+ * condensing.py:182-228, 409-416; tests/test_condensing.py:120-135) while
+ * reading the stage blocks (a_self / a_nbr / b as written by gm_linearize,
+ * c, x0 (B, M, nx)) instead of Gamma's rows; for large batches (cfg4, cfg5).
+ * nx = nu = 6, whole graph (no node range). */
+int gm_mpc_finish_rollout(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_nbr,
+                          const float* b, const double* c, const double* x0, const double* u,
+                          int ldu, const int32_t* status, const int32_t* iterations,
+                          const double* lin_states, const double* lin_inputs,
+                          const double* fb_states, const double* fb_inputs, double sqp_damping,
+                          int fallback, const double* u_prev, int has_prev, double* cur_states,
+                          double* planned_states, double* planned_inputs, double* next_states,
+                          double* next_inputs, double* u_applied, double* summary, void* stream);
 
 /* ---- node-partitioned recursion: halo pack / unpack (multi-GPU) ------- */
 /* Strided row gather / scatter for the per-stage halo exchange of the

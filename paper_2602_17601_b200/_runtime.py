@@ -90,6 +90,8 @@ _SIGNATURES = {
     "gm_reconstruct_states": (c_int, [c_void_p, c_int, c_int, P, c_int, P, c_int, P, c_void_p]),
     "gm_mpc_finish": (c_int, [c_void_p, c_int, c_int, P, c_int, P, c_int, P, P, P, P, P, P, c_double,
                               c_int, P, c_int, P, P, P, P, P, P, P, c_void_p]),
+    "gm_mpc_finish_rollout": (c_int, [c_void_p, c_int, c_int, P, P, P, P, P, P, c_int, P, P, P, P, P, P,
+                                      c_double, c_int, P, c_int, P, P, P, P, P, P, P, c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -191,14 +191,20 @@ class BatchedMpc:
                  warm, ctypes.byref(self.settings_c), self.u.data_ptr(), self.lam.data_ptr(),
                  self.status.data_ptr(), self.iters.data_ptr(), self.resid.data_ptr(), sp)
         mark(3)
-        ctx.call("gm_mpc_finish", B, N, self.W.data_ptr(), self.ld, self.u.data_ptr(), self.n,
-                 self.status.data_ptr(), self.iters.data_ptr(), self.X.data_ptr(),
-                 self.U.data_ptr(), self.X.data_ptr(), self.U.data_ptr(),
-                 float(self.cfg.sqp_damping),
-                 0 if self.cfg.fallback == "hold-previous-input" else 1, self.u_prev.data_ptr(),
-                 self.has_prev, None, self.planned_states.data_ptr(), self.planned_inputs.data_ptr(),
-                 self.next_states.data_ptr(), self.next_inputs.data_ptr(),
-                 self.u_applied.data_ptr(), self.summary.data_ptr(), sp)
+        tail = (self.status.data_ptr(), self.iters.data_ptr(), self.X.data_ptr(),
+                self.U.data_ptr(), self.X.data_ptr(), self.U.data_ptr(),
+                float(self.cfg.sqp_damping),
+                0 if self.cfg.fallback == "hold-previous-input" else 1, self.u_prev.data_ptr(),
+                self.has_prev, None, self.planned_states.data_ptr(), self.planned_inputs.data_ptr(),
+                self.next_states.data_ptr(), self.next_inputs.data_ptr(),
+                self.u_applied.data_ptr(), self.summary.data_ptr(), sp)
+        if _dev.use_rollout(B * M * (N + 1), nx, nu):  # K-RS by linear rollout (large waves)
+            ctx.call("gm_mpc_finish_rollout", B, N, self.a_self.data_ptr(),
+                     self.a_nbr.data_ptr() if E else None, self.b.data_ptr(), self.c.data_ptr(),
+                     self.x0.data_ptr(), self.u.data_ptr(), self.n, *tail)
+        else:
+            ctx.call("gm_mpc_finish", B, N, self.W.data_ptr(), self.ld, self.u.data_ptr(), self.n,
+                     *tail)
         mark(4)
 
     def step(self, x_measured, lin_states, lin_inputs, x_ref, last_applied=None) -> BatchResult:

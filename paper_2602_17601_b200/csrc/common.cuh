@@ -89,6 +89,7 @@ struct gm_ctx {
   // zero between launches) and the CTA dependency lists of the node partition
   int* d_flags = nullptr;
   int64_t flag_cap = 0;
+  unsigned* d_gbar = nullptr;  // grid barrier of the rollout epilogue (count, generation)
   int64_t dep_per = -1;
   int* d_dep_ptr = nullptr;
   int* d_dep = nullptr;

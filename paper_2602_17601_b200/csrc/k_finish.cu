@@ -247,6 +247,112 @@ __global__ void __launch_bounds__(256, 3) k_finish_states_pipe(const FinishArgs 
   }
 }
 
+// K-RS by linear rollout (large batches).  The planned trajectory of
+// reconstruct_states, x = Gamma_u u + Gamma_x (condensing.py:409-416), is the
+// Gamma recursion (condensing.py:182-228) applied to u:
+//     p_0 = x0,  p_{n+1}(i) = A_self p_n(i) + sum_{e in in(i)} A_e p_n(src e)
+//                             + B_n(i) u_n + c_n(i)
+// (reference tests/test_condensing.py:120-135 checks exactly this identity),
+// so it needs the stage blocks (36 (deg + 2) fp32 + 6 fp64 per node-stage)
+// instead of Gamma's 6 x ld fp32 rows.  One thread per (instance, node, row);
+// p ping-pongs through global scratch (L2-resident), stages separated by a
+// grid barrier (cooperative launch: co-residency guaranteed); the epilogue of
+// k_finish_states is applied to every p_k as it is formed.
+struct RolloutArgs {
+  const float* a_self;
+  const float* a_nbr;
+  const float* b;
+  const double* c;
+  const double* x0;
+  const int* ptr;
+  const int* src;
+  double* p0;
+  double* p1;
+  unsigned* bar;  // [count, generation]
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// grid-wide barrier: self-resetting count, monotone generation
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      atomicExch(&bar[0], 0u);
+      st_release_u32(&bar[1], gen + 1);
+    } else {
+      while (ld_acquire_u32(&bar[1]) == gen) __nanosleep(64);
+    }
+  }
+  ++gen;
+  __syncthreads();
+}
+
+template <int NX, int NU>
+__global__ void __launch_bounds__(256) k_rollout(const FinishArgs A, const RolloutArgs R, int B) {
+  const int M = A.M, N = A.N;
+  const int64_t rows = (int64_t)B * M * NX;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  __shared__ unsigned gen_s;
+  if (threadIdx.x == 0) gen_s = ld_acquire_u32(&R.bar[1]);
+  __syncthreads();
+  unsigned gen = gen_s;
+  auto finish = [&](int64_t bi, int i, int a, int k, double p) {
+    const bool ok = solved(A.status[bi]);
+    const int64_t t = ((bi * (N + 1) + k) * M + i) * NX + a;
+    const double x = ok ? (1.0 - A.damp) * A.lin_states[t] + A.damp * p : A.fb_states[t];
+    if (A.cur_states) A.cur_states[t] = x;
+    A.planned_states[((bi * M + i) * (N + 1) + k) * NX + a] = x;
+    const int64_t base = bi * (int64_t)(N + 1) * M * NX;
+    if (k >= 1) A.next_states[base + ((int64_t)(k - 1) * M + i) * NX + a] = x;
+    if (k == N) A.next_states[base + ((int64_t)N * M + i) * NX + a] = x;
+  };
+  for (int64_t r = t0; r < rows; r += nt) {  // stage 0: p_0 = x0
+    const double v = R.x0[r];
+    R.p0[r] = v;
+    const int64_t gi = r / NX;
+    finish(gi / M, (int)(gi % M), (int)(r % NX), 0, v);
+  }
+  for (int n = 0; n < N; ++n) {
+    grid_barrier(R.bar, gen);
+    const double* pin = (n & 1) ? R.p1 : R.p0;
+    double* pout = (n & 1) ? R.p0 : R.p1;
+    for (int64_t r = t0; r < rows; r += nt) {
+      const int a = (int)(r % NX);
+      const int64_t gi = r / NX, bi = gi / M;
+      const int i = (int)(gi - bi * M);
+      const int64_t ps = (bi * N + n) * (int64_t)M + i;  // (instance, stage, node) block index
+      const float* as = R.a_self + ps * NX * NX + a * NX;
+      const double* pi = pin + gi * NX;
+      double acc = R.c[ps * NX + a];
+#pragma unroll
+      for (int q = 0; q < NX; ++q) acc = fma((double)as[q], pi[q], acc);
+      const int e0 = R.ptr[i], e1 = R.ptr[i + 1];
+      const int64_t eb = (bi * N + n) * (int64_t)R.ptr[M];
+      for (int e = e0; e < e1; ++e) {
+        const float* an = R.a_nbr + (eb + e) * NX * NX + a * NX;
+        const double* pj = pin + (bi * M + R.src[e]) * NX;
+#pragma unroll
+        for (int q = 0; q < NX; ++q) acc = fma((double)an[q], pj[q], acc);
+      }
+      const float* bb = R.b + ps * NX * NU + a * NU;
+      const double* un = A.u + bi * A.ldu + n * NU;
+#pragma unroll
+      for (int j = 0; j < NU; ++j) acc = fma((double)bb[j], un[j], acc);
+      pout[r] = acc;
+      finish(bi, i, a, n + 1, acc);
+    }
+  }
+}
+
 __global__ void k_finish_inputs(const FinishArgs A, int B) {
   const int N = A.N, nu = A.nu;
   const int64_t total = (int64_t)B * N * nu;
@@ -356,6 +462,87 @@ int gm_mpc_finish(gm_ctx* ctx, int B, int N, const float* gamma, int ld, const d
   else
     k_finish_states<<<blocks, 256, 0, st>>>(a, items);
   GM_LAUNCH_CHECK(ctx, "k_finish_states");
+  const int64_t ti = (int64_t)B * N * ctx->n_u;
+  k_finish_inputs<<<(int)std::max<int64_t>(1, std::min<int64_t>((ti + 255) / 256, 1024)), 256, 0, st>>>(a, B);
+  GM_LAUNCH_CHECK(ctx, "k_finish_inputs");
+  return GM_OK;
+}
+
+int gm_mpc_finish_rollout(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_nbr, const float* b,
+                          const double* c, const double* x0, const double* u, int ldu, const int32_t* status,
+                          const int32_t* iterations, const double* lin_states, const double* lin_inputs,
+                          const double* fb_states, const double* fb_inputs, double sqp_damping, int fallback,
+                          const double* u_prev, int has_prev, double* cur_states, double* planned_states,
+                          double* planned_inputs, double* next_states, double* next_inputs, double* u_applied,
+                          double* summary, void* stream) {
+  int rc = gm_need_device(ctx);
+  if (rc) return rc;
+  if (ctx->M < 1 || ctx->nx < 1) return gm_fail(ctx, GM_ERR_CONFIG, "graph/dimensions not set");
+  if (ctx->nx != 6 || ctx->n_u != 6) return gm_fail(ctx, GM_ERR_CONFIG, "rollout epilogue: nx = nu = 6 only");
+  if (ctx->node_hi >= 0 && (ctx->node_lo != 0 || ctx->node_hi != ctx->M))
+    return gm_fail(ctx, GM_ERR_CONFIG, "rollout epilogue needs the whole graph (no node range)");
+  if (!a_self || !b || !c || !x0 || (ctx->E > 0 && !a_nbr)) return gm_fail(ctx, GM_ERR_CONFIG, "missing stage blocks");
+  if (B == 0) return GM_OK;
+  FinishArgs a{};
+  a.M = (int)ctx->M;
+  a.N = N;
+  a.nx = ctx->nx;
+  a.nu = ctx->n_u;
+  a.ld = 0;
+  a.ldu = ldu;
+  a.fallback = fallback;
+  a.has_prev = has_prev;
+  a.damp = sqp_damping;
+  a.W = nullptr;
+  a.u = u;
+  a.status = status;
+  a.iters = iterations;
+  a.lin_states = lin_states;
+  a.lin_inputs = lin_inputs;
+  a.fb_states = fb_states ? fb_states : lin_states;
+  a.fb_inputs = fb_inputs ? fb_inputs : lin_inputs;
+  a.u_prev = u_prev;
+  a.cur_states = cur_states;
+  a.planned_states = planned_states;
+  a.planned_inputs = planned_inputs;
+  a.next_states = next_states;
+  a.next_inputs = next_inputs;
+  a.u_applied = u_applied;
+  a.summary = summary;
+  const int64_t rows = (int64_t)B * ctx->M * 6;
+  if (!ctx->d_gbar) {
+    GM_CUDA(ctx, cudaMalloc(&ctx->d_gbar, 2 * sizeof(unsigned)));
+    GM_CUDA(ctx, cudaMemset(ctx->d_gbar, 0, 2 * sizeof(unsigned)));
+  }
+  double* pp = (double*)gm_scratch(ctx, 2 * sizeof(double) * (size_t)rows);
+  if (!pp) return gm_fail(ctx, GM_ERR_CUDA, "scratch allocation failed");
+  RolloutArgs r{};
+  r.a_self = a_self;
+  r.a_nbr = a_nbr;
+  r.b = b;
+  r.c = c;
+  r.x0 = x0;
+  r.ptr = ctx->d_ptr;
+  r.src = ctx->d_src;
+  r.p0 = pp;
+  r.p1 = pp + rows;
+  r.bar = ctx->d_gbar;
+  int occ = 0;
+  GM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rollout<6, 6>, 256, 0));
+  if (occ < 1) return gm_fail(ctx, GM_ERR_CUDA, "k_rollout does not fit an SM");
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, (int64_t)ctx->sm_count * occ));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)grid);
+  lc.blockDim = dim3(256);
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;  // stage barriers need every CTA resident
+  GM_CUDA(ctx, cudaLaunchKernelEx(&lc, k_rollout<6, 6>, a, r, B));
+  GM_LAUNCH_CHECK(ctx, "k_rollout");
   const int64_t ti = (int64_t)B * N * ctx->n_u;
   k_finish_inputs<<<(int)std::max<int64_t>(1, std::min<int64_t>((ti + 255) / 256, 1024)), 256, 0, st>>>(a, B);
   GM_LAUNCH_CHECK(ctx, "k_finish_inputs");

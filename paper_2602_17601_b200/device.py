@@ -142,6 +142,23 @@ class Engine:
         return self.torch.cuda.current_stream(self.device).cuda_stream
 
 
+_ROLLOUT_MIN = 1 << 20  # node-stages per launch from which K-RS rolls out instead of reading Gamma
+
+
+def use_rollout(node_stages: int, nx: int, nu: int) -> bool:
+    """K-RS by linear rollout (gm_mpc_finish_rollout) instead of Gamma rows
+    (gm_mpc_finish): for large batches the stage blocks are ~5x fewer bytes
+    than Gamma's rows (cfg4, cfg5).  GM_FIN_ROLLOUT=0/1 forces either."""
+    import os
+
+    env = os.environ.get("GM_FIN_ROLLOUT")
+    if nx != 6 or nu != 6:
+        return False
+    if env is not None:
+        return env == "1"
+    return node_stages >= _ROLLOUT_MIN
+
+
 def device_index(device=None) -> int:
     """CUDA device ordinal of ``device`` (None: the current device)."""
     torch = require_cuda()

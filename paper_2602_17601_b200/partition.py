@@ -46,6 +46,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .batch import shard_range
+from . import device as _dev
 from .device import topology_csr
 from .errors import ConfigurationError
 
@@ -490,14 +491,20 @@ class PartitionedMpc:
         mark(3)
         # every local node's Gamma rows are valid (halo rows exchanged), so the
         # plan and its shift are formed for owned + halo nodes here
-        ctx.call("gm_mpc_finish", 1, N, self.W.data_ptr(), self.ld, self.u.data_ptr(), self.n,
-                 self.status.data_ptr(), self.iters.data_ptr(), self.ls.data_ptr(),
-                 self.li.data_ptr(), self.ls.data_ptr(), self.li.data_ptr(),
-                 float(self.cfg.sqp_damping),
-                 0 if self.cfg.fallback == "hold-previous-input" else 1, self.u_prev.data_ptr(),
-                 self.has_prev, None, self.planned_states.data_ptr(),
-                 self.planned_inputs.data_ptr(), self.next_states.data_ptr(),
-                 self.next_inputs.data_ptr(), self.u_applied.data_ptr(), self.summary.data_ptr(), sp)
+        tail = (self.status.data_ptr(), self.iters.data_ptr(), self.ls.data_ptr(),
+                self.li.data_ptr(), self.ls.data_ptr(), self.li.data_ptr(),
+                float(self.cfg.sqp_damping),
+                0 if self.cfg.fallback == "hold-previous-input" else 1, self.u_prev.data_ptr(),
+                self.has_prev, None, self.planned_states.data_ptr(),
+                self.planned_inputs.data_ptr(), self.next_states.data_ptr(),
+                self.next_inputs.data_ptr(), self.u_applied.data_ptr(), self.summary.data_ptr(), sp)
+        if self.part.world == 1 and _dev.use_rollout(self.ML * (N + 1), self.nx, nu):
+            # one rank owns the whole graph: K-RS by linear rollout
+            ctx.call("gm_mpc_finish_rollout", 1, N, self.a_self.data_ptr(), a_nbr, self.b.data_ptr(),
+                     self.c.data_ptr(), self.x0.data_ptr(), self.u.data_ptr(), self.n, *tail)
+        else:
+            ctx.call("gm_mpc_finish", 1, N, self.W.data_ptr(), self.ld, self.u.data_ptr(), self.n,
+                     *tail)
         mark(4)
 
     def _stage(self, n):

@@ -115,3 +115,69 @@ def test_partitioned_step_world1_matches_single_device():
         assert np.max(np.abs(pm.next_states.cpu().numpy() - st1.lin_states)) <= 1e-9
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["chain", "mesh"])
+def test_rollout_epilogue_equals_gamma_epilogue(kind, monkeypatch):
+    """K-RS by linear rollout (gm_mpc_finish_rollout, the large-batch path)
+    against the Gamma-row K-RS (gm_mpc_finish) on the same solved QPs, and
+    both against the oracle (reconstruct_states = rollout:
+    reference tests/test_condensing.py:120-135).  fp32 blocks either way:
+    trajectories within 1e-5 of each other, 1e-4 of the oracle."""
+    import paper_2602_17601_b200 as pkg
+    from oracle import ref_port as O
+    from paper_2602_17601_b200 import workloads
+    from paper_2602_17601_b200.batch import BatchedMpc
+
+    N, B = 8, 3
+    if kind == "chain":
+        M = 12
+        topo, model, _, _, spec = workloads.scaling_problem(M, N, 0.01, 0)
+        inst = [workloads.batch_instance(b, M, N) for b in range(B)]
+    else:
+        topo, model, states, inputs, spec = workloads.mesh_problem(6, 5, N, 0.01, 0)
+        M = topo.node_count
+        rng = np.random.default_rng(5)
+        inst = [(states + 0.01 * rng.standard_normal(states.shape), inputs) for _ in range(B)]
+    cfg = pkg.MpcConfig(horizon=N, dt=0.01)
+    xs = np.stack([st[0] for st, _ in inst])
+    ls = np.stack([np.concatenate([st, st[-1:]], axis=0) for st, _ in inst])
+    li = np.stack([inp for _, inp in inst])
+    xr = np.stack([np.repeat(st[0][:, None, :], N + 1, axis=1) for st, _ in inst])
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("GM_FIN_ROLLOUT", mode)
+        bm = BatchedMpc(model, topo, spec, cfg, B)
+        res = bm.step(xs, ls, li, xr)
+        out[mode] = (res, res.next_states.cpu().numpy(), bm.planned_states.cpu().numpy())
+    (r0, n0, p0), (r1, n1, p1) = out["0"], out["1"]
+    assert np.array_equal(r0.u_applied, r1.u_applied)
+    assert [s.value for s in r0.status] == [s.value for s in r1.status]
+    scale = np.max(np.abs(n0))
+    assert np.max(np.abs(n1 - n0)) / scale <= 1e-5
+    assert np.max(np.abs(p1 - p0)) / scale <= 1e-5
+    for b in range(B):
+        spec_b = pkg.OcpSpec(topo, N, spec.q, xr[b], spec.r, spec.u_ref, spec.input_constraints,
+                             spec.state_constraints)
+        ref = O.mpc_step(model, topo, spec_b, xs[b], ls[b], li[b], N)
+        assert r1.status[b].value == ref["status"]
+        assert np.max(np.abs(n1[b] - ref["lin_states"])) / np.max(np.abs(ref["lin_states"])) <= 1e-4
+
+
+def test_rollout_epilogue_rejects_node_range_and_dims():
+    """The rollout entry point fails loudly outside its domain."""
+    import paper_2602_17601_b200 as pkg
+    from paper_2602_17601_b200 import _runtime, workloads
+    from paper_2602_17601_b200.device import engine
+
+    topo, model, _, _, _ = workloads.scaling_problem(12, 4, 0.01, 0)
+    eng = engine(topo, model)
+    ctx = eng.ctx
+    ctx.call("gm_set_node_range", 2, 8)
+    try:
+        with pytest.raises(Exception):
+            ctx.call("gm_mpc_finish_rollout", 1, 4, None, None, None, None, None, None, 24,
+                     None, None, None, None, None, None, 1.0, 0, None, 0, None, None, None,
+                     None, None, None, None, None)
+    finally:
+        ctx.call("gm_set_node_range", 0, 12)
