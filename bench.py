@@ -367,6 +367,29 @@ def hg_flops(M, N, nx=6, nu=6, B=1):
     return B * M * sum(2 * nx * nx * k * nu + 2 * nx * (k * nu) ** 2 for k in range(1, N + 1))
 
 
+FP32_FMA_PER_SM_CLK = 128  # SIMT fp32 FMA lanes per SM per clock (4 SMSPs x 32)
+
+
+def cond_flops(M, E, N, nx=6, nu=6, B=1):
+    """Algorithmic fp32 flops of K-COND: the recursion over the live columns
+    (A blocks of node + in-edges times stage-n Gamma: 6n causal + the Gamma_x
+    column), Qs Gamma on the causal columns, and H's lower block triangle
+    (k(k+1)/2 6x6 pairs over the 6 rows of every node-stage)."""
+    rec = sum(2 * nx * nx * (M + E) * (n * nu + 1) for n in range(N))
+    qg = M * sum(2 * nx * nx * k * nu for k in range(1, N + 1))
+    h = M * sum(2 * nx * nu * nu * k * (k + 1) // 2 for k in range(1, N + 1))
+    return B * (rec + qg + h)
+
+
+def simt_roof(flops, ms, sm_mhz):
+    """K-COND against the SIMT fp32 FMA rate (its arithmetic runs on the FMA
+    pipe, not the tensor cores: see DESIGN 2 on TMEM accumulation)."""
+    peak = 148 * FP32_FMA_PER_SM_CLK * 2 * sm_mhz * 1e6 / 1e12
+    ach = flops / (ms * 1e-3) / 1e12
+    return {"bound": "fp32 FMA (SIMT)", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+            "frac": ach / peak, "algorithmic_flops": flops}
+
+
 def events(n):
     import torch
 
@@ -471,6 +494,7 @@ def cfg3_leg(args, world, rank, local, dev):
             "unit": "GB/s", "frac": cb / (cond * 1e-3) / 1e9 / pk["hbm_gbs"],
             "algorithmic_bytes": cb, "traffic": NCU_TRAFFIC["cfg3"]["k_condense_fused"],
             "h_flops": hfl, "h_tflops": hfl / (cond * 1e-3) / 1e12,
+            "compute": simt_roof(cond_flops(M, int(topo.edge_count), N), cond, pk["sm_mhz"]),
             "note": "stage time incl. constraint rows / soft expansion; Gamma is L2-resident at cfg3; "
                     "H and g accumulate in fp32 FMA inside the recursion kernel (round-to-nearest; "
                     "the tcgen05 variant is opt-in, its accumulator truncates)"},
@@ -619,6 +643,8 @@ def cfg4_leg(args, world, rank, local, dev, steps=None, warmup=None):
                      "achieved": cb / (cond * 1e-3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": cb / (cond * 1e-3) / 1e9 / pk["hbm_gbs"], "algorithmic_bytes": cb,
                      "traffic": NCU_TRAFFIC["cfg4"]["k_condense_fused"],
+                     "compute": simt_roof(cond_flops(M, int(topo.edge_count), N, B=wave), cond,
+                                          pk["sm_mhz"]),
                      "note": f"per wave of {wave} instances; peak {pk['hbm_note']}"},
         "clocks": clk, "cpu_baseline": cpu,
     }
@@ -722,6 +748,7 @@ def cfg5_leg(args, world, rank, local, dev, steps=None, warmup=None):
                      "achieved": cb / (cond * 1e-3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": cb / (cond * 1e-3) / 1e9 / pk["hbm_gbs"], "algorithmic_bytes": cb,
                      "traffic": NCU_TRAFFIC["cfg5"]["k_condense_fused"],
+                     "compute": simt_roof(cond_flops(M, E, N) / world, cond, pk["sm_mhz"]),
                      "note": f"rank 0's share of the compulsory Gamma + block bytes; peak {pk['hbm_note']}"},
         "clocks": clk, "cpu_baseline": cpu,
     }
