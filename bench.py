@@ -49,13 +49,14 @@ METRIC = "MPC step latency ms (linearize+condense+QP) & Hz at N nodes; solves/se
 # dram__bytes_read.sum + dram__bytes_write.sum per launch, from this round's
 # `ncu --set full` captures (profiles/r02/ncu_*); None where not captured
 NCU_TRAFFIC = {
-    # cfg3: profiles/r02/ncu_kernels_cfg3.txt (linearize = the 6 K-LIN
-    # launches of one step; k_solve_qp: the round-1 capture, kernel unchanged)
-    "cfg3": {"k_solve_qp": 757760, "linearize": 42511616, "k_condense_fused": 35475200},
-    # cfg4: one 1024-instance wave of k_condense_tma (profiles/r02/ncu_kernels_cond.txt)
-    "cfg4": {"k_condense_fused": 25940555000},
-    # cfg5: k_condense_fused (the mesh keeps the per-thread-load kernel)
-    "cfg5": {"k_condense_fused": 23642548000},
+    # cfg3: profiles/r02/ncu_final_kernels.txt (linearize = the 6 K-LIN
+    # launches of one step; k_solve_qp: the round-1 capture, kernel unchanged;
+    # K-COND = k_condense_tmap, the warp-specialised TMA pipeline)
+    "cfg3": {"k_solve_qp": 757760, "linearize": 42511616, "k_condense": 30858752},
+    # cfg4: one 1024-instance wave of k_condense_tmap (384 threads)
+    "cfg4": {"k_condense": 28780015000},
+    # cfg5: k_condense_tmap (512 threads, H accumulator in the global partial)
+    "cfg5": {"k_condense": 27825092000},
 }
 M_NODES, HORIZON = 1000, 20
 WORKLOAD = "cfg3: chain graph M=1000 nodes, horizon N=20, _scaling_problem recipe (paper 100 Hz headline)"
@@ -489,10 +490,10 @@ def cfg3_leg(args, world, rank, local, dev):
     hfl = hg_flops(M, N)
     lin = float(np.mean(lin_ms))
     stages = {
-        "k_condense_fused": {
+        "k_condense_tmap": {
             "bound": "hbm", "achieved": cb / (cond * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
             "unit": "GB/s", "frac": cb / (cond * 1e-3) / 1e9 / pk["hbm_gbs"],
-            "algorithmic_bytes": cb, "traffic": NCU_TRAFFIC["cfg3"]["k_condense_fused"],
+            "algorithmic_bytes": cb, "traffic": NCU_TRAFFIC["cfg3"]["k_condense"],
             "h_flops": hfl, "h_tflops": hfl / (cond * 1e-3) / 1e12,
             "compute": simt_roof(cond_flops(M, int(topo.edge_count), N), cond, pk["sm_mhz"]),
             "note": "stage time incl. constraint rows / soft expansion; Gamma is L2-resident at cfg3; "
@@ -639,10 +640,10 @@ def cfg4_leg(args, world, rank, local, dev, steps=None, warmup=None):
                 "path": "batch.WavePipeline.step from pinned host arrays (H2D overlapped with the "
                         "previous wave's kernels; wall clock)"},
         "gpu_launches": launches,
-        "roofline": {"kernel": "k_condense_fused (K-COND) + rows/soft", "bound": "hbm",
+        "roofline": {"kernel": "k_condense_tmap (K-COND) + rows/soft", "bound": "hbm",
                      "achieved": cb / (cond * 1e-3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": cb / (cond * 1e-3) / 1e9 / pk["hbm_gbs"], "algorithmic_bytes": cb,
-                     "traffic": NCU_TRAFFIC["cfg4"]["k_condense_fused"],
+                     "traffic": NCU_TRAFFIC["cfg4"]["k_condense"],
                      "compute": simt_roof(cond_flops(M, int(topo.edge_count), N, B=wave), cond,
                                           pk["sm_mhz"]),
                      "note": f"per wave of {wave} instances; peak {pk['hbm_note']}"},
@@ -743,11 +744,11 @@ def cfg5_leg(args, world, rank, local, dev, steps=None, warmup=None):
                 "path": "PartitionedMpc.step: measurement H2D from pinned host memory, trajectory "
                         "device-resident between steps (like MpcState), D2H of u/status"},
         "gpu_launches": launches,
-        "roofline": {"kernel": "condensing (K-COND fused at 1 GPU; K-REC stages + K-HG when "
+        "roofline": {"kernel": "condensing (K-COND k_condense_tmap at 1 GPU; K-REC stages + K-HG when "
                                "partitioned)", "bound": "hbm",
                      "achieved": cb / (cond * 1e-3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": cb / (cond * 1e-3) / 1e9 / pk["hbm_gbs"], "algorithmic_bytes": cb,
-                     "traffic": NCU_TRAFFIC["cfg5"]["k_condense_fused"],
+                     "traffic": NCU_TRAFFIC["cfg5"]["k_condense"],
                      "compute": simt_roof(cond_flops(M, E, N) / world, cond, pk["sm_mhz"]),
                      "note": f"rank 0's share of the compulsory Gamma + block bytes; peak {pk['hbm_note']}"},
         "clocks": clk, "cpu_baseline": cpu,

@@ -867,13 +867,21 @@ __device__ __forceinline__ void qpb_arrive(int id, int n) {
 // waiting for buffer EMPTY, [2] R waiting on neighbour stage flags, [3] R
 // waiting for its TMA tiles, [4] group H waiting for FULL, [5] H busy, [6] H
 // stage fold, [7] items; [8..11] R: blocks-in barrier + issue, Qs, recursion
-// passes, flag + w; [12..15] H: Qs*G + barrier, H rows, g, rest.
-// gm_cond_profile(1) enables + zeroes.
+// passes, flag + w; [12..15] H: Qs*G + barrier, H rows, g, rest;
+// [16..21] finer R / H splits (scripts/cond_stages.py).  Compiled in only
+// with -DGM_COND_PROF (make NVFLAGS+=-DGM_COND_PROF); gm_cond_profile(1)
+// enables + zeroes.  (Caveat: clock reads may be scheduled across a
+// bar.sync, so a barrier wait can show up in the following segment.)
 __device__ unsigned long long g_cond_prof[32 * 24];
 __device__ int g_cond_prof_on;
-__device__ __forceinline__ long long cprof_clock(bool on) { return on ? clock64() : 0; }
+#ifdef GM_COND_PROF
+constexpr bool kCondProf = true;
+#else
+constexpr bool kCondProf = false;
+#endif
+__device__ __forceinline__ long long cprof_clock(bool on) { return (kCondProf && on) ? clock64() : 0; }
 __device__ __forceinline__ void cprof_add(bool on, int k, int slot, long long v) {
-  if (on && k < 32) atomicAdd(&g_cond_prof[k * 24 + slot], (unsigned long long)v);
+  if (kCondProf && on && k < 32) atomicAdd(&g_cond_prof[k * 24 + slot], (unsigned long long)v);
 }
 
 template <int SC, int CPS, int GW, bool DB, int GH, int GR = 128>
@@ -975,7 +983,7 @@ __global__ void __launch_bounds__(GR + GH, 1) k_condense_tmap(const FusedArgs a,
   if (grpR) {
     // ===================== group R: tiles, recursion, part of QG =====================
     const int lane = tid & 31;
-    const bool pf = g_cond_prof_on && blockIdx.x == 0 && gt == 0;
+    const bool pf = kCondProf && g_cond_prof_on && blockIdx.x == 0 && gt == 0;
     auto prefetch = [&](int j) {
       const int n = j / nsub, s0 = nb + (j % nsub) * SC;
       const int sc = min(SC, ne - s0), k = n + 1;
@@ -1262,7 +1270,7 @@ __global__ void __launch_bounds__(GR + GH, 1) k_condense_tmap(const FusedArgs a,
           pair_of(min(gt + GH, npk - 1), bp1, bq1);
         }
       }
-      const bool pf = g_cond_prof_on && blockIdx.x == 0 && gt == 0;
+      const bool pf = kCondProf && g_cond_prof_on && blockIdx.x == 0 && gt == 0;
       const long long ph0 = cprof_clock(pf);
       qpb_sync(BAR_FULL + b, NT);  // item j from group R
       const long long ph1 = cprof_clock(pf);
@@ -2591,6 +2599,7 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
 }  // extern "C"
 
 extern "C" int gm_cond_profile(int on) {
+  if (!kCondProf) return GM_ERR_CONFIG;  // built without -DGM_COND_PROF
   on = on != 0 ? 1 : 0;
   cudaMemcpyToSymbol(g_cond_prof_on, &on, sizeof(int));
   static const unsigned long long z[32 * 24] = {0};

@@ -1,5 +1,7 @@
 """Per-stage cycle accounting of the pipelined K-COND (CTA 0) on one cfg4
-wave (diagnostics): python scripts/cond_stages.py [B]"""
+wave or the cfg5 mesh (diagnostics): python scripts/cond_stages.py [B|mesh].
+Needs the library built with the counters compiled in:
+    make -C paper_2602_17601_b200/csrc clean && make -C paper_2602_17601_b200/csrc EXTRA=-DGM_COND_PROF"""
 import sys
 from pathlib import Path
 
@@ -38,7 +40,8 @@ for _ in range(2):
     run()
 torch.cuda.synchronize()
 L = _runtime.lib()
-L.gm_cond_profile(1)
+if L.gm_cond_profile(1) != 0:
+    sys.exit("library built without -DGM_COND_PROF (see the docstring)")
 run()
 torch.cuda.synchronize()
 out = np.zeros(768, dtype=np.uint64)
