@@ -244,6 +244,11 @@ int gm_qp_phase_cycles(unsigned long long* out);
  * zeroes; gm_cond_phase_cycles copies 256 counters (synchronous). */
 int gm_cond_profile(int on);
 int gm_cond_phase_cycles(unsigned long long* out);
+/* Diagnostics: the K-COND variant of the context's last gm_condense_fused
+ * call: 0 none, 1 SIMT k_condense_fused, 2 tcgen05 k_condense_tc, 3
+ * k_condense_tma, 4 / 5 k_condense_tmap with 384 / 512 threads, 6 the
+ * two-kernel path. */
+int gm_last_condense_kernel(gm_ctx* ctx);
 /* Diagnostics: factor a dense SPD matrix A (n x n, row-major, device) with
  * K-QP's own Cholesky and solve A x = b; L (n x n) lower, ok = 0 when a pivot
  * failed.  Used by the tests to check the factorisation in isolation. */

@@ -82,6 +82,7 @@ _SIGNATURES = {
     "gm_qp_phase_cycles": (c_int, [P]),
     "gm_cond_profile": (c_int, [c_int]),
     "gm_cond_phase_cycles": (c_int, [P]),
+    "gm_last_condense_kernel": (c_int, [c_void_p]),
     "gm_chol_check": (c_int, [c_void_p, c_int, P, P, P, P, P, c_void_p]),
     "gm_set_condense_mode": (c_int, [c_void_p, c_int]),
     "gm_gram_check": (c_int, [c_void_p, c_int, c_int, P, P, P, c_void_p]),

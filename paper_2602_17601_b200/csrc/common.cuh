@@ -69,6 +69,10 @@ struct gm_ctx {
   int64_t node_lo = 0, node_hi = -1;
   int lin_mode = 0;  // gm_set_linearize_mode
   int cond_mode = 0;  // gm_set_condense_mode
+  // K-COND variant of the last gm_condense_fused launch (gm_last_condense_kernel):
+  // 1 SIMT k_condense_fused, 2 tcgen05 k_condense_tc, 3 k_condense_tma,
+  // 4 k_condense_tmap 384 threads, 5 k_condense_tmap 512 threads, 6 two-kernel path
+  int last_cond_kernel = 0;
   // model
   bool has_model = false;
   int n_p = 0, n_m = 0;

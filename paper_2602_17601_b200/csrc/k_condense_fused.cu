@@ -2264,6 +2264,7 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
   lc.numAttrs = splits > 1 ? 1 : 0;  // stage waits across CTAs need co-residency
   GM_CUDA(ctx, cudaLaunchKernelEx(&lc, kfn, a, tm));
   GM_LAUNCH_CHECK(ctx, "k_condense_tma");
+  ctx->last_cond_kernel = !var->pipe ? 3 : (var->threads == 512 ? 5 : 4);
   return launch_pair_reduce(ctx, B, nu, n0, npairs, splits, groups, a.partH, a.partg,
                             (double*)(scr + up(pH) + up(pg)), (double*)(scr + up(pH) + up(pg) + up(tH)), r,
                             r_stride, u_ref, uref_stride, H, g, st);
@@ -2410,6 +2411,7 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
   if (ctx->nx < 1 || ctx->n_u < 1) return gm_fail(ctx, GM_ERR_CONFIG, "dimensions not set");
   if (B < 0 || N < 1) return gm_fail(ctx, GM_ERR_CONFIG, "need B >= 0 and horizon >= 1");
   if (ld < N * ctx->n_u + 1) return gm_fail(ctx, GM_ERR_CONFIG, "gamma leading dimension too small");
+  ctx->last_cond_kernel = 0;
   if (B == 0) return GM_OK;
   // default (mode 0): the TMA-staged kernel for the reference architecture
   // from 512 node rows (below, e.g. cfg2 at M = 100, the per-stage tile
@@ -2488,6 +2490,7 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
     // shapes outside the fused kernel's instantiations: the two-kernel path
     rc = gm_condense_gammas(ctx, B, N, a_self, a_nbr, b, c, x0, gamma, ld, stream);
     if (rc) return rc;
+    ctx->last_cond_kernel = 6;
     return gm_condense_cost(ctx, B, N, gamma, ld, q, q_stride, x_ref, xref_stride, r, r_stride,
                             u_ref, uref_stride, H, g, 0, stream);
   }
@@ -2572,6 +2575,7 @@ int gm_condense_fused(gm_ctx* ctx, int B, int N, const float* a_self, const floa
     kern<<<(unsigned)grid, (unsigned)threads, sm, st>>>(a);
   }
   GM_LAUNCH_CHECK(ctx, "k_condense_fused");
+  ctx->last_cond_kernel = tck != nullptr ? 2 : 1;
   PairReduceArgs ra{};
   ra.nu = nu;
   ra.n0 = n0;
@@ -2611,3 +2615,5 @@ extern "C" int gm_cond_phase_cycles(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_cond_prof, sizeof(unsigned long long) * 32 * 24) == cudaSuccess ? GM_OK
                                                                                                     : GM_ERR_CUDA;
 }
+
+extern "C" int gm_last_condense_kernel(gm_ctx* ctx) { return ctx ? ctx->last_cond_kernel : 0; }

@@ -68,6 +68,7 @@ def _run(topo, N, nx, nu, B, seed, reps=2, graph=False, mode=0):
     outs = []
     if graph:
         fused()
+        _run.last_kernel = lib().gm_last_condense_kernel(eng.ctx.handle)
         gr = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gr):
             fused()
@@ -81,6 +82,7 @@ def _run(topo, N, nx, nu, B, seed, reps=2, graph=False, mode=0):
             fused()
             torch.cuda.synchronize()
             outs.append((W2.clone(), H2.clone(), g2.clone()))
+        _run.last_kernel = lib().gm_last_condense_kernel(eng.ctx.handle)
     eng.ctx.call("gm_set_condense_mode", 0)
     return (W1, H1, g1), outs
 
@@ -142,6 +144,48 @@ def test_fused_matches_two_kernel_path(graph, N, nx, nu, B, mode):
         topo = GraphTopology(M, tuple(tuple(n) for n in nbrs), 8)
     ref, outs = _run(topo, N, nx, nu, B, seed=11, reps=3, mode=mode)
     _check(ref, outs, N * nu, nu, N, tol=2e-6 if mode in (0, 1) else 1e-5)
+
+
+@pytest.mark.parametrize("graph,N,B,variant", [
+    ("chain1000", 20, 2, 4),   # 384-thread pipeline, tile slots double-buffered by item
+    ("chain301", 16, 2, 4),    # M not a multiple of the 8-node item, ld = 128 with 98 live
+    ("chain600", 15, 1, 4),    # ld = 96
+    ("mesh", 16, 2, 5),        # 512-thread pipeline (degree 4), single tile slot, global H fold
+    ("local", 20, 2, 5),       # irregular degree <= 5 (neighbours within +-8), isolated nodes
+    ("random", 20, 1, 1),      # neighbours anywhere: the unique-neighbour tile ring
+                               # outgrows shared memory -> the per-thread-load kernel
+])
+def test_pipeline_kernel_shapes(graph, N, B, variant):
+    """The warp-specialised K-COND pipeline (k_condense_tmap; nx = nu = 6,
+    >= 512 node rows) across its variants against the SIMT two-kernel
+    reference: Gamma bitwise, H / g to fp32 round-off, bitwise repeatable."""
+    from paper_2602_17601_b200.graph import GraphTopology, chain_topology, mesh_topology
+
+    if graph.startswith("chain"):
+        topo = chain_topology(int(graph[5:]))
+    elif graph == "mesh":
+        topo = mesh_topology(23, 17)
+    else:
+        rng = np.random.default_rng(9)
+        M = 700
+        if graph == "local":
+            draw = lambda i: rng.integers(max(0, i - 8), min(M, i + 9), rng.integers(0, 6))
+        else:
+            draw = lambda i: rng.integers(0, M, rng.integers(0, 6))
+        nbrs = [sorted(set(int(j) for j in draw(i)) - {i}) for i in range(M)]
+        topo = GraphTopology(M, tuple(tuple(n) for n in nbrs), 8)
+    ref, outs = _run(topo, N, 6, 6, B, seed=13, reps=3, mode=0)
+    assert _run.last_kernel == variant  # gm_last_condense_kernel: the pipeline ran
+    _check(ref, outs, N * 6, 6, N, tol=2e-6)
+
+
+def test_pipeline_kernel_graph_replay():
+    """k_condense_tmap (cooperative launch) captured in a CUDA graph."""
+    from paper_2602_17601_b200.graph import chain_topology
+
+    ref, outs = _run(chain_topology(1000), 20, 6, 6, 1, seed=4, reps=3, graph=True, mode=0)
+    assert _run.last_kernel == 4
+    _check(ref, outs, 120, 6, 20, tol=2e-6)
 
 
 @pytest.mark.parametrize("mode", [3, 1, 0])
