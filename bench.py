@@ -84,6 +84,9 @@ def parse():
                          "sweep: chain M = 10^3 .. 10^4 device latency")
     ap.add_argument("--batch", type=int, default=4096, help="cfg4 total instances")
     ap.add_argument("--wave", type=int, default=1024, help="cfg4 instances per launch wave")
+    ap.add_argument("--cfg5-transport", choices=["torch", "native"], default="torch",
+                    help="cfg5 at N > 1: torch.distributed NCCL, or the native NCCL data plane "
+                         "(gm_sendrecv / gm_allreduce_sum) with the e2e step captured in one CUDA graph")
     return ap.parse_args()
 
 
@@ -675,7 +678,14 @@ def cfg5_leg(args, world, rank, local, dev, steps=None, warmup=None):
     spec.freeze()
     cfg = pkg.MpcConfig(horizon=N, dt=0.01)
     part = partition_nodes(topo, world, rank)
-    pm = PartitionedMpc(model, topo, spec, cfg, part)
+    native = args.cfg5_transport == "native" and world > 1
+    transport = None
+    if native:
+        from paper_2602_17601_b200.partition import NcclTransport
+
+        transport = NcclTransport(rank, world, dev)
+    pm = PartitionedMpc(model, topo, spec, cfg, part, transport=transport)
+    step_fn = pm.step_graph if native else pm.step
     loc = part.local_nodes if world > 1 else np.arange(topo.node_count)
     ls = torch.from_numpy(np.ascontiguousarray(np.concatenate([states, states[-1:]], 0)[:, loc])).to(dev)
     li = torch.from_numpy(inputs).to(dev)
@@ -695,9 +705,11 @@ def cfg5_leg(args, world, rank, local, dev, steps=None, warmup=None):
         ms.append(ev[0].elapsed_time(ev[4]))
         stage += [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
     stage /= steps
+    step_fn(xh, ls, li)  # (captures the step graph on the native path)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(steps):
-        u, st, it = pm.step(xh, ls, li)
+        u, st, it = step_fn(xh, ls, li)
     e2e_ms = (time.perf_counter() - t0) / steps * 1e3
     clk = clocks.stop()
     L = _runtime.lib()
@@ -736,6 +748,8 @@ def cfg5_leg(args, world, rank, local, dev, steps=None, warmup=None):
                                    "NCCL halo per stage + one all-reduce" if world > 1
                                    else "single GPU, fused persistent recursion + cost"),
                    "l2": "working set (Gamma 1.07 GB) larger than L2",
+                   "transport": (("native NCCL (gm_sendrecv / gm_allreduce_sum), e2e step as one CUDA "
+                                  "graph" if native else "torch.distributed NCCL") if world > 1 else None),
                    "qp": {"status": st, "iterations": it}},
         "stage_ms": {"linearize": float(stage[0]), "condense_incl_exchange": cond,
                      "qp": float(stage[2]), "epilogue": float(stage[3])},

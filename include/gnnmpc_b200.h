@@ -299,6 +299,27 @@ int gm_mpc_finish_rollout(gm_ctx* ctx, int B, int N, const float* a_self, const 
                           double* planned_states, double* planned_inputs, double* next_states,
                           double* next_inputs, double* u_applied, double* summary, void* stream);
 
+/* ---- native data plane of the partitioned step (multi-GPU) ------------- */
+/* SURVEY 8b gm_init_comm.  An NCCL communicator owned by the context
+ * (NCCL resolved at run time: libnccl.so.2, the copy torch loaded when
+ * present).  Everything is stream-ordered with no host synchronisation, so
+ * a rank's step (kernels + exchanges + all-reduce) can be captured in one
+ * CUDA graph.  The reference has no counterpart (single process; the
+ * node-chunk pool condensing.py:208-227 is what the partition generalises).
+ *   gm_comm_available   1 when libnccl.so.2 and its symbols resolved
+ *   gm_comm_unique_id   rank 0 creates the 128-byte id, the host broadcasts it
+ *   gm_init_comm        ncclCommInitRank on the context's device (collective)
+ *   gm_allreduce_sum    in-place fp64 sum over the ranks ([H | g | C | d])
+ *   gm_sendrecv         one grouped batch of byte sends / receives (halo rows) */
+int gm_comm_available(void);
+int gm_comm_unique_id(void* out128);
+int gm_init_comm(gm_ctx* ctx, const void* unique_id128, int rank, int world);
+int gm_comm_destroy(gm_ctx* ctx);
+int gm_allreduce_sum(gm_ctx* ctx, double* buf, int64_t count, void* stream);
+int gm_sendrecv(gm_ctx* ctx, int nsend, const int* send_peers, void* const* send_bufs,
+                const int64_t* send_bytes, int nrecv, const int* recv_peers, void* const* recv_bufs,
+                const int64_t* recv_bytes, void* stream);
+
 /* ---- node-partitioned recursion: halo pack / unpack (multi-GPU) ------- */
 /* Strided row gather / scatter for the per-stage halo exchange of the
  * node-partitioned Gamma recursion (the reference's node-chunk pool,

@@ -83,6 +83,12 @@ _SIGNATURES = {
     "gm_cond_profile": (c_int, [c_int]),
     "gm_cond_phase_cycles": (c_int, [P]),
     "gm_last_condense_kernel": (c_int, [c_void_p]),
+    "gm_comm_available": (c_int, []),
+    "gm_comm_unique_id": (c_int, [P]),
+    "gm_init_comm": (c_int, [c_void_p, P, c_int, c_int]),
+    "gm_comm_destroy": (c_int, [c_void_p]),
+    "gm_allreduce_sum": (c_int, [c_void_p, P, c_i64, c_void_p]),
+    "gm_sendrecv": (c_int, [c_void_p, c_int, P, P, P, c_int, P, P, P, c_void_p]),
     "gm_chol_check": (c_int, [c_void_p, c_int, P, P, P, P, P, c_void_p]),
     "gm_set_condense_mode": (c_int, [c_void_p, c_int]),
     "gm_gram_check": (c_int, [c_void_p, c_int, c_int, P, P, P, c_void_p]),

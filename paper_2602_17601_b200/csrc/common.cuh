@@ -94,6 +94,9 @@ struct gm_ctx {
   int* d_flags = nullptr;
   int64_t flag_cap = 0;
   unsigned* d_gbar = nullptr;  // grid barrier of the rollout epilogue (count, generation)
+  // native data plane (k_comm.cu): NCCL communicator of the partitioned step
+  void* nccl_comm = nullptr;
+  int comm_rank = 0, comm_world = 1;
   int64_t dep_per = -1;
   int* d_dep_ptr = nullptr;
   int* d_dep = nullptr;
@@ -111,6 +114,7 @@ int gm_fail(gm_ctx* ctx, int code, const std::string& msg);
 int gm_cuda_check(gm_ctx* ctx, cudaError_t e, const char* what);
 int gm_need_device(gm_ctx* ctx);
 void* gm_scratch(gm_ctx* ctx, size_t bytes);
+void gm_comm_release(gm_ctx* ctx);  // k_comm.cu: destroys the context's communicator
 
 #define GM_CUDA(ctx, expr)                                          \
   do {                                                              \

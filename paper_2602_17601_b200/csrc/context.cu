@@ -108,6 +108,7 @@ void gm_destroy(gm_ctx* ctx) {
     cudaFree(ctx->scratch);
     cudaFree(ctx->d_flags);
     cudaFree(ctx->d_gbar);
+    gm_comm_release(ctx);
     cudaFree(ctx->d_dep_ptr);
     cudaFree(ctx->d_dep);
     cudaFree(ctx->d_cu_ptr);

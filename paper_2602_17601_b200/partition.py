@@ -174,6 +174,97 @@ class DistTransport:
         self.dist.all_gather(outs, t, group=self.group)
 
 
+class NcclTransport:
+    """Native data plane (``gm_init_comm`` / ``gm_sendrecv`` /
+    ``gm_allreduce_sum``): an NCCL communicator in its own native context on
+    this rank's device, every operation enqueued on the caller's current
+    stream with no host synchronisation -- so a rank's whole step (kernels and
+    exchanges) can be captured in one CUDA graph, which ``DistTransport``'s
+    waits do not allow.  The 128-byte NCCL id comes from ``unique_id`` or is
+    broadcast from rank 0 over an initialised torch.distributed group."""
+
+    def __init__(self, rank: int, world: int, device=None, unique_id: bytes | None = None, group=None):
+        import ctypes
+
+        import torch
+
+        from ._runtime import Context, lib
+
+        self.torch, self.rank, self.world = torch, int(rank), int(world)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   (device.index if hasattr(device, "index") else int(device)))
+        if not lib().gm_comm_available():
+            raise RuntimeError("libnccl.so.2 not found: the native data plane needs NCCL")
+        if unique_id is None:
+            import torch.distributed as dist
+
+            buf = (ctypes.c_uint8 * 128)()
+            if self.rank == 0 and lib().gm_comm_unique_id(ctypes.addressof(buf)) != 0:
+                raise RuntimeError("ncclGetUniqueId failed")
+            t = torch.tensor(list(bytes(buf)), dtype=torch.uint8, device=self.device)
+            dist.broadcast(t, 0, group=group)
+            unique_id = bytes(t.cpu().tolist())
+        if len(unique_id) != 128:
+            raise ValueError("the NCCL unique id is 128 bytes")
+        self._id = (ctypes.c_uint8 * 128)(*unique_id)
+        self.ctx = Context(self.device.index)
+        self.ctx.call("gm_init_comm", ctypes.addressof(self._id), self.rank, self.world)
+        self._ct = ctypes
+
+    @staticmethod
+    def unique_id() -> bytes:
+        """A fresh NCCL id (rank 0), to hand to the other ranks out of band."""
+        import ctypes
+
+        from ._runtime import lib
+
+        buf = (ctypes.c_uint8 * 128)()
+        if lib().gm_comm_unique_id(ctypes.addressof(buf)) != 0:
+            raise RuntimeError("ncclGetUniqueId failed (is libnccl.so.2 present?)")
+        return bytes(buf)
+
+    def _stream(self):
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def sendrecv(self, sends: dict, recvs: dict):
+        """One grouped batch: sends[peer] -> peer, recvs[peer] <- peer
+        (contiguous device tensors, sizes in bytes from the tensors)."""
+        ct = self._ct
+        sp = sorted(sends.items())
+        rp = sorted(recvs.items())
+
+        def arrays(items):
+            n = len(items)
+            peers = (ct.c_int * max(n, 1))(*[p for p, _ in items])
+            bufs = (ct.c_void_p * max(n, 1))(*[t.data_ptr() for _, t in items])
+            nbytes = (ct.c_int64 * max(n, 1))(*[t.numel() * t.element_size() for _, t in items])
+            return n, peers, bufs, nbytes
+
+        ns, sp_, sb, sn = arrays(sp)
+        nr, rp_, rb, rn = arrays(rp)
+        self.ctx.call("gm_sendrecv", ns, ct.addressof(sp_), ct.addressof(sb), ct.addressof(sn), nr,
+                      ct.addressof(rp_), ct.addressof(rb), ct.addressof(rn), self._stream())
+
+    def allreduce_sum(self, t):
+        if t.dtype != self.torch.float64 or not t.is_contiguous():
+            raise ValueError("allreduce_sum: contiguous float64 tensors only")
+        self.ctx.call("gm_allreduce_sum", t.data_ptr(), t.numel(), self._stream())
+        return t
+
+    def all_gather(self, outs: list, t):
+        """outs[r] <- rank r's t: one grouped batch of sends to / receives
+        from every rank (own slot by copy)."""
+        outs[self.rank].copy_(t)
+        peers = [r for r in range(self.world) if r != self.rank]
+        self.sendrecv({p: t for p in peers}, {p: outs[p] for p in peers})
+
+    def close(self):
+        if self.ctx is not None:
+            self.ctx.call("gm_comm_destroy")
+            self.ctx.close()
+            self.ctx = None
+
+
 class LocalHub:
     """Shared state of the in-process ranks of a LocalTransport group."""
 
@@ -388,6 +479,7 @@ class PartitionedMpc:
         self.settings_c = settings_c(cfg.solver)
         self._ctypes = ctypes
         self.halo = HaloExchange(part, self.W, transport, eng) if part.world > 1 else None
+        self._graphs = {}
 
     # -- inputs ----------------------------------------------------------------
     def _local(self, arr, axis):
@@ -421,6 +513,32 @@ class PartitionedMpc:
         (pass them back as the next step's lin_states / lin_inputs)."""
         self.load(x_measured, lin_states, lin_inputs, last_applied)
         self.enqueue()
+        summ = self.summary.cpu().numpy()
+        nu = self.nu
+        return summ[:nu].copy(), int(summ[nu]), int(summ[nu + 1])
+
+    def capture(self):
+        """Record ``enqueue`` as one CUDA graph -- K-LIN, the per-stage K-REC
+        launches with their halo pack / NCCL exchange / unpack, K-HG, the
+        all-reduce, K-QP and K-RS -- for the current ``has_prev``.  Needs a
+        stream-ordered data plane: ``NcclTransport`` (or world 1)."""
+        import torch
+
+        if self.part.world > 1 and not isinstance(self.transport, NcclTransport):
+            raise ConfigurationError("CUDA-graph capture of the partitioned step needs NcclTransport")
+        self.enqueue()  # first launches (lazy allocations) outside the capture
+        torch.cuda.current_stream(self.eng.device).synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.enqueue()
+        self._graphs[self.has_prev] = g
+        return g
+
+    def step_graph(self, x_measured, lin_states, lin_inputs, last_applied=None):
+        """``step`` through the captured graph (captured on first use)."""
+        self.load(x_measured, lin_states, lin_inputs, last_applied)
+        g = self._graphs.get(self.has_prev) or self.capture()
+        g.replay()
         summ = self.summary.cpu().numpy()
         nu = self.nu
         return summ[:nu].copy(), int(summ[nu]), int(summ[nu + 1])
