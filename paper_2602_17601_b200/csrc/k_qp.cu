@@ -193,34 +193,49 @@ __device__ __forceinline__ bool chol_factor(Qs& S) {
   return ok;
 }
 
-// L -> X = L^{-1} in place (the factor itself is not needed afterwards)
-// Two solve strategies per IPM iteration: (default) X = L^{-1} formed in
-// place once (23 K cycles at cfg3), then every K^{-1} b is two parallel
-// mat-vecs (~9 K per solve); (QP_SOLVE_SUBST) only the diagonal-tile
-// inverses (1.8 K) and single-warp blocked substitution (~24 K per solve,
-// measured: the 15-step chain of shuffle reductions and 23-cycle fp64 FMAs
-// loses to the inverse at two solves per factorisation).
-#ifndef QP_SOLVE_SUBST
+// Solve strategies per IPM iteration (cycles per iteration at cfg3,
+// scripts/qp_phases.py): (default) the diagonal-tile inverses plus the
+// 16x16 block-inverse coupling tiles (3.6 K) and an all-warp blocked
+// substitution with a one-block look-ahead (solve_mw16; the two solves
+// 30.6 K incl. the reduced-system prep) -- 119.8 K per iteration;
+// (QP_SOLVE_MW8) the same with 8-row blocks, 123.4 K; (QP_SOLVE_XXT, round
+// 1) X = L^{-1} formed in place (23 K) and every solve two parallel mat-vecs,
+// 133 K; (QP_SOLVE_SUBST) single-warp substitution (~24 K per solve).
+#if !defined(QP_SOLVE_SUBST) && defined(QP_SOLVE_XXT)
 __device__ __forceinline__ void invert_diag_blocks(Qs& S) {
   if (S.T == 0) return;
   qpchol::invert_full<kQpThreads>(S.K, S.T, S.dinv, S.X, S.scr);
 }
 #else
-// inverses of the diagonal tiles of L (into the X region); L stays in K
+// inverses of the diagonal tiles of L (into the X region); L stays in K;
+// with T <= 16 also the coupling tiles of the 16x16 block inverses (into
+// the scratch area) for solve_mw16
 __device__ __forceinline__ void invert_diag_blocks(Qs& S) {
   if (S.T == 0) return;
   qpchol::diag_inverses<kQpThreads>(S.K, S.T, S.dinv, S.X);
   __syncthreads();
+#if !defined(QP_SOLVE_SUBST) && !defined(QP_SOLVE_MW8)
+  if (S.T <= 16 && 64 * kQpWarps >= 512) qpchol::diag16<kQpThreads>(S.K, S.T, S.X, S.scr);
+#endif
 }
 #endif
 
 // x = K^{-1} b = X' (X b) through the padded solve vector S.yv (padding stays
 // zero); b and x are shared nf-vectors (x may alias b).  Call with all threads.
 __device__ void chol_solve(Qs& S, const double* b, double* x) {
-#ifndef QP_SOLVE_SUBST
+#if defined(QP_SOLVE_SUBST)
+  if (S.T > 0) qpchol::solve_llt<kQpThreads>(S.K, S.X, S.T, S.nf, b, x, S.yv);
+#elif defined(QP_SOLVE_XXT)
   if (S.T > 0) qpchol::solve_xxt<kQpThreads>(S.K, S.T, S.nf, b, x, S.yv + 8 * S.T);
 #else
-  if (S.T > 0) qpchol::solve_llt<kQpThreads>(S.K, S.X, S.T, S.nf, b, x, S.yv);
+  if (S.T > 0) {
+#ifndef QP_SOLVE_MW8
+    if (S.T <= 16 && 64 * kQpWarps >= 512)
+      qpchol::solve_mw16<kQpThreads>(S.K, S.X, S.scr, S.T, S.nf, b, x, S.yv);
+    else
+#endif
+      qpchol::solve_mw<kQpThreads>(S.K, S.X, S.T, S.nf, b, x, S.yv);
+  }
 #endif
 }
 

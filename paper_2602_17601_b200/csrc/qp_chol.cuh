@@ -826,4 +826,317 @@ __device__ __noinline__ void solve_llt(const double* Kt, const double* D, int T,
   __syncthreads();
 }
 
+// x = K^{-1} b = L^{-T} L^{-1} b by blocked substitution over all warps with
+// a look-ahead of one block (the pattern of factor_la): warp 0 runs the chain
+// -- apply the previous block's solution to the next block, then the 8x8
+// mat-vec with the diagonal-tile inverse D_J -- while warps 1.. update every
+// later block with the solution just published.  Named barriers, by step
+// parity: Y (warp 0 arrives after publishing block J, the others sync) and
+// U (the others arrive after their update with block J, warp 0 syncs two
+// steps later, before it needs those contributions).  No L^{-1} is formed:
+// only D (diag_inverses).  b: nf entries (padding reads as zero); x may
+// alias b; s: 8T doubles of shared scratch.  All NT threads call.
+template <int NT>
+__device__ __noinline__ void solve_mw(const double* Kt, const double* D, int T, int nf, const double* b, double* x,
+                                      double* s) {
+  QP_SMEM(Kt);
+  QP_SMEM(D);
+  QP_SMEM(s);
+  constexpr int BY = 8, BU = 10;  // Y: 8, 9; U: 10, 11 (factor_la uses 1-4)
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int rr = lane >> 2, cq = lane & 3;
+  for (int t = tid; t < 8 * T; t += NT) s[t] = t < nf ? b[t] : 0.0;
+  __syncthreads();
+  // warp-0 helpers: 8-vector out[rr] = sum_c M[rr][c] v[c] (lanes (rr, cq)
+  // take columns 2cq, 2cq+1; 4-lane reduce), M read through eo (row, col)
+  auto mv8 = [&](const double* M, const double* v) {
+    double t0 = fma(M[eo(rr, 2 * cq)], v[2 * cq], M[eo(rr, 2 * cq + 1)] * v[2 * cq + 1]);
+    t0 += __shfl_xor_sync(0xffffffffu, t0, 1);
+    t0 += __shfl_xor_sync(0xffffffffu, t0, 2);
+    return t0;
+  };
+  // transposed: out[rr] = sum_r M[r][rr] v[r]
+  auto mv8t = [&](const double* M, const double* v) {
+    double t0 = fma(M[eo(2 * cq, rr)], v[2 * cq], M[eo(2 * cq + 1, rr)] * v[2 * cq + 1]);
+    t0 += __shfl_xor_sync(0xffffffffu, t0, 1);
+    t0 += __shfl_xor_sync(0xffffffffu, t0, 2);
+    return t0;
+  };
+  // ---- forward: y = L^{-1} b (y overwrites s) ----
+  if (wid == 0) {
+    for (int J = 0; J < T; ++J) {
+      if (J >= 2) bar_sync(BU + (J & 1), NT);  // others applied y_0..y_{J-2} to block J
+      double* sJ = s + 8 * J;
+      if (J >= 1) {  // look-ahead: y_{J-1} into block J
+        const double v = mv8(Kt + ti(J, J - 1) * kTS, s + 8 * (J - 1));
+        __syncwarp();
+        if (cq == 0) sJ[rr] -= v;
+        __syncwarp();
+      }
+      const double y = mv8(D + J * kTS, sJ);
+      __syncwarp();
+      if (cq == 0) sJ[rr] = y;
+      __syncwarp();
+      __threadfence_block();
+      bar_arrive(BY + (J & 1), NT);
+    }
+    for (int J = max(T, 2); J < T + 2; ++J) bar_sync(BU + (J & 1), NT);  // the last two U phases
+  } else {
+    const int ut = tid - 32;
+    for (int J = 0; J < T; ++J) {
+      bar_sync(BY + (J & 1), NT);  // y_J published
+      const double* yJ = s + 8 * J;
+      for (int row = 8 * (J + 2) + ut; row < 8 * T; row += NT - 32) {
+        const double* Lt = Kt + ti(row >> 3, J) * kTS;
+        const int r = row & 7;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; c += 2) {
+          a0 = fma(Lt[eo(r, c)], yJ[c], a0);
+          a1 = fma(Lt[eo(r, c + 1)], yJ[c + 1], a1);
+        }
+        s[row] -= a0 + a1;
+      }
+      __threadfence_block();
+      bar_arrive(BU + (J & 1), NT);
+    }
+  }
+  __syncthreads();
+  // ---- backward: x = L^{-T} y (x overwrites s), J = T-1 .. 0 ----
+  // step index q = T-1-J drives the barrier parity
+  if (wid == 0) {
+    for (int q = 0; q < T; ++q) {
+      const int J = T - 1 - q;
+      if (q >= 2) bar_sync(BU + (q & 1), NT);
+      double* tJ = s + 8 * J;
+      if (q >= 1) {  // look-ahead: x_{J+1} into block J: t_J -= L_{J+1,J}^T x_{J+1}
+        const double v = mv8t(Kt + ti(J + 1, J) * kTS, s + 8 * (J + 1));
+        __syncwarp();
+        if (cq == 0) tJ[rr] -= v;
+        __syncwarp();
+      }
+      const double xv = mv8t(D + J * kTS, tJ);
+      __syncwarp();
+      if (cq == 0) tJ[rr] = xv;
+      __syncwarp();
+      __threadfence_block();
+      bar_arrive(BY + (q & 1), NT);
+    }
+    for (int q = max(T, 2); q < T + 2; ++q) bar_sync(BU + (q & 1), NT);
+  } else {
+    const int ut = tid - 32;
+    for (int q = 0; q < T; ++q) {
+      const int J = T - 1 - q;
+      bar_sync(BY + (q & 1), NT);  // x_J published
+      const double* xJ = s + 8 * J;
+      // t_K[c] -= sum_r L_JK[r][c] x_J[r] for the blocks K <= J-2
+      for (int col = ut; col < 8 * (J - 1); col += NT - 32) {
+        const double* Lt = Kt + ti(J, col >> 3) * kTS;
+        const int c = col & 7;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int r = 0; r < 8; r += 2) {
+          a0 = fma(Lt[eo(r, c)], xJ[r], a0);
+          a1 = fma(Lt[eo(r + 1, c)], xJ[r + 1], a1);
+        }
+        s[col] -= a0 + a1;
+      }
+      __threadfence_block();
+      bar_arrive(BU + (q & 1), NT);
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < nf; t += NT) x[t] = s[t];
+  __syncthreads();
+}
+
+// Off-diagonal parts of the 16x16 diagonal-block inverses: for 16-block j
+// (tiles 2j, 2j+1), [[A, 0], [B, C]]^{-1} = [[A^-1, 0], [-C^-1 B A^-1, C^-1]];
+// X21_j = -D_{2j+1} L_{2j+1,2j} D_{2j} into X21 (64 doubles per block, eo
+// layout).  D from diag_inverses.  All NT threads call.
+template <int NT>
+__device__ __noinline__ void diag16(const double* Kt, int T, const double* D, double* X21) {
+  QP_SMEM(Kt);
+  QP_SMEM(D);
+  QP_SMEM(X21);
+  const int nb = T / 2;  // full 16-blocks
+  constexpr int PER = 4;  // items per thread (nb * 64 <= 4 * NT for T <= 16 and NT >= 256)
+  double m[PER];
+  // M = B A^-1 (into registers), then X21 = -C^-1 M after a barrier
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int t = threadIdx.x + u * NT;
+    m[u] = 0.0;
+    if (t < nb * 64) {
+      const int j = t >> 6, r = (t >> 3) & 7, c = t & 7;
+      const double* B = Kt + ti(2 * j + 1, 2 * j) * kTS;
+      const double* A = D + 2 * j * kTS;
+      double a = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a = fma(B[eo(r, k)], A[eo(k, c)], a);
+      m[u] = a;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int t = threadIdx.x + u * NT;
+    if (t < nb * 64) {
+      const int j = t >> 6, r = (t >> 3) & 7, c = t & 7;
+      X21[j * 64 + eo(r, c)] = m[u];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int t = threadIdx.x + u * NT;
+    m[u] = 0.0;
+    if (t < nb * 64) {
+      const int j = t >> 6, r = (t >> 3) & 7, c = t & 7;
+      const double* C = D + (2 * j + 1) * kTS;
+      const double* Mj = X21 + j * 64;
+      double a = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a = fma(C[eo(r, k)], Mj[eo(k, c)], a);
+      m[u] = -a;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int t = threadIdx.x + u * NT;
+    if (t < nb * 64) {
+      const int j = t >> 6, r = (t >> 3) & 7, c = t & 7;
+      X21[j * 64 + eo(r, c)] = m[u];
+    }
+  }
+  __syncthreads();
+}
+
+// solve_mw with 16-row blocks (tiles 2j, 2j+1): the chain step is one 16x16
+// look-ahead product and one 16x16 mat-vec with the block inverse
+// [[D_2j, 0], [X21_j, D_2j+1]], lane (r, h) = (row, column half): 8 FMAs in
+// two chains and one shuffle -- half the chain steps of solve_mw and no
+// 4-lane reduce.  T <= 16 (X21 in 512 doubles); odd T: the last block is
+// 8 rows.  Same arguments as solve_mw plus X21 (diag16).
+template <int NT>
+__device__ __noinline__ void solve_mw16(const double* Kt, const double* D, const double* X21, int T, int nf,
+                                        const double* b, double* x, double* s) {
+  QP_SMEM(Kt);
+  QP_SMEM(D);
+  QP_SMEM(X21);
+  QP_SMEM(s);
+  constexpr int BY = 8, BU = 10;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int r = lane >> 1, h = lane & 1, rr = r & 7, rh = r >> 3;
+  const int T16 = (T + 1) / 2, n8 = 8 * T;
+  for (int t = tid; t < n8; t += NT) s[t] = t < nf ? b[t] : 0.0;
+  __syncthreads();
+  // dot of 8 with two chains
+  auto dot8 = [](const double* M, int row, bool trans, const double* v) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      a0 = fma(trans ? M[eo(k, row)] : M[eo(row, k)], v[k], a0);
+      a1 = fma(trans ? M[eo(k + 1, row)] : M[eo(row, k + 1)], v[k + 1], a1);
+    }
+    return a0 + a1;
+  };
+  // ---- forward ----
+  if (wid == 0) {
+    for (int j = 0; j < T16; ++j) {
+      if (j >= 2) bar_sync(BU + (j & 1), NT);
+      const int tr = 2 * j + rh;          // tile row of this lane's row
+      const bool live = tr < T;
+      if (j >= 1) {  // look-ahead: y of block j-1 into block j
+        double v = (live ? 1.0 : 0.0) *
+                   dot8(Kt + ti(live ? tr : 2 * (j - 1) + h, 2 * (j - 1) + h) * kTS, rr, false, s + 16 * (j - 1) + 8 * h);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        __syncwarp();
+        if (h == 0 && live) s[16 * j + r] -= v;
+        __syncwarp();
+      }
+      // lane -> (matrix, vector) by selects: one uniform dot per lane (no
+      // divergent paths); the (rows 0-7, half 1) lanes contribute zero
+      const bool two = 2 * j + 1 < T;
+      const double* M = rh == 0 ? D + 2 * j * kTS : (h == 0 ? X21 + j * 64 : D + (2 * j + 1) * kTS);
+      const double wgt = (live && !(rh == 0 && h == 1) && (rh == 0 || two)) ? 1.0 : 0.0;
+      double v = wgt * dot8(live ? M : D, rr, false, s + 16 * j + 8 * (h & (live ? 1 : 0)));
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      __syncwarp();
+      if (h == 0 && live) s[16 * j + r] = v;
+      __syncwarp();
+      __threadfence_block();
+      bar_arrive(BY + (j & 1), NT);
+    }
+    for (int j = max(T16, 2); j < T16 + 2; ++j) bar_sync(BU + (j & 1), NT);
+  } else {
+    const int ut = tid - 32;
+    for (int j = 0; j < T16; ++j) {
+      bar_sync(BY + (j & 1), NT);
+      const double* y = s + 16 * j;
+      const bool two = 2 * j + 1 < T;
+      for (int row = 16 * (j + 2) + ut; row < n8; row += NT - 32) {
+        const int rt = row >> 3, ri = row & 7;
+        double a = dot8(Kt + ti(rt, 2 * j) * kTS, ri, false, y);
+        if (two) a += dot8(Kt + ti(rt, 2 * j + 1) * kTS, ri, false, y + 8);
+        s[row] -= a;
+      }
+      __threadfence_block();
+      bar_arrive(BU + (j & 1), NT);
+    }
+  }
+  __syncthreads();
+  // ---- backward (step q = T16-1-j) ----
+  if (wid == 0) {
+    for (int q = 0; q < T16; ++q) {
+      const int j = T16 - 1 - q;
+      if (q >= 2) bar_sync(BU + (q & 1), NT);
+      const int tc = 2 * j + rh;  // tile column (this lane's row of block j as a column of L)
+      const bool live = tc < T;
+      if (q >= 1) {  // look-ahead: x of block j+1 into block j
+        const int trow = 2 * (j + 1) + h;  // tile row of block j+1's half h
+        const bool ok = live && trow < T;
+        double v = (ok ? 1.0 : 0.0) * dot8(Kt + (ok ? ti(trow, tc) : 0) * kTS, rr, true,
+                                           s + 16 * (j + 1) + 8 * (ok ? h : 0));
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        __syncwarp();
+        if (h == 0 && live) s[16 * j + r] -= v;
+        __syncwarp();
+      }
+      // rows 0-7: D_2j^T t_a (half 0) + X21^T t_c (half 1); rows 8-15:
+      // D_2j+1^T t_c (half 1); selects instead of divergent paths
+      const bool two = 2 * j + 1 < T;
+      const double* M = h == 0 ? D + 2 * j * kTS : (rh == 0 ? X21 + j * 64 : D + (2 * j + 1) * kTS);
+      const double wgt = (live && !(rh == 1 && h == 0) && (h == 0 || two)) ? 1.0 : 0.0;
+      double v = wgt * dot8((live && (h == 0 || two)) ? M : D, rr, true, s + 16 * j + 8 * (two ? h : 0));
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      __syncwarp();
+      if (h == 0 && live) s[16 * j + r] = v;
+      __syncwarp();
+      __threadfence_block();
+      bar_arrive(BY + (q & 1), NT);
+    }
+    for (int q = max(T16, 2); q < T16 + 2; ++q) bar_sync(BU + (q & 1), NT);
+  } else {
+    const int ut = tid - 32;
+    for (int q = 0; q < T16; ++q) {
+      const int j = T16 - 1 - q;
+      bar_sync(BY + (q & 1), NT);
+      const double* xj = s + 16 * j;
+      const bool two = 2 * j + 1 < T;
+      for (int col = ut; col < 16 * (j - 1) && col < n8; col += NT - 32) {
+        const int ct = col >> 3, ci = col & 7;
+        double a = dot8(Kt + ti(2 * j, ct) * kTS, ci, true, xj);
+        if (two) a += dot8(Kt + ti(2 * j + 1, ct) * kTS, ci, true, xj + 8);
+        s[col] -= a;
+      }
+      __threadfence_block();
+      bar_arrive(BU + (q & 1), NT);
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < nf; t += NT) x[t] = s[t];
+  __syncthreads();
+}
+
 }  // namespace qpchol
