@@ -277,17 +277,30 @@ __device__ void ct_apply(const Qs& S, const double* tv, double* out) {
   }
 }
 
-// out[r] = (C xv)[r]
+// out[r] = (C xv)[r].  General rows: one 8-lane group per row (all rows at
+// once for ng <= NT/8; a 3-level shuffle instead of a warp-wide 5-level one),
+// two FMA chains per lane.
 __device__ void c_apply(const Qs& S, const double* xv, double* out) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int G = 8;
+  const int lg = threadIdx.x & (G - 1), grp = threadIdx.x / G;
   for (int r = threadIdx.x; r < S.m; r += blockDim.x)
     if (S.rcol[r] >= 0) out[r] = S.rval[r] * xv[S.rcol[r]];
-  for (int gi = wid; gi < S.ng; gi += kQpWarps) {
-    const double* row = S.Cg + (int64_t)gi * S.n;
-    double s = 0.0;
-    for (int k = lane; k < S.nf; k += 32) s = fma(row[k], xv[S.kidx[k]], s);
-    s = warp_sum(s);
-    if (lane == 0) {
+  for (int g0 = 0; g0 < S.ng; g0 += kQpThreads / G) {
+    const int gi = g0 + grp;
+    double s = 0.0, s1 = 0.0;
+    if (gi < S.ng) {
+      const double* row = S.Cg + (int64_t)gi * S.n;
+      int k = lg;
+      for (; k + G < S.nf; k += 2 * G) {
+        s = fma(row[k], xv[S.kidx[k]], s);
+        s1 = fma(row[k + G], xv[S.kidx[k + G]], s1);
+      }
+      if (k < S.nf) s = fma(row[k], xv[S.kidx[k]], s);
+      s += s1;
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (gi < S.ng && lg == 0) {
       if (S.ge[gi] >= 0) s = fma(S.ga[gi], xv[S.eidx[S.ge[gi]]], s);
       out[S.grow[gi]] = s;
     }
@@ -422,6 +435,87 @@ __device__ void h_apply_rows(const Qs& S, const double* uv, double* out) {
 // then the rank-ng update runs with 16 independent accumulators.  Returns
 // false when an eliminated pivot K_ee is not positive (potrf's failure rule
 // applied to the eliminated block).
+// Lower 8x8 tiles of 2H + Cg' diag(wg) Cg on the fp64 tensor cores: the C
+// fragment (row i, cols 2p, 2p+1) starts from 2H, ng/4 DMMAs add the general
+// rows (A[i][g] = wg_g Cg[g][row], B[g][j] = Cg[g][col]); padding rows / cols
+// (>= n) become the identity.  One warp per tile, U tiles in flight.  The
+// operand loads are branch-free (clamped indices, 0/1 masks folded into the
+// products) with 32-bit offsets; SH: H, Cg and wg are in shared memory.
+// explicit shared-window loads: the on-chip / workspace choice of H and the
+// general rows is made at run time, so their pointers are generic and the
+// compiler emits LD.E (generic, 64-bit address math) even with
+// __builtin_assume(__isShared(...)); these helpers force LDS
+__device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ double lds64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+// element i of a double array: shared window when SH (base = sh_addr), else generic
+template <bool SH>
+__device__ __forceinline__ double ldv(const double* p, uint32_t base, int i) {
+  return SH ? lds64(base + 8u * (uint32_t)i) : p[i];
+}
+
+template <bool SH>
+__device__ __noinline__ void build_tiles(const double* Cg, const double* Hp, const double* wg, double* K,
+                                         const unsigned short* tij, int T, int n, int ng, int ldc) {
+  const uint32_t cgb = SH ? sh_addr(Cg) : 0u, hpb = SH ? sh_addr(Hp) : 0u, wgb = SH ? sh_addr(wg) : 0u;
+  QP_SMEM(K);
+  QP_SMEM(tij);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i = lane >> 2, p = lane & 3;
+  const int ntiles = T * (T + 1) / 2;
+  constexpr int U = 3;  // tiles in flight per warp
+  for (int t0 = wid; t0 < ntiles; t0 += U * kQpWarps) {
+    int r[U], ca[U], ra[U], rbc[U];
+    double ma[U], mb[U], h0[U], h1[U];
+    bool live[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int tt = t0 + u * kQpWarps;
+      live[u] = tt < ntiles;
+      const int ij = tij[min(tt, ntiles - 1)];  // (I << 8) | J, built once
+      const int I = ij >> 8, J = ij & 255;
+      r[u] = 8 * I + i;
+      ca[u] = 8 * J + 2 * p;
+      const int rb = 8 * J + i;  // B operand column
+      ra[u] = min(r[u], n - 1);
+      rbc[u] = min(rb, n - 1);
+      ma[u] = r[u] < n ? 1.0 : 0.0;
+      mb[u] = rb < n ? 1.0 : 0.0;
+      const int cb = ca[u] + 1;
+      // strictly lower entries start from 2H; the diagonal is completed below
+      h0[u] = (live[u] && r[u] < n && ca[u] < n && r[u] > ca[u]) ? 2.0 * ldv<SH>(Hp, hpb, colbase(ca[u], n) + r[u])
+                                                                  : 0.0;
+      h1[u] = (live[u] && r[u] < n && cb < n && r[u] > cb) ? 2.0 * ldv<SH>(Hp, hpb, colbase(cb, n) + r[u]) : 0.0;
+    }
+    for (int g0 = 0; g0 < ng; g0 += 4) {
+      const int g = g0 + p;
+      const bool gv = g < ng;
+      const int rowo = (gv ? g : ng - 1) * ldc;
+      const double wgg = gv ? ldv<SH>(wg, wgb, g) : 0.0;
+      double av[U], bv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        av[u] = (wgg * ma[u]) * ldv<SH>(Cg, cgb, rowo + ra[u]);
+        bv[u] = mb[u] * ldv<SH>(Cg, cgb, rowo + rbc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) qpchol::dmma884(h0[u], h1[u], av[u], bv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!live[u]) continue;
+      const int cb = ca[u] + 1;
+      if (r[u] >= n || ca[u] >= n) h0[u] = r[u] == ca[u] ? 1.0 : 0.0;
+      if (r[u] >= n || cb >= n) h1[u] = r[u] == cb ? 1.0 : 0.0;
+      if (r[u] >= ca[u]) K[qpchol::gel(r[u], ca[u])] = h0[u];
+      if (r[u] >= cb) K[qpchol::gel(r[u], cb)] = h1[u];
+    }
+  }
+}
+
 __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
   const int n = S.nf, ng = terms ? S.ng : 0;
   bool ok = true;
@@ -450,57 +544,12 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
   }
   __syncthreads();
   if (!g_qp_chol_split) qmark(const_cast<Qs&>(S), 13);
-  // lower 8x8 tiles of 2H + Cg' diag(wg) Cg on the fp64 tensor cores: the
-  // C fragment (row i, cols 2p, 2p+1) starts from 2H, ng/4 DMMAs add the
-  // general rows (A[i][g] = wg_g Cg[g][row], B[g][j] = Cg[g][col]), padding
-  // rows/cols (>= n) become the identity.  One warp per tile.
-  {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int i = lane >> 2, p = lane & 3;
-    const int T = S.T, ntiles = T * (T + 1) / 2;
-    constexpr int U = 3;  // tiles in flight per warp
-    for (int t0 = wid; t0 < ntiles; t0 += U * kQpWarps) {
-      int r[U], ca[U], rb[U];
-      double h0[U], h1[U];
-      bool live[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int tt = t0 + u * kQpWarps;
-        live[u] = tt < ntiles;
-          const int ij = S.tij[min(tt, ntiles - 1)];  // (I << 8) | J, built once
-        const int I = ij >> 8, J = ij & 255;
-        r[u] = 8 * I + i;
-        ca[u] = 8 * J + 2 * p;
-        rb[u] = 8 * J + i;  // B operand column
-        const int cb = ca[u] + 1;
-        // strictly lower entries start from 2H; the diagonal is completed below
-        h0[u] = (live[u] && r[u] < n && ca[u] < n && r[u] > ca[u]) ? 2.0 * S.Hp[colbase(ca[u], n) + r[u]] : 0.0;
-        h1[u] = (live[u] && r[u] < n && cb < n && r[u] > cb) ? 2.0 * S.Hp[colbase(cb, n) + r[u]] : 0.0;
-      }
-      for (int g0 = 0; g0 < ng; g0 += 4) {
-        const int g = g0 + p;
-        const double* cg = S.Cg + (int64_t)min(g, ng - 1) * S.n;
-        const double wgg = g < ng ? S.wg[g] : 0.0;
-        double av[U], bv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          av[u] = (g < ng && r[u] < n) ? wgg * cg[r[u]] : 0.0;
-          bv[u] = (g < ng && rb[u] < n) ? cg[rb[u]] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) qpchol::dmma884(h0[u], h1[u], av[u], bv[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (!live[u]) continue;
-        const int cb = ca[u] + 1;
-        if (r[u] >= n || ca[u] >= n) h0[u] = r[u] == ca[u] ? 1.0 : 0.0;
-        if (r[u] >= n || cb >= n) h1[u] = r[u] == cb ? 1.0 : 0.0;
-        if (r[u] >= ca[u]) S.K[qpchol::gel(r[u], ca[u])] = h0[u];
-        if (r[u] >= cb) S.K[qpchol::gel(r[u], cb)] = h1[u];
-      }
-    }
-  }
+  // lower 8x8 tiles of 2H + Cg' diag(wg) Cg on the fp64 tensor cores
+  // (build_tiles); on-chip H and Cg take the shared-address instantiation
+  if (__isShared(S.Cg) && __isShared(S.Hp) && __isShared(S.wg))
+    build_tiles<true>(S.Cg, S.Hp, S.wg, S.K, S.tij, S.T, n, ng, S.n);
+  else
+    build_tiles<false>(S.Cg, S.Hp, S.wg, S.K, S.tij, S.T, n, ng, S.n);
   __syncthreads();
   if (!g_qp_chol_split) qmark(const_cast<Qs&>(S), 14);
   // diagonal (holds only the general-row term so far): (2H + reg) +
