@@ -490,7 +490,8 @@ __device__ __noinline__ void build_tiles(const double* Cg, const double* Hp, con
                                                                   : 0.0;
       h1[u] = (live[u] && r[u] < n && cb < n && r[u] > cb) ? 2.0 * ldv<SH>(Hp, hpb, colbase(cb, n) + r[u]) : 0.0;
     }
-    for (int g0 = 0; g0 < ng; g0 += 4) {
+#pragma unroll 5
+    for (int g0 = 0; g0 < ng; g0 += 4) {  // unrolled: the next steps' loads overlap the DMMAs
       const int g = g0 + p;
       const bool gv = g < ng;
       const int rowo = (gv ? g : ng - 1) * ldc;
