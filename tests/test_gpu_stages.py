@@ -419,3 +419,38 @@ def test_single_node_ignores_edge_function(pkg):
     l2 = pkg.linearize_trajectory(m2, topo, x, u)
     for k in ("a_self", "b", "c"):
         assert np.array_equal(getattr(l1, k), getattr(l2, k)), k
+
+
+@pytest.mark.parametrize("n", [120, 128, 136, 160])
+def test_qp_factor_block_sizes(pkg, n):
+    """Dense QPs across the solver's substitution variants: 16-row blocks for
+    T = ceil(n/8) <= 16 (odd and even T), 8-row blocks beyond; box rows plus
+    general rows, against the oracle IPM (qpsolver.py:112-235): same status,
+    iterations +-1, |du| <= 1e-6."""
+    from oracle import ref_port as O
+
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n))
+    H = A @ A.T / n + np.eye(n) * 0.1
+    g = rng.standard_normal(n) * 3.0
+    ng = 12
+    Cg = rng.standard_normal((ng, n))
+    C = np.vstack([np.eye(n), -np.eye(n), Cg])
+    d = np.concatenate([np.full(n, 0.4), np.full(n, 0.4), np.abs(rng.standard_normal(ng)) + 0.2])
+    ref = O.solve_qp(H, g, C, d)
+    sol = pkg.solve_qp(pkg.QpProblem(H, g, C, d))
+    info = (n, sol.status.value, ref.status, sol.iterations, ref.iterations)
+    assert sol.status.value == ref.status, info
+    assert abs(sol.iterations - ref.iterations) <= 1, info
+    assert np.max(np.abs(sol.u - ref.u)) <= 1e-6, info
+
+
+def test_qp_too_large_fails_loudly(pkg):
+    """Beyond the on-chip capacity (vectors + factor tiles > shared memory)
+    the solver refuses with a ConfigurationError instead of degrading."""
+    from paper_2602_17601_b200.errors import ConfigurationError
+
+    n = 200
+    C = np.vstack([np.eye(n), -np.eye(n), np.ones((12, n))])
+    with pytest.raises(ConfigurationError):
+        pkg.solve_qp(pkg.QpProblem(np.eye(n), np.ones(n), C, np.ones(2 * n + 12)))
