@@ -446,9 +446,11 @@ __device__ void h_apply_rows(const Qs& S, const double* uv, double* out) {
 // compiler emits LD.E (generic, 64-bit address math) even with
 // __builtin_assume(__isShared(...)); these helpers force LDS
 __device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// (not volatile: a pure load of data no thread writes during the caller, so
+// the compiler may hoist and batch these loads ahead of the DMMAs)
 __device__ __forceinline__ double lds64(uint32_t a) {
   double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
   return v;
 }
 // element i of a double array: shared window when SH (base = sh_addr), else generic
@@ -490,18 +492,30 @@ __device__ __noinline__ void build_tiles(const double* Cg, const double* Hp, con
                                                                   : 0.0;
       h1[u] = (live[u] && r[u] < n && cb < n && r[u] > cb) ? 2.0 * ldv<SH>(Hp, hpb, colbase(cb, n) + r[u]) : 0.0;
     }
-#pragma unroll 5
-    for (int g0 = 0; g0 < ng; g0 += 4) {  // unrolled: the next steps' loads overlap the DMMAs
+    // software-pipelined over the general-row steps: the operands of step
+    // g0 + 4 are loaded before the DMMAs of step g0 are issued
+    double xa[U], xb[U], wnext;
+    auto load = [&](int g0) {
       const int g = g0 + p;
       const bool gv = g < ng;
       const int rowo = (gv ? g : ng - 1) * ldc;
-      const double wgg = gv ? ldv<SH>(wg, wgb, g) : 0.0;
+      wnext = gv ? ldv<SH>(wg, wgb, g) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        xa[u] = ldv<SH>(Cg, cgb, rowo + ra[u]);
+        xb[u] = ldv<SH>(Cg, cgb, rowo + rbc[u]);
+      }
+    };
+    if (ng > 0) load(0);
+    for (int g0 = 0; g0 < ng; g0 += 4) {
+      const double wgg = wnext;
       double av[U], bv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        av[u] = (wgg * ma[u]) * ldv<SH>(Cg, cgb, rowo + ra[u]);
-        bv[u] = mb[u] * ldv<SH>(Cg, cgb, rowo + rbc[u]);
+        av[u] = (wgg * ma[u]) * xa[u];
+        bv[u] = mb[u] * xb[u];
       }
+      if (g0 + 4 < ng) load(g0 + 4);
 #pragma unroll
       for (int u = 0; u < U; ++u) qpchol::dmma884(h0[u], h1[u], av[u], bv[u]);
     }
