@@ -137,3 +137,22 @@ def test_frozen_model_is_immutable():
     c = m.copy()
     c.psi.weights[0][0, 0] = 1.0
     assert not hasattr(c, "_frozen")
+
+
+def test_native_comm_entry_points_on_cpu():
+    """The native data plane resolves NCCL at run time (no link-time
+    dependency): availability, a unique id, and loud errors on a context
+    without a communicator or with bad arguments -- none needs a GPU."""
+    import ctypes
+
+    from paper_2602_17601_b200._runtime import lib
+
+    L = lib()
+    if not L.gm_comm_available():
+        pytest.skip("libnccl.so.2 not present in this image")
+    a, b = (ctypes.c_uint8 * 128)(), (ctypes.c_uint8 * 128)()
+    assert L.gm_comm_unique_id(ctypes.addressof(a)) == 0
+    assert L.gm_comm_unique_id(ctypes.addressof(b)) == 0
+    assert bytes(a) != bytes(b)  # fresh ids
+    assert L.gm_comm_unique_id(None) != 0
+    assert L.gm_comm_destroy(None) != 0
