@@ -24,9 +24,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "mesh":  # cfg5: 400 x 250 mesh, one ins
     li = torch.from_numpy(inputs).cuda()
     x0 = torch.from_numpy(np.ascontiguousarray(states[0])).cuda()
     run = lambda: (pm.load(x0, ls, li), pm.enqueue())
-else:  # cfg4 wave: B instances of the M=200 chain
-    B = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
-    M = 200
+else:  # cfg4 wave: B instances of the M=200 chain ("cfg3": one M=1000 chain)
+    cfg3 = len(sys.argv) > 1 and sys.argv[1] == "cfg3"
+    B = 1 if cfg3 else (int(sys.argv[1]) if len(sys.argv) > 1 else 1024)
+    M = 1000 if cfg3 else 200
     topo, model, _, _, spec = workloads.scaling_problem(M, N, 0.01, 0)
     xs, ls, li, xr = [], [], [], []
     for i in range(B):
