@@ -20,7 +20,9 @@ import numpy as np
 from .errors import ConfigurationError
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "lib" / "libgnnmpc_b200.so"
+# GM_LIB_PATH: load another build of the same library (A/B measurements of
+# kernel variants within one process environment); default the in-tree build
+LIB_PATH = Path(os.environ["GM_LIB_PATH"]) if os.environ.get("GM_LIB_PATH") else _HERE / "lib" / "libgnnmpc_b200.so"
 
 GM_OK, GM_ERR_CONFIG, GM_ERR_NUMERIC, GM_ERR_CUDA = 0, 2, 3, 4
 QP_STATUS_NAMES = ("optimal", "max_iterations", "primal_infeasible", "numerical_failure")

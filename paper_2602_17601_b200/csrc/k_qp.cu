@@ -243,9 +243,29 @@ __device__ void chol_solve(Qs& S, const double* b, double* x) {
 // QP building blocks
 // ---------------------------------------------------------------------------
 
+// explicit shared-window loads: the on-chip / workspace choice of H and the
+// general rows is made at run time, so their pointers are generic and the
+// compiler emits LD.E (generic, 64-bit address math) even with
+// __builtin_assume(__isShared(...)); these helpers force LDS
+__device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// (not volatile: a pure load of data no thread writes during the caller, so
+// the compiler may hoist and batch these loads ahead of the DMMAs)
+__device__ __forceinline__ double lds64(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+// element i of a double array: shared window when SH (base = sh_addr), else generic
+template <bool SH>
+__device__ __forceinline__ double ldv(const double* p, uint32_t base, int i) {
+  return SH ? lds64(base + 8u * (uint32_t)i) : p[i];
+}
+
 // out = C' tv.  General rows are stored column-permuted: Cg[gi][k] is the
 // coefficient of kept variable kidx[k]; a row's eliminated variable (if any)
 // is (ge[gi], ga[gi]).
+// RHS: write -rd - (C' tv) instead (the KKT right-hand side, fused)
+template <bool RHS = false>
 __device__ void ct_apply(const Qs& S, const double* tv, double* out) {
   for (int k = threadIdx.x; k < S.nf; k += blockDim.x) {
     const int c = S.kidx[k];
@@ -263,7 +283,8 @@ __device__ void ct_apply(const Qs& S, const double* tv, double* out) {
       s3 = fma(cg[(int64_t)(gi + 3) * S.n], tv[S.grow[gi + 3]], s3);
     }
     for (; gi < S.ng; ++gi) s0 = fma(cg[(int64_t)gi * S.n], tv[S.grow[gi]], s0);
-    out[c] = (s0 + s1) + (s2 + s3);
+    const double v = (s0 + s1) + (s2 + s3);
+    out[c] = RHS ? -S.rd[c] - v : v;
   }
   for (int e = threadIdx.x; e < S.ne; e += blockDim.x) {
     const int c = S.eidx[e];
@@ -273,7 +294,7 @@ __device__ void ct_apply(const Qs& S, const double* tv, double* out) {
       s0 = fma(S.rval[r], tv[r], s0);
     }
     if (S.egi[e] >= 0) s0 = fma(S.ea[e], tv[S.grow[S.egi[e]]], s0);
-    out[c] = s0;
+    out[c] = RHS ? -S.rd[c] - s0 : s0;
   }
 }
 
@@ -387,40 +408,51 @@ __device__ void h_apply(const Qs& S, const double* uv, double* out) {
 // accumulators; no shuffles or cross-warp partials (the warp-per-column form
 // above is for H left in global memory, where it batches the L2 round trips).
 __device__ void h_apply_rows(const Qs& S, const double* uv, double* out) {
-  const int n = S.nf, r = threadIdx.x;
+  const int n = S.nf;
   const double* Hp = S.Hp;
-  QP_SMEM(Hp);
-  // kept part of u gathered into out (out != uv; rewritten below) so the
-  // row loops read it directly instead of through kidx
+  const uint32_t hb = sh_addr(Hp);  // the caller checked __isShared(S.Hp)
   double* uk = out;
+  // two threads per row when n <= blockDim/2 (halves of the column range,
+  // combined in a fixed order)
+  const bool split = 2 * n <= (int)blockDim.x;
+  const int half = split ? (int)threadIdx.x / (blockDim.x / 2) : 0;
+  const int r = split ? (int)threadIdx.x % (blockDim.x / 2) : (int)threadIdx.x;
+  const int cmid = split ? n / 2 : n;
+  const int c_lo = half ? cmid : 0, c_hi = half ? n : cmid;
   double uv_r = 0.0;
-  if (r < n) uv_r = uv[S.kidx[r]];
+  if (half == 0 && r < n) uv_r = uv[S.kidx[r]];
   __syncthreads();
-  if (r < n) uk[r] = uv_r;
+  if (half == 0 && r < n) uk[r] = uv_r;
   __syncthreads();
   double acc = 0.0;
   if (r < n) {
+    auto hl = [&](int i) { return lds64(hb + 8u * (uint32_t)i); };
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int c = 0;
-    for (; c + 3 < r; c += 4) {
-      a0 = fma(Hp[colbase(c, n) + r], uk[c], a0);
-      a1 = fma(Hp[colbase(c + 1, n) + r], uk[c + 1], a1);
-      a2 = fma(Hp[colbase(c + 2, n) + r], uk[c + 2], a2);
-      a3 = fma(Hp[colbase(c + 3, n) + r], uk[c + 3], a3);
+    int c = c_lo;
+    const int cl = min(r, c_hi);
+    for (; c + 3 < cl; c += 4) {
+      a0 = fma(hl(colbase(c, n) + r), uk[c], a0);
+      a1 = fma(hl(colbase(c + 1, n) + r), uk[c + 1], a1);
+      a2 = fma(hl(colbase(c + 2, n) + r), uk[c + 2], a2);
+      a3 = fma(hl(colbase(c + 3, n) + r), uk[c + 3], a3);
     }
-    for (; c < r; ++c) a0 = fma(Hp[colbase(c, n) + r], uk[c], a0);
-    const double* colr = Hp + colbase(r, n);
-    for (; c + 3 < n; c += 4) {
-      a0 = fma(colr[c], uk[c], a0);
-      a1 = fma(colr[c + 1], uk[c + 1], a1);
-      a2 = fma(colr[c + 2], uk[c + 2], a2);
-      a3 = fma(colr[c + 3], uk[c + 3], a3);
+    for (; c < cl; ++c) a0 = fma(hl(colbase(c, n) + r), uk[c], a0);
+    const int colr = colbase(r, n);
+    c = max(c, r);
+    for (; c + 3 < c_hi; c += 4) {
+      a0 = fma(hl(colr + c), uk[c], a0);
+      a1 = fma(hl(colr + c + 1), uk[c + 1], a1);
+      a2 = fma(hl(colr + c + 2), uk[c + 2], a2);
+      a3 = fma(hl(colr + c + 3), uk[c + 3], a3);
     }
-    for (; c < n; ++c) a0 = fma(colr[c], uk[c], a0);
+    for (; c < c_hi; ++c) a0 = fma(hl(colr + c), uk[c], a0);
     acc = (a0 + a1) + (a2 + a3);
   }
+  double* part = S.K;  // free at this point (rebuilt by build_k)
+  if (split && half == 1 && r < n) part[r] = acc;
   __syncthreads();
-  if (r < n) out[S.kidx[r]] = acc;
+  if (split && half == 0 && r < n) acc += part[r];
+  if (half == 0 && r < n) out[S.kidx[r]] = acc;
   for (int e = threadIdx.x; e < S.ne; e += blockDim.x) out[S.eidx[e]] = S.hde[e] * uv[S.eidx[e]];
   __syncthreads();
 }
@@ -441,24 +473,6 @@ __device__ void h_apply_rows(const Qs& S, const double* uv, double* out) {
 // (>= n) become the identity.  One warp per tile, U tiles in flight.  The
 // operand loads are branch-free (clamped indices, 0/1 masks folded into the
 // products) with 32-bit offsets; SH: H, Cg and wg are in shared memory.
-// explicit shared-window loads: the on-chip / workspace choice of H and the
-// general rows is made at run time, so their pointers are generic and the
-// compiler emits LD.E (generic, 64-bit address math) even with
-// __builtin_assume(__isShared(...)); these helpers force LDS
-__device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-// (not volatile: a pure load of data no thread writes during the caller, so
-// the compiler may hoist and batch these loads ahead of the DMMAs)
-__device__ __forceinline__ double lds64(uint32_t a) {
-  double v;
-  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-  return v;
-}
-// element i of a double array: shared window when SH (base = sh_addr), else generic
-template <bool SH>
-__device__ __forceinline__ double ldv(const double* p, uint32_t base, int i) {
-  return SH ? lds64(base + 8u * (uint32_t)i) : p[i];
-}
-
 template <bool SH>
 __device__ __noinline__ void build_tiles(const double* Cg, const double* Hp, const double* wg, double* K,
                                          const unsigned short* tij, int T, int n, int ng, int ldc) {
@@ -657,9 +671,7 @@ __device__ void kkt_step(Qs& S, const double* rcv) {
   for (int r = threadIdx.x; r < S.m; r += blockDim.x)
     S.t[r] = (rcv[r] + S.lam[r] * S.rp[r]) / S.s[r];
   __syncthreads();
-  ct_apply(S, S.t, S.ctl);
-  __syncthreads();
-  for (int c = threadIdx.x; c < S.n; c += blockDim.x) S.rhs[c] = -S.rd[c] - S.ctl[c];
+  ct_apply<true>(S, S.t, S.rhs);  // rhs = -rd - C' t
   __syncthreads();
   qmark(S, 10);
   reduced_solve(S, S.rhs, S.du);
