@@ -286,7 +286,10 @@ __device__ void ct_apply(const Qs& S, const double* tv, double* out) {
     const double v = (s0 + s1) + (s2 + s3);
     out[c] = RHS ? -S.rd[c] - v : v;
   }
-  for (int e = threadIdx.x; e < S.ne; e += blockDim.x) {
+  // eliminated variables on the threads the kept loop leaves idle
+  int e = (int)threadIdx.x - S.nf % (int)blockDim.x;
+  if (e < 0) e += blockDim.x;
+  for (; e < S.ne; e += blockDim.x) {
     const int c = S.eidx[e];
     double s0 = 0.0;
     for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
@@ -482,7 +485,7 @@ __device__ __noinline__ void build_tiles(const double* Cg, const double* Hp, con
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int i = lane >> 2, p = lane & 3;
   const int ntiles = T * (T + 1) / 2;
-  constexpr int U = 3;  // tiles in flight per warp
+  constexpr int U = 2;  // tiles in flight per warp (A/B on one box: 2 < 3 < 4 < 5)
   for (int t0 = wid; t0 < ntiles; t0 += U * kQpWarps) {
     int r[U], ca[U], ra[U], rbc[U];
     double ma[U], mb[U], h0[U], h1[U];
