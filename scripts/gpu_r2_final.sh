@@ -18,7 +18,7 @@ PY
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg3.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-legs > /dev/null 2>&1; echo "ncu launches cfg3 rc=$?"
 for w in cfg4 cfg5; do timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$w.csv python bench.py --workload $w --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo "ncu launches $w rc=$?"; done
 # full captures: cfg3 kernels; K-COND at cfg4 / cfg5
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_solve_qp|k_condense_tmap|k_fwd_chain_mma|k_jac_phi_tc|k_jac_psi_tc|k_lin_self|k_lin_c" -c 7 -o gpurun_out/full_cfg3 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-legs > /dev/null 2>&1; echo "ncu full cfg3 rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_solve_qp|k_condense_tmap|k_fwd_chain_mma|k_jac_phi_tc|k_jac_psi_tc|k_lin_self|k_lin_c" -c 8 -o gpurun_out/full_cfg3 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-legs > /dev/null 2>&1; echo "ncu full cfg3 rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_condense_tmap|k_rollout" -c 2 -o gpurun_out/full_cfg4 python bench.py --workload cfg4 --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo "ncu full cfg4 rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_condense_tmap|k_rollout" -c 2 -o gpurun_out/full_cfg5 python bench.py --workload cfg5 --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo "ncu full cfg5 rc=$?"
 ls -la gpurun_out/*.csv gpurun_out/*.ncu-rep
