@@ -271,6 +271,41 @@ __global__ void k_lin_self(const LinDims d, float dtf, const int* __restrict__ p
   }
 }
 
+// k_lin_self for the reference architecture (nx = nu = 6, n_p = 3): constant
+// index divisions, and the inverse normalisation scales formed once per block
+// in shared memory (the generic kernel divides in fp64 in every thread)
+template <int NX, int NU, int NP>
+__global__ void __launch_bounds__(256) k_lin_self_t(const LinDims d, float dtf, const int* __restrict__ ptr,
+                                                    const double* __restrict__ norm, const float* __restrict__ jphi,
+                                                    const float* __restrict__ Pe, float* a_self, float* b) {
+  constexpr int W = NX + NU;
+  __shared__ float inv[W];
+  if (threadIdx.x < NX) inv[threadIdx.x] = (float)(1.0 / norm[NX + threadIdx.x]);
+  else if (threadIdx.x < W) inv[threadIdx.x] = (float)(1.0 / norm[2 * NX + NU + (threadIdx.x - NX)]);
+  __syncthreads();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d.Rn * NP * W) return;
+  const int rn = t / (NP * W);
+  const int rem = t - rn * (NP * W), r = rem / W, cc = rem - r * W;
+  const int p = rn / d.nN;
+  const int i = d.lo + (rn - p * d.nN);
+  const float* jr = jphi + (rn * NP + r) * d.nin;
+  if (cc < NX) {
+    float s = 0.f;
+    for (int e = ptr[i]; e < ptr[i + 1]; ++e) s += Pe[((p * d.nE + (e - d.e0)) * NP + r) * NX + cc];
+    const float dvdx = (jr[cc] + s) * inv[cc] + (cc == NP + r ? 1.f : 0.f);
+    float* blk = a_self + (p * d.M + i) * (int64_t)(NX * NX);
+    blk[r * NX + cc] = (r == cc ? 1.f : 0.f) + dtf * dvdx;
+    blk[(NP + r) * NX + cc] = dvdx;
+  } else {
+    const int cu = cc - NX;
+    const float jv = jr[NX + d.n_m + cu] * inv[cc];
+    float* blk = b + (p * d.M + i) * (int64_t)(NX * NU);
+    blk[r * NU + cu] = dtf * jv;
+    blk[(NP + r) * NU + cu] = jv;
+  }
+}
+
 // affine offset in fp64 from the stored fp32 blocks (gnn.py:291-297)
 __global__ void k_lin_c(const LinDims d, int E, const int* __restrict__ ptr, const int* __restrict__ src,
                         const double* __restrict__ X, const double* __restrict__ U, const double* __restrict__ f,
@@ -1303,8 +1338,12 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
     k_lin_nbr<<<grid_for(Rv * nx), 256, 0, st>>>(d, (float)ctx->dt, ctx->d_norm, Pe, (int)ctx->E, a_nbr);
     GM_LAUNCH_CHECK(ctx, "k_lin_nbr");
   }
-  k_lin_self<<<grid_for(Rj * (nx + d.nu)), 256, 0, st>>>(d, (float)ctx->dt, ctx->d_ptr, ctx->d_norm, jphi, Pe,
-                                                        a_self, b);
+  if (nx == 6 && d.nu == 6 && d.n_p == 3)
+    k_lin_self_t<6, 6, 3><<<grid_for(Rj * (nx + d.nu)), 256, 0, st>>>(d, (float)ctx->dt, ctx->d_ptr, ctx->d_norm,
+                                                                       jphi, Pe, a_self, b);
+  else
+    k_lin_self<<<grid_for(Rj * (nx + d.nu)), 256, 0, st>>>(d, (float)ctx->dt, ctx->d_ptr, ctx->d_norm, jphi, Pe,
+                                                          a_self, b);
   GM_LAUNCH_CHECK(ctx, "k_lin_self");
   k_lin_c<<<grid_for(d.Rn * nx), 256, 0, st>>>(d, (int)ctx->E, ctx->d_ptr, ctx->d_src, X, U, fb, a_self, a_nbr,
                                                b, c);
