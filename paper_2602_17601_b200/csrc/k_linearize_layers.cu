@@ -333,6 +333,37 @@ __global__ void k_lin_c(const LinDims d, int E, const int* __restrict__ ptr, con
   c[(p * d.M + i) * nx + r] = s;
 }
 
+// k_lin_c for nx = nu = 6: constant index divisions, unrolled fp64 products
+template <int NX, int NU>
+__global__ void __launch_bounds__(256) k_lin_c_t(const LinDims d, int E, const int* __restrict__ ptr,
+                                                 const int* __restrict__ src, const double* __restrict__ X,
+                                                 const double* __restrict__ U, const double* __restrict__ f,
+                                                 const float* __restrict__ a_self, const float* __restrict__ a_nbr,
+                                                 const float* __restrict__ b, double* c) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d.Rn * NX) return;
+  const int rn = t / NX;
+  const int r = t - rn * NX;
+  const int p = rn / d.nN;
+  const int i = d.lo + (rn - p * d.nN);
+  const double* Xp = X + p * (int64_t)d.M * NX;
+  const double* xi = Xp + (int64_t)i * NX;
+  const float* As = a_self + ((p * d.M + i) * NX + r) * NX;
+  double s = f[t];
+#pragma unroll
+  for (int k = 0; k < NX; ++k) s -= (double)As[k] * xi[k];
+  const float* Bs = b + ((p * d.M + i) * NX + r) * NU;
+#pragma unroll
+  for (int k = 0; k < NU; ++k) s -= (double)Bs[k] * U[p * NU + k];
+  for (int e = ptr[i]; e < ptr[i + 1]; ++e) {
+    const float* An = a_nbr + ((p * E + e) * NX + r) * NX;
+    const double* xj = Xp + (int64_t)src[e] * NX;
+#pragma unroll
+    for (int k = 0; k < NX; ++k) s -= (double)An[k] * xj[k];
+  }
+  c[(p * d.M + i) * NX + r] = s;
+}
+
 // ---------------------------------------------------------------------------
 // Fused backward Jacobian chains (fp32): seed + every layer of the phi
 // Jacobian (mlp_jacobian, mlp.py:132-145) and of the psi VJP, ONE launch each,
@@ -1345,8 +1376,12 @@ int layers_chunk(gm_ctx* ctx, int64_t P, const double* X, const double* U, float
     k_lin_self<<<grid_for(Rj * (nx + d.nu)), 256, 0, st>>>(d, (float)ctx->dt, ctx->d_ptr, ctx->d_norm, jphi, Pe,
                                                           a_self, b);
   GM_LAUNCH_CHECK(ctx, "k_lin_self");
-  k_lin_c<<<grid_for(d.Rn * nx), 256, 0, st>>>(d, (int)ctx->E, ctx->d_ptr, ctx->d_src, X, U, fb, a_self, a_nbr,
-                                               b, c);
+  if (nx == 6 && d.nu == 6)
+    k_lin_c_t<6, 6><<<grid_for(d.Rn * nx), 256, 0, st>>>(d, (int)ctx->E, ctx->d_ptr, ctx->d_src, X, U, fb, a_self,
+                                                         a_nbr, b, c);
+  else
+    k_lin_c<<<grid_for(d.Rn * nx), 256, 0, st>>>(d, (int)ctx->E, ctx->d_ptr, ctx->d_src, X, U, fb, a_self, a_nbr,
+                                                 b, c);
   GM_LAUNCH_CHECK(ctx, "k_lin_c");
   return GM_OK;
 }
