@@ -181,3 +181,67 @@ def test_rollout_epilogue_rejects_node_range_and_dims():
                      None, None, None, None, None)
     finally:
         ctx.call("gm_set_node_range", 0, 12)
+
+
+def test_rollout_epilogue_abi_statuses_and_damping():
+    """gm_mpc_finish_rollout against gm_mpc_finish through the C ABI on the
+    same synthetic blocks, solution and statuses (optimal / primal infeasible
+    -> fallback plan / max iterations), with damping 0.5 and the
+    hold-previous-input fallback: identical inputs, identical fallback rows,
+    planned / shifted trajectories within fp32 block rounding."""
+    import torch
+
+    from paper_2602_17601_b200 import device as dev
+    from paper_2602_17601_b200._runtime import lib
+    from paper_2602_17601_b200.graph import mesh_topology
+
+    topo = mesh_topology(7, 5)
+    M, N, B, nx, nu = topo.node_count, 6, 3, 6, 6
+    eng = dev.engine(topo)
+    eng.set_dims(nx, nu)
+    rng = np.random.default_rng(17)
+    E = eng.E
+    f32, f64 = np.float32, np.float64
+    a_self = eng.h2d((rng.standard_normal((B * N, M, nx, nx)) * 0.2 + np.eye(nx) * 0.9).astype(f32), f32)
+    a_nbr = eng.h2d((rng.standard_normal((B * N, E, nx, nx)) * 0.1).astype(f32), f32)
+    b = eng.h2d(rng.standard_normal((B * N, M, nx, nu)).astype(f32), f32)
+    c = eng.h2d(rng.standard_normal((B * N, M, nx)) * 0.1, f64)
+    x0 = eng.h2d(rng.standard_normal((B, M, nx)), f64)
+    ld = lib().gm_gamma_ld(N, nu)
+    W = eng.zeros((B, M, N + 1, nx, ld), f32)
+    sp = eng.stream_ptr()
+    eng.ctx.call("gm_condense_gammas", B, N, a_self.data_ptr(), a_nbr.data_ptr(), b.data_ptr(), c.data_ptr(),
+                 x0.data_ptr(), W.data_ptr(), ld, sp)
+    n = N * nu + 4  # solution rows carry trailing slacks like the expanded QP
+    u = eng.h2d(rng.standard_normal((B, n)) * 0.3, f64)
+    status = torch.tensor([0, 2, 1], dtype=torch.int32, device=u.device)
+    iters = torch.tensor([7, 9, 50], dtype=torch.int32, device=u.device)
+    lin_s = eng.h2d(rng.standard_normal((B, N + 1, M, nx)), f64)
+    lin_u = eng.h2d(rng.standard_normal((B, N, nu)), f64)
+    fb_s = eng.h2d(rng.standard_normal((B, N + 1, M, nx)), f64)
+    fb_u = eng.h2d(rng.standard_normal((B, N, nu)), f64)
+    u_prev = eng.h2d(rng.standard_normal((B, nu)), f64)
+
+    def outs():
+        return [eng.zeros(s, f64) for s in ((B, N + 1, M, nx), (B, M, N + 1, nx), (B, N, nu), (B, N + 1, M, nx),
+                                            (B, N, nu), (B, nu), (B, nu + 2))]
+
+    def tail(o):
+        return (status.data_ptr(), iters.data_ptr(), lin_s.data_ptr(), lin_u.data_ptr(), fb_s.data_ptr(),
+                fb_u.data_ptr(), 0.5, 0, u_prev.data_ptr(), 1, *[t.data_ptr() for t in o], sp)
+
+    o1, o2 = outs(), outs()
+    eng.ctx.call("gm_mpc_finish", B, N, W.data_ptr(), ld, u.data_ptr(), n, *tail(o1))
+    eng.ctx.call("gm_mpc_finish_rollout", B, N, a_self.data_ptr(), a_nbr.data_ptr(), b.data_ptr(), c.data_ptr(),
+                 x0.data_ptr(), u.data_ptr(), n, *tail(o2))
+    torch.cuda.synchronize()
+    r1, r2 = [[t.cpu().numpy() for t in o] for o in (o1, o2)]
+    for k in (2, 4, 5, 6):  # inputs, u_applied, summary: no Gamma involved -> identical
+        assert np.array_equal(r1[k], r2[k]), k
+    fb = fb_s.cpu().numpy()
+    for k in (0, 3):  # cur / next states: the failed instance takes the fallback plan exactly
+        assert np.array_equal(r1[k][1], r2[k][1])
+    assert np.array_equal(r2[0][1], fb[1])
+    for k in (0, 1, 3):
+        scale = np.max(np.abs(r1[k]))
+        assert np.max(np.abs(r1[k] - r2[k])) / scale <= 1e-5, k
