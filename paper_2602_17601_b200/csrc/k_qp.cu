@@ -52,9 +52,10 @@ struct QpLayout {
 // m-vectors: d s lam cu rp t dl ds tmp w lb rval              (12)
 // ng-vectors (after the row classification): wg ga cf         (3)
 // nf: dimension of the factorised system, <= n.  K: lower 8x8 tiles of the
-// padded Schur matrix (qp_chol.cuh), overwritten by X = L^{-1} after the
-// factorisation; X region: inverted diagonal tiles, per-warp scratch tiles,
-// 1/diag(L), the padded solve vector and its staging copy.
+// padded Schur matrix (qp_chol.cuh), overwritten by its Cholesky factor L;
+// X region: the inverted diagonal tiles of L, per-warp scratch tiles (the
+// coupling tiles of the 16x16 block inverses of solve_mw16), 1/diag(L), the
+// padded solve vector and its staging copy.
 __host__ __device__ inline size_t xregion_doubles(int nf) {
   const size_t T = qpchol::tiles_for(nf);
   return T * qpchol::kTS + 64 * kQpWarps + 24 * T;
@@ -172,7 +173,8 @@ __device__ double block_reduce(double v, double* red) {
 
 // ---------------------------------------------------------------------------
 // factorisation and solves (qp_chol.cuh): tiled Cholesky of the reduced Schur
-// matrix, X = L^{-1} in place, triangular solves as two parallel mat-vecs
+// matrix, blocked substitution solves (solve_mw16; X = L^{-1} variants behind
+// QP_SOLVE_XXT)
 // ---------------------------------------------------------------------------
 // Packed lower triangle of H, column-major: element (r, c), r >= c, at
 // colbase(c, n) + r.
