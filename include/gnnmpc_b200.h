@@ -65,6 +65,9 @@ int gm_abi_version(void);
 /* Number of kernels this library has launched in the process (all
  * contexts); bench.py reports the per-step delta as gpu_launches. */
 int64_t gm_launch_count(void);
+/* Elapsed ms between consecutive completed CUDA events: out[i] = ev[i] ->
+ * ev[i+1], i < n - 1 (the step's stage times in one call). */
+int gm_event_times(int n, void* const* events, float* out);
 
 /* Context.  device < 0 creates a host-only context: graph index
  * construction works, every device entry point returns GM_ERR_CONFIG. */

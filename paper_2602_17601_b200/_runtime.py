@@ -43,6 +43,7 @@ class QpSettingsC(ctypes.Structure):
 _SIGNATURES = {
     "gm_abi_version": (c_int, []),
     "gm_launch_count": (c_i64, []),
+    "gm_event_times": (c_int, [c_int, P, P]),
     "gm_create": (c_int, [ctypes.POINTER(c_void_p), c_int]),
     "gm_destroy": (None, [c_void_p]),
     "gm_last_error": (ctypes.c_char_p, [c_void_p]),

@@ -67,6 +67,17 @@ int gm_abi_version(void) { return 1; }
 
 int64_t gm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+// elapsed times between consecutive recorded events (ms): out[i] = t(ev[i+1]) -
+// t(ev[i]), i < n - 1; the events must have completed.  One call for a step's
+// stage times (StepTiming) instead of one host round trip per pair.
+int gm_event_times(int n, void* const* events, float* out) {
+  if (n < 2 || !events || !out) return GM_ERR_CONFIG;
+  for (int i = 0; i + 1 < n; ++i)
+    if (cudaEventElapsedTime(&out[i], (cudaEvent_t)events[i], (cudaEvent_t)events[i + 1]) != cudaSuccess)
+      return GM_ERR_CUDA;
+  return GM_OK;
+}
+
 int gm_create(gm_ctx** out, int device) {
   if (!out) return GM_ERR_CONFIG;
   gm_ctx* c = new gm_ctx();

@@ -158,11 +158,16 @@ class StepPlan:
         e = eng.empty
         # static inputs
         self.x_meas = e((M, nx), f64)
-        self.ls = e((N + 1, M, nx), f64)    # linearisation trajectory, [0] = x_measured
-        self.li = e((N, nu), f64)
+        # [lin_states | lin_inputs | u_prev] in one buffer, laid out like the
+        # tail [next_states | next_inputs | u_applied] of the output snapshot,
+        # so a state this function returned comes back in with one copy
+        a, b = (N + 1) * M * nx, N * nu
+        self.inbuf = eng.zeros((a + b + nu,), f64)
+        self.ls = self.inbuf[:a].view(N + 1, M, nx)  # linearisation trajectory, [0] = x_measured
+        self.li = self.inbuf[a:a + b].view(N, nu)
         self.fb_states = self.ls            # RTI: fallback plan == input plan
         self.fb_inputs = self.li
-        self.u_prev = eng.zeros((nu,), f64)  # zeros == "no previous input" (mpc.py:413)
+        self.u_prev = self.inbuf[a + b:]    # zeros == "no previous input" (mpc.py:413)
         # scratch
         self.a_self = e((N, M, nx, nx), f32)
         self.a_nbr = e((N, max(E, 1), nx, nx), f32)
@@ -189,24 +194,26 @@ class StepPlan:
         # static outputs; the four arrays a new MpcState keeps live in one
         # buffer so the state is snapshotted with a single device copy
         self.cur = e((N + 1, M, nx), f64)
-        sizes = [M * (N + 1) * nx, N * nu, (N + 1) * M * nx, N * nu]
+        sizes = [M * (N + 1) * nx, N * nu, (N + 1) * M * nx, N * nu, nu]
         self.outbuf = e((sum(sizes),), f64)
+        self.in_off = sizes[0] + sizes[1]   # where [next_states | next_inputs | u_applied] starts
         self.out_views = self._carve(self.outbuf)
-        self.planned_states, self.planned_inputs, self.next_states, self.next_inputs = self.out_views
-        self.u_applied = e((nu,), f64)
+        (self.planned_states, self.planned_inputs, self.next_states, self.next_inputs,
+         self.u_applied) = self.out_views
         self.summary = e((nu + 2,), f64)
         self.host_summary = torch.empty((nu + 2,), dtype=torch.float64, pin_memory=True)
         self.host_x = torch.empty((M, nx), dtype=torch.float64, pin_memory=True)
         # external timing events: recorded as event nodes inside the step graph
         self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
+        self._ev_handles = None
         self.graphs = None
         self.graph = None
         self.settings_c = settings_c(cfg.solver)
 
     def _carve(self, buf):
         M, N, nx, nu = self.M, self.N, self.nx, self.nu
-        sizes = [M * (N + 1) * nx, N * nu, (N + 1) * M * nx, N * nu]
-        shapes = [(M, N + 1, nx), (N, nu), (N + 1, M, nx), (N, nu)]
+        sizes = [M * (N + 1) * nx, N * nu, (N + 1) * M * nx, N * nu, nu]
+        shapes = [(M, N + 1, nx), (N, nu), (N + 1, M, nx), (N, nu), (nu,)]
         out, o = [], 0
         for sz, sh in zip(sizes, shapes):
             out.append(buf[o:o + sz].view(sh))
@@ -309,8 +316,19 @@ class StepPlan:
             self._issue(self.groups(), eager=True, timed=timed)
 
     def stage_ms(self):
-        ev = self.events
-        return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])
+        """(linearize, condense, solve) ms of the last run: one C call for the
+        three event pairs (gm_event_times)."""
+        import ctypes
+
+        if self._ev_handles is None:
+            self._ev_handles = (ctypes.c_void_p * 4)(*[e.cuda_event for e in self.events])
+            self._ev_out = (ctypes.c_float * 3)()
+        rc = lib().gm_event_times(4, ctypes.addressof(self._ev_handles), ctypes.addressof(self._ev_out))
+        if rc != 0:
+            ev = self.events
+            return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])
+        o = self._ev_out
+        return float(o[0]), float(o[1]), float(o[2])
 
 
 _MAX_PLANS = 16
@@ -396,19 +414,27 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
     # the whole-step graph reads the measurement from the pinned host buffer;
     # a device-resident measurement goes through the per-group graphs
     whole = graphable and plan.graph is not None and not x_on_device
+    # a state this plan returned: its trajectory, inputs and last applied input
+    # are one contiguous piece of its snapshot -> one device copy
+    snap = getattr(state, "_snapshot", None)
+    fast = (snap is not None and snap[1] is plan and _field(state, "lin_states") is snap[2]
+            and lin_in_prev is snap[3] and _field(state, "last_applied") is snap[4])
     if whole:  # the step graph does the H2D from the pinned buffer and ls[0]
         plan.host_x.numpy()[...] = np.asarray(x_measured.array, dtype=float).reshape(plan.host_x.shape)
-        _copy_in(plan.ls, _field(state, "lin_states"))
     else:
         _copy_in(plan.x_meas, x_measured.array, plan.host_x)
-        _copy_in(plan.ls, _field(state, "lin_states"))
-        plan.ls[0].copy_(plan.x_meas)
-    _copy_in(plan.li, lin_in_prev)
-    prev = _field(state, "last_applied")
-    if prev is None:
-        plan.u_prev.zero_()
+    if fast:
+        plan.inbuf.copy_(snap[0][plan.in_off:])
     else:
-        _copy_in(plan.u_prev, prev)
+        _copy_in(plan.ls, _field(state, "lin_states"))
+        _copy_in(plan.li, lin_in_prev)
+        prev = _field(state, "last_applied")
+        if prev is None:
+            plan.u_prev.zero_()
+        else:
+            _copy_in(plan.u_prev, prev)
+    if not whole:
+        plan.ls[0].copy_(plan.x_meas)
 
     timing = StepTiming()
     total_iters = 0
@@ -458,13 +484,19 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
         filtered = u_app.copy()
         last_applied = u_app.copy()
     else:
-        last_applied = plan.u_applied.clone()
-    planned_states, planned_inputs, next_states, next_inputs = plan._carve(plan.outbuf.clone())
+        last_applied = None
+    snap = plan.outbuf.clone()  # one device copy: the new state owns it
+    planned_states, planned_inputs, next_states, next_inputs, u_applied = plan._carve(snap)
+    if last_applied is None:
+        last_applied = u_applied
     new_state = MpcState(lin_states=next_states, lin_inputs=next_inputs,
                          step_count=state.step_count + 1, last_applied=last_applied,
                          planned_states=planned_states, planned_inputs=planned_inputs,
                          last_status=STATUS_BY_CODE[status_code], last_iterations=total_iters,
                          last_timing=timing, filtered_input=filtered)
+    # private: lets the next call on this plan load [trajectory | inputs |
+    # last input] with one copy (checked against the fields it then reads)
+    object.__setattr__(new_state, "_snapshot", (snap, plan, next_states, next_inputs, u_applied))
     timing.total_ms = (time.perf_counter() - t_start) * 1e3
     return InputVector(u_app), new_state
 

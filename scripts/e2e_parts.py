@@ -43,3 +43,6 @@ print("InputVector       us", t(lambda: pkg.InputVector(np.zeros(6))))
 print("stream sync idle  us", t(lambda: torch.cuda.current_stream(dev).synchronize()))
 print("mpc_step total    us", t(lambda: pkg.mpc_step(model, topo, spec, xs, state, cfg), n=300))
 print("graph replay+sync us", t(lambda: (plan.graph.replay(), torch.cuda.current_stream(dev).synchronize()), n=300))
+ev = plan.events
+print("torch elapsed     ", ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]))
+print("gm_event_times    ", plan.stage_ms())
