@@ -150,6 +150,7 @@ def test_fused_matches_two_kernel_path(graph, N, nx, nu, B, mode):
     ("chain1000", 20, 2, 4),   # 384-thread pipeline, tile slots double-buffered by item
     ("chain301", 16, 2, 4),    # M not a multiple of the 8-node item, ld = 128 with 98 live
     ("chain600", 15, 1, 4),    # ld = 96
+    ("chain600", 25, 1, 6),    # N = 25: 325 block pairs > 256 -> the two-kernel path (K-REC + K-HG)
     ("mesh", 16, 2, 5),        # 512-thread pipeline (degree 4), single tile slot, global H fold
     ("local", 20, 2, 5),       # irregular degree <= 5 (neighbours within +-8), isolated nodes
     ("random", 20, 1, 1),      # neighbours anywhere: the unique-neighbour tile ring
