@@ -127,3 +127,19 @@ def test_partitioned_step_native_transport_graph(transport):
 
     assert STATUS_BY_CODE[st_e].value == ref["status"]
     assert np.max(np.abs(u_e - ref["u_applied"])) / max(1.0, np.max(np.abs(ref["u_applied"]))) <= 1e-4
+
+
+def test_capture_requires_stream_ordered_transport():
+    """A world > 1 step can only be captured with the native transport: the
+    in-process / torch.distributed transports wait on the host."""
+    from paper_2602_17601_b200 import MpcConfig, workloads
+    from paper_2602_17601_b200.errors import ConfigurationError
+    from paper_2602_17601_b200.partition import LocalHub, LocalTransport, PartitionedMpc, partition_nodes
+
+    N = 4
+    topo, model, states, inputs, spec = workloads.mesh_problem(6, 5, N, 0.01, 2)
+    part = partition_nodes(topo, 2, 0)
+    pm = PartitionedMpc(model, topo, spec, MpcConfig(horizon=N, dt=0.01), part,
+                        transport=LocalTransport(LocalHub(2), 0))
+    with pytest.raises(ConfigurationError):
+        pm.capture()
