@@ -1100,15 +1100,17 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     // Schur matrix and Cholesky with escalating regularisation (qpsolver.py:178-198)
     for (int r = tid; r < m; r += nt) S.w[r] = S.lam[r] / S.s[r];
     __syncthreads();
-    bool ok = build_k(S, reg, true);
-    qmark(S, 3);
-    ok = ok && chol_factor(S);
-    qmark(S, 4);
+    // build + factor with escalating regularisation: one copy in the code
+    bool ok = false;
     double boost = 0.0;
-    for (int att = 1; att < 4 && !ok; ++att) {
-      const double bump = boost == 0.0 ? fmax(reg * 1e3, 1e-12) : boost * 1e3;
-      boost = bump;
-      ok = build_k(S, reg + boost, true) && chol_factor(S);
+#pragma unroll 1
+    for (int att = 0; att < 4; ++att) {
+      if (att > 0) boost = boost == 0.0 ? fmax(reg * 1e3, 1e-12) : boost * 1e3;
+      ok = build_k(S, reg + boost, true);
+      if (att == 0) qmark(S, 3);
+      ok = ok && chol_factor(S);
+      if (att == 0) qmark(S, 4);
+      if (ok) break;
     }
     if (!ok) {
       status = GM_QP_NUMERICAL_FAILURE;
@@ -1126,24 +1128,27 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
       mu_loc += S.lam[r] * S.s[r];
     }
     const double mu = block_reduce<2>(mu_loc, red) / m;
-    // affine direction: rc = -lam s
+    // affine direction (rc = -lam s), then the corrector with centring (rc =
+    // -lam s - dlam_a ds_a + sigma mu): one copy of the KKT step in the code,
+    // run twice (the instruction working set of an iteration)
     for (int r = tid; r < m; r += nt) S.tmp[r] = -S.lam[r] * S.s[r];
     __syncthreads();
     qmark(S, 6);
-    kkt_step(S, S.tmp);
-    qmark(S, 7);
-    const double ap = max_step(S, S.s, S.ds);
-    const double ad = max_step(S, S.lam, S.dl);
-    double maff = 0.0;
-    for (int r = tid; r < m; r += nt) maff += (S.lam[r] + ad * S.dl[r]) * (S.s[r] + ap * S.ds[r]);
-    const double mu_aff = block_reduce<2>(maff, red) / m;
-    const double sigma = mu > 0.0 ? (mu_aff / mu) * (mu_aff / mu) * (mu_aff / mu) : 0.0;
-    // corrector with centring: rc = -lam s - dlam_a ds_a + sigma mu
-    for (int r = tid; r < m; r += nt) S.tmp[r] = -S.lam[r] * S.s[r] - S.dl[r] * S.ds[r] + sigma * mu;
-    __syncthreads();
-    qmark(S, 8);
-    kkt_step(S, S.tmp);
-    qmark(S, 7);
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      kkt_step(S, S.tmp);
+      qmark(S, 7);
+      if (pass == 1) break;
+      const double ap = max_step(S, S.s, S.ds);
+      const double ad = max_step(S, S.lam, S.dl);
+      double maff = 0.0;
+      for (int r = tid; r < m; r += nt) maff += (S.lam[r] + ad * S.dl[r]) * (S.s[r] + ap * S.ds[r]);
+      const double mu_aff = block_reduce<2>(maff, red) / m;
+      const double sigma = mu > 0.0 ? (mu_aff / mu) * (mu_aff / mu) * (mu_aff / mu) : 0.0;
+      for (int r = tid; r < m; r += nt) S.tmp[r] = -S.lam[r] * S.s[r] - S.dl[r] * S.ds[r] + sigma * mu;
+      __syncthreads();
+      qmark(S, 8);
+    }
     const double alpha = fmin(tau * max_step(S, S.s, S.ds), tau * max_step(S, S.lam, S.dl));
     bool finite = true;
     for (int c = tid; c < n; c += nt) {
