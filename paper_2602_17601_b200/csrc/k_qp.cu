@@ -467,17 +467,15 @@ __device__ void h_apply_rows(const Qs& S, const double* uv, double* out) {
 //   K_ee = 2 H_ee + diag_add + sum_single w val^2 + w_g a^2,
 //   K_red = K_kk - K_ke K_ee^{-1} K_ek  =  ... + w'_g Cg_g' Cg_g,
 //   w'_g = w_g - (w_g a)^2 / K_ee            (a rank-one change per such row).
-// Lower triangle of K_red in 4x4 register tiles: tile (I, J), I >= J, covers
-// rows 4I..4I+3 and columns 4J..4J+3; its 16 entries of H are loaded first,
-// then the rank-ng update runs with 16 independent accumulators.  Returns
-// false when an eliminated pivot K_ee is not positive (potrf's failure rule
-// applied to the eliminated block).
+// build_k returns false when an eliminated pivot K_ee is not positive
+// (potrf's failure rule applied to the eliminated block).
 // Lower 8x8 tiles of 2H + Cg' diag(wg) Cg on the fp64 tensor cores: the C
 // fragment (row i, cols 2p, 2p+1) starts from 2H, ng/4 DMMAs add the general
 // rows (A[i][g] = wg_g Cg[g][row], B[g][j] = Cg[g][col]); padding rows / cols
 // (>= n) become the identity.  One warp per tile, U tiles in flight.  The
-// operand loads are branch-free (clamped indices, 0/1 masks folded into the
-// products) with 32-bit offsets; SH: H, Cg and wg are in shared memory.
+// operand loads are branch-free with 32-bit offsets: padding rows / cols read
+// a clamped (finite) index, which only touches C entries of that padding row /
+// col, overwritten afterwards; SH: H, Cg and wg are in shared memory.
 template <bool SH>
 __device__ __noinline__ void build_tiles(const double* Cg, const double* Hp, const double* wg, double* K,
                                          const unsigned short* tij, int T, int n, int ng, int ldc) {
