@@ -269,21 +269,25 @@ __device__ __forceinline__ double ldv(const double* p, uint32_t base, int i) {
 // RHS: write -rd - (C' tv) instead (the KKT right-hand side, fused)
 template <bool RHS = false>
 __device__ void ct_apply(const Qs& S, const double* tv, double* out) {
+#pragma unroll 1
   for (int k = threadIdx.x; k < S.nf; k += blockDim.x) {
     const int c = S.kidx[k];
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll 1
     for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
       const int r = S.colrows[q];
       s0 = fma(S.rval[r], tv[r], s0);
     }
     const double* cg = S.Cg + k;
     int gi = 0;
+#pragma unroll 1
     for (; gi + 3 < S.ng; gi += 4) {
       s0 = fma(cg[(int64_t)gi * S.n], tv[S.grow[gi]], s0);
       s1 = fma(cg[(int64_t)(gi + 1) * S.n], tv[S.grow[gi + 1]], s1);
       s2 = fma(cg[(int64_t)(gi + 2) * S.n], tv[S.grow[gi + 2]], s2);
       s3 = fma(cg[(int64_t)(gi + 3) * S.n], tv[S.grow[gi + 3]], s3);
     }
+#pragma unroll 1
     for (; gi < S.ng; ++gi) s0 = fma(cg[(int64_t)gi * S.n], tv[S.grow[gi]], s0);
     const double v = (s0 + s1) + (s2 + s3);
     out[c] = RHS ? -S.rd[c] - v : v;
@@ -294,6 +298,7 @@ __device__ void ct_apply(const Qs& S, const double* tv, double* out) {
   for (; e < S.ne; e += blockDim.x) {
     const int c = S.eidx[e];
     double s0 = 0.0;
+#pragma unroll 1
     for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
       const int r = S.colrows[q];
       s0 = fma(S.rval[r], tv[r], s0);
@@ -309,6 +314,7 @@ __device__ void ct_apply(const Qs& S, const double* tv, double* out) {
 __device__ void c_apply(const Qs& S, const double* xv, double* out) {
   constexpr int G = 8;
   const int lg = threadIdx.x & (G - 1), grp = threadIdx.x / G;
+#pragma unroll 1
   for (int r = threadIdx.x; r < S.m; r += blockDim.x)
     if (S.rcol[r] >= 0) out[r] = S.rval[r] * xv[S.rcol[r]];
   for (int g0 = 0; g0 < S.ng; g0 += kQpThreads / G) {
@@ -317,6 +323,7 @@ __device__ void c_apply(const Qs& S, const double* xv, double* out) {
     if (gi < S.ng) {
       const double* row = S.Cg + (int64_t)gi * S.n;
       int k = lg;
+#pragma unroll 1
       for (; k + G < S.nf; k += 2 * G) {
         s = fma(row[k], xv[S.kidx[k]], s);
         s1 = fma(row[k + G], xv[S.kidx[k + G]], s1);
@@ -343,20 +350,18 @@ __device__ void c_apply(const Qs& S, const double* xv, double* out) {
 // are added in a fixed order.  Call with all threads; out is complete after
 // the call's final barrier.
 __device__ void h_apply_rows(const Qs& S, const double* uv, double* out);
-__device__ void h_apply(const Qs& S, const double* uv, double* out) {
-  if (__isShared(S.Hp) && S.nf <= (int)blockDim.x && uv != out) {
-    h_apply_rows(S, uv, out);
-    return;
-  }
+// (out of line: the H-in-global-memory case, kept out of the hot code)
+__device__ __noinline__ void h_apply_cols(const double* Hp, const int* kidx, const int* eidx, const double* hde,
+                                          double* K, int n, int ne, const double* uv, double* out) {
   constexpr int TM = 8;  // n <= 256
-  const int n = S.nf, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* part = S.K;                      // NW x n row partials
-  double* colsum = S.K + kQpWarps * n;     // n upper-part sums
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* part = K;                        // NW x n row partials
+  double* colsum = K + kQpWarps * n;       // n upper-part sums
   double uk[TM], acc[TM];
 #pragma unroll
   for (int t = 0; t < TM; ++t) {
     const int r = lane + 32 * t;
-    uk[t] = r < n ? uv[S.kidx[r]] : 0.0;
+    uk[t] = r < n ? uv[kidx[r]] : 0.0;
     acc[t] = 0.0;
   }
   for (int c0 = wid; c0 < n; c0 += 4 * kQpWarps) {
@@ -366,8 +371,8 @@ __device__ void h_apply(const Qs& S, const double* uv, double* out) {
       const int c = c0 + q * kQpWarps;
       cs[q] = 0.0;
       if (c < n) {
-        const double uc = uv[S.kidx[c]];
-        const double* col = S.Hp + colbase(c, n);
+        const double uc = uv[kidx[c]];
+        const double* col = Hp + colbase(c, n);
 #pragma unroll
         for (int t = 0; t < TM; ++t) {
           const int r = lane + 32 * t;
@@ -397,14 +402,22 @@ __device__ void h_apply(const Qs& S, const double* uv, double* out) {
     if (r < n) part[wid * n + r] = acc[t];
   }
   __syncthreads();
+#pragma unroll 1
   for (int r = threadIdx.x; r < n; r += blockDim.x) {
     double v = colsum[r];
 #pragma unroll
     for (int w = 0; w < kQpWarps; ++w) v += part[w * n + r];
-    out[S.kidx[r]] = v;
+    out[kidx[r]] = v;
   }
-  for (int e = threadIdx.x; e < S.ne; e += blockDim.x) out[S.eidx[e]] = S.hde[e] * uv[S.eidx[e]];
+#pragma unroll 1
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) out[eidx[e]] = hde[e] * uv[eidx[e]];
   __syncthreads();
+}
+__device__ void h_apply(const Qs& S, const double* uv, double* out) {
+  if (__isShared(S.Hp) && S.nf <= (int)blockDim.x && uv != out)
+    h_apply_rows(S, uv, out);
+  else
+    h_apply_cols(S.Hp, S.kidx, S.eidx, S.hde, S.K, S.nf, S.ne, uv, out);
 }
 
 // out = H u with packed H on chip: one thread per kept row r, the row read
@@ -435,21 +448,25 @@ __device__ void h_apply_rows(const Qs& S, const double* uv, double* out) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int c = c_lo;
     const int cl = min(r, c_hi);
+#pragma unroll 1
     for (; c + 3 < cl; c += 4) {
       a0 = fma(hl(colbase(c, n) + r), uk[c], a0);
       a1 = fma(hl(colbase(c + 1, n) + r), uk[c + 1], a1);
       a2 = fma(hl(colbase(c + 2, n) + r), uk[c + 2], a2);
       a3 = fma(hl(colbase(c + 3, n) + r), uk[c + 3], a3);
     }
+#pragma unroll 1
     for (; c < cl; ++c) a0 = fma(hl(colbase(c, n) + r), uk[c], a0);
     const int colr = colbase(r, n);
     c = max(c, r);
+#pragma unroll 1
     for (; c + 3 < c_hi; c += 4) {
       a0 = fma(hl(colr + c), uk[c], a0);
       a1 = fma(hl(colr + c + 1), uk[c + 1], a1);
       a2 = fma(hl(colr + c + 2), uk[c + 2], a2);
       a3 = fma(hl(colr + c + 3), uk[c + 3], a3);
     }
+#pragma unroll 1
     for (; c < c_hi; ++c) a0 = fma(hl(colr + c), uk[c], a0);
     acc = (a0 + a1) + (a2 + a3);
   }
@@ -458,6 +475,7 @@ __device__ void h_apply_rows(const Qs& S, const double* uv, double* out) {
   __syncthreads();
   if (split && half == 0 && r < n) acc += part[r];
   if (half == 0 && r < n) out[S.kidx[r]] = acc;
+#pragma unroll 1
   for (int e = threadIdx.x; e < S.ne; e += blockDim.x) out[S.eidx[e]] = S.hde[e] * uv[S.eidx[e]];
   __syncthreads();
 }
@@ -551,11 +569,13 @@ __device__ __noinline__ void build_tiles(const double* Cg, const double* Hp, con
 __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
   const int n = S.nf, ng = terms ? S.ng : 0;
   bool ok = true;
+#pragma unroll 1
   for (int e = threadIdx.x; e < S.ne; e += blockDim.x) {
     const int c = S.eidx[e];
     double dsum = 0.0;
     if (terms)
-      for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
+  #pragma unroll 1
+    for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
         const int r = S.colrows[q];
         dsum += S.w[r] * S.rval[r] * S.rval[r];
       }
@@ -565,6 +585,7 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
     S.kee[e] = kee;
   }
   __syncthreads();
+#pragma unroll 1
   for (int gi = threadIdx.x; gi < ng; gi += blockDim.x) {
     const double wgi = S.w[S.grow[gi]];
     double wr = wgi;
@@ -587,11 +608,13 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
   // diagonal (holds only the general-row term so far): (2H + reg) +
   // bincount(single rows) first, then the general-row term, as the
   // reference orders it
+#pragma unroll 1
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const int c = S.kidx[k];
     double dsum = 0.0;
     if (terms)
-      for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
+  #pragma unroll 1
+    for (int q = S.colptr[c]; q < S.colptr[c + 1]; ++q) {
         const int r = S.colrows[q];
         dsum += S.w[r] * S.rval[r] * S.rval[r];
       }
@@ -607,6 +630,7 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
 // largest step in [0, 1] with x + a dx > 0 (qpsolver.py:238-243)
 __device__ double max_step(const Qs& S, const double* x, const double* dx) {
   double a = 1.0;
+#pragma unroll 1
   for (int r = threadIdx.x; r < S.m; r += blockDim.x)
     if (dx[r] < 0.0) a = fmin(a, -x[r] / dx[r]);
   return block_reduce<1>(a, S.red);
@@ -620,18 +644,22 @@ __device__ void reduced_solve(Qs& S, const double* b, double* x) {
   double* yr = S.ytmp;
   double* coef = S.cf;
   if (S.ne == 0) {
+#pragma unroll 1
     for (int k = threadIdx.x; k < S.nf; k += blockDim.x) yr[k] = b[S.kidx[k]];
     __syncthreads();
     chol_solve(S, yr, yr);
+#pragma unroll 1
     for (int k = threadIdx.x; k < S.nf; k += blockDim.x) x[S.kidx[k]] = yr[k];
     __syncthreads();
     return;
   }
+#pragma unroll 1
   for (int gi = threadIdx.x; gi < S.ng; gi += blockDim.x) {
     const int e = S.ge[gi];
     coef[gi] = e >= 0 ? S.w[S.grow[gi]] * S.ga[gi] * b[S.eidx[e]] / S.kee[e] : 0.0;
   }
   __syncthreads();
+#pragma unroll 1
   for (int k = threadIdx.x; k < S.nf; k += blockDim.x) {
     double s = b[S.kidx[k]];
     for (int gi = 0; gi < S.ng; ++gi) s = fma(-coef[gi], S.Cg[(int64_t)gi * S.n + k], s);
@@ -639,6 +667,7 @@ __device__ void reduced_solve(Qs& S, const double* b, double* x) {
   }
   __syncthreads();
   chol_solve(S, yr, yr);
+#pragma unroll 1
   for (int k = threadIdx.x; k < S.nf; k += blockDim.x) x[S.kidx[k]] = yr[k];
   // eliminated: one 8-lane group per eliminated variable, all groups at once
   constexpr int G = 8;
@@ -652,6 +681,7 @@ __device__ void reduced_solve(Qs& S, const double* b, double* x) {
       const double* row = S.Cg + (int64_t)gi * S.n;
       double s1 = 0.0;
       int k = lg;
+#pragma unroll 1
       for (; k + G < S.nf; k += 2 * G) {
         s = fma(row[k], yr[k], s);
         s1 = fma(row[k + G], yr[k + G], s1);
@@ -671,6 +701,7 @@ __device__ void reduced_solve(Qs& S, const double* b, double* x) {
 
 // du, dlam, ds for complementarity target rcv (qpsolver.py:204-209)
 __device__ void kkt_step(Qs& S, const double* rcv) {
+#pragma unroll 1
   for (int r = threadIdx.x; r < S.m; r += blockDim.x)
     S.t[r] = (rcv[r] + S.lam[r] * S.rp[r]) / S.s[r];
   __syncthreads();
@@ -681,6 +712,7 @@ __device__ void kkt_step(Qs& S, const double* rcv) {
   qmark(S, 11);
   c_apply(S, S.du, S.t);  // C du
   __syncthreads();
+#pragma unroll 1
   for (int r = threadIdx.x; r < S.m; r += blockDim.x) {
     const double ds = -S.rp[r] - S.t[r];
     S.ds[r] = ds;
@@ -702,11 +734,13 @@ __device__ Resid residuals(Qs& S) {
   c_apply(S, S.u, S.cu);
   __syncthreads();
   double a_rs = 0.0, a_rp = -INFINITY, a_rc = 0.0;
+#pragma unroll 1
   for (int c = threadIdx.x; c < S.n; c += blockDim.x) {
     const double rd = (2.0 * S.hu[c] + S.g[c]) + S.ctl[c];
     S.rd[c] = rd;
     a_rs = fmax(a_rs, fabs(rd));
   }
+#pragma unroll 1
   for (int r = threadIdx.x; r < S.m; r += blockDim.x) {
     const double viol = S.cu[r] - S.d[r];
     a_rp = fmax(a_rp, viol);
@@ -790,6 +824,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   // m or n: they cost ~100 us of L2/shared latency per solve).
   // Pass 1 over C: per-row nonzero count (rcol) and first nonzero column
   // (grow), by shared atomics.
+#pragma unroll 1
   for (int r = tid; r < m; r += nt) {
     S.rcol[r] = 0;
     S.grow[r] = n;
@@ -798,6 +833,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.colptr[c] = 0;
     S.cstart[c] = c * n - (c * (c - 1)) / 2;
   }
+#pragma unroll 1
   for (int c = tid; c < n; c += nt) S.elig[c] = m > 0 ? 1 : 0;
   __syncthreads();
   {
@@ -843,6 +879,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     }
   }
   __syncthreads();
+#pragma unroll 1
   for (int r = tid; r < m; r += nt) {
     const int cnt = S.rcol[r], first = S.grow[r];
     S.rcol[r] = cnt == 1 ? first : -1;
@@ -904,6 +941,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   // ---- eliminable variables: diagonal-only Hessian row (elig, from the H
   // pass), at most one general row, and alone in that row (otherwise K_ee
   // would not be diagonal)
+#pragma unroll 1
   for (int c = tid; c < n; c += nt) {
     if (!S.elig[c]) { S.egi[c] = -1; continue; }
     int cnt = 0, gs = -1;
@@ -912,11 +950,14 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     S.egi[c] = gs;  // temporarily indexed by column
     if (cnt > 1) S.elig[c] = 0;
   }
+#pragma unroll 1
   for (int gi = tid; gi < S.ng; gi += nt) S.ge[gi] = 0;
   __syncthreads();
+#pragma unroll 1
   for (int c = tid; c < n; c += nt)  // rows meeting several candidates keep them all
     if (S.elig[c] && S.egi[c] >= 0) atomicAdd(&S.ge[S.egi[c]], 1);
   __syncthreads();
+#pragma unroll 1
   for (int c = tid; c < n; c += nt)
     if (S.elig[c] && S.egi[c] >= 0 && S.ge[S.egi[c]] > 1) S.elig[c] = 0;
   __syncthreads();
@@ -994,12 +1035,15 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     const double* Hr = H + (int64_t)S.kidx[kr] * n;
     for (int kc = lane; kc <= kr; kc += 32) S.Hp[colbase(kc, S.nf) + kr] = Hr[S.kidx[kc]];
   }
+#pragma unroll 1
   for (int t = tid; t < n; t += nt) S.g[t] = A.g[bi * (int64_t)n + t];
+#pragma unroll 1
   for (int t = tid; t < m; t += nt) S.d[t] = A.d[bi * (int64_t)m + t];
   __syncthreads();
 
   // scale references (qpsolver.py:124-127)
   double hmax = hmax_loc, gmax = 0.0;
+#pragma unroll 1
   for (int t = tid; t < n; t += nt) gmax = fmax(gmax, fabs(S.g[t]));
   hmax = block_reduce<0>(hmax, red);
   gmax = block_reduce<0>(gmax, red);
@@ -1020,6 +1064,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
       ok = chol_factor(S);
     }
     if (!ok) {
+#pragma unroll 1
       for (int t = tid; t < n; t += nt) uo[t] = 0.0;
       if (tid == 0) {
         A.status[bi] = GM_QP_NUMERICAL_FAILURE;
@@ -1029,14 +1074,17 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
       return;
     }
     invert_diag_blocks(S);
+#pragma unroll 1
     for (int t = tid; t < n; t += nt) S.rhs[t] = -S.g[t];
     __syncthreads();
     chol_solve(S, S.rhs, S.u);
     h_apply(S, S.u, S.hu);
     __syncthreads();
     double rs = 0.0;
+#pragma unroll 1
     for (int c = tid; c < n; c += nt) rs = fmax(rs, fabs(2.0 * S.hu[c] + S.g[c]));
     rs = block_reduce<0>(rs, red);
+#pragma unroll 1
     for (int t = tid; t < n; t += nt) uo[t] = S.u[t];
     if (tid == 0) {
       A.status[bi] = GM_QP_OPTIMAL;
@@ -1049,10 +1097,12 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   }
 
   // ---- start point (qpsolver.py:146-150)
+#pragma unroll 1
   for (int t = tid; t < n; t += nt) S.u[t] = A.warm ? A.warm[bi * (int64_t)n + t] : 0.0;
   __syncthreads();
   c_apply(S, S.u, S.cu);
   __syncthreads();
+#pragma unroll 1
   for (int r = tid; r < m; r += nt) {
     S.s[r] = fmax(S.d[r] - S.cu[r], 1.0) * 1.1;
     S.lam[r] = 1.0;
@@ -1074,7 +1124,9 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
       b_rs = R.rs;
       b_rp = R.rp;
       b_rc = R.rc;
+#pragma unroll 1
       for (int t = tid; t < n; t += nt) S.ub[t] = S.u[t];
+#pragma unroll 1
       for (int t = tid; t < m; t += nt) S.lb[t] = S.lam[t];
     }
     if (R.rs <= tol * scale_g && R.rp <= tol && R.rc <= tol * comp_ref) {
@@ -1086,6 +1138,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
       break;
     }
     double lmax = 0.0;
+#pragma unroll 1
     for (int r = tid; r < m; r += nt) lmax = fmax(lmax, S.lam[r]);
     lmax = block_reduce<0>(lmax, red);
     if (lmax > 1e12 && R.rp > 1e-6) {
@@ -1096,6 +1149,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     }
     qmark(S, 2);
     // Schur matrix and Cholesky with escalating regularisation (qpsolver.py:178-198)
+#pragma unroll 1
     for (int r = tid; r < m; r += nt) S.w[r] = S.lam[r] / S.s[r];
     __syncthreads();
     // build + factor with escalating regularisation: one copy in the code
@@ -1121,6 +1175,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     qmark(S, 5);
     // r_pri = C u + s - d, mu = lam.s / m
     double mu_loc = 0.0;
+#pragma unroll 1
     for (int r = tid; r < m; r += nt) {
       S.rp[r] = S.cu[r] + S.s[r] - S.d[r];
       mu_loc += S.lam[r] * S.s[r];
@@ -1129,6 +1184,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     // affine direction (rc = -lam s), then the corrector with centring (rc =
     // -lam s - dlam_a ds_a + sigma mu): one copy of the KKT step in the code,
     // run twice (the instruction working set of an iteration)
+#pragma unroll 1
     for (int r = tid; r < m; r += nt) S.tmp[r] = -S.lam[r] * S.s[r];
     __syncthreads();
     qmark(S, 6);
@@ -1140,19 +1196,23 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
       const double ap = max_step(S, S.s, S.ds);
       const double ad = max_step(S, S.lam, S.dl);
       double maff = 0.0;
+#pragma unroll 1
       for (int r = tid; r < m; r += nt) maff += (S.lam[r] + ad * S.dl[r]) * (S.s[r] + ap * S.ds[r]);
       const double mu_aff = block_reduce<2>(maff, red) / m;
       const double sigma = mu > 0.0 ? (mu_aff / mu) * (mu_aff / mu) * (mu_aff / mu) : 0.0;
+#pragma unroll 1
       for (int r = tid; r < m; r += nt) S.tmp[r] = -S.lam[r] * S.s[r] - S.dl[r] * S.ds[r] + sigma * mu;
       __syncthreads();
       qmark(S, 8);
     }
     const double alpha = fmin(tau * max_step(S, S.s, S.ds), tau * max_step(S, S.lam, S.dl));
     bool finite = true;
+#pragma unroll 1
     for (int c = tid; c < n; c += nt) {
       S.u[c] = S.u[c] + alpha * S.du[c];
       if (!isfinite(S.u[c])) finite = false;
     }
+#pragma unroll 1
     for (int r = tid; r < m; r += nt) {
       S.s[r] = S.s[r] + alpha * S.ds[r];
       S.lam[r] = S.lam[r] + alpha * S.dl[r];
@@ -1175,7 +1235,9 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
       b_rs = R.rs;
       b_rp = R.rp;
       b_rc = R.rc;
+#pragma unroll 1
       for (int t = tid; t < n; t += nt) S.ub[t] = S.u[t];
+#pragma unroll 1
       for (int t = tid; t < m; t += nt) S.lb[t] = S.lam[t];
     }
     iters = A.max_it;
@@ -1192,7 +1254,9 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   __syncthreads();
   const double* us = use_best ? S.ub : S.u;
   const double* ls = use_best ? S.lb : S.lam;
+#pragma unroll 1
   for (int t = tid; t < n; t += nt) uo[t] = us[t];
+#pragma unroll 1
   for (int t = tid; t < m; t += nt) lo[t] = ls[t];
   if (tid == 0) {
     A.status[bi] = status;
@@ -1233,6 +1297,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_chol_check(int n, const doubl
     if (c > r) continue;
     S.K[qpchol::gel(r, c)] = (r < n && c < n) ? A[(int64_t)r * n + c] : (r == c ? 1.0 : 0.0);
   }
+#pragma unroll 1
   for (int r = threadIdx.x; r < n; r += blockDim.x) S.rhs[r] = b[r];
   __syncthreads();
   const bool good = chol_factor(S);
@@ -1246,6 +1311,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_chol_check(int n, const doubl
   invert_diag_blocks(S);
   __syncthreads();
   chol_solve(S, S.rhs, S.du);
+#pragma unroll 1
   for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = S.du[r];
 }
 
