@@ -238,7 +238,8 @@ int gm_solve_qp(gm_ctx* ctx, int B, int n, int m, const double* H, const double*
 /* Diagnostics: per-phase cycle accounting of K-QP (block 0).  gm_qp_profile(1)
  * enables and zeroes the counters (2: counters 13-15 account the Cholesky
  * pivot chain instead of the Schur build); gm_qp_phase_cycles copies 16
- * counters (synchronous). */
+ * counters (synchronous).  The counters are compiled in only with
+ * -DGM_QP_PROF; otherwise gm_qp_profile(on != 0) returns GM_ERR_CONFIG. */
 int gm_qp_profile(int on);
 int gm_qp_phase_cycles(unsigned long long* out);
 /* Diagnostics: per-stage cycle accounting of the pipelined K-COND (CTA 0):

@@ -136,8 +136,15 @@ struct Qs {  // per-CTA views
   long long last;
 };
 
+// the accounting is compiled in with -DGM_QP_PROF only (make EXTRA=-DGM_QP_PROF):
+// its branches cost instruction-cache footprint in the IPM loop
+#ifdef GM_QP_PROF
+constexpr bool kQpProf = true;
+#else
+constexpr bool kQpProf = false;
+#endif
 __device__ __forceinline__ void qmark(Qs& S, int phase) {
-  if (S.prof && threadIdx.x == 0) {
+  if (kQpProf && S.prof && threadIdx.x == 0) {
     const long long t = clock64();
     atomicAdd(&g_qp_prof[phase], (unsigned long long)(t - S.last));
     S.last = t;
@@ -189,7 +196,7 @@ __device__ __forceinline__ bool chol_factor(Qs& S) {
   const bool ok = qpchol::factor<kQpThreads>(S.K, S.T, S.dinv, S.flag);
 #else
   const bool ok = qpchol::factor_la<kQpThreads>(S.K, S.T, S.dinv, S.flag,
-                                                (S.prof && g_qp_chol_split) ? g_qp_prof + 13 : nullptr);
+                                                (kQpProf && S.prof && g_qp_chol_split) ? g_qp_prof + 13 : nullptr);
 #endif
   __syncthreads();
   return ok;
@@ -774,7 +781,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   S.pv = pvbuf;
   S.ys = ysbuf;
   S.flag = &sh_int[1];
-  S.prof = g_qp_prof_on && blockIdx.x == 0;
+  S.prof = kQpProf && g_qp_prof_on && blockIdx.x == 0;
   S.last = clock64();
   {
     const QpLayout L0 = qp_layout(n, m, 0, false, false);
@@ -1331,6 +1338,7 @@ extern "C" int gm_chol_check(gm_ctx* ctx, int n, const double* A, const double* 
 }
 
 extern "C" int gm_qp_profile(int on) {
+  if (on && !kQpProf) return GM_ERR_CONFIG;  // built without -DGM_QP_PROF
   const int split = on == 2 ? 1 : 0;
   on = on != 0 ? 1 : 0;
   cudaMemcpyToSymbol(g_qp_prof_on, &on, sizeof(int));

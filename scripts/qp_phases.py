@@ -1,4 +1,6 @@
-"""Per-phase cycle breakdown of K-QP on a fixture QP (diagnostics)."""
+"""Per-phase cycle breakdown of K-QP on a fixture QP (diagnostics).  Needs the
+library built with the counters: `make -C paper_2602_17601_b200/csrc
+EXTRA=-DGM_QP_PROF` (touch k_qp.cu first); gm_qp_profile fails otherwise."""
 import sys
 from pathlib import Path
 import numpy as np
@@ -24,7 +26,8 @@ for case in [a for a in sys.argv[1:] if not a.startswith("--")] or ["cfg1_chain1
     p = pkg.QpProblem(H, g, C, d)
     s = pkg.solve_qp(p)
     L = _runtime.lib()
-    L.gm_qp_profile(2 if "--chol" in sys.argv else 1)
+    if L.gm_qp_profile(2 if "--chol" in sys.argv else 1) != 0:
+        sys.exit("qp_phases: library built without -DGM_QP_PROF")
     s = pkg.solve_qp(p)
     out = np.zeros(16, dtype=np.uint64)
     L.gm_qp_phase_cycles(out.ctypes.data)
