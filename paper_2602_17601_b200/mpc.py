@@ -443,6 +443,7 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
         plan.fb_inputs = plan.li.clone()
     else:
         plan.fb_states, plan.fb_inputs = plan.ls, plan.li
+    early = None
     for it in range(cfg.sqp_iterations):
         if not gnn:  # plug-in Linearizer (mpc.py:23, :82-87): upload its blocks
             lin = model(plan.ls[:N].cpu().numpy(), plan.li.cpu().numpy())
@@ -452,6 +453,11 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
                     dst.view(-1)[: src.numel()].copy_(src.reshape(-1))
         if whole:
             plan.graph.replay()
+            if cfg.sqp_iterations == 1:
+                # the snapshot copy and its views are enqueued / built while
+                # the step runs (nothing writes outbuf after the graph)
+                early = plan.outbuf.clone()
+                early_views = plan._carve(early)
         else:
             if graphable and plan.graph is None and plan.runs >= 1:
                 # make sure the eager copies of this call are done before the
@@ -485,8 +491,12 @@ def mpc_step(model, topo, spec, x_measured: SystemState, state: MpcState, cfg: M
         last_applied = u_app.copy()
     else:
         last_applied = None
-    snap = plan.outbuf.clone()  # one device copy: the new state owns it
-    planned_states, planned_inputs, next_states, next_inputs, u_applied = plan._carve(snap)
+    if early is not None:
+        snap, views = early, early_views
+    else:
+        snap = plan.outbuf.clone()  # one device copy: the new state owns it
+        views = plan._carve(snap)
+    planned_states, planned_inputs, next_states, next_inputs, u_applied = views
     if last_applied is None:
         last_applied = u_applied
     new_state = MpcState(lin_states=next_states, lin_inputs=next_inputs,
