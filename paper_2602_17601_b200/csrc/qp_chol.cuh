@@ -1014,9 +1014,10 @@ __device__ __noinline__ void diag16(const double* Kt, int T, const double* D, do
 
 // solve_mw with 16-row blocks (tiles 2j, 2j+1): the chain step is one 16x16
 // look-ahead product and one 16x16 mat-vec with the block inverse
-// [[D_2j, 0], [X21_j, D_2j+1]], lane (r, h) = (row, column half): 8 FMAs in
-// two chains and one shuffle -- half the chain steps of solve_mw and no
-// 4-lane reduce.  T <= 16 (X21 in 512 doubles); odd T: the last block is
+// [[D_2j, 0], [X21_j, D_2j+1]]; lane r < 16 owns row r of the block (both
+// 8-column halves in the lane: 4 FMA chains, no shuffle on the chain; the
+// (row, half) lane-pair form was 1.7 % slower at cfg3) -- half the chain
+// steps of solve_mw and no 4-lane reduce.  T <= 16 (X21 in 512 doubles); odd T: the last block is
 // 8 rows.  Same arguments as solve_mw plus X21 (diag16).
 template <int NT>
 __device__ __noinline__ void solve_mw16(const double* Kt, const double* D, const double* X21, int T, int nf,
@@ -1043,27 +1044,32 @@ __device__ __noinline__ void solve_mw16(const double* Kt, const double* D, const
   };
   // ---- forward ----
   if (wid == 0) {
+    // lane q < 16 owns row q of the 16-row block; both halves of every dot
+    // in the lane (4 FMA chains), so the chain has no pair shuffles
+    const int q16 = lane & 15, qh = q16 >> 3, qr = q16 & 7;
+    const bool act = lane < 16;
     for (int j = 0; j < T16; ++j) {
       if (j >= 2) bar_sync(BU + (j & 1), NT);
-      const int tr = 2 * j + rh;          // tile row of this lane's row
-      const bool live = tr < T;
-      if (j >= 1) {  // look-ahead: y of block j-1 into block j
-        double v = (live ? 1.0 : 0.0) *
-                   dot8(Kt + ti(live ? tr : 2 * (j - 1) + h, 2 * (j - 1) + h) * kTS, rr, false, s + 16 * (j - 1) + 8 * h);
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
+      const int tr = 2 * j + qh;  // tile row of this lane's row
+      const bool live = act && tr < T;
+      const int trs = live ? tr : 2 * j;
+      if (j >= 1) {  // look-ahead: y of block j-1 (two full tiles) into block j
+        const double* y = s + 16 * (j - 1);
+        const double v = dot8(Kt + ti(trs, 2 * j - 2) * kTS, qr, false, y) +
+                         dot8(Kt + ti(trs, 2 * j - 1) * kTS, qr, false, y + 8);
         __syncwarp();
-        if (h == 0 && live) s[16 * j + r] -= v;
+        if (live) s[16 * j + q16] -= v;
         __syncwarp();
       }
-      // lane -> (matrix, vector) by selects: one uniform dot per lane (no
-      // divergent paths); the (rows 0-7, half 1) lanes contribute zero
+      // rows 0-7: D_2j y_a; rows 8-15: X21 y_a + D_2j+1 y_c (uniform selects)
       const bool two = 2 * j + 1 < T;
-      const double* M = rh == 0 ? D + 2 * j * kTS : (h == 0 ? X21 + j * 64 : D + (2 * j + 1) * kTS);
-      const double wgt = (live && !(rh == 0 && h == 1) && (rh == 0 || two)) ? 1.0 : 0.0;
-      double v = wgt * dot8(live ? M : D, rr, false, s + 16 * j + 8 * (h & (live ? 1 : 0)));
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      const double* M1 = (qh == 0 || !two) ? D + 2 * j * kTS : X21 + j * 64;
+      const double* M2 = two ? D + (2 * j + 1) * kTS : D + 2 * j * kTS;
+      const double w2 = (qh == 1 && two) ? 1.0 : 0.0;
+      const double* ya = s + 16 * j;
+      const double v = dot8(M1, qr, false, ya) + w2 * dot8(M2, qr, false, two ? ya + 8 : ya);
       __syncwarp();
-      if (h == 0 && live) s[16 * j + r] = v;
+      if (live) s[16 * j + q16] = v;
       __syncwarp();
       __threadfence_block();
       bar_arrive(BY + (j & 1), NT);
@@ -1088,30 +1094,35 @@ __device__ __noinline__ void solve_mw16(const double* Kt, const double* D, const
   __syncthreads();
   // ---- backward (step q = T16-1-j) ----
   if (wid == 0) {
+    const int q16 = lane & 15, qh = q16 >> 3, qr = q16 & 7;
+    const bool act = lane < 16;
     for (int q = 0; q < T16; ++q) {
       const int j = T16 - 1 - q;
       if (q >= 2) bar_sync(BU + (q & 1), NT);
-      const int tc = 2 * j + rh;  // tile column (this lane's row of block j as a column of L)
-      const bool live = tc < T;
+      const int tc = 2 * j + qh;  // this lane's row of block j as a column of L
+      const bool live = act && tc < T;
+      const int tcs = live ? tc : 2 * j;
       if (q >= 1) {  // look-ahead: x of block j+1 into block j
-        const int trow = 2 * (j + 1) + h;  // tile row of block j+1's half h
-        const bool ok = live && trow < T;
-        double v = (ok ? 1.0 : 0.0) * dot8(Kt + (ok ? ti(trow, tc) : 0) * kTS, rr, true,
-                                           s + 16 * (j + 1) + 8 * (ok ? h : 0));
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        const bool two1 = 2 * j + 3 < T;
+        const double* x1 = s + 16 * (j + 1);
+        const double v = dot8(Kt + ti(2 * j + 2, tcs) * kTS, qr, true, x1) +
+                         (two1 ? 1.0 : 0.0) * dot8(Kt + ti(two1 ? 2 * j + 3 : 2 * j + 2, tcs) * kTS, qr, true,
+                                                   two1 ? x1 + 8 : x1);
         __syncwarp();
-        if (h == 0 && live) s[16 * j + r] -= v;
+        if (live) s[16 * j + q16] -= v;
         __syncwarp();
       }
-      // rows 0-7: D_2j^T t_a (half 0) + X21^T t_c (half 1); rows 8-15:
-      // D_2j+1^T t_c (half 1); selects instead of divergent paths
+      // rows 0-7: D_2j' t_a + X21' t_c; rows 8-15: D_2j+1' t_c (uniform selects)
       const bool two = 2 * j + 1 < T;
-      const double* M = h == 0 ? D + 2 * j * kTS : (rh == 0 ? X21 + j * 64 : D + (2 * j + 1) * kTS);
-      const double wgt = (live && !(rh == 1 && h == 0) && (h == 0 || two)) ? 1.0 : 0.0;
-      double v = wgt * dot8((live && (h == 0 || two)) ? M : D, rr, true, s + 16 * j + 8 * (two ? h : 0));
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      const double* ta = s + 16 * j;
+      const double* tcv = two ? ta + 8 : ta;
+      const double* M1 = (qh == 0 || !two) ? D + 2 * j * kTS : D + (2 * j + 1) * kTS;
+      const double w2 = (qh == 0 && two) ? 1.0 : 0.0;
+      // (no X21 for a lone last tile: a finite stand-in under the zero weight)
+      const double v = dot8(M1, qr, true, qh == 0 ? ta : tcv) +
+                       w2 * dot8(two ? X21 + j * 64 : D + 2 * j * kTS, qr, true, tcv);
       __syncwarp();
-      if (h == 0 && live) s[16 * j + r] = v;
+      if (live) s[16 * j + q16] = v;
       __syncwarp();
       __threadfence_block();
       bar_arrive(BY + (q & 1), NT);
