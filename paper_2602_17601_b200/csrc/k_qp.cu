@@ -172,10 +172,18 @@ __device__ double block_reduce(double v, double* red) {
   __syncthreads();
   if (lane == 0) red[wid] = v;
   __syncthreads();
-  double r = red[lane & (kQpWarps - 1)];
+  double w[kQpWarps];
 #pragma unroll
-  for (int o = kQpWarps / 2; o > 0; o >>= 1) r = rop<OP>(r, __shfl_xor_sync(0xffffffffu, r, o));
-  return r;
+  for (int i = 0; i < kQpWarps; i += 2) {
+    const double2 t = *reinterpret_cast<const double2*>(red + i);
+    w[i] = t.x;
+    w[i + 1] = t.y;
+  }
+#pragma unroll
+  for (int o = kQpWarps / 2; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < o; ++i) w[i] = rop<OP>(w[i], w[i + o]);
+  return w[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -762,7 +770,7 @@ __device__ Resid residuals(Qs& S) {
 
 __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[kQpWarps];
+  __shared__ __align__(16) double red[kQpWarps];
   __shared__ double pvbuf[32];
   __shared__ double ysbuf[kTB];
   __shared__ int sh_int[4];
