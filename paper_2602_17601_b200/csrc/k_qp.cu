@@ -521,7 +521,7 @@ __device__ __noinline__ void build_tiles(const double* Cg, const double* Hp, con
   constexpr int U = 2;  // tiles in flight per warp (A/B on one box: 2 < 3 < 4 < 5)
   for (int t0 = wid; t0 < ntiles; t0 += U * kQpWarps) {
     int r[U], ca[U], ra[U], rbc[U];
-    double ma[U], mb[U], h0[U], h1[U];
+    double h0[U], h1[U];
     bool live[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -534,8 +534,6 @@ __device__ __noinline__ void build_tiles(const double* Cg, const double* Hp, con
       const int rb = 8 * J + i;  // B operand column
       ra[u] = min(r[u], n - 1);
       rbc[u] = min(rb, n - 1);
-      ma[u] = r[u] < n ? 1.0 : 0.0;
-      mb[u] = rb < n ? 1.0 : 0.0;
       const int cb = ca[u] + 1;
       // strictly lower entries start from 2H; the diagonal is completed below
       h0[u] = (live[u] && r[u] < n && ca[u] < n && r[u] > ca[u]) ? 2.0 * ldv<SH>(Hp, hpb, colbase(ca[u], n) + r[u])
@@ -562,8 +560,8 @@ __device__ __noinline__ void build_tiles(const double* Cg, const double* Hp, con
       double av[U], bv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        av[u] = (wgg * ma[u]) * xa[u];
-        bv[u] = mb[u] * xb[u];
+        av[u] = wgg * xa[u];
+        bv[u] = xb[u];
       }
       if (g0 + 4 < ng) load(g0 + 4);
 #pragma unroll
