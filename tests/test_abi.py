@@ -156,3 +156,13 @@ def test_native_comm_entry_points_on_cpu():
     assert bytes(a) != bytes(b)  # fresh ids
     assert L.gm_comm_unique_id(None) != 0
     assert L.gm_comm_destroy(None) != 0
+
+
+def test_qp_phase_counters_are_opt_in():
+    """The K-QP per-phase counters cost instruction-cache footprint in the IPM
+    loop, so the product build leaves them out: enabling them fails loudly
+    (GM_ERR_CONFIG) unless the library was built with -DGM_QP_PROF."""
+    from paper_2602_17601_b200._runtime import GM_ERR_CONFIG, lib
+
+    assert lib().gm_qp_profile(1) == GM_ERR_CONFIG
+    assert lib().gm_qp_profile(2) == GM_ERR_CONFIG
