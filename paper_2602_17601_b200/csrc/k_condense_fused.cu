@@ -1306,11 +1306,20 @@ __global__ void __launch_bounds__(GR + GH, 1) k_condense_tmap(const FusedArgs a,
       cprof_add(pf, k, 13, ph4 - ph3);
       const int lk = k * NU;
       for (int cidx = gt; cidx < lk; cidx += GH) {
-        double sg = gs[cidx];
-        for (int li = 0; li < sc; ++li)
+        // three fp64 chains (rows r, r + 3 of each node) instead of one
+        // 6 sc-long chain, folded in a fixed order
+        double s0 = gs[cidx], s1 = 0.0, s2 = 0.0;
+        for (int li = 0; li < sc; ++li) {
+          const float* gcol = Gc + (int64_t)li * NX * ld + cidx;
+          const double* w = wv + li * NX;
 #pragma unroll
-          for (int r = 0; r < NX; ++r) sg += (double)Gc[((int64_t)li * NX + r) * ld + cidx] * wv[li * NX + r];
-        gs[cidx] = sg;
+          for (int r = 0; r < NX; r += 3) {
+            s0 = fma((double)gcol[(int64_t)r * ld], w[r], s0);
+            s1 = fma((double)gcol[(int64_t)(r + 1) * ld], w[r + 1], s1);
+            s2 = fma((double)gcol[(int64_t)(r + 2) * ld], w[r + 2], s2);
+          }
+        }
+        gs[cidx] = s0 + (s1 + s2);
       }
       const long long ph2 = cprof_clock(pf);
       cprof_add(pf, k, 14, ph2 - ph4);
