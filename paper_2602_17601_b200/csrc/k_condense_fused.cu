@@ -1323,7 +1323,30 @@ __global__ void __launch_bounds__(GR + GH, 1) k_condense_tmap(const FusedArgs a,
       }
       const long long ph2 = cprof_clock(pf);
       cprof_add(pf, k, 14, ph2 - ph4);
-      if (sub == nsub - 1) {
+      if (sub == nsub - 1 && R == 1) {
+        // one owner per pair (pair gt, and gt + GH): fold in place, no
+        // staging and no barriers (same sums as the staged fold with R = 1)
+        if (h0) {
+          float* hp = Hacc + (int64_t)gt * NU * NU;
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int v = 0; v < NU; ++v) {
+              hp[u * NU + v] += acc0[u][v];
+              acc0[u][v] = 0.f;
+            }
+        }
+        if (h1) {
+          float* hp = Hacc + (int64_t)(gt + GH) * NU * NU;
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int v = 0; v < NU; ++v) {
+              hp[u * NU + v] += acc1[u][v];
+              acc1[u][v] = 0.f;
+            }
+        }
+      } else if (sub == nsub - 1) {
         // fold the stage into Hacc through this buffer (group R does not
         // touch it before our EMPTY arrival): slot gt <- acc0, gt + 128 <- acc1
         float* stg = Gc;
