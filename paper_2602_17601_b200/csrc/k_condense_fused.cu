@@ -1256,7 +1256,10 @@ __global__ void __launch_bounds__(GR + GH, 1) k_condense_tmap(const FusedArgs a,
       const double* wv = wv2 + b * SC * NX;
       if (sub == 0) {
         if (npk <= GH) {
-          R = max(1, min(SC * NX, GH / npk));
+          // one item per stage (cfg3-like): at most 4 row slices, so the
+          // staged fold sums few slices (A/B: cfg3 K-COND -2 %; with several
+          // items per stage the fold is amortised and wide slicing wins)
+          R = max(1, min(nsub == 1 ? 4 : SC * NX, GH / npk));
           sl = gt / npk;
           h0 = sl < R;
           h1 = false;
