@@ -158,8 +158,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // block-wide reductions (every thread gets the result); op 0 max, 1 min, 2 sum.
-// Warp partials go through shared memory; each warp then folds the 16
-// partials with 4 shuffles (fixed order: bitwise reproducible).
+// Warp partials go through shared memory and every thread folds them in a
+// fixed order (bitwise reproducible); block_reduce_n reduces K values with
+// one pair of barriers.
 template <int OP>
 __device__ __forceinline__ double rop(double a, double b) {
   return OP == 0 ? fmax(a, b) : (OP == 1 ? fmin(a, b) : a + b);
@@ -184,6 +185,53 @@ __device__ double block_reduce(double v, double* red) {
 #pragma unroll
     for (int i = 0; i < o; ++i) w[i] = rop<OP>(w[i], w[i + o]);
   return w[0];
+}
+template <int OP, int K>
+__device__ void block_reduce_n(double (&v)[K], double* red, double* sum = nullptr) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double sv = sum ? *sum : 0.0;  // optional extra value, summed
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) v[q] = rop<OP>(v[q], __shfl_xor_sync(0xffffffffu, v[q], o));
+    if (sum) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) red[q * kQpWarps + wid] = v[q];
+    if (sum) red[K * kQpWarps + wid] = sv;
+  }
+  __syncthreads();
+  if (sum) {
+    double w[kQpWarps];
+#pragma unroll
+    for (int i = 0; i < kQpWarps; i += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(red + K * kQpWarps + i);
+      w[i] = t.x;
+      w[i + 1] = t.y;
+    }
+#pragma unroll
+    for (int o = kQpWarps / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < o; ++i) w[i] = w[i] + w[i + o];
+    *sum = w[0];
+  }
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    double w[kQpWarps];
+#pragma unroll
+    for (int i = 0; i < kQpWarps; i += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(red + q * kQpWarps + i);
+      w[i] = t.x;
+      w[i + 1] = t.y;
+    }
+#pragma unroll
+    for (int o = kQpWarps / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < o; ++i) w[i] = rop<OP>(w[i], w[i + o]);
+    v[q] = w[0];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -640,6 +688,19 @@ __device__ bool build_k(const Qs& S, double diag_add, bool terms) {
   return all_ok;
 }
 
+// step lengths of (s, ds) and (lam, dl) with one block reduction
+__device__ __forceinline__ void max_step2(const Qs& S, double& ap, double& ad) {
+  double a[2] = {1.0, 1.0};
+#pragma unroll 1
+  for (int r = threadIdx.x; r < S.m; r += blockDim.x) {
+    if (S.ds[r] < 0.0) a[0] = fmin(a[0], -S.s[r] / S.ds[r]);
+    if (S.dl[r] < 0.0) a[1] = fmin(a[1], -S.lam[r] / S.dl[r]);
+  }
+  block_reduce_n<1, 2>(a, S.red);
+  ap = a[0];
+  ad = a[1];
+}
+
 // largest step in [0, 1] with x + a dx > 0 (qpsolver.py:238-243)
 __device__ double max_step(const Qs& S, const double* x, const double* dx) {
   double a = 1.0;
@@ -735,7 +796,7 @@ __device__ void kkt_step(Qs& S, const double* rcv) {
 }
 
 struct Resid {
-  double rs, rp, rc;
+  double rs, rp, rc, lmax, musum;
 };
 
 // residuals at (u, lam) (qpsolver.py:90-97); leaves r_dual in rd, C u in cu
@@ -746,7 +807,7 @@ __device__ Resid residuals(Qs& S) {
   ct_apply(S, S.lam, S.ctl);
   c_apply(S, S.u, S.cu);
   __syncthreads();
-  double a_rs = 0.0, a_rp = -INFINITY, a_rc = 0.0;
+  double a_rs = 0.0, a_rp = -INFINITY, a_rc = 0.0, a_lm = 0.0, a_mu = 0.0;
 #pragma unroll 1
   for (int c = threadIdx.x; c < S.n; c += blockDim.x) {
     const double rd = (2.0 * S.hu[c] + S.g[c]) + S.ctl[c];
@@ -758,17 +819,24 @@ __device__ Resid residuals(Qs& S) {
     const double viol = S.cu[r] - S.d[r];
     a_rp = fmax(a_rp, viol);
     a_rc = fmax(a_rc, fabs(S.lam[r] * viol));
+    a_lm = fmax(a_lm, S.lam[r]);  // max lam for the infeasibility test
+    S.rp[r] = S.cu[r] + S.s[r] - S.d[r];  // r_pri and mu of this iterate
+    a_mu += S.lam[r] * S.s[r];
   }
   Resid R;
-  R.rs = block_reduce<0>(a_rs, S.red);
-  R.rp = fmax(0.0, block_reduce<0>(a_rp, S.red));
-  R.rc = block_reduce<0>(a_rc, S.red);
+  double r3[4] = {a_rs, a_rp, a_rc, a_lm};
+  block_reduce_n<0, 4>(r3, S.red, &a_mu);
+  R.rs = r3[0];
+  R.rp = fmax(0.0, r3[1]);
+  R.rc = r3[2];
+  R.lmax = r3[3];
+  R.musum = a_mu;
   return R;
 }
 
 __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ __align__(16) double red[kQpWarps];
+  __shared__ __align__(16) double red[5 * kQpWarps];
   __shared__ double pvbuf[32];
   __shared__ double ysbuf[kTB];
   __shared__ int sh_int[4];
@@ -1150,11 +1218,7 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
       f_rc = R.rc;
       break;
     }
-    double lmax = 0.0;
-#pragma unroll 1
-    for (int r = tid; r < m; r += nt) lmax = fmax(lmax, S.lam[r]);
-    lmax = block_reduce<0>(lmax, red);
-    if (lmax > 1e12 && R.rp > 1e-6) {
+    if (R.lmax > 1e12 && R.rp > 1e-6) {
       status = GM_QP_PRIMAL_INFEASIBLE;
       iters = it;
       use_best = true;
@@ -1186,14 +1250,8 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
     invert_diag_blocks(S);
     __syncthreads();
     qmark(S, 5);
-    // r_pri = C u + s - d, mu = lam.s / m
-    double mu_loc = 0.0;
-#pragma unroll 1
-    for (int r = tid; r < m; r += nt) {
-      S.rp[r] = S.cu[r] + S.s[r] - S.d[r];
-      mu_loc += S.lam[r] * S.s[r];
-    }
-    const double mu = block_reduce<2>(mu_loc, red) / m;
+    // r_pri = C u + s - d and mu = lam.s / m came with the residuals
+    const double mu = R.musum / m;
     // affine direction (rc = -lam s), then the corrector with centring (rc =
     // -lam s - dlam_a ds_a + sigma mu): one copy of the KKT step in the code,
     // run twice (the instruction working set of an iteration)
@@ -1206,8 +1264,8 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
       kkt_step(S, S.tmp);
       qmark(S, 7);
       if (pass == 1) break;
-      const double ap = max_step(S, S.s, S.ds);
-      const double ad = max_step(S, S.lam, S.dl);
+      double ap, ad;
+      max_step2(S, ap, ad);
       double maff = 0.0;
 #pragma unroll 1
       for (int r = tid; r < m; r += nt) maff += (S.lam[r] + ad * S.dl[r]) * (S.s[r] + ap * S.ds[r]);
@@ -1218,7 +1276,9 @@ __global__ void __launch_bounds__(kQpThreads, 1) k_solve_qp(const QpArgs A) {
       __syncthreads();
       qmark(S, 8);
     }
-    const double alpha = fmin(tau * max_step(S, S.s, S.ds), tau * max_step(S, S.lam, S.dl));
+    double ap_f, ad_f;
+    max_step2(S, ap_f, ad_f);
+    const double alpha = fmin(tau * ap_f, tau * ad_f);
     bool finite = true;
 #pragma unroll 1
     for (int c = tid; c < n; c += nt) {
