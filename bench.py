@@ -53,7 +53,7 @@ NCU_TRAFFIC = {
     # launches of one step; K-COND = k_condense_tmap, the warp-specialised
     # TMA pipeline; k_solve_qp with the substitution solves)
     "cfg3": {"k_solve_qp": 660992, "linearize": 42505472, "k_condense": 31421440},
-    # cfg4: one 1024-instance wave of k_condense_tmap (384 threads)
+    # cfg4: one 1024-instance wave of k_condense_tmap (512 threads since v17)
     "cfg4": {"k_condense": 28787045000},
     # cfg5: k_condense_tmap (512 threads, H accumulator in the global partial)
     "cfg5": {"k_condense": 27824387000},

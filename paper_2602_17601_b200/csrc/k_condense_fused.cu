@@ -2181,7 +2181,11 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
     const char* v = std::getenv("GM_TMA_GR");
     return v ? std::atoi(v) : 0;
   }();
-  const int gr_want = gr_env ? gr_env : (dslot >= 4 ? 256 : 128);
+  // group R: 256 threads (the 512-thread pipeline) unless GM_TMA_GR says
+  // otherwise; 128 when the 512-thread variant does not fit.  Chains took 128
+  // until group H's in-place fold and three-chain gradient shifted the balance
+  // (same-box A/B after those: cfg3 K-COND -2 %, cfg4 -4.5 %, M = 10^4 -4 %)
+  const int gr_pref[2] = {gr_env ? gr_env : 256, gr_env ? gr_env : 128};
   const Var vars[12] = {{4, true, true, k_condense_tmap<8, 4, 4, true, 256, 256>, 512, 256},
                        {4, false, true, k_condense_tmap<8, 4, 4, false, 256, 256>, 512, 256},
                        {2, false, true, k_condense_tmap<8, 2, 2, false, 256, 256>, 512, 256},
@@ -2196,14 +2200,22 @@ int condense_tma(gm_ctx* ctx, int B, int N, const float* a_self, const float* a_
                        {2, false, false, k_condense_tma<8, 2, 2, false>, 256}};
   const int npk_max = N * (N + 1) / 2;
   const Var* var = nullptr;
-  for (const Var& v : vars)
-    if ((cps_env == 0 || cps_env == v.cps + (v.db ? 10 : 0)) && (pipe_env != 0 || !v.pipe) &&
-        (!v.pipe || (v.gr == gr_want && v.threads - v.gr == gh_env && npk_max <= 2 * (v.threads - v.gr) &&
-                     36 * std::max(v.threads - v.gr, npk_max) <= 2 * SC * 6 * ld)) &&
-        tma_smem(SC, v.cps, v.db, ctx->cu_umax, ld, dslot, n0, per, v.pipe, !v.pipe) <= budget) {
-      var = &v;
-      break;
-    }
+  for (int pass = 0; pass < 2 && !var && pipe_env != 0; ++pass)
+    for (const Var& v : vars)
+      if (v.pipe && (cps_env == 0 || cps_env == v.cps + (v.db ? 10 : 0)) && v.gr == gr_pref[pass] &&
+          v.threads - v.gr == gh_env && npk_max <= 2 * (v.threads - v.gr) &&
+          36 * std::max(v.threads - v.gr, npk_max) <= 2 * SC * 6 * ld &&
+          tma_smem(SC, v.cps, v.db, ctx->cu_umax, ld, dslot, n0, per, true, false) <= budget) {
+        var = &v;
+        break;
+      }
+  if (!var)  // neither pipeline size fits: the single-group TMA kernel
+    for (const Var& v : vars)
+      if (!v.pipe && (cps_env == 0 || cps_env == v.cps + (v.db ? 10 : 0)) &&
+          tma_smem(SC, v.cps, v.db, ctx->cu_umax, ld, dslot, n0, per, false, true) <= budget) {
+        var = &v;
+        break;
+      }
   if (!var) return 1;
   // the pipeline keeps its H accumulator on chip when that fits (chains),
   // else in its global partial (meshes: 26-row tile ring)

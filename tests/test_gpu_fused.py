@@ -7,6 +7,8 @@ to max|H|.  Gamma must be bitwise identical (same per-column FMA order).
 Also covers repeated launches (self-resetting stage counters), B > 1, graphs
 with remote neighbours (mesh, random), and CUDA-graph replay."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -147,9 +149,9 @@ def test_fused_matches_two_kernel_path(graph, N, nx, nu, B, mode):
 
 
 @pytest.mark.parametrize("graph,N,B,variant", [
-    ("chain1000", 20, 2, 4),   # 384-thread pipeline, tile slots double-buffered by item
-    ("chain301", 16, 2, 4),    # M not a multiple of the 8-node item, ld = 128 with 98 live
-    ("chain600", 15, 1, 4),    # ld = 96
+    ("chain1000", 20, 2, 5),   # 512-thread pipeline, tile slots double-buffered by item
+    ("chain301", 16, 2, 5),    # M not a multiple of the 8-node item, ld = 128 with 98 live
+    ("chain600", 15, 1, 5),    # ld = 96
     ("chain600", 25, 1, 6),    # N = 25: 325 block pairs > 256 -> the two-kernel path (K-REC + K-HG)
     ("mesh", 16, 2, 5),        # 512-thread pipeline (degree 4), single tile slot, global H fold
     ("local", 20, 2, 5),       # irregular degree <= 5 (neighbours within +-8), isolated nodes
@@ -176,6 +178,8 @@ def test_pipeline_kernel_shapes(graph, N, B, variant):
         nbrs = [sorted(set(int(j) for j in draw(i)) - {i}) for i in range(M)]
         topo = GraphTopology(M, tuple(tuple(n) for n in nbrs), 8)
     ref, outs = _run(topo, N, 6, 6, B, seed=13, reps=3, mode=0)
+    if variant == 5 and os.environ.get("GM_TMA_GR") == "128":
+        variant = 4  # the 384-thread pipeline (group R of 128 threads), forced
     assert _run.last_kernel == variant  # gm_last_condense_kernel: the pipeline ran
     _check(ref, outs, N * 6, 6, N, tol=2e-6)
 
@@ -185,7 +189,7 @@ def test_pipeline_kernel_graph_replay():
     from paper_2602_17601_b200.graph import chain_topology
 
     ref, outs = _run(chain_topology(1000), 20, 6, 6, 1, seed=4, reps=3, graph=True, mode=0)
-    assert _run.last_kernel == 4
+    assert _run.last_kernel == (4 if os.environ.get("GM_TMA_GR") == "128" else 5)
     _check(ref, outs, 120, 6, 20, tol=2e-6)
 
 
@@ -251,3 +255,20 @@ def test_cost_tensor_core_matches_simt(graph, N, nx, nu, B, rng_, partial):
     assert np.max(np.abs(Ht - Hs)) <= 1e-5 * np.max(np.abs(Hs))
     assert np.array_equal(Ht, np.swapaxes(Ht, 1, 2))
     assert np.max(np.abs(gt - gs)) <= 1e-5 * max(1.0, np.max(np.abs(gs)))
+
+
+@pytest.mark.skipif(os.environ.get("GM_TMA_GR") == "128", reason="already the forced run")
+def test_pipeline_384_thread_variant():
+    """The 384-thread pipeline (group R of 128 threads; the default is 256)
+    stays correct: the chain pipeline tests rerun in a child process with
+    GM_TMA_GR=128 (the variant choice is read once per process)."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, GM_TMA_GR="128")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                        os.path.join(root, "tests", "test_gpu_fused.py"), "-k",
+                        "test_pipeline_kernel_shapes and chain or test_pipeline_kernel_graph_replay"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
