@@ -1312,7 +1312,9 @@ __global__ void __launch_bounds__(GR + GH, 1) k_condense_tmap(const FusedArgs a,
         // three fp64 chains (rows r, r + 3 of each node) instead of one
         // 6 sc-long chain, folded in a fixed order
         double s0 = gs[cidx], s1 = 0.0, s2 = 0.0;
-        for (int li = 0; li < sc; ++li) {
+#pragma unroll
+        for (int li = 0; li < SC; ++li) {
+          if (li >= sc) break;
           const float* gcol = Gc + (int64_t)li * NX * ld + cidx;
           const double* w = wv + li * NX;
 #pragma unroll
