@@ -1373,6 +1373,7 @@ __global__ void __launch_bounds__(GR + GH, 1) k_condense_tmap(const FusedArgs a,
               acc1[u][v] = 0.f;
             }
         qpb_sync(BAR_H, GH);
+#pragma unroll 4
         for (int t = gt; t < npk * NU * NU; t += GH) {
           const int p2 = t / (NU * NU), e = t - p2 * NU * NU;
           float hs = Hacc[t];
