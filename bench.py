@@ -49,14 +49,14 @@ METRIC = "MPC step latency ms (linearize+condense+QP) & Hz at N nodes; solves/se
 # dram__bytes_read.sum + dram__bytes_write.sum per launch, from this round's
 # `ncu --set full` captures (profiles/r02/ncu_*); None where not captured
 NCU_TRAFFIC = {
-    # cfg3: profiles/r02/ncu_final_kernels_v17.txt (linearize = the 6 K-LIN
+    # cfg3: profiles/r02/ncu_final_kernels_v18.txt (linearize = the 6 K-LIN
     # launches of one step; K-COND = k_condense_tmap, the warp-specialised
     # TMA pipeline; k_solve_qp with the substitution solves)
-    "cfg3": {"k_solve_qp": 660992, "linearize": 42505984, "k_condense": 32269568},
-    # cfg4: one 1024-instance wave of k_condense_tmap (512 threads since v17)
-    "cfg4": {"k_condense": 28782897000},
+    "cfg3": {"k_solve_qp": 661248, "linearize": 42505472, "k_condense": 31912448},
+    # cfg4: one 1024-instance wave of k_condense_tmap (512 threads)
+    "cfg4": {"k_condense": 28780996000},
     # cfg5: k_condense_tmap (512 threads, H accumulator in the global partial)
-    "cfg5": {"k_condense": 27823107000},
+    "cfg5": {"k_condense": 27824988000},
 }
 M_NODES, HORIZON = 1000, 20
 WORKLOAD = "cfg3: chain graph M=1000 nodes, horizon N=20, _scaling_problem recipe (paper 100 Hz headline)"
